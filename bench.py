@@ -1,0 +1,320 @@
+"""Benchmark: SAC/TD3 update frames/s on B200 (BASELINE.json metric) -- one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config walker] [--precision bf16]
+    python bench.py --impl reference ...      # the float64 CPU oracle arm (host cores)
+
+A "step" is one full update over one batch of B transitions
+sampled from a device-resident ring filled with synthetic transitions (synthdata).
+value = B * K * N / (max over ranks of the CUDA-event time of K steps) [frames/s];
+frames/s = update frequency x B.  With N > 1 every rank runs its own learner
+on its own GPU ("replicas", weak scaling; no data-path collective).
+
+Extra keys: roofline (dominant kernel class vs the measured peak in
+MEASURED_PEAKS.json), cpu_baseline (the oracle on this host's cores, bounded sample),
+e2e (through the C ABI with host buffers: each step pushes B fresh transitions from
+pinned host memory and reads the stats back), clocks (nvidia-smi during the timed
+region), gpu_launches (our kernels launched in the timed region).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synthdata  # noqa: E402
+
+METRIC = "SAC update frames/s (transitions consumed) at 1/2/4/8 B200; % of GEMM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="walker", choices=list(synthdata.WORKLOADS))
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--impl", default="spz", choices=["spz", "reference"])
+    ap.add_argument("--batch", type=int, default=None, help="override the workload batch (B sweep)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sust=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sust=1400.0, src="fallback")
+
+
+# ----------------------------------------------------------------------------- algorithmic work per kernel class
+
+def class_flops(w, B):
+    """Algorithmic GEMM FLOPs (2 * M * N * K over the true, unpadded dims) per step, by kernel class."""
+    o, m, h, L = w.obs_dim, w.act_dim, w.hidden, w.n_hidden
+    td3 = w.algo == "td3"
+    aout = m if td3 else 2 * m
+    cin = o + m
+    f = {}
+    add = lambda k, v: f.__setitem__(k, f.get(k, 0) + v)
+    Ma = 2 * B  # SAC: [s2; s]; TD3: target actor on s2 + online actor on s (delayed steps)
+    add("actor_fwd_gemm", 2 * Ma * h * o + (L - 1) * 2 * Ma * h * h)
+    add("actor_head_gemm", 2 * Ma * aout * h)
+    add("target_critic_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))
+    add("critic_fwd_gemm", 2 * (2 * (2 * B) * h * cin + (L - 1) * 2 * (2 * B) * h * h))
+    add("critic_dgrad_gemm", 2 * (L - 1) * 2 * (2 * B) * h * h)
+    add("critic_input_dgrad_gemm", (1 if td3 else 2) * 2 * B * h * m)
+    add("critic_wgrad_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))
+    add("actor_dgrad_gemm", 2 * B * aout * h + (L - 1) * 2 * B * h * h)
+    add("actor_wgrad_gemm", 2 * B * h * o + (L - 1) * 2 * B * h * h + 2 * B * aout * h)
+    return f
+
+
+def class_bytes(w, B, n_params):
+    """Algorithmic HBM bytes per step for the memory-bound classes (§8(d))."""
+    R = (2 * w.obs_dim + w.act_dim + 2 + 3) // 4 * 4
+    return {"gather": B * (4 * R + 4),
+            # Adam+Polyak: read p, m, v, g; write p, m, v (+ target read/write for critics) -- fp32
+            "adam_polyak": n_params * 28 + n_params * 2 // 3 * 8}
+
+
+# ----------------------------------------------------------------------------- clocks sampler
+
+class Clocks:
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 9:
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU baseline / reference arm)
+
+def oracle_rate(w, B, steps):
+    """Time `steps` float64 oracle updates of the workload on this host; returns (frames/s, cores, seconds)."""
+    from oracle import ring as oring, sac as osac, td3 as otd3
+    cores = len(os.sched_getaffinity(0))
+    n = min(w.capacity, 1_000_000)
+    tr = synthdata.workload_transitions(w, n=n)
+    r = oring.Ring(w.obs_dim, w.act_dim, n)
+    r.push(**tr)
+    p = synthdata.init_params(w.obs_dim, w.act_dim, w.hidden, w.n_hidden, algo=w.algo)
+    cfg = osac.Config(obs_dim=w.obs_dim, act_dim=w.act_dim, hidden=w.hidden, n_hidden=w.n_hidden,
+                      alpha_auto=w.algo == "sac")
+    st = osac.State.create(p["actor"], p["q1"], p["q2"], log_alpha=np.log(0.2),
+                           actor_targ=p["actor"] if w.algo == "td3" else None)
+    step = osac.sac_step if w.algo == "sac" else otd3.td3_step
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st, _, _ = step(st, r, B, synthdata.SAMPLE_SEED, cfg)
+    dt = time.perf_counter() - t0
+    return B * steps / dt, cores, dt
+
+
+def reference_arm(a, w, B):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = a.steps
+    # each reference step = one full float64 oracle update at the workload's batch; keep the run to minutes
+    probe_rate, cores, probe_t = oracle_rate(w, B, 1)
+    per_step = probe_t
+    budget_s = 240.0
+    steps = max(1, min(steps, int(budget_s / max(per_step, 1e-3))))
+    warm = 0 if per_step > 5 else min(a.warmup, 3)
+    if warm:
+        oracle_rate(w, B, warm)
+    rate, cores, dt = oracle_rate(w, B, steps)
+    line = {"metric": METRIC, "value": rate, "unit": "frames/s", "impl": "reference", "n_gpus": a.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "global_batch": B, "algo": w.algo, "hidden": f"{w.n_hidden}x{w.hidden}",
+                       "obs_dim": w.obs_dim, "act_dim": w.act_dim, "ring": min(w.capacity, 1_000_000)},
+            "cpu_baseline": {"value": rate, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{steps} full float64 oracle updates at B={B} ({w.name})"},
+            "e2e": {"value": rate, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def main():
+    a = parse()
+    w = synthdata.WORKLOADS[a.config]
+    B = a.batch or w.batch
+    if a.impl == "reference":
+        reference_arm(a, w, B)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2312_06126_b200 import spz
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    assert a.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    # ring filled to capacity with synthetic transitions (ring bytes > L2, so gathers hit HBM)
+    C = w.capacity
+    ring = spz.Replay(w.obs_dim, w.act_dim, C, device=local)
+    chunk = 1_000_000
+    for s0 in range(0, C, chunk):
+        tr = synthdata.workload_transitions(w, n=min(chunk, C - s0), seed=synthdata.DATA_SEED + s0)
+        ring.push(**tr)
+    lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=B,
+                      device=local, seed=synthdata.SAMPLE_SEED + rank)
+    stream = torch.cuda.Stream(device=local)
+    lrn.set_stream(stream.cuda_stream)
+
+    # warm-up (includes CUDA-graph capture)
+    lrn.update(B, a.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        time.sleep(0.3)
+        ev0.record(stream)
+        stats = lrn.update(B, a.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        dist.barrier()
+    torch.cuda.synchronize()
+    frames = B * a.steps * world
+    value = frames / (ms / 1e3)
+    ms_per_step = ms / a.steps
+
+    # per-class device time (event-bracketed, un-graphed, same learner and batch) -> roofline
+    prof = lrn.profile(B, 5)
+    pk = peaks()
+    fl = class_flops(w, B)
+    n_params = sum(lrn.get(n).size for n in ("actor", "q1", "q2"))
+    by = class_bytes(w, B, n_params)
+    kern = {}
+    for k, t in prof.items():
+        e = {"ms": t}
+        if k in fl:
+            e["tflops"] = fl[k] / (t * 1e-3) / 1e12
+        if k in by:
+            e["gbs"] = by[k] / (t * 1e-3) / 1e9
+        kern[k] = e
+    dom = max(prof, key=prof.get)
+    if dom in fl:
+        ach = fl[dom] / (prof[dom] * 1e-3) / 1e12
+        pkv = pk["bf16_sust"] if a.precision == "bf16" else pk["bf16_sust"] / 2.0  # tf32 = bf16 / 2 (nominal ratio)
+        roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pkv, "unit": "TFLOP/s", "frac": ach / pkv,
+                "traffic": None, "peak_src": f"{pk['src']} bf16 sustained" + ("" if a.precision == "bf16" else " x 1/2 (tf32 nominal ratio)")}
+    else:
+        ach = by.get(dom, 0) / (prof[dom] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm"], "unit": "GB/s", "frac": ach / pk["hbm"],
+                "traffic": None, "peak_src": f"{pk['src']} hbm"}
+    gemm_t = sum(t for k, t in prof.items() if k in fl)
+    gemm_f = sum(fl.values())
+    roof["step_gemm_tflops"] = gemm_f / (ms_per_step * 1e-3) / 1e12
+    roof["step_frac_of_bf16_sustained"] = roof["step_gemm_tflops"] / pk["bf16_sust"]
+    roof["gemm_share_of_step"] = gemm_t / sum(prof.values())
+    launches = lrn.launches_per_step(B) * a.steps
+
+    # e2e through the C ABI with host buffers
+    e2e = None
+    if not a.no_e2e:
+        R_fields = 2 * w.obs_dim + w.act_dim + 2
+        host = synthdata.workload_transitions(w, n=B * 4, seed=synthdata.DATA_SEED + 99)
+        pinned = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in host.items()}
+        K2 = max(3, min(a.steps, 50))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(K2):
+            sl = slice((k % 4) * B, (k % 4 + 1) * B)
+            ring.push(**{n: v[sl] for n, v in pinned.items()})
+            lrn.update(B, 1)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = t.item()
+        e2e = {"value": B * K2 * world / dt, "unit": "frames/s", "h2d_bytes_per_step": B * R_fields * 4,
+               "d2h_bytes_per_step": 64 + 32 + 4, "steps": K2,
+               "note": "per step: spz_replay_push of B fresh host transitions (pinned) + spz_update(B, 1) with its stats read-back"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        steps = a.cpu_sample_steps or (3 if w.name in ("walker",) else 1)
+        if w.name == "pendulum":
+            steps = 50
+        rate, cores, dt = oracle_rate(w, B, steps)
+        cpu = {"value": rate, "unit": "frames/s", "cores": cores, "kind": "oracle",
+               "sample": f"{steps} float64 oracle updates at B={B} ({w.name}), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_per_step, "updates_per_s": 1e3 / ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": a.precision, "data": "synthetic",
+            "config": {"workload": w.name, "global_batch": B * world, "batch_per_gpu": B, "algo": w.algo,
+                       "hidden": f"{w.n_hidden}x{w.hidden}", "obs_dim": w.obs_dim, "act_dim": w.act_dim,
+                       "ring": C, "parallelism": "replicas" if world > 1 else "single",
+                       "l2": f"ring {C * ((2 * w.obs_dim + w.act_dim + 2 + 3) // 4 * 4) * 4 / 1e6:.0f} MB > 126 MB L2; fresh random indices each step"},
+            "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clk.summary(), "gpu_launches": launches, "last_stats": stats,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,216 @@
+/*
+ * spz.h -- C ABI of the B200-native Spreeze update hot path.
+ *
+ * Spreeze (arXiv 2312.06126) "Network Update" (§3.2):
+ * experience is "transmitted to a single network update process for
+ * parallelization by GPU" with "a large batch size", and the SAC
+ * update uses "two value networks Q1 and Q2 ... updated ... together with the
+ * target network".  This library implements exactly that step, from a
+ * device-resident replay ring (the paper's shared-memory experience pool,
+ * P:278-288) to the Adam/Polyak parameter update, as hand-written sm_100a
+ * CUDA.  The semantics of every call are those of the float64 oracle in
+ * oracle/ (DESIGN.md "Readings").
+ *
+ * Conventions (all calls):
+ *  - Every call returns spz_status; on a non-OK return spz_last_error() gives a
+ *    thread-local human-readable message naming the failing argument/kernel.
+ *  - Handles are opaque and caller-owned; *_destroy frees them (NULL is a no-op).
+ *  - Input arrays are borrowed for the duration of the call only.
+ *  - Pointers documented "device" must be device pointers on the handle's device
+ *    (any allocator: cudaMalloc, torch); "host" pointers are ordinary host memory.
+ *  - A handle is single-owner: calls on one handle must not run concurrently;
+ *    calls on different handles may ("single-owner").
+ *  - There is no CPU fallback: without a usable sm_100 device every creating
+ *    call fails with SPZ_ECUDA.
+ */
+#ifndef SPZ_H_
+#define SPZ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SPZ_OK = 0,
+  SPZ_EINVAL = -1,        /* bad argument (dims, sizes, NULL, batch > max_batch)    */
+  SPZ_ENODATA = -2,       /* ring fill < batch ("caller retries")             */
+  SPZ_ENONFINITE = -3,    /* non-finite loss/gradient; learner halted */
+  SPZ_ECUDA = -4,         /* CUDA runtime/driver error or no sm_100 device          */
+  SPZ_ENCCL = -5,         /* NCCL error                                             */
+  SPZ_ENOMEM = -6,        /* device allocation failed                               */
+  SPZ_ESTATE = -7,        /* call not valid in the handle's current state           */
+  SPZ_ETIMEOUT = -8,      /* split-mode peer missed the step barrier        */
+  SPZ_EUNSUPPORTED = -9   /* configuration not built in this library                */
+} spz_status;
+
+/* Thread-local message for the last non-OK return on this thread ("" if none). */
+const char* spz_last_error(void);
+/* Library version string and the build's target ("sm_100a"). */
+const char* spz_version(void);
+
+/* ------------------------------------------------------------------ replay ring
+ * Device-resident ring of transitions ("state s, action a, next state s2,
+ * reward r, and done flag d"; SPEC ReplayRing S:172-179).  Record layout: one
+ * fp32 record per transition, [s(o) | a(m) | r | d | s2(o) | pad], padded to
+ * R = round_up(2o+m+2, 4) floats (16-byte aligned rows, read with 128-bit loads).
+ * Global index i lives in slot i mod C; fill = min(cursor, C).
+ */
+typedef struct spz_replay spz_replay;
+
+typedef struct {
+  int32_t obs_dim;      /* o >= 1                                   */
+  int32_t act_dim;      /* m >= 1                                   */
+  int64_t capacity;     /* C >= 1 (capacity 0 is SPZ_EINVAL) */
+  int32_t device;       /* CUDA device ordinal that holds the ring  */
+} spz_replay_desc;
+
+spz_status spz_replay_create(const spz_replay_desc* desc, spz_replay** out);
+
+/* Append n transitions (S:195 ring_push).  obs/next_obs are [n x o] row-major,
+ * act [n x m], rew [n], done [n] (d in {0,1}; time-limit truncation stored as 0,
+ * S:230).  If src_on_device == 0 the arrays are host memory (staged through a
+ * pinned buffer, copied in at most two pieces split at the wrap point); if 1 they
+ * are device pointers on the ring's device.  Synchronous with respect to the
+ * source buffers.  *first_global_index (nullable) receives the global index of
+ * the first record; the oldest records are overwritten when full. */
+spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const float* act,
+                           const float* rew, const float* next_obs, const float* done,
+                           int32_t src_on_device, int64_t* first_global_index);
+
+/* Uniform sample with replacement over slots [0, F), F = current fill (S:203,
+ * S:228): for j in [0, batch), (x0,x1,x2,x3) = Philox4x32-10(key = seed,
+ * ctr = (j, 0, step, 1)) and idx_j = floor((x1*2^32 + x0) * F / 2^64).  Writes
+ * (each output nullable, all device pointers, row-major): idx int32[batch],
+ * obs [batch x o], act [batch x m], rew [batch], next_obs [batch x o],
+ * done [batch].  Returns SPZ_ENODATA if F < batch.  Synchronous. This is the same
+ * draw the learner makes internally at its global step `step`. */
+spz_status spz_replay_sample(spz_replay* r, int64_t batch, uint64_t seed, uint64_t step,
+                             int32_t* idx, float* obs, float* act, float* rew,
+                             float* next_obs, float* done);
+
+spz_status spz_replay_info(const spz_replay* r, int64_t* cursor, int64_t* fill, int64_t* capacity);
+/* Device pointer to the record array [C x R] fp32 and R (for zero-copy inspection). */
+spz_status spz_replay_records(const spz_replay* r, const float** records, int32_t* record_floats);
+void spz_replay_destroy(spz_replay* r);
+
+/* ------------------------------------------------------------------ learner
+ * One SAC (or TD3) update step per the oracle, Jacobi order:
+ * all losses at (theta_k, phi_k, alpha_k), then Adam on each trained network
+ * (own step counter), then Polyak theta' <- tau theta + (1-tau) theta'.
+ */
+typedef enum { SPZ_SAC = 0, SPZ_TD3 = 1 } spz_algo;
+/* FP32: GEMMs in full fp32 (exact-order-independent fp32 FMA); BF16: GEMM operands
+ * rounded to bf16 (RNE) on tcgen05 tensor cores with fp32 accumulation; every
+ * epilogue, master weight and optimizer state stays fp32 (reading #15). */
+typedef enum { SPZ_FP32 = 0, SPZ_BF16 = 1 } spz_precision;
+/* Role of this rank (P:239-247 actor/critic model parallelism). */
+typedef enum { SPZ_ROLE_ALL = 0, SPZ_ROLE_CRITIC = 1, SPZ_ROLE_ACTOR = 2 } spz_role;
+
+typedef struct {
+  spz_algo algo;
+  spz_precision precision;
+  int32_t obs_dim, act_dim;        /* o, m                                       */
+  int32_t hidden, n_hidden;        /* h, L: L hidden ReLU layers of width h      */
+  int64_t max_batch;               /* upper bound on the (global) batch          */
+  double gamma, tau;               /* 0.99, 0.005                                */
+  double lr_actor, lr_critic, lr_alpha, beta1, beta2, adam_eps; /* 3e-4 x3, 0.9, 0.999, 1e-8 */
+  int32_t alpha_auto;              /* 1: learn log alpha (target entropy below)  */
+  double alpha_init, target_entropy, log_std_min, log_std_max; /* 0.2, -m, -20, 2 */
+  double td3_noise, td3_noise_clip; int32_t td3_policy_delay;  /* 0.2, 0.5, 2 */
+  uint64_t seed;                   /* sampling/noise key (Philox)                */
+  uint64_t init_seed;              /* parameter init key (Philox stream 5)       */
+  int32_t device;                  /* CUDA device ordinal                        */
+  int32_t world_size, rank;        /* row sharding: rank handles a contiguous slice of global rows */
+  int32_t n_critic_ranks, n_actor_ranks; /* reserved for split mode (0 = co-located) */
+  spz_role role;
+  const uint8_t* nccl_unique_id;   /* 128 bytes, identical on all ranks; NULL if world_size == 1 */
+  int32_t use_graph;               /* 1 (default): replay the step as a CUDA graph */
+} spz_config;
+
+/* Fill *out with the defaults above for (algo, o, m); h = 256, L = 2, max_batch 8192. */
+spz_status spz_config_default(spz_algo algo, int32_t obs_dim, int32_t act_dim, spz_config* out);
+/* Generate a fresh NCCL unique id (rank 0 calls this and broadcasts the bytes). */
+spz_status spz_nccl_unique_id(uint8_t out[128]);
+
+typedef struct spz_learner spz_learner;
+
+typedef struct {
+  int64_t step;                    /* global step k of the last completed update          */
+  double critic_loss, actor_loss;  /* L_Q, L_pi at step k (TD3: L_pi on delayed steps)    */
+  double alpha, alpha_loss;        /* alpha_k and L_alpha                                 */
+  double q1_mean, q2_mean;         /* mean Q_i(s, a) over the batch                       */
+  double logp_mean;                /* mean log pi(a~|s)                                   */
+} spz_stats;
+
+/* Create a learner on cfg->device that samples from `ring` (borrowed: the ring
+ * must outlive the learner and live on the same device).  Parameters are
+ * initialised W, b ~ U(+-1/sqrt(fan_in)) from Philox(init_seed, stream 5); the
+ * targets copy the online networks; log alpha = ln(alpha_init). */
+spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learner** out);
+
+/* Run n_steps update steps with (global) batch B, each exactly the oracle's step
+ * k = current step.  Step k samples exactly spz_replay_sample(ring, B, seed, k).
+ * Requires fill >= B (else SPZ_ENODATA, nothing run) and B <= max_batch.  B may
+ * change between calls; Adam moments are preserved.  Synchronous at
+ * return (one device->host read of the stats and the non-finite flag).  On a
+ * non-finite loss the learner stops at the state before the failing step and
+ * returns SPZ_ENONFINITE (message names the step).  *last (nullable) receives
+ * the statistics of the last completed step. */
+spz_status spz_update(spz_learner* L, int64_t batch, int64_t n_steps, spz_stats* last);
+
+/* Use `stream` (a cudaStream_t on the learner's device, e.g. a torch stream) for
+ * all subsequent work; NULL restores the learner's private stream. */
+spz_status spz_learner_set_stream(spz_learner* L, void* stream);
+
+typedef enum {
+  SPZ_T_ACTOR = 0, SPZ_T_Q1 = 1, SPZ_T_Q2 = 2, SPZ_T_Q1_TARG = 3, SPZ_T_Q2_TARG = 4,
+  SPZ_T_ACTOR_TARG = 5, /* TD3 only */
+  SPZ_T_LOG_ALPHA = 6
+} spz_tensor;
+typedef enum { SPZ_S_PARAM = 0, SPZ_S_ADAM_M = 1, SPZ_S_ADAM_V = 2 } spz_slot; /* Adam slots: trained nets only */
+
+/* Flat fp32 layout (the oracle's): for each layer l = 1..L+1, W_l row-major
+ * [out x in] then b_l[out].  Actor: in = o, hidden h, out = 2m (SAC: rows 0..m-1
+ * mu, m..2m-1 log sigma) or m (TD3).  Critics: in = o + m (input [s | a]), out 1.
+ * LOG_ALPHA is 1 float.  get: n < n_required -> SPZ_EINVAL and *n_required set. */
+spz_status spz_get_params(spz_learner* L, spz_tensor t, spz_slot s, float* host_out, int64_t n,
+                          int64_t* n_required);
+spz_status spz_set_params(spz_learner* L, spz_tensor t, spz_slot s, const float* host_in, int64_t n);
+/* Adam step counters t of (critic, actor, alpha) optimizers and the global step. */
+spz_status spz_get_counters(spz_learner* L, int64_t* step, int64_t* t_critic, int64_t* t_actor, int64_t* t_alpha);
+
+/* Push the actor parameters peer-to-peer (north_star "actor
+ * parameters pushed peer-to-peer") into a buffer on dst_device laid out as
+ * [u64 version | u64 n_floats | n_floats fp32 (flat actor)]: the payload is
+ * written first and the 16-byte header last in stream order, so a reader that
+ * sees version v sees v's payload, never a blend.  The version is
+ * monotone per learner and returned in *version.  dst_bytes must be
+ * >= 16 + 4 * n_floats.  Synchronous. */
+spz_status spz_sync_actor(spz_learner* L, int32_t dst_device, void* dst, int64_t dst_bytes,
+                          uint64_t* version);
+
+/* Per kernel-class device time (ms per step, averaged over n_steps steps run
+ * un-graphed with CUDA events around each class) -- measurement only; the steps
+ * run are real updates.  names/ms arrays of capacity `cap`; *count set. */
+spz_status spz_learner_profile(spz_learner* L, int64_t batch, int64_t n_steps, int32_t cap,
+                               const char** names, double* ms, int32_t* count);
+/* Number of kernel launches one update step performs (for the bench's gpu_launches). */
+spz_status spz_learner_launches_per_step(spz_learner* L, int64_t batch, int32_t* launches);
+
+/* Copy an internal step buffer (as left by the last completed step) to host memory, for
+ * tests and diagnosis only.  Names: "Xa", "Xc", "H", "dH", "Aact<l>", "dZa<l>",
+ * "Aon<i>_<l>", "Atg<i>_<l>", "dZc<i>_<l>", "q_on<i>", "q_tg<i>", "gq<i>", "dXc<i>",
+ * "logp", "logp2", "r", "d", "y", "idx".  Raw bytes in the buffer's element type
+ * (*elem_size = 2 for bf16 operand buffers, 4 for fp32 / int32), sized for max_batch
+ * rows.  host_out == NULL only reports *bytes_required. */
+spz_status spz_learner_debug_buffer(spz_learner* L, const char* name, void* host_out, int64_t bytes,
+                                    int64_t* bytes_required, int32_t* elem_size);
+
+void spz_learner_destroy(spz_learner* L);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPZ_H_ */

@@ -60,9 +60,11 @@ class Ring:
         """Append n transitions; returns the global index of the first one."""
         rec = self.pack(obs, act, rew, next_obs, done)
         first = self.cursor
-        for t in range(rec.shape[0]):
-            self.records[(first + t) % self.C] = rec[t]
-        self.cursor += rec.shape[0]
+        n = rec.shape[0]
+        keep = min(n, self.C)  # only the last C records of a push survive
+        g = np.arange(first + n - keep, first + n)  # their global indices
+        self.records[g % self.C] = rec[n - keep:]
+        self.cursor += n
         return first
 
     def unpack(self, rows):

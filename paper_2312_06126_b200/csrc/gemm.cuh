@@ -1,0 +1,77 @@
+// gemm.cuh -- the GEMM contract used by every dense layer of the update.
+//
+// C[m, n] = epi( sum_k A(m, k) * B(n, k) ),  m < M (per group), n < N, k < K.
+//   A K-major : A(m,k) = A[m * lda + k]    (activations, row = batch row)
+//   A MN-major: A(m,k) = A[k * lda + m]    (wgrad: dZ stored [batch x out])
+//   B K-major : B(n,k) = B[n * ldb + k]    (forward: W stored [out x in])
+//   B MN-major: B(n,k) = B[k * ldb + n]    (dgrad: W stored [out x in], contraction over out;
+//                                            wgrad: activations stored [batch x in])
+// Split-K (wgrad, contraction over the batch) writes split s's partial sum to
+// C + s * split_stride; the fused Adam kernel sums splits in a fixed order, so
+// the result is deterministic (reading #16).
+// Up to 4 groups (e.g. the twin critics) share N, K, strides and epilogue
+// kind but have their own pointers and M.
+#pragma once
+
+#include "common.cuh"
+
+namespace spz {
+
+enum EpiKind : int {
+  EPI_BIAS_RELU = 0,  // C (T) = relu(acc + bias[n])                -- hidden layer forward
+  EPI_BIAS_F32 = 1,   // C (f32) = acc + bias[n]                    -- linear head forward
+  EPI_MASK = 2,       // C (T) = acc * (aux[m, n] > 0)              -- dgrad through ReLU
+  EPI_F32 = 3,        // C (f32) = acc                              -- wgrad partials / input dgrad
+};
+
+struct GemmGroup {
+  const void* A;
+  const void* B;
+  void* C;
+  const float* bias;
+  const void* aux;
+  int M;
+  int pad_;
+};
+
+struct GemmArgs {
+  int N, K;
+  int lda, ldb, ldc, ldaux;
+  int a_mn, b_mn;  // 0 = K-major, 1 = MN-major
+  int epi;
+  int splits;          // split-K count (>= 1)
+  int k_per_split;     // contraction rows per split (multiple of the K tile)
+  int64_t split_stride;  // elements between split partials in C
+  int n_groups;
+  GemmGroup g[4];
+};
+
+// Apply the epilogue to one accumulator element (shared by every GEMM backend).
+template <typename T>
+__device__ __forceinline__ void epi_store(const GemmArgs& a, const GemmGroup& g, int split, int m, int n, float acc) {
+  const int64_t off = (int64_t)m * a.ldc + n;
+  switch (a.epi) {
+    case EPI_BIAS_RELU: {
+      const float z = acc + g.bias[n];
+      static_cast<T*>(g.C)[off] = from_f<T>(z > 0.f ? z : 0.f);
+      break;
+    }
+    case EPI_BIAS_F32:
+      static_cast<float*>(g.C)[off] = acc + g.bias[n];
+      break;
+    case EPI_MASK: {
+      const float msk = to_f(static_cast<const T*>(g.aux)[(int64_t)m * a.ldaux + n]);
+      static_cast<T*>(g.C)[off] = from_f<T>(msk > 0.f ? acc : 0.f);
+      break;
+    }
+    default:
+      static_cast<float*>(g.C)[off + (int64_t)split * a.split_stride] = acc;
+      break;
+  }
+}
+
+// Portable fp32 SIMT GEMM (FP32 precision path).  Defined in gemm_simt.cu.
+template <typename T>
+cudaError_t gemm_simt(const GemmArgs& a, cudaStream_t st);
+
+}  // namespace spz

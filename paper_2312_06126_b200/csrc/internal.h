@@ -1,0 +1,44 @@
+// internal.h -- host-side objects behind the opaque spz handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/spz.h"
+#include "common.cuh"
+
+namespace spz {
+
+spz_status fail(spz_status st, const std::string& msg);
+spz_status check_device(int device);
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace spz
+
+struct spz_replay {
+  int o = 0, m = 0, R = 0;
+  int64_t C = 0;
+  int64_t cursor = 0;
+  int device = 0;
+  float* rec = nullptr;       // [C x R] fp32, device
+  float* staging = nullptr;   // pinned host staging for pushes
+  size_t staging_bytes = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  int64_t fill() const { return cursor < C ? cursor : C; }
+};

@@ -1,0 +1,487 @@
+// kernels.cuh -- the non-GEMM kernels of one update step.
+//
+// Each kernel cites the step it implements.  All reductions are fixed-order
+// (warp shuffles in a fixed tree, per-block partials summed in block order), so
+// an update is bit-reproducible run to run on a given device count (reading #16).
+#pragma once
+
+#include "common.cuh"
+
+namespace spz {
+
+constexpr int NSTAT = 6;  // per-block partial sums: (q1-y)^2+(q2-y)^2, q1, q2, alpha logp - minQ~ (or -Q1~), logp, spare
+constexpr float LN2F = 0.69314718055994530942f;
+constexpr float HALF_LN_2PI_F = 0.91893853320467274178f;
+
+__device__ __forceinline__ float softplusf(float x) { return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))); }
+
+// ------------------------------------------------------------------ a1 + a2: index + gather
+// Block = 32 rows.  Records are read with 128-bit loads into shared memory; each
+// operand region written by the block is contiguous, so stores are coalesced.
+// Writes (local row j, global row row0 + j):
+//   Xa[j] = s2, Xa[Bl + j] = s                           (actor input, [s2; s])
+//   Xc[j] = [s | a], Xc[Bl + j] = [s | 0], Xc[2Bl + j] = [s2 | 0]  (critic inputs)
+//   r[j], d[j]
+constexpr int GATHER_ROWS = 32;
+
+template <typename T>
+__global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ rec, int R, int o, int m,
+                                                     const int64_t* __restrict__ fill_p, uint64_t seed,
+                                                     const int64_t* __restrict__ step_p, int64_t row0, int Bl,
+                                                     T* __restrict__ Xa, int lda, T* __restrict__ Xc, int ldc,
+                                                     float* __restrict__ r, float* __restrict__ d,
+                                                     int32_t* __restrict__ idx_out) {
+  extern __shared__ float4 sm4[];
+  const float* sm = reinterpret_cast<const float*>(sm4);
+  __shared__ int64_t sidx[GATHER_ROWS];
+  const int j0 = blockIdx.x * GATHER_ROWS;
+  const int nr = min(GATHER_ROWS, Bl - j0);
+  const int64_t fill = *fill_p;
+  const uint64_t step = (uint64_t)*step_p;
+  if (threadIdx.x < nr) {
+    const int64_t i = sample_index(seed, step, (uint64_t)(row0 + j0 + threadIdx.x), (uint64_t)fill);
+    sidx[threadIdx.x] = i;
+    if (idx_out) idx_out[j0 + threadIdx.x] = (int32_t)i;
+  }
+  __syncthreads();
+  const int R4 = R >> 2;
+  for (int e = threadIdx.x; e < nr * R4; e += blockDim.x) {
+    const int rr = e / R4, q = e - rr * R4;
+    sm4[e] = __ldg(reinterpret_cast<const float4*>(rec + sidx[rr] * R) + q);
+  }
+  __syncthreads();
+  const int s2c = o + m + 2;
+  // actor input rows
+  for (int e = threadIdx.x; e < nr * lda; e += blockDim.x) {
+    const int rr = e / lda, c = e - rr * lda;
+    const float* rw = sm + rr * R;
+    Xa[(int64_t)(j0 + rr) * lda + c] = from_f<T>(c < o ? rw[s2c + c] : 0.f);
+    Xa[(int64_t)(Bl + j0 + rr) * lda + c] = from_f<T>(c < o ? rw[c] : 0.f);
+  }
+  for (int e = threadIdx.x; e < nr * ldc; e += blockDim.x) {
+    const int rr = e / ldc, c = e - rr * ldc;
+    const float* rw = sm + rr * R;
+    Xc[(int64_t)(j0 + rr) * ldc + c] = from_f<T>(c < o + m ? rw[c] : 0.f);
+    Xc[(int64_t)(Bl + j0 + rr) * ldc + c] = from_f<T>(c < o ? rw[c] : 0.f);
+    Xc[(int64_t)(2 * Bl + j0 + rr) * ldc + c] = from_f<T>(c < o ? rw[s2c + c] : 0.f);
+  }
+  if (threadIdx.x < nr) {
+    r[j0 + threadIdx.x] = sm[threadIdx.x * R + o + m];
+    d[j0 + threadIdx.x] = sm[threadIdx.x * R + o + m + 1];
+  }
+}
+
+// ------------------------------------------------------------------ a3: SAC actor head (forward)
+// Row r < Bl is the s2-row j = r (noise eps' from S_EPS2) and produces a', log pi';
+// row r >= Bl is the s-row j = r - Bl (eps from S_EPS) and produces a~, log pi~ plus
+// the per-element cache the head backward needs.  [mu | l] = H[r, 0:2m];
+// lc = clamp(l, lo, hi); sigma = exp(lc); u = mu + sigma eps; a = tanh u;
+// log pi = sum_i [-eps^2/2 - lc - ln(2 pi)/2 - 2 (ln 2 - u - softplus(-2u))].
+struct HeadCache {
+  float *u, *a, *eps, *sig, *l;  // [Bl x m] each, s-rows only
+};
+
+template <typename T>
+__global__ void sac_head_fwd_kernel(const float* __restrict__ H, int ldh, int m, int Bl, int64_t row0, uint64_t seed,
+                                    const int64_t* __restrict__ step_p, float lo, float hi, T* __restrict__ Xc, int ldc,
+                                    int o, HeadCache cache, float* __restrict__ logp2, float* __restrict__ logp) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= 2 * Bl) return;
+  const bool s2row = r < Bl;
+  const int j = s2row ? r : r - Bl;
+  const uint64_t step = (uint64_t)*step_p;
+  const uint32_t stream = s2row ? S_EPS2 : S_EPS;
+  T* xa = Xc + (int64_t)(s2row ? 2 * Bl + j : Bl + j) * ldc + o;
+  float lp = 0.f;
+  for (int i = 0; i < m; ++i) {
+    const float mu = H[(int64_t)r * ldh + i];
+    const float l = H[(int64_t)r * ldh + m + i];
+    const float lc = fminf(fmaxf(l, lo), hi);
+    const float sg = expf(lc);
+    const float e = normal_q(seed, step, stream, (uint64_t)(row0 + j), i);
+    const float u = fmaf(sg, e, mu);
+    const float a = tanhf(u);
+    lp += -0.5f * e * e - lc - HALF_LN_2PI_F - 2.f * (LN2F - u - softplusf(-2.f * u));
+    xa[i] = from_f<T>(a);
+    if (!s2row) {
+      const int64_t ci = (int64_t)j * m + i;
+      cache.u[ci] = u;
+      cache.a[ci] = a;
+      cache.eps[ci] = e;
+      cache.sig[ci] = sg;
+      cache.l[ci] = l;
+    }
+  }
+  if (s2row) logp2[j] = lp;
+  else logp[j] = lp;
+}
+
+// ------------------------------------------------------------------ a3: TD3 actor heads (forward)
+// Rows r < Bl: target actor on s2, a' = clip(tanh(z) + clip(noise * n, -c, c), -1, 1) with n from
+// S_SMOOTH (written into Xc[2Bl + r]); rows Bl <= r < M: online actor on s, a~ = tanh(z)
+// (written into Xc[r], cached for the backward).  P:576, reading #18.
+template <typename T>
+__global__ void td3_head_fwd_kernel(const float* __restrict__ H, int ldh, int m, int Bl, int M, int64_t row0,
+                                    uint64_t seed, const int64_t* __restrict__ step_p, float noise, float clipc,
+                                    T* __restrict__ Xc, int ldc, int o, float* __restrict__ a_cache) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= M) return;
+  const uint64_t step = (uint64_t)*step_p;
+  if (r < Bl) {
+    T* xa = Xc + (int64_t)(2 * Bl + r) * ldc + o;
+    for (int i = 0; i < m; ++i) {
+      const float n = normal_q(seed, step, S_SMOOTH, (uint64_t)(row0 + r), i);
+      const float xi = fminf(fmaxf(noise * n, -clipc), clipc);
+      const float a = fminf(fmaxf(tanhf(H[(int64_t)r * ldh + i]) + xi, -1.f), 1.f);
+      xa[i] = from_f<T>(a);
+    }
+  } else {
+    const int j = r - Bl;
+    T* xa = Xc + (int64_t)(Bl + j) * ldc + o;
+    for (int i = 0; i < m; ++i) {
+      const float a = tanhf(H[(int64_t)r * ldh + i]);
+      xa[i] = from_f<T>(a);
+      a_cache[(int64_t)j * m + i] = a;
+    }
+  }
+}
+
+// TD3 actor head backward: dZ_out = g_a (1 - a~^2) with g_a the Q1 input gradient's action columns.
+template <typename T>
+__global__ void td3_head_bwd_kernel(const float* __restrict__ dX1, int ldx, int o, int m, int Bl,
+                                    const float* __restrict__ a_cache, T* __restrict__ dH, int ldh) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)Bl * m) return;
+  const int64_t j = e / m;
+  const int i = (int)(e - j * m);
+  const float a = a_cache[e];
+  dH[j * ldh + i] = from_f<T>(dX1[j * ldx + o + i] * (1.f - a * a));
+}
+
+// ------------------------------------------------------------------ a4/a5: critic head (N = 1) row dot
+// q[r] = sum_n A[r, n] w[n] + b, one warp per row, fixed shuffle tree.
+struct RowdotGroup {
+  const void* A;
+  const float* w;
+  const float* b;
+  float* q;
+};
+struct RowdotArgs {
+  int M, h, ld;
+  RowdotGroup g[4];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) rowdot_kernel(const __grid_constant__ RowdotArgs a) {
+  const RowdotGroup& g = a.g[blockIdx.y];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= a.M) return;
+  const T* row = static_cast<const T*>(g.A) + (int64_t)warp * a.ld;
+  float s = 0.f;
+  for (int n = lane; n < a.h; n += 32) s = fmaf(to_f(row[n]), g.w[n], s);
+  s = warp_sum(s);
+  if (lane == 0) g.q[warp] = s + g.b[0];
+}
+
+// ------------------------------------------------------------------ block reduction of NSTAT doubles
+template <int NT>
+__device__ __forceinline__ void block_stats(double (&v)[NSTAT], double* __restrict__ out) {
+  __shared__ double red[NT / 32][NSTAT];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NSTAT; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NSTAT; ++i) red[w][i] = v[i];
+  __syncthreads();
+  if (threadIdx.x < NSTAT) {
+    double s = 0.0;
+    for (int k = 0; k < NT / 32; ++k) s += red[k][threadIdx.x];
+    out[blockIdx.x * NSTAT + threadIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------------------ a4 + a5: Bellman target, critic losses, head gradients
+// Row j in [0, Bl):  y = r + gamma (1-d) (min(q'1, q'2) - alpha log pi');
+//   loss rows:  g_qi[j] = 2 (q_i(s,a) - y) / B
+//   actor rows: g_qi[Bl + j] = -w_i / B with (w1, w2) = (1,0) | (0,1) | (1/2,1/2) on a tie.
+// TD3 (td3 = 1): no entropy term, actor rows use Q1 only with g = -1/B (only if actor_on).
+constexpr int LOSS_NT = 256;
+
+__global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(
+    const float* __restrict__ qt1, const float* __restrict__ qt2, const float* __restrict__ q1,
+    const float* __restrict__ q2, const float* __restrict__ logp2, const float* __restrict__ logp,
+    const float* __restrict__ r, const float* __restrict__ d, const float* __restrict__ log_alpha, float gamma,
+    float invB, int Bl, int td3, const int64_t* __restrict__ step_p, int delay, float* __restrict__ gq1,
+    float* __restrict__ gq2, float* __restrict__ y_out, double* __restrict__ partials) {
+  const int j = blockIdx.x * LOSS_NT + threadIdx.x;
+  double v[NSTAT] = {0, 0, 0, 0, 0, 0};
+  if (j < Bl) {
+    const float alpha = td3 ? 0.f : expf(*log_alpha);
+    const float qmin = fminf(qt1[j], qt2[j]);
+    const float boot = td3 ? qmin : qmin - alpha * logp2[j];
+    const float y = r[j] + gamma * (1.f - d[j]) * boot;
+    y_out[j] = y;
+    const float e1 = q1[j] - y, e2 = q2[j] - y;
+    gq1[j] = 2.f * e1 * invB;
+    gq2[j] = 2.f * e2 * invB;
+    v[0] = (double)e1 * e1 + (double)e2 * e2;
+    v[1] = q1[j];
+    v[2] = q2[j];
+    const float a1 = q1[Bl + j], a2 = q2[Bl + j];
+    if (!td3) {
+      const float w1 = a1 < a2 ? 1.f : (a1 > a2 ? 0.f : 0.5f);
+      gq1[Bl + j] = -w1 * invB;
+      gq2[Bl + j] = -(1.f - w1) * invB;
+      v[3] = (double)alpha * logp[j] - (double)fminf(a1, a2);
+      v[4] = logp[j];
+    } else {
+      const bool on = ((*step_p + 1) % delay) == 0;
+      gq1[Bl + j] = on ? -invB : 0.f;
+      gq2[Bl + j] = 0.f;
+      v[3] = on ? -(double)a1 : 0.0;
+    }
+  }
+  block_stats<LOSS_NT>(v, partials);
+}
+
+// ------------------------------------------------------------------ a6: critic head backward
+// dZ_L[r, n] = g_q[r] * w_out[n] * 1[A_L[r, n] > 0]   (two critics via blockIdx.y)
+struct HeadBwdGroup {
+  const float* gq;
+  const float* w;
+  const void* A;
+  void* dZ;
+};
+struct HeadBwdArgs {
+  int64_t M;
+  int h, ld;
+  HeadBwdGroup g[2];
+};
+
+template <typename T>
+__global__ void critic_head_bwd_kernel(const __grid_constant__ HeadBwdArgs a) {
+  const HeadBwdGroup& g = a.g[blockIdx.y];
+  const T* A = static_cast<const T*>(g.A);
+  T* dZ = static_cast<T*>(g.dZ);
+  const int64_t total = a.M * a.h;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = e / a.h;
+    const int n = (int)(e - rr * a.h);
+    const float act = to_f(A[rr * a.ld + n]);
+    dZ[rr * a.ld + n] = from_f<T>(act > 0.f ? g.gq[rr] * g.w[n] : 0.f);
+  }
+}
+
+// ------------------------------------------------------------------ a7: SAC actor head backward (eq. H)
+// g_a = dL/da~ = sum over critics of the input-gradient action columns; g_lp = alpha / B.
+// g_u = g_a (1 - a^2) + 2 a g_lp;  g_mu = g_u;  g_l = (g_u sigma eps - g_lp) 1[lo <= l <= hi].
+template <typename T>
+__global__ void sac_head_bwd_kernel(const float* __restrict__ dX1, const float* __restrict__ dX2, int ldx, int o, int m,
+                                    int Bl, HeadCache cache, const float* __restrict__ log_alpha, float invB, float lo,
+                                    float hi, T* __restrict__ dH, int ldh) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)Bl * m) return;
+  const int64_t j = e / m;
+  const int i = (int)(e - j * m);
+  const float g_lp = expf(*log_alpha) * invB;
+  const float ga = dX1[j * ldx + o + i] + dX2[j * ldx + o + i];
+  const float a = cache.a[e];
+  const float gu = ga * (1.f - a * a) + 2.f * a * g_lp;
+  const float l = cache.l[e];
+  const float gl = (l >= lo && l <= hi) ? (gu * cache.sig[e] * cache.eps[e] - g_lp) : 0.f;
+  dH[j * ldh + i] = from_f<T>(gu);
+  dH[j * ldh + m + i] = from_f<T>(gl);
+}
+
+// ------------------------------------------------------------------ bias / head-weight gradients: column sums
+// partial[s][n] = sum_{r in rows of split s} w[r] X[r, n]  (w nullable), fixed order.
+constexpr int CS_COLS = 32, CS_ROWS = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(CS_COLS* CS_ROWS) colsum_kernel(const T* __restrict__ X, int ld, int N, int M,
+                                                                  int rows_per_split, const float* __restrict__ w,
+                                                                  float* __restrict__ partial) {
+  __shared__ float red[CS_ROWS][CS_COLS];
+  const int tc = threadIdx.x % CS_COLS, tr = threadIdx.x / CS_COLS;
+  const int n = blockIdx.x * CS_COLS + tc;
+  const int s = blockIdx.y;
+  const int r0 = s * rows_per_split, r1 = min(M, r0 + rows_per_split);
+  float acc = 0.f;
+  if (n < N)
+    for (int rr = r0 + tr; rr < r1; rr += CS_ROWS) {
+      const float x = to_f(X[(int64_t)rr * ld + n]);
+      acc = w ? fmaf(w[rr], x, acc) : acc + x;
+    }
+  red[tr][tc] = acc;
+  __syncthreads();
+  if (tr == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < CS_ROWS; ++k) t += red[k][tc];
+    partial[(int64_t)s * N + n] = t;
+  }
+}
+
+// ------------------------------------------------------------------ a7 (alpha) + statistics
+// Sums the per-block partials in block order; writes the step statistics, the
+// log-alpha gradient g = -(mean log pi~ + H_bar) and the non-finite flag.
+struct StatsOut {
+  double step, critic_loss, actor_loss, alpha, alpha_loss, q1_mean, q2_mean, logp_mean;
+};
+
+__global__ void stats_kernel(const double* __restrict__ partials, int nblocks, const double* __restrict__ extra,
+                             const float* __restrict__ log_alpha, double target_entropy, double B, int td3,
+                             const int64_t* __restrict__ step_p, int delay, StatsOut* __restrict__ out,
+                             float* __restrict__ g_log_alpha, int* __restrict__ flag) {
+  __shared__ double tot[NSTAT];
+  if (threadIdx.x < NSTAT) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += partials[b * NSTAT + threadIdx.x];
+    if (extra) s = extra[threadIdx.x];  // multi-rank: already all-reduced totals
+    tot[threadIdx.x] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double la = *log_alpha;
+    StatsOut o;
+    o.step = (double)(*step_p + 1);
+    o.critic_loss = tot[0] / B;
+    o.q1_mean = tot[1] / B;
+    o.q2_mean = tot[2] / B;
+    o.actor_loss = tot[3] / B;
+    o.logp_mean = td3 ? 0.0 : tot[4] / B;
+    o.alpha = td3 ? 0.0 : exp(la);
+    o.alpha_loss = td3 ? 0.0 : -la * (o.logp_mean + target_entropy);
+    *out = o;
+    if (g_log_alpha) *g_log_alpha = (float)(-(o.logp_mean + target_entropy));
+    const bool bad = !isfinite(o.critic_loss) || !isfinite(o.actor_loss) || !isfinite(o.q1_mean) ||
+                     !isfinite(o.q2_mean) || !isfinite(o.logp_mean);
+    if (bad) *flag = 1;
+  }
+}
+
+// ------------------------------------------------------------------ a9: fused multi-tensor Adam + Polyak
+// One block per segment of <= ADAM_SEG elements of one tensor.  For each element:
+// g = sum_s partial[s] (fixed order); Adam with the optimizer's own t; master,
+// m, v updated; operand shadow (T, padded row stride) refreshed; if the tensor
+// has a target: theta' = tau theta_new + (1 - tau) theta' (+ its shadow).
+constexpr int ADAM_SEG = 4096;
+
+struct AdamTensor {
+  int64_t p_off;      // master offset of element 0
+  int64_t numel;
+  const float* partials;
+  int32_t n_partials;
+  int32_t opt;        // 0 critic, 1 actor, 2 alpha
+  int32_t cols;       // > 0: weight matrix with shadow row stride ld
+  int32_t ld;
+  int64_t s_off;      // shadow offset (elements) of element 0, -1 if none
+  int64_t t_off;      // target master offset, -1 if none
+  int64_t ts_off;     // target shadow offset, -1 if none
+};
+struct AdamSegment {
+  int32_t tensor;
+  int32_t count;
+  int64_t start;      // element index within the tensor
+};
+struct AdamHyper {
+  float lr[3];
+  float beta1, beta2, eps, tau;
+  int td3, delay;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) adam_polyak_kernel(const AdamTensor* __restrict__ tensors,
+                                                          const AdamSegment* __restrict__ segs, AdamHyper hp,
+                                                          float* __restrict__ P, float* __restrict__ Mo,
+                                                          float* __restrict__ Vo, T* __restrict__ S,
+                                                          const int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
+                                                          int* __restrict__ flag) {
+  if (*flag) return;  // halted: parameters stay at the state before the failing step
+  const AdamSegment sg = segs[blockIdx.x];
+  const AdamTensor tn = tensors[sg.tensor];
+  const int64_t step = counters[0];
+  bool delayed = true;
+  if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
+  if (hp.td3 && tn.opt == 1 && !delayed) return;  // TD3 actor: only on delayed steps
+  const int64_t t = counters[1 + tn.opt] + 1;
+  const float bc1 = (float)(1.0 - pow((double)hp.beta1, (double)t));
+  const float bc2 = (float)(1.0 - pow((double)hp.beta2, (double)t));
+  const float lr = hp.lr[tn.opt];
+  const bool do_polyak = tn.t_off >= 0 && (!hp.td3 || delayed);
+  for (int k = threadIdx.x; k < sg.count; k += blockDim.x) {
+    const int64_t i = sg.start + k;
+    float g = 0.f;
+    for (int s = 0; s < tn.n_partials; ++s) g += tn.partials[(int64_t)s * tn.numel + i];
+    if (!isfinite(g)) {
+      atomicExch(flag, 2);
+      continue;
+    }
+    const int64_t pi = tn.p_off + i;
+    const float m = hp.beta1 * Mo[pi] + (1.f - hp.beta1) * g;
+    const float v = hp.beta2 * Vo[pi] + (1.f - hp.beta2) * g * g;
+    Mo[pi] = m;
+    Vo[pi] = v;
+    const float p = P[pi] - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
+    P[pi] = p;
+    int64_t so = -1;
+    if (tn.cols > 0) {
+      const int64_t row = i / tn.cols, col = i - row * tn.cols;
+      so = row * tn.ld + col;
+      S[tn.s_off + so] = from_f<T>(p);
+    }
+    if (do_polyak) {
+      const int64_t ti = tn.t_off + i;
+      const float tp = hp.tau * p + (1.f - hp.tau) * P[ti];
+      P[ti] = tp;
+      if (so >= 0) S[tn.ts_off + so] = from_f<T>(tp);
+    }
+  }
+}
+
+// Target-only Polyak for tensors without an optimizer on this rank (TD3 target actor
+// when the actor lives elsewhere is not needed in co-located mode) -- unused for now.
+
+// Advance the step and optimizer counters (after every kernel of the step has run).
+__global__ void advance_kernel(int64_t* __restrict__ counters, const int* __restrict__ flag, int td3, int delay,
+                               int alpha_auto, int critic_on, int actor_on) {
+  if (*flag) return;
+  const int64_t step = counters[0];
+  const bool delayed = !td3 || ((step + 1) % delay) == 0;
+  if (critic_on) counters[1] += 1;
+  if (actor_on && delayed) counters[2] += 1;
+  if (actor_on && alpha_auto && !td3) counters[3] += 1;
+  counters[0] = step + 1;
+}
+
+// ------------------------------------------------------------------ shadow refresh + init
+struct ShadowEntry {
+  int64_t p_off;  // master offset of W
+  int32_t rows, cols, ld;
+  int64_t s_off;
+};
+
+template <typename T>
+__global__ void shadow_refresh_kernel(const ShadowEntry* __restrict__ ents, int n_ents, const float* __restrict__ P,
+                                      T* __restrict__ S) {
+  const ShadowEntry e = ents[blockIdx.y];
+  const int64_t total = (int64_t)e.rows * e.ld;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = k / e.ld;
+    const int col = (int)(k - row * e.ld);
+    S[e.s_off + k] = from_f<T>(col < e.cols ? P[e.p_off + row * e.cols + col] : 0.f);
+  }
+}
+
+// W, b ~ U(+-bound) with bound = 1/sqrt(fan_in), from Philox(init_seed, ctr = (e, net, 0, S_INIT)).
+__global__ void init_uniform_kernel(float* __restrict__ P, int64_t off, int64_t n, float bound, uint64_t seed,
+                                    uint32_t net, int64_t e0) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = (uint64_t)(e0 + k);
+    const uint4 x = philox(make_uint4((uint32_t)e, (uint32_t)(e >> 32), net, S_INIT), (uint32_t)seed, (uint32_t)(seed >> 32));
+    P[off + k] = (2.f * u01(x.x) - 1.f) * bound;
+  }
+}
+
+}  // namespace spz

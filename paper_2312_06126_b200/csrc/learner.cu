@@ -1,0 +1,1133 @@
+// learner.cu -- the update step: buffers, the per-batch launch plan, CUDA-graph replay, C API.
+//
+// One step is a fixed chain of device kernels with no host
+// round-trip: gather -> actor forward on [s2; s] -> head -> target critics -> online
+// critics -> Bellman target + losses -> critic backward -> actor backward ->
+// statistics -> fused Adam + Polyak -> counter advance.  The chain is captured once
+// per batch size into a CUDA graph and replayed n_steps times; the step counter and
+// the ring fill live in device memory so the replay needs no host updates.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+
+#include "gemm.cuh"
+#include "internal.h"
+#include "kernels.cuh"
+#include "tc_gemm.cuh"
+
+namespace spz {
+
+enum NetId { NET_ACTOR = 0, NET_Q1 = 1, NET_Q2 = 2, NET_Q1T = 3, NET_Q2T = 4, NET_ACTORT = 5, N_NETS = 6 };
+
+struct NetLayout {
+  int nl = 0;
+  int in[8] = {}, out[8] = {};
+  int64_t w[8] = {}, b[8] = {};  // master offsets relative to the net base
+  int ld[8] = {};                // shadow row stride (elements, multiple of 8 -> 16-byte rows)
+  int64_t sw[8] = {};            // shadow offsets relative to the net shadow base
+  int64_t np = 0, ns = 0;
+};
+
+static NetLayout make_layout(int in, int h, int L, int out) {
+  NetLayout n;
+  n.nl = L + 1;
+  int64_t p = 0, s = 0;
+  for (int l = 0; l <= L; ++l) {
+    n.in[l] = l == 0 ? in : h;
+    n.out[l] = l == L ? out : h;
+    n.w[l] = p;
+    p += (int64_t)n.in[l] * n.out[l];
+    n.b[l] = p;
+    p += n.out[l];
+    n.ld[l] = (int)round_up(n.in[l], 8);
+    n.sw[l] = s;
+    s += round_up((int64_t)n.out[l] * n.ld[l], 64);
+  }
+  n.np = p;
+  n.ns = s;
+  return n;
+}
+
+struct Op {
+  const char* cls;
+  std::function<cudaError_t(cudaStream_t)> fn;
+  int launches = 1;  // kernels this op launches
+};
+
+template <typename T>
+static cudaError_t run_gemm(const GemmArgs& a, cudaStream_t st) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (tc_gemm_supported(a)) return tc_gemm_bf16(a, st);
+  }
+  return gemm_simt<T>(a, st);
+}
+
+}  // namespace spz
+
+using namespace spz;
+
+struct spz_learner {
+  spz_config cfg{};
+  spz_replay* ring = nullptr;
+  int device = 0;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  bool td3 = false, bf16 = false;
+  int o = 0, m = 0, h = 0, L = 0;
+  size_t esz = 4;
+  int64_t max_local = 0;  // rows handled by this rank at max_batch
+  int64_t row0_max = 0;
+
+  NetLayout net[N_NETS];
+  bool has_net[N_NETS] = {};
+  int64_t pbase[N_NETS] = {}, sbase[N_NETS] = {};
+  int64_t p_log_alpha = 0, P_total = 0, S_total = 0;
+  float *P = nullptr, *Mo = nullptr, *Vo = nullptr;
+  void* S = nullptr;
+  int64_t* counters = nullptr;  // step, t_critic, t_actor, t_alpha
+  int64_t* d_fill = nullptr;
+  int* d_flag = nullptr;
+  StatsOut* d_stats = nullptr;
+  StatsOut* h_stats = nullptr;  // pinned
+  int* h_flag = nullptr;        // pinned
+  int64_t* h_counters = nullptr;  // pinned
+
+  // activations (T unless noted); sized for max_local rows
+  void *Xa = nullptr, *Xc = nullptr, *dH = nullptr;
+  int lda = 0, ldc = 0, ldh = 0;
+  void* Aact[8] = {};
+  void* dZa[8] = {};
+  void* Aon[2][8] = {};
+  void* Atg[2][8] = {};
+  void* dZc[2][8] = {};
+  float* H = nullptr;
+  float *q_on[2] = {}, *q_tg[2] = {}, *gq[2] = {}, *dXc[2] = {};
+  float *logp = nullptr, *logp2 = nullptr, *r = nullptr, *d = nullptr, *y = nullptr;
+  HeadCache cache{};
+  int32_t* idx = nullptr;
+  double* stat_partials = nullptr;
+  int max_stat_blocks = 0;
+  float* G = nullptr;  // gradient partials
+  int64_t G_total = 0;
+  AdamTensor* d_tensors = nullptr;
+  AdamSegment* d_segs = nullptr;
+  int max_tensors = 64, max_segs = 0;
+  ShadowEntry* d_shadow = nullptr;
+  int n_shadow = 0;
+
+  // plan
+  int64_t plan_B = -1;
+  std::vector<Op> ops[2];  // [0] = plain step, [1] = TD3 delayed step (SAC uses [0] only)
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  int n_adam_segs = 0;
+  uint64_t sync_version = 0;
+  std::vector<void*> allocs;
+  struct DebugBuf { std::string name; void* ptr; size_t bytes; int esz; };
+  std::vector<DebugBuf> debug;
+
+  ~spz_learner();
+};
+
+namespace spz {
+
+static spz_status dalloc(spz_learner* Lr, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (cudaMalloc(p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SPZ_ENOMEM, "spz_learner_create: cannot allocate " + std::to_string(bytes) + " device bytes");
+  }
+  Lr->allocs.push_back(*p);
+  // ordered on the learner's own (non-blocking) stream: the legacy default stream is not
+  if (cudaMemsetAsync(*p, 0, bytes, Lr->own_stream) != cudaSuccess) return fail(SPZ_ECUDA, "cudaMemsetAsync failed");
+  return SPZ_OK;
+}
+
+#define SPZ_TRY(expr)            \
+  do {                           \
+    spz_status _s = (expr);      \
+    if (_s != SPZ_OK) return _s; \
+  } while (0)
+
+static int wgrad_splits(int64_t Bl) {
+  // enough CTAs to cover the SMs several times over for the skinny [h x Bl] x [Bl x in] products
+  int s = (int)std::max<int64_t>(1, std::min<int64_t>(32, Bl / 256));
+  return s;
+}
+static int64_t wgrad_rows(int64_t Bl, int s) { return round_up(cdiv(Bl, s), 128); }
+static int bias_splits(int64_t Bl) { return (int)std::max<int64_t>(1, std::min<int64_t>(64, cdiv(Bl, 512))); }
+
+// Gradient partial regions (one per trained tensor), laid out at create time for the
+// largest split counts.
+struct TensorSlot {
+  int net, layer;
+  bool weight;
+  int64_t numel;
+  int64_t g_off;
+  int max_partials;
+};
+
+static std::vector<TensorSlot> trained_tensors(spz_learner* Lr) {
+  std::vector<TensorSlot> v;
+  const bool actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC, critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
+  const int Sw = wgrad_splits(Lr->max_local), Sb = bias_splits(Lr->max_local);
+  auto add_net = [&](int id) {
+    const NetLayout& n = Lr->net[id];
+    for (int l = 0; l < n.nl; ++l) {
+      const bool head_vec = (id == NET_Q1 || id == NET_Q2) && l == n.nl - 1;  // N = 1 head: column sums
+      v.push_back({id, l, true, (int64_t)n.out[l] * n.in[l], 0, head_vec ? Sb : Sw});
+      v.push_back({id, l, false, (int64_t)n.out[l], 0, Sb});
+    }
+  };
+  if (critic_on) {
+    add_net(NET_Q1);
+    add_net(NET_Q2);
+  }
+  if (actor_on) add_net(NET_ACTOR);
+  int64_t off = 0;
+  for (auto& t : v) {
+    t.g_off = off;
+    off += round_up(t.numel * t.max_partials, 64);
+  }
+  Lr->G_total = off + 64;  // + log alpha gradient slot at the end
+  return v;
+}
+
+template <typename T>
+static spz_status build_plan(spz_learner* Lr, int64_t B);
+spz_status refresh_shadows(spz_learner* Lr);
+
+}  // namespace spz
+
+spz_learner::~spz_learner() {
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  if (own_stream) cudaStreamSynchronize(own_stream);
+  for (auto& e : exec)
+    if (e) cudaGraphExecDestroy(e);
+  for (void* p : allocs) cudaFree(p);
+  if (h_stats) cudaFreeHost(h_stats);
+  if (h_flag) cudaFreeHost(h_flag);
+  if (h_counters) cudaFreeHost(h_counters);
+  if (own_stream) cudaStreamDestroy(own_stream);
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+namespace spz {
+
+// ----------------------------------------------------------------------------- plan
+template <typename T>
+static spz_status build_plan(spz_learner* Lr, int64_t B) {
+  for (auto& v : Lr->ops) v.clear();
+  for (auto& e : Lr->exec)
+    if (e) {
+      cudaGraphExecDestroy(e);
+      e = nullptr;
+    }
+  const int W = Lr->cfg.world_size, rk = Lr->cfg.rank;
+  const int64_t base = B / W, rem = B % W;
+  const int Bl = (int)(base + (rk < rem ? 1 : 0));
+  const int64_t row0 = rk * base + std::min<int64_t>(rk, rem);
+  const int o = Lr->o, m = Lr->m, h = Lr->h, L = Lr->L;
+  const bool td3 = Lr->td3;
+  const float invB = (float)(1.0 / (double)B);
+  T* S = static_cast<T*>(Lr->S);
+  float* P = Lr->P;
+  const int lda = Lr->lda, ldc = Lr->ldc, ldh = Lr->ldh;
+  const uint64_t seed = Lr->cfg.seed;
+  const float lo = (float)Lr->cfg.log_std_min, hi = (float)Lr->cfg.log_std_max;
+  const int delay = std::max(1, Lr->cfg.td3_policy_delay);
+  const int Sw = wgrad_splits(Bl), Sb = bias_splits(Bl);
+  const int64_t rows_w = wgrad_rows(Bl, Sw), rows_b = cdiv(Bl, Sb);
+  auto Wp = [&](int id, int l) -> const T* { return S + Lr->sbase[id] + Lr->net[id].sw[l]; };
+  auto bp = [&](int id, int l) -> const float* { return P + Lr->pbase[id] + Lr->net[id].b[l]; };
+  auto ldw = [&](int id, int l) { return Lr->net[id].ld[l]; };
+  auto Ta = [&](void* p, int64_t row, int ld) -> T* { return static_cast<T*>(p) + row * ld; };
+
+  std::vector<TensorSlot> slots = trained_tensors(Lr);
+  auto slot_of = [&](int id, int l, bool w) -> TensorSlot& {
+    for (auto& s : slots)
+      if (s.net == id && s.layer == l && s.weight == w) return s;
+    return slots[0];
+  };
+
+  for (int variant = 0; variant < (td3 ? 2 : 1); ++variant) {
+    std::vector<Op>& ops = Lr->ops[variant];
+    const bool actor_step = !td3 || variant == 1;  // TD3: actor work only on delayed steps
+    auto gemm = [&](const char* cls, GemmArgs a) {
+      ops.push_back({cls, [a](cudaStream_t st) { return run_gemm<T>(a, st); }});
+    };
+    auto fwd_args = [&](int N, int K, int ldA, int ldB, int ldC, int epi) {
+      GemmArgs a{};
+      a.N = N;
+      a.K = K;
+      a.lda = ldA;
+      a.ldb = ldB;
+      a.ldc = ldC;
+      a.epi = epi;
+      a.splits = 1;
+      a.k_per_split = K;
+      return a;
+    };
+
+    // ---- a1 + a2: Philox indices + gather
+    {
+      const float* rec = Lr->ring->rec;
+      const int R = Lr->ring->R;
+      const int64_t* fill = Lr->d_fill;
+      const int64_t* stp = Lr->counters;
+      T *Xa = static_cast<T*>(Lr->Xa), *Xc = static_cast<T*>(Lr->Xc);
+      float *rr = Lr->r, *dd = Lr->d;
+      int32_t* idx = Lr->idx;
+      const size_t smem = (size_t)GATHER_ROWS * R * sizeof(float);
+      ops.push_back({"gather", [=](cudaStream_t st) {
+                       gather_kernel<T><<<(unsigned)cdiv(Bl, GATHER_ROWS), 256, smem, st>>>(
+                           rec, R, o, m, fill, seed, stp, row0, Bl, Xa, lda, Xc, ldc, rr, dd, idx);
+                       return cudaGetLastError();
+                     }});
+    }
+    // ---- a3: actor forward.  SAC: online actor on [s2; s] (M = 2Bl).
+    //      TD3: target actor on s2 (rows 0..Bl) every step, online actor on s on delayed steps.
+    {
+      const NetLayout& an = Lr->net[NET_ACTOR];
+      struct Pass { int id; int64_t row; int M; };
+      std::vector<Pass> passes;
+      if (!td3) passes.push_back({NET_ACTOR, 0, 2 * Bl});
+      else {
+        passes.push_back({NET_ACTORT, 0, Bl});
+        if (actor_step) passes.push_back({NET_ACTOR, Bl, Bl});
+      }
+      for (const Pass& ps : passes) {
+        for (int l = 0; l < an.nl; ++l) {
+          const bool last = l == an.nl - 1;
+          GemmArgs a = fwd_args(an.out[l], an.in[l], l == 0 ? lda : h, ldw(ps.id, l), last ? ldh : h,
+                                last ? EPI_BIAS_F32 : EPI_BIAS_RELU);
+          a.n_groups = 1;
+          a.g[0].A = l == 0 ? (const void*)Ta(Lr->Xa, ps.row, lda) : (const void*)Ta(Lr->Aact[l - 1], ps.row, h);
+          a.g[0].B = Wp(ps.id, l);
+          a.g[0].C = last ? (void*)(Lr->H + ps.row * ldh) : (void*)Ta(Lr->Aact[l], ps.row, h);
+          a.g[0].bias = bp(ps.id, l);
+          a.g[0].M = ps.M;
+          gemm(last ? "actor_head_gemm" : "actor_fwd_gemm", a);
+        }
+      }
+      float* Hh = Lr->H;
+      T* Xc = static_cast<T*>(Lr->Xc);
+      HeadCache cache = Lr->cache;
+      float *lp = Lr->logp, *lp2 = Lr->logp2;
+      const int64_t* stp = Lr->counters;
+      if (!td3) {
+        ops.push_back({"actor_head", [=](cudaStream_t st) {
+                         sac_head_fwd_kernel<T><<<(unsigned)cdiv(2 * Bl, 128), 128, 0, st>>>(
+                             Hh, ldh, m, Bl, row0, seed, stp, lo, hi, Xc, ldc, o, cache, lp2, lp);
+                         return cudaGetLastError();
+                       }});
+      } else {
+        const float ns = (float)Lr->cfg.td3_noise, nc = (float)Lr->cfg.td3_noise_clip;
+        const bool on = actor_step;
+        ops.push_back({"actor_head", [=](cudaStream_t st) {
+                         td3_head_fwd_kernel<T><<<(unsigned)cdiv(on ? 2 * Bl : Bl, 128), 128, 0, st>>>(
+                             Hh, ldh, m, Bl, on ? 2 * Bl : Bl, row0, seed, stp, ns, nc, Xc, ldc, o, cache.a);
+                         return cudaGetLastError();
+                       }});
+      }
+    }
+    // ---- a4: target critics on [s2 | a'] (M = Bl), a5: online critics on [s | a ; s | a~] (M = 2Bl)
+    const NetLayout& cn = Lr->net[NET_Q1];
+    const int Mon = actor_step ? 2 * Bl : Bl;
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool tgt = pass == 0;
+      const int M = tgt ? Bl : Mon;
+      const int64_t row = tgt ? 2 * Bl : 0;
+      for (int l = 0; l < L; ++l) {
+        GemmArgs a = fwd_args(h, cn.in[l], l == 0 ? ldc : h, cn.ld[l], h, EPI_BIAS_RELU);
+        a.n_groups = 2;
+        for (int i = 0; i < 2; ++i) {
+          const int id = tgt ? NET_Q1T + i : NET_Q1 + i;
+          void* dst = tgt ? Lr->Atg[i][l] : Lr->Aon[i][l];
+          a.g[i].A = l == 0 ? (const void*)Ta(Lr->Xc, row, ldc) : (const void*)(tgt ? Lr->Atg[i][l - 1] : Lr->Aon[i][l - 1]);
+          a.g[i].B = Wp(id, l);
+          a.g[i].C = dst;
+          a.g[i].bias = bp(id, l);
+          a.g[i].M = M;
+        }
+        gemm(tgt ? "target_critic_gemm" : "critic_fwd_gemm", a);
+      }
+      RowdotArgs ra{};
+      ra.M = M;
+      ra.h = h;
+      ra.ld = h;
+      for (int i = 0; i < 2; ++i) {
+        const int id = tgt ? NET_Q1T + i : NET_Q1 + i;
+        ra.g[i].A = tgt ? Lr->Atg[i][L - 1] : Lr->Aon[i][L - 1];
+        ra.g[i].w = P + Lr->pbase[id] + Lr->net[id].w[L];
+        ra.g[i].b = bp(id, L);
+        ra.g[i].q = tgt ? Lr->q_tg[i] : Lr->q_on[i];
+      }
+      ops.push_back({tgt ? "target_critic_head" : "critic_head", [ra, M](cudaStream_t st) {
+                       rowdot_kernel<T><<<dim3((unsigned)cdiv((int64_t)M * 32, 256), 2), 256, 0, st>>>(ra);
+                       return cudaGetLastError();
+                     }});
+    }
+    // ---- a4/a5: Bellman target, losses, head gradients, stat partials
+    const int nblk = (int)cdiv(Bl, LOSS_NT);
+    {
+      const float gamma = (float)Lr->cfg.gamma;
+      float *qt1 = Lr->q_tg[0], *qt2 = Lr->q_tg[1], *q1 = Lr->q_on[0], *q2 = Lr->q_on[1];
+      float *lp = Lr->logp, *lp2 = Lr->logp2, *rr = Lr->r, *dd = Lr->d, *g1 = Lr->gq[0], *g2 = Lr->gq[1], *yy = Lr->y;
+      const float* la = P + Lr->p_log_alpha;
+      double* part = Lr->stat_partials;
+      const int64_t* stp = Lr->counters;
+      const int t3 = td3;
+      ops.push_back({"critic_loss", [=](cudaStream_t st) {
+                       critic_loss_kernel<<<nblk, LOSS_NT, 0, st>>>(qt1, qt2, q1, q2, lp2, lp, rr, dd, la, gamma, invB,
+                                                                   Bl, t3, stp, delay, g1, g2, yy, part);
+                       return cudaGetLastError();
+                     }});
+    }
+    // ---- a6: critic backward
+    {
+      HeadBwdArgs hb{};
+      hb.M = Mon;
+      hb.h = h;
+      hb.ld = h;
+      for (int i = 0; i < 2; ++i) {
+        hb.g[i].gq = Lr->gq[i];
+        hb.g[i].w = P + Lr->pbase[NET_Q1 + i] + cn.w[L];
+        hb.g[i].A = Lr->Aon[i][L - 1];
+        hb.g[i].dZ = Lr->dZc[i][L - 1];
+      }
+      const int64_t tot = (int64_t)Mon * h;
+      ops.push_back({"critic_head_bwd", [hb, tot](cudaStream_t st) {
+                       critic_head_bwd_kernel<T><<<dim3((unsigned)std::min<int64_t>(cdiv(tot, 256), 148 * 8), 2), 256, 0, st>>>(hb);
+                       return cudaGetLastError();
+                     }});
+      // dgrad through hidden layers l = L-1 .. 1 (all Mon rows)
+      for (int l = L - 1; l >= 1; --l) {
+        GemmArgs a = fwd_args(h, h, h, cn.ld[l], h, EPI_MASK);
+        a.b_mn = 1;
+        a.ldaux = h;
+        a.n_groups = 2;
+        for (int i = 0; i < 2; ++i) {
+          a.g[i].A = Lr->dZc[i][l];
+          a.g[i].B = Wp(NET_Q1 + i, l);
+          a.g[i].C = Lr->dZc[i][l - 1];
+          a.g[i].aux = Lr->Aon[i][l - 1];
+          a.g[i].M = Mon;
+        }
+        gemm("critic_dgrad_gemm", a);
+      }
+      // input dgrad for the actor rows (only the action columns are consumed)
+      if (actor_step) {
+        GemmArgs a = fwd_args(o + m, h, h, cn.ld[0], ldc, EPI_F32);
+        a.b_mn = 1;
+        a.n_groups = td3 ? 1 : 2;
+        for (int i = 0; i < a.n_groups; ++i) {
+          a.g[i].A = Ta(Lr->dZc[i][0], Bl, h);
+          a.g[i].B = Wp(NET_Q1 + i, 0);
+          a.g[i].C = Lr->dXc[i];
+          a.g[i].M = Bl;
+        }
+        gemm("critic_input_dgrad_gemm", a);
+      }
+      // wgrad on the Bl loss rows: dW_l = dZ_l^T A_{l-1}; split-K over the batch
+      for (int l = 0; l < L; ++l) {
+        GemmArgs a = fwd_args(cn.in[l], Bl, h, l == 0 ? ldc : h, cn.in[l], EPI_F32);
+        a.a_mn = 1;
+        a.b_mn = 1;
+        a.splits = Sw;
+        a.k_per_split = (int)rows_w;
+        a.split_stride = (int64_t)h * cn.in[l];
+        a.n_groups = 2;
+        for (int i = 0; i < 2; ++i) {
+          a.g[i].A = Lr->dZc[i][l];
+          a.g[i].B = l == 0 ? Lr->Xc : Lr->Aon[i][l - 1];
+          a.g[i].C = Lr->G + slot_of(NET_Q1 + i, l, true).g_off;
+          a.g[i].M = h;
+        }
+        a.N = cn.in[l];
+        gemm("critic_wgrad_gemm", a);
+      }
+      // bias gradients (column sums of dZ over loss rows) and the N = 1 head
+      for (int i = 0; i < 2; ++i) {
+        for (int l = 0; l < L; ++l) {
+          const T* X = static_cast<const T*>(Lr->dZc[i][l]);
+          float* out = Lr->G + slot_of(NET_Q1 + i, l, false).g_off;
+          ops.push_back({"critic_bias_grad", [=](cudaStream_t st) {
+                           colsum_kernel<T><<<dim3((unsigned)cdiv(h, CS_COLS), Sb), CS_COLS * CS_ROWS, 0, st>>>(
+                               X, h, h, Bl, (int)rows_b, nullptr, out);
+                           return cudaGetLastError();
+                         }});
+        }
+        const T* AL = static_cast<const T*>(Lr->Aon[i][L - 1]);
+        const float* g = Lr->gq[i];
+        float* outw = Lr->G + slot_of(NET_Q1 + i, L, true).g_off;
+        float* outb = Lr->G + slot_of(NET_Q1 + i, L, false).g_off;
+        ops.push_back({"critic_bias_grad", [=](cudaStream_t st) {
+                         colsum_kernel<T><<<dim3((unsigned)cdiv(h, CS_COLS), Sb), CS_COLS * CS_ROWS, 0, st>>>(
+                             AL, h, h, Bl, (int)rows_b, g, outw);
+                         colsum_kernel<float><<<dim3(1, Sb), CS_COLS * CS_ROWS, 0, st>>>(g, 1, 1, Bl, (int)rows_b,
+                                                                                        nullptr, outb);
+                         return cudaGetLastError();
+                       }, 2});
+      }
+    }
+    // ---- a7: actor backward (s-rows Bl..2Bl of the actor activations)
+    if (actor_step) {
+      const NetLayout& an = Lr->net[NET_ACTOR];
+      const int nout = an.out[L];  // 2m (SAC) or m (TD3)
+      T* dH = static_cast<T*>(Lr->dH);
+      {
+        float *x1 = Lr->dXc[0], *x2 = Lr->dXc[1];
+        HeadCache cache = Lr->cache;
+        const float* la = P + Lr->p_log_alpha;
+        if (!td3) {
+          ops.push_back({"actor_head_bwd", [=](cudaStream_t st) {
+                           sac_head_bwd_kernel<T><<<(unsigned)cdiv((int64_t)Bl * m, 256), 256, 0, st>>>(
+                               x1, x2, ldc, o, m, Bl, cache, la, invB, lo, hi, dH, ldh);
+                           return cudaGetLastError();
+                         }});
+        } else {
+          ops.push_back({"actor_head_bwd", [=](cudaStream_t st) {
+                           td3_head_bwd_kernel<T><<<(unsigned)cdiv((int64_t)Bl * m, 256), 256, 0, st>>>(
+                               x1, ldc, o, m, Bl, cache.a, dH, ldh);
+                           return cudaGetLastError();
+                         }});
+        }
+      }
+      // dgrad: dZ_{L-1} = (dH W_out) * 1[A_{L-1} > 0], then down the hidden stack
+      for (int l = L; l >= 1; --l) {
+        GemmArgs a = fwd_args(h, an.out[l], l == L ? ldh : h, an.ld[l], h, EPI_MASK);
+        a.b_mn = 1;
+        a.ldaux = h;
+        a.n_groups = 1;
+        a.g[0].A = l == L ? (const void*)dH : (const void*)Lr->dZa[l];
+        a.g[0].B = Wp(NET_ACTOR, l);
+        a.g[0].C = Lr->dZa[l - 1];
+        a.g[0].aux = Ta(Lr->Aact[l - 1], Bl, h);
+        a.g[0].M = Bl;
+        gemm("actor_dgrad_gemm", a);
+      }
+      // wgrad: dW_l = dZ_l^T A_{l-1} over the Bl s-rows (dZ_L = dH)
+      for (int l = 0; l <= L; ++l) {
+        GemmArgs a = fwd_args(an.in[l], Bl, l == L ? ldh : h, l == 0 ? lda : h, an.in[l], EPI_F32);
+        a.a_mn = 1;
+        a.b_mn = 1;
+        a.splits = Sw;
+        a.k_per_split = (int)rows_w;
+        a.split_stride = (int64_t)an.out[l] * an.in[l];
+        a.n_groups = 1;
+        a.g[0].A = l == L ? (const void*)dH : (const void*)Lr->dZa[l];
+        a.g[0].B = l == 0 ? (const void*)Ta(Lr->Xa, Bl, lda) : (const void*)Ta(Lr->Aact[l - 1], Bl, h);
+        a.g[0].C = Lr->G + slot_of(NET_ACTOR, l, true).g_off;
+        a.g[0].M = an.out[l];
+        gemm("actor_wgrad_gemm", a);
+      }
+      for (int l = 0; l <= L; ++l) {
+        const T* X = l == L ? dH : static_cast<const T*>(Lr->dZa[l]);
+        const int ldx = l == L ? ldh : h;
+        const int N = an.out[l];
+        float* out = Lr->G + slot_of(NET_ACTOR, l, false).g_off;
+        ops.push_back({"actor_bias_grad", [=](cudaStream_t st) {
+                         colsum_kernel<T><<<dim3((unsigned)cdiv(N, CS_COLS), Sb), CS_COLS * CS_ROWS, 0, st>>>(
+                             X, ldx, N, Bl, (int)rows_b, nullptr, out);
+                         return cudaGetLastError();
+                       }});
+      }
+      (void)nout;
+    }
+    // ---- statistics, log-alpha gradient, non-finite flag
+    {
+      double* part = Lr->stat_partials;
+      const float* la = P + Lr->p_log_alpha;
+      const double te = Lr->cfg.target_entropy;
+      const int t3 = td3;
+      const int64_t* stp = Lr->counters;
+      StatsOut* so = Lr->d_stats;
+      float* ga = Lr->G + Lr->G_total - 64;
+      int* fl = Lr->d_flag;
+      const double Bd = (double)B;
+      ops.push_back({"stats", [=](cudaStream_t st) {
+                       stats_kernel<<<1, 32, 0, st>>>(part, nblk, nullptr, la, te, Bd, t3, stp, delay, so, ga, fl);
+                       return cudaGetLastError();
+                     }});
+    }
+    // ---- a9: fused Adam + Polyak (+ shadow refresh) over every trained tensor
+    {
+      std::vector<AdamTensor> tens;
+      std::vector<AdamSegment> segs;
+      for (auto& s : slots) {
+        const NetLayout& n = Lr->net[s.net];
+        AdamTensor t{};
+        t.p_off = Lr->pbase[s.net] + (s.weight ? n.w[s.layer] : n.b[s.layer]);
+        t.numel = s.numel;
+        t.partials = Lr->G + s.g_off;
+        const bool head_vec = (s.net == NET_Q1 || s.net == NET_Q2) && s.layer == n.nl - 1;
+        t.n_partials = s.weight && !head_vec ? Sw : Sb;
+        t.opt = s.net == NET_ACTOR ? 1 : 0;
+        t.cols = s.weight ? n.in[s.layer] : 0;
+        t.ld = n.ld[s.layer];
+        t.s_off = s.weight ? Lr->sbase[s.net] + n.sw[s.layer] : -1;
+        int tid = s.net == NET_Q1 ? NET_Q1T : s.net == NET_Q2 ? NET_Q2T : (td3 ? NET_ACTORT : -1);
+        t.t_off = tid >= 0 ? Lr->pbase[tid] + (s.weight ? n.w[s.layer] : n.b[s.layer]) : -1;
+        t.ts_off = (tid >= 0 && s.weight) ? Lr->sbase[tid] + n.sw[s.layer] : -1;
+        const int ti = (int)tens.size();
+        tens.push_back(t);
+        for (int64_t st = 0; st < t.numel; st += ADAM_SEG)
+          segs.push_back({ti, (int32_t)std::min<int64_t>(ADAM_SEG, t.numel - st), st});
+      }
+      if (!td3 && Lr->cfg.alpha_auto && Lr->cfg.role != SPZ_ROLE_CRITIC) {
+        AdamTensor t{};
+        t.p_off = Lr->p_log_alpha;
+        t.numel = 1;
+        t.partials = Lr->G + Lr->G_total - 64;
+        t.n_partials = 1;
+        t.opt = 2;
+        t.s_off = t.t_off = t.ts_off = -1;
+        tens.push_back(t);
+        segs.push_back({(int)tens.size() - 1, 1, 0});
+      }
+      if ((int)tens.size() > Lr->max_tensors || (int)segs.size() > Lr->max_segs)
+        return fail(SPZ_EINVAL, "internal: Adam table overflow");
+      const size_t tb = tens.size() * sizeof(AdamTensor), sb = segs.size() * sizeof(AdamSegment);
+      AdamTensor* dt = Lr->d_tensors + (variant ? Lr->max_tensors / 2 : 0);
+      AdamSegment* ds = Lr->d_segs + (variant ? Lr->max_segs / 2 : 0);
+      SPZ_CUDA_TRY(cudaMemcpyAsync(dt, tens.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
+      SPZ_CUDA_TRY(cudaMemcpyAsync(ds, segs.data(), sb, cudaMemcpyHostToDevice, Lr->stream));
+      SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+      AdamHyper hp{};
+      hp.lr[0] = (float)Lr->cfg.lr_critic;
+      hp.lr[1] = (float)Lr->cfg.lr_actor;
+      hp.lr[2] = (float)Lr->cfg.lr_alpha;
+      hp.beta1 = (float)Lr->cfg.beta1;
+      hp.beta2 = (float)Lr->cfg.beta2;
+      hp.eps = (float)Lr->cfg.adam_eps;
+      hp.tau = (float)Lr->cfg.tau;
+      hp.td3 = td3;
+      hp.delay = delay;
+      float *Pm = Lr->P, *Mm = Lr->Mo, *Vm = Lr->Vo;
+      int64_t* ctr = Lr->counters;
+      int* fl = Lr->d_flag;
+      const unsigned nseg = (unsigned)segs.size();
+      ops.push_back({"adam_polyak", [=](cudaStream_t st) {
+                       adam_polyak_kernel<T><<<nseg, 256, 0, st>>>(dt, ds, hp, Pm, Mm, Vm, S, ctr, fl);
+                       return cudaGetLastError();
+                     }});
+      const int t3 = td3, aa = Lr->cfg.alpha_auto;
+      const int con = Lr->cfg.role != SPZ_ROLE_ACTOR, aon = Lr->cfg.role != SPZ_ROLE_CRITIC;
+      ops.push_back({"advance", [=](cudaStream_t st) {
+                       advance_kernel<<<1, 1, 0, st>>>(ctr, fl, t3, delay, aa, con, aon);
+                       return cudaGetLastError();
+                     }});
+    }
+  }
+  Lr->plan_B = B;
+  return SPZ_OK;
+}
+
+static spz_status run_ops(spz_learner* Lr, int variant, cudaStream_t st) {
+  for (auto& op : Lr->ops[variant]) {
+    cudaError_t e = op.fn(st);
+    if (e != cudaSuccess) return fail(SPZ_ECUDA, std::string("kernel ") + op.cls + ": " + cudaGetErrorString(e));
+  }
+  return SPZ_OK;
+}
+
+static spz_status ensure_graph(spz_learner* Lr, int variant) {
+  if (Lr->exec[variant]) return SPZ_OK;
+  cudaStream_t cs;
+  SPZ_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t g = nullptr;
+  SPZ_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  spz_status s = run_ops(Lr, variant, cs);
+  cudaError_t e = cudaStreamEndCapture(cs, &g);
+  cudaStreamDestroy(cs);
+  if (s != SPZ_OK) {
+    if (g) cudaGraphDestroy(g);
+    return s;
+  }
+  if (e != cudaSuccess) return fail(SPZ_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&Lr->exec[variant], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(SPZ_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  return SPZ_OK;
+}
+
+static spz_status prepare(spz_learner* Lr, int64_t batch) {
+  if (batch < 1 || batch > Lr->cfg.max_batch)
+    return fail(SPZ_EINVAL, "batch " + std::to_string(batch) + " outside [1, max_batch=" + std::to_string(Lr->cfg.max_batch) + "]");
+  if (batch < Lr->cfg.world_size) return fail(SPZ_EINVAL, "batch smaller than world_size");
+  const int64_t F = Lr->ring->fill();
+  if (F < batch) return fail(SPZ_ENODATA, "ring fill " + std::to_string(F) + " < batch " + std::to_string(batch));
+  if (Lr->plan_B != batch) {
+    SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+    spz_status s = Lr->bf16 ? build_plan<__nv_bfloat16>(Lr, batch) : build_plan<float>(Lr, batch);
+    if (s != SPZ_OK) {
+      Lr->plan_B = -1;
+      return s;
+    }
+  }
+  return SPZ_OK;
+}
+
+static spz_status set_fill(spz_learner* Lr) {
+  static thread_local int64_t hf;
+  hf = Lr->ring->fill();
+  // the pinned counters buffer doubles as the fill staging slot
+  Lr->h_counters[4] = hf;
+  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->d_fill, &Lr->h_counters[4], sizeof(int64_t), cudaMemcpyHostToDevice, Lr->stream));
+  return SPZ_OK;
+}
+
+template <typename T>
+static spz_status refresh_shadows_t(spz_learner* Lr) {
+  shadow_refresh_kernel<T><<<dim3(64, (unsigned)Lr->n_shadow), 256, 0, Lr->stream>>>(Lr->d_shadow, Lr->n_shadow, Lr->P,
+                                                                                     static_cast<T*>(Lr->S));
+  SPZ_CUDA_TRY(cudaGetLastError());
+  return SPZ_OK;
+}
+
+spz_status refresh_shadows(spz_learner* Lr) {
+  return Lr->bf16 ? refresh_shadows_t<__nv_bfloat16>(Lr) : refresh_shadows_t<float>(Lr);
+}
+
+static int variant_of(spz_learner* Lr, int64_t step) {
+  if (!Lr->td3) return 0;
+  const int delay = std::max(1, Lr->cfg.td3_policy_delay);
+  return ((step + 1) % delay) == 0 ? 1 : 0;
+}
+
+static spz_status read_counters(spz_learner* Lr) {
+  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_counters, Lr->counters, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, Lr->stream));
+  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_flag, Lr->d_flag, sizeof(int), cudaMemcpyDeviceToHost, Lr->stream));
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  return SPZ_OK;
+}
+
+}  // namespace spz
+
+// ============================================================================= C API
+extern "C" {
+
+spz_status spz_config_default(spz_algo algo, int32_t obs_dim, int32_t act_dim, spz_config* out) {
+  if (!out) return fail(SPZ_EINVAL, "spz_config_default: NULL out");
+  if (obs_dim < 1 || act_dim < 1) return fail(SPZ_EINVAL, "spz_config_default: dims must be >= 1");
+  std::memset(out, 0, sizeof(*out));
+  out->algo = algo;
+  out->precision = SPZ_BF16;
+  out->obs_dim = obs_dim;
+  out->act_dim = act_dim;
+  out->hidden = 256;
+  out->n_hidden = 2;
+  out->max_batch = 8192;
+  out->gamma = 0.99;
+  out->tau = 0.005;
+  out->lr_actor = out->lr_critic = out->lr_alpha = 3e-4;
+  out->beta1 = 0.9;
+  out->beta2 = 0.999;
+  out->adam_eps = 1e-8;
+  out->alpha_auto = algo == SPZ_SAC ? 1 : 0;
+  out->alpha_init = 0.2;
+  out->target_entropy = -(double)act_dim;
+  out->log_std_min = -20.0;
+  out->log_std_max = 2.0;
+  out->td3_noise = 0.2;
+  out->td3_noise_clip = 0.5;
+  out->td3_policy_delay = 2;
+  out->seed = 6126;
+  out->init_seed = 0;
+  out->device = 0;
+  out->world_size = 1;
+  out->rank = 0;
+  out->role = SPZ_ROLE_ALL;
+  out->use_graph = 1;
+  return SPZ_OK;
+}
+
+spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learner** out) {
+  if (!cfg || !ring || !out) return fail(SPZ_EINVAL, "spz_learner_create: NULL argument");
+  *out = nullptr;
+  if (cfg->obs_dim != ring->o || cfg->act_dim != ring->m)
+    return fail(SPZ_EINVAL, "spz_learner_create: config dims do not match the ring");
+  if (cfg->device != ring->device) return fail(SPZ_EINVAL, "spz_learner_create: ring lives on another device");
+  if (cfg->hidden < 1 || cfg->n_hidden < 1 || cfg->n_hidden > 6) return fail(SPZ_EINVAL, "spz_learner_create: need hidden >= 1 and 1 <= n_hidden <= 6");
+  if (cfg->max_batch < 1) return fail(SPZ_EINVAL, "spz_learner_create: max_batch must be >= 1");
+  if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return fail(SPZ_EINVAL, "spz_learner_create: bad rank/world_size");
+  if (cfg->world_size > 1) return fail(SPZ_EUNSUPPORTED, "spz_learner_create: multi-rank learners are not built yet");
+  if (cfg->role != SPZ_ROLE_ALL) return fail(SPZ_EUNSUPPORTED, "spz_learner_create: split roles are not built yet");
+  if (cfg->algo != SPZ_SAC && cfg->algo != SPZ_TD3) return fail(SPZ_EINVAL, "spz_learner_create: unknown algo");
+  if (cfg->precision != SPZ_FP32 && cfg->precision != SPZ_BF16) return fail(SPZ_EINVAL, "spz_learner_create: unknown precision");
+  spz_status st = check_device(cfg->device);
+  if (st != SPZ_OK) return st;
+  DeviceGuard dg(cfg->device);
+  std::unique_ptr<spz_learner> Lr(new spz_learner());
+  Lr->cfg = *cfg;
+  Lr->ring = ring;
+  Lr->device = cfg->device;
+  Lr->td3 = cfg->algo == SPZ_TD3;
+  Lr->bf16 = cfg->precision == SPZ_BF16;
+  Lr->esz = Lr->bf16 ? 2 : 4;
+  Lr->o = cfg->obs_dim;
+  Lr->m = cfg->act_dim;
+  Lr->h = cfg->hidden;
+  Lr->L = cfg->n_hidden;
+  const int o = Lr->o, m = Lr->m, h = Lr->h, L = Lr->L;
+  if (cudaStreamCreateWithFlags(&Lr->own_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(SPZ_ECUDA, "spz_learner_create: stream creation failed");
+  Lr->stream = Lr->own_stream;
+  const int W = cfg->world_size;
+  Lr->max_local = cfg->max_batch / W + (cfg->max_batch % W ? 1 : 0);
+  // networks
+  const int aout = Lr->td3 ? m : 2 * m;
+  Lr->net[NET_ACTOR] = make_layout(o, h, L, aout);
+  Lr->net[NET_Q1] = Lr->net[NET_Q2] = Lr->net[NET_Q1T] = Lr->net[NET_Q2T] = make_layout(o + m, h, L, 1);
+  Lr->net[NET_ACTORT] = Lr->net[NET_ACTOR];
+  int64_t p = 0, s = 0;
+  for (int id = 0; id < N_NETS; ++id) {
+    Lr->has_net[id] = id != NET_ACTORT || Lr->td3;
+    if (!Lr->has_net[id]) continue;
+    Lr->pbase[id] = p;
+    p += round_up(Lr->net[id].np, 64);
+    Lr->sbase[id] = s;
+    s += Lr->net[id].ns;
+  }
+  Lr->p_log_alpha = p;
+  p += 64;
+  Lr->P_total = p;
+  Lr->S_total = s;
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->P, p * sizeof(float)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->Mo, p * sizeof(float)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->Vo, p * sizeof(float)));
+  SPZ_TRY(dalloc(Lr.get(), &Lr->S, s * Lr->esz));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->counters, 8 * sizeof(int64_t)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_fill, sizeof(int64_t)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_flag, sizeof(int)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_stats, sizeof(StatsOut)));
+  if (cudaMallocHost(&Lr->h_stats, sizeof(StatsOut)) != cudaSuccess || cudaMallocHost(&Lr->h_flag, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&Lr->h_counters, 8 * sizeof(int64_t)) != cudaSuccess)
+    return fail(SPZ_ENOMEM, "spz_learner_create: pinned host allocation failed");
+  // activations
+  const int64_t Bm = Lr->max_local;
+  Lr->lda = (int)round_up(o, 8);
+  Lr->ldc = (int)round_up(o + m, 8);
+  Lr->ldh = (int)round_up(aout, 8);
+  const size_t E = Lr->esz;
+  SPZ_TRY(dalloc(Lr.get(), &Lr->Xa, 2 * Bm * Lr->lda * E));
+  SPZ_TRY(dalloc(Lr.get(), &Lr->Xc, 3 * Bm * Lr->ldc * E));
+  SPZ_TRY(dalloc(Lr.get(), &Lr->dH, Bm * Lr->ldh * E));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->H, 2 * Bm * Lr->ldh * sizeof(float)));
+  for (int l = 0; l < L; ++l) {
+    SPZ_TRY(dalloc(Lr.get(), &Lr->Aact[l], 2 * Bm * h * E));
+    SPZ_TRY(dalloc(Lr.get(), &Lr->dZa[l], Bm * h * E));
+    for (int i = 0; i < 2; ++i) {
+      SPZ_TRY(dalloc(Lr.get(), &Lr->Aon[i][l], 2 * Bm * h * E));
+      SPZ_TRY(dalloc(Lr.get(), &Lr->Atg[i][l], Bm * h * E));
+      SPZ_TRY(dalloc(Lr.get(), &Lr->dZc[i][l], 2 * Bm * h * E));
+    }
+  }
+  for (int i = 0; i < 2; ++i) {
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->q_on[i], 2 * Bm * sizeof(float)));
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->q_tg[i], Bm * sizeof(float)));
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->gq[i], 2 * Bm * sizeof(float)));
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->dXc[i], Bm * Lr->ldc * sizeof(float)));
+  }
+  for (float** f : {&Lr->logp, &Lr->logp2, &Lr->r, &Lr->d, &Lr->y}) SPZ_TRY(dalloc(Lr.get(), (void**)f, Bm * sizeof(float)));
+  for (float** f : {&Lr->cache.u, &Lr->cache.a, &Lr->cache.eps, &Lr->cache.sig, &Lr->cache.l})
+    SPZ_TRY(dalloc(Lr.get(), (void**)f, Bm * m * sizeof(float)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->idx, Bm * sizeof(int32_t)));
+  Lr->max_stat_blocks = (int)cdiv(Bm, LOSS_NT);
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->stat_partials, (size_t)Lr->max_stat_blocks * NSTAT * sizeof(double)));
+  {
+    auto reg = [&](const std::string& n, void* p, size_t bytes, int es) { Lr->debug.push_back({n, p, bytes, es}); };
+    reg("Xa", Lr->Xa, 2 * Bm * Lr->lda * E, (int)E);
+    reg("Xc", Lr->Xc, 3 * Bm * Lr->ldc * E, (int)E);
+    reg("H", Lr->H, 2 * Bm * Lr->ldh * 4, 4);
+    reg("dH", Lr->dH, Bm * Lr->ldh * E, (int)E);
+    for (int l = 0; l < L; ++l) {
+      reg("Aact" + std::to_string(l), Lr->Aact[l], 2 * Bm * h * E, (int)E);
+      reg("dZa" + std::to_string(l), Lr->dZa[l], Bm * h * E, (int)E);
+      for (int i = 0; i < 2; ++i) {
+        reg("Aon" + std::to_string(i) + "_" + std::to_string(l), Lr->Aon[i][l], 2 * Bm * h * E, (int)E);
+        reg("Atg" + std::to_string(i) + "_" + std::to_string(l), Lr->Atg[i][l], Bm * h * E, (int)E);
+        reg("dZc" + std::to_string(i) + "_" + std::to_string(l), Lr->dZc[i][l], 2 * Bm * h * E, (int)E);
+      }
+    }
+    for (int i = 0; i < 2; ++i) {
+      reg("q_on" + std::to_string(i), Lr->q_on[i], 2 * Bm * 4, 4);
+      reg("q_tg" + std::to_string(i), Lr->q_tg[i], Bm * 4, 4);
+      reg("gq" + std::to_string(i), Lr->gq[i], 2 * Bm * 4, 4);
+      reg("dXc" + std::to_string(i), Lr->dXc[i], Bm * Lr->ldc * 4, 4);
+    }
+    reg("logp", Lr->logp, Bm * 4, 4);
+    reg("logp2", Lr->logp2, Bm * 4, 4);
+    reg("r", Lr->r, Bm * 4, 4);
+    reg("d", Lr->d, Bm * 4, 4);
+    reg("y", Lr->y, Bm * 4, 4);
+    reg("idx", Lr->idx, Bm * 4, 4);
+    reg("P", Lr->P, Lr->P_total * 4, 4);
+    reg("S", Lr->S, Lr->S_total * E, (int)E);
+  }
+  // gradients and optimizer tables
+  std::vector<TensorSlot> slots = trained_tensors(Lr.get());
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->G, Lr->G_total * sizeof(float)));
+  int64_t nseg = 0;
+  for (auto& t : slots) nseg += cdiv(t.numel, ADAM_SEG);
+  Lr->max_segs = (int)(2 * (nseg + 4));
+  Lr->max_tensors = 2 * ((int)slots.size() + 4);
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_tensors, Lr->max_tensors * sizeof(AdamTensor)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_segs, Lr->max_segs * sizeof(AdamSegment)));
+  // shadow table: every W of every net
+  std::vector<ShadowEntry> sh;
+  for (int id = 0; id < N_NETS; ++id) {
+    if (!Lr->has_net[id]) continue;
+    const NetLayout& n = Lr->net[id];
+    for (int l = 0; l < n.nl; ++l) sh.push_back({Lr->pbase[id] + n.w[l], n.out[l], n.in[l], n.ld[l], Lr->sbase[id] + n.sw[l]});
+  }
+  Lr->n_shadow = (int)sh.size();
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_shadow, sh.size() * sizeof(ShadowEntry)));
+  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->d_shadow, sh.data(), sh.size() * sizeof(ShadowEntry), cudaMemcpyHostToDevice, Lr->stream));
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  // init: W, b ~ U(+-1/sqrt(fan_in)) (Philox stream S_INIT); targets copy online; log alpha = ln alpha_init
+  for (int id : {NET_ACTOR, NET_Q1, NET_Q2}) {
+    const NetLayout& n = Lr->net[id];
+    for (int l = 0; l < n.nl; ++l) {
+      const float bound = 1.0f / std::sqrt((float)n.in[l]);
+      const int64_t cnt = (int64_t)n.out[l] * n.in[l] + n.out[l];
+      init_uniform_kernel<<<(unsigned)std::min<int64_t>(cdiv(cnt, 256), 1024), 256, 0, Lr->stream>>>(
+          Lr->P, Lr->pbase[id] + n.w[l], cnt, bound, cfg->init_seed, (uint32_t)id, n.w[l]);
+    }
+  }
+  SPZ_CUDA_TRY(cudaGetLastError());
+  auto copy_net = [&](int dst, int src) {
+    return cudaMemcpyAsync(Lr->P + Lr->pbase[dst], Lr->P + Lr->pbase[src], Lr->net[src].np * sizeof(float),
+                           cudaMemcpyDeviceToDevice, Lr->stream);
+  };
+  SPZ_CUDA_TRY(copy_net(NET_Q1T, NET_Q1));
+  SPZ_CUDA_TRY(copy_net(NET_Q2T, NET_Q2));
+  if (Lr->td3) SPZ_CUDA_TRY(copy_net(NET_ACTORT, NET_ACTOR));
+  const float la = (float)std::log(cfg->alpha_init > 0 ? cfg->alpha_init : 1e-30);
+  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->P + Lr->p_log_alpha, &la, sizeof(float), cudaMemcpyHostToDevice, Lr->stream));
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  spz_status rs = refresh_shadows(Lr.get());
+  if (rs != SPZ_OK) return rs;
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  *out = Lr.release();
+  return SPZ_OK;
+}
+
+spz_status spz_learner_set_stream(spz_learner* Lr, void* stream) {
+  if (!Lr) return fail(SPZ_EINVAL, "spz_learner_set_stream: NULL learner");
+  DeviceGuard dg(Lr->device);
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  Lr->stream = stream ? static_cast<cudaStream_t>(stream) : Lr->own_stream;
+  return SPZ_OK;
+}
+
+spz_status spz_update(spz_learner* Lr, int64_t batch, int64_t n_steps, spz_stats* last) {
+  if (!Lr) return fail(SPZ_EINVAL, "spz_update: NULL learner");
+  if (n_steps < 0) return fail(SPZ_EINVAL, "spz_update: n_steps < 0");
+  DeviceGuard dg(Lr->device);
+  SPZ_TRY(prepare(Lr, batch));
+  SPZ_TRY(read_counters(Lr));
+  if (*Lr->h_flag) return fail(SPZ_ENONFINITE, "spz_update: learner halted by an earlier non-finite step " + std::to_string(Lr->h_counters[0]));
+  int64_t step = Lr->h_counters[0];
+  SPZ_TRY(set_fill(Lr));
+  for (int64_t k = 0; k < n_steps; ++k, ++step) {
+    const int v = variant_of(Lr, step);
+    if (Lr->cfg.use_graph) {
+      SPZ_TRY(ensure_graph(Lr, v));
+      SPZ_CUDA_TRY(cudaGraphLaunch(Lr->exec[v], Lr->stream));
+    } else {
+      SPZ_TRY(run_ops(Lr, v, Lr->stream));
+    }
+  }
+  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_stats, Lr->d_stats, sizeof(StatsOut), cudaMemcpyDeviceToHost, Lr->stream));
+  SPZ_TRY(read_counters(Lr));
+  if (*Lr->h_flag)
+    return fail(SPZ_ENONFINITE, "spz_update: non-finite loss or gradient at step " + std::to_string(Lr->h_counters[0]) +
+                                    (*Lr->h_flag == 2 ? " (gradient)" : " (loss)") + "; learner halted");
+  if (last) {
+    const StatsOut& s = *Lr->h_stats;
+    last->step = (int64_t)s.step;
+    last->critic_loss = s.critic_loss;
+    last->actor_loss = s.actor_loss;
+    last->alpha = s.alpha;
+    last->alpha_loss = s.alpha_loss;
+    last->q1_mean = s.q1_mean;
+    last->q2_mean = s.q2_mean;
+    last->logp_mean = s.logp_mean;
+  }
+  return SPZ_OK;
+}
+
+static spz_status tensor_region(spz_learner* Lr, spz_tensor t, spz_slot s, float** base, int64_t* n) {
+  int id;
+  switch (t) {
+    case SPZ_T_ACTOR: id = NET_ACTOR; break;
+    case SPZ_T_Q1: id = NET_Q1; break;
+    case SPZ_T_Q2: id = NET_Q2; break;
+    case SPZ_T_Q1_TARG: id = NET_Q1T; break;
+    case SPZ_T_Q2_TARG: id = NET_Q2T; break;
+    case SPZ_T_ACTOR_TARG: id = NET_ACTORT; break;
+    case SPZ_T_LOG_ALPHA: id = -1; break;
+    default: return fail(SPZ_EINVAL, "unknown tensor id");
+  }
+  if (id >= 0 && !Lr->has_net[id]) return fail(SPZ_EINVAL, "tensor not present for this algorithm");
+  const bool trained = id == NET_ACTOR || id == NET_Q1 || id == NET_Q2 || id == -1;
+  if (s != SPZ_S_PARAM && !trained) return fail(SPZ_EINVAL, "target networks have no Adam state");
+  float* arr = s == SPZ_S_PARAM ? Lr->P : s == SPZ_S_ADAM_M ? Lr->Mo : s == SPZ_S_ADAM_V ? Lr->Vo : nullptr;
+  if (!arr) return fail(SPZ_EINVAL, "unknown slot");
+  *base = arr + (id >= 0 ? Lr->pbase[id] : Lr->p_log_alpha);
+  *n = id >= 0 ? Lr->net[id].np : 1;
+  return SPZ_OK;
+}
+
+spz_status spz_get_params(spz_learner* Lr, spz_tensor t, spz_slot s, float* host_out, int64_t n, int64_t* n_required) {
+  if (!Lr) return fail(SPZ_EINVAL, "spz_get_params: NULL learner");
+  DeviceGuard dg(Lr->device);
+  float* base;
+  int64_t cnt;
+  SPZ_TRY(tensor_region(Lr, t, s, &base, &cnt));
+  if (n_required) *n_required = cnt;
+  if (n < cnt || !host_out) return fail(SPZ_EINVAL, "spz_get_params: output holds " + std::to_string(n) + " < " + std::to_string(cnt) + " floats");
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  SPZ_CUDA_TRY(cudaMemcpyAsync(host_out, base, cnt * sizeof(float), cudaMemcpyDeviceToHost, Lr->stream));
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  return SPZ_OK;
+}
+
+spz_status spz_set_params(spz_learner* Lr, spz_tensor t, spz_slot s, const float* host_in, int64_t n) {
+  if (!Lr || !host_in) return fail(SPZ_EINVAL, "spz_set_params: NULL argument");
+  DeviceGuard dg(Lr->device);
+  float* base;
+  int64_t cnt;
+  SPZ_TRY(tensor_region(Lr, t, s, &base, &cnt));
+  if (n != cnt) return fail(SPZ_EINVAL, "spz_set_params: expected " + std::to_string(cnt) + " floats, got " + std::to_string(n));
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  SPZ_CUDA_TRY(cudaMemcpyAsync(base, host_in, cnt * sizeof(float), cudaMemcpyHostToDevice, Lr->stream));
+  SPZ_TRY(refresh_shadows(Lr));
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  return SPZ_OK;
+}
+
+spz_status spz_get_counters(spz_learner* Lr, int64_t* step, int64_t* t_critic, int64_t* t_actor, int64_t* t_alpha) {
+  if (!Lr) return fail(SPZ_EINVAL, "spz_get_counters: NULL learner");
+  DeviceGuard dg(Lr->device);
+  SPZ_TRY(read_counters(Lr));
+  if (step) *step = Lr->h_counters[0];
+  if (t_critic) *t_critic = Lr->h_counters[1];
+  if (t_actor) *t_actor = Lr->h_counters[2];
+  if (t_alpha) *t_alpha = Lr->h_counters[3];
+  return SPZ_OK;
+}
+
+spz_status spz_sync_actor(spz_learner* Lr, int32_t dst_device, void* dst, int64_t dst_bytes, uint64_t* version) {
+  if (!Lr || !dst) return fail(SPZ_EINVAL, "spz_sync_actor: NULL argument");
+  DeviceGuard dg(Lr->device);
+  const int64_t nf = Lr->net[NET_ACTOR].np;
+  if (dst_bytes < 16 + 4 * nf) return fail(SPZ_EINVAL, "spz_sync_actor: destination smaller than 16 + 4 * " + std::to_string(nf) + " bytes");
+  if (dst_device != Lr->device) {
+    int can = 0;
+    SPZ_CUDA_TRY(cudaDeviceCanAccessPeer(&can, Lr->device, dst_device));
+    if (can) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(dst_device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(SPZ_ECUDA, "cudaDeviceEnablePeerAccess failed");
+      cudaGetLastError();
+    }
+  }
+  uint8_t* d8 = static_cast<uint8_t*>(dst);
+  SPZ_CUDA_TRY(cudaMemcpyPeerAsync(d8 + 16, dst_device, Lr->P + Lr->pbase[NET_ACTOR], Lr->device, nf * sizeof(float), Lr->stream));
+  const uint64_t v = ++Lr->sync_version;
+  uint64_t* hdr = reinterpret_cast<uint64_t*>(&Lr->h_counters[5]);
+  hdr[0] = v;
+  hdr[1] = (uint64_t)nf;
+  SPZ_CUDA_TRY(cudaMemcpyAsync(d8, hdr, 16, cudaMemcpyHostToDevice, Lr->stream));  // header last: never a blend
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  if (version) *version = v;
+  return SPZ_OK;
+}
+
+spz_status spz_learner_profile(spz_learner* Lr, int64_t batch, int64_t n_steps, int32_t cap, const char** names, double* ms,
+                               int32_t* count) {
+  if (!Lr || n_steps < 1) return fail(SPZ_EINVAL, "spz_learner_profile: bad argument");
+  DeviceGuard dg(Lr->device);
+  SPZ_TRY(prepare(Lr, batch));
+  SPZ_TRY(read_counters(Lr));
+  int64_t step = Lr->h_counters[0];
+  SPZ_TRY(set_fill(Lr));
+  std::vector<const char*> cls;
+  std::vector<double> tot;
+  std::vector<cudaEvent_t> ev;
+  for (int64_t k = 0; k < n_steps; ++k, ++step) {
+    const int v = variant_of(Lr, step);
+    auto& ops = Lr->ops[v];
+    if (ev.size() < ops.size() + 1) {
+      while (ev.size() < ops.size() + 1) {
+        cudaEvent_t e;
+        SPZ_CUDA_TRY(cudaEventCreate(&e));
+        ev.push_back(e);
+      }
+    }
+    SPZ_CUDA_TRY(cudaEventRecord(ev[0], Lr->stream));
+    for (size_t i = 0; i < ops.size(); ++i) {
+      cudaError_t e = ops[i].fn(Lr->stream);
+      if (e != cudaSuccess) return fail(SPZ_ECUDA, std::string("kernel ") + ops[i].cls + ": " + cudaGetErrorString(e));
+      SPZ_CUDA_TRY(cudaEventRecord(ev[i + 1], Lr->stream));
+    }
+    SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+    for (size_t i = 0; i < ops.size(); ++i) {
+      float t = 0;
+      SPZ_CUDA_TRY(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+      size_t c = 0;
+      for (; c < cls.size(); ++c)
+        if (std::strcmp(cls[c], ops[i].cls) == 0) break;
+      if (c == cls.size()) {
+        cls.push_back(ops[i].cls);
+        tot.push_back(0.0);
+      }
+      tot[c] += t;
+    }
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  const int nc = (int)std::min<size_t>(cls.size(), (size_t)std::max(cap, 0));
+  for (int i = 0; i < nc; ++i) {
+    if (names) names[i] = cls[i];
+    if (ms) ms[i] = tot[i] / (double)n_steps;
+  }
+  if (count) *count = (int)cls.size();
+  SPZ_TRY(read_counters(Lr));
+  return SPZ_OK;
+}
+
+spz_status spz_learner_launches_per_step(spz_learner* Lr, int64_t batch, int32_t* launches) {
+  if (!Lr || !launches) return fail(SPZ_EINVAL, "spz_learner_launches_per_step: NULL argument");
+  DeviceGuard dg(Lr->device);
+  SPZ_TRY(prepare(Lr, batch));
+  int n = 0;
+  for (auto& op : Lr->ops[0]) n += op.launches;
+  *launches = n;
+  return SPZ_OK;
+}
+
+spz_status spz_learner_debug_buffer(spz_learner* Lr, const char* name, void* host_out, int64_t bytes,
+                                    int64_t* bytes_required, int32_t* elem_size) {
+  if (!Lr || !name) return fail(SPZ_EINVAL, "spz_learner_debug_buffer: NULL argument");
+  DeviceGuard dg(Lr->device);
+  for (auto& b : Lr->debug) {
+    if (b.name != name) continue;
+    if (bytes_required) *bytes_required = (int64_t)b.bytes;
+    if (elem_size) *elem_size = b.esz;
+    if (!host_out) return SPZ_OK;
+    if (bytes < (int64_t)b.bytes) return fail(SPZ_EINVAL, "spz_learner_debug_buffer: output too small");
+    SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+    SPZ_CUDA_TRY(cudaMemcpyAsync(host_out, b.ptr, b.bytes, cudaMemcpyDeviceToHost, Lr->stream));
+    SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+    return SPZ_OK;
+  }
+  return fail(SPZ_EINVAL, std::string("spz_learner_debug_buffer: unknown buffer ") + name);
+}
+
+void spz_learner_destroy(spz_learner* Lr) { delete Lr; }
+
+}  // extern "C"

@@ -1,0 +1,210 @@
+// replay.cu -- device-resident replay ring: create / push / sample (a1-a2 of SURVEY.md §8(a)).
+//
+// PAPER.md §3.3.2: the experience pool the update process reads
+// "without consuming the time of the network update process".  Here the pool
+// lives in HBM as fp32 records [s | a | r | d | s2 | pad] (16-byte aligned rows),
+// slot(i) = i mod C, fill = min(cursor, C).
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+namespace spz {
+
+// ------------------------------------------------------------------ pack (device source)
+__global__ void pack_records_kernel(float* __restrict__ rec, int R, int o, int m, int64_t C, int64_t first, int64_t n,
+                                    const float* __restrict__ obs, const float* __restrict__ act,
+                                    const float* __restrict__ rew, const float* __restrict__ nobs,
+                                    const float* __restrict__ done) {
+  const int64_t total = n * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / R;
+    const int c = (int)(e - t * R);
+    float v = 0.f;
+    if (c < o) v = obs[t * o + c];
+    else if (c < o + m) v = act[t * m + (c - o)];
+    else if (c == o + m) v = rew[t];
+    else if (c == o + m + 1) v = done[t];
+    else if (c < 2 * o + m + 2) v = nobs[t * o + (c - o - m - 2)];
+    rec[((first + t) % C) * R + c] = v;
+  }
+}
+
+// ------------------------------------------------------------------ sample (API form)
+// One warp per row group: indices from Philox, 128-bit record loads, scatter to the
+// caller's separate arrays.
+constexpr int SAMPLE_ROWS = 32;
+
+__global__ void __launch_bounds__(256) sample_kernel(const float* __restrict__ rec, int R, int o, int m, int64_t fill,
+                                                     uint64_t seed, uint64_t step, int64_t B, int32_t* idx_out,
+                                                     float* obs, float* act, float* rew, float* nobs, float* done) {
+  extern __shared__ float4 sm4[];
+  float* sm = reinterpret_cast<float*>(sm4);
+  __shared__ int64_t sidx[SAMPLE_ROWS];
+  const int64_t r0 = (int64_t)blockIdx.x * SAMPLE_ROWS;
+  const int nrows = (int)(B - r0 < SAMPLE_ROWS ? B - r0 : SAMPLE_ROWS);
+  if (threadIdx.x < nrows) {
+    const int64_t i = sample_index(seed, step, (uint64_t)(r0 + threadIdx.x), (uint64_t)fill);
+    sidx[threadIdx.x] = i;
+    if (idx_out) idx_out[r0 + threadIdx.x] = (int32_t)i;
+  }
+  __syncthreads();
+  const int R4 = R >> 2;
+  for (int e = threadIdx.x; e < nrows * R4; e += blockDim.x) {
+    const int r = e / R4, q = e - r * R4;
+    sm4[e] = __ldg(reinterpret_cast<const float4*>(rec + sidx[r] * R) + q);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nrows * o; e += blockDim.x) {
+    const int r = e / o, c = e - r * o;
+    if (obs) obs[(r0 + r) * o + c] = sm[r * R + c];
+    if (nobs) nobs[(r0 + r) * o + c] = sm[r * R + o + m + 2 + c];
+  }
+  for (int e = threadIdx.x; e < nrows * m; e += blockDim.x) {
+    const int r = e / m, c = e - r * m;
+    if (act) act[(r0 + r) * m + c] = sm[r * R + o + c];
+  }
+  if (threadIdx.x < nrows) {
+    if (rew) rew[r0 + threadIdx.x] = sm[threadIdx.x * R + o + m];
+    if (done) done[r0 + threadIdx.x] = sm[threadIdx.x * R + o + m + 1];
+  }
+}
+
+}  // namespace spz
+
+using namespace spz;
+
+extern "C" {
+
+spz_status spz_replay_create(const spz_replay_desc* desc, spz_replay** out) {
+  if (!desc || !out) return fail(SPZ_EINVAL, "spz_replay_create: NULL argument");
+  *out = nullptr;
+  if (desc->obs_dim < 1 || desc->act_dim < 1) return fail(SPZ_EINVAL, "spz_replay_create: obs_dim and act_dim must be >= 1");
+  if (desc->capacity < 1) return fail(SPZ_EINVAL, "spz_replay_create: capacity must be >= 1 (S:193)");
+  spz_status st = check_device(desc->device);
+  if (st != SPZ_OK) return st;
+  auto* r = new spz_replay();
+  r->o = desc->obs_dim;
+  r->m = desc->act_dim;
+  r->C = desc->capacity;
+  r->R = (int)round_up(2 * r->o + r->m + 2, 4);
+  r->device = desc->device;
+  DeviceGuard dg(r->device);
+  const size_t bytes = (size_t)r->C * r->R * sizeof(float);
+  if (cudaMalloc(&r->rec, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    delete r;
+    return fail(SPZ_ENOMEM, "spz_replay_create: cannot allocate " + std::to_string(bytes) + " bytes for the ring");
+  }
+  if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMemsetAsync(r->rec, 0, bytes, r->stream) != cudaSuccess || cudaStreamSynchronize(r->stream) != cudaSuccess) {
+    cudaFree(r->rec);
+    delete r;
+    return fail(SPZ_ECUDA, "spz_replay_create: CUDA setup failed");
+  }
+  *out = r;
+  return SPZ_OK;
+}
+
+spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const float* act, const float* rew,
+                           const float* next_obs, const float* done, int32_t src_on_device, int64_t* first) {
+  if (!r) return fail(SPZ_EINVAL, "spz_replay_push: NULL ring");
+  if (n < 0) return fail(SPZ_EINVAL, "spz_replay_push: n < 0");
+  if (n > 0 && (!obs || !act || !rew || !next_obs || !done)) return fail(SPZ_EINVAL, "spz_replay_push: NULL field array");
+  DeviceGuard dg(r->device);
+  std::lock_guard<std::mutex> lk(r->mu);
+  const int64_t first_idx = r->cursor;
+  if (first) *first = first_idx;
+  if (n == 0) return SPZ_OK;
+  // only the last C records of a push can survive
+  const int64_t skip = n > r->C ? n - r->C : 0;
+  const int64_t nn = n - skip;
+  const int64_t start = first_idx + skip;
+  const int o = r->o, m = r->m, R = r->R;
+  if (src_on_device) {
+    const int64_t total = nn * R;
+    const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+    pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, obs + skip * o, act + skip * m,
+                                                        rew + skip, next_obs + skip * o, done + skip);
+    SPZ_CUDA_TRY(cudaGetLastError());
+  } else {
+    const size_t bytes = (size_t)nn * R * sizeof(float);
+    if (r->staging_bytes < bytes) {
+      if (r->staging) cudaFreeHost(r->staging);
+      r->staging = nullptr;
+      r->staging_bytes = 0;
+      SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+      SPZ_CUDA_TRY(cudaMallocHost(&r->staging, bytes));
+      r->staging_bytes = bytes;
+    } else {
+      SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));  // previous copy out of the staging buffer done
+    }
+    float* s = r->staging;
+    for (int64_t t = 0; t < nn; ++t) {
+      const int64_t src = t + skip;
+      float* d = s + t * R;
+      std::memcpy(d, obs + src * o, sizeof(float) * o);
+      std::memcpy(d + o, act + src * m, sizeof(float) * m);
+      d[o + m] = rew[src];
+      d[o + m + 1] = done[src];
+      std::memcpy(d + o + m + 2, next_obs + src * o, sizeof(float) * o);
+      for (int c = 2 * o + m + 2; c < R; ++c) d[c] = 0.f;
+    }
+    // at most two pieces, split at the wrap point
+    const int64_t slot = start % r->C;
+    const int64_t n1 = std::min(nn, r->C - slot);
+    SPZ_CUDA_TRY(cudaMemcpyAsync(r->rec + slot * R, s, (size_t)n1 * R * sizeof(float), cudaMemcpyHostToDevice, r->stream));
+    if (nn > n1)
+      SPZ_CUDA_TRY(cudaMemcpyAsync(r->rec, s + n1 * R, (size_t)(nn - n1) * R * sizeof(float), cudaMemcpyHostToDevice, r->stream));
+  }
+  SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  r->cursor += n;
+  return SPZ_OK;
+}
+
+spz_status spz_replay_sample(spz_replay* r, int64_t batch, uint64_t seed, uint64_t step, int32_t* idx, float* obs,
+                             float* act, float* rew, float* next_obs, float* done) {
+  if (!r) return fail(SPZ_EINVAL, "spz_replay_sample: NULL ring");
+  if (batch < 0) return fail(SPZ_EINVAL, "spz_replay_sample: batch < 0");
+  DeviceGuard dg(r->device);
+  const int64_t F = r->fill();
+  if (F < batch || F < 1) return fail(SPZ_ENODATA, "spz_replay_sample: fill " + std::to_string(F) + " < batch " + std::to_string(batch));
+  if (batch == 0) return SPZ_OK;
+  const unsigned blocks = (unsigned)cdiv(batch, SAMPLE_ROWS);
+  const size_t smem = (size_t)SAMPLE_ROWS * r->R * sizeof(float);
+  sample_kernel<<<blocks, 256, smem, r->stream>>>(r->rec, r->R, r->o, r->m, F, seed, step, batch, idx, obs, act, rew,
+                                                  next_obs, done);
+  SPZ_CUDA_TRY(cudaGetLastError());
+  SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  return SPZ_OK;
+}
+
+spz_status spz_replay_info(const spz_replay* r, int64_t* cursor, int64_t* fill, int64_t* capacity) {
+  if (!r) return fail(SPZ_EINVAL, "spz_replay_info: NULL ring");
+  if (cursor) *cursor = r->cursor;
+  if (fill) *fill = r->fill();
+  if (capacity) *capacity = r->C;
+  return SPZ_OK;
+}
+
+spz_status spz_replay_records(const spz_replay* r, const float** records, int32_t* record_floats) {
+  if (!r) return fail(SPZ_EINVAL, "spz_replay_records: NULL ring");
+  if (records) *records = r->rec;
+  if (record_floats) *record_floats = r->R;
+  return SPZ_OK;
+}
+
+void spz_replay_destroy(spz_replay* r) {
+  if (!r) return;
+  {
+    DeviceGuard dg(r->device);
+    cudaStreamSynchronize(r->stream);
+    cudaFree(r->rec);
+    if (r->staging) cudaFreeHost(r->staging);
+    cudaStreamDestroy(r->stream);
+  }
+  delete r;
+}
+
+}  // extern "C"

@@ -1,0 +1,13 @@
+// tc_gemm.cuh -- tcgen05 / TMEM / TMA bf16 GEMM (sm_100a) behind the GemmArgs contract.
+#pragma once
+
+#include "gemm.cuh"
+
+namespace spz {
+
+// True if the tensor-core kernel handles this problem (layouts, alignment, sizes).
+bool tc_gemm_supported(const GemmArgs& a);
+// Launch it (bf16 operands, fp32 accumulation in TMEM, shared epilogues).
+cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st);
+
+}  // namespace spz

@@ -1,0 +1,341 @@
+"""ctypes binding of libspz.so (include/spz.h) -- argument marshalling only.
+
+Every function below forwards to the C entry point of the same name; no step of
+the update runs in Python.  There is no CPU fallback: if libspz.so is missing or
+cannot find an sm_100 device the calls fail loudly (``SpzError``).
+
+Convenience classes ``Replay`` and ``Learner`` wrap the handles (RAII + numpy /
+torch marshalling); they add no computation.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspz.so")
+
+SPZ_OK, SPZ_EINVAL, SPZ_ENODATA, SPZ_ENONFINITE, SPZ_ECUDA, SPZ_ENCCL, SPZ_ENOMEM, SPZ_ESTATE, SPZ_ETIMEOUT, SPZ_EUNSUPPORTED = (
+    0, -1, -2, -3, -4, -5, -6, -7, -8, -9)
+STATUS_NAMES = {0: "SPZ_OK", -1: "SPZ_EINVAL", -2: "SPZ_ENODATA", -3: "SPZ_ENONFINITE", -4: "SPZ_ECUDA",
+                -5: "SPZ_ENCCL", -6: "SPZ_ENOMEM", -7: "SPZ_ESTATE", -8: "SPZ_ETIMEOUT", -9: "SPZ_EUNSUPPORTED"}
+SPZ_SAC, SPZ_TD3 = 0, 1
+SPZ_FP32, SPZ_BF16 = 0, 1
+SPZ_ROLE_ALL, SPZ_ROLE_CRITIC, SPZ_ROLE_ACTOR = 0, 1, 2
+SPZ_T_ACTOR, SPZ_T_Q1, SPZ_T_Q2, SPZ_T_Q1_TARG, SPZ_T_Q2_TARG, SPZ_T_ACTOR_TARG, SPZ_T_LOG_ALPHA = range(7)
+SPZ_S_PARAM, SPZ_S_ADAM_M, SPZ_S_ADAM_V = 0, 1, 2
+
+# Every symbol include/spz.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "spz_last_error", "spz_version", "spz_replay_create", "spz_replay_push", "spz_replay_sample", "spz_replay_info",
+    "spz_replay_records", "spz_replay_destroy", "spz_config_default", "spz_nccl_unique_id", "spz_learner_create",
+    "spz_update", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
+    "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
+]
+
+
+class SpzError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class spz_replay_desc(ctypes.Structure):
+    _fields_ = [("obs_dim", ctypes.c_int32), ("act_dim", ctypes.c_int32), ("capacity", ctypes.c_int64),
+                ("device", ctypes.c_int32)]
+
+
+class spz_config(ctypes.Structure):
+    _fields_ = [
+        ("algo", ctypes.c_int), ("precision", ctypes.c_int),
+        ("obs_dim", ctypes.c_int32), ("act_dim", ctypes.c_int32),
+        ("hidden", ctypes.c_int32), ("n_hidden", ctypes.c_int32),
+        ("max_batch", ctypes.c_int64),
+        ("gamma", ctypes.c_double), ("tau", ctypes.c_double),
+        ("lr_actor", ctypes.c_double), ("lr_critic", ctypes.c_double), ("lr_alpha", ctypes.c_double),
+        ("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("adam_eps", ctypes.c_double),
+        ("alpha_auto", ctypes.c_int32),
+        ("alpha_init", ctypes.c_double), ("target_entropy", ctypes.c_double),
+        ("log_std_min", ctypes.c_double), ("log_std_max", ctypes.c_double),
+        ("td3_noise", ctypes.c_double), ("td3_noise_clip", ctypes.c_double), ("td3_policy_delay", ctypes.c_int32),
+        ("seed", ctypes.c_uint64), ("init_seed", ctypes.c_uint64),
+        ("device", ctypes.c_int32), ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
+        ("n_critic_ranks", ctypes.c_int32), ("n_actor_ranks", ctypes.c_int32),
+        ("role", ctypes.c_int),
+        ("nccl_unique_id", ctypes.c_void_p),
+        ("use_graph", ctypes.c_int32),
+    ]
+
+
+class spz_stats(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_int64), ("critic_loss", ctypes.c_double), ("actor_loss", ctypes.c_double),
+                ("alpha", ctypes.c_double), ("alpha_loss", ctypes.c_double), ("q1_mean", ctypes.c_double),
+                ("q2_mean", ctypes.c_double), ("logp_mean", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libspz.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SpzError(SPZ_ECUDA, f"{LIB_PATH} is missing: run `python -m paper_2312_06126_b200.build` "
+                                      "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, U64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+        sig = {
+            "spz_last_error": (ctypes.c_char_p, []),
+            "spz_version": (ctypes.c_char_p, []),
+            "spz_replay_create": (ctypes.c_int, [ctypes.POINTER(spz_replay_desc), ctypes.POINTER(P)]),
+            "spz_replay_push": (ctypes.c_int, [P, I64, P, P, P, P, P, I32, ctypes.POINTER(I64)]),
+            "spz_replay_sample": (ctypes.c_int, [P, I64, U64, U64, P, P, P, P, P, P]),
+            "spz_replay_info": (ctypes.c_int, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+            "spz_replay_records": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(I32)]),
+            "spz_replay_destroy": (None, [P]),
+            "spz_config_default": (ctypes.c_int, [ctypes.c_int, I32, I32, ctypes.POINTER(spz_config)]),
+            "spz_nccl_unique_id": (ctypes.c_int, [P]),
+            "spz_learner_create": (ctypes.c_int, [ctypes.POINTER(spz_config), P, ctypes.POINTER(P)]),
+            "spz_update": (ctypes.c_int, [P, I64, I64, ctypes.POINTER(spz_stats)]),
+            "spz_learner_set_stream": (ctypes.c_int, [P, P]),
+            "spz_get_params": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, I64, ctypes.POINTER(I64)]),
+            "spz_set_params": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, I64]),
+            "spz_get_counters": (ctypes.c_int, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64),
+                                                ctypes.POINTER(I64)]),
+            "spz_sync_actor": (ctypes.c_int, [P, I32, P, I64, ctypes.POINTER(U64)]),
+            "spz_learner_profile": (ctypes.c_int, [P, I64, I64, I32, ctypes.POINTER(ctypes.c_char_p),
+                                                   ctypes.POINTER(D), ctypes.POINTER(I32)]),
+            "spz_learner_launches_per_step": (ctypes.c_int, [P, I64, ctypes.POINTER(I32)]),
+            "spz_learner_debug_buffer": (ctypes.c_int, [P, ctypes.c_char_p, P, I64, ctypes.POINTER(I64),
+                                                        ctypes.POINTER(I32)]),
+            "spz_learner_destroy": (None, [P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status):
+    if status != SPZ_OK:
+        raise SpzError(status, lib().spz_last_error().decode())
+    return status
+
+
+# ----------------------------------------------------------------------------- same-name functions
+
+def spz_version():
+    return lib().spz_version().decode()
+
+
+def spz_last_error():
+    return lib().spz_last_error().decode()
+
+
+def spz_replay_create(obs_dim, act_dim, capacity, device=0):
+    h = ctypes.c_void_p()
+    _check(lib().spz_replay_create(ctypes.byref(spz_replay_desc(obs_dim, act_dim, capacity, device)), ctypes.byref(h)))
+    return h
+
+
+def _ptr(x):
+    """Host numpy array -> pointer (must be float32 C-contiguous); torch tensor -> data_ptr."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return ctypes.c_void_p(x.data_ptr())
+    assert x.flags["C_CONTIGUOUS"]
+    return x.ctypes.data_as(ctypes.c_void_p)
+
+
+def spz_replay_push(ring, obs, act, rew, next_obs, done, src_on_device=False):
+    """Host path: float32 numpy arrays; device path: torch CUDA float32 tensors."""
+    n = len(rew)
+    if not src_on_device:
+        obs, act, rew, next_obs, done = [np.ascontiguousarray(a, dtype=np.float32) for a in (obs, act, rew, next_obs, done)]
+    first = ctypes.c_int64()
+    _check(lib().spz_replay_push(ring, n, _ptr(obs), _ptr(act), _ptr(rew), _ptr(next_obs), _ptr(done),
+                                 1 if src_on_device else 0, ctypes.byref(first)))
+    return first.value
+
+
+def spz_replay_sample(ring, batch, seed, step, idx=None, obs=None, act=None, rew=None, next_obs=None, done=None):
+    """Outputs are device tensors (torch) or None."""
+    _check(lib().spz_replay_sample(ring, batch, seed, step, _ptr(idx), _ptr(obs), _ptr(act), _ptr(rew),
+                                   _ptr(next_obs), _ptr(done)))
+
+
+def spz_replay_info(ring):
+    c, f, cap = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().spz_replay_info(ring, ctypes.byref(c), ctypes.byref(f), ctypes.byref(cap)))
+    return c.value, f.value, cap.value
+
+
+def spz_replay_destroy(ring):
+    lib().spz_replay_destroy(ring)
+
+
+def spz_config_default(algo, obs_dim, act_dim):
+    c = spz_config()
+    _check(lib().spz_config_default(algo, obs_dim, act_dim, ctypes.byref(c)))
+    return c
+
+
+def spz_learner_create(cfg, ring):
+    h = ctypes.c_void_p()
+    _check(lib().spz_learner_create(ctypes.byref(cfg), ring, ctypes.byref(h)))
+    return h
+
+
+def spz_update(learner, batch, n_steps):
+    s = spz_stats()
+    _check(lib().spz_update(learner, batch, n_steps, ctypes.byref(s)))
+    return s.as_dict()
+
+
+def spz_learner_set_stream(learner, stream_handle):
+    _check(lib().spz_learner_set_stream(learner, ctypes.c_void_p(stream_handle) if stream_handle else None))
+
+
+def spz_get_params(learner, tensor, slot=SPZ_S_PARAM):
+    need = ctypes.c_int64()
+    lib().spz_get_params(learner, tensor, slot, None, 0, ctypes.byref(need))
+    if need.value <= 0:
+        _check(lib().spz_get_params(learner, tensor, slot, None, 0, ctypes.byref(need)))
+    out = np.empty(need.value, np.float32)
+    _check(lib().spz_get_params(learner, tensor, slot, _ptr(out), out.size, ctypes.byref(need)))
+    return out
+
+
+def spz_set_params(learner, tensor, values, slot=SPZ_S_PARAM):
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    _check(lib().spz_set_params(learner, tensor, slot, _ptr(v), v.size))
+
+
+def spz_get_counters(learner):
+    a = [ctypes.c_int64() for _ in range(4)]
+    _check(lib().spz_get_counters(learner, *[ctypes.byref(x) for x in a]))
+    return dict(step=a[0].value, t_critic=a[1].value, t_actor=a[2].value, t_alpha=a[3].value)
+
+
+def spz_sync_actor(learner, dst_device, dst_ptr, dst_bytes):
+    v = ctypes.c_uint64()
+    _check(lib().spz_sync_actor(learner, dst_device, ctypes.c_void_p(dst_ptr), dst_bytes, ctypes.byref(v)))
+    return v.value
+
+
+def spz_learner_profile(learner, batch, n_steps, cap=64):
+    names = (ctypes.c_char_p * cap)()
+    ms = (ctypes.c_double * cap)()
+    cnt = ctypes.c_int32()
+    _check(lib().spz_learner_profile(learner, batch, n_steps, cap, names, ms, ctypes.byref(cnt)))
+    return {names[i].decode(): ms[i] for i in range(min(cnt.value, cap))}
+
+
+def spz_learner_launches_per_step(learner, batch):
+    n = ctypes.c_int32()
+    _check(lib().spz_learner_launches_per_step(learner, batch, ctypes.byref(n)))
+    return n.value
+
+
+def spz_learner_debug_buffer(learner, name):
+    """Internal buffer as a numpy array (bf16 buffers widened to float32; "idx" as int32)."""
+    need, es = ctypes.c_int64(), ctypes.c_int32()
+    _check(lib().spz_learner_debug_buffer(learner, name.encode(), None, 0, ctypes.byref(need), ctypes.byref(es)))
+    raw = np.empty(need.value, np.uint8)
+    _check(lib().spz_learner_debug_buffer(learner, name.encode(), _ptr(raw), raw.size, ctypes.byref(need),
+                                          ctypes.byref(es)))
+    if name == "idx":
+        return raw.view(np.int32)
+    if es.value == 2:
+        return (raw.view(np.uint16).astype(np.uint32) << 16).view(np.float32)
+    return raw.view(np.float32)
+
+
+def spz_learner_destroy(learner):
+    lib().spz_learner_destroy(learner)
+
+
+# ----------------------------------------------------------------------------- RAII wrappers
+
+class Replay:
+    def __init__(self, obs_dim, act_dim, capacity, device=0):
+        self.obs_dim, self.act_dim, self.capacity, self.device = obs_dim, act_dim, capacity, device
+        self.h = spz_replay_create(obs_dim, act_dim, capacity, device)
+
+    def push(self, obs, act, rew, next_obs, done, src_on_device=False):
+        return spz_replay_push(self.h, obs, act, rew, next_obs, done, src_on_device)
+
+    def info(self):
+        return spz_replay_info(self.h)
+
+    def close(self):
+        if self.h:
+            spz_replay_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+PARAM_TENSORS = {"actor": SPZ_T_ACTOR, "q1": SPZ_T_Q1, "q2": SPZ_T_Q2, "q1_targ": SPZ_T_Q1_TARG,
+                 "q2_targ": SPZ_T_Q2_TARG, "actor_targ": SPZ_T_ACTOR_TARG, "log_alpha": SPZ_T_LOG_ALPHA}
+
+
+class Learner:
+    def __init__(self, ring: Replay, algo="sac", precision="bf16", hidden=256, n_hidden=2, max_batch=8192,
+                 device=0, use_graph=True, **overrides):
+        cfg = spz_config_default(SPZ_SAC if algo == "sac" else SPZ_TD3, ring.obs_dim, ring.act_dim)
+        cfg.precision = SPZ_BF16 if precision == "bf16" else SPZ_FP32
+        cfg.hidden, cfg.n_hidden, cfg.max_batch, cfg.device = hidden, n_hidden, max_batch, device
+        cfg.use_graph = 1 if use_graph else 0
+        for k, v in overrides.items():
+            setattr(cfg, k, v)
+        self.cfg = cfg
+        self.ring = ring
+        self.h = spz_learner_create(cfg, ring.h)
+
+    def update(self, batch, n_steps=1):
+        return spz_update(self.h, batch, n_steps)
+
+    def get(self, name, slot=SPZ_S_PARAM):
+        return spz_get_params(self.h, PARAM_TENSORS[name], slot)
+
+    def set(self, name, values, slot=SPZ_S_PARAM):
+        spz_set_params(self.h, PARAM_TENSORS[name], values, slot)
+
+    def counters(self):
+        return spz_get_counters(self.h)
+
+    def set_stream(self, handle):
+        spz_learner_set_stream(self.h, handle)
+
+    def profile(self, batch, n_steps):
+        return spz_learner_profile(self.h, batch, n_steps)
+
+    def debug(self, name):
+        return spz_learner_debug_buffer(self.h, name)
+
+    def launches_per_step(self, batch):
+        return spz_learner_launches_per_step(self.h, batch)
+
+    def close(self):
+        if self.h:
+            spz_learner_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

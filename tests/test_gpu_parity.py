@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle.
+
+Bar (BASELINE.json north_star): replay indices and gathered rows
+bit-exact; losses and every parameter / Adam-moment tensor after K updates within
+||x - x*|| / ||x*|| <= 1e-4 (FP32 path) or 2e-2 (BF16 tensor-core path).
+"""
+
+import numpy as np
+import pytest
+
+import synthdata
+from oracle import ring as oring, sac as osac, td3 as otd3
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2312_06126_b200 import spz  # noqa: E402
+
+TOL = {"fp32": 1e-4, "bf16": 2e-2}
+
+
+def rel(x, ref):
+    x, ref = np.asarray(x, np.float64), np.asarray(ref, np.float64)
+    return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-30))
+
+
+def make_rings(o, m, C, n_push=None, seed=synthdata.DATA_SEED, kind="locomotion"):
+    tr = synthdata.transitions(kind, o, m, C if n_push is None else n_push, seed=seed)
+    g = spz.Replay(o, m, C)
+    first = g.push(**tr)
+    r = oring.Ring(o, m, C)
+    assert r.push(**tr) == first
+    return g, r
+
+
+# ----------------------------------------------------------------------------- a1 + a2 bit-exact
+
+@pytest.mark.parametrize("o,m,C,n_push,B", [
+    (3, 1, 10_000, None, 256),        # PEN
+    (3, 1, 100, 1, 1),                # fill 1, batch 1
+    (22, 6, 5000, 3000, 1000),        # partial fill, ragged batch
+    (44, 17, 4096, 10_000, 777),      # wrapped ring (10000 pushes into 4096 slots), odd batch
+    (28, 8, 1_000_000, None, 32768),  # ANT-size ring, full batch
+])
+def test_replay_sample_bit_exact(o, m, C, n_push, B):
+    g, r = make_rings(o, m, C, n_push)
+    for step in (0, 7):
+        idx = torch.empty(B, dtype=torch.int32, device="cuda")
+        obs = torch.empty(B, o, device="cuda")
+        act = torch.empty(B, m, device="cuda")
+        rew = torch.empty(B, device="cuda")
+        nobs = torch.empty(B, o, device="cuda")
+        done = torch.empty(B, device="cuda")
+        spz.spz_replay_sample(g.h, B, synthdata.SAMPLE_SEED, step, idx, obs, act, rew, nobs, done)
+        ridx, rb = r.sample(B, synthdata.SAMPLE_SEED, step)
+        assert np.array_equal(idx.cpu().numpy(), ridx)
+        for name, t in (("obs", obs), ("act", act), ("rew", rew), ("next_obs", nobs), ("done", done)):
+            assert np.array_equal(t.cpu().numpy(), rb[name]), name
+
+
+def test_replay_errors_and_info():
+    g = spz.Replay(3, 1, 8)
+    assert g.info() == (0, 0, 8)
+    with pytest.raises(spz.SpzError) as e:
+        spz.spz_replay_sample(g.h, 1, 1, 0)
+    assert e.value.status == spz.SPZ_ENODATA
+    tr = synthdata.transitions("pendulum", 3, 1, 11)
+    assert g.push(**tr) == 0
+    assert g.info() == (11, 8, 8)
+
+
+def test_replay_push_from_device_matches_host():
+    o, m, C = 22, 6, 1000
+    tr = synthdata.transitions("locomotion", o, m, 1500)
+    a, b = spz.Replay(o, m, C), spz.Replay(o, m, C)
+    a.push(**tr)
+    b.push(**{k: torch.from_numpy(v).cuda() for k, v in tr.items()}, src_on_device=True)
+    B = 512
+    outs = []
+    for g in (a, b):
+        idx = torch.empty(B, dtype=torch.int32, device="cuda")
+        obs = torch.empty(B, o, device="cuda")
+        spz.spz_replay_sample(g.h, B, 5, 3, idx, obs)
+        outs.append((idx.cpu().numpy(), obs.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+# ----------------------------------------------------------------------------- whole update parity
+
+def run_parity(algo, precision, o, m, h, L, B, C, K, kind="locomotion", use_graph=True, check_moments=True):
+    g, r = make_rings(o, m, C, kind=kind)
+    p = synthdata.init_params(o, m, h, L, algo=algo)
+    lrn = spz.Learner(g, algo=algo, precision=precision, hidden=h, n_hidden=L, max_batch=B, use_graph=use_graph)
+    lrn.set("actor", p["actor"])
+    lrn.set("q1", p["q1"])
+    lrn.set("q2", p["q2"])
+    lrn.set("q1_targ", p["q1"])
+    lrn.set("q2_targ", p["q2"])
+    if algo == "td3":
+        lrn.set("actor_targ", p["actor"])
+    cfg = osac.Config(obs_dim=o, act_dim=m, hidden=h, n_hidden=L, alpha_auto=(algo == "sac"))
+    la = float(lrn.get("log_alpha")[0])
+    st = osac.State.create(p["actor"], p["q1"], p["q2"], log_alpha=la,
+                           actor_targ=p["actor"] if algo == "td3" else None)
+    tol = TOL[precision]
+    for k in range(K):
+        gs = lrn.update(B, 1)
+        if algo == "sac":
+            st, os_, _ = osac.sac_step(st, r, B, synthdata.SAMPLE_SEED, cfg)
+        else:
+            st, os_, _ = otd3.td3_step(st, r, B, synthdata.SAMPLE_SEED, cfg)
+        assert gs["step"] == k + 1
+        for key in ("critic_loss", "actor_loss", "q1_mean", "q2_mean", "logp_mean", "alpha"):
+            ref = os_[key]
+            assert abs(gs[key] - ref) <= tol * max(abs(ref), 1e-6) + (tol * 1e-2 if key in ("q1_mean", "q2_mean") else 0), (k, key, gs[key], ref)
+    names = ["actor", "q1", "q2", "q1_targ", "q2_targ"] + (["actor_targ"] if algo == "td3" else [])
+    errs = {}
+    for n in names:
+        errs[n] = rel(lrn.get(n), getattr(st, n))
+        assert errs[n] <= tol, (n, errs)
+    if algo == "sac":
+        assert abs(float(lrn.get("log_alpha")[0]) - st.log_alpha) <= tol * max(1.0, abs(st.log_alpha))
+    if check_moments:
+        for n in ("actor", "q1", "q2"):
+            mm = lrn.get(n, spz.SPZ_S_ADAM_M)
+            assert rel(mm, st.opt[n].m) <= 10 * tol, (n, "m", rel(mm, st.opt[n].m))
+    c = lrn.counters()
+    assert c["step"] == K and c["t_critic"] == K
+    assert c["t_actor"] == (K if algo == "sac" else sum(1 for k in range(K) if otd3.is_delayed(k, cfg)))
+    return errs
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_sac_parity_pendulum(precision):
+    # BASELINE config 0: Pendulum-shaped SAC, 2x64, B 256, 10K ring (200 updates in the bench; 30 here)
+    run_parity("sac", precision, 3, 1, 64, 2, 256, 10_000, 30, kind="pendulum")
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_sac_parity_ragged_multitile(precision):
+    # several 128-row tiles plus a ragged tail; K tails (o + m = 28 not a multiple of 8/16/64)
+    run_parity("sac", precision, 22, 6, 256, 2, 1000, 20_000, 5)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_td3_parity(precision):
+    run_parity("td3", precision, 44, 17, 128, 3, 600, 8000, 4)
+
+
+def test_sac_parity_graph_vs_eager_bit_identical():
+    outs = []
+    for use_graph in (True, False):
+        g, _ = make_rings(5, 2, 3000)
+        lrn = spz.Learner(g, precision="bf16", hidden=64, n_hidden=2, max_batch=512, use_graph=use_graph)
+        lrn.update(512, 3)
+        outs.append([lrn.get(n) for n in ("actor", "q1", "q2", "q1_targ")])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_determinism_two_runs_bit_identical():
+    outs = []
+    for _ in range(2):
+        g, _ = make_rings(22, 6, 20_000)
+        lrn = spz.Learner(g, precision="bf16", hidden=256, n_hidden=2, max_batch=2048)
+        s = lrn.update(2048, 4)
+        outs.append((s, [lrn.get(n) for n in ("actor", "q1", "q2")]))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_walker_full_size_two_steps(precision):
+    """BASELINE config 1 at full size (B 8192, 2x256, 1M ring), in the launch configuration the bench times."""
+    run_parity("sac", precision, 22, 6, 256, 2, 8192, 1_000_000, 2, check_moments=False)
+
+
+# ----------------------------------------------------------------------------- API behaviour
+
+def test_update_errors_and_batch_change():
+    g, _ = make_rings(3, 1, 300, kind="pendulum")
+    lrn = spz.Learner(g, precision="bf16", hidden=64, n_hidden=2, max_batch=256)
+    with pytest.raises(spz.SpzError) as e:
+        lrn.update(512, 1)
+    assert e.value.status == spz.SPZ_EINVAL
+    lrn.update(256, 2)
+    lrn.update(100, 2)  # batch may change between calls; Adam moments preserved
+    assert lrn.counters()["step"] == 4
+    small = spz.Replay(3, 1, 100)
+    small.push(**synthdata.transitions("pendulum", 3, 1, 10))
+    l2 = spz.Learner(small, precision="bf16", hidden=64, n_hidden=2, max_batch=256)
+    with pytest.raises(spz.SpzError) as e:
+        l2.update(64, 1)
+    assert e.value.status == spz.SPZ_ENODATA
+    assert l2.counters()["step"] == 0
+
+
+def test_set_get_roundtrip_and_default_init():
+    g, _ = make_rings(22, 6, 2000)
+    lrn = spz.Learner(g, precision="fp32", hidden=256, n_hidden=2, max_batch=1024)
+    a = lrn.get("actor")
+    # W, b ~ U(+-1/sqrt(fan_in)): first layer fan_in = 22
+    W1 = a[:256 * 22]
+    assert np.abs(W1).max() <= 1 / np.sqrt(22) + 1e-7 and abs(W1.mean()) < 0.01 and W1.std() > 0.1
+    assert np.array_equal(lrn.get("q1"), lrn.get("q1_targ"))
+    v = np.random.default_rng(0).standard_normal(a.size).astype(np.float32)
+    lrn.set("actor", v)
+    assert np.array_equal(lrn.get("actor"), v)
+    assert abs(float(lrn.get("log_alpha")[0]) - np.log(0.2)) < 1e-6
+
+
+def test_sync_actor_versioned_payload():
+    g, _ = make_rings(22, 6, 2000)
+    lrn = spz.Learner(g, precision="bf16", hidden=64, n_hidden=2, max_batch=512)
+    n = lrn.get("actor").size
+    buf = torch.zeros(16 + 4 * n, dtype=torch.uint8, device="cuda")
+    v1 = spz.spz_sync_actor(lrn.h, 0, buf.data_ptr(), buf.numel())
+    lrn.update(512, 1)
+    v2 = spz.spz_sync_actor(lrn.h, 0, buf.data_ptr(), buf.numel())
+    assert v2 == v1 + 1
+    hdr = buf[:16].cpu().numpy().view(np.uint64)
+    assert hdr[0] == v2 and hdr[1] == n
+    assert np.array_equal(buf[16:].cpu().numpy().view(np.float32), lrn.get("actor"))
+
+
+def test_profile_and_launch_count():
+    g, _ = make_rings(22, 6, 20_000)
+    lrn = spz.Learner(g, precision="bf16", hidden=256, n_hidden=2, max_batch=8192)
+    prof = lrn.profile(8192, 3)
+    assert "gather" in prof and "adam_polyak" in prof and all(v > 0 for v in prof.values())
+    assert lrn.launches_per_step(8192) >= 20
+    assert lrn.counters()["step"] == 3

@@ -210,6 +210,17 @@ spz_status spz_learner_debug_buffer(spz_learner* L, const char* name, void* host
 
 void spz_learner_destroy(spz_learner* L);
 
+/* ------------------------------------------------------------------ diagnostics
+ * The dense-layer GEMM of the update on its own, for kernel tests: on `device`,
+ * C[m, n] (fp32, row pitch ldc) = sum_k A(m, k) B(n, k) over bf16 device operands with
+ * A(m,k) = a_mn ? A[k*lda + m] : A[m*lda + k] and B(n,k) = b_mn ? B[k*ldb + n] : B[n*ldb + k].
+ * With splits > 1 the contraction is cut into chunks of k_per_split (multiple of 64) and
+ * chunk s is written to C + s*M*ldc.  tensor_cores = 1 runs the tcgen05 kernel (SPZ_EUNSUPPORTED
+ * if the problem does not qualify), 0 the SIMT kernel.  Synchronous. */
+spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, int64_t N, int64_t K,
+                              const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb,
+                              int32_t b_mn, float* C, int64_t ldc, int32_t splits, int64_t k_per_split);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,4 +45,40 @@ spz_status spz_nccl_unique_id(uint8_t out[128]) {
   return spz::fail(SPZ_EUNSUPPORTED, "spz_nccl_unique_id: NCCL support not built yet");
 }
 
+spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, int64_t N, int64_t K, const void* A,
+                              int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C, int64_t ldc,
+                              int32_t splits, int64_t k_per_split) {
+  spz_status st = spz::check_device(device);
+  if (st != SPZ_OK) return st;
+  if (M < 1 || N < 1 || K < 1 || !A || !B || !C || splits < 1) return spz::fail(SPZ_EINVAL, "spz_diag_gemm_bf16: bad argument");
+  spz::DeviceGuard dg(device);
+  spz::GemmArgs a{};
+  a.N = (int)N;
+  a.K = (int)K;
+  a.lda = (int)lda;
+  a.ldb = (int)ldb;
+  a.ldc = (int)ldc;
+  a.a_mn = a_mn;
+  a.b_mn = b_mn;
+  a.epi = spz::EPI_F32;
+  a.splits = splits;
+  a.k_per_split = splits > 1 ? (int)k_per_split : (int)K;
+  a.split_stride = M * ldc;
+  a.n_groups = 1;
+  a.g[0].A = A;
+  a.g[0].B = B;
+  a.g[0].C = C;
+  a.g[0].M = (int)M;
+  cudaError_t e;
+  if (tensor_cores) {
+    if (!spz::tc_gemm_supported(a)) return spz::fail(SPZ_EUNSUPPORTED, "spz_diag_gemm_bf16: problem not supported by the tcgen05 kernel");
+    e = spz::tc_gemm_bf16(a, 0);
+  } else {
+    e = spz::gemm_simt<__nv_bfloat16>(a, 0);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return spz::fail(SPZ_ECUDA, std::string("spz_diag_gemm_bf16: ") + cudaGetErrorString(e));
+  return SPZ_OK;
+}
+
 }  // extern "C"

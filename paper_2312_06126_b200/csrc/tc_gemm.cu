@@ -1,7 +1,399 @@
-// tc_gemm.cu -- placeholder until the tcgen05 kernel lands: every problem goes to SIMT.
+// tc_gemm.cu -- bf16 GEMM on the 5th-generation tensor cores (sm_100a): TMA -> SMEM (128 B
+// swizzle) -> tcgen05.mma (accumulator in TMEM) -> tcgen05.ld epilogue, with the shared
+// GemmArgs epilogues (bias + ReLU, dgrad ReLU mask, fp32 head / split-K partial stores).
+//
+// One CTA computes a 128 x BN output tile (UMMA M = 128, N = BN, K = 16 per instruction)
+// over a 64-deep K slab per pipeline stage:
+//   warp 0      TMA producer (one elected lane), 4-stage mbarrier ring (full / empty)
+//   warp 1      TMEM allocator + MMA issuer (one lane issues tcgen05.mma, commits to mbarriers)
+//   warps 2..5  epilogue: TMEM lane quarter (warp % 4) -> 32 rows x BN fp32 columns
+// Operands may be K-major (activations [rows x K], weights [out x in] in the forward) or
+// MN-major (weights in dgrad; activations and dZ in wgrad, where the contraction runs over the
+// batch) -- both are native UMMA smem-descriptor layouts, so no transposed copies exist.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
 #include "tc_gemm.cuh"
 
 namespace spz {
-bool tc_gemm_supported(const GemmArgs&) { return false; }
-cudaError_t tc_gemm_bf16(const GemmArgs&, cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace {
+
+constexpr int BM = 128, BK = 64, STAGES = 4, NTHREADS = 192;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+
+struct TcParams {
+  GemmArgs a;
+  CUtensorMap ta[4];
+  CUtensorMap tb[4];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// UMMA shared-memory descriptor (sm_100): start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
+// version 1 [46,48), base offset 0, layout SWIZZLE_128B (2) [61,64).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// K-major SW128 tile (rows x 64 bf16, 128 B rows): 8-row atoms 1024 B apart; K step of 16 = +32 B.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int kk) { return umma_desc(base + kk * 32, 16, 1024); }
+// MN-major SW128 tile (64 K-rows x 64-element MN chunks, chunks 8 KB apart): 8-K-row groups
+// 1024 B apart (SBO), MN chunks 8192 B apart (LBO); K step of 16 = +2048 B.
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int kk) { return umma_desc(base + kk * 2048, 8192, 1024); }
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+
+// Epilogue of 16 consecutive accumulator columns n..n+15 of row m.
+__device__ __forceinline__ void epi16(const GemmArgs& a, const GemmGroup& g, int split, int m, int n, const float (&v)[16]) {
+  const bool full = n + 16 <= a.N;
+  const int64_t off = (int64_t)m * a.ldc + n;
+  switch (a.epi) {
+    case EPI_BIAS_RELU: {
+      __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C);
+      if (full && (a.ldc & 7) == 0) {
+        uint32_t p[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float z0 = v[2 * j] + __ldg(g.bias + n + 2 * j), z1 = v[2 * j + 1] + __ldg(g.bias + n + 2 * j + 1);
+          p[j] = pack_bf16(fmaxf(z0, 0.f), fmaxf(z1, 0.f));
+        }
+        uint4* dst = reinterpret_cast<uint4*>(C + off);
+        dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
+        dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+      } else {
+        for (int j = 0; j < 16 && n + j < a.N; ++j) C[off + j] = __float2bfloat16_rn(fmaxf(v[j] + g.bias[n + j], 0.f));
+      }
+      break;
+    }
+    case EPI_MASK: {
+      __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C);
+      const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(g.aux) + (int64_t)m * a.ldaux + n;
+      if (full && (a.ldc & 7) == 0 && (a.ldaux & 7) == 0) {
+        const uint4 x0 = reinterpret_cast<const uint4*>(X)[0], x1 = reinterpret_cast<const uint4*>(X)[1];
+        const __nv_bfloat16* xs0 = reinterpret_cast<const __nv_bfloat16*>(&x0);
+        const __nv_bfloat16* xs1 = reinterpret_cast<const __nv_bfloat16*>(&x1);
+        uint32_t p[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const __nv_bfloat16 a0 = j < 4 ? xs0[2 * j] : xs1[2 * j - 8];
+          const __nv_bfloat16 a1 = j < 4 ? xs0[2 * j + 1] : xs1[2 * j - 7];
+          p[j] = pack_bf16(__bfloat162float(a0) > 0.f ? v[2 * j] : 0.f, __bfloat162float(a1) > 0.f ? v[2 * j + 1] : 0.f);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(C + off);
+        dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
+        dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+      } else {
+        for (int j = 0; j < 16 && n + j < a.N; ++j)
+          C[off + j] = __float2bfloat16_rn(__bfloat162float(X[j]) > 0.f ? v[j] : 0.f);
+      }
+      break;
+    }
+    case EPI_BIAS_F32: {
+      float* C = static_cast<float*>(g.C) + off;
+      for (int j = 0; j < 16 && n + j < a.N; ++j) C[j] = v[j] + g.bias[n + j];
+      break;
+    }
+    default: {
+      float* C = static_cast<float*>(g.C) + off + (int64_t)split * a.split_stride;
+      if (full && (a.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
+        float4* d4 = reinterpret_cast<float4*>(C);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      } else {
+        for (int j = 0; j < 16 && n + j < a.N; ++j) C[j] = v[j];
+      }
+      break;
+    }
+  }
+}
+
+template <int BN, bool AMN, bool BMN>
+__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN;
+  constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const GemmArgs& a = p.a;
+  const int gz = blockIdx.z;
+  const int grp = gz / a.splits, split = gz % a.splits;
+  const GemmGroup& g = a.g[grp];
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= g.M) return;
+  const int k_begin = split * a.k_per_split;
+  const int k_end = min(a.K, k_begin + a.k_per_split);
+  const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.ta[grp]);
+    tma_prefetch(&p.tb[grp]);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        uint8_t* sA = smem + s * STAGE;
+        uint8_t* sB = sA + A_BYTES;
+        mbar_expect_tx(&full[s], STAGE);
+        const int k = k_begin + kb * BK;
+        if (!AMN) {
+          tma_load_2d(sA, &p.ta[grp], &full[s], k, m0);
+        } else {
+          tma_load_2d(sA, &p.ta[grp], &full[s], m0, k);
+          tma_load_2d(sA + 8192, &p.ta[grp], &full[s], m0 + 64, k);
+        }
+        if (!BMN) {
+          tma_load_2d(sB, &p.tb[grp], &full[s], k, n0);
+        } else {
+#pragma unroll
+          for (int i = 0; i < BN / 64; ++i) tma_load_2d(sB + i * 8192, &p.tb[grp], &full[s], n0 + 64 * i, k);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t sA = smem_u32(smem + s * STAGE);
+        const uint32_t sB = sA + A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t ad = AMN ? desc_mnmajor(sA, kk) : desc_kmajor(sA, kk);
+          const uint64_t bd = BMN ? desc_mnmajor(sB, kk) : desc_kmajor(sB, kk);
+          umma_bf16(tmem, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+      }
+      if (nkb > 0) umma_commit(tmem_full);  // accumulator complete
+    }
+  } else {
+    // ---------------- epilogue: TMEM lane quarter (warp % 4) holds rows q*32 .. q*32+31
+    const int q = warp & 3;
+    const int m = m0 + q * 32 + lane;
+    if (nkb > 0) {
+      mbar_wait(tmem_full, 0);
+      tc_fence_after();
+    }
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+    for (int c = 0; c < BN / 16; ++c) {
+      const int n = n0 + c * 16;
+      if (n >= a.N) break;  // warp-uniform
+      float v[16];
+      if (nkb > 0) {
+        tmem_ld16(trow + c * 16, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      }
+      if (m < g.M) epi16(a, g, split, m, n, v);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+bool get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+// 2-D bf16 tensor map: inner (contiguous) extent, outer extent, row pitch in elements, box.
+bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+              uint32_t box_outer) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool AMN, bool BMN>
+cudaError_t launch(const TcParams& p, int maxM, cudaStream_t st) {
+  constexpr int STAGE = A_BYTES + BN * BK * 2;
+  constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((unsigned)cdiv(p.a.N, BN), (unsigned)cdiv(maxM, BM), (unsigned)(p.a.n_groups * p.a.splits));
+  tc_gemm_kernel<BN, AMN, BMN><<<grid, NTHREADS, SMEM, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <bool AMN, bool BMN>
+cudaError_t launch_bn(const TcParams& p, int bn, int maxM, cudaStream_t st) {
+  switch (bn) {
+    case 16: if constexpr (!BMN) return launch<16, AMN, BMN>(p, maxM, st); break;
+    case 32: if constexpr (!BMN) return launch<32, AMN, BMN>(p, maxM, st); break;
+    case 64: return launch<64, AMN, BMN>(p, maxM, st);
+    case 128: return launch<128, AMN, BMN>(p, maxM, st);
+    default: return launch<256, AMN, BMN>(p, maxM, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int pick_bn(int N, bool bmn) {
+  if (N > 128) return 256;
+  if (N > 64) return 128;
+  if (N > 32 || bmn) return 64;
+  if (N > 16) return 32;
+  return 16;
+}
+
+}  // namespace
+
+bool tc_gemm_supported(const GemmArgs& a) {
+  if (a.N < 1 || a.K < 1 || a.n_groups < 1 || a.n_groups > 4) return false;
+  if ((a.lda & 7) || (a.ldb & 7)) return false;
+  if (a.splits > 1 && (a.k_per_split % BK)) return false;
+  if (a.a_mn && !a.b_mn) return false;  // layout combination not instantiated
+  for (int i = 0; i < a.n_groups; ++i) {
+    if ((reinterpret_cast<uintptr_t>(a.g[i].A) & 15) || (reinterpret_cast<uintptr_t>(a.g[i].B) & 15)) return false;
+  }
+  return get_encode();
+}
+
+cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st) {
+  TcParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.a = a;
+  const int bn = pick_bn(a.N, a.b_mn);
+  int maxM = 0;
+  for (int i = 0; i < a.n_groups; ++i) {
+    const GemmGroup& g = a.g[i];
+    maxM = g.M > maxM ? g.M : maxM;
+    if (g.M < 1) continue;
+    bool ok;
+    if (!a.a_mn) ok = make_map(&p.ta[i], g.A, a.K, g.M, a.lda, BK, BM);      // A [M x K]
+    else ok = make_map(&p.ta[i], g.A, g.M, a.K, a.lda, 64, BK);             // A stored [K x M]
+    if (ok) {
+      if (!a.b_mn) ok = make_map(&p.tb[i], g.B, a.K, a.N, a.ldb, BK, bn);    // B [N x K]
+      else ok = make_map(&p.tb[i], g.B, a.N, a.K, a.ldb, 64, BK);           // B stored [K x N]
+    }
+    if (!ok) return cudaErrorInvalidValue;
+  }
+  if (maxM == 0) return cudaSuccess;
+  if (!a.a_mn && !a.b_mn) return launch_bn<false, false>(p, bn, maxM, st);
+  if (!a.a_mn && a.b_mn) return launch_bn<false, true>(p, bn, maxM, st);
+  return launch_bn<true, true>(p, bn, maxM, st);
+}
+
 }  // namespace spz

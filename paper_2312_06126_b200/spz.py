@@ -32,6 +32,7 @@ EXPORTS = [
     "spz_replay_records", "spz_replay_destroy", "spz_config_default", "spz_nccl_unique_id", "spz_learner_create",
     "spz_update", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
+    "spz_diag_gemm_bf16",
 ]
 
 
@@ -114,6 +115,7 @@ def lib():
             "spz_learner_debug_buffer": (ctypes.c_int, [P, ctypes.c_char_p, P, I64, ctypes.POINTER(I64),
                                                         ctypes.POINTER(I32)]),
             "spz_learner_destroy": (None, [P]),
+            "spz_diag_gemm_bf16": (ctypes.c_int, [I32, I32, I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, I64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -261,6 +263,13 @@ def spz_learner_debug_buffer(learner, name):
 
 def spz_learner_destroy(learner):
     lib().spz_learner_destroy(learner)
+
+
+def spz_diag_gemm_bf16(M, N, K, A, lda, a_mn, B, ldb, b_mn, C, ldc, tensor_cores=True, splits=1, k_per_split=0,
+                       device=0):
+    """A, B: bf16 torch CUDA tensors; C: fp32 torch CUDA tensor (see include/spz.h)."""
+    _check(lib().spz_diag_gemm_bf16(device, 1 if tensor_cores else 0, M, N, K, _ptr(A), lda, a_mn, _ptr(B), ldb, b_mn,
+                                    _ptr(C), ldc, splits, k_per_split))
 
 
 # ----------------------------------------------------------------------------- RAII wrappers

@@ -1,0 +1,78 @@
+"""tcgen05 GEMM kernel unit tests: every operand layout, tile width and split-K path of the
+dense layers, against a float32 matmul of the same bf16 operands (test-only torch)."""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2312_06126_b200 import spz  # noqa: E402
+
+
+def _mk(rows, cols, ld, gen):
+    x = torch.zeros(rows, ld, dtype=torch.bfloat16, device="cuda")
+    x[:, :cols] = torch.randn(rows, cols, generator=gen, device="cuda").to(torch.bfloat16)
+    return x
+
+
+def _ref(A, a_mn, B, b_mn, M, N, K):
+    Af = A.float()
+    Bf = B.float()
+    Am = Af[:K, :M].t() if a_mn else Af[:M, :K]
+    Bm = Bf[:K, :N] if b_mn else Bf[:N, :K].t()
+    return Am @ Bm
+
+
+CASES = [
+    # (M, N, K, a_mn, b_mn)  -- forward (K-major x K-major)
+    (16384, 256, 256, 0, 0), (1000, 256, 22, 0, 0), (300, 12, 256, 0, 0), (257, 512, 64, 0, 0), (130, 33, 100, 0, 0),
+    (128, 1, 256, 0, 0), (4096, 1024, 1024, 0, 0),
+    # dgrad (K-major x MN-major)
+    (16384, 256, 256, 0, 1), (1000, 28, 256, 0, 1), (777, 256, 12, 0, 1), (200, 300, 96, 0, 1),
+    # wgrad (MN-major x MN-major): M = out features, N = in features, K = batch
+    (256, 256, 8192, 1, 1), (256, 28, 1000, 1, 1), (12, 256, 1000, 1, 1), (512, 44, 333, 1, 1),
+]
+
+
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", CASES)
+def test_tc_gemm_matches_fp32_matmul(M, N, K, a_mn, b_mn):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
+    lda = ((M if a_mn else K) + 7) // 8 * 8
+    ldb = ((N if b_mn else K) + 7) // 8 * 8
+    A = _mk(K, M, lda, g) if a_mn else _mk(M, K, lda, g)
+    B = _mk(K, N, ldb, g) if b_mn else _mk(N, K, ldb, g)
+    ldc = N
+    C = torch.full((M, ldc), float("nan"), device="cuda")
+    spz.spz_diag_gemm_bf16(M, N, K, A, lda, a_mn, B, ldb, b_mn, C, ldc)
+    ref = _ref(A, a_mn, B, b_mn, M, N, K)
+    err = (C - ref).abs().max().item() / max(ref.abs().max().item(), 1e-6)
+    assert err < 2e-6 * K ** 0.5, err  # same bf16 products, fp32 accumulation: only summation order differs
+
+
+@pytest.mark.parametrize("K,splits,kps", [(8192, 32, 256), (1000, 3, 384), (65536, 8, 8192)])
+def test_tc_gemm_split_k_partials(K, splits, kps):
+    M, N = 256, 256
+    g = torch.Generator(device="cuda").manual_seed(K)
+    A = _mk(K, M, M, g)
+    B = _mk(K, N, N, g)
+    C = torch.full((splits, M, N), float("nan"), device="cuda")
+    spz.spz_diag_gemm_bf16(M, N, K, A, M, 1, B, N, 1, C, N, splits=splits, k_per_split=kps)
+    ref = _ref(A, 1, B, 1, M, N, K)
+    err = (C.sum(0) - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 2e-6 * K ** 0.5
+    for s in range(splits):
+        lo, hi = s * kps, min(K, (s + 1) * kps)
+        part = _ref(A[lo:hi] if lo < K else A[:0], 1, B[lo:hi] if lo < K else B[:0], 1, M, N, max(hi - lo, 0)) if hi > lo else torch.zeros(M, N, device="cuda")
+        assert (C[s] - part).abs().max().item() <= 2e-6 * K ** 0.5 * max(ref.abs().max().item(), 1.0)
+
+
+def test_simt_and_tc_agree():
+    M, N, K = 1000, 256, 256
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = _mk(M, K, K, g)
+    B = _mk(N, K, K, g)
+    C1 = torch.empty(M, N, device="cuda")
+    C2 = torch.empty(M, N, device="cuda")
+    spz.spz_diag_gemm_bf16(M, N, K, A, K, 0, B, K, 0, C1, N, tensor_cores=True)
+    spz.spz_diag_gemm_bf16(M, N, K, A, K, 0, B, K, 0, C2, N, tensor_cores=False)
+    assert (C1 - C2).abs().max().item() < 1e-4 * C2.abs().max().item()

@@ -55,16 +55,17 @@ spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, i
   spz::GemmArgs a{};
   a.N = (int)N;
   a.K = (int)K;
-  a.lda = (int)lda;
-  a.ldb = (int)ldb;
-  a.ldc = (int)ldc;
   a.a_mn = a_mn;
   a.b_mn = b_mn;
   a.epi = spz::EPI_F32;
   a.splits = splits;
   a.k_per_split = splits > 1 ? (int)k_per_split : (int)K;
-  a.split_stride = M * ldc;
   a.n_groups = 1;
+  a.g[0].lda = (int)lda;
+  a.g[0].ldb = (int)ldb;
+  a.g[0].ldc = (int)ldc;
+  a.g[0].N = (int)N;
+  a.g[0].split_stride = M * ldc;
   a.g[0].A = A;
   a.g[0].B = B;
   a.g[0].C = C;

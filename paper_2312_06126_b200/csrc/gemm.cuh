@@ -1,27 +1,30 @@
 // gemm.cuh -- the GEMM contract used by every dense layer of the update.
 //
-// C[m, n] = epi( sum_k A(m, k) * B(n, k) ),  m < M (per group), n < N, k < K.
+// For each group g:  C[m, n] = epi( sum_k A(m, k) * B(n, k) ),  m < g.M, n < g.N, k < K.
 //   A K-major : A(m,k) = A[m * lda + k]    (activations, row = batch row)
 //   A MN-major: A(m,k) = A[k * lda + m]    (wgrad: dZ stored [batch x out])
 //   B K-major : B(n,k) = B[n * ldb + k]    (forward: W stored [out x in])
 //   B MN-major: B(n,k) = B[k * ldb + n]    (dgrad: W stored [out x in], contraction over out;
 //                                            wgrad: activations stored [batch x in])
 // Split-K (wgrad, contraction over the batch) writes split s's partial sum to
-// C + s * split_stride; the fused Adam kernel sums splits in a fixed order, so
-// the result is deterministic (reading #16).
-// Up to 4 groups (e.g. the twin critics) share N, K, strides and epilogue
-// kind but have their own pointers and M.
+// C + s * split_stride; the fused Adam kernel sums splits in a fixed order, so the
+// result is deterministic (reading #16).
+// Up to 4 groups per launch (twin critics, online + target critics, all wgrads of a
+// network) share K, operand majorness and the epilogue kind; pointers, M, N and row
+// pitches are per group.  The grid covers the largest group; other CTAs exit early.
 #pragma once
 
-#include "common.cuh"
+#include "heads.cuh"
 
 namespace spz {
 
 enum EpiKind : int {
-  EPI_BIAS_RELU = 0,  // C (T) = relu(acc + bias[n])                -- hidden layer forward
-  EPI_BIAS_F32 = 1,   // C (f32) = acc + bias[n]                    -- linear head forward
-  EPI_MASK = 2,       // C (T) = acc * (aux[m, n] > 0)              -- dgrad through ReLU
-  EPI_F32 = 3,        // C (f32) = acc                              -- wgrad partials / input dgrad
+  EPI_BIAS_RELU = 0,  // C (T) = relu(acc + bias[n]); optional fused row dot -> dot_out  -- hidden layer forward
+  EPI_BIAS_F32 = 1,   // C (f32) = acc + bias[n]                                           -- linear head forward
+  EPI_MASK = 2,       // C (T) = acc * (aux[m, n] > 0)                                     -- dgrad through ReLU
+  EPI_F32 = 3,        // C (f32) = acc                                                     -- wgrad partials / input dgrad
+  EPI_SAC_HEAD = 4,   // acc + bias -> squashed-Gaussian head (heads.cuh), nothing stored in C
+  EPI_TD3_HEAD = 5,   // acc + bias -> tanh head with target smoothing (heads.cuh)
 };
 
 struct GemmGroup {
@@ -30,26 +33,31 @@ struct GemmGroup {
   void* C;
   const float* bias;
   const void* aux;
-  int M;
+  const float* dot_w;  // EPI_BIAS_RELU: if set, dot_out[m] = sum_n relu(z[m, n]) dot_w[n] + dot_b[0]
+  const float* dot_b;
+  float* dot_out;
+  int64_t split_stride;  // elements between split partials in C
+  int M, N;
+  int lda, ldb, ldc, ldaux;
+  int row0;  // head epilogues: local actor-pass row of this group's row 0
   int pad_;
 };
 
 struct GemmArgs {
-  int N, K;
-  int lda, ldb, ldc, ldaux;
+  int N, K;  // N: max over groups (grid width)
   int a_mn, b_mn;  // 0 = K-major, 1 = MN-major
   int epi;
-  int splits;          // split-K count (>= 1)
-  int k_per_split;     // contraction rows per split (multiple of the K tile)
-  int64_t split_stride;  // elements between split partials in C
+  int splits;       // split-K count (>= 1)
+  int k_per_split;  // contraction rows per split (multiple of the K tile)
   int n_groups;
   GemmGroup g[4];
+  HeadEpi head;
 };
 
-// Apply the epilogue to one accumulator element (shared by every GEMM backend).
+// Apply the epilogue to one accumulator element (SIMT backend; no fused heads / dots).
 template <typename T>
 __device__ __forceinline__ void epi_store(const GemmArgs& a, const GemmGroup& g, int split, int m, int n, float acc) {
-  const int64_t off = (int64_t)m * a.ldc + n;
+  const int64_t off = (int64_t)m * g.ldc + n;
   switch (a.epi) {
     case EPI_BIAS_RELU: {
       const float z = acc + g.bias[n];
@@ -60,12 +68,12 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, const GemmGroup& g,
       static_cast<float*>(g.C)[off] = acc + g.bias[n];
       break;
     case EPI_MASK: {
-      const float msk = to_f(static_cast<const T*>(g.aux)[(int64_t)m * a.ldaux + n]);
+      const float msk = to_f(static_cast<const T*>(g.aux)[(int64_t)m * g.ldaux + n]);
       static_cast<T*>(g.C)[off] = from_f<T>(msk > 0.f ? acc : 0.f);
       break;
     }
     default:
-      static_cast<float*>(g.C)[off + (int64_t)split * a.split_stride] = acc;
+      static_cast<float*>(g.C)[off + (int64_t)split * g.split_stride] = acc;
       break;
   }
 }

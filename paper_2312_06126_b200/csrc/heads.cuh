@@ -1,0 +1,83 @@
+// heads.cuh -- per-row math of the actor heads, shared by the standalone
+// head kernels and the fused tcgen05 GEMM epilogues.
+#pragma once
+
+#include "common.cuh"
+
+namespace spz {
+
+constexpr float LN2F = 0.69314718055994530942f;
+constexpr float HALF_LN_2PI_F = 0.91893853320467274178f;
+
+__device__ __forceinline__ float softplusf(float x) { return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))); }
+
+// Everything a head epilogue writes, for local rows r in [0, 2 Bl) of the actor pass:
+// r < Bl is the s2-row j = r, r >= Bl is the s-row j = r - Bl.
+struct HeadEpi {
+  int m, o, Bl, ldx;   // action dim, obs dim, local batch, critic-input row pitch
+  int64_t row0;        // global row id of local row 0 (row sharding)
+  uint64_t seed;
+  const int64_t* step_p;
+  float lo, hi;        // log-sigma clamp (SAC)
+  float noise, clipc;  // target smoothing (TD3)
+  void* Xc;            // critic inputs [3 Bl x ldx]: a~ -> rows Bl.., a' -> rows 2 Bl..
+  float *u, *a, *eps, *sig, *l;  // s-row cache [Bl x m] (TD3 uses a only)
+  float *logp, *logp2;
+};
+
+// SAC: [mu | l] -> lc = clamp(l), sigma = exp(lc), u = mu + sigma eps, a = tanh u,
+// log pi = sum_i [-eps^2/2 - lc - ln(2 pi)/2 - 2 (ln 2 - u - softplus(-2u))].
+template <typename T>
+__device__ __forceinline__ void sac_head_row(const HeadEpi& h, int r, const float* mu, const float* lraw) {
+  const bool s2row = r < h.Bl;
+  const int j = s2row ? r : r - h.Bl;
+  const uint64_t step = (uint64_t)*h.step_p;
+  const uint32_t stream = s2row ? S_EPS2 : S_EPS;
+  T* xa = static_cast<T*>(h.Xc) + (int64_t)(s2row ? 2 * h.Bl + j : h.Bl + j) * h.ldx + h.o;
+  float lp = 0.f;
+  for (int i = 0; i < h.m; ++i) {
+    const float l = lraw[i];
+    const float lc = fminf(fmaxf(l, h.lo), h.hi);
+    const float sg = expf(lc);
+    const float e = normal_q(h.seed, step, stream, (uint64_t)(h.row0 + j), i);
+    const float u = fmaf(sg, e, mu[i]);
+    const float a = tanhf(u);
+    lp += -0.5f * e * e - lc - HALF_LN_2PI_F - 2.f * (LN2F - u - softplusf(-2.f * u));
+    xa[i] = from_f<T>(a);
+    if (!s2row) {
+      const int64_t ci = (int64_t)j * h.m + i;
+      h.u[ci] = u;
+      h.a[ci] = a;
+      h.eps[ci] = e;
+      h.sig[ci] = sg;
+      h.l[ci] = l;
+    }
+  }
+  if (s2row) h.logp2[j] = lp;
+  else h.logp[j] = lp;
+}
+
+// TD3: rows r < Bl (target actor on s2): a' = clip(tanh z + clip(noise n, -c, c), -1, 1), n from
+// S_SMOOTH; rows r >= Bl (online actor on s): a~ = tanh z (cached for the backward).
+template <typename T>
+__device__ __forceinline__ void td3_head_row(const HeadEpi& h, int r, const float* z) {
+  const uint64_t step = (uint64_t)*h.step_p;
+  if (r < h.Bl) {
+    T* xa = static_cast<T*>(h.Xc) + (int64_t)(2 * h.Bl + r) * h.ldx + h.o;
+    for (int i = 0; i < h.m; ++i) {
+      const float n = normal_q(h.seed, step, S_SMOOTH, (uint64_t)(h.row0 + r), i);
+      const float xi = fminf(fmaxf(h.noise * n, -h.clipc), h.clipc);
+      xa[i] = from_f<T>(fminf(fmaxf(tanhf(z[i]) + xi, -1.f), 1.f));
+    }
+  } else {
+    const int j = r - h.Bl;
+    T* xa = static_cast<T*>(h.Xc) + (int64_t)(h.Bl + j) * h.ldx + h.o;
+    for (int i = 0; i < h.m; ++i) {
+      const float a = tanhf(z[i]);
+      xa[i] = from_f<T>(a);
+      h.a[(int64_t)j * h.m + i] = a;
+    }
+  }
+}
+
+}  // namespace spz

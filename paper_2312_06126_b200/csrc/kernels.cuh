@@ -5,15 +5,14 @@
 // an update is bit-reproducible run to run on a given device count (reading #16).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
+#include "heads.cuh"
 
 namespace spz {
 
 constexpr int NSTAT = 6;  // per-block partial sums: (q1-y)^2+(q2-y)^2, q1, q2, alpha logp - minQ~ (or -Q1~), logp, spare
-constexpr float LN2F = 0.69314718055994530942f;
-constexpr float HALF_LN_2PI_F = 0.91893853320467274178f;
-
-__device__ __forceinline__ float softplusf(float x) { return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x))); }
 
 // ------------------------------------------------------------------ a1 + a2: index + gather
 // Block = 32 rows.  Records are read with 128-bit loads into shared memory; each
@@ -31,6 +30,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ r
                                                      T* __restrict__ Xa, int lda, T* __restrict__ Xc, int ldc,
                                                      float* __restrict__ r, float* __restrict__ d,
                                                      int32_t* __restrict__ idx_out) {
+  pdl_wait();
+  pdl_launch();
   extern __shared__ float4 sm4[];
   const float* sm = reinterpret_cast<const float*>(sm4);
   __shared__ int64_t sidx[GATHER_ROWS];
@@ -82,38 +83,17 @@ struct HeadCache {
 };
 
 template <typename T>
-__global__ void sac_head_fwd_kernel(const float* __restrict__ H, int ldh, int m, int Bl, int64_t row0, uint64_t seed,
-                                    const int64_t* __restrict__ step_p, float lo, float hi, T* __restrict__ Xc, int ldc,
-                                    int o, HeadCache cache, float* __restrict__ logp2, float* __restrict__ logp) {
+__global__ void sac_head_fwd_kernel(const float* __restrict__ H, int ldh, HeadEpi h, int M) {
+  pdl_wait();
+  pdl_launch();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= 2 * Bl) return;
-  const bool s2row = r < Bl;
-  const int j = s2row ? r : r - Bl;
-  const uint64_t step = (uint64_t)*step_p;
-  const uint32_t stream = s2row ? S_EPS2 : S_EPS;
-  T* xa = Xc + (int64_t)(s2row ? 2 * Bl + j : Bl + j) * ldc + o;
-  float lp = 0.f;
-  for (int i = 0; i < m; ++i) {
-    const float mu = H[(int64_t)r * ldh + i];
-    const float l = H[(int64_t)r * ldh + m + i];
-    const float lc = fminf(fmaxf(l, lo), hi);
-    const float sg = expf(lc);
-    const float e = normal_q(seed, step, stream, (uint64_t)(row0 + j), i);
-    const float u = fmaf(sg, e, mu);
-    const float a = tanhf(u);
-    lp += -0.5f * e * e - lc - HALF_LN_2PI_F - 2.f * (LN2F - u - softplusf(-2.f * u));
-    xa[i] = from_f<T>(a);
-    if (!s2row) {
-      const int64_t ci = (int64_t)j * m + i;
-      cache.u[ci] = u;
-      cache.a[ci] = a;
-      cache.eps[ci] = e;
-      cache.sig[ci] = sg;
-      cache.l[ci] = l;
-    }
+  if (r >= M) return;
+  float mu[32], l[32];
+  for (int i = 0; i < h.m; ++i) {
+    mu[i] = H[(int64_t)r * ldh + i];
+    l[i] = H[(int64_t)r * ldh + h.m + i];
   }
-  if (s2row) logp2[j] = lp;
-  else logp[j] = lp;
+  sac_head_row<T>(h, r, mu, l);
 }
 
 // ------------------------------------------------------------------ a3: TD3 actor heads (forward)
@@ -121,35 +101,22 @@ __global__ void sac_head_fwd_kernel(const float* __restrict__ H, int ldh, int m,
 // S_SMOOTH (written into Xc[2Bl + r]); rows Bl <= r < M: online actor on s, a~ = tanh(z)
 // (written into Xc[r], cached for the backward).  P:576, reading #18.
 template <typename T>
-__global__ void td3_head_fwd_kernel(const float* __restrict__ H, int ldh, int m, int Bl, int M, int64_t row0,
-                                    uint64_t seed, const int64_t* __restrict__ step_p, float noise, float clipc,
-                                    T* __restrict__ Xc, int ldc, int o, float* __restrict__ a_cache) {
+__global__ void td3_head_fwd_kernel(const float* __restrict__ H, int ldh, HeadEpi h, int M) {
+  pdl_wait();
+  pdl_launch();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= M) return;
-  const uint64_t step = (uint64_t)*step_p;
-  if (r < Bl) {
-    T* xa = Xc + (int64_t)(2 * Bl + r) * ldc + o;
-    for (int i = 0; i < m; ++i) {
-      const float n = normal_q(seed, step, S_SMOOTH, (uint64_t)(row0 + r), i);
-      const float xi = fminf(fmaxf(noise * n, -clipc), clipc);
-      const float a = fminf(fmaxf(tanhf(H[(int64_t)r * ldh + i]) + xi, -1.f), 1.f);
-      xa[i] = from_f<T>(a);
-    }
-  } else {
-    const int j = r - Bl;
-    T* xa = Xc + (int64_t)(Bl + j) * ldc + o;
-    for (int i = 0; i < m; ++i) {
-      const float a = tanhf(H[(int64_t)r * ldh + i]);
-      xa[i] = from_f<T>(a);
-      a_cache[(int64_t)j * m + i] = a;
-    }
-  }
+  float z[32];
+  for (int i = 0; i < h.m; ++i) z[i] = H[(int64_t)r * ldh + i];
+  td3_head_row<T>(h, r, z);
 }
 
 // TD3 actor head backward: dZ_out = g_a (1 - a~^2) with g_a the Q1 input gradient's action columns.
 template <typename T>
 __global__ void td3_head_bwd_kernel(const float* __restrict__ dX1, int ldx, int o, int m, int Bl,
                                     const float* __restrict__ a_cache, T* __restrict__ dH, int ldh) {
+  pdl_wait();
+  pdl_launch();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)Bl * m) return;
   const int64_t j = e / m;
@@ -173,12 +140,28 @@ struct RowdotArgs {
 
 template <typename T>
 __global__ void __launch_bounds__(256) rowdot_kernel(const __grid_constant__ RowdotArgs a) {
+  pdl_wait();
+  pdl_launch();
   const RowdotGroup& g = a.g[blockIdx.y];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= a.M) return;
   const T* row = static_cast<const T*>(g.A) + (int64_t)warp * a.ld;
   float s = 0.f;
-  for (int n = lane; n < a.h; n += 32) s = fmaf(to_f(row[n]), g.w[n], s);
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    // h % 8 == 0: each lane takes 8 adjacent columns per pass (16-byte loads)
+    for (int n = lane * 8; n < a.h; n += 256) {
+      const uint4 u = *reinterpret_cast<const uint4*>(row + n);
+      const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(x[i]);
+        s = fmaf(f.x, g.w[n + 2 * i], s);
+        s = fmaf(f.y, g.w[n + 2 * i + 1], s);
+      }
+    }
+  } else {
+    for (int n = lane; n < a.h; n += 32) s = fmaf(to_f(row[n]), g.w[n], s);
+  }
   s = warp_sum(s);
   if (lane == 0) g.q[warp] = s + g.b[0];
 }
@@ -214,6 +197,8 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(
     const float* __restrict__ r, const float* __restrict__ d, const float* __restrict__ log_alpha, float gamma,
     float invB, int Bl, int td3, const int64_t* __restrict__ step_p, int delay, float* __restrict__ gq1,
     float* __restrict__ gq2, float* __restrict__ y_out, double* __restrict__ partials) {
+  pdl_wait();
+  pdl_launch();
   const int j = blockIdx.x * LOSS_NT + threadIdx.x;
   double v[NSTAT] = {0, 0, 0, 0, 0, 0};
   if (j < Bl) {
@@ -261,15 +246,35 @@ struct HeadBwdArgs {
 
 template <typename T>
 __global__ void critic_head_bwd_kernel(const __grid_constant__ HeadBwdArgs a) {
+  pdl_wait();
+  pdl_launch();
   const HeadBwdGroup& g = a.g[blockIdx.y];
   const T* A = static_cast<const T*>(g.A);
   T* dZ = static_cast<T*>(g.dZ);
-  const int64_t total = a.M * a.h;
+  const int hv = a.h / 8;  // 8-wide chunks per row (h % 8 == 0, ld % 8 == 0)
+  const int64_t total = a.M * hv;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rr = e / a.h;
-    const int n = (int)(e - rr * a.h);
-    const float act = to_f(A[rr * a.ld + n]);
-    dZ[rr * a.ld + n] = from_f<T>(act > 0.f ? g.gq[rr] * g.w[n] : 0.f);
+    const int64_t rr = e / hv;
+    const int n = (int)(e - rr * hv) * 8;
+    const float gq = g.gq[rr];
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+      const uint4 u = *reinterpret_cast<const uint4*>(A + rr * a.ld + n);
+      const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&u);
+      uint4 o;
+      __nv_bfloat162* y = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(x[i]);
+        y[i] = __floats2bfloat162_rn(f.x > 0.f ? gq * g.w[n + 2 * i] : 0.f, f.y > 0.f ? gq * g.w[n + 2 * i + 1] : 0.f);
+      }
+      *reinterpret_cast<uint4*>(dZ + rr * a.ld + n) = o;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float act = to_f(A[rr * a.ld + n + i]);
+        dZ[rr * a.ld + n + i] = from_f<T>(act > 0.f ? gq * g.w[n + i] : 0.f);
+      }
+    }
   }
 }
 
@@ -280,6 +285,8 @@ template <typename T>
 __global__ void sac_head_bwd_kernel(const float* __restrict__ dX1, const float* __restrict__ dX2, int ldx, int o, int m,
                                     int Bl, HeadCache cache, const float* __restrict__ log_alpha, float invB, float lo,
                                     float hi, T* __restrict__ dH, int ldh) {
+  pdl_wait();
+  pdl_launch();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)Bl * m) return;
   const int64_t j = e / m;
@@ -295,31 +302,71 @@ __global__ void sac_head_bwd_kernel(const float* __restrict__ dX1, const float* 
 }
 
 // ------------------------------------------------------------------ bias / head-weight gradients: column sums
-// partial[s][n] = sum_{r in rows of split s} w[r] X[r, n]  (w nullable), fixed order.
-constexpr int CS_COLS = 32, CS_ROWS = 8;
+// One launch covers several tensors (jobs).  Block (split s, job j) sums rows
+// [s*rps, (s+1)*rps) of X (optionally weighted by w[r]) for every column and writes
+// partial[s][n]; the fused Adam kernel adds the splits in a fixed order.  Threads own 8
+// adjacent columns (one 16-byte load per row for bf16 rows) x 8 row lanes.
+struct ColsumJob {
+  const void* X;
+  const float* w;
+  float* out;
+  int ld, N, M, f32;
+};
+struct ColsumArgs {
+  int n_jobs, rps;
+  ColsumJob j[12];
+};
+constexpr int CS_VEC = 8, CS_TX = 32, CS_TY = 8;
 
 template <typename T>
-__global__ void __launch_bounds__(CS_COLS* CS_ROWS) colsum_kernel(const T* __restrict__ X, int ld, int N, int M,
-                                                                  int rows_per_split, const float* __restrict__ w,
-                                                                  float* __restrict__ partial) {
-  __shared__ float red[CS_ROWS][CS_COLS];
-  const int tc = threadIdx.x % CS_COLS, tr = threadIdx.x / CS_COLS;
-  const int n = blockIdx.x * CS_COLS + tc;
-  const int s = blockIdx.y;
-  const int r0 = s * rows_per_split, r1 = min(M, r0 + rows_per_split);
-  float acc = 0.f;
-  if (n < N)
-    for (int rr = r0 + tr; rr < r1; rr += CS_ROWS) {
-      const float x = to_f(X[(int64_t)rr * ld + n]);
-      acc = w ? fmaf(w[rr], x, acc) : acc + x;
-    }
-  red[tr][tc] = acc;
-  __syncthreads();
-  if (tr == 0 && n < N) {
-    float t = 0.f;
+__device__ __forceinline__ void load8(const T* row, int n, int N, int ld_aligned, float (&v)[CS_VEC]) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (ld_aligned && n + CS_VEC <= N) {
+      const uint4 u = *reinterpret_cast<const uint4*>(row + n);
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
-    for (int k = 0; k < CS_ROWS; ++k) t += red[k][tc];
-    partial[(int64_t)s * N + n] = t;
+      for (int i = 0; i < CS_VEC; ++i) v[i] = __bfloat162float(b[i]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < CS_VEC; ++i) v[i] = n + i < N ? to_f(row[n + i]) : 0.f;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CS_TX* CS_TY) colsum_multi_kernel(const __grid_constant__ ColsumArgs a) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ float red[CS_TY][CS_TX * CS_VEC + 1];
+  const ColsumJob& jb = a.j[blockIdx.y];
+  const int s = blockIdx.x;
+  const int r0 = s * a.rps, r1 = min(jb.M, r0 + a.rps);
+  const int tx = threadIdx.x % CS_TX, ty = threadIdx.x / CS_TX;
+  for (int c0 = 0; c0 < jb.N; c0 += CS_TX * CS_VEC) {
+    const int n = c0 + tx * CS_VEC;
+    float acc[CS_VEC] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (n < jb.N) {
+      for (int r = r0 + ty; r < r1; r += CS_TY) {
+        float v[CS_VEC];
+        if (jb.f32) load8<float>(static_cast<const float*>(jb.X) + (int64_t)r * jb.ld, n, jb.N, 0, v);
+        else load8<T>(static_cast<const T*>(jb.X) + (int64_t)r * jb.ld, n, jb.N, (jb.ld & 7) == 0, v);
+        const float wr = jb.w ? jb.w[r] : 1.f;
+#pragma unroll
+        for (int i = 0; i < CS_VEC; ++i) acc[i] = fmaf(wr, v[i], acc[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CS_VEC; ++i) red[ty][tx * CS_VEC + i] = acc[i];
+    __syncthreads();
+    for (int c = threadIdx.x; c < CS_TX * CS_VEC; c += blockDim.x) {
+      if (c0 + c < jb.N) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < CS_TY; ++k) t += red[k][c];
+        jb.out[(int64_t)s * jb.N + c0 + c] = t;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -334,6 +381,8 @@ __global__ void stats_kernel(const double* __restrict__ partials, int nblocks, c
                              const float* __restrict__ log_alpha, double target_entropy, double B, int td3,
                              const int64_t* __restrict__ step_p, int delay, StatsOut* __restrict__ out,
                              float* __restrict__ g_log_alpha, int* __restrict__ flag) {
+  pdl_wait();
+  pdl_launch();
   __shared__ double tot[NSTAT];
   if (threadIdx.x < NSTAT) {
     double s = 0.0;
@@ -366,7 +415,7 @@ __global__ void stats_kernel(const double* __restrict__ partials, int nblocks, c
 // g = sum_s partial[s] (fixed order); Adam with the optimizer's own t; master,
 // m, v updated; operand shadow (T, padded row stride) refreshed; if the tensor
 // has a target: theta' = tau theta_new + (1 - tau) theta' (+ its shadow).
-constexpr int ADAM_SEG = 4096;
+constexpr int ADAM_SEG = 1024;
 
 struct AdamTensor {
   int64_t p_off;      // master offset of element 0
@@ -398,6 +447,8 @@ __global__ void __launch_bounds__(256) adam_polyak_kernel(const AdamTensor* __re
                                                           float* __restrict__ Vo, T* __restrict__ S,
                                                           const int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
                                                           int* __restrict__ flag) {
+  pdl_wait();
+  pdl_launch();
   if (*flag) return;  // halted: parameters stay at the state before the failing step
   const AdamSegment sg = segs[blockIdx.x];
   const AdamTensor tn = tensors[sg.tensor];
@@ -413,7 +464,8 @@ __global__ void __launch_bounds__(256) adam_polyak_kernel(const AdamTensor* __re
   for (int k = threadIdx.x; k < sg.count; k += blockDim.x) {
     const int64_t i = sg.start + k;
     float g = 0.f;
-    for (int s = 0; s < tn.n_partials; ++s) g += tn.partials[(int64_t)s * tn.numel + i];
+#pragma unroll 8
+    for (int s = 0; s < tn.n_partials; ++s) g += __ldg(tn.partials + (int64_t)s * tn.numel + i);
     if (!isfinite(g)) {
       atomicExch(flag, 2);
       continue;
@@ -446,6 +498,8 @@ __global__ void __launch_bounds__(256) adam_polyak_kernel(const AdamTensor* __re
 // Advance the step and optimizer counters (after every kernel of the step has run).
 __global__ void advance_kernel(int64_t* __restrict__ counters, const int* __restrict__ flag, int td3, int delay,
                                int alpha_auto, int critic_on, int actor_on) {
+  pdl_wait();
+  pdl_launch();
   if (*flag) return;
   const int64_t step = counters[0];
   const bool delayed = !td3 || ((step + 1) % delay) == 0;

@@ -155,7 +155,7 @@ static int wgrad_splits(int64_t Bl) {
   return s;
 }
 static int64_t wgrad_rows(int64_t Bl, int s) { return round_up(cdiv(Bl, s), 128); }
-static int bias_splits(int64_t Bl) { return (int)std::max<int64_t>(1, std::min<int64_t>(64, cdiv(Bl, 512))); }
+static int bias_splits(int64_t Bl) { return (int)std::max<int64_t>(1, std::min<int64_t>(128, cdiv(Bl, 128))); }
 
 // Gradient partial regions (one per trained tensor), laid out at create time for the
 // largest split counts.
@@ -258,18 +258,56 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     auto gemm = [&](const char* cls, GemmArgs a) {
       ops.push_back({cls, [a](cudaStream_t st) { return run_gemm<T>(a, st); }});
     };
-    auto fwd_args = [&](int N, int K, int ldA, int ldB, int ldC, int epi) {
+    auto mk = [&](int K, int epi, int amn, int bmn) {
       GemmArgs a{};
-      a.N = N;
       a.K = K;
-      a.lda = ldA;
-      a.ldb = ldB;
-      a.ldc = ldC;
       a.epi = epi;
+      a.a_mn = amn;
+      a.b_mn = bmn;
       a.splits = 1;
       a.k_per_split = K;
       return a;
     };
+    auto add = [&](GemmArgs& a, const void* A, int ldA, const void* Bm, int ldB, void* C, int ldC, int M, int N,
+                   const float* bias = nullptr, const void* aux = nullptr, int ldAux = 0) -> GemmGroup& {
+      GemmGroup& g = a.g[a.n_groups++];
+      g = GemmGroup{};
+      g.A = A;
+      g.lda = ldA;
+      g.B = Bm;
+      g.ldb = ldB;
+      g.C = C;
+      g.ldc = ldC;
+      g.M = M;
+      g.N = N;
+      g.bias = bias;
+      g.aux = aux;
+      g.ldaux = ldAux;
+      a.N = std::max(a.N, N);
+      return g;
+    };
+    // fused epilogues (row dot, actor heads) exist only in the tcgen05 kernel
+    auto tc_ok = [&](const GemmArgs& a) { return std::is_same<T, __nv_bfloat16>::value && tc_gemm_supported(a); };
+    HeadEpi he{};
+    he.m = m;
+    he.o = o;
+    he.Bl = Bl;
+    he.ldx = ldc;
+    he.row0 = row0;
+    he.seed = seed;
+    he.step_p = Lr->counters;
+    he.lo = lo;
+    he.hi = hi;
+    he.noise = (float)Lr->cfg.td3_noise;
+    he.clipc = (float)Lr->cfg.td3_noise_clip;
+    he.Xc = Lr->Xc;
+    he.u = Lr->cache.u;
+    he.a = Lr->cache.a;
+    he.eps = Lr->cache.eps;
+    he.sig = Lr->cache.sig;
+    he.l = Lr->cache.l;
+    he.logp = Lr->logp;
+    he.logp2 = Lr->logp2;
 
     // ---- a1 + a2: Philox indices + gather
     {
@@ -282,13 +320,14 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       int32_t* idx = Lr->idx;
       const size_t smem = (size_t)GATHER_ROWS * R * sizeof(float);
       ops.push_back({"gather", [=](cudaStream_t st) {
-                       gather_kernel<T><<<(unsigned)cdiv(Bl, GATHER_ROWS), 256, smem, st>>>(
+                       launch_pdl(gather_kernel<T>, dim3((unsigned)cdiv(Bl, GATHER_ROWS)), dim3(256), smem, st, 
                            rec, R, o, m, fill, seed, stp, row0, Bl, Xa, lda, Xc, ldc, rr, dd, idx);
                        return cudaGetLastError();
                      }});
     }
     // ---- a3: actor forward.  SAC: online actor on [s2; s] (M = 2Bl).
-    //      TD3: target actor on s2 (rows 0..Bl) every step, online actor on s on delayed steps.
+    //      TD3: target actor on s2 (rows 0..Bl) every step, online actor on s on delayed steps
+    //      (two groups of one launch per layer).
     {
       const NetLayout& an = Lr->net[NET_ACTOR];
       struct Pass { int id; int64_t row; int M; };
@@ -298,77 +337,84 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         passes.push_back({NET_ACTORT, 0, Bl});
         if (actor_step) passes.push_back({NET_ACTOR, Bl, Bl});
       }
-      for (const Pass& ps : passes) {
-        for (int l = 0; l < an.nl; ++l) {
-          const bool last = l == an.nl - 1;
-          GemmArgs a = fwd_args(an.out[l], an.in[l], l == 0 ? lda : h, ldw(ps.id, l), last ? ldh : h,
-                                last ? EPI_BIAS_F32 : EPI_BIAS_RELU);
-          a.n_groups = 1;
-          a.g[0].A = l == 0 ? (const void*)Ta(Lr->Xa, ps.row, lda) : (const void*)Ta(Lr->Aact[l - 1], ps.row, h);
-          a.g[0].B = Wp(ps.id, l);
-          a.g[0].C = last ? (void*)(Lr->H + ps.row * ldh) : (void*)Ta(Lr->Aact[l], ps.row, h);
-          a.g[0].bias = bp(ps.id, l);
-          a.g[0].M = ps.M;
-          gemm(last ? "actor_head_gemm" : "actor_fwd_gemm", a);
-        }
+      for (int l = 0; l < L; ++l) {
+        GemmArgs a = mk(an.in[l], EPI_BIAS_RELU, 0, 0);
+        for (const Pass& ps : passes)
+          add(a, l == 0 ? (const void*)Ta(Lr->Xa, ps.row, lda) : (const void*)Ta(Lr->Aact[l - 1], ps.row, h),
+              l == 0 ? lda : h, Wp(ps.id, l), ldw(ps.id, l), Ta(Lr->Aact[l], ps.row, h), h, ps.M, h, bp(ps.id, l));
+        gemm("actor_fwd_gemm", a);
       }
-      float* Hh = Lr->H;
-      T* Xc = static_cast<T*>(Lr->Xc);
-      HeadCache cache = Lr->cache;
-      float *lp = Lr->logp, *lp2 = Lr->logp2;
-      const int64_t* stp = Lr->counters;
-      if (!td3) {
-        ops.push_back({"actor_head", [=](cudaStream_t st) {
-                         sac_head_fwd_kernel<T><<<(unsigned)cdiv(2 * Bl, 128), 128, 0, st>>>(
-                             Hh, ldh, m, Bl, row0, seed, stp, lo, hi, Xc, ldc, o, cache, lp2, lp);
-                         return cudaGetLastError();
-                       }});
+      // head layer: fused squashed-Gaussian (SAC) / tanh + smoothing (TD3) epilogue when possible
+      GemmArgs a = mk(h, td3 ? EPI_TD3_HEAD : EPI_SAC_HEAD, 0, 0);
+      a.head = he;
+      for (const Pass& ps : passes) {
+        GemmGroup& g = add(a, Ta(Lr->Aact[L - 1], ps.row, h), h, Wp(ps.id, L), ldw(ps.id, L), Lr->H + ps.row * ldh,
+                           ldh, ps.M, an.out[L], bp(ps.id, L));
+        g.row0 = (int)ps.row;
+      }
+      if (tc_ok(a)) {
+        gemm("actor_head_gemm", a);
       } else {
-        const float ns = (float)Lr->cfg.td3_noise, nc = (float)Lr->cfg.td3_noise_clip;
-        const bool on = actor_step;
+        a.epi = EPI_BIAS_F32;
+        gemm("actor_head_gemm", a);
+        float* Hh = Lr->H;
+        const int Mh = passes.size() == 2 || !td3 ? 2 * Bl : Bl;
+        const HeadEpi hh = he;
+        const int t3 = td3;
         ops.push_back({"actor_head", [=](cudaStream_t st) {
-                         td3_head_fwd_kernel<T><<<(unsigned)cdiv(on ? 2 * Bl : Bl, 128), 128, 0, st>>>(
-                             Hh, ldh, m, Bl, on ? 2 * Bl : Bl, row0, seed, stp, ns, nc, Xc, ldc, o, cache.a);
-                         return cudaGetLastError();
+                         if (t3) return launch_pdl(td3_head_fwd_kernel<T>, dim3((unsigned)cdiv(Mh, 128)), dim3(128), 0, st, Hh, ldh, hh, Mh);
+                         return launch_pdl(sac_head_fwd_kernel<T>, dim3((unsigned)cdiv(Mh, 128)), dim3(128), 0, st, Hh, ldh, hh, Mh);
                        }});
       }
     }
-    // ---- a4: target critics on [s2 | a'] (M = Bl), a5: online critics on [s | a ; s | a~] (M = 2Bl)
+    // ---- a4: target critics on [s2 | a'] (M = Bl) and a5: online critics on [s | a ; s | a~]
+    //      (M = 2Bl), all four in one launch per layer; the N = 1 head is a row dot fused into
+    //      the last hidden layer's epilogue when the row fits one tile.
     const NetLayout& cn = Lr->net[NET_Q1];
     const int Mon = actor_step ? 2 * Bl : Bl;
-    for (int pass = 0; pass < 2; ++pass) {
-      const bool tgt = pass == 0;
-      const int M = tgt ? Bl : Mon;
-      const int64_t row = tgt ? 2 * Bl : 0;
+    {
       for (int l = 0; l < L; ++l) {
-        GemmArgs a = fwd_args(h, cn.in[l], l == 0 ? ldc : h, cn.ld[l], h, EPI_BIAS_RELU);
-        a.n_groups = 2;
-        for (int i = 0; i < 2; ++i) {
-          const int id = tgt ? NET_Q1T + i : NET_Q1 + i;
-          void* dst = tgt ? Lr->Atg[i][l] : Lr->Aon[i][l];
-          a.g[i].A = l == 0 ? (const void*)Ta(Lr->Xc, row, ldc) : (const void*)(tgt ? Lr->Atg[i][l - 1] : Lr->Aon[i][l - 1]);
-          a.g[i].B = Wp(id, l);
-          a.g[i].C = dst;
-          a.g[i].bias = bp(id, l);
-          a.g[i].M = M;
+        GemmArgs a = mk(cn.in[l], EPI_BIAS_RELU, 0, 0);
+        for (int pass = 0; pass < 2; ++pass) {
+          const bool tgt = pass == 1;
+          for (int i = 0; i < 2; ++i) {
+            const int id = tgt ? NET_Q1T + i : NET_Q1 + i;
+            void* dst = tgt ? Lr->Atg[i][l] : Lr->Aon[i][l];
+            const void* src = l == 0 ? (const void*)Ta(Lr->Xc, tgt ? 2 * Bl : 0, ldc)
+                                     : (const void*)(tgt ? Lr->Atg[i][l - 1] : Lr->Aon[i][l - 1]);
+            GemmGroup& g = add(a, src, l == 0 ? ldc : h, Wp(id, l), cn.ld[l], dst, h, tgt ? Bl : Mon, h, bp(id, l));
+            if (l == L - 1) {
+              g.dot_w = P + Lr->pbase[id] + Lr->net[id].w[L];
+              g.dot_b = bp(id, L);
+              g.dot_out = tgt ? Lr->q_tg[i] : Lr->q_on[i];
+            }
+          }
         }
-        gemm(tgt ? "target_critic_gemm" : "critic_fwd_gemm", a);
+        if (l == L - 1 && !tc_ok(a)) {
+          for (int i = 0; i < a.n_groups; ++i) a.g[i].dot_out = nullptr;
+          gemm("critic_fwd_gemm", a);
+          for (int pass = 0; pass < 2; ++pass) {
+            const bool tgt = pass == 1;
+            const int M = tgt ? Bl : Mon;
+            RowdotArgs ra{};
+            ra.M = M;
+            ra.h = h;
+            ra.ld = h;
+            for (int i = 0; i < 2; ++i) {
+              const int id = tgt ? NET_Q1T + i : NET_Q1 + i;
+              ra.g[i].A = tgt ? Lr->Atg[i][L - 1] : Lr->Aon[i][L - 1];
+              ra.g[i].w = P + Lr->pbase[id] + Lr->net[id].w[L];
+              ra.g[i].b = bp(id, L);
+              ra.g[i].q = tgt ? Lr->q_tg[i] : Lr->q_on[i];
+            }
+            ops.push_back({"critic_head", [ra, M](cudaStream_t st) {
+                             return launch_pdl(rowdot_kernel<T>, dim3((unsigned)cdiv((int64_t)M * 32, 256), 2), dim3(256), 0, st, ra);
+                           }});
+          }
+        } else {
+          gemm("critic_fwd_gemm", a);
+        }
       }
-      RowdotArgs ra{};
-      ra.M = M;
-      ra.h = h;
-      ra.ld = h;
-      for (int i = 0; i < 2; ++i) {
-        const int id = tgt ? NET_Q1T + i : NET_Q1 + i;
-        ra.g[i].A = tgt ? Lr->Atg[i][L - 1] : Lr->Aon[i][L - 1];
-        ra.g[i].w = P + Lr->pbase[id] + Lr->net[id].w[L];
-        ra.g[i].b = bp(id, L);
-        ra.g[i].q = tgt ? Lr->q_tg[i] : Lr->q_on[i];
-      }
-      ops.push_back({tgt ? "target_critic_head" : "critic_head", [ra, M](cudaStream_t st) {
-                       rowdot_kernel<T><<<dim3((unsigned)cdiv((int64_t)M * 32, 256), 2), 256, 0, st>>>(ra);
-                       return cudaGetLastError();
-                     }});
     }
     // ---- a4/a5: Bellman target, losses, head gradients, stat partials
     const int nblk = (int)cdiv(Bl, LOSS_NT);
@@ -381,7 +427,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       const int64_t* stp = Lr->counters;
       const int t3 = td3;
       ops.push_back({"critic_loss", [=](cudaStream_t st) {
-                       critic_loss_kernel<<<nblk, LOSS_NT, 0, st>>>(qt1, qt2, q1, q2, lp2, lp, rr, dd, la, gamma, invB,
+                       launch_pdl(critic_loss_kernel, dim3(nblk), dim3(LOSS_NT), 0, st, qt1, qt2, q1, q2, lp2, lp, rr, dd, la, gamma, invB,
                                                                    Bl, t3, stp, delay, g1, g2, yy, part);
                        return cudaGetLastError();
                      }});
@@ -400,77 +446,55 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       }
       const int64_t tot = (int64_t)Mon * h;
       ops.push_back({"critic_head_bwd", [hb, tot](cudaStream_t st) {
-                       critic_head_bwd_kernel<T><<<dim3((unsigned)std::min<int64_t>(cdiv(tot, 256), 148 * 8), 2), 256, 0, st>>>(hb);
+                       launch_pdl(critic_head_bwd_kernel<T>, dim3(dim3((unsigned)std::min<int64_t>(cdiv(tot / 8, 256), 148 * 16), 2)), dim3(256), 0, st, hb);
                        return cudaGetLastError();
                      }});
       // dgrad through hidden layers l = L-1 .. 1 (all Mon rows)
       for (int l = L - 1; l >= 1; --l) {
-        GemmArgs a = fwd_args(h, h, h, cn.ld[l], h, EPI_MASK);
-        a.b_mn = 1;
-        a.ldaux = h;
-        a.n_groups = 2;
-        for (int i = 0; i < 2; ++i) {
-          a.g[i].A = Lr->dZc[i][l];
-          a.g[i].B = Wp(NET_Q1 + i, l);
-          a.g[i].C = Lr->dZc[i][l - 1];
-          a.g[i].aux = Lr->Aon[i][l - 1];
-          a.g[i].M = Mon;
-        }
+        GemmArgs a = mk(h, EPI_MASK, 0, 1);
+        for (int i = 0; i < 2; ++i)
+          add(a, Lr->dZc[i][l], h, Wp(NET_Q1 + i, l), cn.ld[l], Lr->dZc[i][l - 1], h, Mon, h, nullptr, Lr->Aon[i][l - 1], h);
         gemm("critic_dgrad_gemm", a);
       }
       // input dgrad for the actor rows (only the action columns are consumed)
       if (actor_step) {
-        GemmArgs a = fwd_args(o + m, h, h, cn.ld[0], ldc, EPI_F32);
-        a.b_mn = 1;
-        a.n_groups = td3 ? 1 : 2;
-        for (int i = 0; i < a.n_groups; ++i) {
-          a.g[i].A = Ta(Lr->dZc[i][0], Bl, h);
-          a.g[i].B = Wp(NET_Q1 + i, 0);
-          a.g[i].C = Lr->dXc[i];
-          a.g[i].M = Bl;
-        }
+        GemmArgs a = mk(h, EPI_F32, 0, 1);
+        for (int i = 0; i < (td3 ? 1 : 2); ++i)
+          add(a, Ta(Lr->dZc[i][0], Bl, h), h, Wp(NET_Q1 + i, 0), cn.ld[0], Lr->dXc[i], ldc, Bl, o + m);
         gemm("critic_input_dgrad_gemm", a);
       }
-      // wgrad on the Bl loss rows: dW_l = dZ_l^T A_{l-1}; split-K over the batch
-      for (int l = 0; l < L; ++l) {
-        GemmArgs a = fwd_args(cn.in[l], Bl, h, l == 0 ? ldc : h, cn.in[l], EPI_F32);
-        a.a_mn = 1;
-        a.b_mn = 1;
+      // wgrad on the Bl loss rows: dW_l = dZ_l^T A_{l-1}; split-K over the batch; <= 4 tensors per launch
+      {
+        GemmArgs a = mk(Bl, EPI_F32, 1, 1);
         a.splits = Sw;
         a.k_per_split = (int)rows_w;
-        a.split_stride = (int64_t)h * cn.in[l];
-        a.n_groups = 2;
-        for (int i = 0; i < 2; ++i) {
-          a.g[i].A = Lr->dZc[i][l];
-          a.g[i].B = l == 0 ? Lr->Xc : Lr->Aon[i][l - 1];
-          a.g[i].C = Lr->G + slot_of(NET_Q1 + i, l, true).g_off;
-          a.g[i].M = h;
-        }
-        a.N = cn.in[l];
-        gemm("critic_wgrad_gemm", a);
+        for (int i = 0; i < 2; ++i)
+          for (int l = 0; l < L; ++l) {
+            if (a.n_groups == 4) {
+              gemm("critic_wgrad_gemm", a);
+              a.n_groups = 0;
+              a.N = 0;
+            }
+            GemmGroup& g = add(a, Lr->dZc[i][l], h, l == 0 ? Lr->Xc : Lr->Aon[i][l - 1], l == 0 ? ldc : h,
+                               Lr->G + slot_of(NET_Q1 + i, l, true).g_off, cn.in[l], h, cn.in[l]);
+            g.split_stride = (int64_t)h * cn.in[l];
+          }
+        if (a.n_groups) gemm("critic_wgrad_gemm", a);
       }
-      // bias gradients (column sums of dZ over loss rows) and the N = 1 head
-      for (int i = 0; i < 2; ++i) {
-        for (int l = 0; l < L; ++l) {
-          const T* X = static_cast<const T*>(Lr->dZc[i][l]);
-          float* out = Lr->G + slot_of(NET_Q1 + i, l, false).g_off;
-          ops.push_back({"critic_bias_grad", [=](cudaStream_t st) {
-                           colsum_kernel<T><<<dim3((unsigned)cdiv(h, CS_COLS), Sb), CS_COLS * CS_ROWS, 0, st>>>(
-                               X, h, h, Bl, (int)rows_b, nullptr, out);
-                           return cudaGetLastError();
-                         }});
+      // bias gradients (column sums of dZ over loss rows) and the N = 1 head, one launch
+      {
+        ColsumArgs ca{};
+        ca.rps = (int)rows_b;
+        for (int i = 0; i < 2; ++i) {
+          for (int l = 0; l < L; ++l)
+            ca.j[ca.n_jobs++] = {Lr->dZc[i][l], nullptr, Lr->G + slot_of(NET_Q1 + i, l, false).g_off, h, h, Bl, 0};
+          ca.j[ca.n_jobs++] = {Lr->Aon[i][L - 1], Lr->gq[i], Lr->G + slot_of(NET_Q1 + i, L, true).g_off, h, h, Bl, 0};
+          ca.j[ca.n_jobs++] = {Lr->gq[i], nullptr, Lr->G + slot_of(NET_Q1 + i, L, false).g_off, 1, 1, Bl, 1};
         }
-        const T* AL = static_cast<const T*>(Lr->Aon[i][L - 1]);
-        const float* g = Lr->gq[i];
-        float* outw = Lr->G + slot_of(NET_Q1 + i, L, true).g_off;
-        float* outb = Lr->G + slot_of(NET_Q1 + i, L, false).g_off;
-        ops.push_back({"critic_bias_grad", [=](cudaStream_t st) {
-                         colsum_kernel<T><<<dim3((unsigned)cdiv(h, CS_COLS), Sb), CS_COLS * CS_ROWS, 0, st>>>(
-                             AL, h, h, Bl, (int)rows_b, g, outw);
-                         colsum_kernel<float><<<dim3(1, Sb), CS_COLS * CS_ROWS, 0, st>>>(g, 1, 1, Bl, (int)rows_b,
-                                                                                        nullptr, outb);
+        ops.push_back({"critic_bias_grad", [ca, Sb](cudaStream_t st) {
+                         launch_pdl(colsum_multi_kernel<T>, dim3(dim3(Sb, ca.n_jobs)), dim3(CS_TX * CS_TY), 0, st, ca);
                          return cudaGetLastError();
-                       }, 2});
+                       }});
       }
     }
     // ---- a7: actor backward (s-rows Bl..2Bl of the actor activations)
@@ -484,13 +508,13 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         const float* la = P + Lr->p_log_alpha;
         if (!td3) {
           ops.push_back({"actor_head_bwd", [=](cudaStream_t st) {
-                           sac_head_bwd_kernel<T><<<(unsigned)cdiv((int64_t)Bl * m, 256), 256, 0, st>>>(
+                           launch_pdl(sac_head_bwd_kernel<T>, dim3((unsigned)cdiv((int64_t)Bl * m, 256)), dim3(256), 0, st, 
                                x1, x2, ldc, o, m, Bl, cache, la, invB, lo, hi, dH, ldh);
                            return cudaGetLastError();
                          }});
         } else {
           ops.push_back({"actor_head_bwd", [=](cudaStream_t st) {
-                           td3_head_bwd_kernel<T><<<(unsigned)cdiv((int64_t)Bl * m, 256), 256, 0, st>>>(
+                           launch_pdl(td3_head_bwd_kernel<T>, dim3((unsigned)cdiv((int64_t)Bl * m, 256)), dim3(256), 0, st, 
                                x1, ldc, o, m, Bl, cache.a, dH, ldh);
                            return cudaGetLastError();
                          }});
@@ -498,40 +522,37 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       }
       // dgrad: dZ_{L-1} = (dH W_out) * 1[A_{L-1} > 0], then down the hidden stack
       for (int l = L; l >= 1; --l) {
-        GemmArgs a = fwd_args(h, an.out[l], l == L ? ldh : h, an.ld[l], h, EPI_MASK);
-        a.b_mn = 1;
-        a.ldaux = h;
-        a.n_groups = 1;
-        a.g[0].A = l == L ? (const void*)dH : (const void*)Lr->dZa[l];
-        a.g[0].B = Wp(NET_ACTOR, l);
-        a.g[0].C = Lr->dZa[l - 1];
-        a.g[0].aux = Ta(Lr->Aact[l - 1], Bl, h);
-        a.g[0].M = Bl;
+        GemmArgs a = mk(an.out[l], EPI_MASK, 0, 1);
+        add(a, l == L ? (const void*)dH : (const void*)Lr->dZa[l], l == L ? ldh : h, Wp(NET_ACTOR, l), an.ld[l],
+            Lr->dZa[l - 1], h, Bl, h, nullptr, Ta(Lr->Aact[l - 1], Bl, h), h);
         gemm("actor_dgrad_gemm", a);
       }
-      // wgrad: dW_l = dZ_l^T A_{l-1} over the Bl s-rows (dZ_L = dH)
-      for (int l = 0; l <= L; ++l) {
-        GemmArgs a = fwd_args(an.in[l], Bl, l == L ? ldh : h, l == 0 ? lda : h, an.in[l], EPI_F32);
-        a.a_mn = 1;
-        a.b_mn = 1;
+      // wgrad: dW_l = dZ_l^T A_{l-1} over the Bl s-rows (dZ_L = dH); all layers in one launch (<= 4)
+      {
+        GemmArgs a = mk(Bl, EPI_F32, 1, 1);
         a.splits = Sw;
         a.k_per_split = (int)rows_w;
-        a.split_stride = (int64_t)an.out[l] * an.in[l];
-        a.n_groups = 1;
-        a.g[0].A = l == L ? (const void*)dH : (const void*)Lr->dZa[l];
-        a.g[0].B = l == 0 ? (const void*)Ta(Lr->Xa, Bl, lda) : (const void*)Ta(Lr->Aact[l - 1], Bl, h);
-        a.g[0].C = Lr->G + slot_of(NET_ACTOR, l, true).g_off;
-        a.g[0].M = an.out[l];
-        gemm("actor_wgrad_gemm", a);
+        for (int l = 0; l <= L; ++l) {
+          if (a.n_groups == 4) {
+            gemm("actor_wgrad_gemm", a);
+            a.n_groups = 0;
+            a.N = 0;
+          }
+          GemmGroup& g = add(a, l == L ? (const void*)dH : (const void*)Lr->dZa[l], l == L ? ldh : h,
+                             l == 0 ? (const void*)Ta(Lr->Xa, Bl, lda) : (const void*)Ta(Lr->Aact[l - 1], Bl, h),
+                             l == 0 ? lda : h, Lr->G + slot_of(NET_ACTOR, l, true).g_off, an.in[l], an.out[l], an.in[l]);
+          g.split_stride = (int64_t)an.out[l] * an.in[l];
+        }
+        if (a.n_groups) gemm("actor_wgrad_gemm", a);
       }
-      for (int l = 0; l <= L; ++l) {
-        const T* X = l == L ? dH : static_cast<const T*>(Lr->dZa[l]);
-        const int ldx = l == L ? ldh : h;
-        const int N = an.out[l];
-        float* out = Lr->G + slot_of(NET_ACTOR, l, false).g_off;
-        ops.push_back({"actor_bias_grad", [=](cudaStream_t st) {
-                         colsum_kernel<T><<<dim3((unsigned)cdiv(N, CS_COLS), Sb), CS_COLS * CS_ROWS, 0, st>>>(
-                             X, ldx, N, Bl, (int)rows_b, nullptr, out);
+      {
+        ColsumArgs ca{};
+        ca.rps = (int)rows_b;
+        for (int l = 0; l <= L; ++l)
+          ca.j[ca.n_jobs++] = {l == L ? (const void*)dH : (const void*)Lr->dZa[l], nullptr,
+                               Lr->G + slot_of(NET_ACTOR, l, false).g_off, l == L ? ldh : h, an.out[l], Bl, 0};
+        ops.push_back({"actor_bias_grad", [ca, Sb](cudaStream_t st) {
+                         launch_pdl(colsum_multi_kernel<T>, dim3(dim3(Sb, ca.n_jobs)), dim3(CS_TX * CS_TY), 0, st, ca);
                          return cudaGetLastError();
                        }});
       }
@@ -549,7 +570,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       int* fl = Lr->d_flag;
       const double Bd = (double)B;
       ops.push_back({"stats", [=](cudaStream_t st) {
-                       stats_kernel<<<1, 32, 0, st>>>(part, nblk, nullptr, la, te, Bd, t3, stp, delay, so, ga, fl);
+                       launch_pdl(stats_kernel, dim3(1), dim3(32), 0, st, part, nblk, nullptr, la, te, Bd, t3, stp, delay, so, ga, fl);
                        return cudaGetLastError();
                      }});
     }
@@ -611,13 +632,13 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       int* fl = Lr->d_flag;
       const unsigned nseg = (unsigned)segs.size();
       ops.push_back({"adam_polyak", [=](cudaStream_t st) {
-                       adam_polyak_kernel<T><<<nseg, 256, 0, st>>>(dt, ds, hp, Pm, Mm, Vm, S, ctr, fl);
+                       launch_pdl(adam_polyak_kernel<T>, dim3(nseg), dim3(256), 0, st, dt, ds, hp, Pm, Mm, Vm, S, ctr, fl);
                        return cudaGetLastError();
                      }});
       const int t3 = td3, aa = Lr->cfg.alpha_auto;
       const int con = Lr->cfg.role != SPZ_ROLE_ACTOR, aon = Lr->cfg.role != SPZ_ROLE_CRITIC;
       ops.push_back({"advance", [=](cudaStream_t st) {
-                       advance_kernel<<<1, 1, 0, st>>>(ctr, fl, t3, delay, aa, con, aon);
+                       launch_pdl(advance_kernel, dim3(1), dim3(1), 0, st, ctr, fl, t3, delay, aa, con, aon);
                        return cudaGetLastError();
                      }});
     }
@@ -682,7 +703,7 @@ static spz_status set_fill(spz_learner* Lr) {
 
 template <typename T>
 static spz_status refresh_shadows_t(spz_learner* Lr) {
-  shadow_refresh_kernel<T><<<dim3(64, (unsigned)Lr->n_shadow), 256, 0, Lr->stream>>>(Lr->d_shadow, Lr->n_shadow, Lr->P,
+  launch_pdl(shadow_refresh_kernel<T>, dim3(dim3(64, (unsigned)Lr->n_shadow)), dim3(256), 0, Lr->stream, Lr->d_shadow, Lr->n_shadow, Lr->P,
                                                                                      static_cast<T*>(Lr->S));
   SPZ_CUDA_TRY(cudaGetLastError());
   return SPZ_OK;
@@ -751,8 +772,10 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   if (cfg->obs_dim != ring->o || cfg->act_dim != ring->m)
     return fail(SPZ_EINVAL, "spz_learner_create: config dims do not match the ring");
   if (cfg->device != ring->device) return fail(SPZ_EINVAL, "spz_learner_create: ring lives on another device");
-  if (cfg->hidden < 1 || cfg->n_hidden < 1 || cfg->n_hidden > 6) return fail(SPZ_EINVAL, "spz_learner_create: need hidden >= 1 and 1 <= n_hidden <= 6");
+  if (cfg->hidden < 16 || cfg->hidden % 16 || cfg->n_hidden < 1 || cfg->n_hidden > 6)
+    return fail(SPZ_EINVAL, "spz_learner_create: need hidden a positive multiple of 16 and 1 <= n_hidden <= 6");
   if (cfg->max_batch < 1) return fail(SPZ_EINVAL, "spz_learner_create: max_batch must be >= 1");
+  if (cfg->act_dim > 32) return fail(SPZ_EINVAL, "spz_learner_create: act_dim must be <= 32");
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return fail(SPZ_EINVAL, "spz_learner_create: bad rank/world_size");
   if (cfg->world_size > 1) return fail(SPZ_EUNSUPPORTED, "spz_learner_create: multi-rank learners are not built yet");
   if (cfg->role != SPZ_ROLE_ALL) return fail(SPZ_EUNSUPPORTED, "spz_learner_create: split roles are not built yet");
@@ -894,7 +917,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     for (int l = 0; l < n.nl; ++l) {
       const float bound = 1.0f / std::sqrt((float)n.in[l]);
       const int64_t cnt = (int64_t)n.out[l] * n.in[l] + n.out[l];
-      init_uniform_kernel<<<(unsigned)std::min<int64_t>(cdiv(cnt, 256), 1024), 256, 0, Lr->stream>>>(
+      launch_pdl(init_uniform_kernel, dim3((unsigned)std::min<int64_t>(cdiv(cnt, 256), 1024)), dim3(256), 0, Lr->stream, 
           Lr->P, Lr->pbase[id] + n.w[l], cnt, bound, cfg->init_seed, (uint32_t)id, n.w[l]);
     }
   }

@@ -13,6 +13,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -27,6 +28,7 @@ constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
 struct TcParams {
   GemmArgs a;
+  int stages;  // pipeline depth actually used (<= STAGES; short-K problems use fewer -> 2 CTAs/SM)
   CUtensorMap ta[4];
   CUtensorMap tb[4];
 };
@@ -109,68 +111,75 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&p);
 }
 
-// Epilogue of 16 consecutive accumulator columns n..n+15 of row m.
-__device__ __forceinline__ void epi16(const GemmArgs& a, const GemmGroup& g, int split, int m, int n, const float (&v)[16]) {
-  const bool full = n + 16 <= a.N;
-  const int64_t off = (int64_t)m * a.ldc + n;
+// Epilogue of 16 consecutive accumulator columns n..n+15 of row m (bias / dot vectors staged
+// in shared memory for this column chunk).  Returns the chunk's contribution to the row dot.
+__device__ __forceinline__ float epi16(const GemmArgs& a, const GemmGroup& g, int split, int m, int n, const float (&v)[16],
+                                       const float* __restrict__ bias, const float* __restrict__ dotw) {
+  const bool full = n + 16 <= g.N;
+  const int64_t off = (int64_t)m * g.ldc + n;
+  float dot = 0.f;
   switch (a.epi) {
     case EPI_BIAS_RELU: {
       __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C);
-      if (full && (a.ldc & 7) == 0) {
-        uint32_t p[8];
+      float z[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float z0 = v[2 * j] + __ldg(g.bias + n + 2 * j), z1 = v[2 * j + 1] + __ldg(g.bias + n + 2 * j + 1);
-          p[j] = pack_bf16(fmaxf(z0, 0.f), fmaxf(z1, 0.f));
-        }
+      for (int j = 0; j < 16; ++j) z[j] = fmaxf(v[j] + bias[j], 0.f);
+      if (dotw) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dot = fmaf(z[j], dotw[j], dot);  // dotw is zero past g.N
+      }
+      if (full && (g.ldc & 7) == 0) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pk[j] = pack_bf16(z[2 * j], z[2 * j + 1]);
         uint4* dst = reinterpret_cast<uint4*>(C + off);
-        dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
-        dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       } else {
-        for (int j = 0; j < 16 && n + j < a.N; ++j) C[off + j] = __float2bfloat16_rn(fmaxf(v[j] + g.bias[n + j], 0.f));
+        for (int j = 0; j < 16 && n + j < g.N; ++j) C[off + j] = __float2bfloat16_rn(z[j]);
       }
       break;
     }
     case EPI_MASK: {
       __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C);
-      const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(g.aux) + (int64_t)m * a.ldaux + n;
-      if (full && (a.ldc & 7) == 0 && (a.ldaux & 7) == 0) {
+      const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(g.aux) + (int64_t)m * g.ldaux + n;
+      if (full && (g.ldc & 7) == 0 && (g.ldaux & 7) == 0) {
         const uint4 x0 = reinterpret_cast<const uint4*>(X)[0], x1 = reinterpret_cast<const uint4*>(X)[1];
-        const __nv_bfloat16* xs0 = reinterpret_cast<const __nv_bfloat16*>(&x0);
-        const __nv_bfloat16* xs1 = reinterpret_cast<const __nv_bfloat16*>(&x1);
-        uint32_t p[8];
+        const __nv_bfloat162* xs0 = reinterpret_cast<const __nv_bfloat162*>(&x0);
+        const __nv_bfloat162* xs1 = reinterpret_cast<const __nv_bfloat162*>(&x1);
+        uint32_t pk[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const __nv_bfloat16 a0 = j < 4 ? xs0[2 * j] : xs1[2 * j - 8];
-          const __nv_bfloat16 a1 = j < 4 ? xs0[2 * j + 1] : xs1[2 * j - 7];
-          p[j] = pack_bf16(__bfloat162float(a0) > 0.f ? v[2 * j] : 0.f, __bfloat162float(a1) > 0.f ? v[2 * j + 1] : 0.f);
+          const float2 f = __bfloat1622float2(j < 4 ? xs0[j] : xs1[j - 4]);
+          pk[j] = pack_bf16(f.x > 0.f ? v[2 * j] : 0.f, f.y > 0.f ? v[2 * j + 1] : 0.f);
         }
         uint4* dst = reinterpret_cast<uint4*>(C + off);
-        dst[0] = make_uint4(p[0], p[1], p[2], p[3]);
-        dst[1] = make_uint4(p[4], p[5], p[6], p[7]);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       } else {
-        for (int j = 0; j < 16 && n + j < a.N; ++j)
+        for (int j = 0; j < 16 && n + j < g.N; ++j)
           C[off + j] = __float2bfloat16_rn(__bfloat162float(X[j]) > 0.f ? v[j] : 0.f);
       }
       break;
     }
     case EPI_BIAS_F32: {
       float* C = static_cast<float*>(g.C) + off;
-      for (int j = 0; j < 16 && n + j < a.N; ++j) C[j] = v[j] + g.bias[n + j];
+      for (int j = 0; j < 16 && n + j < g.N; ++j) C[j] = v[j] + bias[j];
       break;
     }
     default: {
-      float* C = static_cast<float*>(g.C) + off + (int64_t)split * a.split_stride;
-      if (full && (a.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
+      float* C = static_cast<float*>(g.C) + off + (int64_t)split * g.split_stride;
+      if (full && (g.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
         float4* d4 = reinterpret_cast<float4*>(C);
 #pragma unroll
         for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
       } else {
-        for (int j = 0; j < 16 && n + j < a.N; ++j) C[j] = v[j];
+        for (int j = 0; j < 16 && n + j < g.N; ++j) C[j] = v[j];
       }
       break;
     }
   }
+  return dot;
 }
 
 template <int BN, bool AMN, bool BMN>
@@ -182,17 +191,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  const int NS = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * STAGE);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  float* bias_s = reinterpret_cast<float*>(tmem_slot + 4);  // [BN] epilogue bias
+  float* dot_s = bias_s + BN;                               // [BN] fused row-dot weights
 
   const GemmArgs& a = p.a;
   const int gz = blockIdx.z;
   const int grp = gz / a.splits, split = gz % a.splits;
   const GemmGroup& g = a.g[grp];
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  if (m0 >= g.M) return;
+  if (m0 >= g.M || n0 >= g.N) return;
   const int k_begin = split * a.k_per_split;
   const int k_end = min(a.K, k_begin + a.k_per_split);
   const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
@@ -201,7 +213,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.ta[grp]);
     tma_prefetch(&p.tb[grp]);
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -218,13 +230,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // everything above overlapped the previous kernel (PDL); from here on we read its outputs
+  pdl_wait();
+  pdl_launch();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+        const int s = kb % NS;
+        const uint32_t ph = (uint32_t)(kb / NS) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
         uint8_t* sA = smem + s * STAGE;
         uint8_t* sB = sA + A_BYTES;
@@ -248,8 +263,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     if (lane == 0) {
       // ---------------- MMA issuer
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+        const int s = kb % NS;
+        const uint32_t ph = (uint32_t)(kb / NS) & 1u;
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint32_t sA = smem_u32(smem + s * STAGE);
@@ -268,23 +283,55 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     // ---------------- epilogue: TMEM lane quarter (warp % 4) holds rows q*32 .. q*32+31
     const int q = warp & 3;
     const int m = m0 + q * 32 + lane;
+    const bool has_bias = a.epi == EPI_BIAS_RELU || a.epi == EPI_BIAS_F32 || a.epi == EPI_SAC_HEAD || a.epi == EPI_TD3_HEAD;
+    const bool has_dot = a.epi == EPI_BIAS_RELU && g.dot_out != nullptr;
+    if (has_bias) {
+      for (int c = threadIdx.x - 64; c < BN; c += 128) {
+        bias_s[c] = n0 + c < g.N ? g.bias[n0 + c] : 0.f;
+        dot_s[c] = (has_dot && n0 + c < g.N) ? g.dot_w[n0 + c] : 0.f;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
+    }
     if (nkb > 0) {
       mbar_wait(tmem_full, 0);
       tc_fence_after();
     }
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-#pragma unroll 1
-    for (int c = 0; c < BN / 16; ++c) {
-      const int n = n0 + c * 16;
-      if (n >= a.N) break;  // warp-uniform
-      float v[16];
-      if (nkb > 0) {
-        tmem_ld16(trow + c * 16, v);
-      } else {
+    if (a.epi == EPI_SAC_HEAD || a.epi == EPI_TD3_HEAD) {
+      if constexpr (BN <= 64) {
+        // the whole head row (2m <= BN columns) lives in this thread's TMEM lane
+        float hrow[BN];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        for (int c = 0; c < BN / 16; ++c) {
+          float v[16];
+          if (nkb > 0) tmem_ld16(trow + c * 16, v);
+          else
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
+        }
+        if (m < g.M) {
+          if (a.epi == EPI_SAC_HEAD) sac_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow, hrow + a.head.m);
+          else td3_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow);
+        }
       }
-      if (m < g.M) epi16(a, g, split, m, n, v);
+    } else {
+      float dot = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN / 16; ++c) {
+        const int n = n0 + c * 16;
+        if (n >= g.N) break;  // warp-uniform
+        float v[16];
+        if (nkb > 0) {
+          tmem_ld16(trow + c * 16, v);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        }
+        if (m < g.M) dot += epi16(a, g, split, m, n, v, bias_s + c * 16, has_dot ? dot_s + c * 16 : nullptr);
+      }
+      if (has_dot && m < g.M) g.dot_out[m] = dot + g.dot_b[0];
     }
   }
   tc_fence_before();
@@ -324,22 +371,24 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 }
 
 template <int BN, bool AMN, bool BMN>
-cudaError_t launch(const TcParams& p, int maxM, cudaStream_t st) {
+cudaError_t launch(TcParams& p, int maxM, cudaStream_t st) {
   constexpr int STAGE = A_BYTES + BN * BK * 2;
-  constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  constexpr int SMEM_MAX = STAGES * STAGE + 1024 + 256 + BN * 8;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  const int kspan = p.a.splits > 1 ? p.a.k_per_split : p.a.K;
+  p.stages = (int)std::min<int64_t>(STAGES, std::max<int64_t>(1, cdiv(kspan, BK)));
+  const int smem = p.stages * STAGE + 1024 + 256 + BN * 8;
   dim3 grid((unsigned)cdiv(p.a.N, BN), (unsigned)cdiv(maxM, BM), (unsigned)(p.a.n_groups * p.a.splits));
-  tc_gemm_kernel<BN, AMN, BMN><<<grid, NTHREADS, SMEM, st>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(tc_gemm_kernel<BN, AMN, BMN>, grid, dim3(NTHREADS), (size_t)smem, st, p);
 }
 
 template <bool AMN, bool BMN>
-cudaError_t launch_bn(const TcParams& p, int bn, int maxM, cudaStream_t st) {
+cudaError_t launch_bn(TcParams& p, int bn, int maxM, cudaStream_t st) {
   switch (bn) {
     case 16: if constexpr (!BMN) return launch<16, AMN, BMN>(p, maxM, st); break;
     case 32: if constexpr (!BMN) return launch<32, AMN, BMN>(p, maxM, st); break;
@@ -362,11 +411,15 @@ int pick_bn(int N, bool bmn) {
 
 bool tc_gemm_supported(const GemmArgs& a) {
   if (a.N < 1 || a.K < 1 || a.n_groups < 1 || a.n_groups > 4) return false;
-  if ((a.lda & 7) || (a.ldb & 7)) return false;
   if (a.splits > 1 && (a.k_per_split % BK)) return false;
   if (a.a_mn && !a.b_mn) return false;  // layout combination not instantiated
+  const int bn = pick_bn(a.N, a.b_mn);
+  if ((a.epi == EPI_SAC_HEAD || a.epi == EPI_TD3_HEAD) && bn > 64) return false;
   for (int i = 0; i < a.n_groups; ++i) {
-    if ((reinterpret_cast<uintptr_t>(a.g[i].A) & 15) || (reinterpret_cast<uintptr_t>(a.g[i].B) & 15)) return false;
+    const GemmGroup& g = a.g[i];
+    if ((g.lda & 7) || (g.ldb & 7)) return false;
+    if ((reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15)) return false;
+    if (g.dot_out && g.N > bn) return false;  // fused row dot needs the whole row in one tile
   }
   return get_encode();
 }
@@ -380,13 +433,13 @@ cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st) {
   for (int i = 0; i < a.n_groups; ++i) {
     const GemmGroup& g = a.g[i];
     maxM = g.M > maxM ? g.M : maxM;
-    if (g.M < 1) continue;
+    if (g.M < 1 || g.N < 1) continue;
     bool ok;
-    if (!a.a_mn) ok = make_map(&p.ta[i], g.A, a.K, g.M, a.lda, BK, BM);      // A [M x K]
-    else ok = make_map(&p.ta[i], g.A, g.M, a.K, a.lda, 64, BK);             // A stored [K x M]
+    if (!a.a_mn) ok = make_map(&p.ta[i], g.A, a.K, g.M, g.lda, BK, BM);      // A [M x K]
+    else ok = make_map(&p.ta[i], g.A, g.M, a.K, g.lda, 64, BK);             // A stored [K x M]
     if (ok) {
-      if (!a.b_mn) ok = make_map(&p.tb[i], g.B, a.K, a.N, a.ldb, BK, bn);    // B [N x K]
-      else ok = make_map(&p.tb[i], g.B, a.N, a.K, a.ldb, 64, BK);           // B stored [K x N]
+      if (!a.b_mn) ok = make_map(&p.tb[i], g.B, a.K, g.N, g.ldb, BK, bn);    // B [N x K]
+      else ok = make_map(&p.tb[i], g.B, g.N, a.K, g.ldb, 64, BK);           // B stored [K x N]
     }
     if (!ok) return cudaErrorInvalidValue;
   }

@@ -6,8 +6,10 @@
 A "step" is one full update over one batch of B transitions
 sampled from a device-resident ring filled with synthetic transitions (synthdata).
 value = B * K * N / (max over ranks of the CUDA-event time of K steps) [frames/s];
-frames/s = update frequency x B.  With N > 1 every rank runs its own learner
-on its own GPU ("replicas", weak scaling; no data-path collective).
+frames/s = update frequency x B.  With N > 1 (torchrun, one process per GPU) the
+default --mode dp runs ONE row-sharded learner group over a global batch of B * N (each
+GPU B rows; gradients all-reduced with NCCL inside the step; weak scaling); --mode
+replicas runs N independent learners instead.
 
 Extra keys: roofline (dominant kernel class vs the measured peak in
 MEASURED_PEAKS.json), cpu_baseline (the oracle on this host's cores, bounded sample),
@@ -47,6 +49,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=None)
+    ap.add_argument("--mode", default="dp", choices=["dp", "replicas"],
+                    help="N > 1: dp = one row-sharded learner group (global batch B*N, NCCL gradient allreduce); "
+                         "replicas = N independent learners")
     return ap.parse_args()
 
 
@@ -72,13 +77,14 @@ def class_flops(w, B):
     Ma = 2 * B  # SAC: [s2; s]; TD3: target actor on s2 + online actor on s (delayed steps)
     add("actor_fwd_gemm", 2 * Ma * h * o + (L - 1) * 2 * Ma * h * h)
     add("actor_head_gemm", 2 * Ma * aout * h)
-    add("target_critic_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))
+    # one launch per layer runs the two target critics (B rows) and the two online critics (2B rows)
+    add("critic_fwd_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))
     add("critic_fwd_gemm", 2 * (2 * (2 * B) * h * cin + (L - 1) * 2 * (2 * B) * h * h))
     add("critic_dgrad_gemm", 2 * (L - 1) * 2 * (2 * B) * h * h)
     add("critic_input_dgrad_gemm", (1 if td3 else 2) * 2 * B * h * m)
-    add("critic_wgrad_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))
+    add("wgrad_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))  # critics ...
     add("actor_dgrad_gemm", 2 * B * aout * h + (L - 1) * 2 * B * h * h)
-    add("actor_wgrad_gemm", 2 * B * h * o + (L - 1) * 2 * B * h * h + 2 * B * aout * h)
+    add("wgrad_gemm", 2 * B * h * o + (L - 1) * 2 * B * h * h + 2 * B * aout * h)  # ... and the actor, one launch
     return f
 
 
@@ -192,13 +198,14 @@ def main():
     import torch.distributed as dist
     from paper_2312_06126_b200 import spz
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2312_06126_b200.dist import broadcast_bytes, env_rank
+    rank, world, local = env_rank()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     assert a.warmup >= 3, "timing rules: at least 3 warm-up steps"
+    dp = world > 1 and a.mode == "dp"
+    GB = B * world if dp else B  # the batch one learner (group) consumes per update
 
     # ring filled to capacity with synthetic transitions (ring bytes > L2, so gathers hit HBM)
     C = w.capacity
@@ -207,13 +214,16 @@ def main():
     for s0 in range(0, C, chunk):
         tr = synthdata.workload_transitions(w, n=min(chunk, C - s0), seed=synthdata.DATA_SEED + s0)
         ring.push(**tr)
-    lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=B,
-                      device=local, seed=synthdata.SAMPLE_SEED + rank)
+    kw = {}
+    if dp:
+        kw = dict(world_size=world, rank=rank, nccl_unique_id=broadcast_bytes(spz.spz_nccl_unique_id() if rank == 0 else None))
+    lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=GB,
+                      device=local, seed=synthdata.SAMPLE_SEED + (0 if dp else rank), **kw)
     stream = torch.cuda.Stream(device=local)
     lrn.set_stream(stream.cuda_stream)
 
     # warm-up (includes CUDA-graph capture)
-    lrn.update(B, a.warmup)
+    lrn.update(GB, a.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -222,7 +232,7 @@ def main():
     with Clocks(local) as clk:
         time.sleep(0.3)
         ev0.record(stream)
-        stats = lrn.update(B, a.steps)
+        stats = lrn.update(GB, a.steps)
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
@@ -232,14 +242,14 @@ def main():
         ms = t.item()
         dist.barrier()
     torch.cuda.synchronize()
-    frames = B * a.steps * world
+    frames = B * a.steps * world  # dp: global batch B*N per update; replicas: N learners x B
     value = frames / (ms / 1e3)
     ms_per_step = ms / a.steps
 
     # per-class device time (event-bracketed, un-graphed, same learner and batch) -> roofline
-    prof = lrn.profile(B, 5)
+    prof = lrn.profile(GB, 5)
     pk = peaks()
-    fl = class_flops(w, B)
+    fl = class_flops(w, B)  # per-GPU rows
     n_params = sum(lrn.get(n).size for n in ("actor", "q1", "q2"))
     by = class_bytes(w, B, n_params)
     kern = {}
@@ -265,28 +275,28 @@ def main():
     roof["step_gemm_tflops"] = gemm_f / (ms_per_step * 1e-3) / 1e12
     roof["step_frac_of_bf16_sustained"] = roof["step_gemm_tflops"] / pk["bf16_sust"]
     roof["gemm_share_of_step"] = gemm_t / sum(prof.values())
-    launches = lrn.launches_per_step(B) * a.steps
+    launches = lrn.launches_per_step(GB) * a.steps
 
     # e2e through the C ABI with host buffers
     e2e = None
     if not a.no_e2e:
         R_fields = 2 * w.obs_dim + w.act_dim + 2
-        host = synthdata.workload_transitions(w, n=B * 4, seed=synthdata.DATA_SEED + 99)
+        host = synthdata.workload_transitions(w, n=GB * 4, seed=synthdata.DATA_SEED + 99)
         pinned = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in host.items()}
         K2 = max(3, min(a.steps, 50))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for k in range(K2):
-            sl = slice((k % 4) * B, (k % 4 + 1) * B)
+            sl = slice((k % 4) * GB, (k % 4 + 1) * GB)  # dp: every rank's ring replica takes the global batch
             ring.push(**{n: v[sl] for n, v in pinned.items()})
-            lrn.update(B, 1)
+            lrn.update(GB, 1)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = t.item()
-        e2e = {"value": B * K2 * world / dt, "unit": "frames/s", "h2d_bytes_per_step": B * R_fields * 4,
+        e2e = {"value": B * K2 * world / dt, "unit": "frames/s", "h2d_bytes_per_step": GB * R_fields * 4 * world,
                "d2h_bytes_per_step": 64 + 32 + 4, "steps": K2,
                "note": "per step: spz_replay_push of B fresh host transitions (pinned) + spz_update(B, 1) with its stats read-back"}
 
@@ -305,8 +315,9 @@ def main():
             "ms_per_step": ms_per_step, "updates_per_s": 1e3 / ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": a.precision, "data": "synthetic",
             "config": {"workload": w.name, "global_batch": B * world, "batch_per_gpu": B, "algo": w.algo,
+                       "mode": ("dp-nccl" if dp else "replicas") if world > 1 else "single",
                        "hidden": f"{w.n_hidden}x{w.hidden}", "obs_dim": w.obs_dim, "act_dim": w.act_dim,
-                       "ring": C, "parallelism": "replicas" if world > 1 else "single",
+                       "ring": C, "parallelism": (f"dp{world}" if dp else f"replicas{world}") if world > 1 else "single",
                        "l2": f"ring {C * ((2 * w.obs_dim + w.act_dim + 2 + 3) // 4 * 4) * 4 / 1e6:.0f} MB > 126 MB L2; fresh random indices each step"},
             "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(), "gpu_launches": launches, "last_stats": stats,

@@ -127,11 +127,14 @@ typedef struct {
   spz_role role;
   const uint8_t* nccl_unique_id;   /* 128 bytes, identical on all ranks; NULL if world_size == 1 */
   int32_t use_graph;               /* 1 (default): replay the step as a CUDA graph */
+  int32_t comm_mode;               /* world_size > 1: 0 = NCCL allreduce (default); 1 = no exchange
+                                      (diagnostics: each rank applies its own shard's gradient) */
 } spz_config;
 
 /* Fill *out with the defaults above for (algo, o, m); h = 256, L = 2, max_batch 8192. */
 spz_status spz_config_default(spz_algo algo, int32_t obs_dim, int32_t act_dim, spz_config* out);
-/* Generate a fresh NCCL unique id (rank 0 calls this and broadcasts the bytes). */
+/* Generate a fresh NCCL unique id (rank 0 calls this and broadcasts the bytes).  NCCL is
+ * loaded at run time (libnccl.so.2); SPZ_ENCCL if unavailable. */
 spz_status spz_nccl_unique_id(uint8_t out[128]);
 
 typedef struct spz_learner spz_learner;

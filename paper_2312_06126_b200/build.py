@@ -19,8 +19,13 @@ OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libspz.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NCCL_INC = os.path.join(os.path.dirname(os.path.dirname(os.__file__)), "site-packages", "nvidia", "nccl", "include")
+if not os.path.isdir(NCCL_INC):
+    import glob as _g
+    _c = _g.glob("/opt/prime-rl/.venv/lib/python3*/site-packages/nvidia/nccl/include")
+    NCCL_INC = _c[0] if _c else NCCL_INC
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-Xptxas", "-warn-spills", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
+         "-Xptxas", "-warn-spills", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}", f"-I{NCCL_INC}"]
 
 
 def _newest_header():

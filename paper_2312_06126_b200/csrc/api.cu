@@ -40,11 +40,6 @@ const char* spz_last_error(void) { return spz::g_last_error.c_str(); }
 
 const char* spz_version(void) { return "spz 0.1 (sm_100a)"; }
 
-spz_status spz_nccl_unique_id(uint8_t out[128]) {
-  (void)out;
-  return spz::fail(SPZ_EUNSUPPORTED, "spz_nccl_unique_id: NCCL support not built yet");
-}
-
 spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, int64_t N, int64_t K, const void* A,
                               int64_t lda, int32_t a_mn, const void* B, int64_t ldb, int32_t b_mn, float* C, int64_t ldc,
                               int32_t splits, int64_t k_per_split) {

@@ -9,7 +9,7 @@
 // Split-K (wgrad, contraction over the batch) writes split s's partial sum to
 // C + s * split_stride; the fused Adam kernel sums splits in a fixed order, so the
 // result is deterministic (reading #16).
-// Up to 4 groups per launch (twin critics, online + target critics, all wgrads of a
+// Up to MAX_GROUPS groups per launch (twin critics, online + target critics, all wgrads of a
 // network) share K, operand majorness and the epilogue kind; pointers, M, N and row
 // pitches are per group.  The grid covers the largest group; other CTAs exit early.
 #pragma once
@@ -25,6 +25,7 @@ enum EpiKind : int {
   EPI_F32 = 3,        // C (f32) = acc                                                     -- wgrad partials / input dgrad
   EPI_SAC_HEAD = 4,   // acc + bias -> squashed-Gaussian head (heads.cuh), nothing stored in C
   EPI_TD3_HEAD = 5,   // acc + bias -> tanh head with target smoothing (heads.cuh)
+  EPI_MASK_BITS = 6,  // C (T) = acc * bit(aux[m, n / 32], n % 32)                        -- dgrad, packed ReLU mask
 };
 
 struct GemmGroup {
@@ -36,12 +37,15 @@ struct GemmGroup {
   const float* dot_w;  // EPI_BIAS_RELU: if set, dot_out[m] = sum_n relu(z[m, n]) dot_w[n] + dot_b[0]
   const float* dot_b;
   float* dot_out;
+  uint32_t* mask_out;  // EPI_BIAS_RELU: if set, bit n % 32 of mask_out[m * mask_ld + n / 32] = (z[m, n] > 0)
   int64_t split_stride;  // elements between split partials in C
   int M, N;
   int lda, ldb, ldc, ldaux;
-  int row0;  // head epilogues: local actor-pass row of this group's row 0
-  int pad_;
+  int row0;     // head epilogues: local actor-pass row of this group's row 0
+  int mask_ld;  // words per row of mask_out
 };
+
+constexpr int MAX_GROUPS = 8;
 
 struct GemmArgs {
   int N, K;  // N: max over groups (grid width)
@@ -50,7 +54,7 @@ struct GemmArgs {
   int splits;       // split-K count (>= 1)
   int k_per_split;  // contraction rows per split (multiple of the K tile)
   int n_groups;
-  GemmGroup g[4];
+  GemmGroup g[MAX_GROUPS];
   HeadEpi head;
 };
 

@@ -184,97 +184,192 @@ __device__ __forceinline__ void block_stats(double (&v)[NSTAT], double* __restri
   }
 }
 
-// ------------------------------------------------------------------ a4 + a5: Bellman target, critic losses, head gradients
-// Row j in [0, Bl):  y = r + gamma (1-d) (min(q'1, q'2) - alpha log pi');
+// ------------------------------------------------------------------ a4 + a5 + a6 head: Bellman target, losses, critic head backward
+// Block = LOSS_ROWS rows j of [0, Bl).  Per row:
+//   y = r + gamma (1-d) (min(q'1, q'2) - alpha log pi');     (TD3: no entropy term)
 //   loss rows:  g_qi[j] = 2 (q_i(s,a) - y) / B
-//   actor rows: g_qi[Bl + j] = -w_i / B with (w1, w2) = (1,0) | (0,1) | (1/2,1/2) on a tie.
-// TD3 (td3 = 1): no entropy term, actor rows use Q1 only with g = -1/B (only if actor_on).
-constexpr int LOSS_NT = 256;
+//   actor rows: g_qi[Bl + j] = -w_i / B, (w1, w2) = (1,0) | (0,1) | (1/2,1/2) on a tie
+//               (TD3: Q1 only, g = -1/B, and only on delayed steps)
+// then the critic head backward for those rows: dZ_L[r, n] = g_q[r] w_out[n] 1[A_L[r, n] > 0].
+// Loss statistics: per-block partials; the last block to finish sums them in block order into
+// `totals` (this rank's loss totals; all-reduced across a row-sharded group).
+constexpr int LOSS_ROWS = 16, LOSS_NT = 256;
 
-__global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(
-    const float* __restrict__ qt1, const float* __restrict__ qt2, const float* __restrict__ q1,
-    const float* __restrict__ q2, const float* __restrict__ logp2, const float* __restrict__ logp,
-    const float* __restrict__ r, const float* __restrict__ d, const float* __restrict__ log_alpha, float gamma,
-    float invB, int Bl, int td3, const int64_t* __restrict__ step_p, int delay, float* __restrict__ gq1,
-    float* __restrict__ gq2, float* __restrict__ y_out, double* __restrict__ partials) {
-  pdl_wait();
-  pdl_launch();
-  const int j = blockIdx.x * LOSS_NT + threadIdx.x;
-  double v[NSTAT] = {0, 0, 0, 0, 0, 0};
-  if (j < Bl) {
-    const float alpha = td3 ? 0.f : expf(*log_alpha);
-    const float qmin = fminf(qt1[j], qt2[j]);
-    const float boot = td3 ? qmin : qmin - alpha * logp2[j];
-    const float y = r[j] + gamma * (1.f - d[j]) * boot;
-    y_out[j] = y;
-    const float e1 = q1[j] - y, e2 = q2[j] - y;
-    gq1[j] = 2.f * e1 * invB;
-    gq2[j] = 2.f * e2 * invB;
-    v[0] = (double)e1 * e1 + (double)e2 * e2;
-    v[1] = q1[j];
-    v[2] = q2[j];
-    const float a1 = q1[Bl + j], a2 = q2[Bl + j];
-    if (!td3) {
-      const float w1 = a1 < a2 ? 1.f : (a1 > a2 ? 0.f : 0.5f);
-      gq1[Bl + j] = -w1 * invB;
-      gq2[Bl + j] = -(1.f - w1) * invB;
-      v[3] = (double)alpha * logp[j] - (double)fminf(a1, a2);
-      v[4] = logp[j];
-    } else {
-      const bool on = ((*step_p + 1) % delay) == 0;
-      gq1[Bl + j] = on ? -invB : 0.f;
-      gq2[Bl + j] = 0.f;
-      v[3] = on ? -(double)a1 : 0.0;
-    }
-  }
-  block_stats<LOSS_NT>(v, partials);
-}
-
-// ------------------------------------------------------------------ a6: critic head backward
-// dZ_L[r, n] = g_q[r] * w_out[n] * 1[A_L[r, n] > 0]   (two critics via blockIdx.y)
-struct HeadBwdGroup {
-  const float* gq;
-  const float* w;
-  const void* A;
-  void* dZ;
-};
-struct HeadBwdArgs {
-  int64_t M;
-  int h, ld;
-  HeadBwdGroup g[2];
+struct LossArgs {
+  const float *qt1, *qt2, *q1, *q2, *logp2, *logp, *r, *d, *log_alpha;
+  const int64_t* step_p;
+  float *gq1, *gq2, *y;
+  double* partials;
+  double* totals;
+  unsigned* ticket;
+  const void* A[2];          // last hidden activations (mask source when mask[] is null)
+  const uint32_t* mask[2];   // packed ReLU masks of the last hidden layer (tcgen05 path)
+  const float* w[2];
+  void* dZ[2];
+  float gamma, invB;
+  int Bl, td3, delay, actor_rows, h, ld, mask_ld;
 };
 
 template <typename T>
-__global__ void critic_head_bwd_kernel(const __grid_constant__ HeadBwdArgs a) {
+__global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_constant__ LossArgs a) {
   pdl_wait();
   pdl_launch();
-  const HeadBwdGroup& g = a.g[blockIdx.y];
-  const T* A = static_cast<const T*>(g.A);
-  T* dZ = static_cast<T*>(g.dZ);
-  const int hv = a.h / 8;  // 8-wide chunks per row (h % 8 == 0, ld % 8 == 0)
-  const int64_t total = a.M * hv;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rr = e / hv;
-    const int n = (int)(e - rr * hv) * 8;
-    const float gq = g.gq[rr];
-    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-      const uint4 u = *reinterpret_cast<const uint4*>(A + rr * a.ld + n);
-      const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&u);
-      uint4 o;
-      __nv_bfloat162* y = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(x[i]);
-        y[i] = __floats2bfloat162_rn(f.x > 0.f ? gq * g.w[n + 2 * i] : 0.f, f.y > 0.f ? gq * g.w[n + 2 * i + 1] : 0.f);
+  __shared__ float gs[2][2][LOSS_ROWS];  // [critic][loss | actor row][row]
+  __shared__ double red[LOSS_NT / 32][NSTAT];
+  __shared__ bool last;
+  const int j0 = blockIdx.x * LOSS_ROWS;
+  const int nr = min(LOSS_ROWS, a.Bl - j0);
+  double v[NSTAT] = {0, 0, 0, 0, 0, 0};
+  if (threadIdx.x < nr) {
+    const int j = j0 + threadIdx.x;
+    const float alpha = a.td3 ? 0.f : expf(*a.log_alpha);
+    const float qmin = fminf(a.qt1[j], a.qt2[j]);
+    const float boot = a.td3 ? qmin : qmin - alpha * a.logp2[j];
+    const float y = a.r[j] + a.gamma * (1.f - a.d[j]) * boot;
+    a.y[j] = y;
+    const float q1 = a.q1[j], q2 = a.q2[j];
+    const float e1 = q1 - y, e2 = q2 - y;
+    float g1 = 2.f * e1 * a.invB, g2 = 2.f * e2 * a.invB;
+    a.gq1[j] = g1;
+    a.gq2[j] = g2;
+    gs[0][0][threadIdx.x] = g1;
+    gs[1][0][threadIdx.x] = g2;
+    v[0] = (double)e1 * e1 + (double)e2 * e2;
+    v[1] = q1;
+    v[2] = q2;
+    if (a.actor_rows) {
+      const float a1 = a.q1[a.Bl + j], a2 = a.q2[a.Bl + j];
+      if (!a.td3) {
+        const float w1 = a1 < a2 ? 1.f : (a1 > a2 ? 0.f : 0.5f);
+        g1 = -w1 * a.invB;
+        g2 = -(1.f - w1) * a.invB;
+        v[3] = (double)alpha * a.logp[j] - (double)fminf(a1, a2);
+        v[4] = a.logp[j];
+      } else {
+        const bool on = ((*a.step_p + 1) % a.delay) == 0;
+        g1 = on ? -a.invB : 0.f;
+        g2 = 0.f;
+        v[3] = on ? -(double)a1 : 0.0;
       }
-      *reinterpret_cast<uint4*>(dZ + rr * a.ld + n) = o;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float act = to_f(A[rr * a.ld + n + i]);
-        dZ[rr * a.ld + n + i] = from_f<T>(act > 0.f ? gq * g.w[n + i] : 0.f);
-      }
+      a.gq1[a.Bl + j] = g1;
+      a.gq2[a.Bl + j] = g2;
+      gs[0][1][threadIdx.x] = g1;
+      gs[1][1][threadIdx.x] = g2;
     }
+  }
+  // block partial of the statistics (fixed shuffle tree, then warps in order)
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NSTAT; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NSTAT; ++i) red[wi][i] = v[i];
+  __syncthreads();
+  if (threadIdx.x < NSTAT) {
+    double t = 0.0;
+    for (int k = 0; k < LOSS_NT / 32; ++k) t += red[k][threadIdx.x];
+    a.partials[blockIdx.x * NSTAT + threadIdx.x] = t;
+  }
+  // critic head backward for this block's rows: per (row, 8-column chunk) item, the (critic, row kind)
+  // combinations are loaded together (independent 16-byte loads), then written
+  const int hv = a.h / 8;
+  const int per = nr * hv;
+  for (int e = threadIdx.x; e < per; e += LOSS_NT) {
+    const int rr = e / hv, n = (e - rr * hv) * 8;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+      if (a.mask[0]) {
+        // packed ReLU masks: 8 bits per 8-column chunk
+        uint32_t mb[2][2];
+#pragma unroll
+        for (int ci = 0; ci < 2; ++ci)
+#pragma unroll
+          for (int kind = 0; kind < 2; ++kind)
+            mb[ci][kind] = (kind == 0 || a.actor_rows)
+                               ? (a.mask[ci][((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.mask_ld + n / 32] >> (n & 31)) & 0xFFu
+                               : 0u;
+#pragma unroll
+        for (int ci = 0; ci < 2; ++ci) {
+          const float4 w0 = *reinterpret_cast<const float4*>(a.w[ci] + n), w1 = *reinterpret_cast<const float4*>(a.w[ci] + n + 4);
+          const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+          for (int kind = 0; kind < 2; ++kind) {
+            if (kind == 1 && !a.actor_rows) continue;
+            const float gq = gs[ci][kind][rr];
+            uint4 o;
+            __nv_bfloat162* yv = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              yv[i] = __floats2bfloat162_rn((mb[ci][kind] >> (2 * i)) & 1u ? gq * wv[2 * i] : 0.f,
+                                            (mb[ci][kind] >> (2 * i + 1)) & 1u ? gq * wv[2 * i + 1] : 0.f);
+            *reinterpret_cast<uint4*>(static_cast<T*>(a.dZ[ci]) + ((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.ld + n) = o;
+          }
+        }
+        continue;
+      }
+      uint4 u[2][2];
+#pragma unroll
+      for (int ci = 0; ci < 2; ++ci)
+#pragma unroll
+        for (int kind = 0; kind < 2; ++kind)
+          if (kind == 0 || a.actor_rows)
+            u[ci][kind] = *reinterpret_cast<const uint4*>(static_cast<const T*>(a.A[ci]) +
+                                                          ((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.ld + n);
+#pragma unroll
+      for (int ci = 0; ci < 2; ++ci) {
+        const float4 w0 = *reinterpret_cast<const float4*>(a.w[ci] + n), w1 = *reinterpret_cast<const float4*>(a.w[ci] + n + 4);
+        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int kind = 0; kind < 2; ++kind) {
+          if (kind == 1 && !a.actor_rows) continue;
+          const float gq = gs[ci][kind][rr];
+          const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&u[ci][kind]);
+          uint4 o;
+          __nv_bfloat162* yv = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(x[i]);
+            yv[i] = __floats2bfloat162_rn(f.x > 0.f ? gq * wv[2 * i] : 0.f, f.y > 0.f ? gq * wv[2 * i + 1] : 0.f);
+          }
+          *reinterpret_cast<uint4*>(static_cast<T*>(a.dZ[ci]) + ((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.ld + n) = o;
+        }
+      }
+    } else {
+      for (int ci = 0; ci < 2; ++ci)
+        for (int kind = 0; kind < (a.actor_rows ? 2 : 1); ++kind) {
+          const int64_t row = (int64_t)(kind ? a.Bl : 0) + j0 + rr;
+          const float gq = gs[ci][kind][rr];
+          const T* A = static_cast<const T*>(a.A[ci]) + row * a.ld + n;
+          T* dZ = static_cast<T*>(a.dZ[ci]) + row * a.ld + n;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) dZ[i] = from_f<T>(to_f(A[i]) > 0.f ? gq * a.w[ci][n + i] : 0.f);
+        }
+    }
+  }
+  // the last block sums every block's partial (fixed order: strided per thread, then a fixed tree)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double t[NSTAT] = {0, 0, 0, 0, 0, 0};
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += LOSS_NT)
+#pragma unroll
+      for (int i = 0; i < NSTAT; ++i) t[i] += __ldcg(a.partials + b * NSTAT + i);
+#pragma unroll
+    for (int i = 0; i < NSTAT; ++i) t[i] = warp_sum(t[i]);
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < NSTAT; ++i) red[wi][i] = t[i];
+    __syncthreads();
+    if (threadIdx.x < NSTAT) {
+      double u = 0.0;
+      for (int k = 0; k < LOSS_NT / 32; ++k) u += red[k][threadIdx.x];
+      a.totals[threadIdx.x] = u;
+    }
+    if (threadIdx.x == 0) *a.ticket = 0u;
   }
 }
 
@@ -312,9 +407,10 @@ struct ColsumJob {
   float* out;
   int ld, N, M, f32;
 };
+constexpr int MAX_COLSUM_JOBS = 16;
 struct ColsumArgs {
   int n_jobs, rps;
-  ColsumJob j[12];
+  ColsumJob j[MAX_COLSUM_JOBS];
 };
 constexpr int CS_VEC = 8, CS_TX = 32, CS_TY = 8;
 
@@ -377,37 +473,21 @@ struct StatsOut {
   double step, critic_loss, actor_loss, alpha, alpha_loss, q1_mean, q2_mean, logp_mean;
 };
 
-__global__ void stats_kernel(const double* __restrict__ partials, int nblocks, const double* __restrict__ extra,
-                             const float* __restrict__ log_alpha, double target_entropy, double B, int td3,
-                             const int64_t* __restrict__ step_p, int delay, StatsOut* __restrict__ out,
-                             float* __restrict__ g_log_alpha, int* __restrict__ flag) {
-  pdl_wait();
-  pdl_launch();
-  __shared__ double tot[NSTAT];
-  if (threadIdx.x < NSTAT) {
-    double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += partials[b * NSTAT + threadIdx.x];
-    if (extra) s = extra[threadIdx.x];  // multi-rank: already all-reduced totals
-    tot[threadIdx.x] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const double la = *log_alpha;
-    StatsOut o;
-    o.step = (double)(*step_p + 1);
-    o.critic_loss = tot[0] / B;
-    o.q1_mean = tot[1] / B;
-    o.q2_mean = tot[2] / B;
-    o.actor_loss = tot[3] / B;
-    o.logp_mean = td3 ? 0.0 : tot[4] / B;
-    o.alpha = td3 ? 0.0 : exp(la);
-    o.alpha_loss = td3 ? 0.0 : -la * (o.logp_mean + target_entropy);
-    *out = o;
-    if (g_log_alpha) *g_log_alpha = (float)(-(o.logp_mean + target_entropy));
-    const bool bad = !isfinite(o.critic_loss) || !isfinite(o.actor_loss) || !isfinite(o.q1_mean) ||
-                     !isfinite(o.q2_mean) || !isfinite(o.logp_mean);
-    if (bad) *flag = 1;
-  }
+// Statistics of the step from the loss totals (called by every Adam block; block 0 publishes).
+// Returns true if a loss is non-finite (the step must not be applied).
+__device__ __forceinline__ bool step_stats(const double* __restrict__ tot, double la, double target_entropy, double B,
+                                           int td3, int64_t step, StatsOut* o, float* g_log_alpha) {
+  o->step = (double)(step + 1);
+  o->critic_loss = tot[0] / B;
+  o->q1_mean = tot[1] / B;
+  o->q2_mean = tot[2] / B;
+  o->actor_loss = tot[3] / B;
+  o->logp_mean = td3 ? 0.0 : tot[4] / B;
+  o->alpha = td3 ? 0.0 : exp(la);
+  o->alpha_loss = td3 ? 0.0 : -la * (o->logp_mean + target_entropy);
+  *g_log_alpha = (float)(-(o->logp_mean + target_entropy));
+  return !isfinite(o->critic_loss) || !isfinite(o->actor_loss) || !isfinite(o->q1_mean) || !isfinite(o->q2_mean) ||
+         !isfinite(o->logp_mean);
 }
 
 // ------------------------------------------------------------------ a9: fused multi-tensor Adam + Polyak
@@ -428,6 +508,7 @@ struct AdamTensor {
   int64_t s_off;      // shadow offset (elements) of element 0, -1 if none
   int64_t t_off;      // target master offset, -1 if none
   int64_t ts_off;     // target shadow offset, -1 if none
+  int64_t red_off;    // offset of this tensor in the contiguous (all-reduced) gradient buffer
 };
 struct AdamSegment {
   int32_t tensor;
@@ -438,6 +519,13 @@ struct AdamHyper {
   float lr[3];
   float beta1, beta2, eps, tau;
   int td3, delay;
+  // statistics + counter advance folded into this kernel
+  const double* totals;  // loss totals of the step (this rank's, or the group's after the allreduce)
+  const float* log_alpha;
+  StatsOut* stats;
+  double target_entropy, B;
+  unsigned* ticket;
+  int alpha_auto, critic_on, actor_on;
 };
 
 template <typename T>
@@ -445,68 +533,102 @@ __global__ void __launch_bounds__(256) adam_polyak_kernel(const AdamTensor* __re
                                                           const AdamSegment* __restrict__ segs, AdamHyper hp,
                                                           float* __restrict__ P, float* __restrict__ Mo,
                                                           float* __restrict__ Vo, T* __restrict__ S,
-                                                          const int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
+                                                          int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
                                                           int* __restrict__ flag) {
   pdl_wait();
   pdl_launch();
-  if (*flag) return;  // halted: parameters stay at the state before the failing step
+  __shared__ float g_alpha;
+  __shared__ bool skip, last;
+  const int64_t step = counters[0];
+  if (threadIdx.x == 0) {
+    // statistics of the step from the loss totals (identical in every block); block 0 publishes them
+    StatsOut o;
+    float ga;
+    const bool bad = step_stats(hp.totals, (double)*hp.log_alpha, hp.target_entropy, hp.B, hp.td3, step, &o, &ga);
+    if (bad) atomicExch(flag, 1);
+    if (blockIdx.x == 0) *hp.stats = o;
+    g_alpha = ga;
+    skip = bad || *flag;  // halted: parameters stay at the state before the failing step
+  }
+  __syncthreads();
   const AdamSegment sg = segs[blockIdx.x];
   const AdamTensor tn = tensors[sg.tensor];
-  const int64_t step = counters[0];
   bool delayed = true;
   if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
-  if (hp.td3 && tn.opt == 1 && !delayed) return;  // TD3 actor: only on delayed steps
-  const int64_t t = counters[1 + tn.opt] + 1;
-  const float bc1 = (float)(1.0 - pow((double)hp.beta1, (double)t));
-  const float bc2 = (float)(1.0 - pow((double)hp.beta2, (double)t));
-  const float lr = hp.lr[tn.opt];
-  const bool do_polyak = tn.t_off >= 0 && (!hp.td3 || delayed);
+  const bool active = !skip && !(hp.td3 && tn.opt == 1 && !delayed);  // TD3 actor: delayed steps only
+  if (active) {
+    const int64_t t = counters[1 + tn.opt] + 1;
+    const float bc1 = (float)(1.0 - pow((double)hp.beta1, (double)t));
+    const float bc2 = (float)(1.0 - pow((double)hp.beta2, (double)t));
+    const float lr = hp.lr[tn.opt];
+    const bool do_polyak = tn.t_off >= 0 && (!hp.td3 || delayed);
+    for (int k = threadIdx.x; k < sg.count; k += blockDim.x) {
+      const int64_t i = sg.start + k;
+      float g = 0.f;
+      if (tn.opt == 2) {
+        g = g_alpha;  // log-alpha gradient -(mean log pi~ + H_bar) from the (group) totals
+      } else {
+#pragma unroll 8
+        for (int s = 0; s < tn.n_partials; ++s) g += __ldg(tn.partials + (int64_t)s * tn.numel + i);
+      }
+      if (!isfinite(g)) {
+        atomicExch(flag, 2);
+        continue;
+      }
+      const int64_t pi = tn.p_off + i;
+      const float m = hp.beta1 * Mo[pi] + (1.f - hp.beta1) * g;
+      const float v = hp.beta2 * Vo[pi] + (1.f - hp.beta2) * g * g;
+      Mo[pi] = m;
+      Vo[pi] = v;
+      const float p = P[pi] - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
+      P[pi] = p;
+      int64_t so = -1;
+      if (tn.cols > 0) {
+        const int64_t row = i / tn.cols, col = i - row * tn.cols;
+        so = row * tn.ld + col;
+        S[tn.s_off + so] = from_f<T>(p);
+      }
+      if (do_polyak) {
+        const int64_t ti = tn.t_off + i;
+        const float tp = hp.tau * p + (1.f - hp.tau) * P[ti];
+        P[ti] = tp;
+        if (so >= 0) S[tn.ts_off + so] = from_f<T>(tp);
+      }
+    }
+  }
+  // the last block to finish advances the step and optimizer counters
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(hp.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    *hp.ticket = 0u;
+    if (!atomicAdd(flag, 0)) {
+      if (hp.critic_on) counters[1] += 1;
+      if (hp.actor_on && delayed) counters[2] += 1;
+      if (hp.actor_on && hp.alpha_auto && !hp.td3) counters[3] += 1;
+      counters[0] = step + 1;
+    }
+  }
+}
+// Row-sharded learners: sum each tensor's split partials (fixed order) into the contiguous
+// gradient buffer that is then all-reduced across the group.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const AdamTensor* __restrict__ tensors,
+                                                              const AdamSegment* __restrict__ segs, float* __restrict__ Gred) {
+  pdl_wait();
+  pdl_launch();
+  const AdamSegment sg = segs[blockIdx.x];
+  const AdamTensor tn = tensors[sg.tensor];
   for (int k = threadIdx.x; k < sg.count; k += blockDim.x) {
     const int64_t i = sg.start + k;
     float g = 0.f;
 #pragma unroll 8
     for (int s = 0; s < tn.n_partials; ++s) g += __ldg(tn.partials + (int64_t)s * tn.numel + i);
-    if (!isfinite(g)) {
-      atomicExch(flag, 2);
-      continue;
-    }
-    const int64_t pi = tn.p_off + i;
-    const float m = hp.beta1 * Mo[pi] + (1.f - hp.beta1) * g;
-    const float v = hp.beta2 * Vo[pi] + (1.f - hp.beta2) * g * g;
-    Mo[pi] = m;
-    Vo[pi] = v;
-    const float p = P[pi] - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
-    P[pi] = p;
-    int64_t so = -1;
-    if (tn.cols > 0) {
-      const int64_t row = i / tn.cols, col = i - row * tn.cols;
-      so = row * tn.ld + col;
-      S[tn.s_off + so] = from_f<T>(p);
-    }
-    if (do_polyak) {
-      const int64_t ti = tn.t_off + i;
-      const float tp = hp.tau * p + (1.f - hp.tau) * P[ti];
-      P[ti] = tp;
-      if (so >= 0) S[tn.ts_off + so] = from_f<T>(tp);
-    }
+    Gred[tn.red_off + i] = g;
   }
-}
-
-// Target-only Polyak for tensors without an optimizer on this rank (TD3 target actor
-// when the actor lives elsewhere is not needed in co-located mode) -- unused for now.
-
-// Advance the step and optimizer counters (after every kernel of the step has run).
-__global__ void advance_kernel(int64_t* __restrict__ counters, const int* __restrict__ flag, int td3, int delay,
-                               int alpha_auto, int critic_on, int actor_on) {
-  pdl_wait();
-  pdl_launch();
-  if (*flag) return;
-  const int64_t step = counters[0];
-  const bool delayed = !td3 || ((step + 1) % delay) == 0;
-  if (critic_on) counters[1] += 1;
-  if (actor_on && delayed) counters[2] += 1;
-  if (actor_on && alpha_auto && !td3) counters[3] += 1;
-  counters[0] = step + 1;
 }
 
 // ------------------------------------------------------------------ shadow refresh + init

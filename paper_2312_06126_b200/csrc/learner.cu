@@ -12,6 +12,7 @@
 #include <functional>
 #include <memory>
 
+#include "comm.h"
 #include "gemm.cuh"
 #include "internal.h"
 #include "kernels.cuh"
@@ -101,6 +102,9 @@ struct spz_learner {
   void* Aon[2][8] = {};
   void* Atg[2][8] = {};
   void* dZc[2][8] = {};
+  uint32_t* mask_a[8] = {};     // packed ReLU masks of the actor hidden layers [2B x mw]
+  uint32_t* mask_c[2][8] = {};  // ... and of the online critics' hidden layers
+  int mw = 0;                   // mask words per row
   float* H = nullptr;
   float *q_on[2] = {}, *q_tg[2] = {}, *gq[2] = {}, *dXc[2] = {};
   float *logp = nullptr, *logp2 = nullptr, *r = nullptr, *d = nullptr, *y = nullptr;
@@ -115,6 +119,11 @@ struct spz_learner {
   int max_tensors = 64, max_segs = 0;
   ShadowEntry* d_shadow = nullptr;
   int n_shadow = 0;
+  // row-sharded group (world_size > 1)
+  Comm comm;
+  float* Gred = nullptr;     // contiguous gradients of every trained tensor (+ log alpha slot)
+  int64_t Gred_total = 0;
+  double* statsum = nullptr;  // this rank's (then the group's) loss statistic totals
 
   // plan
   int64_t plan_B = -1;
@@ -122,6 +131,7 @@ struct spz_learner {
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   int n_adam_segs = 0;
   uint64_t sync_version = 0;
+  unsigned* tickets = nullptr;  // last-block counters of the loss and Adam kernels
   std::vector<void*> allocs;
   struct DebugBuf { std::string name; void* ptr; size_t bytes; int esz; };
   std::vector<DebugBuf> debug;
@@ -204,6 +214,7 @@ spz_learner::~spz_learner() {
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   if (own_stream) cudaStreamSynchronize(own_stream);
+  comm_destroy(&comm);
   for (auto& e : exec)
     if (e) cudaGraphExecDestroy(e);
   for (void* p : allocs) cudaFree(p);
@@ -255,6 +266,8 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
   for (int variant = 0; variant < (td3 ? 2 : 1); ++variant) {
     std::vector<Op>& ops = Lr->ops[variant];
     const bool actor_step = !td3 || variant == 1;  // TD3: actor work only on delayed steps
+    std::vector<GemmGroup> wgrads;
+    std::vector<ColsumJob> colsums;
     auto gemm = [&](const char* cls, GemmArgs a) {
       ops.push_back({cls, [a](cudaStream_t st) { return run_gemm<T>(a, st); }});
     };
@@ -286,8 +299,10 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       a.N = std::max(a.N, N);
       return g;
     };
-    // fused epilogues (row dot, actor heads) exist only in the tcgen05 kernel
+    // fused epilogues (row dot, actor heads, packed ReLU masks) exist only in the tcgen05 kernel
     auto tc_ok = [&](const GemmArgs& a) { return std::is_same<T, __nv_bfloat16>::value && tc_gemm_supported(a); };
+    const bool bits = std::is_same<T, __nv_bfloat16>::value && tc_gemm_available();
+    const int mw = Lr->mw;
     HeadEpi he{};
     he.m = m;
     he.o = o;
@@ -339,9 +354,15 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       }
       for (int l = 0; l < L; ++l) {
         GemmArgs a = mk(an.in[l], EPI_BIAS_RELU, 0, 0);
-        for (const Pass& ps : passes)
-          add(a, l == 0 ? (const void*)Ta(Lr->Xa, ps.row, lda) : (const void*)Ta(Lr->Aact[l - 1], ps.row, h),
-              l == 0 ? lda : h, Wp(ps.id, l), ldw(ps.id, l), Ta(Lr->Aact[l], ps.row, h), h, ps.M, h, bp(ps.id, l));
+        for (const Pass& ps : passes) {
+          GemmGroup& g = add(a, l == 0 ? (const void*)Ta(Lr->Xa, ps.row, lda) : (const void*)Ta(Lr->Aact[l - 1], ps.row, h),
+                             l == 0 ? lda : h, Wp(ps.id, l), ldw(ps.id, l), Ta(Lr->Aact[l], ps.row, h), h, ps.M, h, bp(ps.id, l));
+          if (bits && ps.id == NET_ACTOR) {
+            g.mask_out = Lr->mask_a[l] + ps.row * mw;
+            g.mask_ld = mw;
+          }
+        }
+        if (bits && !tc_ok(a)) return fail(SPZ_EUNSUPPORTED, "internal: actor forward not supported by the tcgen05 kernel");
         gemm("actor_fwd_gemm", a);
       }
       // head layer: fused squashed-Gaussian (SAC) / tanh + smoothing (TD3) epilogue when possible
@@ -383,6 +404,10 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
             const void* src = l == 0 ? (const void*)Ta(Lr->Xc, tgt ? 2 * Bl : 0, ldc)
                                      : (const void*)(tgt ? Lr->Atg[i][l - 1] : Lr->Aon[i][l - 1]);
             GemmGroup& g = add(a, src, l == 0 ? ldc : h, Wp(id, l), cn.ld[l], dst, h, tgt ? Bl : Mon, h, bp(id, l));
+            if (bits && !tgt) {
+              g.mask_out = Lr->mask_c[i][l];
+              g.mask_ld = mw;
+            }
             if (l == L - 1) {
               g.dot_w = P + Lr->pbase[id] + Lr->net[id].w[L];
               g.dot_b = bp(id, L);
@@ -390,6 +415,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
             }
           }
         }
+        if (bits && !tc_ok(a) && l < L - 1) return fail(SPZ_EUNSUPPORTED, "internal: critic forward not supported by the tcgen05 kernel");
         if (l == L - 1 && !tc_ok(a)) {
           for (int i = 0; i < a.n_groups; ++i) a.g[i].dot_out = nullptr;
           gemm("critic_fwd_gemm", a);
@@ -416,44 +442,55 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         }
       }
     }
-    // ---- a4/a5: Bellman target, losses, head gradients, stat partials
-    const int nblk = (int)cdiv(Bl, LOSS_NT);
+    // ---- a4/a5: Bellman target, losses, head gradients, this rank's loss totals; a6 head backward
+    const int nblk = (int)cdiv(Bl, LOSS_ROWS);
     {
-      const float gamma = (float)Lr->cfg.gamma;
-      float *qt1 = Lr->q_tg[0], *qt2 = Lr->q_tg[1], *q1 = Lr->q_on[0], *q2 = Lr->q_on[1];
-      float *lp = Lr->logp, *lp2 = Lr->logp2, *rr = Lr->r, *dd = Lr->d, *g1 = Lr->gq[0], *g2 = Lr->gq[1], *yy = Lr->y;
-      const float* la = P + Lr->p_log_alpha;
-      double* part = Lr->stat_partials;
-      const int64_t* stp = Lr->counters;
-      const int t3 = td3;
-      ops.push_back({"critic_loss", [=](cudaStream_t st) {
-                       launch_pdl(critic_loss_kernel, dim3(nblk), dim3(LOSS_NT), 0, st, qt1, qt2, q1, q2, lp2, lp, rr, dd, la, gamma, invB,
-                                                                   Bl, t3, stp, delay, g1, g2, yy, part);
-                       return cudaGetLastError();
+      LossArgs la{};
+      la.qt1 = Lr->q_tg[0];
+      la.qt2 = Lr->q_tg[1];
+      la.q1 = Lr->q_on[0];
+      la.q2 = Lr->q_on[1];
+      la.logp2 = Lr->logp2;
+      la.logp = Lr->logp;
+      la.r = Lr->r;
+      la.d = Lr->d;
+      la.log_alpha = P + Lr->p_log_alpha;
+      la.step_p = Lr->counters;
+      la.gq1 = Lr->gq[0];
+      la.gq2 = Lr->gq[1];
+      la.y = Lr->y;
+      la.partials = Lr->stat_partials;
+      la.totals = Lr->statsum;
+      la.ticket = Lr->tickets;
+      la.mask_ld = mw;
+      for (int i = 0; i < 2; ++i) {
+        la.mask[i] = bits ? Lr->mask_c[i][L - 1] : nullptr;
+        la.A[i] = Lr->Aon[i][L - 1];
+        la.w[i] = P + Lr->pbase[NET_Q1 + i] + cn.w[L];
+        la.dZ[i] = Lr->dZc[i][L - 1];
+      }
+      la.gamma = (float)Lr->cfg.gamma;
+      la.invB = invB;
+      la.Bl = Bl;
+      la.td3 = td3;
+      la.delay = delay;
+      la.actor_rows = actor_step;
+      la.h = h;
+      la.ld = h;
+      ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
+                       return launch_pdl(critic_loss_kernel<T>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
                      }});
     }
     // ---- a6: critic backward
     {
-      HeadBwdArgs hb{};
-      hb.M = Mon;
-      hb.h = h;
-      hb.ld = h;
-      for (int i = 0; i < 2; ++i) {
-        hb.g[i].gq = Lr->gq[i];
-        hb.g[i].w = P + Lr->pbase[NET_Q1 + i] + cn.w[L];
-        hb.g[i].A = Lr->Aon[i][L - 1];
-        hb.g[i].dZ = Lr->dZc[i][L - 1];
-      }
-      const int64_t tot = (int64_t)Mon * h;
-      ops.push_back({"critic_head_bwd", [hb, tot](cudaStream_t st) {
-                       launch_pdl(critic_head_bwd_kernel<T>, dim3(dim3((unsigned)std::min<int64_t>(cdiv(tot / 8, 256), 148 * 16), 2)), dim3(256), 0, st, hb);
-                       return cudaGetLastError();
-                     }});
       // dgrad through hidden layers l = L-1 .. 1 (all Mon rows)
       for (int l = L - 1; l >= 1; --l) {
-        GemmArgs a = mk(h, EPI_MASK, 0, 1);
-        for (int i = 0; i < 2; ++i)
-          add(a, Lr->dZc[i][l], h, Wp(NET_Q1 + i, l), cn.ld[l], Lr->dZc[i][l - 1], h, Mon, h, nullptr, Lr->Aon[i][l - 1], h);
+        GemmArgs a = mk(h, bits ? EPI_MASK_BITS : EPI_MASK, 0, 1);
+        for (int i = 0; i < 2; ++i) {
+          if (bits) add(a, Lr->dZc[i][l], h, Wp(NET_Q1 + i, l), cn.ld[l], Lr->dZc[i][l - 1], h, Mon, h, nullptr, Lr->mask_c[i][l - 1], mw);
+          else add(a, Lr->dZc[i][l], h, Wp(NET_Q1 + i, l), cn.ld[l], Lr->dZc[i][l - 1], h, Mon, h, nullptr, Lr->Aon[i][l - 1], h);
+        }
+        if (bits && !tc_ok(a)) return fail(SPZ_EUNSUPPORTED, "internal: critic dgrad not supported by the tcgen05 kernel");
         gemm("critic_dgrad_gemm", a);
       }
       // input dgrad for the actor rows (only the action columns are consumed)
@@ -463,38 +500,26 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           add(a, Ta(Lr->dZc[i][0], Bl, h), h, Wp(NET_Q1 + i, 0), cn.ld[0], Lr->dXc[i], ldc, Bl, o + m);
         gemm("critic_input_dgrad_gemm", a);
       }
-      // wgrad on the Bl loss rows: dW_l = dZ_l^T A_{l-1}; split-K over the batch; <= 4 tensors per launch
-      {
-        GemmArgs a = mk(Bl, EPI_F32, 1, 1);
-        a.splits = Sw;
-        a.k_per_split = (int)rows_w;
-        for (int i = 0; i < 2; ++i)
-          for (int l = 0; l < L; ++l) {
-            if (a.n_groups == 4) {
-              gemm("critic_wgrad_gemm", a);
-              a.n_groups = 0;
-              a.N = 0;
-            }
-            GemmGroup& g = add(a, Lr->dZc[i][l], h, l == 0 ? Lr->Xc : Lr->Aon[i][l - 1], l == 0 ? ldc : h,
-                               Lr->G + slot_of(NET_Q1 + i, l, true).g_off, cn.in[l], h, cn.in[l]);
-            g.split_stride = (int64_t)h * cn.in[l];
-          }
-        if (a.n_groups) gemm("critic_wgrad_gemm", a);
-      }
-      // bias gradients (column sums of dZ over loss rows) and the N = 1 head, one launch
-      {
-        ColsumArgs ca{};
-        ca.rps = (int)rows_b;
-        for (int i = 0; i < 2; ++i) {
-          for (int l = 0; l < L; ++l)
-            ca.j[ca.n_jobs++] = {Lr->dZc[i][l], nullptr, Lr->G + slot_of(NET_Q1 + i, l, false).g_off, h, h, Bl, 0};
-          ca.j[ca.n_jobs++] = {Lr->Aon[i][L - 1], Lr->gq[i], Lr->G + slot_of(NET_Q1 + i, L, true).g_off, h, h, Bl, 0};
-          ca.j[ca.n_jobs++] = {Lr->gq[i], nullptr, Lr->G + slot_of(NET_Q1 + i, L, false).g_off, 1, 1, Bl, 1};
+      // wgrad (B loss rows) and bias column sums are collected and launched with the actor's below
+      for (int i = 0; i < 2; ++i)
+        for (int l = 0; l < L; ++l) {
+          GemmGroup g{};
+          g.A = Lr->dZc[i][l];
+          g.lda = h;
+          g.B = l == 0 ? Lr->Xc : Lr->Aon[i][l - 1];
+          g.ldb = l == 0 ? ldc : h;
+          g.C = Lr->G + slot_of(NET_Q1 + i, l, true).g_off;
+          g.ldc = cn.in[l];
+          g.M = h;
+          g.N = cn.in[l];
+          g.split_stride = (int64_t)h * cn.in[l];
+          wgrads.push_back(g);
         }
-        ops.push_back({"critic_bias_grad", [ca, Sb](cudaStream_t st) {
-                         launch_pdl(colsum_multi_kernel<T>, dim3(dim3(Sb, ca.n_jobs)), dim3(CS_TX * CS_TY), 0, st, ca);
-                         return cudaGetLastError();
-                       }});
+      for (int i = 0; i < 2; ++i) {
+        for (int l = 0; l < L; ++l)
+          colsums.push_back({Lr->dZc[i][l], nullptr, Lr->G + slot_of(NET_Q1 + i, l, false).g_off, h, h, Bl, 0});
+        colsums.push_back({Lr->Aon[i][L - 1], Lr->gq[i], Lr->G + slot_of(NET_Q1 + i, L, true).g_off, h, h, Bl, 0});
+        colsums.push_back({Lr->gq[i], nullptr, Lr->G + slot_of(NET_Q1 + i, L, false).g_off, 1, 1, Bl, 1});
       }
     }
     // ---- a7: actor backward (s-rows Bl..2Bl of the actor activations)
@@ -522,58 +547,63 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       }
       // dgrad: dZ_{L-1} = (dH W_out) * 1[A_{L-1} > 0], then down the hidden stack
       for (int l = L; l >= 1; --l) {
-        GemmArgs a = mk(an.out[l], EPI_MASK, 0, 1);
-        add(a, l == L ? (const void*)dH : (const void*)Lr->dZa[l], l == L ? ldh : h, Wp(NET_ACTOR, l), an.ld[l],
-            Lr->dZa[l - 1], h, Bl, h, nullptr, Ta(Lr->Aact[l - 1], Bl, h), h);
+        GemmArgs a = mk(an.out[l], bits ? EPI_MASK_BITS : EPI_MASK, 0, 1);
+        if (bits)
+          add(a, l == L ? (const void*)dH : (const void*)Lr->dZa[l], l == L ? ldh : h, Wp(NET_ACTOR, l), an.ld[l],
+              Lr->dZa[l - 1], h, Bl, h, nullptr, Lr->mask_a[l - 1] + (int64_t)Bl * mw, mw);
+        else
+          add(a, l == L ? (const void*)dH : (const void*)Lr->dZa[l], l == L ? ldh : h, Wp(NET_ACTOR, l), an.ld[l],
+              Lr->dZa[l - 1], h, Bl, h, nullptr, Ta(Lr->Aact[l - 1], Bl, h), h);
+        if (bits && !tc_ok(a)) return fail(SPZ_EUNSUPPORTED, "internal: actor dgrad not supported by the tcgen05 kernel");
         gemm("actor_dgrad_gemm", a);
       }
-      // wgrad: dW_l = dZ_l^T A_{l-1} over the Bl s-rows (dZ_L = dH); all layers in one launch (<= 4)
-      {
-        GemmArgs a = mk(Bl, EPI_F32, 1, 1);
-        a.splits = Sw;
-        a.k_per_split = (int)rows_w;
-        for (int l = 0; l <= L; ++l) {
-          if (a.n_groups == 4) {
-            gemm("actor_wgrad_gemm", a);
-            a.n_groups = 0;
-            a.N = 0;
-          }
-          GemmGroup& g = add(a, l == L ? (const void*)dH : (const void*)Lr->dZa[l], l == L ? ldh : h,
-                             l == 0 ? (const void*)Ta(Lr->Xa, Bl, lda) : (const void*)Ta(Lr->Aact[l - 1], Bl, h),
-                             l == 0 ? lda : h, Lr->G + slot_of(NET_ACTOR, l, true).g_off, an.in[l], an.out[l], an.in[l]);
-          g.split_stride = (int64_t)an.out[l] * an.in[l];
-        }
-        if (a.n_groups) gemm("actor_wgrad_gemm", a);
+      // wgrad: dW_l = dZ_l^T A_{l-1} over the Bl s-rows (dZ_L = dH)
+      for (int l = 0; l <= L; ++l) {
+        GemmGroup g{};
+        g.A = l == L ? (const void*)dH : (const void*)Lr->dZa[l];
+        g.lda = l == L ? ldh : h;
+        g.B = l == 0 ? (const void*)Ta(Lr->Xa, Bl, lda) : (const void*)Ta(Lr->Aact[l - 1], Bl, h);
+        g.ldb = l == 0 ? lda : h;
+        g.C = Lr->G + slot_of(NET_ACTOR, l, true).g_off;
+        g.ldc = an.in[l];
+        g.M = an.out[l];
+        g.N = an.in[l];
+        g.split_stride = (int64_t)an.out[l] * an.in[l];
+        wgrads.push_back(g);
       }
-      {
-        ColsumArgs ca{};
-        ca.rps = (int)rows_b;
-        for (int l = 0; l <= L; ++l)
-          ca.j[ca.n_jobs++] = {l == L ? (const void*)dH : (const void*)Lr->dZa[l], nullptr,
-                               Lr->G + slot_of(NET_ACTOR, l, false).g_off, l == L ? ldh : h, an.out[l], Bl, 0};
-        ops.push_back({"actor_bias_grad", [ca, Sb](cudaStream_t st) {
-                         launch_pdl(colsum_multi_kernel<T>, dim3(dim3(Sb, ca.n_jobs)), dim3(CS_TX * CS_TY), 0, st, ca);
-                         return cudaGetLastError();
-                       }});
-      }
+      for (int l = 0; l <= L; ++l)
+        colsums.push_back({l == L ? (const void*)dH : (const void*)Lr->dZa[l], nullptr,
+                           Lr->G + slot_of(NET_ACTOR, l, false).g_off, l == L ? ldh : h, an.out[l], Bl, 0});
       (void)nout;
     }
-    // ---- statistics, log-alpha gradient, non-finite flag
+    // ---- every weight gradient (split-K over the batch, <= 8 tensors per launch) and every bias
+    //      gradient (one column-sum launch)
     {
-      double* part = Lr->stat_partials;
-      const float* la = P + Lr->p_log_alpha;
-      const double te = Lr->cfg.target_entropy;
-      const int t3 = td3;
-      const int64_t* stp = Lr->counters;
-      StatsOut* so = Lr->d_stats;
-      float* ga = Lr->G + Lr->G_total - 64;
-      int* fl = Lr->d_flag;
-      const double Bd = (double)B;
-      ops.push_back({"stats", [=](cudaStream_t st) {
-                       launch_pdl(stats_kernel, dim3(1), dim3(32), 0, st, part, nblk, nullptr, la, te, Bd, t3, stp, delay, so, ga, fl);
-                       return cudaGetLastError();
-                     }});
+      GemmArgs a = mk(Bl, EPI_F32, 1, 1);
+      a.splits = Sw;
+      a.k_per_split = (int)rows_w;
+      for (const GemmGroup& g : wgrads) {
+        if (a.n_groups == MAX_GROUPS) {
+          gemm("wgrad_gemm", a);
+          a.n_groups = 0;
+          a.N = 0;
+        }
+        a.g[a.n_groups++] = g;
+        a.N = std::max(a.N, g.N);
+      }
+      if (a.n_groups) gemm("wgrad_gemm", a);
+      for (size_t c0 = 0; c0 < colsums.size(); c0 += MAX_COLSUM_JOBS) {
+        ColsumArgs ca{};
+        ca.rps = (int)rows_b;
+        for (size_t c = c0; c < colsums.size() && c < c0 + MAX_COLSUM_JOBS; ++c) ca.j[ca.n_jobs++] = colsums[c];
+        ops.push_back({"bias_grad", [ca, Sb](cudaStream_t st) {
+                         return launch_pdl(colsum_multi_kernel<T>, dim3(Sb, ca.n_jobs), dim3(CS_TX * CS_TY), 0, st, ca);
+                       }});
+      }
     }
+    // row-sharded groups reduce their split partials into one contiguous buffer and all-reduce it
+    // together with the loss totals before the (identical) optimizer step on every rank
+    const bool sharded = Lr->cfg.world_size > 1;
     // ---- a9: fused Adam + Polyak (+ shadow refresh) over every trained tensor
     {
       std::vector<AdamTensor> tens;
@@ -609,14 +639,54 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         tens.push_back(t);
         segs.push_back({(int)tens.size() - 1, 1, 0});
       }
-      if ((int)tens.size() > Lr->max_tensors || (int)segs.size() > Lr->max_segs)
+      // red_off: position of each tensor in the contiguous gradient buffer (sharded mode)
+      {
+        int64_t off = 0;
+        for (auto& t : tens) {
+          t.red_off = off;
+          off += round_up(t.numel, 16);
+        }
+      }
+      const int nten = (int)tens.size(), nsegs = (int)segs.size();
+      if (4 * (nten + 1) > Lr->max_tensors || 4 * (nsegs + 1) > Lr->max_segs)
         return fail(SPZ_EINVAL, "internal: Adam table overflow");
       const size_t tb = tens.size() * sizeof(AdamTensor), sb = segs.size() * sizeof(AdamSegment);
-      AdamTensor* dt = Lr->d_tensors + (variant ? Lr->max_tensors / 2 : 0);
-      AdamSegment* ds = Lr->d_segs + (variant ? Lr->max_segs / 2 : 0);
-      SPZ_CUDA_TRY(cudaMemcpyAsync(dt, tens.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
-      SPZ_CUDA_TRY(cudaMemcpyAsync(ds, segs.data(), sb, cudaMemcpyHostToDevice, Lr->stream));
-      SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+      AdamTensor* dt = Lr->d_tensors + variant * (Lr->max_tensors / 4);
+      AdamSegment* ds = Lr->d_segs + variant * (Lr->max_segs / 4);
+      if (sharded) {
+        // table 1 (partials -> Gred) is `tens`; table 2 (Gred -> Adam) replaces the partial sources
+        AdamTensor* dt2 = Lr->d_tensors + (2 + variant) * (Lr->max_tensors / 4);
+        std::vector<AdamTensor> tens2 = tens;
+        for (auto& t : tens2) {
+          if (t.opt == 2) continue;  // log alpha: gradient computed from the all-reduced totals
+          t.partials = Lr->Gred + t.red_off;
+          t.n_partials = 1;
+        }
+        SPZ_CUDA_TRY(cudaMemcpyAsync(dt2, tens2.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
+        SPZ_CUDA_TRY(cudaMemcpyAsync(dt, tens.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
+        SPZ_CUDA_TRY(cudaMemcpyAsync(ds, segs.data(), sb, cudaMemcpyHostToDevice, Lr->stream));
+        SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+        float* Gr = Lr->Gred;
+        const unsigned nsg = (unsigned)segs.size();
+        ops.push_back({"grad_reduce", [=](cudaStream_t st) {
+                         return launch_pdl(reduce_partials_kernel, dim3(nsg), dim3(256), 0, st, dt, ds, Gr);
+                       }});
+        if (Lr->cfg.comm_mode == 0) {
+          const Comm cm = Lr->comm;
+          const size_t n = (size_t)Lr->Gred_total;
+          double* ss = Lr->statsum;
+          ops.push_back({"allreduce", [=](cudaStream_t st) {
+                           cudaError_t e = comm_allreduce_sum(cm, Gr, n, false, st);
+                           if (e != cudaSuccess) return e;
+                           return comm_allreduce_sum(cm, ss, NSTAT, true, st);
+                         }, 0});
+        }
+        dt = dt2;
+      } else {
+        SPZ_CUDA_TRY(cudaMemcpyAsync(dt, tens.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
+        SPZ_CUDA_TRY(cudaMemcpyAsync(ds, segs.data(), sb, cudaMemcpyHostToDevice, Lr->stream));
+        SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+      }
       AdamHyper hp{};
       hp.lr[0] = (float)Lr->cfg.lr_critic;
       hp.lr[1] = (float)Lr->cfg.lr_actor;
@@ -627,19 +697,21 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       hp.tau = (float)Lr->cfg.tau;
       hp.td3 = td3;
       hp.delay = delay;
+      hp.totals = Lr->statsum;
+      hp.log_alpha = P + Lr->p_log_alpha;
+      hp.stats = Lr->d_stats;
+      hp.target_entropy = Lr->cfg.target_entropy;
+      hp.B = (double)B;
+      hp.ticket = Lr->tickets + 1;
+      hp.alpha_auto = Lr->cfg.alpha_auto;
+      hp.critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
+      hp.actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC;
       float *Pm = Lr->P, *Mm = Lr->Mo, *Vm = Lr->Vo;
       int64_t* ctr = Lr->counters;
       int* fl = Lr->d_flag;
       const unsigned nseg = (unsigned)segs.size();
       ops.push_back({"adam_polyak", [=](cudaStream_t st) {
-                       launch_pdl(adam_polyak_kernel<T>, dim3(nseg), dim3(256), 0, st, dt, ds, hp, Pm, Mm, Vm, S, ctr, fl);
-                       return cudaGetLastError();
-                     }});
-      const int t3 = td3, aa = Lr->cfg.alpha_auto;
-      const int con = Lr->cfg.role != SPZ_ROLE_ACTOR, aon = Lr->cfg.role != SPZ_ROLE_CRITIC;
-      ops.push_back({"advance", [=](cudaStream_t st) {
-                       launch_pdl(advance_kernel, dim3(1), dim3(1), 0, st, ctr, fl, t3, delay, aa, con, aon);
-                       return cudaGetLastError();
+                       return launch_pdl(adam_polyak_kernel<T>, dim3(nseg), dim3(256), 0, st, dt, ds, hp, Pm, Mm, Vm, S, ctr, fl);
                      }});
     }
   }
@@ -777,7 +849,8 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   if (cfg->max_batch < 1) return fail(SPZ_EINVAL, "spz_learner_create: max_batch must be >= 1");
   if (cfg->act_dim > 32) return fail(SPZ_EINVAL, "spz_learner_create: act_dim must be <= 32");
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return fail(SPZ_EINVAL, "spz_learner_create: bad rank/world_size");
-  if (cfg->world_size > 1) return fail(SPZ_EUNSUPPORTED, "spz_learner_create: multi-rank learners are not built yet");
+  if (cfg->world_size > 1 && cfg->comm_mode == 0 && !cfg->nccl_unique_id)
+    return fail(SPZ_EINVAL, "spz_learner_create: world_size > 1 needs nccl_unique_id (or comm_mode = 1)");
   if (cfg->role != SPZ_ROLE_ALL) return fail(SPZ_EUNSUPPORTED, "spz_learner_create: split roles are not built yet");
   if (cfg->algo != SPZ_SAC && cfg->algo != SPZ_TD3) return fail(SPZ_EINVAL, "spz_learner_create: unknown algo");
   if (cfg->precision != SPZ_FP32 && cfg->precision != SPZ_BF16) return fail(SPZ_EINVAL, "spz_learner_create: unknown precision");
@@ -840,7 +913,10 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   SPZ_TRY(dalloc(Lr.get(), &Lr->Xc, 3 * Bm * Lr->ldc * E));
   SPZ_TRY(dalloc(Lr.get(), &Lr->dH, Bm * Lr->ldh * E));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->H, 2 * Bm * Lr->ldh * sizeof(float)));
+  Lr->mw = (int)cdiv(h, 32);
   for (int l = 0; l < L; ++l) {
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->mask_a[l], 2 * Bm * Lr->mw * 4));
+    for (int i = 0; i < 2; ++i) SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->mask_c[i][l], 2 * Bm * Lr->mw * 4));
     SPZ_TRY(dalloc(Lr.get(), &Lr->Aact[l], 2 * Bm * h * E));
     SPZ_TRY(dalloc(Lr.get(), &Lr->dZa[l], Bm * h * E));
     for (int i = 0; i < 2; ++i) {
@@ -859,7 +935,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   for (float** f : {&Lr->cache.u, &Lr->cache.a, &Lr->cache.eps, &Lr->cache.sig, &Lr->cache.l})
     SPZ_TRY(dalloc(Lr.get(), (void**)f, Bm * m * sizeof(float)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->idx, Bm * sizeof(int32_t)));
-  Lr->max_stat_blocks = (int)cdiv(Bm, LOSS_NT);
+  Lr->max_stat_blocks = (int)cdiv(Bm, LOSS_ROWS);
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->stat_partials, (size_t)Lr->max_stat_blocks * NSTAT * sizeof(double)));
   {
     auto reg = [&](const std::string& n, void* p, size_t bytes, int es) { Lr->debug.push_back({n, p, bytes, es}); };
@@ -894,10 +970,25 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   // gradients and optimizer tables
   std::vector<TensorSlot> slots = trained_tensors(Lr.get());
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->G, Lr->G_total * sizeof(float)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->statsum, 8 * sizeof(double)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->tickets, 8 * sizeof(unsigned)));
+  Lr->debug.push_back({"statsum", Lr->statsum, 8 * sizeof(double), 8});
+  if (cfg->world_size > 1) {
+    int64_t tot = 0;
+    for (auto& t : slots) tot += round_up(t.numel, 16);
+    Lr->Gred_total = tot + 16;
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->Gred, Lr->Gred_total * sizeof(float)));
+    Lr->debug.push_back({"Gred", Lr->Gred, (size_t)Lr->Gred_total * 4, 4});
+    if (cfg->comm_mode == 0) {
+      SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+      spz_status cs = comm_init(&Lr->comm, cfg->nccl_unique_id, cfg->world_size, cfg->rank);
+      if (cs != SPZ_OK) return cs;
+    }
+  }
   int64_t nseg = 0;
   for (auto& t : slots) nseg += cdiv(t.numel, ADAM_SEG);
-  Lr->max_segs = (int)(2 * (nseg + 4));
-  Lr->max_tensors = 2 * ((int)slots.size() + 4);
+  Lr->max_segs = (int)(4 * (nseg + 4));
+  Lr->max_tensors = 4 * ((int)slots.size() + 4);
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_tensors, Lr->max_tensors * sizeof(AdamTensor)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_segs, Lr->max_segs * sizeof(AdamSegment)));
   // shadow table: every W of every net

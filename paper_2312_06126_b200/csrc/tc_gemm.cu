@@ -29,8 +29,8 @@ constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 struct TcParams {
   GemmArgs a;
   int stages;  // pipeline depth actually used (<= STAGES; short-K problems use fewer -> 2 CTAs/SM)
-  CUtensorMap ta[4];
-  CUtensorMap tb[4];
+  CUtensorMap ta[MAX_GROUPS];
+  CUtensorMap tb[MAX_GROUPS];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -114,16 +114,37 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // Epilogue of 16 consecutive accumulator columns n..n+15 of row m (bias / dot vectors staged
 // in shared memory for this column chunk).  Returns the chunk's contribution to the row dot.
 __device__ __forceinline__ float epi16(const GemmArgs& a, const GemmGroup& g, int split, int m, int n, const float (&v)[16],
-                                       const float* __restrict__ bias, const float* __restrict__ dotw) {
+                                       const float* __restrict__ bias, const float* __restrict__ dotw, uint32_t& bits) {
   const bool full = n + 16 <= g.N;
   const int64_t off = (int64_t)m * g.ldc + n;
   float dot = 0.f;
   switch (a.epi) {
+    case EPI_MASK_BITS: {
+      // bits: this chunk's 16 ReLU-mask bits (prefetched by the caller)
+      __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C);
+      if (full && (g.ldc & 7) == 0) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          pk[j] = pack_bf16((bits >> (2 * j)) & 1u ? v[2 * j] : 0.f, (bits >> (2 * j + 1)) & 1u ? v[2 * j + 1] : 0.f);
+        uint4* dst = reinterpret_cast<uint4*>(C + off);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      } else {
+        for (int j = 0; j < 16 && n + j < g.N; ++j) C[off + j] = __float2bfloat16_rn((bits >> j) & 1u ? v[j] : 0.f);
+      }
+      break;
+    }
     case EPI_BIAS_RELU: {
       __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C);
       float z[16];
+      bits = 0u;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) z[j] = fmaxf(v[j] + bias[j], 0.f);
+      for (int j = 0; j < 16; ++j) {
+        const float pre = v[j] + bias[j];
+        z[j] = fmaxf(pre, 0.f);
+        bits |= (pre > 0.f && n + j < g.N ? 1u : 0u) << j;
+      }
       if (dotw) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) dot = fmaf(z[j], dotw[j], dot);  // dotw is zero past g.N
@@ -198,6 +219,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   float* bias_s = reinterpret_cast<float*>(tmem_slot + 4);  // [BN] epilogue bias
   float* dot_s = bias_s + BN;                               // [BN] fused row-dot weights
+  uint32_t* mask_s = reinterpret_cast<uint32_t*>(dot_s + BN);  // [128][BN/32 + 1] packed ReLU masks
 
   const GemmArgs& a = p.a;
   const int gz = blockIdx.z;
@@ -318,6 +340,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       }
     } else {
       float dot = 0.f;
+      constexpr int NW = (BN + 31) / 32, MSTR = NW + 1;  // mask words per row, padded smem row stride
+      uint32_t* mrow = mask_s + (q * 32 + lane) * MSTR;     // this thread's row of packed ReLU-mask words
+      const bool mask_in = a.epi == EPI_MASK_BITS;
+      const bool mask_out = a.epi == EPI_BIAS_RELU && g.mask_out != nullptr;
+      if (mask_in) {  // prefetched before the accumulator wait
+        const uint32_t* src = static_cast<const uint32_t*>(g.aux) + (int64_t)m * g.ldaux + n0 / 32;
+        for (int i = 0; i < NW; ++i) mrow[i] = (m < g.M && n0 + 32 * i < g.N) ? src[i] : 0u;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN / 16; ++c) {
         const int n = n0 + c * 16;
@@ -329,9 +359,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = 0.f;
         }
-        if (m < g.M) dot += epi16(a, g, split, m, n, v, bias_s + c * 16, has_dot ? dot_s + c * 16 : nullptr);
+        uint32_t bits = mask_in ? (mrow[c >> 1] >> (16 * (c & 1))) & 0xFFFFu : 0u;
+        if (m < g.M) {
+          dot += epi16(a, g, split, m, n, v, bias_s + c * 16, has_dot ? dot_s + c * 16 : nullptr, bits);
+          if (mask_out) mrow[c >> 1] = (c & 1) ? (mrow[c >> 1] | (bits << 16)) : bits;
+        }
       }
       if (has_dot && m < g.M) g.dot_out[m] = dot + g.dot_b[0];
+      if (mask_out && m < g.M) {
+        // the row's mask words of this tile, written once (16-byte stores when aligned)
+        uint32_t* dst = g.mask_out + (int64_t)m * g.mask_ld + n0 / 32;
+        const int nw = min(NW, (g.N - n0 + 31) / 32);
+        if (nw == NW && (NW % 4) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          for (int i = 0; i < NW; i += 4) *reinterpret_cast<uint4*>(dst + i) = make_uint4(mrow[i], mrow[i + 1], mrow[i + 2], mrow[i + 3]);
+        } else {
+          for (int i = 0; i < nw; ++i) dst[i] = mrow[i];
+        }
+      }
     }
   }
   tc_fence_before();
@@ -373,7 +417,7 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 template <int BN, bool AMN, bool BMN>
 cudaError_t launch(TcParams& p, int maxM, cudaStream_t st) {
   constexpr int STAGE = A_BYTES + BN * BK * 2;
-  constexpr int SMEM_MAX = STAGES * STAGE + 1024 + 256 + BN * 8;
+  constexpr int SMEM_MAX = STAGES * STAGE + 1024 + 256 + BN * 8 + 128 * ((BN + 31) / 32 + 1) * 4;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
@@ -382,7 +426,7 @@ cudaError_t launch(TcParams& p, int maxM, cudaStream_t st) {
   }
   const int kspan = p.a.splits > 1 ? p.a.k_per_split : p.a.K;
   p.stages = (int)std::min<int64_t>(STAGES, std::max<int64_t>(1, cdiv(kspan, BK)));
-  const int smem = p.stages * STAGE + 1024 + 256 + BN * 8;
+  const int smem = p.stages * STAGE + 1024 + 256 + BN * 8 + 128 * ((BN + 31) / 32 + 1) * 4;
   dim3 grid((unsigned)cdiv(p.a.N, BN), (unsigned)cdiv(maxM, BM), (unsigned)(p.a.n_groups * p.a.splits));
   return launch_pdl(tc_gemm_kernel<BN, AMN, BMN>, grid, dim3(NTHREADS), (size_t)smem, st, p);
 }
@@ -409,8 +453,10 @@ int pick_bn(int N, bool bmn) {
 
 }  // namespace
 
+bool tc_gemm_available() { return get_encode(); }
+
 bool tc_gemm_supported(const GemmArgs& a) {
-  if (a.N < 1 || a.K < 1 || a.n_groups < 1 || a.n_groups > 4) return false;
+  if (a.N < 1 || a.K < 1 || a.n_groups < 1 || a.n_groups > MAX_GROUPS) return false;
   if (a.splits > 1 && (a.k_per_split % BK)) return false;
   if (a.a_mn && !a.b_mn) return false;  // layout combination not instantiated
   const int bn = pick_bn(a.N, a.b_mn);

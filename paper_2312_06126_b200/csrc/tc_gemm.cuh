@@ -7,6 +7,8 @@ namespace spz {
 
 // True if the tensor-core kernel handles this problem (layouts, alignment, sizes).
 bool tc_gemm_supported(const GemmArgs& a);
+// True if the tcgen05 path can run at all (driver entry point for tensor maps resolved).
+bool tc_gemm_available();
 // Launch it (bf16 operands, fp32 accumulation in TMEM, shared epilogues).
 cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st);
 

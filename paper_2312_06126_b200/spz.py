@@ -66,6 +66,7 @@ class spz_config(ctypes.Structure):
         ("role", ctypes.c_int),
         ("nccl_unique_id", ctypes.c_void_p),
         ("use_graph", ctypes.c_int32),
+        ("comm_mode", ctypes.c_int32),
     ]
 
 
@@ -184,6 +185,12 @@ def spz_replay_destroy(ring):
     lib().spz_replay_destroy(ring)
 
 
+def spz_nccl_unique_id():
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().spz_nccl_unique_id(buf))
+    return bytes(buf)
+
+
 def spz_config_default(algo, obs_dim, act_dim):
     c = spz_config()
     _check(lib().spz_config_default(algo, obs_dim, act_dim, ctypes.byref(c)))
@@ -258,6 +265,8 @@ def spz_learner_debug_buffer(learner, name):
         return raw.view(np.int32)
     if es.value == 2:
         return (raw.view(np.uint16).astype(np.uint32) << 16).view(np.float32)
+    if es.value == 8:
+        return raw.view(np.float64)
     return raw.view(np.float32)
 
 
@@ -308,6 +317,11 @@ class Learner:
         cfg.precision = SPZ_BF16 if precision == "bf16" else SPZ_FP32
         cfg.hidden, cfg.n_hidden, cfg.max_batch, cfg.device = hidden, n_hidden, max_batch, device
         cfg.use_graph = 1 if use_graph else 0
+        self._uid = None
+        if "nccl_unique_id" in overrides:
+            uid = overrides.pop("nccl_unique_id")
+            self._uid = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+            cfg.nccl_unique_id = ctypes.cast(self._uid, ctypes.c_void_p)
         for k, v in overrides.items():
             setattr(cfg, k, v)
         self.cfg = cfg

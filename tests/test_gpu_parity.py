@@ -229,5 +229,5 @@ def test_profile_and_launch_count():
     lrn = spz.Learner(g, precision="bf16", hidden=256, n_hidden=2, max_batch=8192)
     prof = lrn.profile(8192, 3)
     assert "gather" in prof and "adam_polyak" in prof and all(v > 0 for v in prof.values())
-    assert lrn.launches_per_step(8192) >= 20
+    assert lrn.launches_per_step(8192) >= 10
     assert lrn.counters()["step"] == 3

@@ -14,6 +14,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -23,12 +24,16 @@ namespace spz {
 
 namespace {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, NTHREADS = 192;
+constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int NUM_EPI_WARPS = 8, NTHREADS = 64 + NUM_EPI_WARPS * 32;  // producer, MMA, 8 epilogue warps
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
 struct TcParams {
   GemmArgs a;
-  int stages;  // pipeline depth actually used (<= STAGES; short-K problems use fewer -> 2 CTAs/SM)
+  int stages;       // pipeline depth actually used (<= STAGES)
+  int total_tiles;  // persistent schedule
+  int tile0[MAX_GROUPS + 1];
+  int mtiles[MAX_GROUPS], ntiles[MAX_GROUPS];
   CUtensorMap ta[MAX_GROUPS];
   CUtensorMap tb[MAX_GROUPS];
 };
@@ -203,11 +208,36 @@ __device__ __forceinline__ float epi16(const GemmArgs& a, const GemmGroup& g, in
   return dot;
 }
 
+// Linear tile index -> (group, m0, n0, split).  Tiles of group g occupy [tile0[g], tile0[g+1]);
+// within a group the M tile varies fastest, then the N tile, then the split.
+struct TileInfo {
+  int grp, m0, n0, split;
+};
+__device__ __forceinline__ TileInfo decode_tile(const TcParams& p, int t, int bn) {
+  int g = 0;
+  while (g + 1 < p.a.n_groups && t >= p.tile0[g + 1]) ++g;
+  const int r = t - p.tile0[g];
+  const int mt = r % p.mtiles[g];
+  const int rest = r / p.mtiles[g];
+  const int nt = rest % p.ntiles[g];
+  return {g, mt * BM, nt * bn, rest / p.ntiles[g]};
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NUM_EPI_WARPS * 32) : "memory"); }
+
+// Persistent, warp-specialized: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the TMA producer
+// and the MMA issuer run ahead into the next tile while the epilogue drains the previous one
+// from the other TMEM accumulator buffer.
 template <int BN, bool AMN, bool BMN>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN;
+  constexpr uint32_t ACC_COLS = BN < 32 ? 32 : BN;  // one accumulator buffer
+  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;       // double-buffered
+  constexpr int NW = (BN + 31) / 32, MSTR = NW + 1;
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) |
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -215,31 +245,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   const int NS = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * STAGE);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  float* bias_s = reinterpret_cast<float*>(tmem_slot + 4);  // [BN] epilogue bias
-  float* dot_s = bias_s + BN;                               // [BN] fused row-dot weights
-  uint32_t* mask_s = reinterpret_cast<uint32_t*>(dot_s + BN);  // [128][BN/32 + 1] packed ReLU masks
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* bias_s = reinterpret_cast<float*>(tmem_slot + 4);     // [BN] epilogue bias of the current tile
+  float* dot_s = bias_s + BN;                                  // [BN] fused row-dot weights
+  float* dotpart = dot_s + BN;                                 // [2][BM] row-dot halves
+  uint32_t* mask_s = reinterpret_cast<uint32_t*>(dotpart + 2 * BM);  // [BM][MSTR] packed ReLU masks
 
   const GemmArgs& a = p.a;
-  const int gz = blockIdx.z;
-  const int grp = gz / a.splits, split = gz % a.splits;
-  const GemmGroup& g = a.g[grp];
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  if (m0 >= g.M || n0 >= g.N) return;
-  const int k_begin = split * a.k_per_split;
-  const int k_end = min(a.K, k_begin + a.k_per_split);
-  const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = p.total_tiles;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&p.ta[grp]);
-    tma_prefetch(&p.tb[grp]);
+    for (int i = 0; i < a.n_groups; ++i) {
+      tma_prefetch(&p.ta[i]);
+      tma_prefetch(&p.tb[i]);
+    }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], NUM_EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -258,122 +288,168 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % NS;
-        const uint32_t ph = (uint32_t)(kb / NS) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        uint8_t* sA = smem + s * STAGE;
-        uint8_t* sB = sA + A_BYTES;
-        mbar_expect_tx(&full[s], STAGE);
-        const int k = k_begin + kb * BK;
-        if (!AMN) {
-          tma_load_2d(sA, &p.ta[grp], &full[s], k, m0);
-        } else {
-          tma_load_2d(sA, &p.ta[grp], &full[s], m0, k);
-          tma_load_2d(sA + 8192, &p.ta[grp], &full[s], m0 + 64, k);
-        }
-        if (!BMN) {
-          tma_load_2d(sB, &p.tb[grp], &full[s], k, n0);
-        } else {
+      // ---------------- TMA producer: a continuous stream of k-blocks over this CTA's tiles
+      int kg = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+        const TileInfo ti = decode_tile(p, t, BN);
+        const int k_begin = ti.split * a.k_per_split;
+        const int k_end = min(a.K, k_begin + a.k_per_split);
+        const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
+        for (int kb = 0; kb < nkb; ++kb, ++kg) {
+          const int s = kg % NS;
+          const uint32_t ph = (uint32_t)(kg / NS) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* sA = smem + s * STAGE;
+          uint8_t* sB = sA + A_BYTES;
+          mbar_expect_tx(&full[s], STAGE);
+          const int k = k_begin + kb * BK;
+          if (!AMN) {
+            tma_load_2d(sA, &p.ta[ti.grp], &full[s], k, ti.m0);
+          } else {
+            tma_load_2d(sA, &p.ta[ti.grp], &full[s], ti.m0, k);
+            tma_load_2d(sA + 8192, &p.ta[ti.grp], &full[s], ti.m0 + 64, k);
+          }
+          if (!BMN) {
+            tma_load_2d(sB, &p.tb[ti.grp], &full[s], k, ti.n0);
+          } else {
 #pragma unroll
-          for (int i = 0; i < BN / 64; ++i) tma_load_2d(sB + i * 8192, &p.tb[grp], &full[s], n0 + 64 * i, k);
+            for (int i = 0; i < BN / 64; ++i) tma_load_2d(sB + i * 8192, &p.tb[ti.grp], &full[s], ti.n0 + 64 * i, k);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % NS;
-        const uint32_t ph = (uint32_t)(kb / NS) & 1u;
-        mbar_wait(&full[s], ph);
+      // ---------------- MMA issuer: accumulator buffer (tile_i & 1), freed by the epilogue warps
+      int kg = 0, tile_i = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x, ++tile_i) {
+        const TileInfo ti = decode_tile(p, t, BN);
+        const int k_begin = ti.split * a.k_per_split;
+        const int k_end = min(a.K, k_begin + a.k_per_split);
+        const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
+        const int b = tile_i & 1;
+        mbar_wait(&acc_empty[b], (((uint32_t)tile_i >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t sA = smem_u32(smem + s * STAGE);
-        const uint32_t sB = sA + A_BYTES;
+        const uint32_t acc = tmem + (uint32_t)b * ACC_COLS;
+        for (int kb = 0; kb < nkb; ++kb, ++kg) {
+          const int s = kg % NS;
+          const uint32_t ph = (uint32_t)(kg / NS) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sA = smem_u32(smem + s * STAGE);
+          const uint32_t sB = sA + A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint64_t ad = AMN ? desc_mnmajor(sA, kk) : desc_kmajor(sA, kk);
-          const uint64_t bd = BMN ? desc_mnmajor(sB, kk) : desc_kmajor(sB, kk);
-          umma_bf16(tmem, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = AMN ? desc_mnmajor(sA, kk) : desc_kmajor(sA, kk);
+            const uint64_t bd = BMN ? desc_mnmajor(sB, kk) : desc_kmajor(sB, kk);
+            umma_bf16(acc, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
         }
-        umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+        umma_commit(&acc_full[b]);  // accumulator complete (immediately if the split is empty)
       }
-      if (nkb > 0) umma_commit(tmem_full);  // accumulator complete
     }
   } else {
-    // ---------------- epilogue: TMEM lane quarter (warp % 4) holds rows q*32 .. q*32+31
+    // ---------------- epilogue: 8 warps; warp % 4 selects the TMEM lane quarter (32 rows) and
+    //                  the two warps of a quarter split the columns (heads: one warp takes the row)
+    const int e = warp - 2;
     const int q = warp & 3;
-    const int m = m0 + q * 32 + lane;
-    const bool has_bias = a.epi == EPI_BIAS_RELU || a.epi == EPI_BIAS_F32 || a.epi == EPI_SAC_HEAD || a.epi == EPI_TD3_HEAD;
-    const bool has_dot = a.epi == EPI_BIAS_RELU && g.dot_out != nullptr;
-    if (has_bias) {
-      for (int c = threadIdx.x - 64; c < BN; c += 128) {
-        bias_s[c] = n0 + c < g.N ? g.bias[n0 + c] : 0.f;
-        dot_s[c] = (has_dot && n0 + c < g.N) ? g.dot_w[n0 + c] : 0.f;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
-    }
-    if (nkb > 0) {
-      mbar_wait(tmem_full, 0);
-      tc_fence_after();
-    }
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    if (a.epi == EPI_SAC_HEAD || a.epi == EPI_TD3_HEAD) {
-      if constexpr (BN <= 64) {
-        // the whole head row (2m <= BN columns) lives in this thread's TMEM lane
-        float hrow[BN];
-#pragma unroll
-        for (int c = 0; c < BN / 16; ++c) {
-          float v[16];
-          if (nkb > 0) tmem_ld16(trow + c * 16, v);
-          else
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0.f;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
-        }
-        if (m < g.M) {
-          if (a.epi == EPI_SAC_HEAD) sac_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow, hrow + a.head.m);
-          else td3_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow);
-        }
-      }
-    } else {
-      float dot = 0.f;
-      constexpr int NW = (BN + 31) / 32, MSTR = NW + 1;  // mask words per row, padded smem row stride
-      uint32_t* mrow = mask_s + (q * 32 + lane) * MSTR;     // this thread's row of packed ReLU-mask words
+    const int hh = e >> 2;
+    const bool head = a.epi == EPI_SAC_HEAD || a.epi == EPI_TD3_HEAD;
+    const bool split_cols = BN >= 64 && !head;
+    const int c_lo = split_cols ? hh * (BN / 32) : 0;            // first 16-column chunk of this warp
+    const int c_hi = split_cols ? (hh + 1) * (BN / 32) : (hh == 0 ? BN / 16 : 0);
+    const int r = q * 32 + lane;  // tile row of this thread
+    uint32_t* mrow = mask_s + r * MSTR;
+    int tile_i = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x, ++tile_i) {
+      const TileInfo ti = decode_tile(p, t, BN);
+      const GemmGroup& g = a.g[ti.grp];
+      const int m = ti.m0 + r;
+      const int n0 = ti.n0;
+      const int k_begin = ti.split * a.k_per_split;
+      const int nkb = min(a.K, k_begin + a.k_per_split) > k_begin ? 1 : 0;
+      const bool has_bias = a.epi == EPI_BIAS_RELU || a.epi == EPI_BIAS_F32 || head;
+      const bool has_dot = a.epi == EPI_BIAS_RELU && g.dot_out != nullptr;
       const bool mask_in = a.epi == EPI_MASK_BITS;
       const bool mask_out = a.epi == EPI_BIAS_RELU && g.mask_out != nullptr;
-      if (mask_in) {  // prefetched before the accumulator wait
+      // stage this tile's bias / row-dot weights (after every epilogue warp left the previous tile)
+      epi_bar(1);
+      if (has_bias)
+        for (int c = e * 32 + lane; c < BN; c += NUM_EPI_WARPS * 32) {
+          bias_s[c] = n0 + c < g.N ? g.bias[n0 + c] : 0.f;
+          dot_s[c] = (has_dot && n0 + c < g.N) ? g.dot_w[n0 + c] : 0.f;
+        }
+      if (mask_in) {  // this warp's words of the row's packed mask, prefetched before the accumulator wait
         const uint32_t* src = static_cast<const uint32_t*>(g.aux) + (int64_t)m * g.ldaux + n0 / 32;
-        for (int i = 0; i < NW; ++i) mrow[i] = (m < g.M && n0 + 32 * i < g.N) ? src[i] : 0u;
+        for (int i = c_lo / 2; i < (c_hi + 1) / 2; ++i) mrow[i] = (m < g.M && n0 + 32 * i < g.N) ? src[i] : 0u;
       }
-#pragma unroll 1
-      for (int c = 0; c < BN / 16; ++c) {
-        const int n = n0 + c * 16;
-        if (n >= g.N) break;  // warp-uniform
-        float v[16];
-        if (nkb > 0) {
-          tmem_ld16(trow + c * 16, v);
-        } else {
+      if (mask_out)
+        for (int i = c_lo / 2; i < (c_hi + 1) / 2; ++i) mrow[i] = 0u;
+      epi_bar(1);
+      const int b = tile_i & 1;
+      mbar_wait(&acc_full[b], ((uint32_t)tile_i >> 1) & 1u);
+      tc_fence_after();
+      const uint32_t trow = tmem + (uint32_t)b * ACC_COLS + ((uint32_t)(q * 32) << 16);
+      if (head) {
+        if constexpr (BN <= 64) {
+          if (hh == 0) {
+            float hrow[BN];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = 0.f;
+            for (int c = 0; c < BN / 16; ++c) {
+              float v[16];
+              if (nkb > 0) tmem_ld16(trow + c * 16, v);
+              else
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0.f;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
+            }
+            tc_fence_before();
+            if (m < g.M) {
+              if (a.epi == EPI_SAC_HEAD) sac_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow, hrow + a.head.m);
+              else td3_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow);
+            }
+          }
         }
-        uint32_t bits = mask_in ? (mrow[c >> 1] >> (16 * (c & 1))) & 0xFFFFu : 0u;
-        if (m < g.M) {
-          dot += epi16(a, g, split, m, n, v, bias_s + c * 16, has_dot ? dot_s + c * 16 : nullptr, bits);
-          if (mask_out) mrow[c >> 1] = (c & 1) ? (mrow[c >> 1] | (bits << 16)) : bits;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+      } else {
+        float dot = 0.f;
+#pragma unroll 1
+        for (int c = c_lo; c < c_hi; ++c) {
+          const int n = n0 + c * 16;
+          if (n >= g.N) break;  // warp-uniform
+          float v[16];
+          if (nkb > 0) {
+            tmem_ld16(trow + c * 16, v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+          }
+          uint32_t bits = mask_in ? (mrow[c >> 1] >> (16 * (c & 1))) & 0xFFFFu : 0u;
+          if (m < g.M) {
+            dot += epi16(a, g, ti.split, m, n, v, bias_s + c * 16, has_dot ? dot_s + c * 16 : nullptr, bits);
+            if (mask_out) mrow[c >> 1] |= bits << (16 * (c & 1));
+          }
         }
-      }
-      if (has_dot && m < g.M) g.dot_out[m] = dot + g.dot_b[0];
-      if (mask_out && m < g.M) {
-        // the row's mask words of this tile, written once (16-byte stores when aligned)
-        uint32_t* dst = g.mask_out + (int64_t)m * g.mask_ld + n0 / 32;
-        const int nw = min(NW, (g.N - n0 + 31) / 32);
-        if (nw == NW && (NW % 4) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-          for (int i = 0; i < NW; i += 4) *reinterpret_cast<uint4*>(dst + i) = make_uint4(mrow[i], mrow[i + 1], mrow[i + 2], mrow[i + 3]);
-        } else {
-          for (int i = 0; i < nw; ++i) dst[i] = mrow[i];
+        // accumulator buffer drained by this warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        if (has_dot) {
+          dotpart[hh * BM + r] = dot;
+          epi_bar(2);
+          if (hh == 0 && m < g.M) g.dot_out[m] = (split_cols ? dotpart[r] + dotpart[BM + r] : dot) + g.dot_b[0];
+        }
+        if (mask_out && m < g.M) {
+          const int w_lo = c_lo / 2, w_hi = min((c_hi + 1) / 2, (g.N - n0 + 31) / 32);
+          uint32_t* dst = g.mask_out + (int64_t)m * g.mask_ld + n0 / 32;
+          if (w_hi - w_lo == 4 && ((reinterpret_cast<uintptr_t>(dst + w_lo) & 15) == 0)) {
+            *reinterpret_cast<uint4*>(dst + w_lo) = make_uint4(mrow[w_lo], mrow[w_lo + 1], mrow[w_lo + 2], mrow[w_lo + 3]);
+          } else {
+            for (int i = w_lo; i < w_hi; ++i) dst[i] = mrow[i];
+          }
         }
       }
     }
@@ -387,6 +463,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
 }
 
 // ------------------------------------------------------------------ host side
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
@@ -414,21 +500,51 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
   return r == CUDA_SUCCESS;
 }
 
+template <int BN>
+constexpr int smem_extras() {
+  return 1024 /* alignment */ + 128 /* barriers + TMEM slot */ + BN * 8 /* bias, dot */ + 2 * BM * 4 /* dot halves */ +
+         BM * ((BN + 31) / 32 + 1) * 4 /* masks */;
+}
+
 template <int BN, bool AMN, bool BMN>
 cudaError_t launch(TcParams& p, int maxM, cudaStream_t st) {
   constexpr int STAGE = A_BYTES + BN * BK * 2;
-  constexpr int SMEM_MAX = STAGES * STAGE + 1024 + 256 + BN * 8 + 128 * ((BN + 31) / 32 + 1) * 4;
+  constexpr int SMEM_MAX = STAGES * STAGE + smem_extras<BN>();
+  static_assert(SMEM_MAX <= 227 * 1024, "shared memory budget");
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  (void)maxM;
+  // persistent schedule: tiles of every group, one CTA per SM (or more when TMEM and smem allow)
+  int T = 0;
+  for (int i = 0; i < p.a.n_groups; ++i) {
+    const GemmGroup& g = p.a.g[i];
+    p.tile0[i] = T;
+    p.mtiles[i] = g.M > 0 && g.N > 0 ? (int)cdiv(g.M, BM) : 0;
+    p.ntiles[i] = g.M > 0 && g.N > 0 ? (int)cdiv(g.N, BN) : 1;
+    if (p.mtiles[i] == 0) p.mtiles[i] = 1, p.ntiles[i] = 0;
+    T += p.mtiles[i] * p.ntiles[i] * p.a.splits;
+  }
+  p.tile0[p.a.n_groups] = T;
+  p.total_tiles = T;
+  if (T == 0) return cudaSuccess;
+  constexpr int TMEM_COLS = 2 * (BN < 32 ? 32 : BN);
+  static int occ = [] {
+    int o = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tc_gemm_kernel<BN, AMN, BMN>, NTHREADS, STAGE + smem_extras<BN>());
+    return std::max(1, o);
+  }();
+  const int per_sm = std::max(1, std::min(512 / TMEM_COLS, occ));
+  const int budget = 227 * 1024 / per_sm;
   const int kspan = p.a.splits > 1 ? p.a.k_per_split : p.a.K;
-  p.stages = (int)std::min<int64_t>(STAGES, std::max<int64_t>(1, cdiv(kspan, BK)));
-  const int smem = p.stages * STAGE + 1024 + 256 + BN * 8 + 128 * ((BN + 31) / 32 + 1) * 4;
-  dim3 grid((unsigned)cdiv(p.a.N, BN), (unsigned)cdiv(maxM, BM), (unsigned)(p.a.n_groups * p.a.splits));
-  return launch_pdl(tc_gemm_kernel<BN, AMN, BMN>, grid, dim3(NTHREADS), (size_t)smem, st, p);
+  const int want = (int)std::min<int64_t>(STAGES, std::max<int64_t>(1, cdiv(kspan, BK)));
+  p.stages = std::max(1, std::min(want, (budget - smem_extras<BN>()) / STAGE));
+  const int smem = p.stages * STAGE + smem_extras<BN>();
+  const int grid = std::min(T, num_sms() * per_sm);
+  return launch_pdl(tc_gemm_kernel<BN, AMN, BMN>, dim3(grid), dim3(NTHREADS), (size_t)smem, st, p);
 }
 
 template <bool AMN, bool BMN>

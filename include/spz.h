@@ -123,8 +123,9 @@ typedef struct {
   uint64_t init_seed;              /* parameter init key (Philox stream 5)       */
   int32_t device;                  /* CUDA device ordinal                        */
   int32_t world_size, rank;        /* row sharding: rank handles a contiguous slice of global rows */
-  int32_t n_critic_ranks, n_actor_ranks; /* reserved for split mode (0 = co-located) */
-  spz_role role;
+  int32_t n_critic_ranks, n_actor_ranks; /* split roles over world_size ranks: ranks [0, n_critic_ranks)
+                                            are the critic group, the rest the actor group */
+  spz_role role;                   /* ALL (default), or one half of the Jacobi step  */
   const uint8_t* nccl_unique_id;   /* 128 bytes, identical on all ranks; NULL if world_size == 1 */
   int32_t use_graph;               /* 1 (default): replay the step as a CUDA graph */
   int32_t comm_mode;               /* world_size > 1: 0 = NCCL allreduce (default); 1 = no exchange
@@ -193,6 +194,14 @@ spz_status spz_get_counters(spz_learner* L, int64_t* step, int64_t* t_critic, in
  * >= 16 + 4 * n_floats.  Synchronous. */
 spz_status spz_sync_actor(spz_learner* L, int32_t dst_device, void* dst, int64_t dst_bytes,
                           uint64_t* version);
+
+/* Actor/critic model parallelism on one host process: after each spz_update of a
+ * critic-role learner and an actor-role learner (each world_size 1, any devices), copy the
+ * updated actor parameters and log alpha (TD3: also the target actor) into the critic side and
+ * the online critics into the actor side (peer copies), refreshing the receivers' operand
+ * shadows.  With world_size > 1 and NCCL the same exchange runs inside every step instead.
+ * Together the two halves compute exactly the single-learner step (Jacobi order, reading #3). */
+spz_status spz_split_exchange(spz_learner* critic_side, spz_learner* actor_side);
 
 /* Per kernel-class device time (ms per step, averaged over n_steps steps run
  * un-graphed with CUDA events around each class) -- measurement only; the steps

@@ -20,6 +20,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
   std::string why;
@@ -44,7 +46,10 @@ void load_nccl() {
   g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
   g_nccl.AllReduce = reinterpret_cast<decltype(g_nccl.AllReduce)>(dlsym(h, "ncclAllReduce"));
   g_nccl.GetErrorString = reinterpret_cast<decltype(g_nccl.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce && g_nccl.GetErrorString;
+  g_nccl.Broadcast = reinterpret_cast<decltype(g_nccl.Broadcast)>(dlsym(h, "ncclBroadcast"));
+  g_nccl.CommSplit = reinterpret_cast<decltype(g_nccl.CommSplit)>(dlsym(h, "ncclCommSplit"));
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce && g_nccl.GetErrorString &&
+              g_nccl.Broadcast && g_nccl.CommSplit;
   if (!g_nccl.ok) g_nccl.why = "libnccl.so.2 lacks required symbols";
 }
 
@@ -71,6 +76,25 @@ spz_status comm_init(Comm* c, const uint8_t* uid, int world, int rank) {
   c->world = world;
   c->rank = rank;
   return SPZ_OK;
+}
+
+spz_status comm_split(const Comm& world, int color, int key, Comm* out) {
+  ncclComm_t nc;
+  ncclResult_t r = g_nccl.CommSplit(static_cast<ncclComm_t>(world.handle), color, key, &nc, nullptr);
+  if (r != ncclSuccess) return nccl_fail("ncclCommSplit", r);
+  out->handle = nc;
+  out->rank = key;
+  out->world = -1;
+  return SPZ_OK;
+}
+
+cudaError_t comm_broadcast_f32(const Comm& c, float* buf, size_t count, int root, cudaStream_t st) {
+  ncclResult_t r = g_nccl.Broadcast(buf, buf, count, ncclFloat32, root, static_cast<ncclComm_t>(c.handle), st);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclBroadcast: ") + g_nccl.GetErrorString(r));
+    return cudaErrorUnknown;
+  }
+  return cudaSuccess;
 }
 
 void comm_destroy(Comm* c) {

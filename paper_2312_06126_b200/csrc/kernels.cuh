@@ -207,7 +207,7 @@ struct LossArgs {
   const float* w[2];
   void* dZ[2];
   float gamma, invB;
-  int Bl, td3, delay, actor_rows, h, ld, mask_ld;
+  int Bl, td3, delay, loss_rows, actor_rows, h, ld, mask_ld;
 };
 
 template <typename T>
@@ -223,20 +223,24 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   if (threadIdx.x < nr) {
     const int j = j0 + threadIdx.x;
     const float alpha = a.td3 ? 0.f : expf(*a.log_alpha);
-    const float qmin = fminf(a.qt1[j], a.qt2[j]);
-    const float boot = a.td3 ? qmin : qmin - alpha * a.logp2[j];
-    const float y = a.r[j] + a.gamma * (1.f - a.d[j]) * boot;
-    a.y[j] = y;
-    const float q1 = a.q1[j], q2 = a.q2[j];
-    const float e1 = q1 - y, e2 = q2 - y;
-    float g1 = 2.f * e1 * a.invB, g2 = 2.f * e2 * a.invB;
-    a.gq1[j] = g1;
-    a.gq2[j] = g2;
-    gs[0][0][threadIdx.x] = g1;
-    gs[1][0][threadIdx.x] = g2;
-    v[0] = (double)e1 * e1 + (double)e2 * e2;
-    v[1] = q1;
-    v[2] = q2;
+    float g1, g2;
+    if (a.loss_rows) {
+      const float qmin = fminf(a.qt1[j], a.qt2[j]);
+      const float boot = a.td3 ? qmin : qmin - alpha * a.logp2[j];
+      const float y = a.r[j] + a.gamma * (1.f - a.d[j]) * boot;
+      a.y[j] = y;
+      const float q1 = a.q1[j], q2 = a.q2[j];
+      const float e1 = q1 - y, e2 = q2 - y;
+      g1 = 2.f * e1 * a.invB;
+      g2 = 2.f * e2 * a.invB;
+      a.gq1[j] = g1;
+      a.gq2[j] = g2;
+      gs[0][0][threadIdx.x] = g1;
+      gs[1][0][threadIdx.x] = g2;
+      v[0] = (double)e1 * e1 + (double)e2 * e2;
+      v[1] = q1;
+      v[2] = q2;
+    }
     if (a.actor_rows) {
       const float a1 = a.q1[a.Bl + j], a2 = a.q2[a.Bl + j];
       if (!a.td3) {
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   // combinations are loaded together (independent 16-byte loads), then written
   const int hv = a.h / 8;
   const int per = nr * hv;
+  const int k_lo = a.loss_rows ? 0 : 1, k_hi = a.actor_rows ? 2 : 1;  // row kinds present: loss, actor
   for (int e = threadIdx.x; e < per; e += LOSS_NT) {
     const int rr = e / hv, n = (e - rr * hv) * 8;
     if constexpr (std::is_same<T, __nv_bfloat16>::value) {
@@ -284,7 +289,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
         for (int ci = 0; ci < 2; ++ci)
 #pragma unroll
           for (int kind = 0; kind < 2; ++kind)
-            mb[ci][kind] = (kind == 0 || a.actor_rows)
+            mb[ci][kind] = (kind >= k_lo && kind < k_hi)
                                ? (a.mask[ci][((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.mask_ld + n / 32] >> (n & 31)) & 0xFFu
                                : 0u;
 #pragma unroll
@@ -293,7 +298,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
           const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
           for (int kind = 0; kind < 2; ++kind) {
-            if (kind == 1 && !a.actor_rows) continue;
+            if (kind < k_lo || kind >= k_hi) continue;
             const float gq = gs[ci][kind][rr];
             uint4 o;
             __nv_bfloat162* yv = reinterpret_cast<__nv_bfloat162*>(&o);
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
       for (int ci = 0; ci < 2; ++ci)
 #pragma unroll
         for (int kind = 0; kind < 2; ++kind)
-          if (kind == 0 || a.actor_rows)
+          if (kind >= k_lo && kind < k_hi)
             u[ci][kind] = *reinterpret_cast<const uint4*>(static_cast<const T*>(a.A[ci]) +
                                                           ((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.ld + n);
 #pragma unroll
@@ -320,7 +325,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
         const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
         for (int kind = 0; kind < 2; ++kind) {
-          if (kind == 1 && !a.actor_rows) continue;
+          if (kind < k_lo || kind >= k_hi) continue;
           const float gq = gs[ci][kind][rr];
           const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&u[ci][kind]);
           uint4 o;
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
       }
     } else {
       for (int ci = 0; ci < 2; ++ci)
-        for (int kind = 0; kind < (a.actor_rows ? 2 : 1); ++kind) {
+        for (int kind = k_lo; kind < k_hi; ++kind) {
           const int64_t row = (int64_t)(kind ? a.Bl : 0) + j0 + rr;
           const float gq = gs[ci][kind][rr];
           const T* A = static_cast<const T*>(a.A[ci]) + row * a.ld + n;

@@ -119,8 +119,13 @@ struct spz_learner {
   int max_tensors = 64, max_segs = 0;
   ShadowEntry* d_shadow = nullptr;
   int n_shadow = 0;
-  // row-sharded group (world_size > 1)
-  Comm comm;
+  // row-sharded group (world_size > 1) and actor/critic split roles
+  bool split = false;  // role != ALL: this learner runs one half of the Jacobi step
+  int gsize = 1;       // ranks sharing this learner's role (row-sharded group)
+  Comm comm;           // all ranks (exchange between the role groups)
+  Comm gcomm;          // this role's group (gradient allreduce); == comm when not split
+  ShadowEntry* d_shadow_recv = nullptr;  // shadows of the networks this role receives
+  int n_shadow_recv = 0;
   float* Gred = nullptr;     // contiguous gradients of every trained tensor (+ log alpha slot)
   int64_t Gred_total = 0;
   double* statsum = nullptr;  // this rank's (then the group's) loss statistic totals
@@ -214,6 +219,7 @@ spz_learner::~spz_learner() {
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   if (own_stream) cudaStreamSynchronize(own_stream);
+  if (gcomm.handle && gcomm.handle != comm.handle) comm_destroy(&gcomm);
   comm_destroy(&comm);
   for (auto& e : exec)
     if (e) cudaGraphExecDestroy(e);
@@ -236,7 +242,17 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       cudaGraphExecDestroy(e);
       e = nullptr;
     }
-  const int W = Lr->cfg.world_size, rk = Lr->cfg.rank;
+  // rows of this rank: contiguous share of the global batch inside its group (reading #17);
+  // with split roles the critic group is ranks [0, n_critic) and the actor group the rest
+  int W = Lr->cfg.world_size, rk = Lr->cfg.rank;
+  if (Lr->split) {
+    const int nc = Lr->cfg.n_critic_ranks;
+    if (rk < nc) W = nc;
+    else {
+      W = Lr->cfg.world_size - nc;
+      rk -= nc;
+    }
+  }
   const int64_t base = B / W, rem = B % W;
   const int Bl = (int)(base + (rk < rem ? 1 : 0));
   const int64_t row0 = rk * base + std::min<int64_t>(rk, rem);
@@ -266,9 +282,19 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
   for (int variant = 0; variant < (td3 ? 2 : 1); ++variant) {
     std::vector<Op>& ops = Lr->ops[variant];
     const bool actor_step = !td3 || variant == 1;  // TD3: actor work only on delayed steps
+    // roles: the critic side needs the actor only on s2 (a', log pi'); the actor side
+    // needs the critics only on [s | a~] (Q(s, a~) and dQ/da~)
+    const bool do_critic = Lr->cfg.role != SPZ_ROLE_ACTOR;
+    const bool do_actor = Lr->cfg.role != SPZ_ROLE_CRITIC && actor_step;
     std::vector<GemmGroup> wgrads;
     std::vector<ColsumJob> colsums;
+    auto empty_gemm = [](const GemmArgs& a) {
+      for (int i = 0; i < a.n_groups; ++i)
+        if (a.g[i].M > 0 && a.g[i].N > 0) return false;
+      return true;
+    };
     auto gemm = [&](const char* cls, GemmArgs a) {
+      if (empty_gemm(a)) return;  // e.g. the TD3 actor role on a non-delayed step
       ops.push_back({cls, [a](cudaStream_t st) { return run_gemm<T>(a, st); }});
     };
     auto mk = [&](int K, int epi, int amn, int bmn) {
@@ -347,12 +373,15 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       const NetLayout& an = Lr->net[NET_ACTOR];
       struct Pass { int id; int64_t row; int M; };
       std::vector<Pass> passes;
-      if (!td3) passes.push_back({NET_ACTOR, 0, 2 * Bl});
-      else {
-        passes.push_back({NET_ACTORT, 0, Bl});
-        if (actor_step) passes.push_back({NET_ACTOR, Bl, Bl});
+      if (!td3) {
+        if (do_critic && do_actor) passes.push_back({NET_ACTOR, 0, 2 * Bl});
+        else if (do_critic) passes.push_back({NET_ACTOR, 0, Bl});
+        else if (do_actor) passes.push_back({NET_ACTOR, Bl, Bl});
+      } else {
+        if (do_critic) passes.push_back({NET_ACTORT, 0, Bl});
+        if (do_actor) passes.push_back({NET_ACTOR, Bl, Bl});
       }
-      for (int l = 0; l < L; ++l) {
+      for (int l = 0; l < L && !passes.empty(); ++l) {
         GemmArgs a = mk(an.in[l], EPI_BIAS_RELU, 0, 0);
         for (const Pass& ps : passes) {
           GemmGroup& g = add(a, l == 0 ? (const void*)Ta(Lr->Xa, ps.row, lda) : (const void*)Ta(Lr->Aact[l - 1], ps.row, h),
@@ -366,6 +395,8 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         gemm("actor_fwd_gemm", a);
       }
       // head layer: fused squashed-Gaussian (SAC) / tanh + smoothing (TD3) epilogue when possible
+      // (TD3 actor role on a non-delayed step: no actor work at all)
+      if (!passes.empty()) {
       GemmArgs a = mk(h, td3 ? EPI_TD3_HEAD : EPI_SAC_HEAD, 0, 0);
       a.head = he;
       for (const Pass& ps : passes) {
@@ -379,7 +410,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         a.epi = EPI_BIAS_F32;
         gemm("actor_head_gemm", a);
         float* Hh = Lr->H;
-        const int Mh = passes.size() == 2 || !td3 ? 2 * Bl : Bl;
+        const int Mh = (int)(passes.back().row + passes.back().M);  // rows [0, Mh) of the actor pass
         const HeadEpi hh = he;
         const int t3 = td3;
         ops.push_back({"actor_head", [=](cudaStream_t st) {
@@ -387,51 +418,61 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
                          return launch_pdl(sac_head_fwd_kernel<T>, dim3((unsigned)cdiv(Mh, 128)), dim3(128), 0, st, Hh, ldh, hh, Mh);
                        }});
       }
+      }
     }
     // ---- a4: target critics on [s2 | a'] (M = Bl) and a5: online critics on [s | a ; s | a~]
     //      (M = 2Bl), all four in one launch per layer; the N = 1 head is a row dot fused into
     //      the last hidden layer's epilogue when the row fits one tile.
     const NetLayout& cn = Lr->net[NET_Q1];
-    const int Mon = actor_step ? 2 * Bl : Bl;
+    // online-critic rows [on0, on0 + Mon): loss rows [0, Bl) on the critic side, actor rows [Bl, 2Bl)
+    const int on0 = do_critic ? 0 : Bl;
+    const int Mon = (do_critic ? Bl : 0) + (do_actor ? Bl : 0);
     {
       for (int l = 0; l < L; ++l) {
         GemmArgs a = mk(cn.in[l], EPI_BIAS_RELU, 0, 0);
         for (int pass = 0; pass < 2; ++pass) {
           const bool tgt = pass == 1;
+          if (tgt && !do_critic) continue;
+          if (!tgt && Mon == 0) continue;
+          const int r0c = tgt ? 2 * Bl : on0;  // row in Xc
+          const int ra = tgt ? 0 : on0;        // row in the activation buffers
           for (int i = 0; i < 2; ++i) {
             const int id = tgt ? NET_Q1T + i : NET_Q1 + i;
-            void* dst = tgt ? Lr->Atg[i][l] : Lr->Aon[i][l];
-            const void* src = l == 0 ? (const void*)Ta(Lr->Xc, tgt ? 2 * Bl : 0, ldc)
-                                     : (const void*)(tgt ? Lr->Atg[i][l - 1] : Lr->Aon[i][l - 1]);
+            void* dst = Ta(tgt ? Lr->Atg[i][l] : Lr->Aon[i][l], ra, h);
+            const void* src = l == 0 ? (const void*)Ta(Lr->Xc, r0c, ldc)
+                                     : (const void*)Ta(tgt ? Lr->Atg[i][l - 1] : Lr->Aon[i][l - 1], ra, h);
             GemmGroup& g = add(a, src, l == 0 ? ldc : h, Wp(id, l), cn.ld[l], dst, h, tgt ? Bl : Mon, h, bp(id, l));
             if (bits && !tgt) {
-              g.mask_out = Lr->mask_c[i][l];
+              g.mask_out = Lr->mask_c[i][l] + (int64_t)ra * mw;
               g.mask_ld = mw;
             }
             if (l == L - 1) {
               g.dot_w = P + Lr->pbase[id] + Lr->net[id].w[L];
               g.dot_b = bp(id, L);
-              g.dot_out = tgt ? Lr->q_tg[i] : Lr->q_on[i];
+              g.dot_out = (tgt ? Lr->q_tg[i] : Lr->q_on[i]) + ra;
             }
           }
         }
-        if (bits && !tc_ok(a) && l < L - 1) return fail(SPZ_EUNSUPPORTED, "internal: critic forward not supported by the tcgen05 kernel");
-        if (l == L - 1 && !tc_ok(a)) {
+        if (bits && !empty_gemm(a) && !tc_ok(a) && l < L - 1)
+          return fail(SPZ_EUNSUPPORTED, "internal: critic forward not supported by the tcgen05 kernel");
+        if (l == L - 1 && !empty_gemm(a) && !tc_ok(a)) {
           for (int i = 0; i < a.n_groups; ++i) a.g[i].dot_out = nullptr;
           gemm("critic_fwd_gemm", a);
           for (int pass = 0; pass < 2; ++pass) {
             const bool tgt = pass == 1;
+            if ((tgt && !do_critic) || (!tgt && Mon == 0)) continue;
             const int M = tgt ? Bl : Mon;
+            const int rr0 = tgt ? 0 : on0;
             RowdotArgs ra{};
             ra.M = M;
             ra.h = h;
             ra.ld = h;
             for (int i = 0; i < 2; ++i) {
               const int id = tgt ? NET_Q1T + i : NET_Q1 + i;
-              ra.g[i].A = tgt ? Lr->Atg[i][L - 1] : Lr->Aon[i][L - 1];
+              ra.g[i].A = Ta(tgt ? Lr->Atg[i][L - 1] : Lr->Aon[i][L - 1], rr0, h);
               ra.g[i].w = P + Lr->pbase[id] + Lr->net[id].w[L];
               ra.g[i].b = bp(id, L);
-              ra.g[i].q = tgt ? Lr->q_tg[i] : Lr->q_on[i];
+              ra.g[i].q = (tgt ? Lr->q_tg[i] : Lr->q_on[i]) + rr0;
             }
             ops.push_back({"critic_head", [ra, M](cudaStream_t st) {
                              return launch_pdl(rowdot_kernel<T>, dim3((unsigned)cdiv((int64_t)M * 32, 256), 2), dim3(256), 0, st, ra);
@@ -474,7 +515,8 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       la.Bl = Bl;
       la.td3 = td3;
       la.delay = delay;
-      la.actor_rows = actor_step;
+      la.loss_rows = do_critic;
+      la.actor_rows = do_actor;
       la.h = h;
       la.ld = h;
       ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
@@ -483,25 +525,29 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     }
     // ---- a6: critic backward
     {
-      // dgrad through hidden layers l = L-1 .. 1 (all Mon rows)
+      // dgrad through hidden layers l = L-1 .. 1 (the online rows [on0, on0 + Mon))
       for (int l = L - 1; l >= 1; --l) {
         GemmArgs a = mk(h, bits ? EPI_MASK_BITS : EPI_MASK, 0, 1);
         for (int i = 0; i < 2; ++i) {
-          if (bits) add(a, Lr->dZc[i][l], h, Wp(NET_Q1 + i, l), cn.ld[l], Lr->dZc[i][l - 1], h, Mon, h, nullptr, Lr->mask_c[i][l - 1], mw);
-          else add(a, Lr->dZc[i][l], h, Wp(NET_Q1 + i, l), cn.ld[l], Lr->dZc[i][l - 1], h, Mon, h, nullptr, Lr->Aon[i][l - 1], h);
+          if (bits)
+            add(a, Ta(Lr->dZc[i][l], on0, h), h, Wp(NET_Q1 + i, l), cn.ld[l], Ta(Lr->dZc[i][l - 1], on0, h), h, Mon, h,
+                nullptr, Lr->mask_c[i][l - 1] + (int64_t)on0 * mw, mw);
+          else
+            add(a, Ta(Lr->dZc[i][l], on0, h), h, Wp(NET_Q1 + i, l), cn.ld[l], Ta(Lr->dZc[i][l - 1], on0, h), h, Mon, h,
+                nullptr, Ta(Lr->Aon[i][l - 1], on0, h), h);
         }
-        if (bits && !tc_ok(a)) return fail(SPZ_EUNSUPPORTED, "internal: critic dgrad not supported by the tcgen05 kernel");
+        if (bits && !empty_gemm(a) && !tc_ok(a)) return fail(SPZ_EUNSUPPORTED, "internal: critic dgrad not supported by the tcgen05 kernel");
         gemm("critic_dgrad_gemm", a);
       }
       // input dgrad for the actor rows (only the action columns are consumed)
-      if (actor_step) {
+      if (do_actor) {
         GemmArgs a = mk(h, EPI_F32, 0, 1);
         for (int i = 0; i < (td3 ? 1 : 2); ++i)
           add(a, Ta(Lr->dZc[i][0], Bl, h), h, Wp(NET_Q1 + i, 0), cn.ld[0], Lr->dXc[i], ldc, Bl, o + m);
         gemm("critic_input_dgrad_gemm", a);
       }
       // wgrad (B loss rows) and bias column sums are collected and launched with the actor's below
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < (do_critic ? 2 : 0); ++i)
         for (int l = 0; l < L; ++l) {
           GemmGroup g{};
           g.A = Lr->dZc[i][l];
@@ -515,7 +561,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           g.split_stride = (int64_t)h * cn.in[l];
           wgrads.push_back(g);
         }
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < (do_critic ? 2 : 0); ++i) {
         for (int l = 0; l < L; ++l)
           colsums.push_back({Lr->dZc[i][l], nullptr, Lr->G + slot_of(NET_Q1 + i, l, false).g_off, h, h, Bl, 0});
         colsums.push_back({Lr->Aon[i][L - 1], Lr->gq[i], Lr->G + slot_of(NET_Q1 + i, L, true).g_off, h, h, Bl, 0});
@@ -523,7 +569,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       }
     }
     // ---- a7: actor backward (s-rows Bl..2Bl of the actor activations)
-    if (actor_step) {
+    if (do_actor) {
       const NetLayout& an = Lr->net[NET_ACTOR];
       const int nout = an.out[L];  // 2m (SAC) or m (TD3)
       T* dH = static_cast<T*>(Lr->dH);
@@ -603,7 +649,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     }
     // row-sharded groups reduce their split partials into one contiguous buffer and all-reduce it
     // together with the loss totals before the (identical) optimizer step on every rank
-    const bool sharded = Lr->cfg.world_size > 1;
+    const bool sharded = Lr->gsize > 1;
     // ---- a9: fused Adam + Polyak (+ shadow refresh) over every trained tensor
     {
       std::vector<AdamTensor> tens;
@@ -672,7 +718,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
                          return launch_pdl(reduce_partials_kernel, dim3(nsg), dim3(256), 0, st, dt, ds, Gr);
                        }});
         if (Lr->cfg.comm_mode == 0) {
-          const Comm cm = Lr->comm;
+          const Comm cm = Lr->gcomm;
           const size_t n = (size_t)Lr->Gred_total;
           double* ss = Lr->statsum;
           ops.push_back({"allreduce", [=](cudaStream_t st) {
@@ -713,6 +759,28 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       ops.push_back({"adam_polyak", [=](cudaStream_t st) {
                        return launch_pdl(adam_polyak_kernel<T>, dim3(nseg), dim3(256), 0, st, dt, ds, hp, Pm, Mm, Vm, S, ctr, fl);
                      }});
+    }
+    // ---- a10: split roles exchange the updated parameters at the step boundary:
+    //      phi_{k+1} (+ log alpha, TD3 phi') from the actor leader, theta_{k+1} from the critic leader
+    if (Lr->split && Lr->cfg.world_size > 1 && Lr->cfg.comm_mode == 0) {
+      const Comm cm = Lr->comm;
+      const int nc = Lr->cfg.n_critic_ranks;
+      float* pa = P + Lr->pbase[NET_ACTOR];
+      const size_t na = (size_t)Lr->net[NET_ACTOR].np;
+      float* pat = Lr->has_net[NET_ACTORT] ? P + Lr->pbase[NET_ACTORT] : nullptr;
+      float* pla = P + Lr->p_log_alpha;
+      float* pq = P + Lr->pbase[NET_Q1];
+      const size_t nq = (size_t)(Lr->pbase[NET_Q2] + Lr->net[NET_Q2].np - Lr->pbase[NET_Q1]);
+      const ShadowEntry* sh = Lr->d_shadow_recv;
+      const int nsh = Lr->n_shadow_recv;
+      ops.push_back({"exchange", [=](cudaStream_t st) {
+                       cudaError_t e = comm_broadcast_f32(cm, pa, na, nc, st);
+                       if (e == cudaSuccess) e = comm_broadcast_f32(cm, pla, 1, nc, st);
+                       if (e == cudaSuccess && pat) e = comm_broadcast_f32(cm, pat, na, nc, st);
+                       if (e == cudaSuccess) e = comm_broadcast_f32(cm, pq, nq, 0, st);
+                       if (e != cudaSuccess) return e;
+                       return launch_pdl(shadow_refresh_kernel<T>, dim3(64, nsh), dim3(256), 0, st, sh, nsh, (const float*)P, S);
+                     }, 1});
     }
   }
   Lr->plan_B = B;
@@ -851,7 +919,15 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return fail(SPZ_EINVAL, "spz_learner_create: bad rank/world_size");
   if (cfg->world_size > 1 && cfg->comm_mode == 0 && !cfg->nccl_unique_id)
     return fail(SPZ_EINVAL, "spz_learner_create: world_size > 1 needs nccl_unique_id (or comm_mode = 1)");
-  if (cfg->role != SPZ_ROLE_ALL) return fail(SPZ_EUNSUPPORTED, "spz_learner_create: split roles are not built yet");
+  if (cfg->role != SPZ_ROLE_ALL && cfg->role != SPZ_ROLE_CRITIC && cfg->role != SPZ_ROLE_ACTOR)
+    return fail(SPZ_EINVAL, "spz_learner_create: unknown role");
+  if (cfg->role != SPZ_ROLE_ALL && cfg->world_size > 1) {
+    // critic group = ranks [0, n_critic_ranks), actor group = the rest (P:239-247 generalised)
+    const int nc = cfg->n_critic_ranks;
+    if (nc < 1 || nc >= cfg->world_size) return fail(SPZ_EINVAL, "spz_learner_create: split roles need 1 <= n_critic_ranks < world_size");
+    if ((cfg->rank < nc) != (cfg->role == SPZ_ROLE_CRITIC))
+      return fail(SPZ_EINVAL, "spz_learner_create: ranks [0, n_critic_ranks) must be critic, the others actor");
+  }
   if (cfg->algo != SPZ_SAC && cfg->algo != SPZ_TD3) return fail(SPZ_EINVAL, "spz_learner_create: unknown algo");
   if (cfg->precision != SPZ_FP32 && cfg->precision != SPZ_BF16) return fail(SPZ_EINVAL, "spz_learner_create: unknown precision");
   spz_status st = check_device(cfg->device);
@@ -872,7 +948,12 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   if (cudaStreamCreateWithFlags(&Lr->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SPZ_ECUDA, "spz_learner_create: stream creation failed");
   Lr->stream = Lr->own_stream;
-  const int W = cfg->world_size;
+  Lr->split = cfg->role != SPZ_ROLE_ALL;
+  Lr->gsize = !Lr->split ? cfg->world_size
+                         : (cfg->world_size == 1 ? 1
+                                                 : (cfg->role == SPZ_ROLE_CRITIC ? cfg->n_critic_ranks
+                                                                                 : cfg->world_size - cfg->n_critic_ranks));
+  const int W = Lr->gsize;
   Lr->max_local = cfg->max_batch / W + (cfg->max_batch % W ? 1 : 0);
   // networks
   const int aout = Lr->td3 ? m : 2 * m;
@@ -973,15 +1054,22 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->statsum, 8 * sizeof(double)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->tickets, 8 * sizeof(unsigned)));
   Lr->debug.push_back({"statsum", Lr->statsum, 8 * sizeof(double), 8});
-  if (cfg->world_size > 1) {
+  if (Lr->gsize > 1) {
     int64_t tot = 0;
     for (auto& t : slots) tot += round_up(t.numel, 16);
     Lr->Gred_total = tot + 16;
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->Gred, Lr->Gred_total * sizeof(float)));
     Lr->debug.push_back({"Gred", Lr->Gred, (size_t)Lr->Gred_total * 4, 4});
-    if (cfg->comm_mode == 0) {
-      SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
-      spz_status cs = comm_init(&Lr->comm, cfg->nccl_unique_id, cfg->world_size, cfg->rank);
+  }
+  if (cfg->world_size > 1 && cfg->comm_mode == 0) {
+    SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+    spz_status cs = comm_init(&Lr->comm, cfg->nccl_unique_id, cfg->world_size, cfg->rank);
+    if (cs != SPZ_OK) return cs;
+    Lr->gcomm = Lr->comm;
+    if (Lr->split) {  // the role's own group for the gradient allreduce
+      const int color = cfg->role == SPZ_ROLE_CRITIC ? 0 : 1;
+      const int key = cfg->role == SPZ_ROLE_CRITIC ? cfg->rank : cfg->rank - cfg->n_critic_ranks;
+      cs = comm_split(Lr->comm, color, key, &Lr->gcomm);
       if (cs != SPZ_OK) return cs;
     }
   }
@@ -999,6 +1087,25 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     for (int l = 0; l < n.nl; ++l) sh.push_back({Lr->pbase[id] + n.w[l], n.out[l], n.in[l], n.ld[l], Lr->sbase[id] + n.sw[l]});
   }
   Lr->n_shadow = (int)sh.size();
+  {
+    // networks this role receives at the step boundary: the actor (and TD3 target actor) on the
+    // critic side, the online critics on the actor side
+    std::vector<ShadowEntry> rv;
+    for (int id = 0; id < N_NETS; ++id) {
+      if (!Lr->has_net[id]) continue;
+      const bool recv = (cfg->role == SPZ_ROLE_CRITIC && (id == NET_ACTOR || id == NET_ACTORT)) ||
+                        (cfg->role == SPZ_ROLE_ACTOR && (id == NET_Q1 || id == NET_Q2));
+      if (!recv) continue;
+      const NetLayout& n = Lr->net[id];
+      for (int l = 0; l < n.nl; ++l) rv.push_back({Lr->pbase[id] + n.w[l], n.out[l], n.in[l], n.ld[l], Lr->sbase[id] + n.sw[l]});
+    }
+    Lr->n_shadow_recv = (int)rv.size();
+    if (!rv.empty()) {
+      SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_shadow_recv, rv.size() * sizeof(ShadowEntry)));
+      SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->d_shadow_recv, rv.data(), rv.size() * sizeof(ShadowEntry), cudaMemcpyHostToDevice, Lr->stream));
+      SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+    }
+  }
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_shadow, sh.size() * sizeof(ShadowEntry)));
   SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->d_shadow, sh.data(), sh.size() * sizeof(ShadowEntry), cudaMemcpyHostToDevice, Lr->stream));
   SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
@@ -1221,6 +1328,43 @@ spz_status spz_learner_launches_per_step(spz_learner* Lr, int64_t batch, int32_t
   int n = 0;
   for (auto& op : Lr->ops[0]) n += op.launches;
   *launches = n;
+  return SPZ_OK;
+}
+
+spz_status spz_split_exchange(spz_learner* critic_side, spz_learner* actor_side) {
+  if (!critic_side || !actor_side) return fail(SPZ_EINVAL, "spz_split_exchange: NULL learner");
+  if (critic_side->cfg.role != SPZ_ROLE_CRITIC || actor_side->cfg.role != SPZ_ROLE_ACTOR)
+    return fail(SPZ_EINVAL, "spz_split_exchange: need a critic-role and an actor-role learner");
+  if (critic_side->bf16 != actor_side->bf16 || critic_side->td3 != actor_side->td3 || critic_side->h != actor_side->h ||
+      critic_side->L != actor_side->L || critic_side->o != actor_side->o || critic_side->m != actor_side->m)
+    return fail(SPZ_EINVAL, "spz_split_exchange: learners of different configurations");
+  spz_learner* C = critic_side;
+  spz_learner* A = actor_side;
+  {
+    DeviceGuard g1(A->device);
+    SPZ_CUDA_TRY(cudaStreamSynchronize(A->stream));
+  }
+  DeviceGuard dg(C->device);
+  SPZ_CUDA_TRY(cudaStreamSynchronize(C->stream));
+  auto cp = [&](spz_learner* dst, spz_learner* src, int64_t off, int64_t n) {
+    return cudaMemcpyPeerAsync(dst->P + off, dst->device, src->P + off, src->device, n * sizeof(float), C->stream);
+  };
+  SPZ_CUDA_TRY(cp(C, A, A->pbase[NET_ACTOR], A->net[NET_ACTOR].np));
+  SPZ_CUDA_TRY(cp(C, A, A->p_log_alpha, 1));
+  if (A->td3) SPZ_CUDA_TRY(cp(C, A, A->pbase[NET_ACTORT], A->net[NET_ACTORT].np));
+  SPZ_CUDA_TRY(cp(A, C, C->pbase[NET_Q1], C->pbase[NET_Q2] + C->net[NET_Q2].np - C->pbase[NET_Q1]));
+  SPZ_CUDA_TRY(cudaStreamSynchronize(C->stream));
+  for (spz_learner* Lr : {C, A}) {
+    DeviceGuard g2(Lr->device);
+    if (Lr->bf16)
+      launch_pdl(shadow_refresh_kernel<__nv_bfloat16>, dim3(64, Lr->n_shadow_recv), dim3(256), 0, Lr->stream,
+                 (const ShadowEntry*)Lr->d_shadow_recv, Lr->n_shadow_recv, (const float*)Lr->P, static_cast<__nv_bfloat16*>(Lr->S));
+    else
+      launch_pdl(shadow_refresh_kernel<float>, dim3(64, Lr->n_shadow_recv), dim3(256), 0, Lr->stream,
+                 (const ShadowEntry*)Lr->d_shadow_recv, Lr->n_shadow_recv, (const float*)Lr->P, static_cast<float*>(Lr->S));
+    SPZ_CUDA_TRY(cudaGetLastError());
+    SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  }
   return SPZ_OK;
 }
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "spz_replay_records", "spz_replay_destroy", "spz_config_default", "spz_nccl_unique_id", "spz_learner_create",
     "spz_update", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
-    "spz_diag_gemm_bf16",
+    "spz_diag_gemm_bf16", "spz_split_exchange",
 ]
 
 
@@ -116,6 +116,7 @@ def lib():
             "spz_learner_debug_buffer": (ctypes.c_int, [P, ctypes.c_char_p, P, I64, ctypes.POINTER(I64),
                                                         ctypes.POINTER(I32)]),
             "spz_learner_destroy": (None, [P]),
+            "spz_split_exchange": (ctypes.c_int, [P, P]),
             "spz_diag_gemm_bf16": (ctypes.c_int, [I32, I32, I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, I64]),
         }
         for name, (res, args) in sig.items():
@@ -272,6 +273,10 @@ def spz_learner_debug_buffer(learner, name):
 
 def spz_learner_destroy(learner):
     lib().spz_learner_destroy(learner)
+
+
+def spz_split_exchange(critic_learner, actor_learner):
+    _check(lib().spz_split_exchange(critic_learner, actor_learner))
 
 
 def spz_diag_gemm_bf16(M, N, K, A, lda, a_mn, B, ldb, b_mn, C, ldc, tensor_cores=True, splits=1, k_per_split=0,

@@ -49,9 +49,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=None)
-    ap.add_argument("--mode", default="dp", choices=["dp", "replicas"],
+    ap.add_argument("--mode", default="dp", choices=["dp", "split", "replicas"],
                     help="N > 1: dp = one row-sharded learner group (global batch B*N, NCCL gradient allreduce); "
-                         "replicas = N independent learners")
+                         "split = actor/critic model parallelism (critic group ranks [0, N*c), actor group the rest; "
+                         "each group row-shards the global batch B*N/2); replicas = N independent learners")
+    ap.add_argument("--critic-frac", type=float, default=0.5,
+                    help="split mode: fraction of the ranks in the critic group (SAC critic:actor work ~1.7:1)")
     return ap.parse_args()
 
 
@@ -205,7 +208,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     assert a.warmup >= 3, "timing rules: at least 3 warm-up steps"
     dp = world > 1 and a.mode == "dp"
-    GB = B * world if dp else B  # the batch one learner (group) consumes per update
+    split = world > 1 and a.mode == "split"
+    # the batch one learner group consumes per update: dp B*N; split B*N/2 (both groups read every row)
+    GB = B * world if dp else (B * world // 2 if split else B)
 
     # ring filled to capacity with synthetic transitions (ring bytes > L2, so gathers hit HBM)
     C = w.capacity
@@ -215,10 +220,14 @@ def main():
         tr = synthdata.workload_transitions(w, n=min(chunk, C - s0), seed=synthdata.DATA_SEED + s0)
         ring.push(**tr)
     kw = {}
-    if dp:
+    if dp or split:
         kw = dict(world_size=world, rank=rank, nccl_unique_id=broadcast_bytes(spz.spz_nccl_unique_id() if rank == 0 else None))
+    if split:
+        nc = min(world - 1, max(1, int(round(world * a.critic_frac))))
+        kw.update(role=spz.SPZ_ROLE_CRITIC if rank < nc else spz.SPZ_ROLE_ACTOR, n_critic_ranks=nc,
+                  n_actor_ranks=world - nc)
     lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=GB,
-                      device=local, seed=synthdata.SAMPLE_SEED + (0 if dp else rank), **kw)
+                      device=local, seed=synthdata.SAMPLE_SEED + (0 if (dp or split) else rank), **kw)
     stream = torch.cuda.Stream(device=local)
     lrn.set_stream(stream.cuda_stream)
 
@@ -242,7 +251,9 @@ def main():
         ms = t.item()
         dist.barrier()
     torch.cuda.synchronize()
-    frames = B * a.steps * world  # dp: global batch B*N per update; replicas: N learners x B
+    # transitions consumed: dp B*N per update; split B*N/2 per update (counted once, though both groups read it);
+    # replicas N learners x B
+    frames = GB * a.steps if (dp or split) else B * a.steps * world
     value = frames / (ms / 1e3)
     ms_per_step = ms / a.steps
 
@@ -296,7 +307,8 @@ def main():
             t = torch.tensor([dt], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = t.item()
-        e2e = {"value": B * K2 * world / dt, "unit": "frames/s", "h2d_bytes_per_step": GB * R_fields * 4 * world,
+        e2e = {"value": (GB if (dp or split) else B * world) * K2 / dt, "unit": "frames/s",
+               "h2d_bytes_per_step": GB * R_fields * 4 * world,
                "d2h_bytes_per_step": 64 + 32 + 4, "steps": K2,
                "note": "per step: spz_replay_push of B fresh host transitions (pinned) + spz_update(B, 1) with its stats read-back"}
 
@@ -314,10 +326,11 @@ def main():
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_per_step, "updates_per_s": 1e3 / ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": a.precision, "data": "synthetic",
-            "config": {"workload": w.name, "global_batch": B * world, "batch_per_gpu": B, "algo": w.algo,
-                       "mode": ("dp-nccl" if dp else "replicas") if world > 1 else "single",
+            "config": {"workload": w.name, "global_batch": GB if (dp or split) else B * world,
+                       "batch_per_gpu": B if not split else GB // max(1, (world // 2)), "algo": w.algo,
+                       "mode": ("dp-nccl" if dp else "split-nccl" if split else "replicas") if world > 1 else "single",
                        "hidden": f"{w.n_hidden}x{w.hidden}", "obs_dim": w.obs_dim, "act_dim": w.act_dim,
-                       "ring": C, "parallelism": (f"dp{world}" if dp else f"replicas{world}") if world > 1 else "single",
+                       "ring": C, "parallelism": (f"dp{world}" if dp else f"split{world}" if split else f"replicas{world}") if world > 1 else "single",
                        "l2": f"ring {C * ((2 * w.obs_dim + w.act_dim + 2 + 3) // 4 * 4) * 4 / 1e6:.0f} MB > 126 MB L2; fresh random indices each step"},
             "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(), "gpu_launches": launches, "last_stats": stats,

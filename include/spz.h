@@ -129,7 +129,9 @@ typedef struct {
   const uint8_t* nccl_unique_id;   /* 128 bytes, identical on all ranks; NULL if world_size == 1 */
   int32_t use_graph;               /* 1 (default): replay the step as a CUDA graph */
   int32_t comm_mode;               /* world_size > 1: 0 = NCCL allreduce (default); 1 = no exchange
-                                      (diagnostics: each rank applies its own shard's gradient) */
+                                      (diagnostics: each rank applies its own shard's gradient);
+                                      2 = (world_size 1 only) run the sharded path through a
+                                      single-rank NCCL communicator (diagnostics) */
 } spz_config;
 
 /* Fill *out with the defaults above for (algo, o, m); h = 256, L = 2, max_batch 8192. */

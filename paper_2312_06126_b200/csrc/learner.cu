@@ -649,7 +649,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     }
     // row-sharded groups reduce their split partials into one contiguous buffer and all-reduce it
     // together with the loss totals before the (identical) optimizer step on every rank
-    const bool sharded = Lr->gsize > 1;
+    const bool sharded = Lr->gsize > 1 || Lr->cfg.comm_mode == 2;
     // ---- a9: fused Adam + Polyak (+ shadow refresh) over every trained tensor
     {
       std::vector<AdamTensor> tens;
@@ -717,7 +717,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         ops.push_back({"grad_reduce", [=](cudaStream_t st) {
                          return launch_pdl(reduce_partials_kernel, dim3(nsg), dim3(256), 0, st, dt, ds, Gr);
                        }});
-        if (Lr->cfg.comm_mode == 0) {
+        if (Lr->cfg.comm_mode == 0 || Lr->cfg.comm_mode == 2) {
           const Comm cm = Lr->gcomm;
           const size_t n = (size_t)Lr->Gred_total;
           double* ss = Lr->statsum;
@@ -1054,12 +1054,21 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->statsum, 8 * sizeof(double)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->tickets, 8 * sizeof(unsigned)));
   Lr->debug.push_back({"statsum", Lr->statsum, 8 * sizeof(double), 8});
-  if (Lr->gsize > 1) {
+  if (Lr->gsize > 1 || cfg->comm_mode == 2) {
     int64_t tot = 0;
     for (auto& t : slots) tot += round_up(t.numel, 16);
     Lr->Gred_total = tot + 16;
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->Gred, Lr->Gred_total * sizeof(float)));
     Lr->debug.push_back({"Gred", Lr->Gred, (size_t)Lr->Gred_total * 4, 4});
+  }
+  if (cfg->comm_mode == 2) {
+    // diagnostic: a single-rank NCCL group runs the sharded path (partials -> reduce -> allreduce -> Adam)
+    if (cfg->world_size != 1 || Lr->split) return fail(SPZ_EINVAL, "spz_learner_create: comm_mode 2 needs world_size 1 and role ALL");
+    uint8_t uid[128];
+    SPZ_TRY(spz_nccl_unique_id(uid));
+    SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+    SPZ_TRY(comm_init(&Lr->comm, uid, 1, 0));
+    Lr->gcomm = Lr->comm;
   }
   if (cfg->world_size > 1 && cfg->comm_mode == 0) {
     SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));

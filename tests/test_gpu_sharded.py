@@ -119,3 +119,19 @@ def test_nccl_group_matches_single_gpu():
     s1 = single.update(B, K)
     assert rel(res[0][2], single.get("actor")) < 2e-2 and rel(res[0][3], single.get("q1")) < 2e-2
     assert abs(res[0][1]["critic_loss"] - s1["critic_loss"]) < 2e-2 * abs(s1["critic_loss"])
+
+
+@pytest.mark.parametrize("algo,precision", [("sac", "bf16"), ("td3", "fp32")])
+def test_single_rank_nccl_path_equals_plain_learner(algo, precision):
+    """comm_mode 2: the sharded code path (partials -> contiguous reduce -> in-graph ncclAllReduce over a
+    one-rank communicator -> Adam from the reduced buffer) gives bit-identical results to the plain path."""
+    o, m, h, L, B, C = 22, 6, 256, 2, 2048, 20_000
+    g, _ = make_rings(o, m, C)
+    p = synthdata.init_params(o, m, h, L, algo=algo)
+    plain = make_learner(g, p, algo, precision, h, L, B)
+    nccl = make_learner(g, p, algo, precision, h, L, B, comm_mode=2)
+    s1 = plain.update(B, 4)
+    s2 = nccl.update(B, 4)
+    for n in ("actor", "q1", "q2", "q1_targ"):
+        assert np.array_equal(plain.get(n), nccl.get(n)), n
+    assert s1["critic_loss"] == s2["critic_loss"]

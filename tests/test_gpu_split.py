@@ -51,3 +51,50 @@ def test_split_roles_match_single_and_oracle(algo, precision):
         assert rel(act.get("actor_targ"), st.actor_targ) <= tol
         assert np.array_equal(crit.get("actor_targ"), act.get("actor_targ"))
     assert crit.counters()["t_actor"] == 0 and act.counters()["t_critic"] == 0
+
+
+def _split_worker(rank, world, port, q, B, K, algo):
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2312_06126_b200.dist import broadcast_bytes
+    uid = broadcast_bytes(spz.spz_nccl_unique_id() if rank == 0 else None)
+    o, m, h, L, C = 22, 6, 256, 2, 50_000
+    tr = synthdata.transitions("locomotion", o, m, C)
+    g = spz.Replay(o, m, C, device=rank)
+    g.push(**tr)
+    p = synthdata.init_params(o, m, h, L, algo=algo)
+    role = spz.SPZ_ROLE_CRITIC if rank < world // 2 else spz.SPZ_ROLE_ACTOR
+    lrn = make_learner(g, p, algo, "bf16", h, L, B, device=rank, world_size=world, rank=rank, role=role,
+                       n_critic_ranks=world // 2, n_actor_ranks=world - world // 2, nccl_unique_id=uid)
+    lrn.update(B, K)
+    q.put((rank, lrn.get("actor"), lrn.get("q1")))
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="NCCL split test needs >= 2 GPUs")
+@pytest.mark.parametrize("algo", ["sac", "td3"])
+def test_nccl_split_roles_match_single_gpu(algo):
+    """Critic group and actor group on different GPUs (in-graph NCCL exchange) == one co-located learner."""
+    import os
+    import torch.multiprocessing as mp
+    world = 4 if torch.cuda.device_count() >= 4 else 2
+    B, K = 4096, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + os.getpid() % 1000
+    ps = [ctx.Process(target=_split_worker, args=(r, world, port, q, B, K, algo)) for r in range(world)]
+    for pr in ps:
+        pr.start()
+    res = sorted([q.get(timeout=600) for _ in ps], key=lambda x: x[0])
+    for pr in ps:
+        pr.join(timeout=60)
+    for r in range(1, world):  # every rank holds identical (exchanged) parameters
+        assert np.array_equal(res[r][1], res[0][1]) and np.array_equal(res[r][2], res[0][2])
+    o, m, h, L, C = 22, 6, 256, 2, 50_000
+    g, _ = make_rings(o, m, C)
+    single = make_learner(g, synthdata.init_params(o, m, h, L, algo=algo), algo, "bf16", h, L, B)
+    single.update(B, K)
+    assert rel(res[0][1], single.get("actor")) < 2e-2 and rel(res[0][2], single.get("q1")) < 2e-2

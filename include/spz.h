@@ -225,7 +225,12 @@ spz_status spz_learner_debug_buffer(spz_learner* L, const char* name, void* host
 void spz_learner_destroy(spz_learner* L);
 
 /* ------------------------------------------------------------------ diagnostics
- * The dense-layer GEMM of the update on its own, for kernel tests: on `device`,
+ * spz_diag_tc_trace: enable (on = 1) / disable per-tile %globaltimer stamps in the tcgen05 GEMM
+ * (160 CTAs x 8 tiles x 4 events: producer start, MMA issued, accumulator ready, epilogue done) and,
+ * if host_out != NULL, copy up to n stamps of the last traced launch.  Synchronous. */
+spz_status spz_diag_tc_trace(int32_t device, int32_t on, uint64_t* host_out, int32_t n);
+
+/* The dense-layer GEMM of the update on its own, for kernel tests: on `device`,
  * C[m, n] (fp32, row pitch ldc) = sum_k A(m, k) B(n, k) over bf16 device operands with
  * A(m,k) = a_mn ? A[k*lda + m] : A[m*lda + k] and B(n,k) = b_mn ? B[k*ldb + n] : B[n*ldb + k].
  * With splits > 1 the contraction is cut into chunks of k_per_split (multiple of 64) and

@@ -77,4 +77,14 @@ spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, i
   return SPZ_OK;
 }
 
+spz_status spz_diag_tc_trace(int32_t device, int32_t on, uint64_t* host_out, int32_t n) {
+  spz_status st = spz::check_device(device);
+  if (st != SPZ_OK) return st;
+  spz::DeviceGuard dg(device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = spz::tc_trace(on, reinterpret_cast<unsigned long long*>(host_out), n);
+  if (e != cudaSuccess) return spz::fail(SPZ_ECUDA, std::string("spz_diag_tc_trace: ") + cudaGetErrorString(e));
+  return SPZ_OK;
+}
+
 }  // extern "C"

@@ -514,7 +514,25 @@ struct AdamTensor {
   int64_t t_off;      // target master offset, -1 if none
   int64_t ts_off;     // target shadow offset, -1 if none
   int64_t red_off;    // offset of this tensor in the contiguous (all-reduced) gradient buffer
+  int64_t pstride;    // elements between split partials
+  int32_t pld;        // partial row pitch: weight (r, c) at r * pld + c; bias i at i * pld
+  int32_t pad_;
 };
+
+// Split-K partial sum of element i of tensor tn (fixed split order).
+__device__ __forceinline__ float partial_sum(const AdamTensor& tn, int64_t i) {
+  int64_t idx;
+  if (tn.cols > 0) {
+    const int64_t row = i / tn.cols;
+    idx = row * tn.pld + (i - row * tn.cols);
+  } else {
+    idx = i * tn.pld;
+  }
+  float g = 0.f;
+#pragma unroll 8
+  for (int s = 0; s < tn.n_partials; ++s) g += __ldg(tn.partials + (int64_t)s * tn.pstride + idx);
+  return g;
+}
 struct AdamSegment {
   int32_t tensor;
   int32_t count;
@@ -573,8 +591,7 @@ __global__ void __launch_bounds__(256) adam_polyak_kernel(const AdamTensor* __re
       if (tn.opt == 2) {
         g = g_alpha;  // log-alpha gradient -(mean log pi~ + H_bar) from the (group) totals
       } else {
-#pragma unroll 8
-        for (int s = 0; s < tn.n_partials; ++s) g += __ldg(tn.partials + (int64_t)s * tn.numel + i);
+        g = partial_sum(tn, i);
       }
       if (!isfinite(g)) {
         atomicExch(flag, 2);
@@ -629,10 +646,7 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const AdamTensor* 
   const AdamTensor tn = tensors[sg.tensor];
   for (int k = threadIdx.x; k < sg.count; k += blockDim.x) {
     const int64_t i = sg.start + k;
-    float g = 0.f;
-#pragma unroll 8
-    for (int s = 0; s < tn.n_partials; ++s) g += __ldg(tn.partials + (int64_t)s * tn.numel + i);
-    Gred[tn.red_off + i] = g;
+    Gred[tn.red_off + i] = partial_sum(tn, i);
   }
 }
 

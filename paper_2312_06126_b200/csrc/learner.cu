@@ -190,7 +190,8 @@ static std::vector<TensorSlot> trained_tensors(spz_learner* Lr) {
     const NetLayout& n = Lr->net[id];
     for (int l = 0; l < n.nl; ++l) {
       const bool head_vec = (id == NET_Q1 || id == NET_Q2) && l == n.nl - 1;  // N = 1 head: column sums
-      v.push_back({id, l, true, (int64_t)n.out[l] * n.in[l], 0, head_vec ? Sb : Sw});
+      // weight partials keep a 16-byte row pitch (TMA stores): out x round_up(in, 4)
+      v.push_back({id, l, true, (int64_t)n.out[l] * (head_vec ? n.in[l] : round_up(n.in[l], 4)), 0, head_vec ? Sb : Sw});
       v.push_back({id, l, false, (int64_t)n.out[l], 0, Sb});
     }
   };
@@ -555,10 +556,10 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           g.B = l == 0 ? Lr->Xc : Lr->Aon[i][l - 1];
           g.ldb = l == 0 ? ldc : h;
           g.C = Lr->G + slot_of(NET_Q1 + i, l, true).g_off;
-          g.ldc = cn.in[l];
+          g.ldc = (int)round_up(cn.in[l], 4);
           g.M = h;
           g.N = cn.in[l];
-          g.split_stride = (int64_t)h * cn.in[l];
+          g.split_stride = (int64_t)h * g.ldc;
           wgrads.push_back(g);
         }
       for (int i = 0; i < (do_critic ? 2 : 0); ++i) {
@@ -611,10 +612,10 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         g.B = l == 0 ? (const void*)Ta(Lr->Xa, Bl, lda) : (const void*)Ta(Lr->Aact[l - 1], Bl, h);
         g.ldb = l == 0 ? lda : h;
         g.C = Lr->G + slot_of(NET_ACTOR, l, true).g_off;
-        g.ldc = an.in[l];
+        g.ldc = (int)round_up(an.in[l], 4);
         g.M = an.out[l];
         g.N = an.in[l];
-        g.split_stride = (int64_t)an.out[l] * an.in[l];
+        g.split_stride = (int64_t)an.out[l] * g.ldc;
         wgrads.push_back(g);
       }
       for (int l = 0; l <= L; ++l)
@@ -658,10 +659,12 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         const NetLayout& n = Lr->net[s.net];
         AdamTensor t{};
         t.p_off = Lr->pbase[s.net] + (s.weight ? n.w[s.layer] : n.b[s.layer]);
-        t.numel = s.numel;
-        t.partials = Lr->G + s.g_off;
         const bool head_vec = (s.net == NET_Q1 || s.net == NET_Q2) && s.layer == n.nl - 1;
+        t.numel = s.weight ? (int64_t)n.out[s.layer] * n.in[s.layer] : n.out[s.layer];
+        t.partials = Lr->G + s.g_off;
         t.n_partials = s.weight && !head_vec ? Sw : Sb;
+        t.pld = s.weight ? (head_vec ? n.in[s.layer] : (int)round_up(n.in[s.layer], 4)) : 1;
+        t.pstride = s.weight ? (int64_t)n.out[s.layer] * t.pld : n.out[s.layer];
         t.opt = s.net == NET_ACTOR ? 1 : 0;
         t.cols = s.weight ? n.in[s.layer] : 0;
         t.ld = n.ld[s.layer];
@@ -707,6 +710,8 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           if (t.opt == 2) continue;  // log alpha: gradient computed from the all-reduced totals
           t.partials = Lr->Gred + t.red_off;
           t.n_partials = 1;
+          t.pld = t.cols > 0 ? t.cols : 1;  // dense
+          t.pstride = t.numel;
         }
         SPZ_CUDA_TRY(cudaMemcpyAsync(dt2, tens2.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
         SPZ_CUDA_TRY(cudaMemcpyAsync(dt, tens.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
@@ -1056,7 +1061,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   Lr->debug.push_back({"statsum", Lr->statsum, 8 * sizeof(double), 8});
   if (Lr->gsize > 1 || cfg->comm_mode == 2) {
     int64_t tot = 0;
-    for (auto& t : slots) tot += round_up(t.numel, 16);
+    for (auto& t : slots) tot += round_up(t.numel, 16);  // >= the dense tensor sizes
     Lr->Gred_total = tot + 16;
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->Gred, Lr->Gred_total * sizeof(float)));
     Lr->debug.push_back({"Gred", Lr->Gred, (size_t)Lr->Gred_total * 4, 4});

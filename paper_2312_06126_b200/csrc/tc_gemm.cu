@@ -14,6 +14,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <vector>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -25,7 +26,11 @@ namespace spz {
 namespace {
 
 constexpr int BM = 128, BK = 64, STAGES = 4;
-constexpr int NUM_EPI_WARPS = 8, NTHREADS = 64 + NUM_EPI_WARPS * 32;  // producer, MMA, 8 epilogue warps
+// producer warp, MMA warp, WPQ epilogue warps per TMEM lane quarter (each a slice of the columns)
+#ifndef SPZ_TC_WPQ
+#define SPZ_TC_WPQ 2
+#endif
+constexpr int WPQ = SPZ_TC_WPQ, NUM_EPI_WARPS = 4 * WPQ, NTHREADS = 64 + NUM_EPI_WARPS * 32;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
 struct TcParams {
@@ -34,11 +39,29 @@ struct TcParams {
   int total_tiles;  // persistent schedule
   int tile0[MAX_GROUPS + 1];
   int mtiles[MAX_GROUPS], ntiles[MAX_GROUPS];
+  int trace;      // diagnostics: record per-tile timestamps in this launch
+  int tma_out;    // 1: outputs leave through TMA bulk tensor stores (tc[] valid), 0: direct stores
+  int out_bytes;  // 2 (bf16) or 4 (fp32) output elements
   CUtensorMap ta[MAX_GROUPS];
   CUtensorMap tb[MAX_GROUPS];
+  CUtensorMap tc[MAX_GROUPS];  // C as [splits][M][N]; box = 64 bytes x 32 rows, 64-byte swizzle
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Diagnostics: per-CTA, per-tile %globaltimer stamps (spz_diag_tc_trace).  Event e of the i-th tile of
+// CTA c lands in g_trace[(c * TRACE_TILES + i) * 4 + e]: 0 producer starts the tile, 1 MMA issue done,
+// 2 epilogue sees the accumulator, 3 epilogue done.
+constexpr int TRACE_CTAS = 160, TRACE_TILES = 8;
+__device__ unsigned long long g_trace[TRACE_CTAS * TRACE_TILES * 4];
+#define trace(tile_i, ev) trace_(p.trace, tile_i, ev)
+__device__ __forceinline__ void trace_(int on, int tile_i, int ev) {
+  if (on && blockIdx.x < TRACE_CTAS && tile_i < TRACE_TILES) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[(blockIdx.x * TRACE_TILES + tile_i) * 4 + ev] = t;
+  }
+}
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -64,6 +87,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -231,6 +265,51 @@ __device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, %1;
 // Persistent, warp-specialized: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the TMA producer
 // and the MMA issuer run ahead into the next tile while the epilogue drains the previous one
 // from the other TMEM accumulator buffer.
+// Output values of 16 accumulator columns (TMA-store path): v is overwritten with what C receives.
+__device__ __forceinline__ float epi16_vals(int epi, int n, int N, float (&v)[16], const float* __restrict__ bias,
+                                            const float* __restrict__ dotw, uint32_t& bits) {
+  float dot = 0.f;
+  if (epi == EPI_BIAS_RELU) {
+    uint32_t b = 0u;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float pre = v[j] + bias[j];
+      v[j] = fmaxf(pre, 0.f);
+      b |= (pre > 0.f && n + j < N ? 1u : 0u) << j;
+    }
+    if (dotw) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) dot = fmaf(v[j], dotw[j], dot);  // dotw is zero past N
+    }
+    bits = b;
+  } else if (epi == EPI_MASK_BITS) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = (bits >> j) & 1u ? v[j] : 0.f;
+  } else if (epi == EPI_BIAS_F32) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] += bias[j];
+  }
+  return dot;
+}
+
+// Write 16 output values of row `row` into a 64-byte-row staging block (64-byte TMA swizzle:
+// 16-byte unit u of row r sits at unit u ^ ((r >> 1) & 3)); `unit0` = first 16-byte unit.
+__device__ __forceinline__ void stage16(uint8_t* blk, int row, int unit0, const float (&v)[16], bool bf16) {
+  uint8_t* rp = blk + row * 64;
+  const int sw = (row >> 1) & 3;
+  if (bf16) {
+    const uint4 u0 = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+    const uint4 u1 = make_uint4(pack_bf16(v[8], v[9]), pack_bf16(v[10], v[11]), pack_bf16(v[12], v[13]),
+                                pack_bf16(v[14], v[15]));
+    *reinterpret_cast<uint4*>(rp + (((unit0 + 0) ^ sw) << 4)) = u0;
+    *reinterpret_cast<uint4*>(rp + (((unit0 + 1) ^ sw) << 4)) = u1;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<float4*>(rp + (((unit0 + k) ^ sw) << 4)) = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  }
+}
+
 template <int BN, bool AMN, bool BMN>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
   constexpr int B_BYTES = BN * BK * 2;
@@ -250,8 +329,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* bias_s = reinterpret_cast<float*>(tmem_slot + 4);     // [BN] epilogue bias of the current tile
   float* dot_s = bias_s + BN;                                  // [BN] fused row-dot weights
-  float* dotpart = dot_s + BN;                                 // [2][BM] row-dot halves
-  uint32_t* mask_s = reinterpret_cast<uint32_t*>(dotpart + 2 * BM);  // [BM][MSTR] packed ReLU masks
+  float* dotpart = dot_s + BN;                                 // [WPQ][BM] row-dot slices
+  uint32_t* mask_s = reinterpret_cast<uint32_t*>(dotpart + WPQ * BM);  // [BM][MSTR] packed ReLU masks
+  // per epilogue warp: two 32-row x 64-byte staging blocks for the TMA stores (1024-byte aligned)
+  uint8_t* stage_s = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(mask_s + BM * MSTR) + 1023) & ~uintptr_t(1023));
 
   const GemmArgs& a = p.a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -285,12 +367,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   // everything above overlapped the previous kernel (PDL); from here on we read its outputs
   pdl_wait();
   pdl_launch();
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) g_trace[TRACE_CTAS * TRACE_TILES * 4 - 1] = (unsigned long long)T;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer: a continuous stream of k-blocks over this CTA's tiles
-      int kg = 0;
-      for (int t = blockIdx.x; t < T; t += gridDim.x) {
+      int kg = 0, tile_p = 0;
+      for (int t = blockIdx.x; t < T; t += gridDim.x, ++tile_p) {
+        trace(tile_p, 0);
         const TileInfo ti = decode_tile(p, t, BN);
         const int k_begin = ti.split * a.k_per_split;
         const int k_end = min(a.K, k_begin + a.k_per_split);
@@ -347,6 +431,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
         }
         umma_commit(&acc_full[b]);  // accumulator complete (immediately if the split is empty)
+        trace(tile_i, 1);
       }
     }
   } else {
@@ -356,12 +441,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     const int q = warp & 3;
     const int hh = e >> 2;
     const bool head = a.epi == EPI_SAC_HEAD || a.epi == EPI_TD3_HEAD;
+    // 16-column chunks per warp: whole 32-bit mask words per warp (>= 2 chunks)
+    constexpr int CPW = (BN / 16) / WPQ >= 2 ? (BN / 16) / WPQ : 2;
     const bool split_cols = BN >= 64 && !head;
-    const int c_lo = split_cols ? hh * (BN / 32) : 0;            // first 16-column chunk of this warp
-    const int c_hi = split_cols ? (hh + 1) * (BN / 32) : (hh == 0 ? BN / 16 : 0);
+    const int c_lo = split_cols ? min(hh * CPW, BN / 16) : 0;    // first 16-column chunk of this warp
+    const int c_hi = split_cols ? min((hh + 1) * CPW, BN / 16) : (hh == 0 ? BN / 16 : 0);
     const int r = q * 32 + lane;  // tile row of this thread
     uint32_t* mrow = mask_s + r * MSTR;
     int tile_i = 0;
+    int st_count = 0;  // TMA store blocks issued by this warp
     for (int t = blockIdx.x; t < T; t += gridDim.x, ++tile_i) {
       const TileInfo ti = decode_tile(p, t, BN);
       const GemmGroup& g = a.g[ti.grp];
@@ -390,6 +478,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       const int b = tile_i & 1;
       mbar_wait(&acc_full[b], ((uint32_t)tile_i >> 1) & 1u);
       tc_fence_after();
+      if (e == 0 && lane == 0) trace(tile_i, 2);
       const uint32_t trow = tmem + (uint32_t)b * ACC_COLS + ((uint32_t)(q * 32) << 16);
       if (head) {
         if constexpr (BN <= 64) {
@@ -414,6 +503,73 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[b]);
+      } else if (p.tma_out) {
+        // ---- outputs staged in shared memory, written by TMA bulk tensor stores (64-byte x 32-row
+        //      blocks, double-buffered per warp)
+        float dot = 0.f;
+        const bool obf = p.out_bytes == 2;
+        const int cpb = obf ? 2 : 1;  // 16-column chunks per 64-byte store block
+        uint8_t* wstage = stage_s + e * 4096;
+#pragma unroll 1
+        for (int c = c_lo; c < c_hi; c += cpb) {
+          if (n0 + c * 16 >= g.N) break;  // warp-uniform
+          if (st_count >= 2) {
+            if (lane == 0) bulk_wait_read1();  // the block issued two stores ago has left this slot
+            __syncwarp();
+          }
+          uint8_t* blk = wstage + (st_count & 1) * 2048;
+          for (int cc = 0; cc < cpb; ++cc) {
+            const int ch = c + cc;
+            const int n = n0 + ch * 16;
+            float v[16];
+            if (nkb > 0 && n < g.N) {
+              tmem_ld16(trow + ch * 16, v);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = 0.f;
+            }
+            uint32_t bits = mask_in ? (mrow[ch >> 1] >> (16 * (ch & 1))) & 0xFFFFu : 0u;
+            const float d = epi16_vals(a.epi, n, g.N, v, bias_s + ch * 16, has_dot ? dot_s + ch * 16 : nullptr, bits);
+            if (m < g.M) {
+              dot += d;
+              if (mask_out) mrow[ch >> 1] |= bits << (16 * (ch & 1));
+            }
+            stage16(blk, lane, cc * (obf ? 2 : 4), v, obf);
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&p.tc[ti.grp], blk, n0 + c * 16, ti.m0 + q * 32, ti.split);
+            bulk_commit();
+          }
+          ++st_count;
+        }
+        if (e == 0 && lane == 0) trace(tile_i, 3);
+        // accumulator buffer drained by this warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        if (has_dot) {
+          dotpart[hh * BM + r] = dot;
+          epi_bar(2);
+          if (hh == 0 && m < g.M) {
+            float tot = dot;
+            if (split_cols) {
+              tot = 0.f;
+              for (int k = 0; k < WPQ; ++k) tot += dotpart[k * BM + r];  // fixed order
+            }
+            g.dot_out[m] = tot + g.dot_b[0];
+          }
+        }
+        if (mask_out && m < g.M) {
+          const int w_lo = c_lo / 2, w_hi = min((c_hi + 1) / 2, (g.N - n0 + 31) / 32);
+          uint32_t* dst = g.mask_out + (int64_t)m * g.mask_ld + n0 / 32;
+          if (w_hi - w_lo == 4 && ((reinterpret_cast<uintptr_t>(dst + w_lo) & 15) == 0)) {
+            *reinterpret_cast<uint4*>(dst + w_lo) = make_uint4(mrow[w_lo], mrow[w_lo + 1], mrow[w_lo + 2], mrow[w_lo + 3]);
+          } else {
+            for (int i = w_lo; i < w_hi; ++i) dst[i] = mrow[i];
+          }
+        }
       } else {
         float dot = 0.f;
 #pragma unroll 1
@@ -440,13 +596,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         if (has_dot) {
           dotpart[hh * BM + r] = dot;
           epi_bar(2);
-          if (hh == 0 && m < g.M) g.dot_out[m] = (split_cols ? dotpart[r] + dotpart[BM + r] : dot) + g.dot_b[0];
+          if (hh == 0 && m < g.M) {
+            float tot = dot;
+            if (split_cols) {
+              tot = 0.f;
+              for (int k = 0; k < WPQ; ++k) tot += dotpart[k * BM + r];  // fixed order
+            }
+            g.dot_out[m] = tot + g.dot_b[0];
+          }
         }
+        if (e == 0 && lane == 0) trace(tile_i, 3);
         if (mask_out && m < g.M) {
           const int w_lo = c_lo / 2, w_hi = min((c_hi + 1) / 2, (g.N - n0 + 31) / 32);
           uint32_t* dst = g.mask_out + (int64_t)m * g.mask_ld + n0 / 32;
           if (w_hi - w_lo == 4 && ((reinterpret_cast<uintptr_t>(dst + w_lo) & 15) == 0)) {
             *reinterpret_cast<uint4*>(dst + w_lo) = make_uint4(mrow[w_lo], mrow[w_lo + 1], mrow[w_lo + 2], mrow[w_lo + 3]);
+          } else if (w_hi - w_lo == 2 && ((reinterpret_cast<uintptr_t>(dst + w_lo) & 7) == 0)) {
+            *reinterpret_cast<uint2*>(dst + w_lo) = make_uint2(mrow[w_lo], mrow[w_lo + 1]);
           } else {
             for (int i = w_lo; i < w_hi; ++i) dst[i] = mrow[i];
           }
@@ -454,6 +620,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       }
     }
   }
+  if (warp >= 2 && lane == 0) bulk_wait_all();  // every TMA store of this warp has completed
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -463,6 +630,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
 }
 
 // ------------------------------------------------------------------ host side
+// tile tracing: 0 off; 1 every launch records (the last one wins); k >= 2 only the (k-2)-th launch from now
+int g_trace_mode = 0;
+long g_trace_count = 0;
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -502,15 +673,16 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 
 template <int BN>
 constexpr int smem_extras() {
-  return 1024 /* alignment */ + 128 /* barriers + TMEM slot */ + BN * 8 /* bias, dot */ + 2 * BM * 4 /* dot halves */ +
-         BM * ((BN + 31) / 32 + 1) * 4 /* masks */;
+  return 1024 /* alignment */ + 128 /* barriers + TMEM slot */ + BN * 8 /* bias, dot */ + WPQ * BM * 4 /* dot slices */ +
+         BM * ((BN + 31) / 32 + 1) * 4 /* masks */ + 1024 + NUM_EPI_WARPS * 4096 /* TMA store staging */;
 }
 
 template <int BN, bool AMN, bool BMN>
 cudaError_t launch(TcParams& p, int maxM, cudaStream_t st) {
   constexpr int STAGE = A_BYTES + BN * BK * 2;
-  constexpr int SMEM_MAX = STAGES * STAGE + smem_extras<BN>();
-  static_assert(SMEM_MAX <= 227 * 1024, "shared memory budget");
+  constexpr int MAX_ST = std::min(STAGES, (227 * 1024 - smem_extras<BN>()) / STAGE);
+  static_assert(MAX_ST >= 1, "shared memory budget");
+  constexpr int SMEM_MAX = MAX_ST * STAGE + smem_extras<BN>();
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
@@ -541,9 +713,11 @@ cudaError_t launch(TcParams& p, int maxM, cudaStream_t st) {
   const int budget = 227 * 1024 / per_sm;
   const int kspan = p.a.splits > 1 ? p.a.k_per_split : p.a.K;
   const int want = (int)std::min<int64_t>(STAGES, std::max<int64_t>(1, cdiv(kspan, BK)));
-  p.stages = std::max(1, std::min(want, (budget - smem_extras<BN>()) / STAGE));
+  p.stages = std::max(1, std::min(std::min(want, MAX_ST), (budget - smem_extras<BN>()) / STAGE));
   const int smem = p.stages * STAGE + smem_extras<BN>();
   const int grid = std::min(T, num_sms() * per_sm);
+  p.trace = g_trace_mode == 1 || (g_trace_mode >= 2 && g_trace_count == g_trace_mode - 2);
+  ++g_trace_count;
   return launch_pdl(tc_gemm_kernel<BN, AMN, BMN>, dim3(grid), dim3(NTHREADS), (size_t)smem, st, p);
 }
 
@@ -571,6 +745,19 @@ int pick_bn(int N, bool bmn) {
 
 bool tc_gemm_available() { return get_encode(); }
 
+cudaError_t tc_trace(int on, unsigned long long* out, int n) {
+  g_trace_mode = on;
+  g_trace_count = 0;
+  cudaError_t e = cudaSuccess;
+  if (on) {
+    static std::vector<unsigned long long> zeros(TRACE_CTAS * TRACE_TILES * 4, 0ull);
+    e = cudaMemcpyToSymbol(g_trace, zeros.data(), zeros.size() * sizeof(unsigned long long));
+  }
+  if (e != cudaSuccess || !out) return e;
+  n = std::min(n, TRACE_CTAS * TRACE_TILES * 4);
+  return cudaMemcpyFromSymbol(out, g_trace, n * sizeof(unsigned long long));
+}
+
 bool tc_gemm_supported(const GemmArgs& a) {
   if (a.N < 1 || a.K < 1 || a.n_groups < 1 || a.n_groups > MAX_GROUPS) return false;
   if (a.splits > 1 && (a.k_per_split % BK)) return false;
@@ -586,10 +773,33 @@ bool tc_gemm_supported(const GemmArgs& a) {
   return get_encode();
 }
 
+// Output C of a group as a 3-D tensor [splits][M][N] for TMA bulk stores (64-byte inner box).
+bool make_map_out(CUtensorMap* m, void* ptr, int esz, uint64_t N, uint64_t M, uint64_t splits, uint64_t ld,
+                  uint64_t split_stride) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16 || (splits > 1 && (split_stride * esz) % 16)) return false;
+  cuuint64_t dims[3] = {N, M, splits};
+  cuuint64_t strides[2] = {ld * esz, (splits > 1 ? split_stride : ld * M) * esz};
+  cuuint32_t box[3] = {(cuuint32_t)(64 / esz), 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims,
+                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st) {
   TcParams p;
   std::memset(&p, 0, sizeof(p));
   p.a = a;
+  // epilogue stores through TMA when every group's C qualifies (heads store nothing through C)
+  const bool f32out = a.epi == EPI_F32 || a.epi == EPI_BIAS_F32;
+  p.out_bytes = f32out ? 4 : 2;
+  p.tma_out = (a.epi == EPI_BIAS_RELU || a.epi == EPI_MASK_BITS || f32out) ? 1 : 0;
+  for (int i = 0; i < a.n_groups && p.tma_out; ++i) {
+    const GemmGroup& g = a.g[i];
+    if (g.M < 1 || g.N < 1) continue;
+    if (!g.C || !make_map_out(&p.tc[i], g.C, p.out_bytes, g.N, g.M, a.splits, g.ldc, g.split_stride)) p.tma_out = 0;
+  }
   const int bn = pick_bn(a.N, a.b_mn);
   int maxM = 0;
   for (int i = 0; i < a.n_groups; ++i) {

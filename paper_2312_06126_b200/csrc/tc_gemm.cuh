@@ -9,6 +9,8 @@ namespace spz {
 bool tc_gemm_supported(const GemmArgs& a);
 // True if the tcgen05 path can run at all (driver entry point for tensor maps resolved).
 bool tc_gemm_available();
+// Diagnostics: enable/disable per-tile timestamps and copy them out (see tc_gemm.cu).
+cudaError_t tc_trace(int on, unsigned long long* out, int n);
 // Launch it (bf16 operands, fp32 accumulation in TMEM, shared epilogues).
 cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st);
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "spz_replay_records", "spz_replay_destroy", "spz_config_default", "spz_nccl_unique_id", "spz_learner_create",
     "spz_update", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
-    "spz_diag_gemm_bf16", "spz_split_exchange",
+    "spz_diag_gemm_bf16", "spz_split_exchange", "spz_diag_tc_trace",
 ]
 
 
@@ -117,6 +117,7 @@ def lib():
                                                         ctypes.POINTER(I32)]),
             "spz_learner_destroy": (None, [P]),
             "spz_split_exchange": (ctypes.c_int, [P, P]),
+            "spz_diag_tc_trace": (ctypes.c_int, [I32, I32, P, I32]),
             "spz_diag_gemm_bf16": (ctypes.c_int, [I32, I32, I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, I64]),
         }
         for name, (res, args) in sig.items():
@@ -273,6 +274,13 @@ def spz_learner_debug_buffer(learner, name):
 
 def spz_learner_destroy(learner):
     lib().spz_learner_destroy(learner)
+
+
+def spz_diag_tc_trace(on, read=False, device=0):
+    """Enable/disable GEMM tile timestamps; with read=True return them as uint64 [160, 8, 4]."""
+    out = np.zeros(160 * 8 * 4, np.uint64) if read else None
+    _check(lib().spz_diag_tc_trace(device, int(on), _ptr(out) if read else None, out.size if read else 0))
+    return out.reshape(160, 8, 4) if read else None
 
 
 def spz_split_exchange(critic_learner, actor_learner):

@@ -133,113 +133,39 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
+// tcgen05.ld of 16 / 32 consecutive fp32 accumulator columns of this warp's 32 TMEM lanes; the
+// wait names the destination registers so no consumer can be scheduled above it.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v0)[16], float (&v1)[16]) {
+  uint32_t r[32];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    v0[i] = __uint_as_float(r[i]);
+    v1[i] = __uint_as_float(r[16 + i]);
+  }
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&p);
-}
-
-// Epilogue of 16 consecutive accumulator columns n..n+15 of row m (bias / dot vectors staged
-// in shared memory for this column chunk).  Returns the chunk's contribution to the row dot.
-__device__ __forceinline__ float epi16(const GemmArgs& a, const GemmGroup& g, int split, int m, int n, const float (&v)[16],
-                                       const float* __restrict__ bias, const float* __restrict__ dotw, uint32_t& bits) {
-  const bool full = n + 16 <= g.N;
-  const int64_t off = (int64_t)m * g.ldc + n;
-  float dot = 0.f;
-  switch (a.epi) {
-    case EPI_MASK_BITS: {
-      // bits: this chunk's 16 ReLU-mask bits (prefetched by the caller)
-      __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C);
-      if (full && (g.ldc & 7) == 0) {
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          pk[j] = pack_bf16((bits >> (2 * j)) & 1u ? v[2 * j] : 0.f, (bits >> (2 * j + 1)) & 1u ? v[2 * j + 1] : 0.f);
-        uint4* dst = reinterpret_cast<uint4*>(C + off);
-        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      } else {
-        for (int j = 0; j < 16 && n + j < g.N; ++j) C[off + j] = __float2bfloat16_rn((bits >> j) & 1u ? v[j] : 0.f);
-      }
-      break;
-    }
-    case EPI_BIAS_RELU: {
-      __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C);
-      float z[16];
-      bits = 0u;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float pre = v[j] + bias[j];
-        z[j] = fmaxf(pre, 0.f);
-        bits |= (pre > 0.f && n + j < g.N ? 1u : 0u) << j;
-      }
-      if (dotw) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) dot = fmaf(z[j], dotw[j], dot);  // dotw is zero past g.N
-      }
-      if (full && (g.ldc & 7) == 0) {
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) pk[j] = pack_bf16(z[2 * j], z[2 * j + 1]);
-        uint4* dst = reinterpret_cast<uint4*>(C + off);
-        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      } else {
-        for (int j = 0; j < 16 && n + j < g.N; ++j) C[off + j] = __float2bfloat16_rn(z[j]);
-      }
-      break;
-    }
-    case EPI_MASK: {
-      __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C);
-      const __nv_bfloat16* X = static_cast<const __nv_bfloat16*>(g.aux) + (int64_t)m * g.ldaux + n;
-      if (full && (g.ldc & 7) == 0 && (g.ldaux & 7) == 0) {
-        const uint4 x0 = reinterpret_cast<const uint4*>(X)[0], x1 = reinterpret_cast<const uint4*>(X)[1];
-        const __nv_bfloat162* xs0 = reinterpret_cast<const __nv_bfloat162*>(&x0);
-        const __nv_bfloat162* xs1 = reinterpret_cast<const __nv_bfloat162*>(&x1);
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float2 f = __bfloat1622float2(j < 4 ? xs0[j] : xs1[j - 4]);
-          pk[j] = pack_bf16(f.x > 0.f ? v[2 * j] : 0.f, f.y > 0.f ? v[2 * j + 1] : 0.f);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(C + off);
-        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      } else {
-        for (int j = 0; j < 16 && n + j < g.N; ++j)
-          C[off + j] = __float2bfloat16_rn(__bfloat162float(X[j]) > 0.f ? v[j] : 0.f);
-      }
-      break;
-    }
-    case EPI_BIAS_F32: {
-      float* C = static_cast<float*>(g.C) + off;
-      for (int j = 0; j < 16 && n + j < g.N; ++j) C[j] = v[j] + bias[j];
-      break;
-    }
-    default: {
-      float* C = static_cast<float*>(g.C) + off + (int64_t)split * g.split_stride;
-      if (full && (g.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
-        float4* d4 = reinterpret_cast<float4*>(C);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-      } else {
-        for (int j = 0; j < 16 && n + j < g.N; ++j) C[j] = v[j];
-      }
-      break;
-    }
-  }
-  return dot;
 }
 
 // Linear tile index -> (group, m0, n0, split).  Tiles of group g occupy [tile0[g], tile0[g+1]);
@@ -260,44 +186,22 @@ __device__ __forceinline__ TileInfo decode_tile(const TcParams& p, int t, int bn
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NUM_EPI_WARPS * 32) : "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// Persistent, warp-specialized: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the TMA producer
-// and the MMA issuer run ahead into the next tile while the epilogue drains the previous one
-// from the other TMEM accumulator buffer.
-// Output values of 16 accumulator columns (TMA-store path): v is overwritten with what C receives.
-__device__ __forceinline__ float epi16_vals(int epi, int n, int N, float (&v)[16], const float* __restrict__ bias,
-                                            const float* __restrict__ dotw, uint32_t& bits) {
-  float dot = 0.f;
-  if (epi == EPI_BIAS_RELU) {
-    uint32_t b = 0u;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float pre = v[j] + bias[j];
-      v[j] = fmaxf(pre, 0.f);
-      b |= (pre > 0.f && n + j < N ? 1u : 0u) << j;
-    }
-    if (dotw) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) dot = fmaf(v[j], dotw[j], dot);  // dotw is zero past N
-    }
-    bits = b;
-  } else if (epi == EPI_MASK_BITS) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = (bits >> j) & 1u ? v[j] : 0.f;
-  } else if (epi == EPI_BIAS_F32) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] += bias[j];
-  }
-  return dot;
+// 0xFFFFFFFF if x > 0 else 0 (one FSET), so a ReLU-mask bit costs FSET + LOP3
+__device__ __forceinline__ uint32_t gt0_mask(float x) {
+  uint32_t d;
+  asm("set.gt.u32.f32 %0, %1, 0f00000000;" : "=r"(d) : "f"(x));
+  return d;
 }
 
 // Write 16 output values of row `row` into a 64-byte-row staging block (64-byte TMA swizzle:
 // 16-byte unit u of row r sits at unit u ^ ((r >> 1) & 3)); `unit0` = first 16-byte unit.
-__device__ __forceinline__ void stage16(uint8_t* blk, int row, int unit0, const float (&v)[16], bool bf16) {
+template <bool OBF>
+__device__ __forceinline__ void stage16(uint8_t* blk, int row, int unit0, const float (&v)[16]) {
   uint8_t* rp = blk + row * 64;
   const int sw = (row >> 1) & 3;
-  if (bf16) {
+  if constexpr (OBF) {
     const uint4 u0 = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
     const uint4 u1 = make_uint4(pack_bf16(v[8], v[9]), pack_bf16(v[10], v[11]), pack_bf16(v[12], v[13]),
                                 pack_bf16(v[14], v[15]));
@@ -310,15 +214,66 @@ __device__ __forceinline__ void stage16(uint8_t* blk, int row, int unit0, const 
   }
 }
 
-template <int BN, bool AMN, bool BMN>
+// Direct (non-TMA) store of 16 output values at C(m, n..n+15) + split partial offset; used when
+// an output pitch cannot be described by a tensor map.
+template <bool OBF>
+__device__ __forceinline__ void direct16(const GemmGroup& g, int split, int m, int n, const float (&v)[16]) {
+  if (m >= g.M) return;
+  const int64_t off = (int64_t)m * g.ldc + n;
+  const bool full = n + 16 <= g.N;
+  if constexpr (OBF) {
+    __nv_bfloat16* C = static_cast<__nv_bfloat16*>(g.C) + off;
+    if (full && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
+      uint4* d = reinterpret_cast<uint4*>(C);
+      d[0] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+      d[1] = make_uint4(pack_bf16(v[8], v[9]), pack_bf16(v[10], v[11]), pack_bf16(v[12], v[13]), pack_bf16(v[14], v[15]));
+    } else {
+      for (int j = 0; j < 16 && n + j < g.N; ++j) C[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    float* C = static_cast<float*>(g.C) + off + (int64_t)split * g.split_stride;
+    if (full && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
+      float4* d4 = reinterpret_cast<float4*>(C);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    } else {
+      for (int j = 0; j < 16 && n + j < g.N; ++j) C[j] = v[j];
+    }
+  }
+}
+
+// Epilogue shape of one (BN, EK) instantiation.
+template <int BN, int EK>
+struct EpiShape {
+  static constexpr bool HEAD = EK == EPI_SAC_HEAD;
+  static constexpr bool RELU = EK == EPI_BIAS_RELU;
+  static constexpr bool MASKB = EK == EPI_MASK_BITS;
+  static constexpr bool BIAS = RELU || HEAD || EK == EPI_BIAS_F32;
+  static constexpr bool OBF = RELU || MASKB;            // bf16 output, else fp32
+  static constexpr bool SPLIT = BN >= 64 && !HEAD;      // the WPQ warps of a lane quarter split the columns
+  static constexpr int CPW = SPLIT ? BN / 16 / WPQ : BN / 16;  // 16-column chunks per warp
+  static constexpr int CPB = OBF ? 2 : 1;               // chunks per 64-byte store block (= one mask word)
+  static constexpr int NB = (CPW + CPB - 1) / CPB;      // store blocks per warp
+  static constexpr int SLICE = CPW * 16;                // columns per warp
+};
+
+// Persistent, warp-specialized: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the TMA producer
+// and the MMA issuer run ahead into the next tile while the epilogue drains the previous one
+// from the other TMEM accumulator buffer.  EK (the epilogue kind) is a template parameter so the
+// epilogue compiles to straight-line code for exactly one kind (SAC_HEAD also covers TD3_HEAD).
+template <int BN, bool AMN, bool BMN, int EK>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
+  using S = EpiShape<BN, EK>;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t ACC_COLS = BN < 32 ? 32 : BN;  // one accumulator buffer
   constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;       // double-buffered
-  constexpr int NW = (BN + 31) / 32, MSTR = NW + 1;
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) |
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  // per epilogue warp: its slice of the tile's bias / row-dot weights; row-dot partials per quarter
+  __shared__ __align__(16) float bias_w[S::BIAS ? NUM_EPI_WARPS : 1][S::BIAS ? S::SLICE : 4];
+  __shared__ __align__(16) float dotw_w[S::RELU ? NUM_EPI_WARPS : 1][S::RELU ? S::SLICE : 4];
+  __shared__ float dotpart[S::RELU ? 2 : 1][S::RELU ? WPQ : 1][S::RELU ? BM : 1];
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NS = p.stages;
@@ -327,13 +282,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   uint64_t* acc_full = empty + STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  float* bias_s = reinterpret_cast<float*>(tmem_slot + 4);     // [BN] epilogue bias of the current tile
-  float* dot_s = bias_s + BN;                                  // [BN] fused row-dot weights
-  float* dotpart = dot_s + BN;                                 // [WPQ][BM] row-dot slices
-  uint32_t* mask_s = reinterpret_cast<uint32_t*>(dotpart + WPQ * BM);  // [BM][MSTR] packed ReLU masks
   // per epilogue warp: two 32-row x 64-byte staging blocks for the TMA stores (1024-byte aligned)
-  uint8_t* stage_s = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(mask_s + BM * MSTR) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_s = smem + NS * STAGE + 1024;
 
   const GemmArgs& a = p.a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -435,186 +385,177 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       }
     }
   } else {
-    // ---------------- epilogue: 8 warps; warp % 4 selects the TMEM lane quarter (32 rows) and
-    //                  the two warps of a quarter split the columns (heads: one warp takes the row)
+    // ---------------- epilogue: warp % 4 selects the TMEM lane quarter (32 rows); the WPQ warps of
+    //                  a quarter split the columns (heads: one warp takes the whole row)
     const int e = warp - 2;
     const int q = warp & 3;
     const int hh = e >> 2;
-    const bool head = a.epi == EPI_SAC_HEAD || a.epi == EPI_TD3_HEAD;
-    // 16-column chunks per warp: whole 32-bit mask words per warp (>= 2 chunks)
-    constexpr int CPW = (BN / 16) / WPQ >= 2 ? (BN / 16) / WPQ : 2;
-    const bool split_cols = BN >= 64 && !head;
-    const int c_lo = split_cols ? min(hh * CPW, BN / 16) : 0;    // first 16-column chunk of this warp
-    const int c_hi = split_cols ? min((hh + 1) * CPW, BN / 16) : (hh == 0 ? BN / 16 : 0);
-    const int r = q * 32 + lane;  // tile row of this thread
-    uint32_t* mrow = mask_s + r * MSTR;
+    const bool active = S::SPLIT || hh == 0;
+    const int c_lo = S::SPLIT ? hh * S::CPW : 0;  // first 16-column chunk of this warp
+    const int r = q * 32 + lane;                  // tile row of this thread
+    float* bias_s = bias_w[S::BIAS ? e : 0];
+    float* dot_s = dotw_w[S::RELU ? e : 0];
     int tile_i = 0;
-    int st_count = 0;  // TMA store blocks issued by this warp
+    int st_count = 0;   // TMA store blocks issued by this warp
+    int dot_tiles = 0;  // fused row-dot tiles seen (dotpart buffer parity)
     for (int t = blockIdx.x; t < T; t += gridDim.x, ++tile_i) {
       const TileInfo ti = decode_tile(p, t, BN);
       const GemmGroup& g = a.g[ti.grp];
       const int m = ti.m0 + r;
       const int n0 = ti.n0;
+      const int ncol0 = n0 + c_lo * 16;  // first output column of this warp
       const int k_begin = ti.split * a.k_per_split;
-      const int nkb = min(a.K, k_begin + a.k_per_split) > k_begin ? 1 : 0;
-      const bool has_bias = a.epi == EPI_BIAS_RELU || a.epi == EPI_BIAS_F32 || head;
-      const bool has_dot = a.epi == EPI_BIAS_RELU && g.dot_out != nullptr;
-      const bool mask_in = a.epi == EPI_MASK_BITS;
-      const bool mask_out = a.epi == EPI_BIAS_RELU && g.mask_out != nullptr;
-      // stage this tile's bias / row-dot weights (after every epilogue warp left the previous tile)
-      epi_bar(1);
-      if (has_bias)
-        for (int c = e * 32 + lane; c < BN; c += NUM_EPI_WARPS * 32) {
-          bias_s[c] = n0 + c < g.N ? g.bias[n0 + c] : 0.f;
-          dot_s[c] = (has_dot && n0 + c < g.N) ? g.dot_w[n0 + c] : 0.f;
+      const bool has_acc = min(a.K, k_begin + a.k_per_split) > k_begin;
+      const bool has_dot = S::RELU && g.dot_out != nullptr;
+      const bool mask_out = S::RELU && g.mask_out != nullptr;
+      // this warp's slice of the bias / row-dot weights (the previous tile's reads of the slice
+      // are ordered by the __syncwarp that precedes every acc_empty arrival)
+      if constexpr (S::BIAS) {
+#pragma unroll
+        for (int c = lane; c < S::SLICE; c += 32) {
+          const int n = ncol0 + c;
+          bias_s[c] = n < g.N ? g.bias[n] : 0.f;
+          if constexpr (S::RELU) dot_s[c] = (has_dot && n < g.N) ? g.dot_w[n] : 0.f;
         }
-      if (mask_in) {  // this warp's words of the row's packed mask, prefetched before the accumulator wait
-        const uint32_t* src = static_cast<const uint32_t*>(g.aux) + (int64_t)m * g.ldaux + n0 / 32;
-        for (int i = c_lo / 2; i < (c_hi + 1) / 2; ++i) mrow[i] = (m < g.M && n0 + 32 * i < g.N) ? src[i] : 0u;
       }
-      if (mask_out)
-        for (int i = c_lo / 2; i < (c_hi + 1) / 2; ++i) mrow[i] = 0u;
-      epi_bar(1);
+      // packed ReLU mask words of this row (dgrad), prefetched before the accumulator wait
+      uint32_t mw[S::NB];
+#pragma unroll
+      for (int i = 0; i < S::NB; ++i) mw[i] = 0u;
+      if constexpr (S::MASKB) {
+        if (active && m < g.M) {
+          const uint32_t* src = static_cast<const uint32_t*>(g.aux) + (int64_t)m * g.ldaux + ncol0 / 32;
+#pragma unroll
+          for (int i = 0; i < S::NB; ++i)
+            if (ncol0 + 32 * i < g.N) mw[i] = __ldg(src + i);
+        }
+      }
+      __syncwarp();
       const int b = tile_i & 1;
       mbar_wait(&acc_full[b], ((uint32_t)tile_i >> 1) & 1u);
       tc_fence_after();
       if (e == 0 && lane == 0) trace(tile_i, 2);
       const uint32_t trow = tmem + (uint32_t)b * ACC_COLS + ((uint32_t)(q * 32) << 16);
-      if (head) {
-        if constexpr (BN <= 64) {
-          if (hh == 0) {
-            float hrow[BN];
+      if constexpr (S::HEAD) {
+        if (hh == 0) {
+          float hrow[BN];
 #pragma unroll
-            for (int c = 0; c < BN / 16; ++c) {
-              float v[16];
-              if (nkb > 0) tmem_ld16(trow + c * 16, v);
-              else
+          for (int c = 0; c < BN / 16; ++c) {
+            float v[16];
+            if (has_acc) tmem_ld16(trow + c * 16, v);
+            else
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = 0.f;
+              for (int j = 0; j < 16; ++j) v[j] = 0.f;
 #pragma unroll
-              for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
-            }
-            tc_fence_before();
-            if (m < g.M) {
-              if (a.epi == EPI_SAC_HEAD) sac_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow, hrow + a.head.m);
-              else td3_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow);
-            }
+            for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
+          }
+          tc_fence_before();
+          if (m < g.M) {
+            if (a.epi == EPI_SAC_HEAD) sac_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow, hrow + a.head.m);
+            else td3_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow);
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[b]);
-      } else if (p.tma_out) {
-        // ---- outputs staged in shared memory, written by TMA bulk tensor stores (64-byte x 32-row
-        //      blocks, double-buffered per warp)
+      } else {
         float dot = 0.f;
-        const bool obf = p.out_bytes == 2;
-        const int cpb = obf ? 2 : 1;  // 16-column chunks per 64-byte store block
         uint8_t* wstage = stage_s + e * 4096;
-#pragma unroll 1
-        for (int c = c_lo; c < c_hi; c += cpb) {
-          if (n0 + c * 16 >= g.N) break;  // warp-uniform
-          if (st_count >= 2) {
+#pragma unroll
+        for (int ib = 0; ib < S::NB; ++ib) {
+          const int c = c_lo + ib * S::CPB;           // first chunk of this store block
+          if (!active || n0 + c * 16 >= g.N) break;  // warp-uniform
+          uint8_t* blk = wstage + (st_count & 1) * 2048;
+          if (p.tma_out && st_count >= 2) {
             if (lane == 0) bulk_wait_read1();  // the block issued two stores ago has left this slot
             __syncwarp();
           }
-          uint8_t* blk = wstage + (st_count & 1) * 2048;
-          for (int cc = 0; cc < cpb; ++cc) {
-            const int ch = c + cc;
-            const int n = n0 + ch * 16;
-            float v[16];
-            if (nkb > 0 && n < g.N) {
-              tmem_ld16(trow + ch * 16, v);
+          float v[S::CPB][16];
+          if (has_acc) {
+            if constexpr (S::CPB == 2 && S::CPW >= 2) {
+              tmem_ld32(trow + c * 16, v[0], v[1]);
+            } else {
+              tmem_ld16(trow + c * 16, v[0]);
+#pragma unroll
+              for (int cc = 1; cc < S::CPB; ++cc)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[cc][j] = 0.f;  // past the tile (BN = 16)
+            }
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < S::CPB; ++cc)
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[cc][j] = 0.f;
+          }
+          uint32_t word = 0u;
+#pragma unroll
+          for (int cc = 0; cc < S::CPB; ++cc) {
+            const int cl = ib * S::CPB + cc;  // chunk within this warp's slice
+            if (cl >= S::CPW) break;          // past the tile (BN = 16): stays zero
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if constexpr (S::RELU) {
+                // columns past N: zero-filled B rows and zero bias -> pre = 0 -> bit 0, value 0
+                const float pre = v[cc][j] + bias_s[cl * 16 + j];
+                word |= gt0_mask(pre) & (1u << (16 * cc + j));
+                v[cc][j] = fmaxf(pre, 0.f);
+                dot = fmaf(v[cc][j], dot_s[cl * 16 + j], dot);
+              } else if constexpr (S::MASKB) {
+                v[cc][j] = (mw[ib] >> (16 * cc + j)) & 1u ? v[cc][j] : 0.f;
+              } else if constexpr (S::BIAS) {
+                v[cc][j] += bias_s[cl * 16 + j];
+              }
+            }
+          }
+          if constexpr (S::RELU) mw[ib] = word;
+          if (p.tma_out) {
+#pragma unroll
+            for (int cc = 0; cc < S::CPB; ++cc) stage16<S::OBF>(blk, lane, cc * (S::OBF ? 2 : 4), v[cc]);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&p.tc[ti.grp], blk, n0 + c * 16, ti.m0 + q * 32, ti.split);
+              bulk_commit();
+            }
+            ++st_count;
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < S::CPB; ++cc)
+              if (n0 + (c + cc) * 16 < g.N) direct16<S::OBF>(g, ti.split, m, n0 + (c + cc) * 16, v[cc]);
+          }
+        }
+        if (e == 0 && lane == 0) trace(tile_i, 3);
+        // accumulator buffer drained by this warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        if constexpr (S::RELU) {
+          if (has_dot) {
+            // the WPQ warps of this lane quarter combine their row-dot slices in a fixed order
+            // (dotpart double-buffered by tile parity; the quarter barrier orders reuse)
+            float tot = dot;
+            if constexpr (S::SPLIT) {
+              const int pb = dot_tiles & 1;
+              dotpart[pb][hh][r] = dot;
+              named_bar(2 + q, WPQ * 32);
+              tot = 0.f;
+#pragma unroll
+              for (int k = 0; k < WPQ; ++k) tot += dotpart[pb][k][r];
+            }
+            ++dot_tiles;
+            if (hh == 0 && m < g.M) g.dot_out[m] = tot + g.dot_b[0];
+          }
+          if (mask_out && active && m < g.M) {
+            const int w_hi = min(S::NB, (g.N - ncol0 + 31) / 32);
+            uint32_t* dst = g.mask_out + (int64_t)m * g.mask_ld + ncol0 / 32;
+            if (S::NB == 4 && w_hi == 4 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+              *reinterpret_cast<uint4*>(dst) = make_uint4(mw[0], mw[S::NB > 1 ? 1 : 0], mw[S::NB > 2 ? 2 : 0], mw[S::NB > 3 ? 3 : 0]);
+            } else if (S::NB == 2 && w_hi == 2 && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+              *reinterpret_cast<uint2*>(dst) = make_uint2(mw[0], mw[S::NB > 1 ? 1 : 0]);
             } else {
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = 0.f;
+              for (int i = 0; i < S::NB; ++i)
+                if (i < w_hi) dst[i] = mw[i];
             }
-            uint32_t bits = mask_in ? (mrow[ch >> 1] >> (16 * (ch & 1))) & 0xFFFFu : 0u;
-            const float d = epi16_vals(a.epi, n, g.N, v, bias_s + ch * 16, has_dot ? dot_s + ch * 16 : nullptr, bits);
-            if (m < g.M) {
-              dot += d;
-              if (mask_out) mrow[ch >> 1] |= bits << (16 * (ch & 1));
-            }
-            stage16(blk, lane, cc * (obf ? 2 : 4), v, obf);
-          }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&p.tc[ti.grp], blk, n0 + c * 16, ti.m0 + q * 32, ti.split);
-            bulk_commit();
-          }
-          ++st_count;
-        }
-        if (e == 0 && lane == 0) trace(tile_i, 3);
-        // accumulator buffer drained by this warp
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[b]);
-        if (has_dot) {
-          dotpart[hh * BM + r] = dot;
-          epi_bar(2);
-          if (hh == 0 && m < g.M) {
-            float tot = dot;
-            if (split_cols) {
-              tot = 0.f;
-              for (int k = 0; k < WPQ; ++k) tot += dotpart[k * BM + r];  // fixed order
-            }
-            g.dot_out[m] = tot + g.dot_b[0];
-          }
-        }
-        if (mask_out && m < g.M) {
-          const int w_lo = c_lo / 2, w_hi = min((c_hi + 1) / 2, (g.N - n0 + 31) / 32);
-          uint32_t* dst = g.mask_out + (int64_t)m * g.mask_ld + n0 / 32;
-          if (w_hi - w_lo == 4 && ((reinterpret_cast<uintptr_t>(dst + w_lo) & 15) == 0)) {
-            *reinterpret_cast<uint4*>(dst + w_lo) = make_uint4(mrow[w_lo], mrow[w_lo + 1], mrow[w_lo + 2], mrow[w_lo + 3]);
-          } else {
-            for (int i = w_lo; i < w_hi; ++i) dst[i] = mrow[i];
-          }
-        }
-      } else {
-        float dot = 0.f;
-#pragma unroll 1
-        for (int c = c_lo; c < c_hi; ++c) {
-          const int n = n0 + c * 16;
-          if (n >= g.N) break;  // warp-uniform
-          float v[16];
-          if (nkb > 0) {
-            tmem_ld16(trow + c * 16, v);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0.f;
-          }
-          uint32_t bits = mask_in ? (mrow[c >> 1] >> (16 * (c & 1))) & 0xFFFFu : 0u;
-          if (m < g.M) {
-            dot += epi16(a, g, ti.split, m, n, v, bias_s + c * 16, has_dot ? dot_s + c * 16 : nullptr, bits);
-            if (mask_out) mrow[c >> 1] |= bits << (16 * (c & 1));
-          }
-        }
-        // accumulator buffer drained by this warp
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[b]);
-        if (has_dot) {
-          dotpart[hh * BM + r] = dot;
-          epi_bar(2);
-          if (hh == 0 && m < g.M) {
-            float tot = dot;
-            if (split_cols) {
-              tot = 0.f;
-              for (int k = 0; k < WPQ; ++k) tot += dotpart[k * BM + r];  // fixed order
-            }
-            g.dot_out[m] = tot + g.dot_b[0];
-          }
-        }
-        if (e == 0 && lane == 0) trace(tile_i, 3);
-        if (mask_out && m < g.M) {
-          const int w_lo = c_lo / 2, w_hi = min((c_hi + 1) / 2, (g.N - n0 + 31) / 32);
-          uint32_t* dst = g.mask_out + (int64_t)m * g.mask_ld + n0 / 32;
-          if (w_hi - w_lo == 4 && ((reinterpret_cast<uintptr_t>(dst + w_lo) & 15) == 0)) {
-            *reinterpret_cast<uint4*>(dst + w_lo) = make_uint4(mrow[w_lo], mrow[w_lo + 1], mrow[w_lo + 2], mrow[w_lo + 3]);
-          } else if (w_hi - w_lo == 2 && ((reinterpret_cast<uintptr_t>(dst + w_lo) & 7) == 0)) {
-            *reinterpret_cast<uint2*>(dst + w_lo) = make_uint2(mrow[w_lo], mrow[w_lo + 1]);
-          } else {
-            for (int i = w_lo; i < w_hi; ++i) dst[i] = mrow[i];
           }
         }
       }
@@ -671,25 +612,31 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
   return r == CUDA_SUCCESS;
 }
 
-template <int BN>
-constexpr int smem_extras() {
-  return 1024 /* alignment */ + 128 /* barriers + TMEM slot */ + BN * 8 /* bias, dot */ + WPQ * BM * 4 /* dot slices */ +
-         BM * ((BN + 31) / 32 + 1) * 4 /* masks */ + 1024 + NUM_EPI_WARPS * 4096 /* TMA store staging */;
+// dynamic shared memory besides the pipeline stages: alignment slack, barriers + TMEM slot,
+// per-warp TMA store staging
+constexpr int smem_extras() { return 1024 + 1024 + NUM_EPI_WARPS * 4096; }
+// static shared memory of one instantiation (per-warp bias / row-dot slices, row-dot partials)
+template <int BN, int EK>
+constexpr int smem_static() {
+  using S = EpiShape<BN, EK>;
+  return (S::BIAS ? NUM_EPI_WARPS * S::SLICE * 4 : 16) + (S::RELU ? NUM_EPI_WARPS * S::SLICE * 4 : 16) +
+         (S::RELU ? 2 * WPQ * BM * 4 : 4) + 64;
 }
 
-template <int BN, bool AMN, bool BMN>
-cudaError_t launch(TcParams& p, int maxM, cudaStream_t st) {
+template <int BN, bool AMN, bool BMN, int EK>
+cudaError_t launch(TcParams& p, cudaStream_t st) {
   constexpr int STAGE = A_BYTES + BN * BK * 2;
-  constexpr int MAX_ST = std::min(STAGES, (227 * 1024 - smem_extras<BN>()) / STAGE);
+  constexpr int AVAIL = 227 * 1024 - smem_static<BN, EK>() - smem_extras();
+  constexpr int MAX_ST = std::min(STAGES, AVAIL / STAGE);
   static_assert(MAX_ST >= 1, "shared memory budget");
-  constexpr int SMEM_MAX = MAX_ST * STAGE + smem_extras<BN>();
+  constexpr int SMEM_MAX = MAX_ST * STAGE + smem_extras();
+  auto kern = tc_gemm_kernel<BN, AMN, BMN, EK>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  (void)maxM;
   // persistent schedule: tiles of every group, one CTA per SM (or more when TMEM and smem allow)
   int T = 0;
   for (int i = 0; i < p.a.n_groups; ++i) {
@@ -704,31 +651,65 @@ cudaError_t launch(TcParams& p, int maxM, cudaStream_t st) {
   p.total_tiles = T;
   if (T == 0) return cudaSuccess;
   constexpr int TMEM_COLS = 2 * (BN < 32 ? 32 : BN);
-  static int occ = [] {
+  static int occ = [&] {
     int o = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, tc_gemm_kernel<BN, AMN, BMN>, NTHREADS, STAGE + smem_extras<BN>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, NTHREADS, STAGE + smem_extras());
     return std::max(1, o);
   }();
   const int per_sm = std::max(1, std::min(512 / TMEM_COLS, occ));
-  const int budget = 227 * 1024 / per_sm;
+  const int budget = 227 * 1024 / per_sm - smem_static<BN, EK>();
   const int kspan = p.a.splits > 1 ? p.a.k_per_split : p.a.K;
   const int want = (int)std::min<int64_t>(STAGES, std::max<int64_t>(1, cdiv(kspan, BK)));
-  p.stages = std::max(1, std::min(std::min(want, MAX_ST), (budget - smem_extras<BN>()) / STAGE));
-  const int smem = p.stages * STAGE + smem_extras<BN>();
+  p.stages = std::max(1, std::min(std::min(want, MAX_ST), (budget - smem_extras()) / STAGE));
+  const int smem = p.stages * STAGE + smem_extras();
   const int grid = std::min(T, num_sms() * per_sm);
   p.trace = g_trace_mode == 1 || (g_trace_mode >= 2 && g_trace_count == g_trace_mode - 2);
   ++g_trace_count;
-  return launch_pdl(tc_gemm_kernel<BN, AMN, BMN>, dim3(grid), dim3(NTHREADS), (size_t)smem, st, p);
+  return launch_pdl(kern, dim3(grid), dim3(NTHREADS), (size_t)smem, st, p);
+}
+
+// epilogue kinds instantiated per operand layout: forward (K-major A and B), dgrad (MN-major B),
+// wgrad (both MN-major)
+template <bool AMN, bool BMN>
+constexpr bool ek_ok(int epi, int bn) {
+  if (!AMN && !BMN)
+    return epi == EPI_BIAS_RELU || epi == EPI_BIAS_F32 || epi == EPI_F32 ||
+           ((epi == EPI_SAC_HEAD || epi == EPI_TD3_HEAD) && bn <= 64);
+  if (!AMN && BMN) return epi == EPI_MASK_BITS || epi == EPI_F32;
+  if (AMN && BMN) return epi == EPI_F32;
+  return false;
+}
+
+template <int BN, bool AMN, bool BMN>
+cudaError_t launch_ek(TcParams& p, cudaStream_t st) {
+  if constexpr (!AMN && !BMN) {
+    switch (p.a.epi) {
+      case EPI_BIAS_RELU: return launch<BN, AMN, BMN, EPI_BIAS_RELU>(p, st);
+      case EPI_BIAS_F32: return launch<BN, AMN, BMN, EPI_BIAS_F32>(p, st);
+      case EPI_F32: return launch<BN, AMN, BMN, EPI_F32>(p, st);
+      case EPI_SAC_HEAD:
+      case EPI_TD3_HEAD:
+        if constexpr (BN <= 64) return launch<BN, AMN, BMN, EPI_SAC_HEAD>(p, st);
+        break;
+      default: break;
+    }
+  } else if constexpr (!AMN && BMN) {
+    if (p.a.epi == EPI_MASK_BITS) return launch<BN, AMN, BMN, EPI_MASK_BITS>(p, st);
+    if (p.a.epi == EPI_F32) return launch<BN, AMN, BMN, EPI_F32>(p, st);
+  } else {
+    if (p.a.epi == EPI_F32) return launch<BN, AMN, BMN, EPI_F32>(p, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 template <bool AMN, bool BMN>
-cudaError_t launch_bn(TcParams& p, int bn, int maxM, cudaStream_t st) {
+cudaError_t launch_bn(TcParams& p, int bn, cudaStream_t st) {
   switch (bn) {
-    case 16: if constexpr (!BMN) return launch<16, AMN, BMN>(p, maxM, st); break;
-    case 32: if constexpr (!BMN) return launch<32, AMN, BMN>(p, maxM, st); break;
-    case 64: return launch<64, AMN, BMN>(p, maxM, st);
-    case 128: return launch<128, AMN, BMN>(p, maxM, st);
-    default: return launch<256, AMN, BMN>(p, maxM, st);
+    case 16: if constexpr (!BMN) return launch_ek<16, AMN, BMN>(p, st); break;
+    case 32: if constexpr (!BMN) return launch_ek<32, AMN, BMN>(p, st); break;
+    case 64: return launch_ek<64, AMN, BMN>(p, st);
+    case 128: return launch_ek<128, AMN, BMN>(p, st);
+    default: return launch_ek<256, AMN, BMN>(p, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -761,9 +742,10 @@ cudaError_t tc_trace(int on, unsigned long long* out, int n) {
 bool tc_gemm_supported(const GemmArgs& a) {
   if (a.N < 1 || a.K < 1 || a.n_groups < 1 || a.n_groups > MAX_GROUPS) return false;
   if (a.splits > 1 && (a.k_per_split % BK)) return false;
-  if (a.a_mn && !a.b_mn) return false;  // layout combination not instantiated
   const int bn = pick_bn(a.N, a.b_mn);
-  if ((a.epi == EPI_SAC_HEAD || a.epi == EPI_TD3_HEAD) && bn > 64) return false;
+  const bool ek = a.a_mn ? (a.b_mn && ek_ok<true, true>(a.epi, bn))
+                         : (a.b_mn ? ek_ok<false, true>(a.epi, bn) : ek_ok<false, false>(a.epi, bn));
+  if (!ek) return false;  // layout / epilogue combination not instantiated
   for (int i = 0; i < a.n_groups; ++i) {
     const GemmGroup& g = a.g[i];
     if ((g.lda & 7) || (g.ldb & 7)) return false;
@@ -816,9 +798,9 @@ cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st) {
     if (!ok) return cudaErrorInvalidValue;
   }
   if (maxM == 0) return cudaSuccess;
-  if (!a.a_mn && !a.b_mn) return launch_bn<false, false>(p, bn, maxM, st);
-  if (!a.a_mn && a.b_mn) return launch_bn<false, true>(p, bn, maxM, st);
-  return launch_bn<true, true>(p, bn, maxM, st);
+  if (!a.a_mn && !a.b_mn) return launch_bn<false, false>(p, bn, st);
+  if (!a.a_mn && a.b_mn) return launch_bn<false, true>(p, bn, st);
+  return launch_bn<true, true>(p, bn, st);
 }
 
 }  // namespace spz

@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(CS_TX* CS_TY) colsum_multi_kernel(const __grid
     const int n = c0 + tx * CS_VEC;
     float acc[CS_VEC] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (n < jb.N) {
+#pragma unroll 4
       for (int r = r0 + ty; r < r1; r += CS_TY) {
         float v[CS_VEC];
         if (jb.f32) load8<float>(static_cast<const float*>(jb.X) + (int64_t)r * jb.ld, n, jb.N, 0, v);
@@ -496,11 +497,11 @@ __device__ __forceinline__ bool step_stats(const double* __restrict__ tot, doubl
 }
 
 // ------------------------------------------------------------------ a9: fused multi-tensor Adam + Polyak
-// One block per segment of <= ADAM_SEG elements of one tensor.  For each element:
+// One block per segment of <= ADAM_SEG elements of one tensor, one element per thread:
 // g = sum_s partial[s] (fixed order); Adam with the optimizer's own t; master,
 // m, v updated; operand shadow (T, padded row stride) refreshed; if the tensor
 // has a target: theta' = tau theta_new + (1 - tau) theta' (+ its shadow).
-constexpr int ADAM_SEG = 1024;
+constexpr int ADAM_SEG = 256;  // one element per thread
 
 struct AdamTensor {
   int64_t p_off;      // master offset of element 0
@@ -519,18 +520,25 @@ struct AdamTensor {
   int32_t pad_;
 };
 
-// Split-K partial sum of element i of tensor tn (fixed split order).
-__device__ __forceinline__ float partial_sum(const AdamTensor& tn, int64_t i) {
-  int64_t idx;
+// Split-K partial sum of element i of tensor tn (fixed split order; loads issued 16 at a time).
+__device__ __forceinline__ float partial_sum(const AdamTensor& tn, int64_t i64) {
+  const int i = (int)i64;  // tensors hold < 2^31 elements
+  int idx;
   if (tn.cols > 0) {
-    const int64_t row = i / tn.cols;
+    const int row = i / tn.cols;
     idx = row * tn.pld + (i - row * tn.cols);
   } else {
     idx = i * tn.pld;
   }
+  const float* src = tn.partials + idx;
   float g = 0.f;
-#pragma unroll 8
-  for (int s = 0; s < tn.n_partials; ++s) g += __ldg(tn.partials + (int64_t)s * tn.pstride + idx);
+  for (int s0 = 0; s0 < tn.n_partials; s0 += 16) {
+    float t[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) t[j] = s0 + j < tn.n_partials ? __ldg(src + (int64_t)(s0 + j) * tn.pstride) : 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) g += t[j];
+  }
   return g;
 }
 struct AdamSegment {
@@ -552,17 +560,35 @@ struct AdamHyper {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) adam_polyak_kernel(const AdamTensor* __restrict__ tensors,
-                                                          const AdamSegment* __restrict__ segs, AdamHyper hp,
-                                                          float* __restrict__ P, float* __restrict__ Mo,
-                                                          float* __restrict__ Vo, T* __restrict__ S,
-                                                          int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
-                                                          int* __restrict__ flag) {
+__global__ void __launch_bounds__(ADAM_SEG) adam_polyak_kernel(const AdamTensor* __restrict__ tensors,
+                                                               const AdamSegment* __restrict__ segs, AdamHyper hp,
+                                                               float* __restrict__ P, float* __restrict__ Mo,
+                                                               float* __restrict__ Vo, T* __restrict__ S,
+                                                               int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
+                                                               int* __restrict__ flag) {
   pdl_wait();
   pdl_launch();
-  __shared__ float g_alpha;
+  __shared__ float g_alpha, bc1_s, bc2_s;
   __shared__ bool skip, last;
+  const AdamSegment sg = segs[blockIdx.x];
+  const AdamTensor tn = tensors[sg.tensor];
+  const int k = threadIdx.x;
+  const bool valid = k < sg.count;
+  const int64_t i = sg.start + k;
+  const int64_t pi = tn.p_off + i;
+  // gradient and optimizer state first: these loads are in flight while thread 0 works out the
+  // statistics of the step
+  float g = 0.f, m0 = 0.f, v0 = 0.f, p0 = 0.f, tp0 = 0.f;
+  if (valid) {
+    if (tn.opt != 2) g = partial_sum(tn, i);
+    m0 = Mo[pi];
+    v0 = Vo[pi];
+    p0 = P[pi];
+    if (tn.t_off >= 0) tp0 = P[tn.t_off + i];
+  }
   const int64_t step = counters[0];
+  bool delayed = true;
+  if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
   if (threadIdx.x == 0) {
     // statistics of the step from the loss totals (identical in every block); block 0 publishes them
     StatsOut o;
@@ -572,48 +598,36 @@ __global__ void __launch_bounds__(256) adam_polyak_kernel(const AdamTensor* __re
     if (blockIdx.x == 0) *hp.stats = o;
     g_alpha = ga;
     skip = bad || *flag;  // halted: parameters stay at the state before the failing step
+    const double t = (double)(counters[1 + tn.opt] + 1);
+    bc1_s = (float)(1.0 - pow((double)hp.beta1, t));
+    bc2_s = (float)(1.0 - pow((double)hp.beta2, t));
   }
   __syncthreads();
-  const AdamSegment sg = segs[blockIdx.x];
-  const AdamTensor tn = tensors[sg.tensor];
-  bool delayed = true;
-  if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
   const bool active = !skip && !(hp.td3 && tn.opt == 1 && !delayed);  // TD3 actor: delayed steps only
-  if (active) {
-    const int64_t t = counters[1 + tn.opt] + 1;
-    const float bc1 = (float)(1.0 - pow((double)hp.beta1, (double)t));
-    const float bc2 = (float)(1.0 - pow((double)hp.beta2, (double)t));
+  if (active && valid) {
+    const float bc1 = bc1_s, bc2 = bc2_s;
     const float lr = hp.lr[tn.opt];
     const bool do_polyak = tn.t_off >= 0 && (!hp.td3 || delayed);
-    for (int k = threadIdx.x; k < sg.count; k += blockDim.x) {
-      const int64_t i = sg.start + k;
-      float g = 0.f;
-      if (tn.opt == 2) {
-        g = g_alpha;  // log-alpha gradient -(mean log pi~ + H_bar) from the (group) totals
-      } else {
-        g = partial_sum(tn, i);
-      }
-      if (!isfinite(g)) {
-        atomicExch(flag, 2);
-        continue;
-      }
-      const int64_t pi = tn.p_off + i;
-      const float m = hp.beta1 * Mo[pi] + (1.f - hp.beta1) * g;
-      const float v = hp.beta2 * Vo[pi] + (1.f - hp.beta2) * g * g;
+    if (tn.opt == 2) g = g_alpha;  // log-alpha gradient -(mean log pi~ + H_bar) from the (group) totals
+    if (!isfinite(g)) {
+      atomicExch(flag, 2);
+    } else {
+      const float m = hp.beta1 * m0 + (1.f - hp.beta1) * g;
+      const float v = hp.beta2 * v0 + (1.f - hp.beta2) * g * g;
       Mo[pi] = m;
       Vo[pi] = v;
-      const float p = P[pi] - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
+      const float p = p0 - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
       P[pi] = p;
-      int64_t so = -1;
+      int so = -1;
       if (tn.cols > 0) {
-        const int64_t row = i / tn.cols, col = i - row * tn.cols;
+        const int ii = (int)i;
+        const int row = ii / tn.cols, col = ii - row * tn.cols;
         so = row * tn.ld + col;
         S[tn.s_off + so] = from_f<T>(p);
       }
       if (do_polyak) {
-        const int64_t ti = tn.t_off + i;
-        const float tp = hp.tau * p + (1.f - hp.tau) * P[ti];
-        P[ti] = tp;
+        const float tp = hp.tau * p + (1.f - hp.tau) * tp0;
+        P[tn.t_off + i] = tp;
         if (so >= 0) S[tn.ts_off + so] = from_f<T>(tp);
       }
     }
@@ -638,7 +652,7 @@ __global__ void __launch_bounds__(256) adam_polyak_kernel(const AdamTensor* __re
 }
 // Row-sharded learners: sum each tensor's split partials (fixed order) into the contiguous
 // gradient buffer that is then all-reduced across the group.
-__global__ void __launch_bounds__(256) reduce_partials_kernel(const AdamTensor* __restrict__ tensors,
+__global__ void __launch_bounds__(ADAM_SEG) reduce_partials_kernel(const AdamTensor* __restrict__ tensors,
                                                               const AdamSegment* __restrict__ segs, float* __restrict__ Gred) {
   pdl_wait();
   pdl_launch();

@@ -164,10 +164,22 @@ static spz_status dalloc(spz_learner* Lr, void** p, size_t bytes) {
     if (_s != SPZ_OK) return _s; \
   } while (0)
 
-static int wgrad_splits(int64_t Bl) {
-  // enough CTAs to cover the SMs several times over for the skinny [h x Bl] x [Bl x in] products
-  int s = (int)std::max<int64_t>(1, std::min<int64_t>(32, Bl / 256));
-  return s;
+// Split-K count of the merged weight-gradient GEMM: enough splits that the output tiles of all
+// trained weights (128 x 256 each) cover the SMs about once -- more splits only add partial traffic
+// for the Adam kernel.  Monotone in Bl (partials are allocated for the largest batch).
+static int wgrad_splits(const spz_learner* Lr, int64_t Bl) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC, critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
+  int64_t tiles = 0;
+  auto net_tiles = [&](const NetLayout& n, int layers) {
+    for (int l = 0; l < layers; ++l) tiles += cdiv(n.out[l], 128) * cdiv(n.in[l], 256);
+  };
+  if (critic_on) net_tiles(Lr->net[NET_Q1], Lr->net[NET_Q1].nl - 1), net_tiles(Lr->net[NET_Q2], Lr->net[NET_Q2].nl - 1);
+  if (actor_on) net_tiles(Lr->net[NET_ACTOR], Lr->net[NET_ACTOR].nl);
+  const int64_t fill = std::max<int64_t>(1, sms / std::max<int64_t>(1, tiles));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(32, fill), Bl / 256));
 }
 static int64_t wgrad_rows(int64_t Bl, int s) { return round_up(cdiv(Bl, s), 128); }
 static int bias_splits(int64_t Bl) { return (int)std::max<int64_t>(1, std::min<int64_t>(128, cdiv(Bl, 128))); }
@@ -185,7 +197,7 @@ struct TensorSlot {
 static std::vector<TensorSlot> trained_tensors(spz_learner* Lr) {
   std::vector<TensorSlot> v;
   const bool actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC, critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
-  const int Sw = wgrad_splits(Lr->max_local), Sb = bias_splits(Lr->max_local);
+  const int Sw = wgrad_splits(Lr, Lr->max_local), Sb = bias_splits(Lr->max_local);
   auto add_net = [&](int id) {
     const NetLayout& n = Lr->net[id];
     for (int l = 0; l < n.nl; ++l) {
@@ -266,7 +278,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
   const uint64_t seed = Lr->cfg.seed;
   const float lo = (float)Lr->cfg.log_std_min, hi = (float)Lr->cfg.log_std_max;
   const int delay = std::max(1, Lr->cfg.td3_policy_delay);
-  const int Sw = wgrad_splits(Bl), Sb = bias_splits(Bl);
+  const int Sw = wgrad_splits(Lr, Bl), Sb = bias_splits(Bl);
   const int64_t rows_w = wgrad_rows(Bl, Sw), rows_b = cdiv(Bl, Sb);
   auto Wp = [&](int id, int l) -> const T* { return S + Lr->sbase[id] + Lr->net[id].sw[l]; };
   auto bp = [&](int id, int l) -> const float* { return P + Lr->pbase[id] + Lr->net[id].b[l]; };
@@ -720,7 +732,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         float* Gr = Lr->Gred;
         const unsigned nsg = (unsigned)segs.size();
         ops.push_back({"grad_reduce", [=](cudaStream_t st) {
-                         return launch_pdl(reduce_partials_kernel, dim3(nsg), dim3(256), 0, st, dt, ds, Gr);
+                         return launch_pdl(reduce_partials_kernel, dim3(nsg), dim3(ADAM_SEG), 0, st, dt, ds, Gr);
                        }});
         if (Lr->cfg.comm_mode == 0 || Lr->cfg.comm_mode == 2) {
           const Comm cm = Lr->gcomm;
@@ -762,7 +774,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       int* fl = Lr->d_flag;
       const unsigned nseg = (unsigned)segs.size();
       ops.push_back({"adam_polyak", [=](cudaStream_t st) {
-                       return launch_pdl(adam_polyak_kernel<T>, dim3(nseg), dim3(256), 0, st, dt, ds, hp, Pm, Mm, Vm, S, ctr, fl);
+                       return launch_pdl(adam_polyak_kernel<T>, dim3(nseg), dim3(ADAM_SEG), 0, st, dt, ds, hp, Pm, Mm, Vm, S, ctr, fl);
                      }});
     }
     // ---- a10: split roles exchange the updated parameters at the step boundary:

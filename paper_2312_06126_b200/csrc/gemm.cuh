@@ -26,6 +26,8 @@ enum EpiKind : int {
   EPI_SAC_HEAD = 4,   // acc + bias -> squashed-Gaussian head (heads.cuh), nothing stored in C
   EPI_TD3_HEAD = 5,   // acc + bias -> tanh head with target smoothing (heads.cuh)
   EPI_MASK_BITS = 6,  // C (T) = acc * bit(aux[m, n / 32], n % 32)                        -- dgrad, packed ReLU mask
+  EPI_WGRAD_BIAS = 7, // C (f32) = acc, and colsum_out[split][m] = sum_k A(m, k)               -- wgrad + bias grad
+                      // (tcgen05 only: one extra MMA against an all-ones operand on the n-tile 0 tiles)
 };
 
 struct GemmGroup {
@@ -39,13 +41,15 @@ struct GemmGroup {
   float* dot_out;
   uint32_t* mask_out;  // EPI_BIAS_RELU: if set, bit n % 32 of mask_out[m * mask_ld + n / 32] = (z[m, n] > 0)
   int64_t split_stride;  // elements between split partials in C
+  float* colsum_out;     // EPI_WGRAD_BIAS: per-split row sums of A (bias gradient partials), may be null
+  int64_t colsum_stride; // elements between split partials in colsum_out
   int M, N;
   int lda, ldb, ldc, ldaux;
   int row0;     // head epilogues: local actor-pass row of this group's row 0
   int mask_ld;  // words per row of mask_out
 };
 
-constexpr int MAX_GROUPS = 8;
+constexpr int MAX_GROUPS = 12;
 
 struct GemmArgs {
   int N, K;  // N: max over groups (grid width)

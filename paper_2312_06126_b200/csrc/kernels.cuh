@@ -199,6 +199,8 @@ struct LossArgs {
   const float *qt1, *qt2, *q1, *q2, *logp2, *logp, *r, *d, *log_alpha;
   const int64_t* step_p;
   float *gq1, *gq2, *y;
+  __nv_bfloat16* gq16[2];  // optional: bf16 copies of the loss-row g_q (pitch 8, column 0) -- the A operand
+                           // of the critic-head weight / bias gradients on the tensor cores
   double* partials;
   double* totals;
   unsigned* ticket;
@@ -235,6 +237,10 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
       g2 = 2.f * e2 * a.invB;
       a.gq1[j] = g1;
       a.gq2[j] = g2;
+      if (a.gq16[0]) {
+        a.gq16[0][(int64_t)j * 8] = __float2bfloat16_rn(g1);
+        a.gq16[1][(int64_t)j * 8] = __float2bfloat16_rn(g2);
+      }
       gs[0][0][threadIdx.x] = g1;
       gs[1][0][threadIdx.x] = g2;
       v[0] = (double)e1 * e1 + (double)e2 * e2;
@@ -559,77 +565,91 @@ struct AdamHyper {
   int alpha_auto, critic_on, actor_on;
 };
 
+// beta^t for integer t >= 0 by repeated squaring (double; ~2 log2 t multiplies)
+__device__ __forceinline__ double ipow(double beta, int64_t t) {
+  double r = 1.0;
+  while (t > 0) {
+    if (t & 1) r *= beta;
+    beta *= beta;
+    t >>= 1;
+  }
+  return r;
+}
+
+// Persistent: block b handles segments b, b + gridDim.x, ...  Per block, thread 0 works out what
+// every element needs (non-finite losses -> skip, bias corrections of the three optimizers, the
+// log-alpha gradient) while the block's first gradient loads are in flight; block 0's warp 1
+// publishes the full statistics off that path.
 template <typename T>
 __global__ void __launch_bounds__(ADAM_SEG) adam_polyak_kernel(const AdamTensor* __restrict__ tensors,
-                                                               const AdamSegment* __restrict__ segs, AdamHyper hp,
-                                                               float* __restrict__ P, float* __restrict__ Mo,
-                                                               float* __restrict__ Vo, T* __restrict__ S,
+                                                               const AdamSegment* __restrict__ segs, int n_segs,
+                                                               AdamHyper hp, float* __restrict__ P,
+                                                               float* __restrict__ Mo, float* __restrict__ Vo,
+                                                               T* __restrict__ S,
                                                                int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
                                                                int* __restrict__ flag) {
   pdl_wait();
   pdl_launch();
-  __shared__ float g_alpha, bc1_s, bc2_s;
+  __shared__ float g_alpha, bc1_s[3], bc2_s[3];
   __shared__ bool skip, last;
-  const AdamSegment sg = segs[blockIdx.x];
-  const AdamTensor tn = tensors[sg.tensor];
-  const int k = threadIdx.x;
-  const bool valid = k < sg.count;
-  const int64_t i = sg.start + k;
-  const int64_t pi = tn.p_off + i;
-  // gradient and optimizer state first: these loads are in flight while thread 0 works out the
-  // statistics of the step
-  float g = 0.f, m0 = 0.f, v0 = 0.f, p0 = 0.f, tp0 = 0.f;
-  if (valid) {
-    if (tn.opt != 2) g = partial_sum(tn, i);
-    m0 = Mo[pi];
-    v0 = Vo[pi];
-    p0 = P[pi];
-    if (tn.t_off >= 0) tp0 = P[tn.t_off + i];
-  }
   const int64_t step = counters[0];
   bool delayed = true;
   if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
+  const double* tot = hp.totals;
   if (threadIdx.x == 0) {
-    // statistics of the step from the loss totals (identical in every block); block 0 publishes them
+    // the step's losses are finite iff their totals are (B > 0); TD3 has no log-prob total
+    const bool bad = !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) ||
+                     (!hp.td3 && !isfinite(tot[4]));
+    if (bad) atomicExch(flag, 1);
+    skip = bad || *flag;  // halted: parameters stay at the state before the failing step
+    g_alpha = (float)(-(tot[4] / hp.B + hp.target_entropy));
+    for (int o = 0; o < 3; ++o) {
+      const int64_t t = counters[1 + o] + 1;
+      bc1_s[o] = (float)(1.0 - ipow((double)hp.beta1, t));
+      bc2_s[o] = (float)(1.0 - ipow((double)hp.beta2, t));
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 32) {
     StatsOut o;
     float ga;
-    const bool bad = step_stats(hp.totals, (double)*hp.log_alpha, hp.target_entropy, hp.B, hp.td3, step, &o, &ga);
-    if (bad) atomicExch(flag, 1);
-    if (blockIdx.x == 0) *hp.stats = o;
-    g_alpha = ga;
-    skip = bad || *flag;  // halted: parameters stay at the state before the failing step
-    const double t = (double)(counters[1 + tn.opt] + 1);
-    bc1_s = (float)(1.0 - pow((double)hp.beta1, t));
-    bc2_s = (float)(1.0 - pow((double)hp.beta2, t));
+    step_stats(tot, (double)*hp.log_alpha, hp.target_entropy, hp.B, hp.td3, step, &o, &ga);
+    *hp.stats = o;
   }
   __syncthreads();
-  const bool active = !skip && !(hp.td3 && tn.opt == 1 && !delayed);  // TD3 actor: delayed steps only
-  if (active && valid) {
-    const float bc1 = bc1_s, bc2 = bc2_s;
-    const float lr = hp.lr[tn.opt];
-    const bool do_polyak = tn.t_off >= 0 && (!hp.td3 || delayed);
-    if (tn.opt == 2) g = g_alpha;  // log-alpha gradient -(mean log pi~ + H_bar) from the (group) totals
+  for (int seg = blockIdx.x; seg < n_segs; seg += gridDim.x) {
+    const AdamSegment sg = segs[seg];
+    const AdamTensor tn = tensors[sg.tensor];
+    const int k = threadIdx.x;
+    if (k >= sg.count) continue;
+    const int64_t i = sg.start + k;
+    const int64_t pi = tn.p_off + i;
+    const bool active = !skip && !(hp.td3 && tn.opt == 1 && !delayed);  // TD3 actor: delayed steps only
+    if (!active) continue;
+    const float g = tn.opt == 2 ? g_alpha  // log-alpha gradient -(mean log pi~ + H_bar) from the (group) totals
+                                : partial_sum(tn, i);
     if (!isfinite(g)) {
       atomicExch(flag, 2);
-    } else {
-      const float m = hp.beta1 * m0 + (1.f - hp.beta1) * g;
-      const float v = hp.beta2 * v0 + (1.f - hp.beta2) * g * g;
-      Mo[pi] = m;
-      Vo[pi] = v;
-      const float p = p0 - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
-      P[pi] = p;
-      int so = -1;
-      if (tn.cols > 0) {
-        const int ii = (int)i;
-        const int row = ii / tn.cols, col = ii - row * tn.cols;
-        so = row * tn.ld + col;
-        S[tn.s_off + so] = from_f<T>(p);
-      }
-      if (do_polyak) {
-        const float tp = hp.tau * p + (1.f - hp.tau) * tp0;
-        P[tn.t_off + i] = tp;
-        if (so >= 0) S[tn.ts_off + so] = from_f<T>(tp);
-      }
+      continue;
+    }
+    const float bc1 = bc1_s[tn.opt], bc2 = bc2_s[tn.opt];
+    const float lr = hp.lr[tn.opt];
+    const float m = hp.beta1 * Mo[pi] + (1.f - hp.beta1) * g;
+    const float v = hp.beta2 * Vo[pi] + (1.f - hp.beta2) * g * g;
+    Mo[pi] = m;
+    Vo[pi] = v;
+    const float p = P[pi] - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
+    P[pi] = p;
+    int so = -1;
+    if (tn.cols > 0) {
+      const int ii = (int)i;
+      const int row = ii / tn.cols, col = ii - row * tn.cols;
+      so = row * tn.ld + col;
+      S[tn.s_off + so] = from_f<T>(p);
+    }
+    if (tn.t_off >= 0 && (!hp.td3 || delayed)) {  // Polyak
+      const float tp = hp.tau * p + (1.f - hp.tau) * P[tn.t_off + i];
+      P[tn.t_off + i] = tp;
+      if (so >= 0) S[tn.ts_off + so] = from_f<T>(tp);
     }
   }
   // the last block to finish advances the step and optimizer counters

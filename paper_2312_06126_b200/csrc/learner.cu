@@ -107,6 +107,7 @@ struct spz_learner {
   int mw = 0;                   // mask words per row
   float* H = nullptr;
   float *q_on[2] = {}, *q_tg[2] = {}, *gq[2] = {}, *dXc[2] = {};
+  __nv_bfloat16* gq16[2] = {};  // bf16 loss-row g_q, pitch 8 (tensor-core head gradients)
   float *logp = nullptr, *logp2 = nullptr, *r = nullptr, *d = nullptr, *y = nullptr;
   HeadCache cache{};
   int32_t* idx = nullptr;
@@ -176,7 +177,7 @@ static int wgrad_splits(const spz_learner* Lr, int64_t Bl) {
   auto net_tiles = [&](const NetLayout& n, int layers) {
     for (int l = 0; l < layers; ++l) tiles += cdiv(n.out[l], 128) * cdiv(n.in[l], 256);
   };
-  if (critic_on) net_tiles(Lr->net[NET_Q1], Lr->net[NET_Q1].nl - 1), net_tiles(Lr->net[NET_Q2], Lr->net[NET_Q2].nl - 1);
+  if (critic_on) net_tiles(Lr->net[NET_Q1], Lr->net[NET_Q1].nl), net_tiles(Lr->net[NET_Q2], Lr->net[NET_Q2].nl);
   if (actor_on) net_tiles(Lr->net[NET_ACTOR], Lr->net[NET_ACTOR].nl);
   const int64_t fill = std::max<int64_t>(1, sms / std::max<int64_t>(1, tiles));
   return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(32, fill), Bl / 256));
@@ -203,8 +204,9 @@ static std::vector<TensorSlot> trained_tensors(spz_learner* Lr) {
     for (int l = 0; l < n.nl; ++l) {
       const bool head_vec = (id == NET_Q1 || id == NET_Q2) && l == n.nl - 1;  // N = 1 head: column sums
       // weight partials keep a 16-byte row pitch (TMA stores): out x round_up(in, 4)
-      v.push_back({id, l, true, (int64_t)n.out[l] * (head_vec ? n.in[l] : round_up(n.in[l], 4)), 0, head_vec ? Sb : Sw});
-      v.push_back({id, l, false, (int64_t)n.out[l], 0, Sb});
+      v.push_back({id, l, true, (int64_t)n.out[l] * (head_vec ? n.in[l] : round_up(n.in[l], 4)), 0,
+                   head_vec ? std::max(Sb, Sw) : Sw});
+      v.push_back({id, l, false, (int64_t)n.out[l], 0, std::max(Sb, Sw)});
     }
   };
   if (critic_on) {
@@ -341,6 +343,9 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     // fused epilogues (row dot, actor heads, packed ReLU masks) exist only in the tcgen05 kernel
     auto tc_ok = [&](const GemmArgs& a) { return std::is_same<T, __nv_bfloat16>::value && tc_gemm_supported(a); };
     const bool bits = std::is_same<T, __nv_bfloat16>::value && tc_gemm_available();
+    // bias (and critic-head) gradients come out of the weight-gradient GEMM (EPI_WGRAD_BIAS) on the
+    // tensor-core path; the FP32 path sums columns (colsum_multi_kernel)
+    const bool fuse_bias = bits;
     const int mw = Lr->mw;
     HeadEpi he{};
     he.m = m;
@@ -522,6 +527,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         la.A[i] = Lr->Aon[i][L - 1];
         la.w[i] = P + Lr->pbase[NET_Q1 + i] + cn.w[L];
         la.dZ[i] = Lr->dZc[i][L - 1];
+        la.gq16[i] = fuse_bias ? Lr->gq16[i] : nullptr;
       }
       la.gamma = (float)Lr->cfg.gamma;
       la.invB = invB;
@@ -572,9 +578,30 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           g.M = h;
           g.N = cn.in[l];
           g.split_stride = (int64_t)h * g.ldc;
+          if (fuse_bias) {
+            g.colsum_out = Lr->G + slot_of(NET_Q1 + i, l, false).g_off;
+            g.colsum_stride = h;
+          }
           wgrads.push_back(g);
         }
       for (int i = 0; i < (do_critic ? 2 : 0); ++i) {
+        if (fuse_bias) {
+          // critic head: dw_L = g_q^T A_{L-1}, db_L = sum g_q, with g_q (bf16) as a one-row A operand
+          GemmGroup g{};
+          g.A = Lr->gq16[i];
+          g.lda = 8;
+          g.B = Lr->Aon[i][L - 1];
+          g.ldb = h;
+          g.C = Lr->G + slot_of(NET_Q1 + i, L, true).g_off;
+          g.ldc = h;
+          g.M = 1;
+          g.N = h;
+          g.split_stride = h;
+          g.colsum_out = Lr->G + slot_of(NET_Q1 + i, L, false).g_off;
+          g.colsum_stride = 1;
+          wgrads.push_back(g);
+          continue;
+        }
         for (int l = 0; l < L; ++l)
           colsums.push_back({Lr->dZc[i][l], nullptr, Lr->G + slot_of(NET_Q1 + i, l, false).g_off, h, h, Bl, 0});
         colsums.push_back({Lr->Aon[i][L - 1], Lr->gq[i], Lr->G + slot_of(NET_Q1 + i, L, true).g_off, h, h, Bl, 0});
@@ -628,9 +655,13 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         g.M = an.out[l];
         g.N = an.in[l];
         g.split_stride = (int64_t)an.out[l] * g.ldc;
+        if (fuse_bias) {
+          g.colsum_out = Lr->G + slot_of(NET_ACTOR, l, false).g_off;
+          g.colsum_stride = an.out[l];
+        }
         wgrads.push_back(g);
       }
-      for (int l = 0; l <= L; ++l)
+      for (int l = 0; l <= L && !fuse_bias; ++l)
         colsums.push_back({l == L ? (const void*)dH : (const void*)Lr->dZa[l], nullptr,
                            Lr->G + slot_of(NET_ACTOR, l, false).g_off, l == L ? ldh : h, an.out[l], Bl, 0});
       (void)nout;
@@ -638,7 +669,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     // ---- every weight gradient (split-K over the batch, <= 8 tensors per launch) and every bias
     //      gradient (one column-sum launch)
     {
-      GemmArgs a = mk(Bl, EPI_F32, 1, 1);
+      GemmArgs a = mk(Bl, fuse_bias ? EPI_WGRAD_BIAS : EPI_F32, 1, 1);
       a.splits = Sw;
       a.k_per_split = (int)rows_w;
       for (const GemmGroup& g : wgrads) {
@@ -674,7 +705,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         const bool head_vec = (s.net == NET_Q1 || s.net == NET_Q2) && s.layer == n.nl - 1;
         t.numel = s.weight ? (int64_t)n.out[s.layer] * n.in[s.layer] : n.out[s.layer];
         t.partials = Lr->G + s.g_off;
-        t.n_partials = s.weight && !head_vec ? Sw : Sb;
+        t.n_partials = (s.weight && !head_vec) || fuse_bias ? Sw : Sb;
         t.pld = s.weight ? (head_vec ? n.in[s.layer] : (int)round_up(n.in[s.layer], 4)) : 1;
         t.pstride = s.weight ? (int64_t)n.out[s.layer] * t.pld : n.out[s.layer];
         t.opt = s.net == NET_ACTOR ? 1 : 0;
@@ -772,9 +803,13 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       float *Pm = Lr->P, *Mm = Lr->Mo, *Vm = Lr->Vo;
       int64_t* ctr = Lr->counters;
       int* fl = Lr->d_flag;
-      const unsigned nseg = (unsigned)segs.size();
+      const int nseg = (int)segs.size();
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, Lr->device);
+      const unsigned ngrid = (unsigned)std::min(nseg, 4 * sms);  // persistent: <= 4 blocks per SM
       ops.push_back({"adam_polyak", [=](cudaStream_t st) {
-                       return launch_pdl(adam_polyak_kernel<T>, dim3(nseg), dim3(ADAM_SEG), 0, st, dt, ds, hp, Pm, Mm, Vm, S, ctr, fl);
+                       return launch_pdl(adam_polyak_kernel<T>, dim3(ngrid), dim3(ADAM_SEG), 0, st, dt, ds, nseg, hp, Pm, Mm, Vm,
+                                         S, ctr, fl);
                      }});
     }
     // ---- a10: split roles exchange the updated parameters at the step boundary:
@@ -1027,6 +1062,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->q_on[i], 2 * Bm * sizeof(float)));
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->q_tg[i], Bm * sizeof(float)));
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->gq[i], 2 * Bm * sizeof(float)));
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->gq16[i], Bm * 8 * sizeof(__nv_bfloat16)));
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->dXc[i], Bm * Lr->ldc * sizeof(float)));
   }
   for (float** f : {&Lr->logp, &Lr->logp2, &Lr->r, &Lr->d, &Lr->y}) SPZ_TRY(dalloc(Lr.get(), (void**)f, Bm * sizeof(float)));

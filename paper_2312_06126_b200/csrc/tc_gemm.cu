@@ -248,6 +248,7 @@ struct EpiShape {
   static constexpr bool HEAD = EK == EPI_SAC_HEAD;
   static constexpr bool RELU = EK == EPI_BIAS_RELU;
   static constexpr bool MASKB = EK == EPI_MASK_BITS;
+  static constexpr bool BIASCOL = EK == EPI_WGRAD_BIAS;  // + row sums of A through an all-ones MMA
   static constexpr bool BIAS = RELU || HEAD || EK == EPI_BIAS_F32;
   static constexpr bool OBF = RELU || MASKB;            // bf16 output, else fp32
   static constexpr bool SPLIT = BN >= 64 && !HEAD;      // the WPQ warps of a lane quarter split the columns
@@ -255,6 +256,12 @@ struct EpiShape {
   static constexpr int CPB = OBF ? 2 : 1;               // chunks per 64-byte store block (= one mask word)
   static constexpr int NB = (CPW + CPB - 1) / CPB;      // store blocks per warp
   static constexpr int SLICE = CPW * 16;                // columns per warp
+  // TMEM: NBUF accumulator buffers of BUF_COLS columns (BIASCOL: + 16 row-sum columns at BN)
+  static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
+  static constexpr int BUF_COLS = BIASCOL ? ACC_COLS + 16 : ACC_COLS;
+  static constexpr int NBUF = 2 * BUF_COLS <= 512 ? 2 : 1;
+  static constexpr int TMEM_COLS = NBUF * BUF_COLS <= 32 ? 32 : NBUF * BUF_COLS <= 64 ? 64 : NBUF * BUF_COLS <= 128 ? 128
+                                   : NBUF * BUF_COLS <= 256 ? 256 : 512;
 };
 
 // Persistent, warp-specialized: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the TMA producer
@@ -266,8 +273,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   using S = EpiShape<BN, EK>;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int STAGE = A_BYTES + B_BYTES;
-  constexpr uint32_t ACC_COLS = BN < 32 ? 32 : BN;  // one accumulator buffer
-  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;       // double-buffered
+  constexpr uint32_t BUF_COLS = S::BUF_COLS;    // one accumulator buffer
+  constexpr uint32_t TMEM_COLS = S::TMEM_COLS;
+  constexpr int NBUF = S::NBUF;
+  // all-ones operand (N = 16, K-major) for the row sums of A
+  constexpr uint32_t IDESC1 = (1u << 4) | (1u << 7) | (1u << 10) | ((AMN ? 1u : 0u) << 15) | (2u << 17) |
+                              ((uint32_t)(BM >> 4) << 24);
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) |
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   // per epilogue warp: its slice of the tile's bias / row-dot weights; row-dot partials per quarter
@@ -284,6 +295,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   // per epilogue warp: two 32-row x 64-byte staging blocks for the TMA stores (1024-byte aligned)
   uint8_t* stage_s = smem + NS * STAGE + 1024;
+  uint8_t* ones_s = stage_s + NUM_EPI_WARPS * 4096;  // 16 x 64 bf16 ones (2 KB, 1024-aligned)
+  if constexpr (S::BIASCOL) {
+    for (int i = threadIdx.x; i < 2048 / 16; i += NTHREADS)
+      reinterpret_cast<uint4*>(ones_s)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    fence_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
+  }
 
   const GemmArgs& a = p.a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -361,10 +378,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         const int k_begin = ti.split * a.k_per_split;
         const int k_end = min(a.K, k_begin + a.k_per_split);
         const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
-        const int b = tile_i & 1;
-        mbar_wait(&acc_empty[b], (((uint32_t)tile_i >> 1) & 1u) ^ 1u);
+        const int b = tile_i % NBUF;
+        mbar_wait(&acc_empty[b], (((uint32_t)(tile_i / NBUF)) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t acc = tmem + (uint32_t)b * ACC_COLS;
+        const uint32_t acc = tmem + (uint32_t)b * BUF_COLS;
+        const bool bcol = S::BIASCOL && ti.n0 == 0 && a.g[ti.grp].colsum_out != nullptr;
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
           const int s = kg % NS;
           const uint32_t ph = (uint32_t)(kg / NS) & 1u;
@@ -377,6 +395,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
             const uint64_t ad = AMN ? desc_mnmajor(sA, kk) : desc_kmajor(sA, kk);
             const uint64_t bd = BMN ? desc_mnmajor(sB, kk) : desc_kmajor(sB, kk);
             umma_bf16(acc, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+          }
+          if constexpr (S::BIASCOL) {
+            if (bcol) {
+              const uint32_t so = smem_u32(ones_s);
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint64_t ad = AMN ? desc_mnmajor(sA, kk) : desc_kmajor(sA, kk);
+                umma_bf16(acc + S::ACC_COLS, ad, desc_kmajor(so, kk), IDESC1, (kb | kk) != 0 ? 1u : 0u);
+              }
+            }
           }
           umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
         }
@@ -431,11 +459,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         }
       }
       __syncwarp();
-      const int b = tile_i & 1;
-      mbar_wait(&acc_full[b], ((uint32_t)tile_i >> 1) & 1u);
+      const int b = tile_i % NBUF;
+      mbar_wait(&acc_full[b], ((uint32_t)(tile_i / NBUF)) & 1u);
       tc_fence_after();
       if (e == 0 && lane == 0) trace(tile_i, 2);
-      const uint32_t trow = tmem + (uint32_t)b * ACC_COLS + ((uint32_t)(q * 32) << 16);
+      const uint32_t trow = tmem + (uint32_t)b * BUF_COLS + ((uint32_t)(q * 32) << 16);
       if constexpr (S::HEAD) {
         if (hh == 0) {
           float hrow[BN];
@@ -521,6 +549,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
 #pragma unroll
             for (int cc = 0; cc < S::CPB; ++cc)
               if (n0 + (c + cc) * 16 < g.N) direct16<S::OBF>(g, ti.split, m, n0 + (c + cc) * 16, v[cc]);
+          }
+        }
+        if constexpr (S::BIASCOL) {
+          // row sums of A (every one of the 16 columns holds the same sum)
+          if (hh == 0 && ti.n0 == 0 && g.colsum_out != nullptr) {
+            float v[16];
+            if (has_acc) tmem_ld16(trow + S::ACC_COLS, v);
+            else v[0] = 0.f;
+            if (m < g.M) g.colsum_out[(int64_t)ti.split * g.colsum_stride + m] = v[0];
           }
         }
         if (e == 0 && lane == 0) trace(tile_i, 3);
@@ -613,8 +650,8 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 }
 
 // dynamic shared memory besides the pipeline stages: alignment slack, barriers + TMEM slot,
-// per-warp TMA store staging
-constexpr int smem_extras() { return 1024 + 1024 + NUM_EPI_WARPS * 4096; }
+// per-warp TMA store staging, the all-ones operand
+constexpr int smem_extras() { return 1024 + 1024 + NUM_EPI_WARPS * 4096 + 2048; }
 // static shared memory of one instantiation (per-warp bias / row-dot slices, row-dot partials)
 template <int BN, int EK>
 constexpr int smem_static() {
@@ -650,7 +687,7 @@ cudaError_t launch(TcParams& p, cudaStream_t st) {
   p.tile0[p.a.n_groups] = T;
   p.total_tiles = T;
   if (T == 0) return cudaSuccess;
-  constexpr int TMEM_COLS = 2 * (BN < 32 ? 32 : BN);
+  constexpr int TMEM_COLS = EpiShape<BN, EK>::TMEM_COLS;
   static int occ = [&] {
     int o = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, NTHREADS, STAGE + smem_extras());
@@ -676,7 +713,7 @@ constexpr bool ek_ok(int epi, int bn) {
     return epi == EPI_BIAS_RELU || epi == EPI_BIAS_F32 || epi == EPI_F32 ||
            ((epi == EPI_SAC_HEAD || epi == EPI_TD3_HEAD) && bn <= 64);
   if (!AMN && BMN) return epi == EPI_MASK_BITS || epi == EPI_F32;
-  if (AMN && BMN) return epi == EPI_F32;
+  if (AMN && BMN) return epi == EPI_F32 || epi == EPI_WGRAD_BIAS;
   return false;
 }
 
@@ -698,6 +735,7 @@ cudaError_t launch_ek(TcParams& p, cudaStream_t st) {
     if (p.a.epi == EPI_F32) return launch<BN, AMN, BMN, EPI_F32>(p, st);
   } else {
     if (p.a.epi == EPI_F32) return launch<BN, AMN, BMN, EPI_F32>(p, st);
+    if (p.a.epi == EPI_WGRAD_BIAS) return launch<BN, AMN, BMN, EPI_WGRAD_BIAS>(p, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -774,7 +812,7 @@ cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st) {
   std::memset(&p, 0, sizeof(p));
   p.a = a;
   // epilogue stores through TMA when every group's C qualifies (heads store nothing through C)
-  const bool f32out = a.epi == EPI_F32 || a.epi == EPI_BIAS_F32;
+  const bool f32out = a.epi == EPI_F32 || a.epi == EPI_BIAS_F32 || a.epi == EPI_WGRAD_BIAS;
   p.out_bytes = f32out ? 4 : 2;
   p.tma_out = (a.epi == EPI_BIAS_RELU || a.epi == EPI_MASK_BITS || f32out) ? 1 : 0;
   for (int i = 0; i < a.n_groups && p.tma_out; ++i) {

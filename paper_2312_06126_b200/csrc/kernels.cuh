@@ -203,6 +203,8 @@ struct LossArgs {
                            // of the critic-head weight / bias gradients on the tensor cores
   double* partials;
   double* totals;
+  int64_t* ctr_snap;  // the step's counters (step, t_c, t_a, t_al) as read before the optimizer advances them
+  float* la_snap;     // the step's log alpha (statistics), likewise
   unsigned* ticket;
   const void* A[2];          // last hidden activations (mask source when mask[] is null)
   const uint32_t* mask[2];   // packed ReLU masks of the last hidden layer (tcgen05 path)
@@ -381,6 +383,8 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
       a.totals[threadIdx.x] = u;
     }
     if (threadIdx.x == 0) *a.ticket = 0u;
+    if (threadIdx.x < 4) a.ctr_snap[threadIdx.x] = a.step_p[threadIdx.x];
+    if (threadIdx.x == 4) *a.la_snap = *a.log_alpha;
   }
 }
 
@@ -503,11 +507,11 @@ __device__ __forceinline__ bool step_stats(const double* __restrict__ tot, doubl
 }
 
 // ------------------------------------------------------------------ a9: fused multi-tensor Adam + Polyak
-// One block per segment of <= ADAM_SEG elements of one tensor, one element per thread:
+// Per element of every trained tensor:
 // g = sum_s partial[s] (fixed order); Adam with the optimizer's own t; master,
 // m, v updated; operand shadow (T, padded row stride) refreshed; if the tensor
 // has a target: theta' = tau theta_new + (1 - tau) theta' (+ its shadow).
-constexpr int ADAM_SEG = 256;  // one element per thread
+constexpr int ADAM_NT = 256, ADAM_EPT = 2, ADAM_SEG = ADAM_NT * ADAM_EPT;  // elements per block
 
 struct AdamTensor {
   int64_t p_off;      // master offset of element 0
@@ -548,9 +552,10 @@ __device__ __forceinline__ float partial_sum(const AdamTensor& tn, int64_t i64) 
   return g;
 }
 struct AdamSegment {
-  int32_t tensor;
-  int32_t count;
+  AdamTensor t;       // the tensor (embedded: one dependent load per segment)
   int64_t start;      // element index within the tensor
+  int32_t count;
+  int32_t pad_;
 };
 struct AdamHyper {
   float lr[3];
@@ -558,128 +563,118 @@ struct AdamHyper {
   int td3, delay;
   // statistics + counter advance folded into this kernel
   const double* totals;  // loss totals of the step (this rank's, or the group's after the allreduce)
-  const float* log_alpha;
+  const float* log_alpha;  // as of the start of the step (loss-kernel snapshot)
   StatsOut* stats;
   double target_entropy, B;
-  unsigned* ticket;
+  const int64_t* snap;  // counters of this step (written by the loss kernel); the kernel advances `counters`
   int alpha_auto, critic_on, actor_on;
 };
 
-// beta^t for integer t >= 0 by repeated squaring (double; ~2 log2 t multiplies)
-__device__ __forceinline__ double ipow(double beta, int64_t t) {
-  double r = 1.0;
-  while (t > 0) {
-    if (t & 1) r *= beta;
-    beta *= beta;
-    t >>= 1;
-  }
-  return r;
-}
-
-// Persistent: block b handles segments b, b + gridDim.x, ...  Per block, thread 0 works out what
-// every element needs (non-finite losses -> skip, bias corrections of the three optimizers, the
-// log-alpha gradient) while the block's first gradient loads are in flight; block 0's warp 1
-// publishes the full statistics off that path.
+// One block per segment of ADAM_SEG elements (ADAM_EPT per thread, independent).  Every load of a
+// thread is issued before the block barrier behind which thread 0 decides whether the step is
+// applied (non-finite loss totals or an earlier halt); block 0 also publishes the statistics and
+// advances the counters from the loss kernel's snapshot -- no block reads `counters` here, so no
+// grid-wide handshake is needed.  (A non-finite gradient element sets the sticky flag 2: the step
+// itself counts, every later step is skipped.)
 template <typename T>
-__global__ void __launch_bounds__(ADAM_SEG) adam_polyak_kernel(const AdamTensor* __restrict__ tensors,
-                                                               const AdamSegment* __restrict__ segs, int n_segs,
-                                                               AdamHyper hp, float* __restrict__ P,
-                                                               float* __restrict__ Mo, float* __restrict__ Vo,
-                                                               T* __restrict__ S,
-                                                               int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
-                                                               int* __restrict__ flag) {
+__global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegment* __restrict__ segs, AdamHyper hp,
+                                                                 float* __restrict__ P, float* __restrict__ Mo,
+                                                                 float* __restrict__ Vo, T* __restrict__ S,
+                                                                 int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
+                                                                 int* __restrict__ flag) {
   pdl_wait();
   pdl_launch();
-  __shared__ float g_alpha, bc1_s[3], bc2_s[3];
-  __shared__ bool skip, last;
-  const int64_t step = counters[0];
-  bool delayed = true;
-  if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
+  __shared__ bool skip;
+  const AdamTensor tn = segs[blockIdx.x].t;
+  const int64_t start = segs[blockIdx.x].start;
+  const int count = segs[blockIdx.x].count;
+  const int64_t step = hp.snap[0];
+  const int64_t topt = hp.snap[1 + tn.opt];
   const double* tot = hp.totals;
-  if (threadIdx.x == 0) {
-    // the step's losses are finite iff their totals are (B > 0); TD3 has no log-prob total
-    const bool bad = !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) ||
-                     (!hp.td3 && !isfinite(tot[4]));
-    if (bad) atomicExch(flag, 1);
-    skip = bad || *flag;  // halted: parameters stay at the state before the failing step
-    g_alpha = (float)(-(tot[4] / hp.B + hp.target_entropy));
-    for (int o = 0; o < 3; ++o) {
-      const int64_t t = counters[1 + o] + 1;
-      bc1_s[o] = (float)(1.0 - ipow((double)hp.beta1, t));
-      bc2_s[o] = (float)(1.0 - ipow((double)hp.beta2, t));
+  float g[ADAM_EPT], m0[ADAM_EPT], v0[ADAM_EPT], p0[ADAM_EPT], tp0[ADAM_EPT];
+#pragma unroll
+  for (int u = 0; u < ADAM_EPT; ++u) {
+    const int k = threadIdx.x + u * ADAM_NT;
+    g[u] = m0[u] = v0[u] = p0[u] = tp0[u] = 0.f;
+    if (k < count) {
+      const int64_t i = start + k, pi = tn.p_off + i;
+      m0[u] = Mo[pi];
+      v0[u] = Vo[pi];
+      p0[u] = P[pi];
+      if (tn.t_off >= 0) tp0[u] = P[tn.t_off + i];
+      g[u] = tn.opt == 2 ? (float)(-(tot[4] / hp.B + hp.target_entropy))  // log-alpha gradient
+                         : partial_sum(tn, i);
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 32) {
+  // bias corrections 1 - beta^t without cancellation (computed while the loads are in flight)
+  const double t = (double)(topt + 1);
+  const float bc1 = (float)(-expm1(t * log1p((double)hp.beta1 - 1.0)));
+  const float bc2 = (float)(-expm1(t * log1p((double)hp.beta2 - 1.0)));
+  bool delayed = true;
+  if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
+  bool bad = false;
+  if (threadIdx.x == 0) {
+    // the step's losses are finite iff their totals are (B > 0); TD3 has no log-prob total
+    bad = !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) || (!hp.td3 && !isfinite(tot[4]));
+    const int f = *flag;
+    if (bad && blockIdx.x == 0) atomicExch(flag, 1);
+    skip = bad || f;  // halted: parameters stay at the state before the failing step
+  }
+  __syncthreads();
+  const bool active = !skip && !(hp.td3 && tn.opt == 1 && !delayed);  // TD3 actor: delayed steps only
+  if (active) {
+    const float lr = hp.lr[tn.opt];
+#pragma unroll
+    for (int u = 0; u < ADAM_EPT; ++u) {
+      const int k = threadIdx.x + u * ADAM_NT;
+      if (k >= count) continue;
+      if (!isfinite(g[u])) {
+        atomicExch(flag, 2);
+        continue;
+      }
+      const int64_t i = start + k, pi = tn.p_off + i;
+      const float m = hp.beta1 * m0[u] + (1.f - hp.beta1) * g[u];
+      const float v = hp.beta2 * v0[u] + (1.f - hp.beta2) * g[u] * g[u];
+      Mo[pi] = m;
+      Vo[pi] = v;
+      const float p = p0[u] - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
+      P[pi] = p;
+      int so = -1;
+      if (tn.cols > 0) {
+        const int ii = (int)i;
+        const int row = ii / tn.cols, col = ii - row * tn.cols;
+        so = row * tn.ld + col;
+        S[tn.s_off + so] = from_f<T>(p);
+      }
+      if (tn.t_off >= 0 && (!hp.td3 || delayed)) {  // Polyak
+        const float tp = hp.tau * p + (1.f - hp.tau) * tp0[u];
+        P[tn.t_off + i] = tp;
+        if (so >= 0) S[tn.ts_off + so] = from_f<T>(tp);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     StatsOut o;
     float ga;
     step_stats(tot, (double)*hp.log_alpha, hp.target_entropy, hp.B, hp.td3, step, &o, &ga);
     *hp.stats = o;
-  }
-  __syncthreads();
-  for (int seg = blockIdx.x; seg < n_segs; seg += gridDim.x) {
-    const AdamSegment sg = segs[seg];
-    const AdamTensor tn = tensors[sg.tensor];
-    const int k = threadIdx.x;
-    if (k >= sg.count) continue;
-    const int64_t i = sg.start + k;
-    const int64_t pi = tn.p_off + i;
-    const bool active = !skip && !(hp.td3 && tn.opt == 1 && !delayed);  // TD3 actor: delayed steps only
-    if (!active) continue;
-    const float g = tn.opt == 2 ? g_alpha  // log-alpha gradient -(mean log pi~ + H_bar) from the (group) totals
-                                : partial_sum(tn, i);
-    if (!isfinite(g)) {
-      atomicExch(flag, 2);
-      continue;
-    }
-    const float bc1 = bc1_s[tn.opt], bc2 = bc2_s[tn.opt];
-    const float lr = hp.lr[tn.opt];
-    const float m = hp.beta1 * Mo[pi] + (1.f - hp.beta1) * g;
-    const float v = hp.beta2 * Vo[pi] + (1.f - hp.beta2) * g * g;
-    Mo[pi] = m;
-    Vo[pi] = v;
-    const float p = P[pi] - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
-    P[pi] = p;
-    int so = -1;
-    if (tn.cols > 0) {
-      const int ii = (int)i;
-      const int row = ii / tn.cols, col = ii - row * tn.cols;
-      so = row * tn.ld + col;
-      S[tn.s_off + so] = from_f<T>(p);
-    }
-    if (tn.t_off >= 0 && (!hp.td3 || delayed)) {  // Polyak
-      const float tp = hp.tau * p + (1.f - hp.tau) * P[tn.t_off + i];
-      P[tn.t_off + i] = tp;
-      if (so >= 0) S[tn.ts_off + so] = from_f<T>(tp);
-    }
-  }
-  // the last block to finish advances the step and optimizer counters
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(hp.ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    *hp.ticket = 0u;
-    if (!atomicAdd(flag, 0)) {
-      if (hp.critic_on) counters[1] += 1;
-      if (hp.actor_on && delayed) counters[2] += 1;
-      if (hp.actor_on && hp.alpha_auto && !hp.td3) counters[3] += 1;
+    if (!skip) {
+      counters[1] = hp.snap[1] + (hp.critic_on ? 1 : 0);
+      counters[2] = hp.snap[2] + (hp.actor_on && delayed ? 1 : 0);
+      counters[3] = hp.snap[3] + (hp.actor_on && hp.alpha_auto && !hp.td3 ? 1 : 0);
       counters[0] = step + 1;
     }
   }
 }
 // Row-sharded learners: sum each tensor's split partials (fixed order) into the contiguous
 // gradient buffer that is then all-reduced across the group.
-__global__ void __launch_bounds__(ADAM_SEG) reduce_partials_kernel(const AdamTensor* __restrict__ tensors,
-                                                              const AdamSegment* __restrict__ segs, float* __restrict__ Gred) {
+__global__ void __launch_bounds__(ADAM_NT) reduce_partials_kernel(const AdamSegment* __restrict__ segs,
+                                                                 float* __restrict__ Gred) {
   pdl_wait();
   pdl_launch();
-  const AdamSegment sg = segs[blockIdx.x];
-  const AdamTensor tn = tensors[sg.tensor];
-  for (int k = threadIdx.x; k < sg.count; k += blockDim.x) {
-    const int64_t i = sg.start + k;
+  const AdamTensor tn = segs[blockIdx.x].t;
+  for (int k = threadIdx.x; k < segs[blockIdx.x].count; k += blockDim.x) {
+    const int64_t i = segs[blockIdx.x].start + k;
     Gred[tn.red_off + i] = partial_sum(tn, i);
   }
 }

@@ -115,9 +115,8 @@ struct spz_learner {
   int max_stat_blocks = 0;
   float* G = nullptr;  // gradient partials
   int64_t G_total = 0;
-  AdamTensor* d_tensors = nullptr;
   AdamSegment* d_segs = nullptr;
-  int max_tensors = 64, max_segs = 0;
+  int max_segs = 0;
   ShadowEntry* d_shadow = nullptr;
   int n_shadow = 0;
   // row-sharded group (world_size > 1) and actor/critic split roles
@@ -137,7 +136,8 @@ struct spz_learner {
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   int n_adam_segs = 0;
   uint64_t sync_version = 0;
-  unsigned* tickets = nullptr;  // last-block counters of the loss and Adam kernels
+  unsigned* tickets = nullptr;  // last-block counter of the loss kernel
+  int64_t* ctr_snap = nullptr;  // counters as read at the start of the step (loss kernel -> Adam)
   std::vector<void*> allocs;
   struct DebugBuf { std::string name; void* ptr; size_t bytes; int esz; };
   std::vector<DebugBuf> debug;
@@ -521,6 +521,8 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       la.partials = Lr->stat_partials;
       la.totals = Lr->statsum;
       la.ticket = Lr->tickets;
+      la.ctr_snap = Lr->ctr_snap;
+      la.la_snap = reinterpret_cast<float*>(Lr->ctr_snap + 4);
       la.mask_ld = mw;
       for (int i = 0; i < 2; ++i) {
         la.mask[i] = bits ? Lr->mask_c[i][L - 1] : nullptr;
@@ -715,10 +717,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         int tid = s.net == NET_Q1 ? NET_Q1T : s.net == NET_Q2 ? NET_Q2T : (td3 ? NET_ACTORT : -1);
         t.t_off = tid >= 0 ? Lr->pbase[tid] + (s.weight ? n.w[s.layer] : n.b[s.layer]) : -1;
         t.ts_off = (tid >= 0 && s.weight) ? Lr->sbase[tid] + n.sw[s.layer] : -1;
-        const int ti = (int)tens.size();
         tens.push_back(t);
-        for (int64_t st = 0; st < t.numel; st += ADAM_SEG)
-          segs.push_back({ti, (int32_t)std::min<int64_t>(ADAM_SEG, t.numel - st), st});
       }
       if (!td3 && Lr->cfg.alpha_auto && Lr->cfg.role != SPZ_ROLE_CRITIC) {
         AdamTensor t{};
@@ -729,7 +728,6 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         t.opt = 2;
         t.s_off = t.t_off = t.ts_off = -1;
         tens.push_back(t);
-        segs.push_back({(int)tens.size() - 1, 1, 0});
       }
       // red_off: position of each tensor in the contiguous gradient buffer (sharded mode)
       {
@@ -739,15 +737,26 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           off += round_up(t.numel, 16);
         }
       }
-      const int nten = (int)tens.size(), nsegs = (int)segs.size();
-      if (4 * (nten + 1) > Lr->max_tensors || 4 * (nsegs + 1) > Lr->max_segs)
-        return fail(SPZ_EINVAL, "internal: Adam table overflow");
-      const size_t tb = tens.size() * sizeof(AdamTensor), sb = segs.size() * sizeof(AdamSegment);
-      AdamTensor* dt = Lr->d_tensors + variant * (Lr->max_tensors / 4);
+      auto segments = [](const std::vector<AdamTensor>& ts) {
+        std::vector<AdamSegment> v;
+        for (const AdamTensor& t : ts)
+          for (int64_t st = 0; st < t.numel; st += ADAM_SEG) {
+            AdamSegment sg{};
+            sg.t = t;
+            sg.start = st;
+            sg.count = (int32_t)std::min<int64_t>(ADAM_SEG, t.numel - st);
+            v.push_back(sg);
+          }
+        return v;
+      };
+      segs = segments(tens);
+      const int nsegs = (int)segs.size();
+      if (4 * (nsegs + 1) > Lr->max_segs) return fail(SPZ_EINVAL, "internal: Adam table overflow");
+      const size_t sb = segs.size() * sizeof(AdamSegment);
       AdamSegment* ds = Lr->d_segs + variant * (Lr->max_segs / 4);
       if (sharded) {
-        // table 1 (partials -> Gred) is `tens`; table 2 (Gred -> Adam) replaces the partial sources
-        AdamTensor* dt2 = Lr->d_tensors + (2 + variant) * (Lr->max_tensors / 4);
+        // table 1 (partials -> Gred) is `segs`; table 2 (Gred -> Adam) replaces the partial sources
+        AdamSegment* ds2 = Lr->d_segs + (2 + variant) * (Lr->max_segs / 4);
         std::vector<AdamTensor> tens2 = tens;
         for (auto& t : tens2) {
           if (t.opt == 2) continue;  // log alpha: gradient computed from the all-reduced totals
@@ -756,14 +765,14 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           t.pld = t.cols > 0 ? t.cols : 1;  // dense
           t.pstride = t.numel;
         }
-        SPZ_CUDA_TRY(cudaMemcpyAsync(dt2, tens2.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
-        SPZ_CUDA_TRY(cudaMemcpyAsync(dt, tens.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
+        const std::vector<AdamSegment> segs2 = segments(tens2);
+        SPZ_CUDA_TRY(cudaMemcpyAsync(ds2, segs2.data(), sb, cudaMemcpyHostToDevice, Lr->stream));
         SPZ_CUDA_TRY(cudaMemcpyAsync(ds, segs.data(), sb, cudaMemcpyHostToDevice, Lr->stream));
         SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
         float* Gr = Lr->Gred;
         const unsigned nsg = (unsigned)segs.size();
         ops.push_back({"grad_reduce", [=](cudaStream_t st) {
-                         return launch_pdl(reduce_partials_kernel, dim3(nsg), dim3(ADAM_SEG), 0, st, dt, ds, Gr);
+                         return launch_pdl(reduce_partials_kernel, dim3(nsg), dim3(ADAM_NT), 0, st, (const AdamSegment*)ds, Gr);
                        }});
         if (Lr->cfg.comm_mode == 0 || Lr->cfg.comm_mode == 2) {
           const Comm cm = Lr->gcomm;
@@ -775,9 +784,8 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
                            return comm_allreduce_sum(cm, ss, NSTAT, true, st);
                          }, 0});
         }
-        dt = dt2;
+        ds = ds2;
       } else {
-        SPZ_CUDA_TRY(cudaMemcpyAsync(dt, tens.data(), tb, cudaMemcpyHostToDevice, Lr->stream));
         SPZ_CUDA_TRY(cudaMemcpyAsync(ds, segs.data(), sb, cudaMemcpyHostToDevice, Lr->stream));
         SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
       }
@@ -792,24 +800,21 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       hp.td3 = td3;
       hp.delay = delay;
       hp.totals = Lr->statsum;
-      hp.log_alpha = P + Lr->p_log_alpha;
+      hp.log_alpha = reinterpret_cast<const float*>(Lr->ctr_snap + 4);
       hp.stats = Lr->d_stats;
       hp.target_entropy = Lr->cfg.target_entropy;
       hp.B = (double)B;
-      hp.ticket = Lr->tickets + 1;
+      hp.snap = Lr->ctr_snap;
       hp.alpha_auto = Lr->cfg.alpha_auto;
       hp.critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
       hp.actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC;
       float *Pm = Lr->P, *Mm = Lr->Mo, *Vm = Lr->Vo;
       int64_t* ctr = Lr->counters;
       int* fl = Lr->d_flag;
-      const int nseg = (int)segs.size();
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, Lr->device);
-      const unsigned ngrid = (unsigned)std::min(nseg, 4 * sms);  // persistent: <= 4 blocks per SM
+      const unsigned nseg = (unsigned)segs.size();
       ops.push_back({"adam_polyak", [=](cudaStream_t st) {
-                       return launch_pdl(adam_polyak_kernel<T>, dim3(ngrid), dim3(ADAM_SEG), 0, st, dt, ds, nseg, hp, Pm, Mm, Vm,
-                                         S, ctr, fl);
+                       return launch_pdl(adam_polyak_kernel<T>, dim3(nseg), dim3(ADAM_NT), 0, st, (const AdamSegment*)ds, hp, Pm,
+                                         Mm, Vm, S, ctr, fl);
                      }});
     }
     // ---- a10: split roles exchange the updated parameters at the step boundary:
@@ -1106,6 +1111,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->G, Lr->G_total * sizeof(float)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->statsum, 8 * sizeof(double)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->tickets, 8 * sizeof(unsigned)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->ctr_snap, 8 * sizeof(int64_t)));
   Lr->debug.push_back({"statsum", Lr->statsum, 8 * sizeof(double), 8});
   if (Lr->gsize > 1 || cfg->comm_mode == 2) {
     int64_t tot = 0;
@@ -1138,8 +1144,6 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   int64_t nseg = 0;
   for (auto& t : slots) nseg += cdiv(t.numel, ADAM_SEG);
   Lr->max_segs = (int)(4 * (nseg + 4));
-  Lr->max_tensors = 4 * ((int)slots.size() + 4);
-  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_tensors, Lr->max_tensors * sizeof(AdamTensor)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_segs, Lr->max_segs * sizeof(AdamSegment)));
   // shadow table: every W of every net
   std::vector<ShadowEntry> sh;

@@ -31,7 +31,9 @@ struct NetLayout {
   int64_t np = 0, ns = 0;
 };
 
-static NetLayout make_layout(int in, int h, int L, int out) {
+// kpad: row pitch granule of the layer-0 weight shadow (64 on the tensor-core path: 128-byte rows, so
+// the first layer's TMA boxes are whole rows and its contraction runs over the zero-padded width)
+static NetLayout make_layout(int in, int h, int L, int out, int kpad) {
   NetLayout n;
   n.nl = L + 1;
   int64_t p = 0, s = 0;
@@ -42,7 +44,7 @@ static NetLayout make_layout(int in, int h, int L, int out) {
     p += (int64_t)n.in[l] * n.out[l];
     n.b[l] = p;
     p += n.out[l];
-    n.ld[l] = (int)round_up(n.in[l], 8);
+    n.ld[l] = (int)round_up(n.in[l], l == 0 ? kpad : 8);
     n.sw[l] = s;
     s += round_up((int64_t)n.out[l] * n.ld[l], 64);
   }
@@ -400,7 +402,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         if (do_actor) passes.push_back({NET_ACTOR, Bl, Bl});
       }
       for (int l = 0; l < L && !passes.empty(); ++l) {
-        GemmArgs a = mk(an.in[l], EPI_BIAS_RELU, 0, 0);
+        GemmArgs a = mk(l == 0 ? lda : an.in[l], EPI_BIAS_RELU, 0, 0);  // layer 0: over the zero-padded width
         for (const Pass& ps : passes) {
           GemmGroup& g = add(a, l == 0 ? (const void*)Ta(Lr->Xa, ps.row, lda) : (const void*)Ta(Lr->Aact[l - 1], ps.row, h),
                              l == 0 ? lda : h, Wp(ps.id, l), ldw(ps.id, l), Ta(Lr->Aact[l], ps.row, h), h, ps.M, h, bp(ps.id, l));
@@ -447,7 +449,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     const int Mon = (do_critic ? Bl : 0) + (do_actor ? Bl : 0);
     {
       for (int l = 0; l < L; ++l) {
-        GemmArgs a = mk(cn.in[l], EPI_BIAS_RELU, 0, 0);
+        GemmArgs a = mk(l == 0 ? ldc : cn.in[l], EPI_BIAS_RELU, 0, 0);  // layer 0: over the zero-padded width
         for (int pass = 0; pass < 2; ++pass) {
           const bool tgt = pass == 1;
           if (tgt && !do_critic) continue;
@@ -1014,8 +1016,9 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   Lr->max_local = cfg->max_batch / W + (cfg->max_batch % W ? 1 : 0);
   // networks
   const int aout = Lr->td3 ? m : 2 * m;
-  Lr->net[NET_ACTOR] = make_layout(o, h, L, aout);
-  Lr->net[NET_Q1] = Lr->net[NET_Q2] = Lr->net[NET_Q1T] = Lr->net[NET_Q2T] = make_layout(o + m, h, L, 1);
+  const int kpad = Lr->bf16 ? 64 : 8;
+  Lr->net[NET_ACTOR] = make_layout(o, h, L, aout, kpad);
+  Lr->net[NET_Q1] = Lr->net[NET_Q2] = Lr->net[NET_Q1T] = Lr->net[NET_Q2T] = make_layout(o + m, h, L, 1, kpad);
   Lr->net[NET_ACTORT] = Lr->net[NET_ACTOR];
   int64_t p = 0, s = 0;
   for (int id = 0; id < N_NETS; ++id) {
@@ -1043,8 +1046,9 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     return fail(SPZ_ENOMEM, "spz_learner_create: pinned host allocation failed");
   // activations
   const int64_t Bm = Lr->max_local;
-  Lr->lda = (int)round_up(o, 8);
-  Lr->ldc = (int)round_up(o + m, 8);
+  // input rows padded like the layer-0 weights (the padding columns stay zero)
+  Lr->lda = (int)round_up(o, kpad);
+  Lr->ldc = (int)round_up(o + m, kpad);
   Lr->ldh = (int)round_up(aout, 8);
   const size_t E = Lr->esz;
   SPZ_TRY(dalloc(Lr.get(), &Lr->Xa, 2 * Bm * Lr->lda * E));

@@ -90,6 +90,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 // until the previous grid has completed and its writes are visible (so semantics equal
 // plain stream order).  Both are no-ops for ordinary launches.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Release/acquire fence at GPU scope (cheaper than __threadfence's sequentially consistent fence):
+// publishes this thread's prior writes before a subsequent atomic, or orders an atomic's
+// observation before subsequent reads.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 template <typename... KArgs, typename... Args>

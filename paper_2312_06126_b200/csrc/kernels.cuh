@@ -193,7 +193,7 @@ __device__ __forceinline__ void block_stats(double (&v)[NSTAT], double* __restri
 // then the critic head backward for those rows: dZ_L[r, n] = g_q[r] w_out[n] 1[A_L[r, n] > 0].
 // Loss statistics: per-block partials; the last block to finish sums them in block order into
 // `totals` (this rank's loss totals; all-reduced across a row-sharded group).
-constexpr int LOSS_ROWS = 16, LOSS_NT = 256;
+constexpr int LOSS_ROWS = 32, LOSS_NT = 256, LOSS_RPW = LOSS_ROWS / (LOSS_NT / 32);  // rows per warp
 
 struct LossArgs {
   const float *qt1, *qt2, *q1, *q2, *logp2, *logp, *r, *d, *log_alpha;
@@ -214,159 +214,200 @@ struct LossArgs {
   int Bl, td3, delay, loss_rows, actor_rows, h, ld, mask_ld;
 };
 
+// Block = LOSS_ROWS rows, warp w owns rows w, w + 8, ... (LOSS_RPW of them).  Every lane loads the
+// row scalars (broadcast) and computes g_q itself, then writes its 8-column chunks of dZ_L; all of
+// a warp's loads are issued before any of its arithmetic.  Lane 0 accumulates the statistics of
+// the warp's rows in row order; the block partial sums the warps in order.
 template <typename T>
 __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_constant__ LossArgs a) {
   pdl_wait();
   pdl_launch();
-  __shared__ float gs[2][2][LOSS_ROWS];  // [critic][loss | actor row][row]
   __shared__ double red[LOSS_NT / 32][NSTAT];
   __shared__ bool last;
   const int j0 = blockIdx.x * LOSS_ROWS;
-  const int nr = min(LOSS_ROWS, a.Bl - j0);
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int hv = a.h / 8;
+  const bool lr = a.loss_rows, ar = a.actor_rows;
+  const bool bits = std::is_same<T, __nv_bfloat16>::value && a.mask[0] != nullptr;
+  const float alpha = a.td3 ? 0.f : expf(*a.log_alpha);
+  const bool td3_on = a.td3 && ((*a.step_p + 1) % a.delay) == 0;
+  // ---- loads, all issued before any use: row scalars of the warp's rows (row index clamped, so
+  //      every address is valid; rows past Bl are discarded below), mask words and head weights of
+  //      this lane's 8-column chunk (h <= 256: one chunk per lane)
+  float qt1[LOSS_RPW], qt2[LOSS_RPW], q1[LOSS_RPW], q2[LOSS_RPW], lp2[LOSS_RPW], rw[LOSS_RPW], dn[LOSS_RPW];
+  float a1[LOSS_RPW], a2[LOSS_RPW], lp[LOSS_RPW];
+  const bool one_chunk = hv <= 32;
+  const int n0 = lane * 8;
+  const bool has_chunk = one_chunk && lane < hv;
+  const int nc = has_chunk ? n0 : 0;
+  uint32_t mk[LOSS_RPW][2][2];
+#pragma unroll
+  for (int i = 0; i < LOSS_RPW; ++i) {
+    const int j = min(j0 + wi + 8 * i, a.Bl - 1);
+    qt1[i] = __ldg(a.qt1 + j);
+    qt2[i] = __ldg(a.qt2 + j);
+    q1[i] = __ldg(a.q1 + j);
+    q2[i] = __ldg(a.q2 + j);
+    rw[i] = __ldg(a.r + j);
+    dn[i] = __ldg(a.d + j);
+    lp2[i] = a.td3 ? 0.f : __ldg(a.logp2 + j);
+    a1[i] = __ldg(a.q1 + a.Bl + j);
+    a2[i] = __ldg(a.q2 + a.Bl + j);
+    lp[i] = a.td3 ? 0.f : __ldg(a.logp + j);
+#pragma unroll
+    for (int ci = 0; ci < 2; ++ci)
+#pragma unroll
+      for (int kind = 0; kind < 2; ++kind)
+        mk[i][ci][kind] = bits ? __ldg(a.mask[ci] + ((int64_t)(kind ? a.Bl : 0) + j) * a.mask_ld + nc / 32) : 0u;
+  }
+  float wv[2][8];
+#pragma unroll
+  for (int ci = 0; ci < 2; ++ci) {
+    const float4 w0 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + nc));
+    const float4 w1 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + nc + 4));
+    wv[ci][0] = w0.x, wv[ci][1] = w0.y, wv[ci][2] = w0.z, wv[ci][3] = w0.w;
+    wv[ci][4] = w1.x, wv[ci][5] = w1.y, wv[ci][6] = w1.z, wv[ci][7] = w1.w;
+  }
+  // mask bytes of the chunk (bit k = column nc + k)
+#pragma unroll
+  for (int i = 0; i < LOSS_RPW; ++i)
+#pragma unroll
+    for (int ci = 0; ci < 2; ++ci)
+#pragma unroll
+      for (int kind = 0; kind < 2; ++kind) {
+        if (bits) {
+          mk[i][ci][kind] = (mk[i][ci][kind] >> (nc & 31)) & 0xFFu;
+          continue;
+        }
+        const int64_t row = (int64_t)(kind ? a.Bl : 0) + min(j0 + wi + 8 * i, a.Bl - 1);
+        uint32_t mb = 0u;
+        if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(static_cast<const T*>(a.A[ci]) + row * a.ld + nc));
+          const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(x[k]);
+            mb |= (f.x > 0.f ? 1u : 0u) << (2 * k);
+            mb |= (f.y > 0.f ? 1u : 0u) << (2 * k + 1);
+          }
+        } else {
+          const T* A = static_cast<const T*>(a.A[ci]) + row * a.ld + nc;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mb |= (to_f(__ldg(A + k)) > 0.f ? 1u : 0u) << k;
+        }
+        mk[i][ci][kind] = mb;
+      }
   double v[NSTAT] = {0, 0, 0, 0, 0, 0};
-  if (threadIdx.x < nr) {
-    const int j = j0 + threadIdx.x;
-    const float alpha = a.td3 ? 0.f : expf(*a.log_alpha);
-    float g1, g2;
-    if (a.loss_rows) {
-      const float qmin = fminf(a.qt1[j], a.qt2[j]);
-      const float boot = a.td3 ? qmin : qmin - alpha * a.logp2[j];
-      const float y = a.r[j] + a.gamma * (1.f - a.d[j]) * boot;
-      a.y[j] = y;
-      const float q1 = a.q1[j], q2 = a.q2[j];
-      const float e1 = q1 - y, e2 = q2 - y;
-      g1 = 2.f * e1 * a.invB;
-      g2 = 2.f * e2 * a.invB;
-      a.gq1[j] = g1;
-      a.gq2[j] = g2;
-      if (a.gq16[0]) {
-        a.gq16[0][(int64_t)j * 8] = __float2bfloat16_rn(g1);
-        a.gq16[1][(int64_t)j * 8] = __float2bfloat16_rn(g2);
+  // ---- per row: g_q (every lane), statistics (lane 0), dZ_L chunk of this lane
+#pragma unroll
+  for (int i = 0; i < LOSS_RPW; ++i) {
+    const int rr = wi + 8 * i, j = j0 + rr;
+    if (j >= a.Bl) break;  // warp-uniform
+    float g[2][2] = {{0.f, 0.f}, {0.f, 0.f}};  // [critic][loss | actor row]
+    if (lr) {
+      const float qmin = fminf(qt1[i], qt2[i]);
+      const float boot = a.td3 ? qmin : qmin - alpha * lp2[i];
+      const float y = rw[i] + a.gamma * (1.f - dn[i]) * boot;
+      const float e1 = q1[i] - y, e2 = q2[i] - y;
+      g[0][0] = 2.f * e1 * a.invB;
+      g[1][0] = 2.f * e2 * a.invB;
+      if (lane == 0) {
+        a.y[j] = y;
+        a.gq1[j] = g[0][0];
+        a.gq2[j] = g[1][0];
+        if (a.gq16[0]) {
+          a.gq16[0][(int64_t)j * 8] = __float2bfloat16_rn(g[0][0]);
+          a.gq16[1][(int64_t)j * 8] = __float2bfloat16_rn(g[1][0]);
+        }
+        v[0] += (double)e1 * e1 + (double)e2 * e2;
+        v[1] += q1[i];
+        v[2] += q2[i];
       }
-      gs[0][0][threadIdx.x] = g1;
-      gs[1][0][threadIdx.x] = g2;
-      v[0] = (double)e1 * e1 + (double)e2 * e2;
-      v[1] = q1;
-      v[2] = q2;
     }
-    if (a.actor_rows) {
-      const float a1 = a.q1[a.Bl + j], a2 = a.q2[a.Bl + j];
+    if (ar) {
       if (!a.td3) {
-        const float w1 = a1 < a2 ? 1.f : (a1 > a2 ? 0.f : 0.5f);
-        g1 = -w1 * a.invB;
-        g2 = -(1.f - w1) * a.invB;
-        v[3] = (double)alpha * a.logp[j] - (double)fminf(a1, a2);
-        v[4] = a.logp[j];
+        const float w1 = a1[i] < a2[i] ? 1.f : (a1[i] > a2[i] ? 0.f : 0.5f);
+        g[0][1] = -w1 * a.invB;
+        g[1][1] = -(1.f - w1) * a.invB;
       } else {
-        const bool on = ((*a.step_p + 1) % a.delay) == 0;
-        g1 = on ? -a.invB : 0.f;
-        g2 = 0.f;
-        v[3] = on ? -(double)a1 : 0.0;
+        g[0][1] = td3_on ? -a.invB : 0.f;
       }
-      a.gq1[a.Bl + j] = g1;
-      a.gq2[a.Bl + j] = g2;
-      gs[0][1][threadIdx.x] = g1;
-      gs[1][1][threadIdx.x] = g2;
+      if (lane == 0) {
+        a.gq1[a.Bl + j] = g[0][1];
+        a.gq2[a.Bl + j] = g[1][1];
+        if (!a.td3) {
+          v[3] += (double)alpha * lp[i] - (double)fminf(a1[i], a2[i]);
+          v[4] += lp[i];
+        } else {
+          v[3] += td3_on ? -(double)a1[i] : 0.0;
+        }
+      }
+    }
+    if (one_chunk) {
+      if (!has_chunk) continue;
+#pragma unroll
+      for (int ci = 0; ci < 2; ++ci)
+#pragma unroll
+        for (int kind = 0; kind < 2; ++kind) {
+          if (kind == 0 ? !lr : !ar) continue;
+          const int64_t row = (int64_t)(kind ? a.Bl : 0) + j;
+          const float gq = g[ci][kind];
+          const uint32_t mb = mk[i][ci][kind];
+          T* dZ = static_cast<T*>(a.dZ[ci]) + row * a.ld + n0;
+          if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+            uint4 o;
+            __nv_bfloat162* yv = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              yv[k] = __floats2bfloat162_rn((mb >> (2 * k)) & 1u ? gq * wv[ci][2 * k] : 0.f,
+                                            (mb >> (2 * k + 1)) & 1u ? gq * wv[ci][2 * k + 1] : 0.f);
+            *reinterpret_cast<uint4*>(dZ) = o;
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) dZ[k] = (mb >> k) & 1u ? gq * wv[ci][k] : 0.f;
+          }
+        }
+      continue;
+    }
+    // wide layers (h > 256): chunks c = lane, lane + 32, ... with inline mask loads
+    for (int c = lane; c < hv; c += 32) {
+      const int n = c * 8;
+#pragma unroll
+      for (int ci = 0; ci < 2; ++ci)
+#pragma unroll
+        for (int kind = 0; kind < 2; ++kind) {
+          if (kind == 0 ? !lr : !ar) continue;
+          const int64_t row = (int64_t)(kind ? a.Bl : 0) + j;
+          const float gq = g[ci][kind];
+          T* dZ = static_cast<T*>(a.dZ[ci]) + row * a.ld + n;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const bool on = bits ? ((a.mask[ci][row * a.mask_ld + (n + k) / 32] >> ((n + k) & 31)) & 1u)
+                                 : (to_f(static_cast<const T*>(a.A[ci])[row * a.ld + n + k]) > 0.f);
+            dZ[k] = from_f<T>(on ? gq * a.w[ci][n + k] : 0.f);
+          }
+        }
     }
   }
-  // block partial of the statistics (fixed shuffle tree, then warps in order)
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-#pragma unroll
-  for (int i = 0; i < NSTAT; ++i) v[i] = warp_sum(v[i]);
+  // block partial of the statistics: warps in order
   if (lane == 0)
 #pragma unroll
-    for (int i = 0; i < NSTAT; ++i) red[wi][i] = v[i];
+    for (int k = 0; k < NSTAT; ++k) red[wi][k] = v[k];
   __syncthreads();
   if (threadIdx.x < NSTAT) {
     double t = 0.0;
     for (int k = 0; k < LOSS_NT / 32; ++k) t += red[k][threadIdx.x];
     a.partials[blockIdx.x * NSTAT + threadIdx.x] = t;
   }
-  // critic head backward for this block's rows: per (row, 8-column chunk) item, the (critic, row kind)
-  // combinations are loaded together (independent 16-byte loads), then written
-  const int hv = a.h / 8;
-  const int per = nr * hv;
-  const int k_lo = a.loss_rows ? 0 : 1, k_hi = a.actor_rows ? 2 : 1;  // row kinds present: loss, actor
-  for (int e = threadIdx.x; e < per; e += LOSS_NT) {
-    const int rr = e / hv, n = (e - rr * hv) * 8;
-    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-      if (a.mask[0]) {
-        // packed ReLU masks: 8 bits per 8-column chunk
-        uint32_t mb[2][2];
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci)
-#pragma unroll
-          for (int kind = 0; kind < 2; ++kind)
-            mb[ci][kind] = (kind >= k_lo && kind < k_hi)
-                               ? (a.mask[ci][((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.mask_ld + n / 32] >> (n & 31)) & 0xFFu
-                               : 0u;
-#pragma unroll
-        for (int ci = 0; ci < 2; ++ci) {
-          const float4 w0 = *reinterpret_cast<const float4*>(a.w[ci] + n), w1 = *reinterpret_cast<const float4*>(a.w[ci] + n + 4);
-          const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-          for (int kind = 0; kind < 2; ++kind) {
-            if (kind < k_lo || kind >= k_hi) continue;
-            const float gq = gs[ci][kind][rr];
-            uint4 o;
-            __nv_bfloat162* yv = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              yv[i] = __floats2bfloat162_rn((mb[ci][kind] >> (2 * i)) & 1u ? gq * wv[2 * i] : 0.f,
-                                            (mb[ci][kind] >> (2 * i + 1)) & 1u ? gq * wv[2 * i + 1] : 0.f);
-            *reinterpret_cast<uint4*>(static_cast<T*>(a.dZ[ci]) + ((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.ld + n) = o;
-          }
-        }
-        continue;
-      }
-      uint4 u[2][2];
-#pragma unroll
-      for (int ci = 0; ci < 2; ++ci)
-#pragma unroll
-        for (int kind = 0; kind < 2; ++kind)
-          if (kind >= k_lo && kind < k_hi)
-            u[ci][kind] = *reinterpret_cast<const uint4*>(static_cast<const T*>(a.A[ci]) +
-                                                          ((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.ld + n);
-#pragma unroll
-      for (int ci = 0; ci < 2; ++ci) {
-        const float4 w0 = *reinterpret_cast<const float4*>(a.w[ci] + n), w1 = *reinterpret_cast<const float4*>(a.w[ci] + n + 4);
-        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-        for (int kind = 0; kind < 2; ++kind) {
-          if (kind < k_lo || kind >= k_hi) continue;
-          const float gq = gs[ci][kind][rr];
-          const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&u[ci][kind]);
-          uint4 o;
-          __nv_bfloat162* yv = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float2 f = __bfloat1622float2(x[i]);
-            yv[i] = __floats2bfloat162_rn(f.x > 0.f ? gq * wv[2 * i] : 0.f, f.y > 0.f ? gq * wv[2 * i + 1] : 0.f);
-          }
-          *reinterpret_cast<uint4*>(static_cast<T*>(a.dZ[ci]) + ((int64_t)(kind ? a.Bl : 0) + j0 + rr) * a.ld + n) = o;
-        }
-      }
-    } else {
-      for (int ci = 0; ci < 2; ++ci)
-        for (int kind = k_lo; kind < k_hi; ++kind) {
-          const int64_t row = (int64_t)(kind ? a.Bl : 0) + j0 + rr;
-          const float gq = gs[ci][kind][rr];
-          const T* A = static_cast<const T*>(a.A[ci]) + row * a.ld + n;
-          T* dZ = static_cast<T*>(a.dZ[ci]) + row * a.ld + n;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) dZ[i] = from_f<T>(to_f(A[i]) > 0.f ? gq * a.w[ci][n + i] : 0.f);
-        }
-    }
-  }
   // the last block sums every block's partial (fixed order: strided per thread, then a fixed tree)
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    fence_acq_rel_gpu();
     last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (last) {
-    __threadfence();
+    fence_acq_rel_gpu();
     double t[NSTAT] = {0, 0, 0, 0, 0, 0};
     for (unsigned b = threadIdx.x; b < gridDim.x; b += LOSS_NT)
 #pragma unroll

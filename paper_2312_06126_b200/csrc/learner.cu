@@ -7,6 +7,7 @@
 // per batch size into a CUDA graph and replayed n_steps times; the step counter and
 // the ring fill live in device memory so the replay needs no host updates.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -841,6 +842,17 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
                        return launch_pdl(shadow_refresh_kernel<T>, dim3(64, nsh), dim3(256), 0, st, sh, nsh, (const float*)P, S);
                      }, 1});
     }
+  }
+  // diagnostics only (results are wrong): SPZ_DIAG_SKIP_OPS="cls1,cls2" drops those op classes so a
+  // timing run shows their marginal cost inside the graph replay
+  if (const char* skip = std::getenv("SPZ_DIAG_SKIP_OPS")) {
+    for (auto& v : Lr->ops)
+      v.erase(std::remove_if(v.begin(), v.end(),
+                             [skip](const Op& op) {
+                               const std::string list = std::string(",") + skip + ",";
+                               return list.find(std::string(",") + op.cls + ",") != std::string::npos;
+                             }),
+              v.end());
   }
   Lr->plan_B = B;
   return SPZ_OK;

@@ -17,6 +17,7 @@
 #include "gemm.cuh"
 #include "internal.h"
 #include "kernels.cuh"
+#include "tc_mlp.cuh"
 #include "tc_gemm.cuh"
 
 namespace spz {
@@ -402,7 +403,47 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         if (do_critic) passes.push_back({NET_ACTORT, 0, Bl});
         if (do_actor) passes.push_back({NET_ACTOR, Bl, Bl});
       }
-      for (int l = 0; l < L && !passes.empty(); ++l) {
+      // fused multi-layer forward (hidden activations stay in SMEM between layers): one launch for
+      // every hidden layer and the head; s2 rows store nothing, s rows their activations + masks
+      bool fused = false;
+      if (bits && !passes.empty()) {
+        MlpArgs ma{};
+        ma.L = L;
+        ma.h = h;
+        ma.k0 = lda;
+        ma.head_n = an.out[L];
+        ma.head_epi = td3 ? EPI_TD3_HEAD : EPI_SAC_HEAD;
+        ma.mask_ld = mw;
+        ma.head = he;
+        for (const Pass& ps : passes) {
+          // split an [s2; s] pass at Bl: the s2 half needs no backward state
+          for (int half = 0; half < 2; ++half) {
+            const int64_t r0 = ps.row + (half ? Bl : 0);
+            if (r0 >= ps.row + ps.M) continue;
+            const int rows = (int)std::min<int64_t>(Bl, ps.row + ps.M - r0);
+            const bool srows = r0 >= Bl;  // s rows: the actor loss backpropagates through them
+            MlpPass& q = ma.p[ma.n_pass++];
+            q.X = Ta(Lr->Xa, r0, lda);
+            q.ldx = lda;
+            q.rows = rows;
+            q.row0 = (int)r0;
+            for (int l = 0; l <= L; ++l) {
+              q.W[l] = Wp(ps.id, l);
+              q.ldw[l] = ldw(ps.id, l);
+              q.bias[l] = bp(ps.id, l);
+            }
+            for (int l = 0; l < L && srows; ++l) {
+              q.act[l] = Ta(Lr->Aact[l], r0, h);
+              q.mask[l] = Lr->mask_a[l] + r0 * mw;
+            }
+          }
+        }
+        if (tc_mlp_supported(ma)) {
+          fused = true;
+          ops.push_back({"actor_fwd_mlp", [ma](cudaStream_t st) { return tc_mlp_fwd(ma, st); }});
+        }
+      }
+      for (int l = 0; l < L && !passes.empty() && !fused; ++l) {
         GemmArgs a = mk(l == 0 ? lda : an.in[l], EPI_BIAS_RELU, 0, 0);  // layer 0: over the zero-padded width
         for (const Pass& ps : passes) {
           GemmGroup& g = add(a, l == 0 ? (const void*)Ta(Lr->Xa, ps.row, lda) : (const void*)Ta(Lr->Aact[l - 1], ps.row, h),
@@ -417,7 +458,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       }
       // head layer: fused squashed-Gaussian (SAC) / tanh + smoothing (TD3) epilogue when possible
       // (TD3 actor role on a non-delayed step: no actor work at all)
-      if (!passes.empty()) {
+      if (!passes.empty() && !fused) {
       GemmArgs a = mk(h, td3 ? EPI_TD3_HEAD : EPI_SAC_HEAD, 0, 0);
       a.head = he;
       for (const Pass& ps : passes) {
@@ -448,7 +489,46 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     // online-critic rows [on0, on0 + Mon): loss rows [0, Bl) on the critic side, actor rows [Bl, 2Bl)
     const int on0 = do_critic ? 0 : Bl;
     const int Mon = (do_critic ? Bl : 0) + (do_actor ? Bl : 0);
-    {
+    bool cfused = false;
+    if (bits && (do_critic || do_actor)) {
+      // fused multi-layer critic forward: online loss rows (activations + masks stored), online
+      // actor rows (masks only: no critic weight gradient over them), target rows (nothing stored)
+      MlpArgs ma{};
+      ma.L = L;
+      ma.h = h;
+      ma.k0 = ldc;
+      ma.mask_ld = mw;
+      for (int kind = 0; kind < 3; ++kind) {
+        if (kind == 0 && !do_critic) continue;
+        if (kind == 1 && !do_actor) continue;
+        if (kind == 2 && !do_critic) continue;
+        for (int i = 0; i < 2; ++i) {
+          const int id = kind == 2 ? NET_Q1T + i : NET_Q1 + i;
+          const int64_t xr = kind * (int64_t)Bl;          // row in Xc
+          const int64_t ar = kind == 2 ? 0 : kind * (int64_t)Bl;  // row in the per-critic buffers
+          MlpPass& q = ma.p[ma.n_pass++];
+          q.X = Ta(Lr->Xc, xr, ldc);
+          q.ldx = ldc;
+          q.rows = Bl;
+          for (int l = 0; l < L; ++l) {
+            q.W[l] = Wp(id, l);
+            q.ldw[l] = cn.ld[l];
+            q.bias[l] = bp(id, l);
+            if (kind == 0) q.act[l] = Ta(Lr->Aon[i][l], ar, h);
+            if (kind != 2) q.mask[l] = Lr->mask_c[i][l] + ar * mw;
+          }
+          q.bias[L] = bp(id, L);
+          q.dot_w = P + Lr->pbase[id] + Lr->net[id].w[L];
+          q.dot_b = bp(id, L);
+          q.dot_out = (kind == 2 ? Lr->q_tg[i] : Lr->q_on[i]) + ar;
+        }
+      }
+      if (tc_mlp_supported(ma)) {
+        cfused = true;
+        ops.push_back({"critic_fwd_mlp", [ma](cudaStream_t st) { return tc_mlp_fwd(ma, st); }});
+      }
+    }
+    if (!cfused) {
       for (int l = 0; l < L; ++l) {
         GemmArgs a = mk(l == 0 ? ldc : cn.in[l], EPI_BIAS_RELU, 0, 0);  // layer 0: over the zero-padded width
         for (int pass = 0; pass < 2; ++pass) {

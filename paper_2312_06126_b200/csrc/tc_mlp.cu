@@ -1,0 +1,411 @@
+// tc_mlp.cu -- fused multi-layer MLP forward on the 5th-generation tensor cores (see tc_mlp.cuh).
+//
+// Warp roles (persistent CTA, one per SM):
+//   warp 0      TMA producer: for every (unit, layer, k-block) one pipeline stage -- layer 0 loads the
+//               input tile and the weight slab, deeper layers only the weight slab
+//   warp 1      TMEM allocator + MMA issuer: A from the stage (layer 0) or from the hidden buffer H
+//               (deeper layers), accumulator in TMEM buffer (unit & 1); one acc_full commit per layer
+//   warps 2..9  epilogue: TMEM lane quarter (warp % 4) x column half; per hidden layer bias + ReLU ->
+//               H (128B-swizzled K-major bf16, the next layer's A operand) + packed masks + row dot;
+//               activations leave by TMA bulk stores from H; the actor head runs on the last MMA.
+// Ordering: H is single-buffered.  The epilogue of (unit u, layer l) writes H only after the MMA of
+// layer l (which read H) has completed (its acc_full), and after the TMA stores issued from H for
+// layer l-1 have read it; it then signals h_full, on which the MMA of layer l+1 waits.  The next
+// unit's layer 0 runs in the other TMEM buffer meanwhile.
+#include "tc_mlp.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+#include "tc_common.cuh"
+
+namespace spz {
+
+namespace {
+
+constexpr int MBM = 128, MBK = 64, MSTAGES = 4;
+constexpr int M_EPI_WARPS = 8, M_NTHREADS = 64 + M_EPI_WARPS * 32;
+constexpr int MA_BYTES = MBM * MBK * 2;  // 16 KB input tile per k-block
+
+struct MlpDev {
+  int rows, row0;
+  const float* bias[MLP_MAXL + 1];
+  uint32_t* mask[MLP_MAXL];
+  int store[MLP_MAXL];  // activations of hidden layer l stored (tact valid)
+  const float* dot_w;
+  const float* dot_b;
+  float* dot_out;
+};
+
+struct MlpParams {
+  int n_pass, L, n_mma, k0, nh, head_n, head_epi, mask_ld, stages;
+  int total_units;
+  int unit0[MLP_MAXN + 1];
+  HeadEpi head;
+  MlpDev d[MLP_MAXN];
+  CUtensorMap tx[MLP_MAXN];
+  CUtensorMap tw[MLP_MAXN][MLP_MAXL + 1];
+  CUtensorMap tact[MLP_MAXN][MLP_MAXL];
+};
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+__device__ __forceinline__ int unit_pass(const MlpParams& p, int u) {
+  int g = 0;
+  while (g + 1 < p.n_pass && u >= p.unit0[g + 1]) ++g;
+  return g;
+}
+
+// H: hidden width of this instantiation; ACTOR: the last MMA layer is the actor head (else: critic,
+// row-dot head fused into the last hidden layer's epilogue).
+template <int H, bool ACTOR>
+__global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_constant__ MlpParams p) {
+  constexpr int STAGE = MA_BYTES + H * MBK * 2;  // input tile + weight slab (largest layer)
+  constexpr uint32_t BUF = H < 32 ? 32 : H;      // TMEM columns per accumulator buffer
+  constexpr uint32_t TMEM_COLS = 2 * BUF <= 64 ? 64 : 2 * BUF <= 128 ? 128 : 2 * BUF <= 256 ? 256 : 512;
+  constexpr int SLABS = H / 64;                  // 64-column slabs of H (16 KB each)
+  constexpr int CPW = H / 16 / 2;                // 16-column chunks per epilogue warp (two per quarter)
+  constexpr int NB = CPW / 2;                    // 32-column blocks (= mask words) per warp
+  constexpr int SLICE = CPW * 16;
+  static_assert(H % 64 == 0 && H <= 256, "hidden width");
+  __shared__ __align__(16) float bias_w[M_EPI_WARPS][SLICE > 16 ? SLICE : 16];
+  __shared__ __align__(16) float dotw_w[M_EPI_WARPS][SLICE];
+  __shared__ float dotpart[2][2][MBM];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int NS = p.stages;
+  uint8_t* Hs = smem + NS * STAGE;  // hidden buffer: SLABS x [128 rows x 128 B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Hs + SLABS * 16384);
+  uint64_t* empty = full + MSTAGES;
+  uint64_t* acc_full = empty + MSTAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* h_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = p.total_units;
+  const int L = p.L, NMMA = p.n_mma;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < p.n_pass; ++i) {
+      tma_prefetch(&p.tx[i]);
+      for (int l = 0; l < NMMA; ++l) tma_prefetch(&p.tw[i][l]);
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], M_EPI_WARPS);
+    }
+    mbar_init(h_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int kg = 0;
+      for (int u = blockIdx.x; u < T; u += gridDim.x) {
+        const int g = unit_pass(p, u);
+        const int m0 = (u - p.unit0[g]) * MBM;
+        for (int l = 0; l < NMMA; ++l) {
+          const int nkb = l == 0 ? p.k0 / MBK : H / MBK;
+          const int nrows = (ACTOR && l == L) ? p.nh : H;
+          const uint32_t bytes = (l == 0 ? MA_BYTES : 0) + (uint32_t)nrows * MBK * 2;
+          for (int kb = 0; kb < nkb; ++kb, ++kg) {
+            const int s = kg % NS;
+            mbar_wait(&empty[s], ((uint32_t)(kg / NS) & 1u) ^ 1u);
+            uint8_t* sA = smem + s * STAGE;
+            mbar_expect_tx(&full[s], bytes);
+            if (l == 0) tma_load_2d(sA, &p.tx[g], &full[s], kb * MBK, m0);
+            tma_load_2d(sA + MA_BYTES, &p.tw[g][l], &full[s], kb * MBK, 0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int kg = 0, ui = 0, hcnt = 0;
+      constexpr uint32_t IDESC_H = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(H >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
+      const uint32_t IDESC_HEAD = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.nh >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
+      const uint32_t sH = smem_u32(Hs);
+      for (int u = blockIdx.x; u < T; u += gridDim.x, ++ui) {
+        const int b = ui & 1;
+        mbar_wait(&acc_empty[b], (((uint32_t)ui >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)b * BUF;
+        for (int l = 0; l < NMMA; ++l) {
+          if (l > 0) {  // H holds this unit's layer l-1 output
+            mbar_wait(h_full, (uint32_t)hcnt & 1u);
+            ++hcnt;
+            tc_fence_after();
+          }
+          const int nkb = l == 0 ? p.k0 / MBK : H / MBK;
+          const uint32_t idesc = (ACTOR && l == L) ? IDESC_HEAD : IDESC_H;
+          for (int kb = 0; kb < nkb; ++kb, ++kg) {
+            const int s = kg % NS;
+            mbar_wait(&full[s], (uint32_t)(kg / NS) & 1u);
+            tc_fence_after();
+            const uint32_t sA = smem_u32(smem + s * STAGE);
+            const uint32_t aBase = l == 0 ? sA : sH + kb * 16384;
+#pragma unroll
+            for (int kk = 0; kk < MBK / 16; ++kk)
+              umma_bf16(acc, desc_kmajor(aBase, kk), desc_kmajor(sA + MA_BYTES, kk), idesc, (kb | kk) != 0 ? 1u : 0u);
+            umma_commit(&empty[s]);
+          }
+          umma_commit(&acc_full[b]);  // layer l complete
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue
+    const int e = warp - 2;
+    const int q = warp & 3;
+    const int hh = e >> 2;
+    const int c_lo = hh * CPW;      // first 16-column chunk of this warp
+    const int r = q * 32 + lane;    // tile row of this thread
+    float* bias_s = bias_w[e];
+    float* dot_s = dotw_w[e];
+    int ui = 0, dot_tiles = 0;
+    uint32_t acnt[2] = {0u, 0u};    // acc_full commits consumed per buffer
+    for (int u = blockIdx.x; u < T; u += gridDim.x, ++ui) {
+      const int g = unit_pass(p, u);
+      const MlpDev& d = p.d[g];
+      const int m0 = (u - p.unit0[g]) * MBM;
+      const int m = m0 + r;
+      const int b = ui & 1;
+      const uint32_t trow = tmem + (uint32_t)b * BUF + ((uint32_t)(q * 32) << 16);
+      for (int l = 0; l < NMMA; ++l) {
+        const bool head = ACTOR && l == L;
+        const bool last_hidden = !ACTOR && l == L - 1;
+        const bool has_dot = last_hidden && d.dot_out != nullptr;
+        // this warp's bias slice (and row-dot weights) of layer l; previous reads ordered by the
+        // __syncwarp / barriers that end every layer
+        if (!head) {
+#pragma unroll
+          for (int c = lane; c < SLICE; c += 32) {
+            bias_s[c] = d.bias[l][c_lo * 16 + c];
+            dot_s[c] = has_dot ? d.dot_w[c_lo * 16 + c] : 0.f;
+          }
+        } else if (hh == 0 && lane < 16) {
+          for (int c = lane; c < p.nh; c += 16) bias_s[c] = c < p.head_n ? d.bias[l][c] : 0.f;
+        }
+        __syncwarp();
+        mbar_wait(&acc_full[b], acnt[b] & 1u);
+        ++acnt[b];
+        tc_fence_after();
+        if (head) {
+          // ---- actor head: one warp per lane quarter takes the whole row
+          if (hh == 0) {
+            float hrow[32];
+            for (int c = 0; c < p.nh / 16 && c < 2; ++c) {
+              float v[16];
+              tmem_ld16(trow + c * 16, v);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
+            }
+            tc_fence_before();
+            if (m < d.rows) {
+              if (p.head_epi == EPI_SAC_HEAD) sac_head_row<__nv_bfloat16>(p.head, d.row0 + m, hrow, hrow + p.head.m);
+              else td3_head_row<__nv_bfloat16>(p.head, d.row0 + m, hrow);
+            }
+          } else {
+            tc_fence_before();
+          }
+          continue;
+        }
+        // ---- hidden layer l: H must be free of the TMA stores issued from it for layer l-1
+        if (e == 0 && lane == 0) bulk_wait_read0();
+        named_bar(1, M_EPI_WARPS * 32);
+        float dot = 0.f;
+        uint32_t mw[NB > 0 ? NB : 1];
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib) {
+          const int c = c_lo + ib * 2;  // first chunk of this 32-column block
+          float v[2][16];
+          tmem_ld32(trow + c * 16, v[0], v[1]);
+          uint32_t word = 0u;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float pre = v[cc][j] + bias_s[(ib * 2 + cc) * 16 + j];
+              word |= gt0_mask(pre) & (1u << (16 * cc + j));
+              v[cc][j] = fmaxf(pre, 0.f);
+              dot = fmaf(v[cc][j], dot_s[(ib * 2 + cc) * 16 + j], dot);
+            }
+          mw[ib] = word;
+          // 32 columns = four 16-byte units of row r in slab (c * 16) / 64 (128B swizzle)
+          uint8_t* rowp = Hs + ((c * 16) / 64) * 16384 + r * 128;
+          const int u0 = ((c * 16) % 64) / 8;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int cc = k >> 1, j0 = (k & 1) * 8;
+            const uint4 pk = make_uint4(pack_bf16(v[cc][j0], v[cc][j0 + 1]), pack_bf16(v[cc][j0 + 2], v[cc][j0 + 3]),
+                                        pack_bf16(v[cc][j0 + 4], v[cc][j0 + 5]), pack_bf16(v[cc][j0 + 6], v[cc][j0 + 7]));
+            *reinterpret_cast<uint4*>(rowp + (((u0 + k) ^ (r & 7)) << 4)) = pk;
+          }
+        }
+        tc_fence_before();   // TMEM reads of this layer done
+        fence_async_smem();  // H writes -> async proxy (MMA, TMA store)
+        named_bar(1, M_EPI_WARPS * 32);
+        if (e == 0 && lane == 0) {
+          if (l + 1 < NMMA) mbar_arrive(h_full);
+          if (d.store[l]) {
+#pragma unroll
+            for (int sl = 0; sl < SLABS; ++sl) tma_store_2d(&p.tact[g][l], Hs + sl * 16384, sl * 64, m0);
+            bulk_commit();
+          }
+        }
+        if (d.mask[l] != nullptr && m < d.rows) {
+          uint32_t* dst = d.mask[l] + (int64_t)m * p.mask_ld + (c_lo * 16) / 32;
+          if constexpr (NB == 4) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(mw[0], mw[1 % NB], mw[2 % NB], mw[3 % NB]);
+          } else if constexpr (NB == 2) {
+            *reinterpret_cast<uint2*>(dst) = make_uint2(mw[0], mw[1 % NB]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NB; ++i) dst[i] = mw[i];
+          }
+        }
+        if (has_dot) {
+          // the two warps of this lane quarter combine their slices in a fixed order
+          const int pb = dot_tiles & 1;
+          dotpart[pb][hh][r] = dot;
+          named_bar(2 + q, 64);
+          if (hh == 0 && m < d.rows) d.dot_out[m] = (dotpart[pb][0][r] + dotpart[pb][1][r]) + d.dot_b[0];
+          ++dot_tiles;
+        }
+      }
+      // accumulator buffer b drained by this warp
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
+    }
+  }
+  if (warp >= 2 && lane == 0) bulk_wait_all();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+template <int H, bool ACTOR>
+cudaError_t launch_mlp(MlpParams& p, cudaStream_t st) {
+  constexpr int STAGE = MA_BYTES + H * MBK * 2;
+  constexpr int EXTRA = 1024 /* align */ + (H / 64) * 16384 /* H */ + 1024 /* barriers */;
+  constexpr int MAX_ST = std::min(MSTAGES, (227 * 1024 - EXTRA - 16 * 1024 /* static */) / STAGE);
+  static_assert(MAX_ST >= 2, "shared memory budget");
+  auto kern = tc_mlp_kernel<H, ACTOR>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_ST * STAGE + EXTRA);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  p.stages = MAX_ST;
+  const int grid = std::min(p.total_units, num_sms());
+  if (grid == 0) return cudaSuccess;
+  return launch_pdl(kern, dim3(grid), dim3(M_NTHREADS), (size_t)(MAX_ST * STAGE + EXTRA), st, p);
+}
+
+// bf16 [rows x inner] map with a 64 x box_rows box, 128-byte swizzle (load or store)
+bool map_rows(CUtensorMap* m, const void* ptr, int inner, int rows, int ld, int box_rows) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld % 8)) return false;
+  return make_map(m, ptr, (uint64_t)inner, (uint64_t)rows, (uint64_t)ld, 64, (uint32_t)box_rows);
+}
+
+}  // namespace
+
+bool tc_mlp_supported(const MlpArgs& a) {
+  if (!get_encode()) return false;
+  if (a.n_pass < 1 || a.n_pass > MLP_MAXN || a.L < 1 || a.L > MLP_MAXL) return false;
+  if (a.h != 64 && a.h != 128 && a.h != 256) return false;
+  if (a.k0 < 64 || a.k0 % 64 || a.k0 > 256) return false;
+  if (a.head_n > 32 || (a.head_n == 0 && a.mask_ld * 32 < a.h)) return false;
+  if (a.mask_ld % 4) return false;
+  for (int i = 0; i < a.n_pass; ++i) {
+    const MlpPass& s = a.p[i];
+    if ((reinterpret_cast<uintptr_t>(s.X) & 15) || s.ldx % 8) return false;
+    for (int l = 0; l <= a.L; ++l)
+      if (l < a.L || a.head_n > 0)
+        if ((reinterpret_cast<uintptr_t>(s.W[l]) & 15) || s.ldw[l] % 8) return false;
+    for (int l = 0; l < a.L; ++l)
+      if (s.mask[l] && (reinterpret_cast<uintptr_t>(s.mask[l]) & 15)) return false;
+    if (a.head_n == 0 && !s.dot_out) return false;
+  }
+  return true;
+}
+
+cudaError_t tc_mlp_fwd(const MlpArgs& a, cudaStream_t st) {
+  MlpParams p;
+  std::memset(&p, 0, sizeof(p));
+  const bool actor = a.head_n > 0;
+  p.n_pass = a.n_pass;
+  p.L = a.L;
+  p.n_mma = actor ? a.L + 1 : a.L;
+  p.k0 = a.k0;
+  p.head_n = a.head_n;
+  p.nh = actor ? (a.head_n + 15) / 16 * 16 : 16;
+  p.head_epi = a.head_epi;
+  p.mask_ld = a.mask_ld;
+  p.head = a.head;
+  int T = 0;
+  for (int i = 0; i < a.n_pass; ++i) {
+    const MlpPass& s = a.p[i];
+    MlpDev& d = p.d[i];
+    p.unit0[i] = T;
+    T += (int)cdiv(s.rows, MBM);
+    d.rows = s.rows;
+    d.row0 = s.row0;
+    d.dot_w = s.dot_w;
+    d.dot_b = s.dot_b;
+    d.dot_out = s.dot_out;
+    if (s.rows < 1) continue;
+    if (!map_rows(&p.tx[i], s.X, a.k0, s.rows, s.ldx, MBM)) return cudaErrorInvalidValue;
+    for (int l = 0; l < p.n_mma; ++l) {
+      const int in = l == 0 ? a.k0 : a.h;
+      const int out = (actor && l == a.L) ? a.head_n : a.h;
+      const int box = (actor && l == a.L) ? p.nh : a.h;
+      if (!map_rows(&p.tw[i][l], s.W[l], in, out, s.ldw[l], box)) return cudaErrorInvalidValue;
+    }
+    for (int l = 0; l <= a.L; ++l) d.bias[l] = s.bias[l];
+    for (int l = 0; l < a.L; ++l) {
+      d.mask[l] = s.mask[l];
+      d.store[l] = s.act != nullptr && s.act[l] != nullptr;
+      if (d.store[l] && !map_rows(&p.tact[i][l], s.act[l], a.h, s.rows, a.h, MBM)) return cudaErrorInvalidValue;
+    }
+  }
+  p.unit0[a.n_pass] = T;
+  p.total_units = T;
+  if (T == 0) return cudaSuccess;
+  switch (a.h) {
+    case 64: return actor ? launch_mlp<64, true>(p, st) : launch_mlp<64, false>(p, st);
+    case 128: return actor ? launch_mlp<128, true>(p, st) : launch_mlp<128, false>(p, st);
+    default: return actor ? launch_mlp<256, true>(p, st) : launch_mlp<256, false>(p, st);
+  }
+}
+
+}  // namespace spz

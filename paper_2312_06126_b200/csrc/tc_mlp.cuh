@@ -1,0 +1,50 @@
+// tc_mlp.cuh -- fused multi-layer forward of the actor / critic MLPs on the tensor cores (sm_100a).
+//
+// One launch runs every hidden layer (and the actor's head layer) of up to MLP_MAXN network passes.
+// A unit is (pass, 128-row block).  Layer 0 reads its input rows by TMA; every hidden layer's
+// epilogue (bias + ReLU) writes its bf16 output into a shared-memory buffer in exactly the
+// 128-byte-swizzled K-major layout the next layer's tcgen05.mma consumes, so hidden activations
+// never make a round trip through L2 between layers.  Activations and packed ReLU masks go to HBM
+// only for the passes whose backward needs them (TMA bulk stores straight from that buffer).
+// Heads: critic -> N = 1 row dot fused into the last hidden epilogue; actor -> an N = 16k MMA on the
+// last hidden buffer followed by the SAC / TD3 head epilogue (heads.cuh).
+#pragma once
+
+#include "gemm.cuh"
+
+namespace spz {
+
+constexpr int MLP_MAXN = 6;  // passes per launch
+constexpr int MLP_MAXL = 4;  // hidden layers
+
+struct MlpPass {
+  const void* X;  // input rows [rows x k0] (bf16, pitch ldx)
+  int ldx;
+  int rows;
+  int row0;  // actor head: local actor-pass row of this pass's row 0
+  const void* W[MLP_MAXL + 1];  // bf16 weight shadows [out x in], pitch ldw
+  int ldw[MLP_MAXL + 1];
+  const float* bias[MLP_MAXL + 1];
+  void* act[MLP_MAXL];        // bf16 hidden outputs [rows x h] (pitch h), or null (not stored)
+  uint32_t* mask[MLP_MAXL];   // packed ReLU masks [rows x mask_ld] u32, or null
+  const float* dot_w;         // critic head: q[m] = sum_n relu(z[m, n]) dot_w[n] + dot_b[0]
+  const float* dot_b;
+  float* dot_out;
+};
+
+struct MlpArgs {
+  int n_pass;
+  int L;       // hidden layers
+  int h;       // hidden width (64, 128 or 256)
+  int k0;      // input width (multiple of 64; zero-padded columns)
+  int head_n;  // actor head width (2m SAC, m TD3); 0 = critic (row-dot head)
+  int head_epi;  // EPI_SAC_HEAD / EPI_TD3_HEAD (actor)
+  int mask_ld;
+  HeadEpi head;
+  MlpPass p[MLP_MAXN];
+};
+
+bool tc_mlp_supported(const MlpArgs& a);
+cudaError_t tc_mlp_fwd(const MlpArgs& a, cudaStream_t st);
+
+}  // namespace spz

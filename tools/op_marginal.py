@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synthdata  # noqa: E402
 from paper_2312_06126_b200 import spz  # noqa: E402
 
-CLASSES = ["gather", "actor_fwd_gemm", "actor_head_gemm", "critic_fwd_gemm", "critic_loss", "critic_dgrad_gemm",
+CLASSES = ["gather", "actor_fwd_mlp", "critic_fwd_mlp", "actor_fwd_gemm", "actor_head_gemm", "critic_fwd_gemm", "critic_loss", "critic_dgrad_gemm",
            "critic_input_dgrad_gemm", "actor_head_bwd", "actor_dgrad_gemm", "wgrad_gemm", "adam_polyak"]
 
 

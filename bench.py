@@ -88,6 +88,10 @@ def class_flops(w, B):
     add("wgrad_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))  # critics ...
     add("actor_dgrad_gemm", 2 * B * aout * h + (L - 1) * 2 * B * h * h)
     add("wgrad_gemm", 2 * B * h * o + (L - 1) * 2 * B * h * h + 2 * B * aout * h)  # ... and the actor, one launch
+    add("wgrad_gemm", 2 * 2 * B * h)  # critic-head weight gradients (g_q as a one-row operand)
+    # fused multi-layer forwards (h <= 256): every hidden layer (+ the actor head) in one launch
+    f["actor_fwd_mlp"] = f["actor_fwd_gemm"] + f["actor_head_gemm"]
+    f["critic_fwd_mlp"] = f["critic_fwd_gemm"]
     return f
 
 
@@ -282,7 +286,7 @@ def main():
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm"], "unit": "GB/s", "frac": ach / pk["hbm"],
                 "traffic": None, "peak_src": f"{pk['src']} hbm"}
     gemm_t = sum(t for k, t in prof.items() if k in fl)
-    gemm_f = sum(fl.values())
+    gemm_f = sum(v for k, v in fl.items() if not k.endswith("_mlp"))  # the fused classes repeat per-layer work
     roof["step_gemm_tflops"] = gemm_f / (ms_per_step * 1e-3) / 1e12
     roof["step_frac_of_bf16_sustained"] = roof["step_gemm_tflops"] / pk["bf16_sust"]
     roof["gemm_share_of_step"] = gemm_t / sum(prof.values())

@@ -227,7 +227,10 @@ void spz_learner_destroy(spz_learner* L);
 /* ------------------------------------------------------------------ diagnostics
  * spz_diag_tc_trace: enable (on = 1) / disable per-tile %globaltimer stamps in the tcgen05 GEMM
  * (160 CTAs x 8 tiles x 4 events: producer start, MMA issued, accumulator ready, epilogue done) and,
- * if host_out != NULL, copy up to n stamps of the last traced launch.  Synchronous. */
+ * if host_out != NULL, copy up to n stamps of the last traced launch.  on = k >= 2 traces only the
+ * (k-2)-th launch from now.  on >= 100 addresses the fused MLP forward instead (mode on - 100;
+ * 160 CTAs x 4 units x 3 layers x 4 events: MMA start, MMA issued, accumulator ready, epilogue
+ * done).  Synchronous. */
 spz_status spz_diag_tc_trace(int32_t device, int32_t on, uint64_t* host_out, int32_t n);
 
 /* The dense-layer GEMM of the update on its own, for kernel tests: on `device`,

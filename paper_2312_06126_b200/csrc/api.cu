@@ -4,6 +4,7 @@
 
 #include "internal.h"
 #include "tc_gemm.cuh"
+#include "tc_mlp.cuh"
 
 namespace spz {
 
@@ -82,7 +83,9 @@ spz_status spz_diag_tc_trace(int32_t device, int32_t on, uint64_t* host_out, int
   if (st != SPZ_OK) return st;
   spz::DeviceGuard dg(device);
   cudaError_t e = cudaDeviceSynchronize();
-  if (e == cudaSuccess) e = spz::tc_trace(on, reinterpret_cast<unsigned long long*>(host_out), n);
+  if (e == cudaSuccess)
+    e = on >= 100 ? spz::mlp_trace(on - 100, reinterpret_cast<unsigned long long*>(host_out), n)
+                  : spz::tc_trace(on, reinterpret_cast<unsigned long long*>(host_out), n);
   if (e != cudaSuccess) return spz::fail(SPZ_ECUDA, std::string("spz_diag_tc_trace: ") + cudaGetErrorString(e));
   return SPZ_OK;
 }

@@ -27,15 +27,16 @@ struct HeadEpi {
 
 // SAC: [mu | l] -> lc = clamp(l), sigma = exp(lc), u = mu + sigma eps, a = tanh u,
 // log pi = sum_i [-eps^2/2 - lc - ln(2 pi)/2 - 2 (ln 2 - u - softplus(-2u))].
+// Actions [i0, i1) of row r; returns their part of log pi (the caller sums the parts in order).
 template <typename T>
-__device__ __forceinline__ void sac_head_row(const HeadEpi& h, int r, const float* mu, const float* lraw) {
+__device__ __forceinline__ float sac_head_part(const HeadEpi& h, int r, const float* mu, const float* lraw, int i0, int i1) {
   const bool s2row = r < h.Bl;
   const int j = s2row ? r : r - h.Bl;
   const uint64_t step = (uint64_t)*h.step_p;
   const uint32_t stream = s2row ? S_EPS2 : S_EPS;
   T* xa = static_cast<T*>(h.Xc) + (int64_t)(s2row ? 2 * h.Bl + j : h.Bl + j) * h.ldx + h.o;
   float lp = 0.f;
-  for (int i = 0; i < h.m; ++i) {
+  for (int i = i0; i < i1; ++i) {
     const float l = lraw[i];
     const float lc = fminf(fmaxf(l, h.lo), h.hi);
     const float sg = expf(lc);
@@ -53,18 +54,25 @@ __device__ __forceinline__ void sac_head_row(const HeadEpi& h, int r, const floa
       h.l[ci] = l;
     }
   }
-  if (s2row) h.logp2[j] = lp;
-  else h.logp[j] = lp;
+  return lp;
+}
+__device__ __forceinline__ void sac_head_logp(const HeadEpi& h, int r, float lp) {
+  if (r < h.Bl) h.logp2[r] = lp;
+  else h.logp[r - h.Bl] = lp;
+}
+template <typename T>
+__device__ __forceinline__ void sac_head_row(const HeadEpi& h, int r, const float* mu, const float* lraw) {
+  sac_head_logp(h, r, sac_head_part<T>(h, r, mu, lraw, 0, h.m));
 }
 
 // TD3: rows r < Bl (target actor on s2): a' = clip(tanh z + clip(noise n, -c, c), -1, 1), n from
-// S_SMOOTH; rows r >= Bl (online actor on s): a~ = tanh z (cached for the backward).
+// S_SMOOTH; rows r >= Bl (online actor on s): a~ = tanh z (cached for the backward).  Actions [i0, i1).
 template <typename T>
-__device__ __forceinline__ void td3_head_row(const HeadEpi& h, int r, const float* z) {
+__device__ __forceinline__ void td3_head_part(const HeadEpi& h, int r, const float* z, int i0, int i1) {
   const uint64_t step = (uint64_t)*h.step_p;
   if (r < h.Bl) {
     T* xa = static_cast<T*>(h.Xc) + (int64_t)(2 * h.Bl + r) * h.ldx + h.o;
-    for (int i = 0; i < h.m; ++i) {
+    for (int i = i0; i < i1; ++i) {
       const float n = normal_q(h.seed, step, S_SMOOTH, (uint64_t)(h.row0 + r), i);
       const float xi = fminf(fmaxf(h.noise * n, -h.clipc), h.clipc);
       xa[i] = from_f<T>(fminf(fmaxf(tanhf(z[i]) + xi, -1.f), 1.f));
@@ -72,12 +80,16 @@ __device__ __forceinline__ void td3_head_row(const HeadEpi& h, int r, const floa
   } else {
     const int j = r - h.Bl;
     T* xa = static_cast<T*>(h.Xc) + (int64_t)(h.Bl + j) * h.ldx + h.o;
-    for (int i = 0; i < h.m; ++i) {
+    for (int i = i0; i < i1; ++i) {
       const float a = tanhf(z[i]);
       xa[i] = from_f<T>(a);
       h.a[(int64_t)j * h.m + i] = a;
     }
   }
+}
+template <typename T>
+__device__ __forceinline__ void td3_head_row(const HeadEpi& h, int r, const float* z) {
+  td3_head_part<T>(h, r, z, 0, h.m);
 }
 
 }  // namespace spz

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "tc_common.cuh"
 
@@ -37,8 +38,21 @@ struct MlpDev {
   float* dot_out;
 };
 
+// Diagnostics (spz_diag_tc_trace, modes >= 100): %globaltimer stamps per (CTA, unit, layer):
+// 0 MMA starts the layer, 1 MMA issue done, 2 epilogue sees the accumulator, 3 epilogue done,
+// 4 first weight slab of the layer present, 5 last weight slab present.
+constexpr int MT_CTAS = 160, MT_UNITS = 4, MT_LAYERS = 3, MT_EV = 6;
+__device__ unsigned long long g_mtrace[MT_CTAS * MT_UNITS * MT_LAYERS * MT_EV];
+__device__ __forceinline__ void mtrace(int on, int ui, int l, int ev) {
+  if (on && blockIdx.x < MT_CTAS && ui < MT_UNITS && l < MT_LAYERS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_mtrace[((blockIdx.x * MT_UNITS + ui) * MT_LAYERS + l) * MT_EV + ev] = t;
+  }
+}
+
 struct MlpParams {
-  int n_pass, L, n_mma, k0, nh, head_n, head_epi, mask_ld, stages;
+  int n_pass, L, n_mma, k0, nh, head_n, head_epi, mask_ld, stages, trace;
   int total_units;
   int unit0[MLP_MAXN + 1];
   HeadEpi head;
@@ -56,6 +70,56 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
+
+// relu(lo), relu(hi) -> packed bf16x2 (RNE) in one instruction
+__device__ __forceinline__ uint32_t pack_relu_bf16(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
+// Hidden-layer epilogue of one warp: NB blocks of 32 accumulator columns of row r -> bias + ReLU ->
+// bf16 into H (128B swizzle); MASK: packed ReLU-mask words (pre-activation > 0); DOT: row dot of the
+// fp32 ReLU outputs with dot_s.
+template <int NB, bool MASK, bool DOT>
+__device__ __forceinline__ float hidden_epi(uint32_t trow, int c_lo, int r, uint8_t* Hs, const float* __restrict__ bias_s,
+                                            const float* __restrict__ dot_s, uint32_t (&mw)[NB > 0 ? NB : 1]) {
+  float dot = 0.f;
+#pragma unroll
+  for (int ib = 0; ib < NB; ++ib) {
+    const int c = c_lo + ib * 2;  // first chunk of this 32-column block
+    float v[2][16];
+    tmem_ld32(trow + c * 16, v[0], v[1]);
+    uint32_t word = 0u;
+    uint32_t pk[16];
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const int bi = (ib * 2 + cc) * 16 + j;
+        const float p0 = v[cc][j] + bias_s[bi], p1 = v[cc][j + 1] + bias_s[bi + 1];
+        if constexpr (MASK) {
+          word |= gt0_mask(p0) & (1u << (16 * cc + j));
+          word |= gt0_mask(p1) & (1u << (16 * cc + j + 1));
+        }
+        if constexpr (DOT) {
+          dot = fmaf(fmaxf(p0, 0.f), dot_s[bi], dot);
+          dot = fmaf(fmaxf(p1, 0.f), dot_s[bi + 1], dot);
+        }
+        pk[cc * 8 + j / 2] = pack_relu_bf16(p0, p1);
+      }
+    if constexpr (MASK) mw[ib] = word;
+    // 32 columns = four 16-byte units of row r in slab (c * 16) / 64 (128B swizzle)
+    uint8_t* rowp = Hs + ((c * 16) / 64) * 16384 + r * 128;
+    const int u0 = ((c * 16) % 64) / 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<uint4*>(rowp + (((u0 + k) ^ (r & 7)) << 4)) =
+          make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+  }
+  return dot;
+}
+
 __device__ __forceinline__ int unit_pass(const MlpParams& p, int u) {
   int g = 0;
   while (g + 1 < p.n_pass && u >= p.unit0[g + 1]) ++g;
@@ -66,7 +130,7 @@ __device__ __forceinline__ int unit_pass(const MlpParams& p, int u) {
 // row-dot head fused into the last hidden layer's epilogue).
 template <int H, bool ACTOR>
 __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_constant__ MlpParams p) {
-  constexpr int STAGE = MA_BYTES + H * MBK * 2;  // input tile + weight slab (largest layer)
+  constexpr int STAGE = H * MBK * 2;  // one weight slab (largest layer) per ring stage
   constexpr uint32_t BUF = H < 32 ? 32 : H;      // TMEM columns per accumulator buffer
   constexpr uint32_t TMEM_COLS = 2 * BUF <= 64 ? 64 : 2 * BUF <= 128 ? 128 : 2 * BUF <= 256 ? 256 : 512;
   constexpr int SLABS = H / 64;                  // 64-column slabs of H (16 KB each)
@@ -80,13 +144,16 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NS = p.stages;
-  uint8_t* Hs = smem + NS * STAGE;  // hidden buffer: SLABS x [128 rows x 128 B]
+  uint8_t* Xs = smem + NS * STAGE;                  // layer-0 input tile: k0/64 x [128 rows x 128 B]
+  uint8_t* Hs = Xs + (p.k0 / MBK) * MA_BYTES;       // hidden buffer: SLABS x [128 rows x 128 B]
   uint64_t* full = reinterpret_cast<uint64_t*>(Hs + SLABS * 16384);
   uint64_t* empty = full + MSTAGES;
   uint64_t* acc_full = empty + MSTAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* h_full = acc_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_full + 1);
+  uint64_t* x_full = h_full + 1;
+  uint64_t* x_empty = x_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = p.total_units;
@@ -106,6 +173,8 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
       mbar_init(&acc_empty[b], M_EPI_WARPS);
     }
     mbar_init(h_full, 1);
+    mbar_init(x_full, 1);
+    mbar_init(x_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -123,22 +192,26 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
-      int kg = 0;
-      for (int u = blockIdx.x; u < T; u += gridDim.x) {
+      // ---------------- TMA producer: the input tile of each unit into Xs (freed by the MMA after
+      //                  layer 0), every layer's weight slabs through the stage ring
+      int kg = 0, ui = 0;
+      for (int u = blockIdx.x; u < T; u += gridDim.x, ++ui) {
         const int g = unit_pass(p, u);
         const int m0 = (u - p.unit0[g]) * MBM;
+        const int nx = p.k0 / MBK;
         for (int l = 0; l < NMMA; ++l) {
-          const int nkb = l == 0 ? p.k0 / MBK : H / MBK;
+          if (l == 0) {
+            mbar_wait(x_empty, ((uint32_t)ui & 1u) ^ 1u);
+            mbar_expect_tx(x_full, (uint32_t)nx * MA_BYTES);
+            for (int kb = 0; kb < nx; ++kb) tma_load_2d(Xs + kb * MA_BYTES, &p.tx[g], x_full, kb * MBK, m0);
+          }
+          const int nkb = l == 0 ? nx : H / MBK;
           const int nrows = (ACTOR && l == L) ? p.nh : H;
-          const uint32_t bytes = (l == 0 ? MA_BYTES : 0) + (uint32_t)nrows * MBK * 2;
           for (int kb = 0; kb < nkb; ++kb, ++kg) {
             const int s = kg % NS;
             mbar_wait(&empty[s], ((uint32_t)(kg / NS) & 1u) ^ 1u);
-            uint8_t* sA = smem + s * STAGE;
-            mbar_expect_tx(&full[s], bytes);
-            if (l == 0) tma_load_2d(sA, &p.tx[g], &full[s], kb * MBK, m0);
-            tma_load_2d(sA + MA_BYTES, &p.tw[g][l], &full[s], kb * MBK, 0);
+            mbar_expect_tx(&full[s], (uint32_t)nrows * MBK * 2);
+            tma_load_2d(smem + s * STAGE, &p.tw[g][l], &full[s], kb * MBK, 0);
           }
         }
       }
@@ -149,7 +222,7 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
       int kg = 0, ui = 0, hcnt = 0;
       constexpr uint32_t IDESC_H = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(H >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
       const uint32_t IDESC_HEAD = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.nh >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
-      const uint32_t sH = smem_u32(Hs);
+      const uint32_t sH = smem_u32(Hs), sX = smem_u32(Xs);
       for (int u = blockIdx.x; u < T; u += gridDim.x, ++ui) {
         const int b = ui & 1;
         mbar_wait(&acc_empty[b], (((uint32_t)ui >> 1) & 1u) ^ 1u);
@@ -161,20 +234,29 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
             ++hcnt;
             tc_fence_after();
           }
+          mtrace(p.trace, ui, l, 0);
           const int nkb = l == 0 ? p.k0 / MBK : H / MBK;
           const uint32_t idesc = (ACTOR && l == L) ? IDESC_HEAD : IDESC_H;
+          if (l == 0) {
+            mbar_wait(x_full, (uint32_t)ui & 1u);
+            tc_fence_after();
+          }
           for (int kb = 0; kb < nkb; ++kb, ++kg) {
             const int s = kg % NS;
             mbar_wait(&full[s], (uint32_t)(kg / NS) & 1u);
             tc_fence_after();
-            const uint32_t sA = smem_u32(smem + s * STAGE);
-            const uint32_t aBase = l == 0 ? sA : sH + kb * 16384;
+            if (kb == 0) mtrace(p.trace, ui, l, 4);
+            if (kb == nkb - 1) mtrace(p.trace, ui, l, 5);
+            const uint32_t sB = smem_u32(smem + s * STAGE);
+            const uint32_t aBase = l == 0 ? sX + kb * MA_BYTES : sH + kb * 16384;
 #pragma unroll
             for (int kk = 0; kk < MBK / 16; ++kk)
-              umma_bf16(acc, desc_kmajor(aBase, kk), desc_kmajor(sA + MA_BYTES, kk), idesc, (kb | kk) != 0 ? 1u : 0u);
+              umma_bf16(acc, desc_kmajor(aBase, kk), desc_kmajor(sB, kk), idesc, (kb | kk) != 0 ? 1u : 0u);
             umma_commit(&empty[s]);
           }
+          if (l == 0) umma_commit(x_empty);  // input tile consumed
           umma_commit(&acc_full[b]);  // layer l complete
+          mtrace(p.trace, ui, l, 1);
         }
       }
     }
@@ -208,69 +290,60 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
             bias_s[c] = d.bias[l][c_lo * 16 + c];
             dot_s[c] = has_dot ? d.dot_w[c_lo * 16 + c] : 0.f;
           }
-        } else if (hh == 0 && lane < 16) {
+        } else if (lane < 16) {
           for (int c = lane; c < p.nh; c += 16) bias_s[c] = c < p.head_n ? d.bias[l][c] : 0.f;
         }
         __syncwarp();
         mbar_wait(&acc_full[b], acnt[b] & 1u);
         ++acnt[b];
         tc_fence_after();
+        if (e == 0 && lane == 0) mtrace(p.trace, ui, l, 2);
         if (head) {
-          // ---- actor head: one warp per lane quarter takes the whole row
-          if (hh == 0) {
-            float hrow[32];
-            for (int c = 0; c < p.nh / 16 && c < 2; ++c) {
-              float v[16];
-              tmem_ld16(trow + c * 16, v);
+          // ---- actor head: the two warps of a lane quarter take the row's actions [0, m/2) and
+          //      [m/2, m); SAC log pi = part 0 + part 1 (fixed order)
+          float hrow[32];
+          for (int c = 0; c < p.nh / 16 && c < 2; ++c) {
+            float v[16];
+            tmem_ld16(trow + c * 16, v);
 #pragma unroll
-              for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
-            }
-            tc_fence_before();
-            if (m < d.rows) {
-              if (p.head_epi == EPI_SAC_HEAD) sac_head_row<__nv_bfloat16>(p.head, d.row0 + m, hrow, hrow + p.head.m);
-              else td3_head_row<__nv_bfloat16>(p.head, d.row0 + m, hrow);
-            }
-          } else {
-            tc_fence_before();
+            for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
           }
+          tc_fence_before();
+          const int mh = p.head.m, half = (mh + 1) / 2;
+          const int i0 = hh ? half : 0, i1 = hh ? mh : half;
+          const bool live = m < d.rows;
+          if (p.head_epi == EPI_SAC_HEAD) {
+            const float lp = live ? sac_head_part<__nv_bfloat16>(p.head, d.row0 + m, hrow, hrow + mh, i0, i1) : 0.f;
+            const int pb = dot_tiles & 1;
+            dotpart[pb][hh][r] = lp;
+            named_bar(2 + q, 64);
+            if (hh == 0 && live) sac_head_logp(p.head, d.row0 + m, dotpart[pb][0][r] + dotpart[pb][1][r]);
+            ++dot_tiles;
+          } else if (live) {
+            td3_head_part<__nv_bfloat16>(p.head, d.row0 + m, hrow, i0, i1);
+          }
+          __syncwarp();
+          if (e == 0 && lane == 0) mtrace(p.trace, ui, l, 3);
           continue;
         }
         // ---- hidden layer l: H must be free of the TMA stores issued from it for layer l-1
         if (e == 0 && lane == 0) bulk_wait_read0();
         named_bar(1, M_EPI_WARPS * 32);
-        float dot = 0.f;
         uint32_t mw[NB > 0 ? NB : 1];
-#pragma unroll
-        for (int ib = 0; ib < NB; ++ib) {
-          const int c = c_lo + ib * 2;  // first chunk of this 32-column block
-          float v[2][16];
-          tmem_ld32(trow + c * 16, v[0], v[1]);
-          uint32_t word = 0u;
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const float pre = v[cc][j] + bias_s[(ib * 2 + cc) * 16 + j];
-              word |= gt0_mask(pre) & (1u << (16 * cc + j));
-              v[cc][j] = fmaxf(pre, 0.f);
-              dot = fmaf(v[cc][j], dot_s[(ib * 2 + cc) * 16 + j], dot);
-            }
-          mw[ib] = word;
-          // 32 columns = four 16-byte units of row r in slab (c * 16) / 64 (128B swizzle)
-          uint8_t* rowp = Hs + ((c * 16) / 64) * 16384 + r * 128;
-          const int u0 = ((c * 16) % 64) / 8;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int cc = k >> 1, j0 = (k & 1) * 8;
-            const uint4 pk = make_uint4(pack_bf16(v[cc][j0], v[cc][j0 + 1]), pack_bf16(v[cc][j0 + 2], v[cc][j0 + 3]),
-                                        pack_bf16(v[cc][j0 + 4], v[cc][j0 + 5]), pack_bf16(v[cc][j0 + 6], v[cc][j0 + 7]));
-            *reinterpret_cast<uint4*>(rowp + (((u0 + k) ^ (r & 7)) << 4)) = pk;
-          }
+        const bool want_mask = d.mask[l] != nullptr;
+        float dot;
+        if (has_dot) {
+          dot = want_mask ? hidden_epi<NB, true, true>(trow, c_lo, r, Hs, bias_s, dot_s, mw)
+                          : hidden_epi<NB, false, true>(trow, c_lo, r, Hs, bias_s, dot_s, mw);
+        } else {
+          dot = want_mask ? hidden_epi<NB, true, false>(trow, c_lo, r, Hs, bias_s, dot_s, mw)
+                          : hidden_epi<NB, false, false>(trow, c_lo, r, Hs, bias_s, dot_s, mw);
         }
         tc_fence_before();   // TMEM reads of this layer done
         fence_async_smem();  // H writes -> async proxy (MMA, TMA store)
         named_bar(1, M_EPI_WARPS * 32);
         if (e == 0 && lane == 0) {
+          mtrace(p.trace, ui, l, 3);
           if (l + 1 < NMMA) mbar_arrive(h_full);
           if (d.store[l]) {
 #pragma unroll
@@ -312,23 +385,32 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
   }
 }
 
+int g_mtrace_mode = 0;
+long g_mtrace_count = 0;
+
 template <int H, bool ACTOR>
 cudaError_t launch_mlp(MlpParams& p, cudaStream_t st) {
-  constexpr int STAGE = MA_BYTES + H * MBK * 2;
-  constexpr int EXTRA = 1024 /* align */ + (H / 64) * 16384 /* H */ + 1024 /* barriers */;
-  constexpr int MAX_ST = std::min(MSTAGES, (227 * 1024 - EXTRA - 16 * 1024 /* static */) / STAGE);
-  static_assert(MAX_ST >= 2, "shared memory budget");
+  constexpr int STAGE = H * MBK * 2;
+  // dynamic: alignment slack + weight ring + input tile + H + barriers; static (bias / dot slices,
+  // dot partials) <= 12 KB
+  const int xbytes = (p.k0 / MBK) * MA_BYTES;
+  const int fixed = 1024 + xbytes + (H / 64) * 16384 + 1024;
+  const int ns = std::min(MSTAGES, (227 * 1024 - 12 * 1024 - fixed) / STAGE);
+  if (ns < 2) return cudaErrorInvalidValue;
+  constexpr int SMEM_ATTR = 227 * 1024 - 12 * 1024;
   auto kern = tc_mlp_kernel<H, ACTOR>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_ST * STAGE + EXTRA);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  p.stages = MAX_ST;
+  p.stages = ns;
+  p.trace = g_mtrace_mode == 1 || (g_mtrace_mode >= 2 && g_mtrace_count == g_mtrace_mode - 2);
+  ++g_mtrace_count;
   const int grid = std::min(p.total_units, num_sms());
   if (grid == 0) return cudaSuccess;
-  return launch_pdl(kern, dim3(grid), dim3(M_NTHREADS), (size_t)(MAX_ST * STAGE + EXTRA), st, p);
+  return launch_pdl(kern, dim3(grid), dim3(M_NTHREADS), (size_t)(ns * STAGE + fixed), st, p);
 }
 
 // bf16 [rows x inner] map with a 64 x box_rows box, 128-byte swizzle (load or store)
@@ -338,6 +420,19 @@ bool map_rows(CUtensorMap* m, const void* ptr, int inner, int rows, int ld, int 
 }
 
 }  // namespace
+
+cudaError_t mlp_trace(int on, unsigned long long* out, int n) {
+  g_mtrace_mode = on;
+  g_mtrace_count = 0;
+  cudaError_t e = cudaSuccess;
+  if (on) {
+    static std::vector<unsigned long long> zeros(MT_CTAS * MT_UNITS * MT_LAYERS * MT_EV, 0ull);
+    e = cudaMemcpyToSymbol(g_mtrace, zeros.data(), zeros.size() * sizeof(unsigned long long));
+  }
+  if (e != cudaSuccess || !out) return e;
+  n = std::min(n, MT_CTAS * MT_UNITS * MT_LAYERS * MT_EV);
+  return cudaMemcpyFromSymbol(out, g_mtrace, n * sizeof(unsigned long long));
+}
 
 bool tc_mlp_supported(const MlpArgs& a) {
   if (!get_encode()) return false;

@@ -46,5 +46,7 @@ struct MlpArgs {
 
 bool tc_mlp_supported(const MlpArgs& a);
 cudaError_t tc_mlp_fwd(const MlpArgs& a, cudaStream_t st);
+// Diagnostics: per-(CTA, unit, layer) timestamps of the fused kernel (see tc_mlp.cu).
+cudaError_t mlp_trace(int on, unsigned long long* out, int n);
 
 }  // namespace spz

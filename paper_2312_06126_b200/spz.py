@@ -283,6 +283,15 @@ def spz_diag_tc_trace(on, read=False, device=0):
     return out.reshape(160, 8, 4) if read else None
 
 
+def spz_diag_mlp_trace(on, read=False, device=0):
+    """Fused-MLP timestamps (spz_diag_tc_trace modes >= 100); with read=True: uint64 [160, 4, 3, 6]
+    = (CTA, unit, layer, event: MMA start, MMA issued, epilogue sees accumulator, epilogue done,
+    first / last weight slab present)."""
+    out = np.zeros(160 * 4 * 3 * 6, np.uint64) if read else None
+    _check(lib().spz_diag_tc_trace(device, 100 + int(on), _ptr(out) if read else None, out.size if read else 0))
+    return out.reshape(160, 4, 3, 6) if read else None
+
+
 def spz_split_exchange(critic_learner, actor_learner):
     _check(lib().spz_split_exchange(critic_learner, actor_learner))
 

@@ -205,6 +205,8 @@ struct LossArgs {
   double* totals;
   int64_t* ctr_snap;  // the step's counters (step, t_c, t_a, t_al) as read before the optimizer advances them
   float* la_snap;     // the step's log alpha (statistics), likewise
+  float* bc_snap;     // Adam bias corrections 1 - beta^t of the three optimizers: [bc1 x 3 | bc2 x 3]
+  float beta1, beta2;
   unsigned* ticket;
   const void* A[2];          // last hidden activations (mask source when mask[] is null)
   const uint32_t* mask[2];   // packed ReLU masks of the last hidden layer (tcgen05 path)
@@ -426,6 +428,13 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
     if (threadIdx.x == 0) *a.ticket = 0u;
     if (threadIdx.x < 4) a.ctr_snap[threadIdx.x] = a.step_p[threadIdx.x];
     if (threadIdx.x == 4) *a.la_snap = *a.log_alpha;
+    if (threadIdx.x >= 8 && threadIdx.x < 14) {
+      // 1 - beta^t = -expm1(t log1p(beta - 1)) without cancellation, t = the optimizer's next step
+      const int k = threadIdx.x - 8, o = k % 3;
+      const double beta = k < 3 ? (double)a.beta1 : (double)a.beta2;
+      const double t = (double)(a.step_p[1 + o] + 1);
+      a.bc_snap[k] = (float)(-expm1(t * log1p(beta - 1.0)));
+    }
   }
 }
 
@@ -571,27 +580,34 @@ struct AdamTensor {
   int32_t pad_;
 };
 
-// Split-K partial sum of element i of tensor tn (fixed split order; loads issued 16 at a time).
-__device__ __forceinline__ float partial_sum(const AdamTensor& tn, int64_t i64) {
-  const int i = (int)i64;  // tensors hold < 2^31 elements
+// Split-K partial sum of element i of tensor tn (fixed split order; 32-bit offsets, 4 loads in flight).
+__device__ __forceinline__ float partial_sum(const float* __restrict__ partials, int n_partials, int pstride, int pld,
+                                             int cols, int i) {
   int idx;
-  if (tn.cols > 0) {
-    const int row = i / tn.cols;
-    idx = row * tn.pld + (i - row * tn.cols);
+  if (cols > 0) {
+    const int row = i / cols;
+    idx = row * pld + (i - row * cols);
   } else {
-    idx = i * tn.pld;
+    idx = i * pld;
   }
-  const float* src = tn.partials + idx;
+  const float* src = partials + idx;
   float g = 0.f;
-  for (int s0 = 0; s0 < tn.n_partials; s0 += 16) {
-    float t[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) t[j] = s0 + j < tn.n_partials ? __ldg(src + (int64_t)(s0 + j) * tn.pstride) : 0.f;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) g += t[j];
+  int s = 0;
+  for (; s + 4 <= n_partials; s += 4) {
+    const float t0 = __ldg(src + s * pstride), t1 = __ldg(src + (s + 1) * pstride);
+    const float t2 = __ldg(src + (s + 2) * pstride), t3 = __ldg(src + (s + 3) * pstride);
+    g += t0;
+    g += t1;
+    g += t2;
+    g += t3;
   }
+  for (; s < n_partials; ++s) g += __ldg(src + s * pstride);
   return g;
 }
+__device__ __forceinline__ float partial_sum(const AdamTensor& tn, int64_t i) {
+  return partial_sum(tn.partials, tn.n_partials, (int)tn.pstride, tn.pld, tn.cols, (int)i);
+}
+
 struct AdamSegment {
   AdamTensor t;       // the tensor (embedded: one dependent load per segment)
   int64_t start;      // element index within the tensor
@@ -608,6 +624,7 @@ struct AdamHyper {
   StatsOut* stats;
   double target_entropy, B;
   const int64_t* snap;  // counters of this step (written by the loss kernel); the kernel advances `counters`
+  const float* bc;      // bias corrections of this step (loss-kernel snapshot): [bc1 x 3 | bc2 x 3]
   int alpha_auto, critic_on, actor_on;
 };
 
@@ -626,45 +643,49 @@ __global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegme
   pdl_wait();
   pdl_launch();
   __shared__ bool skip;
-  const AdamTensor tn = segs[blockIdx.x].t;
-  const int64_t start = segs[blockIdx.x].start;
-  const int count = segs[blockIdx.x].count;
-  const int64_t step = hp.snap[0];
-  const int64_t topt = hp.snap[1 + tn.opt];
+  const AdamSegment* sg = segs + blockIdx.x;
+  const int opt = __ldg(&sg->t.opt);
+  const int count = __ldg(&sg->count);
+  const int start = (int)__ldg(&sg->start);
+  const int p_off = (int)__ldg(&sg->t.p_off);
+  const int t_off = (int)__ldg(&sg->t.t_off);
+  const float* partials = reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(&sg->t.partials)));
+  const int n_partials = __ldg(&sg->t.n_partials), pld = __ldg(&sg->t.pld), cols = __ldg(&sg->t.cols);
+  const int pstride = (int)__ldg(&sg->t.pstride);
+  const int64_t step = __ldg(hp.snap);
   const double* tot = hp.totals;
+  const float bc1 = __ldg(hp.bc + opt), bc2 = __ldg(hp.bc + 3 + opt);
   float g[ADAM_EPT], m0[ADAM_EPT], v0[ADAM_EPT], p0[ADAM_EPT], tp0[ADAM_EPT];
 #pragma unroll
   for (int u = 0; u < ADAM_EPT; ++u) {
     const int k = threadIdx.x + u * ADAM_NT;
     g[u] = m0[u] = v0[u] = p0[u] = tp0[u] = 0.f;
     if (k < count) {
-      const int64_t i = start + k, pi = tn.p_off + i;
+      const int i = start + k, pi = p_off + i;
       m0[u] = Mo[pi];
       v0[u] = Vo[pi];
       p0[u] = P[pi];
-      if (tn.t_off >= 0) tp0[u] = P[tn.t_off + i];
-      g[u] = tn.opt == 2 ? (float)(-(tot[4] / hp.B + hp.target_entropy))  // log-alpha gradient
-                         : partial_sum(tn, i);
+      if (t_off >= 0) tp0[u] = P[t_off + i];
+      g[u] = opt == 2 ? (float)(-(tot[4] / hp.B + hp.target_entropy))  // log-alpha gradient
+                      : partial_sum(partials, n_partials, pstride, pld, cols, i);
     }
   }
-  // bias corrections 1 - beta^t without cancellation (computed while the loads are in flight)
-  const double t = (double)(topt + 1);
-  const float bc1 = (float)(-expm1(t * log1p((double)hp.beta1 - 1.0)));
-  const float bc2 = (float)(-expm1(t * log1p((double)hp.beta2 - 1.0)));
   bool delayed = true;
   if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
-  bool bad = false;
   if (threadIdx.x == 0) {
     // the step's losses are finite iff their totals are (B > 0); TD3 has no log-prob total
-    bad = !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) || (!hp.td3 && !isfinite(tot[4]));
+    const bool bad =
+        !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) || (!hp.td3 && !isfinite(tot[4]));
     const int f = *flag;
     if (bad && blockIdx.x == 0) atomicExch(flag, 1);
     skip = bad || f;  // halted: parameters stay at the state before the failing step
   }
   __syncthreads();
-  const bool active = !skip && !(hp.td3 && tn.opt == 1 && !delayed);  // TD3 actor: delayed steps only
+  const bool active = !skip && !(hp.td3 && opt == 1 && !delayed);  // TD3 actor: delayed steps only
   if (active) {
-    const float lr = hp.lr[tn.opt];
+    const float lr = hp.lr[opt];
+    const int s_off = (int)__ldg(&sg->t.s_off), ts_off = (int)__ldg(&sg->t.ts_off), ld = __ldg(&sg->t.ld);
+    const bool polyak = t_off >= 0 && (!hp.td3 || delayed);
 #pragma unroll
     for (int u = 0; u < ADAM_EPT; ++u) {
       const int k = threadIdx.x + u * ADAM_NT;
@@ -673,7 +694,7 @@ __global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegme
         atomicExch(flag, 2);
         continue;
       }
-      const int64_t i = start + k, pi = tn.p_off + i;
+      const int i = start + k, pi = p_off + i;
       const float m = hp.beta1 * m0[u] + (1.f - hp.beta1) * g[u];
       const float v = hp.beta2 * v0[u] + (1.f - hp.beta2) * g[u] * g[u];
       Mo[pi] = m;
@@ -681,29 +702,42 @@ __global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegme
       const float p = p0[u] - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
       P[pi] = p;
       int so = -1;
-      if (tn.cols > 0) {
-        const int ii = (int)i;
-        const int row = ii / tn.cols, col = ii - row * tn.cols;
-        so = row * tn.ld + col;
-        S[tn.s_off + so] = from_f<T>(p);
+      if (cols > 0) {
+        const int row = i / cols, col = i - row * cols;
+        so = row * ld + col;
+        S[s_off + so] = from_f<T>(p);
       }
-      if (tn.t_off >= 0 && (!hp.td3 || delayed)) {  // Polyak
+      if (polyak) {
         const float tp = hp.tau * p + (1.f - hp.tau) * tp0[u];
-        P[tn.t_off + i] = tp;
-        if (so >= 0) S[tn.ts_off + so] = from_f<T>(tp);
+        P[t_off + i] = tp;
+        if (so >= 0) S[ts_off + so] = from_f<T>(tp);
       }
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    StatsOut o;
-    float ga;
-    step_stats(tot, (double)*hp.log_alpha, hp.target_entropy, hp.B, hp.td3, step, &o, &ga);
-    *hp.stats = o;
-    if (!skip) {
-      counters[1] = hp.snap[1] + (hp.critic_on ? 1 : 0);
-      counters[2] = hp.snap[2] + (hp.actor_on && delayed ? 1 : 0);
-      counters[3] = hp.snap[3] + (hp.actor_on && hp.alpha_auto && !hp.td3 ? 1 : 0);
-      counters[0] = step + 1;
+  // block 0: statistics (one field per thread) and the counter advance
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const double B = hp.B;
+    const double la = (double)*hp.log_alpha;
+    const double lpm = hp.td3 ? 0.0 : tot[4] / B;
+    double* o = reinterpret_cast<double*>(hp.stats);
+    switch (threadIdx.x) {
+      case 0: o[0] = (double)(step + 1); break;
+      case 1: o[1] = tot[0] / B; break;
+      case 2: o[2] = tot[3] / B; break;
+      case 3: o[3] = hp.td3 ? 0.0 : exp(la); break;
+      case 4: o[4] = hp.td3 ? 0.0 : -la * (lpm + hp.target_entropy); break;
+      case 5: o[5] = tot[1] / B; break;
+      case 6: o[6] = tot[2] / B; break;
+      case 7: o[7] = lpm; break;
+      case 8:
+        if (!skip) {
+          counters[1] = hp.snap[1] + (hp.critic_on ? 1 : 0);
+          counters[2] = hp.snap[2] + (hp.actor_on && delayed ? 1 : 0);
+          counters[3] = hp.snap[3] + (hp.actor_on && hp.alpha_auto && !hp.td3 ? 1 : 0);
+          counters[0] = step + 1;
+        }
+        break;
+      default: break;
     }
   }
 }

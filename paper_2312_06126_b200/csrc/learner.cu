@@ -606,6 +606,9 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       la.ticket = Lr->tickets;
       la.ctr_snap = Lr->ctr_snap;
       la.la_snap = reinterpret_cast<float*>(Lr->ctr_snap + 4);
+      la.bc_snap = reinterpret_cast<float*>(Lr->ctr_snap + 5);
+      la.beta1 = (float)Lr->cfg.beta1;
+      la.beta2 = (float)Lr->cfg.beta2;
       la.mask_ld = mw;
       for (int i = 0; i < 2; ++i) {
         la.mask[i] = bits ? Lr->mask_c[i][L - 1] : nullptr;
@@ -888,6 +891,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       hp.target_entropy = Lr->cfg.target_entropy;
       hp.B = (double)B;
       hp.snap = Lr->ctr_snap;
+      hp.bc = reinterpret_cast<const float*>(Lr->ctr_snap + 5);
       hp.alpha_auto = Lr->cfg.alpha_auto;
       hp.critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
       hp.actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC;
@@ -1207,7 +1211,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->G, Lr->G_total * sizeof(float)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->statsum, 8 * sizeof(double)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->tickets, 8 * sizeof(unsigned)));
-  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->ctr_snap, 8 * sizeof(int64_t)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->ctr_snap, 16 * sizeof(int64_t)));
   Lr->debug.push_back({"statsum", Lr->statsum, 8 * sizeof(double), 8});
   if (Lr->gsize > 1 || cfg->comm_mode == 2) {
     int64_t tot = 0;

@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synthdata  # noqa: E402
 from paper_2312_06126_b200 import spz  # noqa: E402
 
-CLASSES = ["gather", "actor_fwd_mlp", "critic_fwd_mlp", "actor_fwd_gemm", "actor_head_gemm", "critic_fwd_gemm", "critic_loss", "critic_dgrad_gemm",
+CLASSES = ["gather", "actor_fwd_mlp", "critic_fwd_mlp", "critic_loss", "critic_dgrad_gemm",
            "critic_input_dgrad_gemm", "actor_head_bwd", "actor_dgrad_gemm", "wgrad_gemm", "adam_polyak"]
 
 
@@ -21,7 +21,10 @@ def per_update_ms(ring, skip, B=8192, K=300, reps=3):
     else:
         os.environ.pop("SPZ_DIAG_SKIP_OPS", None)
     lrn = spz.Learner(ring, precision="bf16", hidden=256, n_hidden=2, max_batch=B)
-    lrn.update(B, 20)
+    try:
+        lrn.update(B, 20)
+    except spz.SpzError:  # e.g. without critic_loss Adam has no bias-correction snapshot
+        return float("nan")
     best = 1e9
     for _ in range(reps):
         t = time.perf_counter()

@@ -754,6 +754,13 @@ __global__ void __launch_bounds__(ADAM_NT) reduce_partials_kernel(const AdamSegm
   }
 }
 
+// Diagnostics: an empty kernel in the PDL chain (SPZ_DIAG_NOOP_OPS) to measure the cost of one
+// kernel boundary inside the graph replay.
+__global__ void noop_kernel(int) {
+  pdl_wait();
+  pdl_launch();
+}
+
 // ------------------------------------------------------------------ shadow refresh + init
 struct ShadowEntry {
   int64_t p_off;  // master offset of W

@@ -927,6 +927,14 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
                      }, 1});
     }
   }
+  // diagnostics only: SPZ_DIAG_NOOP_OPS=k appends k empty PDL kernels to the step (kernel-boundary cost)
+  if (const char* nn = std::getenv("SPZ_DIAG_NOOP_OPS")) {
+    const int k = std::atoi(nn);
+    for (auto& v : Lr->ops)
+      if (!v.empty())
+        for (int i = 0; i < k; ++i)
+          v.push_back({"noop", [](cudaStream_t st) { return launch_pdl(noop_kernel, dim3(148), dim3(128), 0, st, 0); }});
+  }
   // diagnostics only (results are wrong): SPZ_DIAG_SKIP_OPS="cls1,cls2" drops those op classes so a
   // timing run shows their marginal cost inside the graph replay
   if (const char* skip = std::getenv("SPZ_DIAG_SKIP_OPS")) {

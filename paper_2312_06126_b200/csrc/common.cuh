@@ -73,6 +73,8 @@ __host__ __device__ __forceinline__ int64_t round_up(int64_t x, int64_t a) { ret
 __host__ __device__ __forceinline__ int64_t cdiv(int64_t x, int64_t a) { return (x + a - 1) / a; }
 
 // ------------------------------------------------------------------ reductions
+constexpr int NSTAT = 6;  // per-block partial sums: (q1-y)^2+(q2-y)^2, q1, q2, alpha logp - minQ~ (or -Q1~), logp, spare
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

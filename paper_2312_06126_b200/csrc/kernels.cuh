@@ -12,7 +12,6 @@
 
 namespace spz {
 
-constexpr int NSTAT = 6;  // per-block partial sums: (q1-y)^2+(q2-y)^2, q1, q2, alpha logp - minQ~ (or -Q1~), logp, spare
 
 // ------------------------------------------------------------------ a1 + a2: index + gather
 // Block = 32 rows.  Records are read with 128-bit loads into shared memory; each

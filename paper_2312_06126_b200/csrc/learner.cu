@@ -489,7 +489,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     // online-critic rows [on0, on0 + Mon): loss rows [0, Bl) on the critic side, actor rows [Bl, 2Bl)
     const int on0 = do_critic ? 0 : Bl;
     const int Mon = (do_critic ? Bl : 0) + (do_actor ? Bl : 0);
-    bool cfused = false;
+    bool cfused = false, lfused = false;  // fused critic forward / fused critic loss
     if (bits && (do_critic || do_actor)) {
       // fused multi-layer critic forward: online loss rows (activations + masks stored), online
       // actor rows (masks only: no critic weight gradient over them), target rows (nothing stored)
@@ -523,8 +523,65 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           q.dot_out = (kind == 2 ? Lr->q_tg[i] : Lr->q_on[i]) + ar;
         }
       }
+      // optionally (SPZ_FUSE_CRITIC_LOSS=1) the Bellman target, losses, g_q, statistics and
+      // critic-head backward run in the same launch: loss rows as one group (q1, q2, q1', q2' per
+      // row block), actor rows as another (q1, q2).  Parity-tested, but off by default: at WLK the
+      // serial 4-pass groups (one per CTA) cost more than the separate critic_loss kernel
+      // (118.2 vs 114.7 us/update) because a unit's layer-1 weight delivery dominates its time.
+      const char* fl = std::getenv("SPZ_FUSE_CRITIC_LOSS");
+      if (fl && std::atoi(fl) == 1) {
+        int idx[3][2], n = 0;
+        for (int kind = 0; kind < 3; ++kind)
+          for (int i = 0; i < 2; ++i) {
+            const bool present = kind == 1 ? do_actor : do_critic;
+            idx[kind][i] = present ? n++ : -1;
+          }
+        if (do_critic) {
+          MlpGroup& gr = ma.grp[ma.n_group++];
+          gr.n = 4;
+          gr.loss = 1;
+          gr.rows = Bl;
+          gr.pass[0] = idx[0][0], gr.pass[1] = idx[0][1], gr.pass[2] = idx[2][0], gr.pass[3] = idx[2][1];
+        }
+        if (do_actor) {
+          MlpGroup& gr = ma.grp[ma.n_group++];
+          gr.n = 2;
+          gr.loss = 2;
+          gr.rows = Bl;
+          gr.pass[0] = idx[1][0], gr.pass[1] = idx[1][1];
+        }
+        MlpLoss& ls = ma.loss;
+        ls.r = Lr->r;
+        ls.d = Lr->d;
+        ls.logp2 = Lr->logp2;
+        ls.logp = Lr->logp;
+        ls.log_alpha = P + Lr->p_log_alpha;
+        ls.step_p = Lr->counters;
+        for (int i = 0; i < 2; ++i) {
+          ls.w[i] = P + Lr->pbase[NET_Q1 + i] + cn.w[L];
+          ls.dZ[i] = Lr->dZc[i][L - 1];
+          ls.gq16[i] = fuse_bias ? Lr->gq16[i] : nullptr;
+        }
+        ls.gq1 = Lr->gq[0];
+        ls.gq2 = Lr->gq[1];
+        ls.y = Lr->y;
+        ls.partials = Lr->stat_partials;
+        ls.totals = Lr->statsum;
+        ls.ctr_snap = Lr->ctr_snap;
+        ls.la_snap = reinterpret_cast<float*>(Lr->ctr_snap + 4);
+        ls.bc_snap = reinterpret_cast<float*>(Lr->ctr_snap + 5);
+        ls.ticket = Lr->tickets;
+        ls.gamma = (float)Lr->cfg.gamma;
+        ls.invB = invB;
+        ls.beta1 = (float)Lr->cfg.beta1;
+        ls.beta2 = (float)Lr->cfg.beta2;
+        ls.Bl = Bl;
+        ls.td3 = td3;
+        ls.delay = delay;
+      }
       if (tc_mlp_supported(ma)) {
         cfused = true;
+        lfused = ma.n_group > 0;
         ops.push_back({"critic_fwd_mlp", [ma](cudaStream_t st) { return tc_mlp_fwd(ma, st); }});
       }
     }
@@ -626,6 +683,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       la.actor_rows = do_actor;
       la.h = h;
       la.ld = h;
+      if (!lfused)  // (the fused critic forward with loss groups computes all of this itself)
       ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
                        return launch_pdl(critic_loss_kernel<T>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
                      }});

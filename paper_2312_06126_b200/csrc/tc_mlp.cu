@@ -15,6 +15,7 @@
 #include "tc_mlp.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -53,13 +54,18 @@ __device__ __forceinline__ void mtrace(int on, int ui, int l, int ev) {
 
 struct MlpParams {
   int n_pass, L, n_mma, k0, nh, head_n, head_epi, mask_ld, stages, trace;
-  int total_units;
-  int unit0[MLP_MAXN + 1];
+  // super-unit schedule: group kind k covers super-units [su0[k], su0[k+1]); each runs passes
+  // gpass[k][0..gn[k]) on row block (su - su0[k])
+  int n_grp, total_su, any_loss;
+  int su0[MLP_MAXN + 1];
+  int gn[MLP_MAXN], gloss[MLP_MAXN], gpass[MLP_MAXN][4];
   HeadEpi head;
+  MlpLoss loss;
   MlpDev d[MLP_MAXN];
   CUtensorMap tx[MLP_MAXN];
   CUtensorMap tw[MLP_MAXN][MLP_MAXL + 1];
   CUtensorMap tact[MLP_MAXN][MLP_MAXL];
+  CUtensorMap tdz[2][2];  // dZ_L [critic][loss rows | actor rows]
 };
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
@@ -120,10 +126,163 @@ __device__ __forceinline__ float hidden_epi(uint32_t trow, int c_lo, int r, uint
   return dot;
 }
 
-__device__ __forceinline__ int unit_pass(const MlpParams& p, int u) {
-  int g = 0;
-  while (g + 1 < p.n_pass && u >= p.unit0[g + 1]) ++g;
-  return g;
+__device__ __forceinline__ int su_kind(const MlpParams& p, int su) {
+  int k = 0;
+  while (k + 1 < p.n_grp && su >= p.su0[k + 1]) ++k;
+  return k;
+}
+
+// Fused critic loss of one super-unit (critic_loss_kernel's arithmetic): rows
+// j = m0 + r of the block.  Loss rows: y = r + gamma (1-d)(min(q'1, q'2) - alpha log pi'), g_qi =
+// 2 (q_i - y) / B; actor rows: g_qi = -w_i / B ((1,0) | (0,1) | (1/2,1/2) on a tie; TD3: q1 only,
+// delayed steps).  Then dZ_L[ci] = g_qci w_ci 1[A_L > 0] (masks of this launch's online passes),
+// written through H by TMA, and the block's statistics partial (fixed order).
+template <int H>
+__device__ __forceinline__ void loss_epilogue(const MlpParams& p, int kind, int su, int m0, int r, int hh, int e,
+                                              int lane, uint8_t* Hs, float (*qv_s)[MBM], float* dot_s,
+                                              double (*red_s)[NSTAT]) {
+  constexpr int CPW = H / 16 / 2, NB = CPW / 2, SLICE = CPW * 16;
+  const MlpLoss& a = p.loss;
+  const int lk = p.gloss[kind];
+  const int j = m0 + r;
+  const bool valid = j < a.Bl;
+  named_bar(1, M_EPI_WARPS * 32);  // every pass's q of this block is in qv_s
+  double v[NSTAT] = {0, 0, 0, 0, 0, 0};
+  float g[2] = {0.f, 0.f};
+  if (valid) {
+    if (lk == 1) {
+      const float q1 = qv_s[0][r], q2 = qv_s[1][r], qt1 = qv_s[2][r], qt2 = qv_s[3][r];
+      const float alpha = a.td3 ? 0.f : expf(*a.log_alpha);
+      const float qmin = fminf(qt1, qt2);
+      const float boot = a.td3 ? qmin : qmin - alpha * a.logp2[j];
+      const float y = a.r[j] + a.gamma * (1.f - a.d[j]) * boot;
+      const float e1 = q1 - y, e2 = q2 - y;
+      g[0] = 2.f * e1 * a.invB;
+      g[1] = 2.f * e2 * a.invB;
+      if (hh == 0) {
+        a.y[j] = y;
+        a.gq1[j] = g[0];
+        a.gq2[j] = g[1];
+        if (a.gq16[0]) {
+          a.gq16[0][(int64_t)j * 8] = __float2bfloat16_rn(g[0]);
+          a.gq16[1][(int64_t)j * 8] = __float2bfloat16_rn(g[1]);
+        }
+        v[0] = (double)e1 * e1 + (double)e2 * e2;
+        v[1] = q1;
+        v[2] = q2;
+      }
+    } else {
+      const float a1 = qv_s[0][r], a2 = qv_s[1][r];
+      if (!a.td3) {
+        const float alpha = expf(*a.log_alpha);
+        const float w1 = a1 < a2 ? 1.f : (a1 > a2 ? 0.f : 0.5f);
+        g[0] = -w1 * a.invB;
+        g[1] = -(1.f - w1) * a.invB;
+        if (hh == 0) {
+          v[3] = (double)alpha * a.logp[j] - (double)fminf(a1, a2);
+          v[4] = a.logp[j];
+        }
+      } else {
+        const bool on = ((*a.step_p + 1) % a.delay) == 0;
+        g[0] = on ? -a.invB : 0.f;
+        if (hh == 0) v[3] = on ? -(double)a1 : 0.0;
+      }
+      if (hh == 0) {
+        a.gq1[a.Bl + j] = g[0];
+        a.gq2[a.Bl + j] = g[1];
+      }
+    }
+  }
+  const int c_lo = hh * CPW;
+  for (int ci = 0; ci < 2; ++ci) {
+    // this thread's mask words of row j (stored by this same thread in pass ci's last epilogue)
+    uint32_t mw[NB > 0 ? NB : 1];
+    const MlpDev& dd = p.d[p.gpass[kind][ci]];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) mw[i] = valid ? dd.mask[p.L - 1][(int64_t)j * p.mask_ld + (c_lo * 16) / 32 + i] : 0u;
+#pragma unroll
+    for (int c = lane; c < SLICE; c += 32) dot_s[c] = a.w[ci][c_lo * 16 + c];
+    if (e == 0 && lane == 0) bulk_wait_read0();  // H free of earlier TMA stores
+    named_bar(1, M_EPI_WARPS * 32);
+    const float gq = g[ci];
+#pragma unroll
+    for (int ib = 0; ib < NB; ++ib) {
+      const int c = c_lo + ib * 2;
+      uint32_t pk[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int n = 2 * k;
+        const float z0 = (mw[ib] >> n) & 1u ? gq * dot_s[ib * 32 + n] : 0.f;
+        const float z1 = (mw[ib] >> (n + 1)) & 1u ? gq * dot_s[ib * 32 + n + 1] : 0.f;
+        pk[k] = pack_bf16(z0, z1);
+      }
+      uint8_t* rowp = Hs + ((c * 16) / 64) * 16384 + r * 128;
+      const int u0 = ((c * 16) % 64) / 8;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        *reinterpret_cast<uint4*>(rowp + (((u0 + k) ^ (r & 7)) << 4)) =
+            make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+    }
+    fence_async_smem();
+    named_bar(1, M_EPI_WARPS * 32);
+    if (e == 0 && lane == 0) {
+#pragma unroll
+      for (int sl = 0; sl < H / 64; ++sl) tma_store_2d(&p.tdz[ci][lk - 1], Hs + sl * 16384, sl * 64, m0);
+      bulk_commit();
+    }
+  }
+  // statistics partial of this block: fixed shuffle tree per warp, warps in order
+#pragma unroll
+  for (int i = 0; i < NSTAT; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NSTAT; ++i) red_s[e][i] = v[i];
+  named_bar(1, M_EPI_WARPS * 32);
+  if (e == 0 && lane == 0)
+    for (int i = 0; i < NSTAT; ++i) {
+      double t = 0.0;
+      for (int k = 0; k < M_EPI_WARPS; ++k) t += red_s[k][i];
+      a.partials[(int64_t)su * NSTAT + i] = t;
+    }
+}
+
+// After the last super-unit of every CTA: the last CTA to finish sums the statistics partials in
+// block order into the step totals and snapshots the counters, log alpha and the Adam bias
+// corrections for the optimizer (critic_loss_kernel's tail).
+__device__ __forceinline__ void loss_finish(const MlpParams& p, int e, int lane, double (*red_s)[NSTAT], bool& last) {
+  const MlpLoss& a = p.loss;
+  const int tid = e * 32 + lane;
+  if (tid == 0) {
+    fence_acq_rel_gpu();  // this thread wrote every partial of this CTA
+    last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  }
+  named_bar(1, M_EPI_WARPS * 32);
+  if (!last) return;
+  fence_acq_rel_gpu();
+  double t[NSTAT] = {0, 0, 0, 0, 0, 0};
+  for (int su = tid; su < p.total_su; su += M_EPI_WARPS * 32)
+#pragma unroll
+    for (int i = 0; i < NSTAT; ++i) t[i] += __ldcg(a.partials + (int64_t)su * NSTAT + i);
+#pragma unroll
+  for (int i = 0; i < NSTAT; ++i) t[i] = warp_sum(t[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NSTAT; ++i) red_s[e][i] = t[i];
+  named_bar(1, M_EPI_WARPS * 32);
+  if (tid < NSTAT) {
+    double u = 0.0;
+    for (int k = 0; k < M_EPI_WARPS; ++k) u += red_s[k][tid];
+    a.totals[tid] = u;
+  }
+  if (tid == 0) *a.ticket = 0u;
+  if (tid < 4) a.ctr_snap[tid] = a.step_p[tid];
+  if (tid == 4) *a.la_snap = *a.log_alpha;
+  if (tid >= 8 && tid < 14) {
+    const int k = tid - 8, o = k % 3;
+    const double beta = k < 3 ? (double)a.beta1 : (double)a.beta2;
+    const double tt = (double)(a.step_p[1 + o] + 1);
+    a.bc_snap[k] = (float)(-expm1(tt * log1p(beta - 1.0)));
+  }
 }
 
 // H: hidden width of this instantiation; ACTOR: the last MMA layer is the actor head (else: critic,
@@ -141,6 +300,9 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
   __shared__ __align__(16) float bias_w[M_EPI_WARPS][SLICE > 16 ? SLICE : 16];
   __shared__ __align__(16) float dotw_w[M_EPI_WARPS][SLICE];
   __shared__ float dotpart[2][2][MBM];
+  __shared__ float qv_s[4][MBM];                    // critic groups: q of each pass, per row
+  __shared__ double red_s[M_EPI_WARPS][NSTAT];      // statistics reduction
+  __shared__ bool last_s;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NS = p.stages;
@@ -156,7 +318,7 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = p.total_units;
+  const int TSU = p.total_su;
   const int L = p.L, NMMA = p.n_mma;
 
   if (warp == 0 && lane == 0) {
@@ -195,23 +357,26 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
       // ---------------- TMA producer: the input tile of each unit into Xs (freed by the MMA after
       //                  layer 0), every layer's weight slabs through the stage ring
       int kg = 0, ui = 0;
-      for (int u = blockIdx.x; u < T; u += gridDim.x, ++ui) {
-        const int g = unit_pass(p, u);
-        const int m0 = (u - p.unit0[g]) * MBM;
-        const int nx = p.k0 / MBK;
-        for (int l = 0; l < NMMA; ++l) {
-          if (l == 0) {
-            mbar_wait(x_empty, ((uint32_t)ui & 1u) ^ 1u);
-            mbar_expect_tx(x_full, (uint32_t)nx * MA_BYTES);
-            for (int kb = 0; kb < nx; ++kb) tma_load_2d(Xs + kb * MA_BYTES, &p.tx[g], x_full, kb * MBK, m0);
-          }
-          const int nkb = l == 0 ? nx : H / MBK;
-          const int nrows = (ACTOR && l == L) ? p.nh : H;
-          for (int kb = 0; kb < nkb; ++kb, ++kg) {
-            const int s = kg % NS;
-            mbar_wait(&empty[s], ((uint32_t)(kg / NS) & 1u) ^ 1u);
-            mbar_expect_tx(&full[s], (uint32_t)nrows * MBK * 2);
-            tma_load_2d(smem + s * STAGE, &p.tw[g][l], &full[s], kb * MBK, 0);
+      for (int su = blockIdx.x; su < TSU; su += gridDim.x) {
+        const int k = su_kind(p, su);
+        const int m0 = (su - p.su0[k]) * MBM;
+        for (int j = 0; j < p.gn[k]; ++j, ++ui) {
+          const int g = p.gpass[k][j];
+          const int nx = p.k0 / MBK;
+          for (int l = 0; l < NMMA; ++l) {
+            if (l == 0) {
+              mbar_wait(x_empty, ((uint32_t)ui & 1u) ^ 1u);
+              mbar_expect_tx(x_full, (uint32_t)nx * MA_BYTES);
+              for (int kb = 0; kb < nx; ++kb) tma_load_2d(Xs + kb * MA_BYTES, &p.tx[g], x_full, kb * MBK, m0);
+            }
+            const int nkb = l == 0 ? nx : H / MBK;
+            const int nrows = (ACTOR && l == L) ? p.nh : H;
+            for (int kb = 0; kb < nkb; ++kb, ++kg) {
+              const int s = kg % NS;
+              mbar_wait(&empty[s], ((uint32_t)(kg / NS) & 1u) ^ 1u);
+              mbar_expect_tx(&full[s], (uint32_t)nrows * MBK * 2);
+              tma_load_2d(smem + s * STAGE, &p.tw[g][l], &full[s], kb * MBK, 0);
+            }
           }
         }
       }
@@ -223,7 +388,8 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
       constexpr uint32_t IDESC_H = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(H >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
       const uint32_t IDESC_HEAD = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.nh >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
       const uint32_t sH = smem_u32(Hs), sX = smem_u32(Xs);
-      for (int u = blockIdx.x; u < T; u += gridDim.x, ++ui) {
+      for (int su = blockIdx.x; su < TSU; su += gridDim.x)
+      for (int j = 0; j < p.gn[su_kind(p, su)]; ++j, ++ui) {
         const int b = ui & 1;
         mbar_wait(&acc_empty[b], (((uint32_t)ui >> 1) & 1u) ^ 1u);
         tc_fence_after();
@@ -271,11 +437,13 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
     float* dot_s = dotw_w[e];
     int ui = 0, dot_tiles = 0;
     uint32_t acnt[2] = {0u, 0u};    // acc_full commits consumed per buffer
-    for (int u = blockIdx.x; u < T; u += gridDim.x, ++ui) {
-      const int g = unit_pass(p, u);
+    for (int su = blockIdx.x; su < TSU; su += gridDim.x) {
+    const int kind = su_kind(p, su);
+    const int m0 = (su - p.su0[kind]) * MBM;
+    const int m = m0 + r;
+    for (int jp = 0; jp < p.gn[kind]; ++jp, ++ui) {
+      const int g = p.gpass[kind][jp];
       const MlpDev& d = p.d[g];
-      const int m0 = (u - p.unit0[g]) * MBM;
-      const int m = m0 + r;
       const int b = ui & 1;
       const uint32_t trow = tmem + (uint32_t)b * BUF + ((uint32_t)(q * 32) << 16);
       for (int l = 0; l < NMMA; ++l) {
@@ -367,13 +535,22 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
           const int pb = dot_tiles & 1;
           dotpart[pb][hh][r] = dot;
           named_bar(2 + q, 64);
-          if (hh == 0 && m < d.rows) d.dot_out[m] = (dotpart[pb][0][r] + dotpart[pb][1][r]) + d.dot_b[0];
+          const float qv = (dotpart[pb][0][r] + dotpart[pb][1][r]) + d.dot_b[0];
+          if (hh == 0 && m < d.rows) d.dot_out[m] = qv;
+          if (hh == 0) qv_s[jp][r] = qv;
           ++dot_tiles;
         }
       }
       // accumulator buffer b drained by this warp
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
+    }
+    if constexpr (!ACTOR) {
+      if (p.gloss[kind]) loss_epilogue<H>(p, kind, su, m0, r, hh, e, lane, Hs, qv_s, dot_s, red_s);
+    }
+    }
+    if constexpr (!ACTOR) {
+      if (p.any_loss) loss_finish(p, e, lane, red_s, last_s);
     }
   }
   if (warp >= 2 && lane == 0) bulk_wait_all();
@@ -392,12 +569,12 @@ template <int H, bool ACTOR>
 cudaError_t launch_mlp(MlpParams& p, cudaStream_t st) {
   constexpr int STAGE = H * MBK * 2;
   // dynamic: alignment slack + weight ring + input tile + H + barriers; static (bias / dot slices,
-  // dot partials) <= 12 KB
+  // dot partials, q values, statistics) <= 14 KB
   const int xbytes = (p.k0 / MBK) * MA_BYTES;
   const int fixed = 1024 + xbytes + (H / 64) * 16384 + 1024;
-  const int ns = std::min(MSTAGES, (227 * 1024 - 12 * 1024 - fixed) / STAGE);
+  const int ns = std::min(MSTAGES, (227 * 1024 - 14 * 1024 - fixed) / STAGE);
   if (ns < 2) return cudaErrorInvalidValue;
-  constexpr int SMEM_ATTR = 227 * 1024 - 12 * 1024;
+  constexpr int SMEM_ATTR = 227 * 1024 - 14 * 1024;
   auto kern = tc_mlp_kernel<H, ACTOR>;
   static bool attr = false;
   if (!attr) {
@@ -408,7 +585,8 @@ cudaError_t launch_mlp(MlpParams& p, cudaStream_t st) {
   p.stages = ns;
   p.trace = g_mtrace_mode == 1 || (g_mtrace_mode >= 2 && g_mtrace_count == g_mtrace_mode - 2);
   ++g_mtrace_count;
-  const int grid = std::min(p.total_units, num_sms());
+  int grid = std::min(p.total_su, num_sms());
+  if (const char* cap = std::getenv("SPZ_DIAG_MLP_GRID")) grid = std::max(1, std::min(grid, std::atoi(cap)));  // diagnostics
   if (grid == 0) return cudaSuccess;
   return launch_pdl(kern, dim3(grid), dim3(M_NTHREADS), (size_t)(ns * STAGE + fixed), st, p);
 }
@@ -451,6 +629,18 @@ bool tc_mlp_supported(const MlpArgs& a) {
       if (s.mask[l] && (reinterpret_cast<uintptr_t>(s.mask[l]) & 15)) return false;
     if (a.head_n == 0 && !s.dot_out) return false;
   }
+  if (a.n_group < 0 || a.n_group > MLP_MAXG) return false;
+  for (int k = 0; k < a.n_group; ++k) {
+    const MlpGroup& gr = a.grp[k];
+    if (gr.n < 1 || gr.n > 4 || gr.rows < 0) return false;
+    for (int jj = 0; jj < gr.n; ++jj)
+      if (gr.pass[jj] < 0 || gr.pass[jj] >= a.n_pass || a.p[gr.pass[jj]].rows != gr.rows) return false;
+    if (gr.loss) {
+      if (a.head_n != 0 || gr.n != (gr.loss == 1 ? 4 : 2)) return false;
+      for (int ci = 0; ci < 2; ++ci)
+        if (!a.p[gr.pass[ci]].mask[a.L - 1] || (reinterpret_cast<uintptr_t>(a.loss.dZ[ci]) & 15)) return false;
+    }
+  }
   return true;
 }
 
@@ -467,12 +657,9 @@ cudaError_t tc_mlp_fwd(const MlpArgs& a, cudaStream_t st) {
   p.head_epi = a.head_epi;
   p.mask_ld = a.mask_ld;
   p.head = a.head;
-  int T = 0;
   for (int i = 0; i < a.n_pass; ++i) {
     const MlpPass& s = a.p[i];
     MlpDev& d = p.d[i];
-    p.unit0[i] = T;
-    T += (int)cdiv(s.rows, MBM);
     d.rows = s.rows;
     d.row0 = s.row0;
     d.dot_w = s.dot_w;
@@ -493,9 +680,39 @@ cudaError_t tc_mlp_fwd(const MlpArgs& a, cudaStream_t st) {
       if (d.store[l] && !map_rows(&p.tact[i][l], s.act[l], a.h, s.rows, a.h, MBM)) return cudaErrorInvalidValue;
     }
   }
-  p.unit0[a.n_pass] = T;
-  p.total_units = T;
-  if (T == 0) return cudaSuccess;
+  // super-unit schedule
+  int TSU = 0;
+  if (a.n_group == 0) {
+    p.n_grp = a.n_pass;
+    for (int i = 0; i < a.n_pass; ++i) {
+      p.su0[i] = TSU;
+      p.gn[i] = 1;
+      p.gpass[i][0] = i;
+      TSU += (int)cdiv(a.p[i].rows, MBM);
+    }
+  } else {
+    p.n_grp = a.n_group;
+    for (int k = 0; k < a.n_group; ++k) {
+      const MlpGroup& gr = a.grp[k];
+      p.su0[k] = TSU;
+      p.gn[k] = gr.n;
+      p.gloss[k] = gr.loss;
+      for (int jj = 0; jj < gr.n; ++jj) p.gpass[k][jj] = gr.pass[jj];
+      TSU += (int)cdiv(gr.rows, MBM);
+      if (gr.loss) {
+        p.any_loss = 1;
+        const int koff = gr.loss == 1 ? 0 : 1;
+        for (int ci = 0; ci < 2; ++ci) {
+          const void* base = static_cast<const __nv_bfloat16*>(a.loss.dZ[ci]) + (int64_t)koff * a.loss.Bl * a.h;
+          if (!map_rows(&p.tdz[ci][koff], base, a.h, a.loss.Bl, a.h, MBM)) return cudaErrorInvalidValue;
+        }
+      }
+    }
+  }
+  p.su0[p.n_grp] = TSU;
+  p.total_su = TSU;
+  p.loss = a.loss;
+  if (TSU == 0) return cudaSuccess;
   switch (a.h) {
     case 64: return actor ? launch_mlp<64, true>(p, st) : launch_mlp<64, false>(p, st);
     case 128: return actor ? launch_mlp<128, true>(p, st) : launch_mlp<128, false>(p, st);

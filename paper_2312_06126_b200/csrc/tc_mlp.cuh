@@ -8,6 +8,13 @@
 // only for the passes whose backward needs them (TMA bulk stores straight from that buffer).
 // Heads: critic -> N = 1 row dot fused into the last hidden epilogue; actor -> an N = 16k MMA on the
 // last hidden buffer followed by the SAC / TD3 head epilogue (heads.cuh).
+//
+// Units are processed in groups ("super-units"): the passes of a group run back to back on the same
+// 128-row block in one CTA.  A critic group may end with the fused loss epilogue (SURVEY.md §8(a)
+// a4-a6; the same arithmetic as critic_loss_kernel): Bellman target y, g_q, the loss statistics
+// partial of the block, and the critic-head backward dZ_L = g_q w_out 1[A_L > 0] for both critics,
+// written through the shared buffer by TMA.  The last CTA reduces the statistics partials in block
+// order into the step totals and snapshots the step counters for the optimizer.
 #pragma once
 
 #include "gemm.cuh"
@@ -16,6 +23,7 @@ namespace spz {
 
 constexpr int MLP_MAXN = 6;  // passes per launch
 constexpr int MLP_MAXL = 4;  // hidden layers
+constexpr int MLP_MAXG = 2;  // group kinds per launch
 
 struct MlpPass {
   const void* X;  // input rows [rows x k0] (bf16, pitch ldx)
@@ -32,6 +40,31 @@ struct MlpPass {
   float* dot_out;
 };
 
+// A group kind: passes p[pass[0..n)] run on the same row block, for every row block of rows rows.
+// loss: 0 none; 1 loss rows (passes = q1, q2, q1', q2' on [s|a] / [s2|a']); 2 actor rows
+// (passes = q1, q2 on [s|a~]).
+struct MlpGroup {
+  int n, loss, rows;
+  int pass[4];
+};
+
+struct MlpLoss {
+  const float *r, *d, *logp2, *logp, *log_alpha;
+  const int64_t* step_p;  // step counters (step, t_c, t_a, t_al)
+  const float* w[2];      // critic head weights (fp32 master)
+  void* dZ[2];            // dZ_L of each critic [2 Bl x h] bf16: loss rows 0.., actor rows Bl..
+  float *gq1, *gq2, *y;
+  __nv_bfloat16* gq16[2];  // bf16 loss-row g_q, pitch 8 (tensor-core head gradients), may be null
+  double* partials;       // [groups x NSTAT] statistics partials (one per super-unit)
+  double* totals;
+  int64_t* ctr_snap;
+  float* la_snap;
+  float* bc_snap;
+  unsigned* ticket;
+  float gamma, invB, beta1, beta2;
+  int Bl, td3, delay;
+};
+
 struct MlpArgs {
   int n_pass;
   int L;       // hidden layers
@@ -42,6 +75,10 @@ struct MlpArgs {
   int mask_ld;
   HeadEpi head;
   MlpPass p[MLP_MAXN];
+  // grouping: if n_group == 0 every pass is its own group
+  int n_group;
+  MlpGroup grp[MLP_MAXG];
+  MlpLoss loss;  // used when a group has loss != 0
 };
 
 bool tc_mlp_supported(const MlpArgs& a);

@@ -103,6 +103,16 @@ def class_bytes(w, B, n_params):
             "adam_polyak": n_params * 28 + n_params * 2 // 3 * 8}
 
 
+def traffic(workload, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full capture, or None."""
+    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    try:
+        e = json.load(open(p))[workload][kernel]
+    except (OSError, KeyError, ValueError):
+        return None
+    return e["dram_read"] + e["dram_write"]
+
+
 # ----------------------------------------------------------------------------- clocks sampler
 
 class Clocks:
@@ -285,6 +295,10 @@ def main():
         ach = by.get(dom, 0) / (prof[dom] * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm"], "unit": "GB/s", "frac": ach / pk["hbm"],
                 "traffic": None, "peak_src": f"{pk['src']} hbm"}
+    tr = traffic(w.name, roof["kernel"])
+    if tr is not None:
+        roof["traffic"] = tr
+        roof["traffic_src"] = "profiles/r01_traffic.json (ncu --set full, per launch)"
     gemm_t = sum(t for k, t in prof.items() if k in fl)
     gemm_f = sum(v for k, v in fl.items() if not k.endswith("_mlp"))  # the fused classes repeat per-layer work
     roof["step_gemm_tflops"] = gemm_f / (ms_per_step * 1e-3) / 1e12
@@ -318,9 +332,12 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        steps = a.cpu_sample_steps or (3 if w.name in ("walker",) else 1)
-        if w.name == "pendulum":
-            steps = 50
+        # bounded sample: ~15 s of oracle work (one probe update sizes it), at least one update
+        if a.cpu_sample_steps:
+            steps = a.cpu_sample_steps
+        else:
+            _, _, probe = oracle_rate(w, B, 1)
+            steps = max(1, min(2000, int(15.0 / max(probe, 1e-3))))
         rate, cores, dt = oracle_rate(w, B, steps)
         cpu = {"value": rate, "unit": "frames/s", "cores": cores, "kind": "oracle",
                "sample": f"{steps} float64 oracle updates at B={B} ({w.name}), {dt:.1f} s"}

@@ -200,6 +200,7 @@ def sac_grads(st, batch, eps, eps2, cfg, B_global, critic=True, actor=True):
             grads[f"q{i + 1}"] = mlp.flatten(g)
             lq = lq + np.sum((q - y) ** 2)
             sums[f"q{i + 1}"] = np.sum(q)
+            sums[f"q{i + 1}_abs"] = np.sum(np.abs(q))  # conditioning of the mean (test tolerance scale)
         sums["lq"] = lq
         sums["y"] = y
     if actor:
@@ -222,6 +223,7 @@ def sac_grads(st, batch, eps, eps2, cfg, B_global, critic=True, actor=True):
         if cfg.alpha_auto:
             grads["log_alpha"] = np.array([-np.sum(logpt + cfg.target_entropy) / B_global])
         sums["lpi"] = np.sum(alpha * logpt - np.minimum(qs[0], qs[1]))
+        sums["lpi_abs"] = np.sum(np.abs(alpha * logpt - np.minimum(qs[0], qs[1])))  # conditioning of the mean
         sums["logp"] = np.sum(logpt)
     return grads, sums
 
@@ -249,10 +251,13 @@ def stats_of(st, sums, B, cfg):
         step=st.step,
         critic_loss=float(sums["lq"] / B),
         actor_loss=float(sums["lpi"] / B),
+        actor_loss_abs=float(sums.get("lpi_abs", 0.0) / B),
         alpha=alpha,
         alpha_loss=float(-st.log_alpha * (sums["logp"] / B + cfg.target_entropy)),
         q1_mean=float(sums["q1"] / B),
         q2_mean=float(sums["q2"] / B),
+        q1_mean_abs=float(sums.get("q1_abs", 0.0) / B),
+        q2_mean_abs=float(sums.get("q2_abs", 0.0) / B),
         logp_mean=float(sums["logp"] / B),
     )
 

@@ -48,6 +48,7 @@ def td3_grads(st, batch, xi, cfg, B_global, step, critic=True, actor=True):
             grads[f"q{i + 1}"] = mlp.flatten(g)
             lq = lq + np.sum((q - y) ** 2)
             sums[f"q{i + 1}"] = np.sum(q)
+            sums[f"q{i + 1}_abs"] = np.sum(np.abs(q))  # conditioning of the mean (test tolerance scale)
         sums["lq"] = lq
         sums["y"] = y
     if actor and is_delayed(step, cfg):
@@ -62,6 +63,7 @@ def td3_grads(st, batch, xi, cfg, B_global, step, critic=True, actor=True):
         g, _ = mlp.backward(A, acache, dZ)
         grads["actor"] = mlp.flatten(g)
         sums["lpi"] = -np.sum(q)
+        sums["lpi_abs"] = np.sum(np.abs(q))  # conditioning of the mean (test tolerance scale)
     return grads, sums
 
 
@@ -91,8 +93,9 @@ def draw_smoothing(seed, step, batch, cfg, row0=0):
 
 def stats_of(st, sums, B):
     return dict(step=st.step, critic_loss=float(sums["lq"] / B),
-                actor_loss=float(sums.get("lpi", 0.0) / B), alpha=0.0, alpha_loss=0.0,
-                q1_mean=float(sums["q1"] / B), q2_mean=float(sums["q2"] / B), logp_mean=0.0)
+                actor_loss=float(sums.get("lpi", 0.0) / B), actor_loss_abs=float(sums.get("lpi_abs", 0.0) / B), alpha=0.0, alpha_loss=0.0,
+                q1_mean=float(sums["q1"] / B), q2_mean=float(sums["q2"] / B), logp_mean=0.0,
+                q1_mean_abs=float(sums.get("q1_abs", 0.0) / B), q2_mean_abs=float(sums.get("q2_abs", 0.0) / B))
 
 
 def td3_step(st, ring, B, seed, cfg):

@@ -39,6 +39,8 @@ struct GemmGroup {
   const float* dot_w;  // EPI_BIAS_RELU: if set, dot_out[m] = sum_n relu(z[m, n]) dot_w[n] + dot_b[0]
   const float* dot_b;
   float* dot_out;
+  int64_t dot_pstride;  // N wider than one tile: tile n0 / BN writes its partial row dot at dot_out + (n0 / BN) *
+                        // dot_pstride (tile 0 adds dot_b); the consumer sums the partials in tile order
   uint32_t* mask_out;  // EPI_BIAS_RELU: if set, bit n % 32 of mask_out[m * mask_ld + n / 32] = (z[m, n] > 0)
   int64_t split_stride;  // elements between split partials in C
   float* colsum_out;     // EPI_WGRAD_BIAS: per-split row sums of A (bias gradient partials), may be null

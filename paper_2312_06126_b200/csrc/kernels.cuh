@@ -213,7 +213,16 @@ struct LossArgs {
   void* dZ[2];
   float gamma, invB;
   int Bl, td3, delay, loss_rows, actor_rows, h, ld, mask_ld;
+  int dz_separate;        // wide layers: dZ_L is written by critic_dz_kernel (after this kernel), not here
+  int qp;                 // q partials per row (fused row dot over qp 256-column tiles), summed in tile order
+  int64_t qps_tg, qps_on;  // partial strides of the target / online q buffers
 };
+
+__device__ __forceinline__ float ld_q(const float* __restrict__ q, int64_t j, int qp, int64_t ps) {
+  float s = __ldg(q + j);
+  for (int p = 1; p < qp; ++p) s += __ldg(q + p * ps + j);
+  return s;
+}
 
 // Block = LOSS_ROWS rows, warp w owns rows w, w + 8, ... (LOSS_RPW of them).  Every lane loads the
 // row scalars (broadcast) and computes g_q itself, then writes its 8-column chunks of dZ_L; all of
@@ -245,15 +254,15 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
 #pragma unroll
   for (int i = 0; i < LOSS_RPW; ++i) {
     const int j = min(j0 + wi + 8 * i, a.Bl - 1);
-    qt1[i] = __ldg(a.qt1 + j);
-    qt2[i] = __ldg(a.qt2 + j);
-    q1[i] = __ldg(a.q1 + j);
-    q2[i] = __ldg(a.q2 + j);
+    qt1[i] = ld_q(a.qt1, j, a.qp, a.qps_tg);
+    qt2[i] = ld_q(a.qt2, j, a.qp, a.qps_tg);
+    q1[i] = ld_q(a.q1, j, a.qp, a.qps_on);
+    q2[i] = ld_q(a.q2, j, a.qp, a.qps_on);
     rw[i] = __ldg(a.r + j);
     dn[i] = __ldg(a.d + j);
     lp2[i] = a.td3 ? 0.f : __ldg(a.logp2 + j);
-    a1[i] = __ldg(a.q1 + a.Bl + j);
-    a2[i] = __ldg(a.q2 + a.Bl + j);
+    a1[i] = ld_q(a.q1, a.Bl + j, a.qp, a.qps_on);
+    a2[i] = ld_q(a.q2, a.Bl + j, a.qp, a.qps_on);
     lp[i] = a.td3 ? 0.f : __ldg(a.logp + j);
 #pragma unroll
     for (int ci = 0; ci < 2; ++ci)
@@ -371,6 +380,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
       continue;
     }
     // wide layers (h > 256): chunks c = lane, lane + 32, ... with inline mask loads
+    if (a.dz_separate) continue;
     for (int c = lane; c < hv; c += 32) {
       const int n = c * 8;
 #pragma unroll
@@ -381,11 +391,27 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
           const int64_t row = (int64_t)(kind ? a.Bl : 0) + j;
           const float gq = g[ci][kind];
           T* dZ = static_cast<T*>(a.dZ[ci]) + row * a.ld + n;
+          uint32_t mb = 0u;
+          if (bits) {
+            mb = (__ldg(a.mask[ci] + row * a.mask_ld + n / 32) >> (n & 31)) & 0xFFu;
+          } else {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const bool on = bits ? ((a.mask[ci][row * a.mask_ld + (n + k) / 32] >> ((n + k) & 31)) & 1u)
-                                 : (to_f(static_cast<const T*>(a.A[ci])[row * a.ld + n + k]) > 0.f);
-            dZ[k] = from_f<T>(on ? gq * a.w[ci][n + k] : 0.f);
+            for (int k = 0; k < 8; ++k) mb |= (to_f(static_cast<const T*>(a.A[ci])[row * a.ld + n + k]) > 0.f ? 1u : 0u) << k;
+          }
+          const float4 w0 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + n));
+          const float4 w1 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + n + 4));
+          const float wk[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+          if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+            uint4 o;
+            __nv_bfloat162* yv = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              yv[k] = __floats2bfloat162_rn((mb >> (2 * k)) & 1u ? gq * wk[2 * k] : 0.f,
+                                            (mb >> (2 * k + 1)) & 1u ? gq * wk[2 * k + 1] : 0.f);
+            *reinterpret_cast<uint4*>(dZ) = o;
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) dZ[k] = (mb >> k) & 1u ? gq * wk[k] : 0.f;
           }
         }
     }
@@ -433,6 +459,65 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
       const double beta = k < 3 ? (double)a.beta1 : (double)a.beta2;
       const double t = (double)(a.step_p[1 + o] + 1);
       a.bc_snap[k] = (float)(-expm1(t * log1p(beta - 1.0)));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a6 head backward for wide layers (h > 256)
+// dZ_L[r, n] = g_q[r] w_out[n] 1[z_L[r, n] > 0] over rows [r0, r0 + rows) of both critics; one thread per
+// (row, 8-column chunk): every load (g_q, mask byte, head weights) is independent and issued up front,
+// then one 16-byte store per critic.  Runs after critic_loss_kernel (which wrote g_q).
+struct DzArgs {
+  const float* gq[2];
+  const uint32_t* mask[2];  // packed ReLU masks (tcgen05 path), or null: sign of A
+  const void* A[2];
+  const float* w[2];
+  void* dZ[2];
+  int64_t r0, rows;
+  int hv, ld, mask_ld;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) critic_dz_kernel(const __grid_constant__ DzArgs a) {
+  pdl_wait();
+  pdl_launch();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.rows * a.hv) return;
+  const int64_t row = a.r0 + t / a.hv;
+  const int n = (int)(t % a.hv) * 8;
+  float g[2], wk[2][8];
+  uint32_t mb[2];
+#pragma unroll
+  for (int ci = 0; ci < 2; ++ci) {
+    g[ci] = __ldg(a.gq[ci] + row);
+    const float4 w0 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + n));
+    const float4 w1 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + n + 4));
+    wk[ci][0] = w0.x, wk[ci][1] = w0.y, wk[ci][2] = w0.z, wk[ci][3] = w0.w;
+    wk[ci][4] = w1.x, wk[ci][5] = w1.y, wk[ci][6] = w1.z, wk[ci][7] = w1.w;
+    if (a.mask[ci]) {
+      mb[ci] = (__ldg(a.mask[ci] + row * a.mask_ld + n / 32) >> (n & 31)) & 0xFFu;
+    } else {
+      const T* A = static_cast<const T*>(a.A[ci]) + row * a.ld + n;
+      uint32_t m = 0u;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m |= (to_f(A[k]) > 0.f ? 1u : 0u) << k;
+      mb[ci] = m;
+    }
+  }
+#pragma unroll
+  for (int ci = 0; ci < 2; ++ci) {
+    T* dZ = static_cast<T*>(a.dZ[ci]) + row * a.ld + n;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+      uint4 o;
+      __nv_bfloat162* yv = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        yv[k] = __floats2bfloat162_rn((mb[ci] >> (2 * k)) & 1u ? g[ci] * wk[ci][2 * k] : 0.f,
+                                      (mb[ci] >> (2 * k + 1)) & 1u ? g[ci] * wk[ci][2 * k + 1] : 0.f);
+      *reinterpret_cast<uint4*>(dZ) = o;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) dZ[k] = (mb[ci] >> k) & 1u ? g[ci] * wk[ci][k] : 0.f;
     }
   }
 }

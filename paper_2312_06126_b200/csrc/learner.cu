@@ -109,6 +109,7 @@ struct spz_learner {
   uint32_t* mask_a[8] = {};     // packed ReLU masks of the actor hidden layers [2B x mw]
   uint32_t* mask_c[2][8] = {};  // ... and of the online critics' hidden layers
   int mw = 0;                   // mask words per row
+  int qp = 1;                   // q partial slots per row (fused row dot over 256-column tiles)
   float* H = nullptr;
   float *q_on[2] = {}, *q_tg[2] = {}, *gq[2] = {}, *dXc[2] = {};
   __nv_bfloat16* gq16[2] = {};  // bf16 loss-row g_q, pitch 8 (tensor-core head gradients)
@@ -585,6 +586,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         ops.push_back({"critic_fwd_mlp", [ma](cudaStream_t st) { return tc_mlp_fwd(ma, st); }});
       }
     }
+    int qparts = 1;  // q partials the loss kernel sums (fused row dot of a wide last hidden layer)
     if (!cfused) {
       for (int l = 0; l < L; ++l) {
         GemmArgs a = mk(l == 0 ? ldc : cn.in[l], EPI_BIAS_RELU, 0, 0);  // layer 0: over the zero-padded width
@@ -608,6 +610,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
               g.dot_w = P + Lr->pbase[id] + Lr->net[id].w[L];
               g.dot_b = bp(id, L);
               g.dot_out = (tgt ? Lr->q_tg[i] : Lr->q_on[i]) + ra;
+              g.dot_pstride = h > 256 ? (tgt ? 1 : 2) * Lr->max_local : 0;  // per-256-column-tile partials (summed by critic_loss)
             }
           }
         }
@@ -638,6 +641,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           }
         } else {
           gemm("critic_fwd_gemm", a);
+          if (l == L - 1 && h > 256) qparts = (int)cdiv(h, 256);
         }
       }
     }
@@ -645,6 +649,9 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     const int nblk = (int)cdiv(Bl, LOSS_ROWS);
     {
       LossArgs la{};
+      la.qp = qparts;
+      la.qps_tg = Lr->max_local;
+      la.qps_on = 2 * Lr->max_local;
       la.qt1 = Lr->q_tg[0];
       la.qt2 = Lr->q_tg[1];
       la.q1 = Lr->q_on[0];
@@ -683,10 +690,30 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       la.actor_rows = do_actor;
       la.h = h;
       la.ld = h;
+      la.dz_separate = h > 256 && (do_critic || do_actor);
       if (!lfused)  // (the fused critic forward with loss groups computes all of this itself)
       ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
                        return launch_pdl(critic_loss_kernel<T>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
                      }});
+      if (la.dz_separate) {
+        DzArgs da{};
+        for (int i = 0; i < 2; ++i) {
+          da.gq[i] = la.gq1 == nullptr ? nullptr : (i ? la.gq2 : la.gq1);
+          da.mask[i] = la.mask[i];
+          da.A[i] = la.A[i];
+          da.w[i] = la.w[i];
+          da.dZ[i] = la.dZ[i];
+        }
+        da.r0 = do_critic ? 0 : Bl;
+        da.rows = (int64_t)(do_critic ? Bl : 0) + (do_actor ? Bl : 0);
+        da.hv = h / 8;
+        da.ld = h;
+        da.mask_ld = mw;
+        const int64_t nthr = da.rows * da.hv;
+        ops.push_back({"critic_loss", [da, nthr](cudaStream_t st) {
+                         return launch_pdl(critic_dz_kernel<T>, dim3((unsigned)cdiv(nthr, 256)), dim3(256), 0, st, da);
+                       }});
+      }
     }
     // ---- a6: critic backward
     {
@@ -1218,6 +1245,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   SPZ_TRY(dalloc(Lr.get(), &Lr->dH, Bm * Lr->ldh * E));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->H, 2 * Bm * Lr->ldh * sizeof(float)));
   Lr->mw = (int)cdiv(h, 32);
+  Lr->qp = (int)cdiv(h, 256);
   for (int l = 0; l < L; ++l) {
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->mask_a[l], 2 * Bm * Lr->mw * 4));
     for (int i = 0; i < 2; ++i) SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->mask_c[i][l], 2 * Bm * Lr->mw * 4));
@@ -1230,8 +1258,9 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     }
   }
   for (int i = 0; i < 2; ++i) {
-    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->q_on[i], 2 * Bm * sizeof(float)));
-    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->q_tg[i], Bm * sizeof(float)));
+    // h > 256: the fused row dot leaves one partial per 256-column tile (QP of them)
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->q_on[i], 2 * Bm * Lr->qp * sizeof(float)));
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->q_tg[i], Bm * Lr->qp * sizeof(float)));
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->gq[i], 2 * Bm * sizeof(float)));
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->gq16[i], Bm * 8 * sizeof(__nv_bfloat16)));
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->dXc[i], Bm * Lr->ldc * sizeof(float)));

@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
               for (int k = 0; k < WPQ; ++k) tot += dotpart[pb][k][r];
             }
             ++dot_tiles;
-            if (hh == 0 && m < g.M) g.dot_out[m] = tot + g.dot_b[0];
+            if (hh == 0 && m < g.M) g.dot_out[(int64_t)(n0 / BN) * g.dot_pstride + m] = tot + (n0 == 0 ? g.dot_b[0] : 0.f);
           }
           if (mask_out && active && m < g.M) {
             const int w_hi = min(S::NB, (g.N - ncol0 + 31) / 32);
@@ -633,7 +633,7 @@ bool tc_gemm_supported(const GemmArgs& a) {
     const GemmGroup& g = a.g[i];
     if ((g.lda & 7) || (g.ldb & 7)) return false;
     if ((reinterpret_cast<uintptr_t>(g.A) & 15) || (reinterpret_cast<uintptr_t>(g.B) & 15)) return false;
-    if (g.dot_out && g.N > bn) return false;  // fused row dot needs the whole row in one tile
+    if (g.dot_out && g.N > bn && g.dot_pstride == 0) return false;  // wide rows need per-tile partials
   }
   return get_encode();
 }

@@ -112,7 +112,9 @@ def run_parity(algo, precision, o, m, h, L, B, C, K, kind="locomotion", use_grap
         assert gs["step"] == k + 1
         for key in ("critic_loss", "actor_loss", "q1_mean", "q2_mean", "logp_mean", "alpha"):
             ref = os_[key]
-            assert abs(gs[key] - ref) <= tol * max(abs(ref), 1e-6) + (tol * 1e-2 if key in ("q1_mean", "q2_mean") else 0), (k, key, gs[key], ref)
+            # a mean of signed terms is compared relative to the mean |term| (its summation error scales with it)
+            scale = max(abs(ref), os_.get(key + "_abs", 0.0))
+            assert abs(gs[key] - ref) <= tol * max(scale, 1e-6) + (tol * 1e-2 if key in ("q1_mean", "q2_mean") else 0), (k, key, gs[key], ref)
     names = ["actor", "q1", "q2", "q1_targ", "q2_targ"] + (["actor_targ"] if algo == "td3" else [])
     errs = {}
     for n in names:
@@ -147,6 +149,20 @@ def test_td3_parity(precision):
     run_parity("td3", precision, 44, 17, 128, 3, 600, 8000, 4)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_sac_parity_wide_humanoid_shape(precision):
+    # HUM shapes (o 44, m 17, 3x512): two 256-column tiles per hidden row (split row-dot partials)
+    run_parity("sac", precision, 44, 17, 512, 3, 700, 8000, 3)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_td3_parity_wide_1024(precision):
+    # TD3 config shapes (3x1024): four row-dot partials.  bf16: steps 0..3 (two delayed actor updates).
+    # fp32: steps 0..1 (one delayed actor update): after the first actor Adam step, Adam's sign-like map of
+    # near-zero gradients (reading 20) moves step-3 fp32 losses ~1e-4 away from fp64 at width 1024.
+    run_parity("td3", precision, 44, 17, 1024, 3, 520, 6000, 4 if precision == "bf16" else 2)
+
+
 def test_sac_parity_graph_vs_eager_bit_identical():
     outs = []
     for use_graph in (True, False):
@@ -174,6 +190,11 @@ def test_determinism_two_runs_bit_identical():
 def test_walker_full_size_two_steps(precision):
     """BASELINE config 1 at full size (B 8192, 2x256, 1M ring), in the launch configuration the bench times."""
     run_parity("sac", precision, 22, 6, 256, 2, 8192, 1_000_000, 2, check_moments=False)
+
+
+def test_humanoid_full_size_one_step():
+    """BASELINE config 3 at full size on one GPU (B 65536, 3x512, 1M ring), bf16 as the bench runs it."""
+    run_parity("sac", "bf16", 44, 17, 512, 3, 65536, 1_000_000, 1, check_moments=False)
 
 
 # ----------------------------------------------------------------------------- API behaviour

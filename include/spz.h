@@ -243,6 +243,17 @@ spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, i
                               const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb,
                               int32_t b_mn, float* C, int64_t ldc, int32_t splits, int64_t k_per_split);
 
+/* Diagnostics (GEMM unit tests): the FP32-precision GEMM, C = A * B in fp32 with the same operand
+ * conventions as spz_diag_gemm_bf16 but fp32 operands (row pitches multiple of 4 elements, 16-byte
+ * aligned device pointers).  tensor_cores = 1 runs the 3xTF32 tcgen05 kernel (SURVEY.md §8(a) a3,
+ * §8(c) reading 15: hi = x with the low 13 mantissa bits cleared, lo = x - hi, D = hi*hi + hi*lo +
+ * lo*hi accumulated in fp32; k_per_split a multiple of 32), 0 the fp32 SIMT kernel.  Synchronous.
+ * Errors: SPZ_EINVAL (bad sizes / NULL), SPZ_EUNSUPPORTED (layout the kernel does not take),
+ * SPZ_ECUDA. */
+spz_status spz_diag_gemm_f32(int32_t device, int32_t tensor_cores, int64_t M, int64_t N, int64_t K,
+                             const float* A, int64_t lda, int32_t a_mn, const float* B, int64_t ldb,
+                             int32_t b_mn, float* C, int64_t ldc, int32_t splits, int64_t k_per_split);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,43 @@ spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, i
   return SPZ_OK;
 }
 
+spz_status spz_diag_gemm_f32(int32_t device, int32_t tensor_cores, int64_t M, int64_t N, int64_t K, const float* A,
+                             int64_t lda, int32_t a_mn, const float* B, int64_t ldb, int32_t b_mn, float* C, int64_t ldc,
+                             int32_t splits, int64_t k_per_split) {
+  spz_status st = spz::check_device(device);
+  if (st != SPZ_OK) return st;
+  if (M < 1 || N < 1 || K < 1 || !A || !B || !C || splits < 1) return spz::fail(SPZ_EINVAL, "spz_diag_gemm_f32: bad argument");
+  spz::DeviceGuard dg(device);
+  spz::GemmArgs a{};
+  a.N = (int)N;
+  a.K = (int)K;
+  a.a_mn = a_mn;
+  a.b_mn = b_mn;
+  a.epi = spz::EPI_F32;
+  a.splits = splits;
+  a.k_per_split = splits > 1 ? (int)k_per_split : (int)K;
+  a.n_groups = 1;
+  a.g[0].lda = (int)lda;
+  a.g[0].ldb = (int)ldb;
+  a.g[0].ldc = (int)ldc;
+  a.g[0].N = (int)N;
+  a.g[0].split_stride = M * ldc;
+  a.g[0].A = A;
+  a.g[0].B = B;
+  a.g[0].C = C;
+  a.g[0].M = (int)M;
+  cudaError_t e;
+  if (tensor_cores) {
+    if (!spz::tc_gemm_tf32_supported(a)) return spz::fail(SPZ_EUNSUPPORTED, "spz_diag_gemm_f32: problem not supported by the 3xTF32 kernel");
+    e = spz::tc_gemm_tf32x3(a, 0);
+  } else {
+    e = spz::gemm_simt<float>(a, 0);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return spz::fail(SPZ_ECUDA, std::string("spz_diag_gemm_f32: ") + cudaGetErrorString(e));
+  return SPZ_OK;
+}
+
 spz_status spz_diag_tc_trace(int32_t device, int32_t on, uint64_t* host_out, int32_t n) {
   spz_status st = spz::check_device(device);
   if (st != SPZ_OK) return st;

@@ -213,22 +213,27 @@ struct LossArgs {
   void* dZ[2];
   float gamma, invB;
   int Bl, td3, delay, loss_rows, actor_rows, h, ld, mask_ld;
-  int dz_separate;        // wide layers: dZ_L is written by critic_dz_kernel (after this kernel), not here
   int qp;                 // q partials per row (fused row dot over qp 256-column tiles), summed in tile order
   int64_t qps_tg, qps_on;  // partial strides of the target / online q buffers
 };
 
 __device__ __forceinline__ float ld_q(const float* __restrict__ q, int64_t j, int qp, int64_t ps) {
-  float s = __ldg(q + j);
-  for (int p = 1; p < qp; ++p) s += __ldg(q + p * ps + j);
+  // qp <= 4 (h <= 1024): predicated loads, so every row scalar's loads can issue back to back
+  float s = __ldg(q + j), t[3];
+#pragma unroll
+  for (int p = 1; p < 4; ++p) t[p - 1] = p < qp ? __ldg(q + p * ps + j) : 0.f;
+#pragma unroll
+  for (int p = 1; p < 4; ++p)
+    if (p < qp) s += t[p - 1];
   return s;
 }
 
 // Block = LOSS_ROWS rows, warp w owns rows w, w + 8, ... (LOSS_RPW of them).  Every lane loads the
-// row scalars (broadcast) and computes g_q itself, then writes its 8-column chunks of dZ_L; all of
-// a warp's loads are issued before any of its arithmetic.  Lane 0 accumulates the statistics of
-// the warp's rows in row order; the block partial sums the warps in order.
-template <typename T>
+// row scalars (broadcast) and computes g_q itself; with DZ (h <= 256: one 8-column chunk per lane) it
+// then writes its chunk of dZ_L, otherwise critic_dz_kernel does that afterwards.  All of a warp's
+// loads are issued before any of its arithmetic.  Lane 0 accumulates the statistics of the warp's
+// rows in row order; the block partial sums the warps in order.
+template <typename T, bool DZ>
 __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_constant__ LossArgs a) {
   pdl_wait();
   pdl_launch();
@@ -236,21 +241,13 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   __shared__ bool last;
   const int j0 = blockIdx.x * LOSS_ROWS;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const int hv = a.h / 8;
   const bool lr = a.loss_rows, ar = a.actor_rows;
-  const bool bits = std::is_same<T, __nv_bfloat16>::value && a.mask[0] != nullptr;
   const float alpha = a.td3 ? 0.f : expf(*a.log_alpha);
   const bool td3_on = a.td3 && ((*a.step_p + 1) % a.delay) == 0;
   // ---- loads, all issued before any use: row scalars of the warp's rows (row index clamped, so
-  //      every address is valid; rows past Bl are discarded below), mask words and head weights of
-  //      this lane's 8-column chunk (h <= 256: one chunk per lane)
+  //      every address is valid; rows past Bl are discarded below)
   float qt1[LOSS_RPW], qt2[LOSS_RPW], q1[LOSS_RPW], q2[LOSS_RPW], lp2[LOSS_RPW], rw[LOSS_RPW], dn[LOSS_RPW];
   float a1[LOSS_RPW], a2[LOSS_RPW], lp[LOSS_RPW];
-  const bool one_chunk = hv <= 32;
-  const int n0 = lane * 8;
-  const bool has_chunk = one_chunk && lane < hv;
-  const int nc = has_chunk ? n0 : 0;
-  uint32_t mk[LOSS_RPW][2][2];
 #pragma unroll
   for (int i = 0; i < LOSS_RPW; ++i) {
     const int j = min(j0 + wi + 8 * i, a.Bl - 1);
@@ -264,49 +261,40 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
     a1[i] = ld_q(a.q1, a.Bl + j, a.qp, a.qps_on);
     a2[i] = ld_q(a.q2, a.Bl + j, a.qp, a.qps_on);
     lp[i] = a.td3 ? 0.f : __ldg(a.logp + j);
-#pragma unroll
-    for (int ci = 0; ci < 2; ++ci)
-#pragma unroll
-      for (int kind = 0; kind < 2; ++kind)
-        mk[i][ci][kind] = bits ? __ldg(a.mask[ci] + ((int64_t)(kind ? a.Bl : 0) + j) * a.mask_ld + nc / 32) : 0u;
   }
+  // ---- DZ: mask bytes (bit k = column n0 + k) and head weights of this lane's chunk
+  const int n0 = lane * 8;
+  const bool has_chunk = DZ && n0 < a.h;
+  const int nc = has_chunk ? n0 : 0;
+  uint32_t mk[DZ ? LOSS_RPW : 1][2][2];
   float wv[2][8];
+  if constexpr (DZ) {
+    const bool bits = std::is_same<T, __nv_bfloat16>::value && a.mask[0] != nullptr;
 #pragma unroll
-  for (int ci = 0; ci < 2; ++ci) {
-    const float4 w0 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + nc));
-    const float4 w1 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + nc + 4));
-    wv[ci][0] = w0.x, wv[ci][1] = w0.y, wv[ci][2] = w0.z, wv[ci][3] = w0.w;
-    wv[ci][4] = w1.x, wv[ci][5] = w1.y, wv[ci][6] = w1.z, wv[ci][7] = w1.w;
-  }
-  // mask bytes of the chunk (bit k = column nc + k)
+    for (int i = 0; i < LOSS_RPW; ++i)
 #pragma unroll
-  for (int i = 0; i < LOSS_RPW; ++i)
+      for (int ci = 0; ci < 2; ++ci)
 #pragma unroll
-    for (int ci = 0; ci < 2; ++ci)
+        for (int kind = 0; kind < 2; ++kind) {
+          const int64_t row = (int64_t)(kind ? a.Bl : 0) + min(j0 + wi + 8 * i, a.Bl - 1);
+          if (bits) {
+            mk[i][ci][kind] = (__ldg(a.mask[ci] + row * a.mask_ld + nc / 32) >> (nc & 31)) & 0xFFu;
+          } else {
+            const T* A = static_cast<const T*>(a.A[ci]) + row * a.ld + nc;
+            uint32_t mb = 0u;
 #pragma unroll
-      for (int kind = 0; kind < 2; ++kind) {
-        if (bits) {
-          mk[i][ci][kind] = (mk[i][ci][kind] >> (nc & 31)) & 0xFFu;
-          continue;
-        }
-        const int64_t row = (int64_t)(kind ? a.Bl : 0) + min(j0 + wi + 8 * i, a.Bl - 1);
-        uint32_t mb = 0u;
-        if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-          const uint4 u = __ldg(reinterpret_cast<const uint4*>(static_cast<const T*>(a.A[ci]) + row * a.ld + nc));
-          const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float2 f = __bfloat1622float2(x[k]);
-            mb |= (f.x > 0.f ? 1u : 0u) << (2 * k);
-            mb |= (f.y > 0.f ? 1u : 0u) << (2 * k + 1);
+            for (int k = 0; k < 8; ++k) mb |= (to_f(__ldg(A + k)) > 0.f ? 1u : 0u) << k;
+            mk[i][ci][kind] = mb;
           }
-        } else {
-          const T* A = static_cast<const T*>(a.A[ci]) + row * a.ld + nc;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mb |= (to_f(__ldg(A + k)) > 0.f ? 1u : 0u) << k;
         }
-        mk[i][ci][kind] = mb;
-      }
+#pragma unroll
+    for (int ci = 0; ci < 2; ++ci) {
+      const float4 w0 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + nc));
+      const float4 w1 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + nc + 4));
+      wv[ci][0] = w0.x, wv[ci][1] = w0.y, wv[ci][2] = w0.z, wv[ci][3] = w0.w;
+      wv[ci][4] = w1.x, wv[ci][5] = w1.y, wv[ci][6] = w1.z, wv[ci][7] = w1.w;
+    }
+  }
   double v[NSTAT] = {0, 0, 0, 0, 0, 0};
   // ---- per row: g_q (every lane), statistics (lane 0), dZ_L chunk of this lane
 #pragma unroll
@@ -353,7 +341,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
         }
       }
     }
-    if (one_chunk) {
+    if constexpr (DZ) {
       if (!has_chunk) continue;
 #pragma unroll
       for (int ci = 0; ci < 2; ++ci)
@@ -375,43 +363,6 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
           } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) dZ[k] = (mb >> k) & 1u ? gq * wv[ci][k] : 0.f;
-          }
-        }
-      continue;
-    }
-    // wide layers (h > 256): chunks c = lane, lane + 32, ... with inline mask loads
-    if (a.dz_separate) continue;
-    for (int c = lane; c < hv; c += 32) {
-      const int n = c * 8;
-#pragma unroll
-      for (int ci = 0; ci < 2; ++ci)
-#pragma unroll
-        for (int kind = 0; kind < 2; ++kind) {
-          if (kind == 0 ? !lr : !ar) continue;
-          const int64_t row = (int64_t)(kind ? a.Bl : 0) + j;
-          const float gq = g[ci][kind];
-          T* dZ = static_cast<T*>(a.dZ[ci]) + row * a.ld + n;
-          uint32_t mb = 0u;
-          if (bits) {
-            mb = (__ldg(a.mask[ci] + row * a.mask_ld + n / 32) >> (n & 31)) & 0xFFu;
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) mb |= (to_f(static_cast<const T*>(a.A[ci])[row * a.ld + n + k]) > 0.f ? 1u : 0u) << k;
-          }
-          const float4 w0 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + n));
-          const float4 w1 = __ldg(reinterpret_cast<const float4*>(a.w[ci] + n + 4));
-          const float wk[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-          if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-            uint4 o;
-            __nv_bfloat162* yv = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              yv[k] = __floats2bfloat162_rn((mb >> (2 * k)) & 1u ? gq * wk[2 * k] : 0.f,
-                                            (mb >> (2 * k + 1)) & 1u ? gq * wk[2 * k + 1] : 0.f);
-            *reinterpret_cast<uint4*>(dZ) = o;
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) dZ[k] = (mb >> k) & 1u ? gq * wk[k] : 0.f;
           }
         }
     }

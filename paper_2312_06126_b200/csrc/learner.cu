@@ -61,10 +61,27 @@ struct Op {
   int launches = 1;  // kernels this op launches
 };
 
+// diagnostics: SPZ_DZ_SPLIT=1 writes dZ_L in critic_dz_kernel at every width
+static bool dz_split_env() {
+  const char* e = std::getenv("SPZ_DZ_SPLIT");
+  return e && e[0] == '1';
+}
+
+// diagnostics: SPZ_FP32_SIMT=1 runs the FP32 precision path on the SIMT kernel instead of 3xTF32
+static bool fp32_simt_env() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPZ_FP32_SIMT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <typename T>
 static cudaError_t run_gemm(const GemmArgs& a, cudaStream_t st) {
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
     if (tc_gemm_supported(a)) return tc_gemm_bf16(a, st);
+  } else {
+    if (!fp32_simt_env() && tc_gemm_tf32_supported(a)) return tc_gemm_tf32x3(a, st);
   }
   return gemm_simt<T>(a, st);
 }
@@ -610,7 +627,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
               g.dot_w = P + Lr->pbase[id] + Lr->net[id].w[L];
               g.dot_b = bp(id, L);
               g.dot_out = (tgt ? Lr->q_tg[i] : Lr->q_on[i]) + ra;
-              g.dot_pstride = h > 256 ? (tgt ? 1 : 2) * Lr->max_local : 0;  // per-256-column-tile partials (summed by critic_loss)
+              g.dot_pstride = (h > 256 && h <= 1024) ? (tgt ? 1 : 2) * Lr->max_local : 0;  // per-256-column-tile partials (summed by critic_loss)
             }
           }
         }
@@ -641,7 +658,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           }
         } else {
           gemm("critic_fwd_gemm", a);
-          if (l == L - 1 && h > 256) qparts = (int)cdiv(h, 256);
+          if (l == L - 1 && h > 256) qparts = (int)cdiv(h, 256);  // <= 4 (wider rows take the rowdot path)
         }
       }
     }
@@ -690,12 +707,19 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       la.actor_rows = do_actor;
       la.h = h;
       la.ld = h;
-      la.dz_separate = h > 256 && (do_critic || do_actor);
-      if (!lfused)  // (the fused critic forward with loss groups computes all of this itself)
-      ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
-                       return launch_pdl(critic_loss_kernel<T>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
-                     }});
-      if (la.dz_separate) {
+      // h <= 256: one 8-column chunk per lane, dZ_L written by the loss kernel; wider: critic_dz_kernel
+      const bool dz_sep = (h > 256 || dz_split_env()) && (do_critic || do_actor);
+      if (!lfused) {  // (the fused critic forward with loss groups computes all of this itself)
+        if (dz_sep)
+          ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
+                           return launch_pdl(critic_loss_kernel<T, false>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
+                         }});
+        else
+          ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
+                           return launch_pdl(critic_loss_kernel<T, true>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
+                         }});
+      }
+      if (dz_sep && !lfused) {
         DzArgs da{};
         for (int i = 0; i < 2; ++i) {
           da.gq[i] = la.gq1 == nullptr ? nullptr : (i ? la.gq2 : la.gq1);

@@ -13,5 +13,8 @@ bool tc_gemm_available();
 cudaError_t tc_trace(int on, unsigned long long* out, int n);
 // Launch it (bf16 operands, fp32 accumulation in TMEM, shared epilogues).
 cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st);
+// FP32 precision on the tensor cores: 3xTF32 (tc_gemm_tf32.cu); fp32 operands, fp32 epilogue kinds.
+bool tc_gemm_tf32_supported(const GemmArgs& a);
+cudaError_t tc_gemm_tf32x3(const GemmArgs& a, cudaStream_t st);
 
 }  // namespace spz

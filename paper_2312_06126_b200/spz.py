@@ -32,7 +32,7 @@ EXPORTS = [
     "spz_replay_records", "spz_replay_destroy", "spz_config_default", "spz_nccl_unique_id", "spz_learner_create",
     "spz_update", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
-    "spz_diag_gemm_bf16", "spz_split_exchange", "spz_diag_tc_trace",
+    "spz_diag_gemm_bf16", "spz_diag_gemm_f32", "spz_split_exchange", "spz_diag_tc_trace",
 ]
 
 
@@ -119,6 +119,7 @@ def lib():
             "spz_split_exchange": (ctypes.c_int, [P, P]),
             "spz_diag_tc_trace": (ctypes.c_int, [I32, I32, P, I32]),
             "spz_diag_gemm_bf16": (ctypes.c_int, [I32, I32, I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, I64]),
+            "spz_diag_gemm_f32": (ctypes.c_int, [I32, I32, I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, I64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -294,6 +295,13 @@ def spz_diag_mlp_trace(on, read=False, device=0):
 
 def spz_split_exchange(critic_learner, actor_learner):
     _check(lib().spz_split_exchange(critic_learner, actor_learner))
+
+
+def spz_diag_gemm_f32(M, N, K, A, lda, a_mn, B, ldb, b_mn, C, ldc, tensor_cores=True, splits=1, k_per_split=0,
+                      device=0):
+    """A, B, C: fp32 torch CUDA tensors (see include/spz.h); tensor_cores=True runs the 3xTF32 kernel."""
+    _check(lib().spz_diag_gemm_f32(device, 1 if tensor_cores else 0, M, N, K, _ptr(A), lda, a_mn, _ptr(B), ldb, b_mn,
+                                   _ptr(C), ldc, splits, k_per_split))
 
 
 def spz_diag_gemm_bf16(M, N, K, A, lda, a_mn, B, ldb, b_mn, C, ldc, tensor_cores=True, splits=1, k_per_split=0,

@@ -76,3 +76,65 @@ def test_simt_and_tc_agree():
     spz.spz_diag_gemm_bf16(M, N, K, A, K, 0, B, K, 0, C1, N, tensor_cores=True)
     spz.spz_diag_gemm_bf16(M, N, K, A, K, 0, B, K, 0, C2, N, tensor_cores=False)
     assert (C1 - C2).abs().max().item() < 1e-4 * C2.abs().max().item()
+
+
+# ----------------------------------------------------------------------------- 3xTF32 (FP32 precision path)
+
+def _mk32(rows, cols, ld, gen):
+    x = torch.zeros(rows, ld, dtype=torch.float32, device="cuda")
+    x[:, :cols] = torch.randn(rows, cols, generator=gen, device="cuda")
+    return x
+
+
+CASES32 = [
+    (16384, 256, 256, 0, 0), (1000, 256, 28, 0, 0), (300, 12, 256, 0, 0), (257, 512, 64, 0, 0), (130, 33, 100, 0, 0),
+    (128, 1, 256, 0, 0), (2048, 1024, 1024, 0, 0),
+    (16384, 256, 256, 0, 1), (1000, 28, 256, 0, 1), (777, 256, 12, 0, 1), (200, 300, 96, 0, 1),
+    (256, 256, 8192, 1, 1), (256, 28, 1000, 1, 1), (12, 256, 1000, 1, 1), (512, 44, 333, 1, 1),
+]
+
+
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", CASES32)
+def test_tf32x3_gemm_matches_fp64(M, N, K, a_mn, b_mn):
+    """3xTF32 keeps ~fp32 accuracy: error vs a float64 matmul of the same fp32 operands within a small
+    multiple of fp32 rounding (plain tf32 would be ~2^-11 relative: 500x larger)."""
+    g = torch.Generator(device="cuda").manual_seed(M * 5 + N * 11 + K)
+    lda = ((M if a_mn else K) + 3) // 4 * 4
+    ldb = ((N if b_mn else K) + 3) // 4 * 4
+    A = _mk32(K, M, lda, g) if a_mn else _mk32(M, K, lda, g)
+    B = _mk32(K, N, ldb, g) if b_mn else _mk32(N, K, ldb, g)
+    C = torch.full((M, N), float("nan"), device="cuda")
+    spz.spz_diag_gemm_f32(M, N, K, A, lda, a_mn, B, ldb, b_mn, C, N)
+    Ad, Bd = A.double(), B.double()
+    Am = Ad[:K, :M].t() if a_mn else Ad[:M, :K]
+    Bm = Bd[:K, :N] if b_mn else Bd[:N, :K].t()
+    ref = Am @ Bm
+    scale = (Am.abs() @ Bm.abs())  # the fp32 error bound of each dot product scales with sum |a||b|
+    err = ((C.double() - ref).abs() / scale.clamp_min(1e-30)).max().item()
+    assert err < 3e-7 * K ** 0.5 + 1e-6, err  # fp32-accumulation scale; plain tf32 is ~5e-4
+
+
+def test_tf32x3_split_k_partials():
+    M, N, K, splits, kps = 256, 256, 1000, 3, 384
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = _mk32(K, M, M, g)
+    B = _mk32(K, N, N, g)
+    C = torch.full((splits, M, N), float("nan"), device="cuda")
+    spz.spz_diag_gemm_f32(M, N, K, A, M, 1, B, N, 1, C, N, splits=splits, k_per_split=kps)
+    for s in range(splits):
+        lo, hi = s * kps, min(K, (s + 1) * kps)
+        ref = A[lo:hi].double().t() @ B[lo:hi].double()
+        scale = A[lo:hi].double().abs().t() @ B[lo:hi].double().abs()
+        assert ((C[s].double() - ref).abs() / scale).max().item() < 2e-6
+
+
+def test_tf32x3_and_simt_agree():
+    M, N, K = 1000, 256, 256
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = _mk32(M, K, K, g)
+    B = _mk32(N, K, K, g)
+    C1 = torch.empty(M, N, device="cuda")
+    C2 = torch.empty(M, N, device="cuda")
+    spz.spz_diag_gemm_f32(M, N, K, A, K, 0, B, K, 0, C1, N, tensor_cores=True)
+    spz.spz_diag_gemm_f32(M, N, K, A, K, 0, B, K, 0, C2, N, tensor_cores=False)
+    assert (C1 - C2).abs().max().item() < 1e-5 * C2.abs().max().item()

@@ -38,7 +38,14 @@ struct spz_replay {
   float* rec = nullptr;       // [C x R] fp32, device
   float* staging = nullptr;   // pinned host staging for pushes
   size_t staging_bytes = 0;
+  float* dstage = nullptr;    // device staging of the five field arrays (pinned-host pushes)
+  size_t dstage_bytes = 0;
   cudaStream_t stream = nullptr;
+  // ordering against in-flight updates (the update reads the pool while samplers write it):
+  // every write to `rec` is enqueued after the readers' last recorded reads; learners wait on ev_pack
+  cudaEvent_t ev_copy = nullptr;       // pinned push: the caller's buffers have been read (H2D done)
+  cudaEvent_t ev_pack = nullptr;       // the last push's records are in `rec`
+  std::vector<cudaEvent_t> readers;    // one per learner: its last enqueued update (registered at create)
   std::mutex mu;
   int64_t fill() const { return cursor < C ? cursor : C; }
 };

@@ -110,6 +110,10 @@ struct spz_learner {
   int64_t* counters = nullptr;  // step, t_critic, t_actor, t_alpha
   int64_t* d_fill = nullptr;
   int* d_flag = nullptr;
+  cudaEvent_t ev_read = nullptr;  // recorded after every enqueued update: ring pushes wait on it
+  bool pending = false;           // an update enqueued by spz_update_async not yet waited for
+  bool ctr_cached = false;  // h_counters[0..3] / h_flag mirror the device (set by read_counters; cleared while
+                            // steps are enqueued): spz_update skips the leading device round trip
   StatsOut* d_stats = nullptr;
   StatsOut* h_stats = nullptr;  // pinned
   int* h_flag = nullptr;        // pinned
@@ -255,7 +259,16 @@ spz_learner::~spz_learner() {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
   if (own_stream) cudaStreamSynchronize(own_stream);
+  if (ev_read) {
+    if (ring) {
+      std::lock_guard<std::mutex> lk(ring->mu);
+      auto& v = ring->readers;
+      v.erase(std::remove(v.begin(), v.end(), ev_read), v.end());
+    }
+    cudaEventDestroy(ev_read);
+  }
   if (gcomm.handle && gcomm.handle != comm.handle) comm_destroy(&gcomm);
   comm_destroy(&comm);
   for (auto& e : exec)
@@ -1135,6 +1148,7 @@ static spz_status read_counters(spz_learner* Lr) {
   SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_counters, Lr->counters, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, Lr->stream));
   SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_flag, Lr->d_flag, sizeof(int), cudaMemcpyDeviceToHost, Lr->stream));
   SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  Lr->ctr_cached = true;
   return SPZ_OK;
 }
 
@@ -1220,6 +1234,12 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   if (cudaStreamCreateWithFlags(&Lr->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SPZ_ECUDA, "spz_learner_create: stream creation failed");
   Lr->stream = Lr->own_stream;
+  if (cudaEventCreateWithFlags(&Lr->ev_read, cudaEventDisableTiming) != cudaSuccess)
+    return fail(SPZ_ECUDA, "spz_learner_create: event creation failed");
+  {
+    std::lock_guard<std::mutex> lk(ring->mu);
+    ring->readers.push_back(Lr->ev_read);
+  }
   Lr->split = cfg->role != SPZ_ROLE_ALL;
   Lr->gsize = !Lr->split ? cfg->world_size
                          : (cfg->world_size == 1 ? 1
@@ -1430,26 +1450,12 @@ spz_status spz_learner_set_stream(spz_learner* Lr, void* stream) {
   return SPZ_OK;
 }
 
-spz_status spz_update(spz_learner* Lr, int64_t batch, int64_t n_steps, spz_stats* last) {
-  if (!Lr) return fail(SPZ_EINVAL, "spz_update: NULL learner");
-  if (n_steps < 0) return fail(SPZ_EINVAL, "spz_update: n_steps < 0");
-  DeviceGuard dg(Lr->device);
-  SPZ_TRY(prepare(Lr, batch));
-  SPZ_TRY(read_counters(Lr));
-  if (*Lr->h_flag) return fail(SPZ_ENONFINITE, "spz_update: learner halted by an earlier non-finite step " + std::to_string(Lr->h_counters[0]));
-  int64_t step = Lr->h_counters[0];
-  SPZ_TRY(set_fill(Lr));
-  for (int64_t k = 0; k < n_steps; ++k, ++step) {
-    const int v = variant_of(Lr, step);
-    if (Lr->cfg.use_graph) {
-      SPZ_TRY(ensure_graph(Lr, v));
-      SPZ_CUDA_TRY(cudaGraphLaunch(Lr->exec[v], Lr->stream));
-    } else {
-      SPZ_TRY(run_ops(Lr, v, Lr->stream));
-    }
-  }
-  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_stats, Lr->d_stats, sizeof(StatsOut), cudaMemcpyDeviceToHost, Lr->stream));
-  SPZ_TRY(read_counters(Lr));
+namespace spz {
+// completes the update enqueued by spz_update_async: statistics, counters and the non-finite flag
+static spz_status update_finish(spz_learner* Lr, spz_stats* last) {
+  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+  Lr->pending = false;
+  Lr->ctr_cached = true;
   if (*Lr->h_flag)
     return fail(SPZ_ENONFINITE, "spz_update: non-finite loss or gradient at step " + std::to_string(Lr->h_counters[0]) +
                                     (*Lr->h_flag == 2 ? " (gradient)" : " (loss)") + "; learner halted");
@@ -1465,6 +1471,48 @@ spz_status spz_update(spz_learner* Lr, int64_t batch, int64_t n_steps, spz_stats
     last->logp_mean = s.logp_mean;
   }
   return SPZ_OK;
+}
+}  // namespace spz
+
+spz_status spz_update_async(spz_learner* Lr, int64_t batch, int64_t n_steps) {
+  if (!Lr) return fail(SPZ_EINVAL, "spz_update_async: NULL learner");
+  if (n_steps < 0) return fail(SPZ_EINVAL, "spz_update_async: n_steps < 0");
+  DeviceGuard dg(Lr->device);
+  if (Lr->pending) SPZ_TRY(update_finish(Lr, nullptr));  // at most one update in flight
+  SPZ_TRY(prepare(Lr, batch));
+  if (!Lr->ctr_cached) SPZ_TRY(read_counters(Lr));
+  if (*Lr->h_flag) return fail(SPZ_ENONFINITE, "spz_update: learner halted by an earlier non-finite step " + std::to_string(Lr->h_counters[0]));
+  int64_t step = Lr->h_counters[0];
+  Lr->ctr_cached = false;
+  SPZ_TRY(set_fill(Lr));
+  SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));  // the last push's records are written
+  for (int64_t k = 0; k < n_steps; ++k, ++step) {
+    const int v = variant_of(Lr, step);
+    if (Lr->cfg.use_graph) {
+      SPZ_TRY(ensure_graph(Lr, v));
+      SPZ_CUDA_TRY(cudaGraphLaunch(Lr->exec[v], Lr->stream));
+    } else {
+      SPZ_TRY(run_ops(Lr, v, Lr->stream));
+    }
+  }
+  SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_read, Lr->stream));  // pushes overwrite records only after these reads
+  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_stats, Lr->d_stats, sizeof(StatsOut), cudaMemcpyDeviceToHost, Lr->stream));
+  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_counters, Lr->counters, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, Lr->stream));
+  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_flag, Lr->d_flag, sizeof(int), cudaMemcpyDeviceToHost, Lr->stream));
+  Lr->pending = true;
+  return SPZ_OK;
+}
+
+spz_status spz_update_wait(spz_learner* Lr, spz_stats* last) {
+  if (!Lr) return fail(SPZ_EINVAL, "spz_update_wait: NULL learner");
+  DeviceGuard dg(Lr->device);
+  return update_finish(Lr, last);  // (nothing in flight: the statistics of the last completed update)
+}
+
+spz_status spz_update(spz_learner* Lr, int64_t batch, int64_t n_steps, spz_stats* last) {
+  SPZ_TRY(spz_update_async(Lr, batch, n_steps));
+  DeviceGuard dg(Lr->device);
+  return update_finish(Lr, last);
 }
 
 static spz_status tensor_region(spz_learner* Lr, spz_tensor t, spz_slot s, float** base, int64_t* n) {
@@ -1558,10 +1606,13 @@ spz_status spz_learner_profile(spz_learner* Lr, int64_t batch, int64_t n_steps, 
                                int32_t* count) {
   if (!Lr || n_steps < 1) return fail(SPZ_EINVAL, "spz_learner_profile: bad argument");
   DeviceGuard dg(Lr->device);
+  if (Lr->pending) SPZ_TRY(update_finish(Lr, nullptr));
   SPZ_TRY(prepare(Lr, batch));
   SPZ_TRY(read_counters(Lr));
   int64_t step = Lr->h_counters[0];
+  Lr->ctr_cached = false;
   SPZ_TRY(set_fill(Lr));
+  SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));
   std::vector<const char*> cls;
   std::vector<double> tot;
   std::vector<cudaEvent_t> ev;
@@ -1595,6 +1646,7 @@ spz_status spz_learner_profile(spz_learner* Lr, int64_t batch, int64_t n_steps, 
       tot[c] += t;
     }
   }
+  SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_read, Lr->stream));
   for (auto e : ev) cudaEventDestroy(e);
   const int nc = (int)std::min<size_t>(cls.size(), (size_t)std::max(cap, 0));
   for (int i = 0; i < nc; ++i) {

@@ -4,7 +4,9 @@
 // "without consuming the time of the network update process".  Here the pool
 // lives in HBM as fp32 records [s | a | r | d | s2 | pad] (16-byte aligned rows),
 // slot(i) = i mod C, fill = min(cursor, C).
+#include <algorithm>
 #include <cstring>
+#include <initializer_list>
 #include <mutex>
 #include <vector>
 
@@ -71,6 +73,19 @@ __global__ void __launch_bounds__(256) sample_kernel(const float* __restrict__ r
   }
 }
 
+// true if every pointer is page-locked host memory (cudaHostAlloc / cudaHostRegister / torch pin_memory)
+static bool all_pinned(std::initializer_list<const float*> ps) {
+  for (const float* p : ps) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (at.type != cudaMemoryTypeHost) return false;
+  }
+  return true;
+}
+
 }  // namespace spz
 
 using namespace spz;
@@ -98,6 +113,8 @@ spz_status spz_replay_create(const spz_replay_desc* desc, spz_replay** out) {
     return fail(SPZ_ENOMEM, "spz_replay_create: cannot allocate " + std::to_string(bytes) + " bytes for the ring");
   }
   if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&r->ev_copy, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&r->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
       cudaMemsetAsync(r->rec, 0, bytes, r->stream) != cudaSuccess || cudaStreamSynchronize(r->stream) != cudaSuccess) {
     cudaFree(r->rec);
     delete r;
@@ -122,19 +139,66 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
   const int64_t nn = n - skip;
   const int64_t start = first_idx + skip;
   const int o = r->o, m = r->m, R = r->R;
+  // writes to the records wait for every learner's last enqueued read of them
+  const auto wait_readers = [&]() -> cudaError_t {
+    for (cudaEvent_t e : r->readers) {
+      cudaError_t err = cudaStreamWaitEvent(r->stream, e, 0);
+      if (err != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+  };
   if (src_on_device) {
+    SPZ_CUDA_TRY(wait_readers());
     const int64_t total = nn * R;
     const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
     pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, obs + skip * o, act + skip * m,
                                                         rew + skip, next_obs + skip * o, done + skip);
     SPZ_CUDA_TRY(cudaGetLastError());
+  } else if (all_pinned({obs, act, rew, next_obs, done})) {
+    // page-locked host fields: DMA them as they are into device staging and pack on the device (no
+    // host-side record assembly); the copies read the caller's buffers, so the call still waits for them
+    const size_t F = (size_t)(2 * o + m + 2);
+    const size_t bytes = (size_t)nn * F * sizeof(float);
+    if (r->dstage_bytes < bytes) {
+      SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+      if (r->dstage) cudaFree(r->dstage);
+      r->dstage = nullptr;
+      r->dstage_bytes = 0;
+      SPZ_CUDA_TRY(cudaMalloc(&r->dstage, bytes));
+      r->dstage_bytes = bytes;
+    }
+    float* d_obs = r->dstage;
+    float* d_act = d_obs + nn * o;
+    float* d_nobs = d_act + nn * m;
+    float* d_rew = d_nobs + nn * o;
+    float* d_done = d_rew + nn;
+    const auto h2d = [&](float* dst, const float* src, int w) {
+      return cudaMemcpyAsync(dst, src + skip * w, (size_t)nn * w * sizeof(float), cudaMemcpyHostToDevice, r->stream);
+    };
+    SPZ_CUDA_TRY(h2d(d_obs, obs, o));
+    SPZ_CUDA_TRY(h2d(d_act, act, m));
+    SPZ_CUDA_TRY(h2d(d_nobs, next_obs, o));
+    SPZ_CUDA_TRY(h2d(d_rew, rew, 1));
+    SPZ_CUDA_TRY(h2d(d_done, done, 1));
+    SPZ_CUDA_TRY(cudaEventRecord(r->ev_copy, r->stream));
+    SPZ_CUDA_TRY(wait_readers());
+    const int64_t total = nn * R;
+    const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+    pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, d_obs, d_act, d_rew, d_nobs, d_done);
+    SPZ_CUDA_TRY(cudaGetLastError());
+    SPZ_CUDA_TRY(cudaEventRecord(r->ev_pack, r->stream));
+    // return once the caller's buffers are read; the pack may still wait for an in-flight update, and
+    // the next update waits for ev_pack
+    SPZ_CUDA_TRY(cudaEventSynchronize(r->ev_copy));
+    r->cursor += n;
+    return SPZ_OK;
   } else {
     const size_t bytes = (size_t)nn * R * sizeof(float);
     if (r->staging_bytes < bytes) {
+      SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
       if (r->staging) cudaFreeHost(r->staging);
       r->staging = nullptr;
       r->staging_bytes = 0;
-      SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
       SPZ_CUDA_TRY(cudaMallocHost(&r->staging, bytes));
       r->staging_bytes = bytes;
     } else {
@@ -152,12 +216,14 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
       for (int c = 2 * o + m + 2; c < R; ++c) d[c] = 0.f;
     }
     // at most two pieces, split at the wrap point
+    SPZ_CUDA_TRY(wait_readers());
     const int64_t slot = start % r->C;
     const int64_t n1 = std::min(nn, r->C - slot);
     SPZ_CUDA_TRY(cudaMemcpyAsync(r->rec + slot * R, s, (size_t)n1 * R * sizeof(float), cudaMemcpyHostToDevice, r->stream));
     if (nn > n1)
       SPZ_CUDA_TRY(cudaMemcpyAsync(r->rec, s + n1 * R, (size_t)(nn - n1) * R * sizeof(float), cudaMemcpyHostToDevice, r->stream));
   }
+  SPZ_CUDA_TRY(cudaEventRecord(r->ev_pack, r->stream));
   SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
   r->cursor += n;
   return SPZ_OK;
@@ -202,6 +268,9 @@ void spz_replay_destroy(spz_replay* r) {
     cudaStreamSynchronize(r->stream);
     cudaFree(r->rec);
     if (r->staging) cudaFreeHost(r->staging);
+    if (r->dstage) cudaFree(r->dstage);
+    cudaEventDestroy(r->ev_copy);
+    cudaEventDestroy(r->ev_pack);
     cudaStreamDestroy(r->stream);
   }
   delete r;

@@ -30,7 +30,7 @@ SPZ_S_PARAM, SPZ_S_ADAM_M, SPZ_S_ADAM_V = 0, 1, 2
 EXPORTS = [
     "spz_last_error", "spz_version", "spz_replay_create", "spz_replay_push", "spz_replay_sample", "spz_replay_info",
     "spz_replay_records", "spz_replay_destroy", "spz_config_default", "spz_nccl_unique_id", "spz_learner_create",
-    "spz_update", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
+    "spz_update", "spz_update_async", "spz_update_wait", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
     "spz_diag_gemm_bf16", "spz_diag_gemm_f32", "spz_split_exchange", "spz_diag_tc_trace",
 ]
@@ -104,6 +104,8 @@ def lib():
             "spz_nccl_unique_id": (ctypes.c_int, [P]),
             "spz_learner_create": (ctypes.c_int, [ctypes.POINTER(spz_config), P, ctypes.POINTER(P)]),
             "spz_update": (ctypes.c_int, [P, I64, I64, ctypes.POINTER(spz_stats)]),
+            "spz_update_async": (ctypes.c_int, [P, I64, I64]),
+            "spz_update_wait": (ctypes.c_int, [P, ctypes.POINTER(spz_stats)]),
             "spz_learner_set_stream": (ctypes.c_int, [P, P]),
             "spz_get_params": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, I64, ctypes.POINTER(I64)]),
             "spz_set_params": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, I64]),
@@ -209,6 +211,16 @@ def spz_learner_create(cfg, ring):
 def spz_update(learner, batch, n_steps):
     s = spz_stats()
     _check(lib().spz_update(learner, batch, n_steps, ctypes.byref(s)))
+    return s.as_dict()
+
+
+def spz_update_async(learner, batch, n_steps):
+    _check(lib().spz_update_async(learner, batch, n_steps))
+
+
+def spz_update_wait(learner):
+    s = spz_stats()
+    _check(lib().spz_update_wait(learner, ctypes.byref(s)))
     return s.as_dict()
 
 
@@ -360,6 +372,12 @@ class Learner:
 
     def update(self, batch, n_steps=1):
         return spz_update(self.h, batch, n_steps)
+
+    def update_async(self, batch, n_steps=1):
+        spz_update_async(self.h, batch, n_steps)
+
+    def wait(self):
+        return spz_update_wait(self.h)
 
     def get(self, name, slot=SPZ_S_PARAM):
         return spz_get_params(self.h, PARAM_TENSORS[name], slot)

@@ -85,6 +85,66 @@ def test_replay_push_from_device_matches_host():
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
+def test_replay_push_pinned_matches_pageable():
+    """Page-locked host fields take the DMA + device-pack path; the ring must be bit-identical to the
+    host-pack path, including a push that wraps and one longer than the capacity."""
+    o, m, C = 17, 5, 700
+    rings = []
+    for pinned in (False, True):
+        g = spz.Replay(o, m, C)
+        for n, seed in ((500, 1), (450, 2), (1600, 3)):
+            tr = synthdata.transitions("locomotion", o, m, n, seed=seed)
+            if pinned:
+                tr = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in tr.items()}
+            g.push(**tr)
+        rings.append(g)
+    assert rings[0].info() == rings[1].info()
+    B = 700
+    outs = []
+    for g in rings:
+        bufs = [torch.empty(B, dtype=torch.int32, device="cuda"), torch.empty(B, o, device="cuda"),
+                torch.empty(B, m, device="cuda"), torch.empty(B, device="cuda"), torch.empty(B, o, device="cuda"),
+                torch.empty(B, device="cuda")]
+        spz.spz_replay_sample(g.h, B, 9, 4, *bufs)
+        outs.append([b.cpu().numpy() for b in bufs])
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
+
+
+def test_update_async_overlapped_pushes_bit_identical():
+    """push(k+1) issued while update k runs (spz_update_async / spz_update_wait) gives bit-identical
+    parameters and statistics to the synchronous push, update sequence (device-side ordering of the
+    ring writes after the in-flight reads); pinned and pageable pushes."""
+    o, m, C, B, K = 22, 6, 3000, 1024, 6
+    fresh = [synthdata.transitions("locomotion", o, m, B, seed=100 + k) for k in range(K)]
+    res = []
+    for mode in ("sync", "async_pinned", "async_pageable"):
+        g, _ = make_rings(o, m, C)
+        lrn = spz.Learner(g, precision="bf16", hidden=64, n_hidden=2, max_batch=B)
+        stats = []
+        for k in range(K):
+            tr = fresh[k]
+            if mode == "async_pinned":
+                tr = {n: torch.from_numpy(v).pin_memory().numpy() for n, v in tr.items()}
+            if mode == "sync":
+                g.push(**tr)
+                stats.append(lrn.update(B, 1))
+            else:
+                if k > 0:
+                    g.push(**tr)  # overlaps update k-1 on the GPU
+                    stats.append(lrn.wait())
+                else:
+                    g.push(**tr)
+                lrn.update_async(B, 1)
+        if mode != "sync":
+            stats.append(lrn.wait())
+        res.append((stats, [lrn.get(n) for n in ("actor", "q1", "q2", "q1_targ")]))
+    for other in res[1:]:
+        assert other[0] == res[0][0]
+        for a, b in zip(other[1], res[0][1]):
+            assert np.array_equal(a, b)
+
+
 # ----------------------------------------------------------------------------- whole update parity
 
 def run_parity(algo, precision, o, m, h, L, B, C, K, kind="locomotion", use_graph=True, check_moments=True):

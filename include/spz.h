@@ -256,6 +256,39 @@ spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, i
                               const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb,
                               int32_t b_mn, float* C, int64_t ldc, int32_t splits, int64_t k_per_split);
 
+/* ---------------------------------------------------------------- sampler-side policy (§8(f) f1)
+ * Batched actor inference for the samplers, fed by spz_sync_actor (sampler actions are
+ * "generate[d] ... by forward propagation"; the test process acts deterministically).
+ *   SAC  deterministic a = tanh(mu);  stochastic a = tanh(mu + exp(clamp(l, lo, hi)) * n)
+ *   TD3  deterministic a = tanh(z);   stochastic a = clip(tanh(z) + expl_noise * n, -1, 1)
+ * n[j, i]: normal i of call row j, Philox(seed, (j, i / 4, step, S_ACT = 7)) Box-Muller as in the
+ * update (readings #13, #21).  Same dense layers as the update: bf16 tcgen05 GEMMs, or
+ * 3xTF32 in FP32 precision. */
+typedef struct spz_policy spz_policy;     /* opaque, caller-owned */
+typedef struct {
+  spz_algo algo;
+  spz_precision precision;
+  int32_t obs_dim, act_dim, hidden, n_hidden;  /* must match the learner whose actor is loaded */
+  int64_t max_batch;                           /* rows per spz_policy_act call                  */
+  int32_t device;
+  double log_std_min, log_std_max;             /* SAC clamp (learner defaults: -20, 2)           */
+  double expl_noise;                           /* TD3 exploration std (0.1)                      */
+} spz_policy_desc;
+/* Errors: SPZ_EINVAL (bad dims), SPZ_ENOMEM, SPZ_ECUDA. */
+spz_status spz_policy_create(const spz_policy_desc* desc, spz_policy** out);
+/* Load the actor from a spz_sync_actor payload [u64 version | u64 n_floats | floats] in device or host
+ * memory (borrowed for the call).  Seqlock read (header, payload, header): a concurrent writer makes
+ * it retry, so the loaded parameters are exactly one version's; *version (nullable) receives
+ * it.  SPZ_EINVAL if n_floats does not match the policy's shape; SPZ_ETIMEOUT if the payload kept
+ * changing.  Synchronous. */
+spz_status spz_policy_load(spz_policy* P, const void* payload, int64_t bytes, uint64_t* version);
+/* Actions act [n x m] (fp32, row-major) for observations obs [n x o]; each pointer may be host or
+ * device memory (detected).  0 <= n <= max_batch.  deterministic != 0 selects the test-process
+ * action.  SPZ_ESTATE before the first spz_policy_load.  Synchronous. */
+spz_status spz_policy_act(spz_policy* P, int64_t n, const float* obs, int32_t deterministic, uint64_t seed,
+                          uint64_t step, float* act);
+void spz_policy_destroy(spz_policy* P);
+
 /* Diagnostics (GEMM unit tests): the FP32-precision GEMM, C = A * B in fp32 with the same operand
  * conventions as spz_diag_gemm_bf16 but fp32 operands (row pitches multiple of 4 elements, 16-byte
  * aligned device pointers).  tensor_cores = 1 runs the 3xTF32 tcgen05 kernel (SURVEY.md §8(a) a3,

@@ -30,6 +30,12 @@ struct DeviceGuard {
 
 }  // namespace spz
 
+#define SPZ_TRY(expr)            \
+  do {                           \
+    spz_status _s = (expr);      \
+    if (_s != SPZ_OK) return _s; \
+  } while (0)
+
 struct spz_replay {
   int o = 0, m = 0, R = 0;
   int64_t C = 0;

@@ -185,11 +185,6 @@ static spz_status dalloc(spz_learner* Lr, void** p, size_t bytes) {
   return SPZ_OK;
 }
 
-#define SPZ_TRY(expr)            \
-  do {                           \
-    spz_status _s = (expr);      \
-    if (_s != SPZ_OK) return _s; \
-  } while (0)
 
 // Split-K count of the merged weight-gradient GEMM: enough splits that the output tiles of all
 // trained weights (128 x 256 each) cover the SMs about once -- more splits only add partial traffic

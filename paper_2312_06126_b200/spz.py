@@ -33,6 +33,7 @@ EXPORTS = [
     "spz_update", "spz_update_async", "spz_update_wait", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
     "spz_diag_gemm_bf16", "spz_diag_gemm_f32", "spz_split_exchange", "spz_diag_tc_trace",
+    "spz_policy_create", "spz_policy_load", "spz_policy_act", "spz_policy_destroy",
 ]
 
 
@@ -40,6 +41,13 @@ class SpzError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
         self.status = status
+
+
+class spz_policy_desc(ctypes.Structure):
+    _fields_ = [("algo", ctypes.c_int), ("precision", ctypes.c_int),
+                ("obs_dim", ctypes.c_int32), ("act_dim", ctypes.c_int32), ("hidden", ctypes.c_int32),
+                ("n_hidden", ctypes.c_int32), ("max_batch", ctypes.c_int64), ("device", ctypes.c_int32),
+                ("log_std_min", ctypes.c_double), ("log_std_max", ctypes.c_double), ("expl_noise", ctypes.c_double)]
 
 
 class spz_replay_desc(ctypes.Structure):
@@ -122,6 +130,10 @@ def lib():
             "spz_diag_tc_trace": (ctypes.c_int, [I32, I32, P, I32]),
             "spz_diag_gemm_bf16": (ctypes.c_int, [I32, I32, I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, I64]),
             "spz_diag_gemm_f32": (ctypes.c_int, [I32, I32, I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, I64]),
+            "spz_policy_create": (ctypes.c_int, [ctypes.POINTER(spz_policy_desc), ctypes.POINTER(P)]),
+            "spz_policy_load": (ctypes.c_int, [P, P, I64, ctypes.POINTER(U64)]),
+            "spz_policy_act": (ctypes.c_int, [P, I64, P, I32, U64, U64, P]),
+            "spz_policy_destroy": (None, [P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -403,6 +415,62 @@ class Learner:
     def close(self):
         if self.h:
             spz_learner_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ----------------------------------------------------------------------------- sampler-side policy (f1)
+
+def spz_policy_create(desc):
+    h = ctypes.c_void_p()
+    _check(lib().spz_policy_create(ctypes.byref(desc), ctypes.byref(h)))
+    return h
+
+
+def spz_policy_load(policy, payload_ptr, nbytes):
+    v = ctypes.c_uint64()
+    _check(lib().spz_policy_load(policy, ctypes.c_void_p(payload_ptr), nbytes, ctypes.byref(v)))
+    return v.value
+
+
+def spz_policy_act(policy, n, obs, deterministic, seed, step, act):
+    """obs [n x o] / act [n x m]: float32 numpy arrays (host) or torch CUDA tensors."""
+    _check(lib().spz_policy_act(policy, n, _ptr(obs), 1 if deterministic else 0, seed, step, _ptr(act)))
+
+
+def spz_policy_destroy(policy):
+    lib().spz_policy_destroy(policy)
+
+
+class Policy:
+    """Sampler-side actor inference (include/spz.h), fed by Learner.sync_actor payloads."""
+
+    def __init__(self, obs_dim, act_dim, algo="sac", precision="bf16", hidden=256, n_hidden=2, max_batch=4096,
+                 device=0, log_std_min=-20.0, log_std_max=2.0, expl_noise=0.1):
+        d = spz_policy_desc(SPZ_SAC if algo == "sac" else SPZ_TD3, SPZ_BF16 if precision == "bf16" else SPZ_FP32,
+                            obs_dim, act_dim, hidden, n_hidden, max_batch, device, log_std_min, log_std_max,
+                            expl_noise)
+        self.obs_dim, self.act_dim = obs_dim, act_dim
+        self.h = spz_policy_create(d)
+
+    def load(self, payload_ptr, nbytes):
+        return spz_policy_load(self.h, payload_ptr, nbytes)
+
+    def act(self, obs, deterministic=False, seed=0, step=0, out=None):
+        n = obs.shape[0]
+        if out is None:
+            out = np.empty((n, self.act_dim), dtype=np.float32)
+        spz_policy_act(self.h, n, obs, deterministic, seed, step, out)
+        return out
+
+    def close(self):
+        if self.h:
+            spz_policy_destroy(self.h)
             self.h = None
 
     def __del__(self):

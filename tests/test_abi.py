@@ -55,6 +55,9 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(spz.SpzError) as e:
         spz.spz_replay_create(3, 1, 100)
     assert e.value.status in (spz.SPZ_ECUDA,)
+    with pytest.raises(spz.SpzError) as e:
+        spz.Policy(3, 1, hidden=64, n_hidden=2)
+    assert e.value.status in (spz.SPZ_ECUDA,)
 
 
 def test_invalid_arguments_rejected_before_device_use():

@@ -62,6 +62,26 @@ __device__ __forceinline__ float normal_q(uint64_t seed, uint64_t step, uint32_t
   return (q & 1) ? R * s : R * c;
 }
 
+// The four normals q = 4c .. 4c+3 of row j (one Philox block, two Box-Muller pairs); n[k] equals
+// normal_q(seed, step, stream, row, 4c + k) bit for bit.  `pairs` = 1 skips the second pair.
+__device__ __forceinline__ void normals4(uint64_t seed, uint64_t step, uint32_t stream, uint64_t row, int c, int pairs,
+                                         float (&n)[4]) {
+  const uint4 x = philox(make_uint4((uint32_t)row, (uint32_t)c, (uint32_t)step, stream), (uint32_t)seed,
+                         (uint32_t)(seed >> 32));
+  float s, co;
+  const float R0 = sqrtf(-2.0f * logf(u01(x.x)));
+  sincospif(2.0f * u01(x.y), &s, &co);
+  n[0] = R0 * co;
+  n[1] = R0 * s;
+  n[2] = n[3] = 0.f;
+  if (pairs > 1) {
+    const float R1 = sqrtf(-2.0f * logf(u01(x.z)));
+    sincospif(2.0f * u01(x.w), &s, &co);
+    n[2] = R1 * co;
+    n[3] = R1 * s;
+  }
+}
+
 // ------------------------------------------------------------------ element types
 template <typename T> __device__ __forceinline__ T from_f(float x);
 template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }

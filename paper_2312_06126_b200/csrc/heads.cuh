@@ -27,31 +27,41 @@ struct HeadEpi {
 
 // SAC: [mu | l] -> lc = clamp(l), sigma = exp(lc), u = mu + sigma eps, a = tanh u,
 // log pi = sum_i [-eps^2/2 - lc - ln(2 pi)/2 - 2 (ln 2 - u - softplus(-2u))].
-// Actions [i0, i1) of row r; returns their part of log pi (the caller sums the parts in order).
+// Processes the actions of Philox blocks c = b0, b0 + bstep, ... (4 actions per block: one Philox call
+// and two Box-Muller pairs serve all four) of row r; returns their part of log pi (the caller sums
+// the parts in a fixed order).
 template <typename T>
-__device__ __forceinline__ float sac_head_part(const HeadEpi& h, int r, const float* mu, const float* lraw, int i0, int i1) {
+__device__ __forceinline__ float sac_head_blocks(const HeadEpi& h, int r, const float* mu, const float* lraw, int b0,
+                                                 int bstep) {
   const bool s2row = r < h.Bl;
   const int j = s2row ? r : r - h.Bl;
   const uint64_t step = (uint64_t)*h.step_p;
   const uint32_t stream = s2row ? S_EPS2 : S_EPS;
   T* xa = static_cast<T*>(h.Xc) + (int64_t)(s2row ? 2 * h.Bl + j : h.Bl + j) * h.ldx + h.o;
   float lp = 0.f;
-  for (int i = i0; i < i1; ++i) {
-    const float l = lraw[i];
-    const float lc = fminf(fmaxf(l, h.lo), h.hi);
-    const float sg = expf(lc);
-    const float e = normal_q(h.seed, step, stream, (uint64_t)(h.row0 + j), i);
-    const float u = fmaf(sg, e, mu[i]);
-    const float a = tanhf(u);
-    lp += -0.5f * e * e - lc - HALF_LN_2PI_F - 2.f * (LN2F - u - softplusf(-2.f * u));
-    xa[i] = from_f<T>(a);
-    if (!s2row) {
-      const int64_t ci = (int64_t)j * h.m + i;
-      h.u[ci] = u;
-      h.a[ci] = a;
-      h.eps[ci] = e;
-      h.sig[ci] = sg;
-      h.l[ci] = l;
+  for (int c = b0; 4 * c < h.m; c += bstep) {
+    float e4[4];
+    normals4(h.seed, step, stream, (uint64_t)(h.row0 + j), c, h.m - 4 * c > 2 ? 2 : 1, e4);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = 4 * c + k;
+      if (i >= h.m) break;
+      const float l = lraw[i];
+      const float lc = fminf(fmaxf(l, h.lo), h.hi);
+      const float sg = expf(lc);
+      const float e = e4[k];
+      const float u = fmaf(sg, e, mu[i]);
+      const float a = tanhf(u);
+      lp += -0.5f * e * e - lc - HALF_LN_2PI_F - 2.f * (LN2F - u - softplusf(-2.f * u));
+      xa[i] = from_f<T>(a);
+      if (!s2row) {
+        const int64_t ci = (int64_t)j * h.m + i;
+        h.u[ci] = u;
+        h.a[ci] = a;
+        h.eps[ci] = e;
+        h.sig[ci] = sg;
+        h.l[ci] = l;
+      }
     }
   }
   return lp;
@@ -62,34 +72,39 @@ __device__ __forceinline__ void sac_head_logp(const HeadEpi& h, int r, float lp)
 }
 template <typename T>
 __device__ __forceinline__ void sac_head_row(const HeadEpi& h, int r, const float* mu, const float* lraw) {
-  sac_head_logp(h, r, sac_head_part<T>(h, r, mu, lraw, 0, h.m));
+  sac_head_logp(h, r, sac_head_blocks<T>(h, r, mu, lraw, 0, 1));
 }
 
 // TD3: rows r < Bl (target actor on s2): a' = clip(tanh z + clip(noise n, -c, c), -1, 1), n from
-// S_SMOOTH; rows r >= Bl (online actor on s): a~ = tanh z (cached for the backward).  Actions [i0, i1).
+// S_SMOOTH; rows r >= Bl (online actor on s): a~ = tanh z (cached for the backward).  Philox blocks
+// c = b0, b0 + bstep, ... of the row's actions.
 template <typename T>
-__device__ __forceinline__ void td3_head_part(const HeadEpi& h, int r, const float* z, int i0, int i1) {
+__device__ __forceinline__ void td3_head_blocks(const HeadEpi& h, int r, const float* z, int b0, int bstep) {
   const uint64_t step = (uint64_t)*h.step_p;
-  if (r < h.Bl) {
-    T* xa = static_cast<T*>(h.Xc) + (int64_t)(2 * h.Bl + r) * h.ldx + h.o;
-    for (int i = i0; i < i1; ++i) {
-      const float n = normal_q(h.seed, step, S_SMOOTH, (uint64_t)(h.row0 + r), i);
-      const float xi = fminf(fmaxf(h.noise * n, -h.clipc), h.clipc);
-      xa[i] = from_f<T>(fminf(fmaxf(tanhf(z[i]) + xi, -1.f), 1.f));
-    }
-  } else {
-    const int j = r - h.Bl;
-    T* xa = static_cast<T*>(h.Xc) + (int64_t)(h.Bl + j) * h.ldx + h.o;
-    for (int i = i0; i < i1; ++i) {
-      const float a = tanhf(z[i]);
-      xa[i] = from_f<T>(a);
-      h.a[(int64_t)j * h.m + i] = a;
+  const bool trow = r < h.Bl;
+  const int j = trow ? r : r - h.Bl;
+  T* xa = static_cast<T*>(h.Xc) + (int64_t)(trow ? 2 * h.Bl + r : h.Bl + j) * h.ldx + h.o;
+  for (int c = b0; 4 * c < h.m; c += bstep) {
+    float n4[4] = {0.f, 0.f, 0.f, 0.f};
+    if (trow) normals4(h.seed, step, S_SMOOTH, (uint64_t)(h.row0 + r), c, h.m - 4 * c > 2 ? 2 : 1, n4);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = 4 * c + k;
+      if (i >= h.m) break;
+      if (trow) {
+        const float xi = fminf(fmaxf(h.noise * n4[k], -h.clipc), h.clipc);
+        xa[i] = from_f<T>(fminf(fmaxf(tanhf(z[i]) + xi, -1.f), 1.f));
+      } else {
+        const float a = tanhf(z[i]);
+        xa[i] = from_f<T>(a);
+        h.a[(int64_t)j * h.m + i] = a;
+      }
     }
   }
 }
 template <typename T>
 __device__ __forceinline__ void td3_head_row(const HeadEpi& h, int r, const float* z) {
-  td3_head_part<T>(h, r, z, 0, h.m);
+  td3_head_blocks<T>(h, r, z, 0, 1);
 }
 
 }  // namespace spz

@@ -19,6 +19,7 @@
 #include "kernels.cuh"
 #include "tc_mlp.cuh"
 #include "tc_gemm.cuh"
+#include "tc_actor_bwd.cuh"
 
 namespace spz {
 
@@ -61,9 +62,15 @@ struct Op {
   int launches = 1;  // kernels this op launches
 };
 
-// diagnostics: SPZ_DZ_SPLIT=1 writes dZ_L in critic_dz_kernel at every width
-static bool dz_split_env() {
-  const char* e = std::getenv("SPZ_DZ_SPLIT");
+// diagnostics: SPZ_DZ_FUSED=1 writes dZ_L inside critic_loss_kernel (h <= 256) instead of critic_dz_kernel
+static bool dz_fused_env() {
+  const char* e = std::getenv("SPZ_DZ_FUSED");
+  return e && e[0] == '1';
+}
+
+// diagnostics: SPZ_ACTOR_BWD_UNFUSED=1 runs the actor backward as separate GEMM / head launches
+static bool actor_bwd_unfused_env() {
+  const char* e = std::getenv("SPZ_ACTOR_BWD_UNFUSED");
   return e && e[0] == '1';
 }
 
@@ -715,8 +722,9 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       la.actor_rows = do_actor;
       la.h = h;
       la.ld = h;
-      // h <= 256: one 8-column chunk per lane, dZ_L written by the loss kernel; wider: critic_dz_kernel
-      const bool dz_sep = (h > 256 || dz_split_env()) && (do_critic || do_actor);
+      // dZ_L is written by critic_dz_kernel (one thread per 8-column chunk: the loss kernel's
+      // warp-per-row layout has too few stores in flight at large batches -- ANT 55 us)
+      const bool dz_sep = (h > 256 || !dz_fused_env()) && (do_critic || do_actor);
       if (!lfused) {  // (the fused critic forward with loss groups computes all of this itself)
         if (dz_sep)
           ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
@@ -747,6 +755,47 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
                        }});
       }
     }
+    // ---- a6 (actor rows) + a7: one fused launch on the tensor-core path (tc_actor_bwd.cuh): critic
+    //      input gradient of the action columns, head backward (eq. H), dgrad down the actor stack
+    ActorBwdArgs ab{};
+    bool abwd_fused = false;
+    if (bits && do_actor && !actor_bwd_unfused_env()) {
+      const NetLayout& an = Lr->net[NET_ACTOR];
+      ab.Bl = (int)Bl;
+      ab.o = o;
+      ab.m = m;
+      ab.h = h;
+      ab.L = L;
+      ab.nout = an.out[L];
+      ab.td3 = td3;
+      ab.ncrit = td3 ? 1 : 2;
+      ab.ldw0c = cn.ld[0];
+      ab.ldh = ldh;
+      ab.mask_ld = mw;
+      for (int i = 0; i < 2; ++i) {
+        ab.dZ1[i] = Ta(Lr->dZc[i][0], Bl, h);
+        ab.W0c[i] = Wp(NET_Q1 + i, 0);
+      }
+      for (int l = 0; l <= L; ++l) {
+        ab.Wa[l] = Wp(NET_ACTOR, l);
+        ab.ldwa[l] = an.ld[l];
+      }
+      for (int l = 0; l < L; ++l) {
+        ab.mask[l] = Lr->mask_a[l] + (int64_t)Bl * mw;
+        ab.dZa[l] = Lr->dZa[l];
+      }
+      ab.dH = Lr->dH;
+      ab.u = Lr->cache.u;
+      ab.a = Lr->cache.a;
+      ab.eps = Lr->cache.eps;
+      ab.sig = Lr->cache.sig;
+      ab.l = Lr->cache.l;
+      ab.log_alpha = P + Lr->p_log_alpha;
+      ab.invB = invB;
+      ab.lo = lo;
+      ab.hi = hi;
+      abwd_fused = tc_actor_bwd_supported(ab);
+    }
     // ---- a6: critic backward
     {
       // dgrad through hidden layers l = L-1 .. 1 (the online rows [on0, on0 + Mon))
@@ -764,7 +813,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         gemm("critic_dgrad_gemm", a);
       }
       // input dgrad for the actor rows (only the action columns are consumed)
-      if (do_actor) {
+      if (do_actor && !abwd_fused) {
         GemmArgs a = mk(h, EPI_F32, 0, 1);
         for (int i = 0; i < (td3 ? 1 : 2); ++i)
           add(a, Ta(Lr->dZc[i][0], Bl, h), h, Wp(NET_Q1 + i, 0), cn.ld[0], Lr->dXc[i], ldc, Bl, o + m);
@@ -818,7 +867,9 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       const NetLayout& an = Lr->net[NET_ACTOR];
       const int nout = an.out[L];  // 2m (SAC) or m (TD3)
       T* dH = static_cast<T*>(Lr->dH);
-      {
+      if (abwd_fused) {
+        ops.push_back({"actor_bwd_fused", [ab](cudaStream_t st) { return tc_actor_bwd(ab, st); }});
+      } else {
         float *x1 = Lr->dXc[0], *x2 = Lr->dXc[1];
         HeadCache cache = Lr->cache;
         const float* la = P + Lr->p_log_alpha;
@@ -837,7 +888,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         }
       }
       // dgrad: dZ_{L-1} = (dH W_out) * 1[A_{L-1} > 0], then down the hidden stack
-      for (int l = L; l >= 1; --l) {
+      for (int l = L; l >= 1 && !abwd_fused; --l) {
         GemmArgs a = mk(an.out[l], bits ? EPI_MASK_BITS : EPI_MASK, 0, 1);
         if (bits)
           add(a, l == L ? (const void*)dH : (const void*)Lr->dZa[l], l == L ? ldh : h, Wp(NET_ACTOR, l), an.ld[l],

@@ -467,8 +467,8 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
         tc_fence_after();
         if (e == 0 && lane == 0) mtrace(p.trace, ui, l, 2);
         if (head) {
-          // ---- actor head: the two warps of a lane quarter take the row's actions [0, m/2) and
-          //      [m/2, m); SAC log pi = part 0 + part 1 (fixed order)
+          // ---- actor head: the two warps of a lane quarter take the row's Philox blocks of 4 actions
+          //      alternately (warp hh: blocks hh, hh + 2, ...); SAC log pi = part 0 + part 1 (fixed order)
           float hrow[32];
           for (int c = 0; c < p.nh / 16 && c < 2; ++c) {
             float v[16];
@@ -477,18 +477,17 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
             for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
           }
           tc_fence_before();
-          const int mh = p.head.m, half = (mh + 1) / 2;
-          const int i0 = hh ? half : 0, i1 = hh ? mh : half;
+          const int mh = p.head.m;
           const bool live = m < d.rows;
           if (p.head_epi == EPI_SAC_HEAD) {
-            const float lp = live ? sac_head_part<__nv_bfloat16>(p.head, d.row0 + m, hrow, hrow + mh, i0, i1) : 0.f;
+            const float lp = live ? sac_head_blocks<__nv_bfloat16>(p.head, d.row0 + m, hrow, hrow + mh, hh, 2) : 0.f;
             const int pb = dot_tiles & 1;
             dotpart[pb][hh][r] = lp;
             named_bar(2 + q, 64);
             if (hh == 0 && live) sac_head_logp(p.head, d.row0 + m, dotpart[pb][0][r] + dotpart[pb][1][r]);
             ++dot_tiles;
           } else if (live) {
-            td3_head_part<__nv_bfloat16>(p.head, d.row0 + m, hrow, i0, i1);
+            td3_head_blocks<__nv_bfloat16>(p.head, d.row0 + m, hrow, hh, 2);
           }
           __syncwarp();
           if (e == 0 && lane == 0) mtrace(p.trace, ui, l, 3);

@@ -310,5 +310,6 @@ def test_profile_and_launch_count():
     lrn = spz.Learner(g, precision="bf16", hidden=256, n_hidden=2, max_batch=8192)
     prof = lrn.profile(8192, 3)
     assert "gather" in prof and "adam_polyak" in prof and all(v > 0 for v in prof.values())
-    assert lrn.launches_per_step(8192) >= 10
+    # gather, 2 fused forwards, loss, critic dgrad, fused actor backward, wgrad, Adam (+ unfused variants)
+    assert 8 <= lrn.launches_per_step(8192) <= 16
     assert lrn.counters()["step"] == 3

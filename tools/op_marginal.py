@@ -12,7 +12,7 @@ import synthdata  # noqa: E402
 from paper_2312_06126_b200 import spz  # noqa: E402
 
 CLASSES = ["gather", "actor_fwd_mlp", "critic_fwd_mlp", "critic_loss", "critic_dgrad_gemm",
-           "critic_input_dgrad_gemm", "actor_head_bwd", "actor_dgrad_gemm", "wgrad_gemm", "adam_polyak"]
+           "actor_bwd_fused", "wgrad_gemm", "adam_polyak"]
 
 
 def per_update_ms(ring, skip, B=8192, K=300, reps=3):

@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="override the workload batch (B sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="also run the batch-size adaptation (spz_tune_batch, §8(f) f3) over the §8(d) B ladder")
     ap.add_argument("--cpu-sample-steps", type=int, default=None)
     ap.add_argument("--mode", default="dp", choices=["dp", "split", "replicas"],
                     help="N > 1: dp = one row-sharded learner group (global batch B*N, NCCL gradient allreduce); "
@@ -339,6 +341,15 @@ def main():
                "note": "per step: spz_replay_push of B fresh host transitions (pinned, H2D) overlapping the previous "
                        "update, spz_update_wait (stats D2H), spz_update_async(B, 1)"}
 
+    sweep = None
+    if a.sweep and world == 1:
+        ladder = [128, 512, 2048, 8192, 32768, 65536]
+        tl = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden,
+                         max_batch=ladder[-1], device=local)
+        best, pts = tl.tune_batch(ladder, warmup=5, steps=50, tol=1.0, restore=True)
+        sweep = {"best_batch": best, "points": pts, "note": "spz_tune_batch, 50 timed updates per B (CUDA events)"}
+        tl.close()
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         # bounded sample: ~15 s of oracle work (one probe update sizes it), at least one update
@@ -364,6 +375,7 @@ def main():
                        "l2": f"ring {C * ((2 * w.obs_dim + w.act_dim + 2 + 3) // 4 * 4) * 4 / 1e6:.0f} MB > 126 MB L2; fresh random indices each step"},
             "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(), "gpu_launches": launches, "last_stats": stats,
+            **({"batch_sweep": sweep} if sweep else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

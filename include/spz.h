@@ -235,6 +235,28 @@ spz_status spz_learner_launches_per_step(spz_learner* L, int64_t batch, int32_t*
 spz_status spz_learner_debug_buffer(spz_learner* L, const char* name, void* host_out, int64_t bytes,
                                     int64_t* bytes_required, int32_t* elem_size);
 
+/* ---------------------------------------------------------------- batch-size adaptation (§8(f) f3)
+ * The paper adapts its batch size to the largest one the GPU sustains ("BS mainly loads
+ * the GPU"; enumeration assuming a unimodal response).  spz_tune_batch probes the
+ * ascending ladder[0..n): at each B it runs max(warmup, 1) untimed then `steps` timed update steps
+ * (CUDA events on the learner's stream) and records the update frequency and frames/s = B x
+ * updates/s.  It stops climbing once frames/s falls more than `tol` (relative) below the best so far
+ * (past the peak) or the update frequency falls below min_update_hz; *best = the probed B with the
+ * most frames/s among those meeting min_update_hz (ladder[0] if none does).  With restore != 0 the
+ * parameters, Adam moments, step counters and the non-finite flag are restored afterwards, so training
+ * continues exactly as if the tuner had not run; else the probe steps count as training.  Needs
+ * fill >= B and B <= max_batch for every probed B (else SPZ_EINVAL / SPZ_ENODATA); the ladder must
+ * be strictly ascending.  out[0..*n_out) receives the probed points (caller-allocated, n entries). */
+typedef struct {
+  int64_t batch;
+  double updates_per_s;
+  double frames_per_s;
+  double ms_per_update;
+} spz_tune_point;
+spz_status spz_tune_batch(spz_learner* L, const int64_t* ladder, int32_t n, int64_t warmup, int64_t steps,
+                          double min_update_hz, double tol, int32_t restore, spz_tune_point* out, int32_t* n_out,
+                          int64_t* best);
+
 void spz_learner_destroy(spz_learner* L);
 
 /* ------------------------------------------------------------------ diagnostics

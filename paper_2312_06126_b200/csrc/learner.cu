@@ -1611,6 +1611,76 @@ spz_status spz_set_params(spz_learner* Lr, spz_tensor t, spz_slot s, const float
   return SPZ_OK;
 }
 
+spz_status spz_tune_batch(spz_learner* Lr, const int64_t* ladder, int32_t n, int64_t warmup, int64_t steps,
+                          double min_update_hz, double tol, int32_t restore, spz_tune_point* out, int32_t* n_out,
+                          int64_t* best) {
+  if (!Lr || !ladder || !out || !n_out || !best) return fail(SPZ_EINVAL, "spz_tune_batch: NULL argument");
+  if (n < 1 || steps < 1 || warmup < 0 || !(tol >= 0.0)) return fail(SPZ_EINVAL, "spz_tune_batch: bad n / steps / warmup / tol");
+  for (int i = 1; i < n; ++i)
+    if (ladder[i] <= ladder[i - 1]) return fail(SPZ_EINVAL, "spz_tune_batch: ladder must be strictly ascending");
+  DeviceGuard dg(Lr->device);
+  if (Lr->pending) SPZ_TRY(update_finish(Lr, nullptr));
+  *n_out = 0;
+  *best = ladder[0];
+  // snapshot of everything the probe steps change (the bf16 operand shadow is refreshed from P)
+  void* snap = nullptr;
+  const size_t pbytes = (size_t)Lr->P_total * sizeof(float);
+  if (restore) {
+    SPZ_CUDA_TRY(cudaMalloc(&snap, 3 * pbytes + 8 * sizeof(int64_t) + sizeof(int)));
+    uint8_t* s8 = static_cast<uint8_t*>(snap);
+    SPZ_CUDA_TRY(cudaMemcpyAsync(s8, Lr->P, pbytes, cudaMemcpyDeviceToDevice, Lr->stream));
+    SPZ_CUDA_TRY(cudaMemcpyAsync(s8 + pbytes, Lr->Mo, pbytes, cudaMemcpyDeviceToDevice, Lr->stream));
+    SPZ_CUDA_TRY(cudaMemcpyAsync(s8 + 2 * pbytes, Lr->Vo, pbytes, cudaMemcpyDeviceToDevice, Lr->stream));
+    SPZ_CUDA_TRY(cudaMemcpyAsync(s8 + 3 * pbytes, Lr->counters, 8 * sizeof(int64_t), cudaMemcpyDeviceToDevice, Lr->stream));
+    SPZ_CUDA_TRY(cudaMemcpyAsync(s8 + 3 * pbytes + 8 * sizeof(int64_t), Lr->d_flag, sizeof(int), cudaMemcpyDeviceToDevice, Lr->stream));
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  spz_status st = SPZ_OK;
+  double best_fps = -1.0, peak_fps = 0.0;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) st = fail(SPZ_ECUDA, "spz_tune_batch: events");
+  for (int i = 0; i < n && st == SPZ_OK; ++i) {
+    const int64_t B = ladder[i];
+    // at least one untimed step: the plan and CUDA graph of this B are built outside the timed region
+    if ((st = spz_update(Lr, B, std::max<int64_t>(warmup, 1), nullptr)) != SPZ_OK) break;
+    if ((st = prepare(Lr, B)) != SPZ_OK) break;  // plan + graph before the timed region
+    if (cudaEventRecord(e0, Lr->stream) != cudaSuccess) { st = fail(SPZ_ECUDA, "spz_tune_batch: event record"); break; }
+    if ((st = spz_update_async(Lr, B, steps)) != SPZ_OK) break;
+    if (cudaEventRecord(e1, Lr->stream) != cudaSuccess) { st = fail(SPZ_ECUDA, "spz_tune_batch: event record"); break; }
+    if ((st = update_finish(Lr, nullptr)) != SPZ_OK) break;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    spz_tune_point& pt = out[(*n_out)++];
+    pt.batch = B;
+    pt.ms_per_update = (double)ms / (double)steps;
+    pt.updates_per_s = 1e3 / pt.ms_per_update;
+    pt.frames_per_s = (double)B * pt.updates_per_s;
+    const bool ok_hz = pt.updates_per_s >= min_update_hz;
+    if (ok_hz && pt.frames_per_s > best_fps) {
+      best_fps = pt.frames_per_s;
+      *best = B;
+    }
+    peak_fps = std::max(peak_fps, pt.frames_per_s);
+    if (!ok_hz || pt.frames_per_s < peak_fps * (1.0 - tol)) break;  // below the floor, or past the peak
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (restore) {
+    cudaStreamSynchronize(Lr->stream);
+    uint8_t* s8 = static_cast<uint8_t*>(snap);
+    cudaMemcpyAsync(Lr->P, s8, pbytes, cudaMemcpyDeviceToDevice, Lr->stream);
+    cudaMemcpyAsync(Lr->Mo, s8 + pbytes, pbytes, cudaMemcpyDeviceToDevice, Lr->stream);
+    cudaMemcpyAsync(Lr->Vo, s8 + 2 * pbytes, pbytes, cudaMemcpyDeviceToDevice, Lr->stream);
+    cudaMemcpyAsync(Lr->counters, s8 + 3 * pbytes, 8 * sizeof(int64_t), cudaMemcpyDeviceToDevice, Lr->stream);
+    cudaMemcpyAsync(Lr->d_flag, s8 + 3 * pbytes + 8 * sizeof(int64_t), sizeof(int), cudaMemcpyDeviceToDevice, Lr->stream);
+    spz_status rs = refresh_shadows(Lr);
+    if (cudaStreamSynchronize(Lr->stream) != cudaSuccess && st == SPZ_OK) st = fail(SPZ_ECUDA, "spz_tune_batch: restore");
+    cudaFree(snap);
+    Lr->ctr_cached = false;
+    if (st == SPZ_OK) st = rs;
+  }
+  return st;
+}
+
 spz_status spz_get_counters(spz_learner* Lr, int64_t* step, int64_t* t_critic, int64_t* t_actor, int64_t* t_alpha) {
   if (!Lr) return fail(SPZ_EINVAL, "spz_get_counters: NULL learner");
   DeviceGuard dg(Lr->device);

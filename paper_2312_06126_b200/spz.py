@@ -33,7 +33,7 @@ EXPORTS = [
     "spz_update", "spz_update_async", "spz_update_wait", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
     "spz_diag_gemm_bf16", "spz_diag_gemm_f32", "spz_split_exchange", "spz_diag_tc_trace",
-    "spz_policy_create", "spz_policy_load", "spz_policy_act", "spz_policy_destroy",
+    "spz_policy_create", "spz_policy_load", "spz_policy_act", "spz_policy_destroy", "spz_tune_batch",
 ]
 
 
@@ -48,6 +48,11 @@ class spz_policy_desc(ctypes.Structure):
                 ("obs_dim", ctypes.c_int32), ("act_dim", ctypes.c_int32), ("hidden", ctypes.c_int32),
                 ("n_hidden", ctypes.c_int32), ("max_batch", ctypes.c_int64), ("device", ctypes.c_int32),
                 ("log_std_min", ctypes.c_double), ("log_std_max", ctypes.c_double), ("expl_noise", ctypes.c_double)]
+
+
+class spz_tune_point(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int64), ("updates_per_s", ctypes.c_double), ("frames_per_s", ctypes.c_double),
+                ("ms_per_update", ctypes.c_double)]
 
 
 class spz_replay_desc(ctypes.Structure):
@@ -134,6 +139,8 @@ def lib():
             "spz_policy_load": (ctypes.c_int, [P, P, I64, ctypes.POINTER(U64)]),
             "spz_policy_act": (ctypes.c_int, [P, I64, P, I32, U64, U64, P]),
             "spz_policy_destroy": (None, [P]),
+            "spz_tune_batch": (ctypes.c_int, [P, ctypes.POINTER(I64), I32, I64, I64, D, D, I32,
+                                              ctypes.POINTER(spz_tune_point), ctypes.POINTER(I32), ctypes.POINTER(I64)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -412,6 +419,9 @@ class Learner:
     def launches_per_step(self, batch):
         return spz_learner_launches_per_step(self.h, batch)
 
+    def tune_batch(self, ladder, warmup=3, steps=20, min_update_hz=0.0, tol=0.05, restore=True):
+        return spz_tune_batch(self.h, ladder, warmup, steps, min_update_hz, tol, restore)
+
     def close(self):
         if self.h:
             spz_learner_destroy(self.h)
@@ -478,3 +488,17 @@ class Policy:
             self.close()
         except Exception:
             pass
+
+
+# ----------------------------------------------------------------------------- batch-size adaptation (f3)
+
+def spz_tune_batch(learner, ladder, warmup=3, steps=20, min_update_hz=0.0, tol=0.05, restore=True):
+    """Returns (best_batch, [dict(batch, updates_per_s, frames_per_s, ms_per_update), ...])."""
+    n = len(ladder)
+    lad = (ctypes.c_int64 * n)(*ladder)
+    pts = (spz_tune_point * n)()
+    n_out, best = ctypes.c_int32(), ctypes.c_int64()
+    _check(lib().spz_tune_batch(learner, lad, n, warmup, steps, min_update_hz, tol, 1 if restore else 0, pts,
+                                ctypes.byref(n_out), ctypes.byref(best)))
+    return best.value, [dict(batch=p.batch, updates_per_s=p.updates_per_s, frames_per_s=p.frames_per_s,
+                             ms_per_update=p.ms_per_update) for p in pts[:n_out.value]]

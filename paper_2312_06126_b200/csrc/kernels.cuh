@@ -192,7 +192,8 @@ __device__ __forceinline__ void block_stats(double (&v)[NSTAT], double* __restri
 // then the critic head backward for those rows: dZ_L[r, n] = g_q[r] w_out[n] 1[A_L[r, n] > 0].
 // Loss statistics: per-block partials; the last block to finish sums them in block order into
 // `totals` (this rank's loss totals; all-reduced across a row-sharded group).
-constexpr int LOSS_ROWS = 32, LOSS_NT = 256, LOSS_RPW = LOSS_ROWS / (LOSS_NT / 32);  // rows per warp
+constexpr int LOSS_NT = 256, LOSS_WARPS = LOSS_NT / 32;
+constexpr int LOSS_MIN_ROWS = LOSS_WARPS;  // rows per block at RPW = 1 (sizes the statistics partials)
 
 struct LossArgs {
   const float *qt1, *qt2, *q1, *q2, *logp2, *logp, *r, *d, *log_alpha;
@@ -233,8 +234,9 @@ __device__ __forceinline__ float ld_q(const float* __restrict__ q, int64_t j, in
 // then writes its chunk of dZ_L, otherwise critic_dz_kernel does that afterwards.  All of a warp's
 // loads are issued before any of its arithmetic.  Lane 0 accumulates the statistics of the warp's
 // rows in row order; the block partial sums the warps in order.
-template <typename T, bool DZ>
+template <typename T, bool DZ, int LOSS_RPW>
 __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_constant__ LossArgs a) {
+  constexpr int LOSS_ROWS = LOSS_WARPS * LOSS_RPW;
   pdl_wait();
   pdl_launch();
   __shared__ double red[LOSS_NT / 32][NSTAT];

@@ -62,9 +62,9 @@ struct Op {
   int launches = 1;  // kernels this op launches
 };
 
-// diagnostics: SPZ_DZ_FUSED=1 writes dZ_L inside critic_loss_kernel (h <= 256) instead of critic_dz_kernel
-static bool dz_fused_env() {
-  const char* e = std::getenv("SPZ_DZ_FUSED");
+// diagnostics: SPZ_DZ_SPLIT=1 writes dZ_L in critic_dz_kernel at every width (h <= 256: in the loss kernel)
+static bool dz_split_env() {
+  const char* e = std::getenv("SPZ_DZ_SPLIT");
   return e && e[0] == '1';
 }
 
@@ -678,7 +678,11 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       }
     }
     // ---- a4/a5: Bellman target, losses, head gradients, this rank's loss totals; a6 head backward
-    const int nblk = (int)cdiv(Bl, LOSS_ROWS);
+    // dZ_L written by the loss kernel itself (one row per warp) at h <= 256 up to 16K local rows (WLK
+    // 109.1 -> 108.2 us); larger batches do better with the separate critic_dz_kernel (ANT 319.5 -> 315.4 us)
+    const bool dz_in_loss = h <= 256 && Bl <= 16384 && !dz_split_env();
+    const int loss_rpw = dz_in_loss ? 1 : 4;
+    const int nblk = (int)cdiv(Bl, LOSS_WARPS * loss_rpw);
     {
       LossArgs la{};
       la.qp = qparts;
@@ -722,17 +726,16 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       la.actor_rows = do_actor;
       la.h = h;
       la.ld = h;
-      // dZ_L is written by critic_dz_kernel (one thread per 8-column chunk: the loss kernel's
-      // warp-per-row layout has too few stores in flight at large batches -- ANT 55 us)
-      const bool dz_sep = (h > 256 || !dz_fused_env()) && (do_critic || do_actor);
+      // h <= 256: dZ_L written by the loss kernel (one row per warp); wider rows: critic_dz_kernel
+      const bool dz_sep = !dz_in_loss && (do_critic || do_actor);
       if (!lfused) {  // (the fused critic forward with loss groups computes all of this itself)
-        if (dz_sep)
+        if (!dz_in_loss)
           ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
-                           return launch_pdl(critic_loss_kernel<T, false>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
+                           return launch_pdl(critic_loss_kernel<T, false, 4>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
                          }});
         else
           ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
-                           return launch_pdl(critic_loss_kernel<T, true>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
+                           return launch_pdl(critic_loss_kernel<T, true, 1>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
                          }});
       }
       if (dz_sep && !lfused) {
@@ -1359,7 +1362,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   for (float** f : {&Lr->cache.u, &Lr->cache.a, &Lr->cache.eps, &Lr->cache.sig, &Lr->cache.l})
     SPZ_TRY(dalloc(Lr.get(), (void**)f, Bm * m * sizeof(float)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->idx, Bm * sizeof(int32_t)));
-  Lr->max_stat_blocks = (int)cdiv(Bm, LOSS_ROWS);
+  Lr->max_stat_blocks = (int)cdiv(Bm, LOSS_MIN_ROWS);
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->stat_partials, (size_t)Lr->max_stat_blocks * NSTAT * sizeof(double)));
   {
     auto reg = [&](const std::string& n, void* p, size_t bytes, int es) { Lr->debug.push_back({n, p, bytes, es}); };

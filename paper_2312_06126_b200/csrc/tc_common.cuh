@@ -115,6 +115,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v0)[16], float
   }
 }
 
+// four single-column loads (columns c0 .. c0 + 3 of this warp's lanes, any alignment), one wait
+__device__ __forceinline__ void tmem_ld1x4(uint32_t taddr, float (&v)[4]) {
+  uint32_t r[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[i]) : "r"(taddr + (uint32_t)i));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]) : : "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&p);

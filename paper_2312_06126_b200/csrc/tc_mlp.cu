@@ -315,7 +315,11 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
   uint64_t* h_full = acc_empty + 2;
   uint64_t* x_full = h_full + 1;
   uint64_t* x_empty = x_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
+  // actor: the head weights (<= 16 KB) are loaded into the input-tile region once layer 0 has consumed
+  // it, early in the unit and outside the stage ring (whose slots free only as layer 1 completes)
+  uint64_t* hw_full = x_empty + 1;
+  uint64_t* hw_empty = hw_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hw_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TSU = p.total_su;
@@ -337,6 +341,8 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
     mbar_init(h_full, 1);
     mbar_init(x_full, 1);
     mbar_init(x_empty, 1);
+    mbar_init(hw_full, 1);
+    mbar_init(hw_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -349,13 +355,42 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();
+  // Everything above overlapped the previous kernel (PDL).  The producer also issues the first ring
+  // stages before its wait: they hold weight slabs only, written by the optimizer at least two
+  // kernels back -- complete before the previous kernel passed its own wait, which precedes its
+  // launch_dependents -- so they do not depend on the previous kernel.
+  if (!(warp == 0 && lane == 0)) pdl_wait();
   pdl_launch();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer: the input tile of each unit into Xs (freed by the MMA after
       //                  layer 0), every layer's weight slabs through the stage ring
+      int pre = 0;  // ring stages issued before the PDL wait
+      {
+        bool stop = false;
+        for (int su = blockIdx.x; su < TSU && !stop; su += gridDim.x) {
+          const int k = su_kind(p, su);
+          for (int j = 0; j < p.gn[k] && !stop; ++j) {
+            const int g = p.gpass[k][j];
+            for (int l = 0; l < NMMA && !stop; ++l) {
+              if (ACTOR && l == L) continue;  // head weights go through the input-tile region
+              const int nkb = l == 0 ? p.k0 / MBK : H / MBK;
+              const int nrows = H;
+              for (int kb = 0; kb < nkb; ++kb) {
+                if (pre == NS) {
+                  stop = true;
+                  break;
+                }
+                mbar_expect_tx(&full[pre], (uint32_t)nrows * MBK * 2);
+                tma_load_2d(smem + pre * STAGE, &p.tw[g][l], &full[pre], kb * MBK, 0);
+                ++pre;
+              }
+            }
+          }
+        }
+      }
+      pdl_wait();
       int kg = 0, ui = 0;
       for (int su = blockIdx.x; su < TSU; su += gridDim.x) {
         const int k = su_kind(p, su);
@@ -365,13 +400,22 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
           const int nx = p.k0 / MBK;
           for (int l = 0; l < NMMA; ++l) {
             if (l == 0) {
-              mbar_wait(x_empty, ((uint32_t)ui & 1u) ^ 1u);
+              // the region is free once the previous unit's head MMAs (actor) / layer 0 (critic) are done
+              mbar_wait(ACTOR ? hw_empty : x_empty, ((uint32_t)ui & 1u) ^ 1u);
               mbar_expect_tx(x_full, (uint32_t)nx * MA_BYTES);
               for (int kb = 0; kb < nx; ++kb) tma_load_2d(Xs + kb * MA_BYTES, &p.tx[g], x_full, kb * MBK, m0);
             }
+            if (ACTOR && l == L) {
+              // head weights into the input-tile region as soon as layer 0 has consumed the input tile
+              mbar_wait(x_empty, (uint32_t)ui & 1u);
+              mbar_expect_tx(hw_full, (uint32_t)(H / MBK) * p.nh * 128);
+              for (int kb = 0; kb < H / MBK; ++kb) tma_load_2d(Xs + kb * p.nh * 128, &p.tw[g][l], hw_full, kb * MBK, 0);
+              continue;
+            }
             const int nkb = l == 0 ? nx : H / MBK;
-            const int nrows = (ACTOR && l == L) ? p.nh : H;
+            const int nrows = H;
             for (int kb = 0; kb < nkb; ++kb, ++kg) {
+              if (kg < pre) continue;  // issued before the PDL wait
               const int s = kg % NS;
               mbar_wait(&empty[s], ((uint32_t)(kg / NS) & 1u) ^ 1u);
               mbar_expect_tx(&full[s], (uint32_t)nrows * MBK * 2);
@@ -406,6 +450,24 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
           if (l == 0) {
             mbar_wait(x_full, (uint32_t)ui & 1u);
             tc_fence_after();
+          }
+          if (ACTOR && l == L) {
+            // head: B from the input-tile region (loaded there after layer 0), not from the ring
+            mbar_wait(hw_full, (uint32_t)ui & 1u);
+            tc_fence_after();
+            mtrace(p.trace, ui, l, 4);
+            mtrace(p.trace, ui, l, 5);
+            for (int kb = 0; kb < nkb; ++kb) {
+              const uint32_t sB = sX + kb * p.nh * 128;
+              const uint32_t aBase = sH + kb * 16384;
+#pragma unroll
+              for (int kk = 0; kk < MBK / 16; ++kk)
+                umma_bf16(acc, desc_kmajor(aBase, kk), desc_kmajor(sB, kk), idesc, (kb | kk) != 0 ? 1u : 0u);
+            }
+            umma_commit(hw_empty);      // the region may take the next unit's input tile
+            umma_commit(&acc_full[b]);  // head complete
+            mtrace(p.trace, ui, l, 1);
+            continue;
           }
           for (int kb = 0; kb < nkb; ++kb, ++kg) {
             const int s = kg % NS;
@@ -469,25 +531,33 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
         if (head) {
           // ---- actor head: the two warps of a lane quarter take the row's Philox blocks of 4 actions
           //      alternately (warp hh: blocks hh, hh + 2, ...); SAC log pi = part 0 + part 1 (fixed order)
-          float hrow[32];
-          for (int c = 0; c < p.nh / 16 && c < 2; ++c) {
-            float v[16];
-            tmem_ld16(trow + c * 16, v);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
-          }
-          tc_fence_before();
+          // per Philox block: the 4 mu (or z) and 4 log-sigma columns straight from TMEM into
+          // registers (no per-row array, so nothing is indexed at run time)
           const int mh = p.head.m;
           const bool live = m < d.rows;
-          if (p.head_epi == EPI_SAC_HEAD) {
-            const float lp = live ? sac_head_blocks<__nv_bfloat16>(p.head, d.row0 + m, hrow, hrow + mh, hh, 2) : 0.f;
+          const bool sac = p.head_epi == EPI_SAC_HEAD;
+          float lp = 0.f;
+          for (int c = hh; 4 * c < mh; c += 2) {
+            float v4[4], l4[4] = {0.f, 0.f, 0.f, 0.f};
+            tmem_ld1x4(trow + (uint32_t)(4 * c), v4);
+            if (sac) tmem_ld1x4(trow + (uint32_t)(mh + 4 * c), l4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int i = min(4 * c + k, mh - 1);
+              v4[k] += bias_s[i];
+              l4[k] += sac ? bias_s[mh + i] : 0.f;
+            }
+            if (!live) continue;
+            if (sac) lp += sac_head_block4<__nv_bfloat16>(p.head, d.row0 + m, v4, l4, c);
+            else td3_head_block4<__nv_bfloat16>(p.head, d.row0 + m, v4, c);
+          }
+          tc_fence_before();
+          if (sac) {
             const int pb = dot_tiles & 1;
             dotpart[pb][hh][r] = lp;
             named_bar(2 + q, 64);
             if (hh == 0 && live) sac_head_logp(p.head, d.row0 + m, dotpart[pb][0][r] + dotpart[pb][1][r]);
             ++dot_tiles;
-          } else if (live) {
-            td3_head_blocks<__nv_bfloat16>(p.head, d.row0 + m, hrow, hh, 2);
           }
           __syncwarp();
           if (e == 0 && lane == 0) mtrace(p.trace, ui, l, 3);

@@ -40,6 +40,35 @@ class Ring:
         self.R = record_floats(obs_dim, act_dim)
         self.records = np.zeros((self.C, self.R), dtype=np.float32)
         self.cursor = 0
+        self.tags = None  # transmission-loss accounting (track())
+
+    # ---- experience transmission loss (Table 3 column): the share of
+    #      pushed records overwritten before ever being sampled.  Every resident record carries a
+    #      "sampled" tag; a landing record that overwrites an unsampled one counts it as lost, and so does
+    #      a record that never lands (a push longer than C keeps only its last C records).
+    def track(self):
+        self.tags = np.zeros(self.C, dtype=bool)
+        self.lost = 0
+        self.pushed0 = self.cursor  # pushes before tracking started are not accounted
+
+    def loss_stats(self):
+        """(pushed, lost, resident_unsampled, sampled) since track(); pushed = lost + resident_unsampled + sampled."""
+        pushed = self.cursor - self.pushed0
+        occ = np.arange(self.C) < self.fill
+        # resident records pushed before track() are not counted as pushed
+        first_tracked = max(self.pushed0, self.cursor - self.C)
+        g_slot = np.arange(self.C)
+        resident = 0
+        for s in g_slot[occ]:
+            g = self._global_of_slot(s)
+            if g >= first_tracked and not self.tags[s]:
+                resident += 1
+        return pushed, self.lost, resident, pushed - self.lost - resident
+
+    def _global_of_slot(self, s):
+        """Global index of the record resident in slot s (the most recent g with g mod C = s, g < cursor)."""
+        c = self.cursor
+        return (c - 1) - ((c - 1 - s) % self.C)
 
     @property
     def fill(self):
@@ -63,6 +92,15 @@ class Ring:
         n = rec.shape[0]
         keep = min(n, self.C)  # only the last C records of a push survive
         g = np.arange(first + n - keep, first + n)  # their global indices
+        if self.tags is not None:
+            self.lost += n - keep  # never resident
+            occupied = min(first, self.C)  # slots holding a record before this push
+            for s in np.unique(g % self.C):
+                if s < occupied:
+                    old = (first - 1) - ((first - 1 - s) % self.C)  # the record about to be overwritten
+                    if old >= self.pushed0 and not self.tags[s]:
+                        self.lost += 1
+            self.tags[g % self.C] = False
         self.records[g % self.C] = rec[n - keep:]
         self.cursor += n
         return first
@@ -88,4 +126,6 @@ class Ring:
         if F < gb:
             raise NotEnoughData(f"fill {F} < batch {gb}")
         idx = philox.sample_indices(seed, step, F, batch, row0=row0)
+        if self.tags is not None:
+            self.tags[idx] = True
         return idx, self.unpack(self.records[idx])

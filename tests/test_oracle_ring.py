@@ -74,3 +74,56 @@ def test_sample_repeatable_and_gathers_rows():
     i2, b2 = r.sample(64, 9, 3)
     assert np.array_equal(i1, i2) and np.array_equal(b1["obs"], b2["obs"])
     assert np.array_equal(b1["rew"], i1.astype(np.float32))  # row tag == slot here
+
+
+# ----------------------------------------------------------------------------- transmission loss
+
+def _trl(n, o=2, m=1, seed=0):
+    import synthdata
+    return synthdata.transitions("locomotion", o, m, n, seed=seed)
+
+
+def test_loss_no_sampling_capacity_100_ten_thousand_pushes():
+    # capacity-100 ring, 10^4 pushes, no sampling -> loss 9900 / 10^4 = 99 %
+    r = oring.Ring(2, 1, 100)
+    r.track()
+    for k in range(100):
+        r.push(**_trl(100, seed=k))
+    pushed, lost, resident, sampled = r.loss_stats()
+    assert (pushed, lost, resident, sampled) == (10_000, 9_900, 100, 0)
+
+
+def test_loss_conservation_and_brute_force():
+    # brute force over push sizes (including pushes longer than C) with interleaved sampling: a plain
+    # per-record tag model (every pushed record's fate tracked individually) gives the same counts
+    rng = np.random.default_rng(3)
+    for C in (1, 3, 8):
+        r = oring.Ring(2, 1, C)
+        r.track()
+        fate = {}          # global index -> "resident" | "lost" | "sampled"
+        slot_owner = {}    # slot -> global index resident there
+        g = 0
+        for step in range(40):
+            n = int(rng.integers(0, 3 * C + 1))
+            r.push(**_trl(n, seed=step))
+            for gi in range(g, g + n):
+                s = gi % C
+                prev = slot_owner.get(s)
+                if prev is not None and fate[prev] == "resident":
+                    fate[prev] = "lost"
+                if prev is not None and fate[prev] == "sampled_resident":
+                    fate[prev] = "sampled"
+                slot_owner[s] = gi
+                fate[gi] = "resident"
+            g += n
+            if r.fill and rng.random() < 0.5:
+                B = int(rng.integers(1, r.fill + 1))
+                idx, _ = r.sample(B, 7, step)
+                for s in idx:
+                    gi = slot_owner[int(s)]
+                    if fate[gi] == "resident":
+                        fate[gi] = "sampled_resident"
+        pushed, lost, resident, sampled = r.loss_stats()
+        assert pushed == g == lost + resident + sampled
+        assert lost == sum(v == "lost" for v in fate.values())
+        assert resident == sum(v == "resident" for v in fate.values())

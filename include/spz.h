@@ -93,6 +93,16 @@ spz_status spz_replay_sample(spz_replay* r, int64_t batch, uint64_t seed, uint64
 spz_status spz_replay_info(const spz_replay* r, int64_t* cursor, int64_t* fill, int64_t* capacity);
 /* Device pointer to the record array [C x R] fp32 and R (for zero-copy inspection). */
 spz_status spz_replay_records(const spz_replay* r, const float** records, int32_t* record_floats);
+/* Experience transmission loss (Table 3 column): the fraction of
+ * pushed records overwritten before ever being sampled.  spz_replay_track(r, 1) starts accounting
+ * (a one-bit "sampled" tag per slot, set by every sample -- the learners' gathers and
+ * spz_replay_sample; a push counts each unsampled tracked record it overwrites, and every record
+ * of a push longer than the capacity that never lands); 0 stops it.  Learners pick the change up
+ * at their next update (their plan is rebuilt).  spz_replay_loss reports, since tracking started:
+ * pushed = lost + resident_unsampled + sampled_at_least_once.  SPZ_ESTATE if tracking is
+ * off.  Synchronous.  (Row-sharded learners each mark their own ring replica.) */
+spz_status spz_replay_track(spz_replay* r, int32_t on);
+spz_status spz_replay_loss(spz_replay* r, int64_t* pushed, int64_t* lost, int64_t* resident_unsampled);
 void spz_replay_destroy(spz_replay* r);
 
 /* ------------------------------------------------------------------ learner

@@ -52,6 +52,12 @@ struct spz_replay {
   cudaEvent_t ev_copy = nullptr;       // pinned push: the caller's buffers have been read (H2D done)
   cudaEvent_t ev_pack = nullptr;       // the last push's records are in `rec`
   std::vector<cudaEvent_t> readers;    // one per learner: its last enqueued update (registered at create)
+  // experience transmission loss (spz_replay_track): one "sampled" bit per slot, set by every sample;
+  // a push counts the unsampled records it overwrites (device) and the records that never land (host)
+  uint32_t* tags = nullptr;
+  unsigned long long* d_lost = nullptr;
+  int64_t lost_host = 0, pushed0 = 0;
+  int track_gen = 0;                   // bumped on every spz_replay_track call (learners rebuild their plan)
   std::mutex mu;
   int64_t fill() const { return cursor < C ? cursor : C; }
 };

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ r
                                                      const int64_t* __restrict__ step_p, int64_t row0, int Bl,
                                                      T* __restrict__ Xa, int lda, T* __restrict__ Xc, int ldc,
                                                      float* __restrict__ r, float* __restrict__ d,
-                                                     int32_t* __restrict__ idx_out) {
+                                                     int32_t* __restrict__ idx_out, uint32_t* __restrict__ tags) {
   pdl_wait();
   pdl_launch();
   extern __shared__ float4 sm4[];
@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ r
     const int64_t i = sample_index(seed, step, (uint64_t)(row0 + j0 + threadIdx.x), (uint64_t)fill);
     sidx[threadIdx.x] = i;
     if (idx_out) idx_out[j0 + threadIdx.x] = (int32_t)i;
+    if (tags) atomicOr(&tags[i >> 5], 1u << (i & 31));  // transmission-loss tags (spz_replay_track)
   }
   __syncthreads();
   const int R4 = R >> 2;

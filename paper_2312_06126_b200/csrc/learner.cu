@@ -119,6 +119,7 @@ struct spz_learner {
   int* d_flag = nullptr;
   cudaEvent_t ev_read = nullptr;  // recorded after every enqueued update: ring pushes wait on it
   bool pending = false;           // an update enqueued by spz_update_async not yet waited for
+  int plan_track_gen = 0;         // ring->track_gen the plan's gather was built for
   bool ctr_cached = false;  // h_counters[0..3] / h_flag mirror the device (set by read_counters; cleared while
                             // steps are enqueued): spz_update skips the leading device round trip
   StatsOut* d_stats = nullptr;
@@ -414,10 +415,11 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       T *Xa = static_cast<T*>(Lr->Xa), *Xc = static_cast<T*>(Lr->Xc);
       float *rr = Lr->r, *dd = Lr->d;
       int32_t* idx = Lr->idx;
+      uint32_t* tags = Lr->ring->tags;
       const size_t smem = (size_t)GATHER_ROWS * R * sizeof(float);
       ops.push_back({"gather", [=](cudaStream_t st) {
                        launch_pdl(gather_kernel<T>, dim3((unsigned)cdiv(Bl, GATHER_ROWS)), dim3(256), smem, st, 
-                           rec, R, o, m, fill, seed, stp, row0, Bl, Xa, lda, Xc, ldc, rr, dd, idx);
+                           rec, R, o, m, fill, seed, stp, row0, Bl, Xa, lda, Xc, ldc, rr, dd, idx, tags);
                        return cudaGetLastError();
                      }});
     }
@@ -1117,6 +1119,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
                              }),
               v.end());
   }
+  Lr->plan_track_gen = Lr->ring->track_gen;
   Lr->plan_B = B;
   return SPZ_OK;
 }
@@ -1155,7 +1158,7 @@ static spz_status prepare(spz_learner* Lr, int64_t batch) {
   if (batch < Lr->cfg.world_size) return fail(SPZ_EINVAL, "batch smaller than world_size");
   const int64_t F = Lr->ring->fill();
   if (F < batch) return fail(SPZ_ENODATA, "ring fill " + std::to_string(F) + " < batch " + std::to_string(batch));
-  if (Lr->plan_B != batch) {
+  if (Lr->plan_B != batch || Lr->plan_track_gen != Lr->ring->track_gen) {
     SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
     spz_status s = Lr->bf16 ? build_plan<__nv_bfloat16>(Lr, batch) : build_plan<float>(Lr, batch);
     if (s != SPZ_OK) {

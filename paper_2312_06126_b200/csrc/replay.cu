@@ -33,6 +33,35 @@ __global__ void pack_records_kernel(float* __restrict__ rec, int R, int o, int m
   }
 }
 
+// ------------------------------------------------------------------ transmission-loss accounting
+// A push lands records on slots [slot0, slot0 + n) mod C.  Each landing slot that held a tracked record
+// (slot < occupied; its record global index >= pushed0) whose sampled bit is clear counts one lost
+// record; the bits of the landing slots are then cleared for the new records.  One thread per slot.
+__global__ void loss_account_kernel(uint32_t* __restrict__ tags, int64_t C, int64_t slot0, int64_t n, int64_t occupied,
+                                    int64_t first, int64_t pushed0, unsigned long long* __restrict__ lost) {
+  __shared__ unsigned cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned mine = 0;
+  if (t < n) {
+    const int64_t s = (slot0 + t) % C;
+    if (s < occupied) {
+      const int64_t old = (first - 1) - ((first - 1 - s) % C);  // the record being overwritten
+      const bool sampled = (tags[s >> 5] >> (s & 31)) & 1u;
+      if (old >= pushed0 && !sampled) mine = 1;
+    }
+  }
+  if (mine) atomicAdd(&cnt, 1u);
+  __syncthreads();
+  if (threadIdx.x == 0 && cnt) atomicAdd(lost, (unsigned long long)cnt);
+  // clear after every thread of the block has read its bit (a word may span blocks: clear bit-wise)
+  if (t < n) {
+    const int64_t s = (slot0 + t) % C;
+    atomicAnd(&tags[s >> 5], ~(1u << (s & 31)));
+  }
+}
+
 // ------------------------------------------------------------------ sample (API form)
 // One warp per row group: indices from Philox, 128-bit record loads, scatter to the
 // caller's separate arrays.
@@ -40,7 +69,8 @@ constexpr int SAMPLE_ROWS = 32;
 
 __global__ void __launch_bounds__(256) sample_kernel(const float* __restrict__ rec, int R, int o, int m, int64_t fill,
                                                      uint64_t seed, uint64_t step, int64_t B, int32_t* idx_out,
-                                                     float* obs, float* act, float* rew, float* nobs, float* done) {
+                                                     float* obs, float* act, float* rew, float* nobs, float* done,
+                                                     uint32_t* tags) {
   extern __shared__ float4 sm4[];
   float* sm = reinterpret_cast<float*>(sm4);
   __shared__ int64_t sidx[SAMPLE_ROWS];
@@ -50,6 +80,7 @@ __global__ void __launch_bounds__(256) sample_kernel(const float* __restrict__ r
     const int64_t i = sample_index(seed, step, (uint64_t)(r0 + threadIdx.x), (uint64_t)fill);
     sidx[threadIdx.x] = i;
     if (idx_out) idx_out[r0 + threadIdx.x] = (int32_t)i;
+    if (tags) atomicOr(&tags[i >> 5], 1u << (i & 31));  // sampled at least once
   }
   __syncthreads();
   const int R4 = R >> 2;
@@ -147,8 +178,18 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
     }
     return cudaSuccess;
   };
+  // transmission loss: records that never land, and the unsampled records the landing ones overwrite
+  const auto account = [&]() -> cudaError_t {
+    if (!r->tags || nn == 0) return cudaSuccess;
+    r->lost_host += skip;
+    const int64_t occupied = first_idx < r->C ? first_idx : r->C;
+    loss_account_kernel<<<(unsigned)cdiv(nn, 256), 256, 0, r->stream>>>(r->tags, r->C, start % r->C, nn, occupied,
+                                                                        first_idx, r->pushed0, r->d_lost);
+    return cudaGetLastError();
+  };
   if (src_on_device) {
     SPZ_CUDA_TRY(wait_readers());
+    SPZ_CUDA_TRY(account());
     const int64_t total = nn * R;
     const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
     pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, obs + skip * o, act + skip * m,
@@ -182,6 +223,7 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
     SPZ_CUDA_TRY(h2d(d_done, done, 1));
     SPZ_CUDA_TRY(cudaEventRecord(r->ev_copy, r->stream));
     SPZ_CUDA_TRY(wait_readers());
+    SPZ_CUDA_TRY(account());
     const int64_t total = nn * R;
     const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
     pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, d_obs, d_act, d_rew, d_nobs, d_done);
@@ -217,6 +259,7 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
     }
     // at most two pieces, split at the wrap point
     SPZ_CUDA_TRY(wait_readers());
+    SPZ_CUDA_TRY(account());
     const int64_t slot = start % r->C;
     const int64_t n1 = std::min(nn, r->C - slot);
     SPZ_CUDA_TRY(cudaMemcpyAsync(r->rec + slot * R, s, (size_t)n1 * R * sizeof(float), cudaMemcpyHostToDevice, r->stream));
@@ -240,7 +283,7 @@ spz_status spz_replay_sample(spz_replay* r, int64_t batch, uint64_t seed, uint64
   const unsigned blocks = (unsigned)cdiv(batch, SAMPLE_ROWS);
   const size_t smem = (size_t)SAMPLE_ROWS * r->R * sizeof(float);
   sample_kernel<<<blocks, 256, smem, r->stream>>>(r->rec, r->R, r->o, r->m, F, seed, step, batch, idx, obs, act, rew,
-                                                  next_obs, done);
+                                                  next_obs, done, r->tags);
   SPZ_CUDA_TRY(cudaGetLastError());
   SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
   return SPZ_OK;
@@ -261,6 +304,55 @@ spz_status spz_replay_records(const spz_replay* r, const float** records, int32_
   return SPZ_OK;
 }
 
+spz_status spz_replay_track(spz_replay* r, int32_t on) {
+  if (!r) return fail(SPZ_EINVAL, "spz_replay_track: NULL ring");
+  DeviceGuard dg(r->device);
+  std::lock_guard<std::mutex> lk(r->mu);
+  SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  for (cudaEvent_t e : r->readers) SPZ_CUDA_TRY(cudaEventSynchronize(e));  // no update still marks the old bitmap
+  if (r->tags) cudaFree(r->tags);
+  if (r->d_lost) cudaFree(r->d_lost);
+  r->tags = nullptr;
+  r->d_lost = nullptr;
+  if (on) {
+    const size_t words = (size_t)cdiv(r->C, 32);
+    if (cudaMalloc(&r->tags, words * 4) != cudaSuccess || cudaMalloc(&r->d_lost, 8) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SPZ_ENOMEM, "spz_replay_track: cannot allocate the tag bitmap");
+    }
+    SPZ_CUDA_TRY(cudaMemsetAsync(r->tags, 0, words * 4, r->stream));
+    SPZ_CUDA_TRY(cudaMemsetAsync(r->d_lost, 0, 8, r->stream));
+    SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  }
+  r->lost_host = 0;
+  r->pushed0 = r->cursor;
+  ++r->track_gen;
+  return SPZ_OK;
+}
+
+spz_status spz_replay_loss(spz_replay* r, int64_t* pushed, int64_t* lost, int64_t* resident_unsampled) {
+  if (!r) return fail(SPZ_EINVAL, "spz_replay_loss: NULL ring");
+  if (!r->tags) return fail(SPZ_ESTATE, "spz_replay_loss: tracking is off (spz_replay_track)");
+  DeviceGuard dg(r->device);
+  std::lock_guard<std::mutex> lk(r->mu);
+  for (cudaEvent_t e : r->readers) SPZ_CUDA_TRY(cudaEventSynchronize(e));
+  SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  unsigned long long dl = 0;
+  std::vector<uint32_t> bits((size_t)cdiv(r->C, 32));
+  SPZ_CUDA_TRY(cudaMemcpy(&dl, r->d_lost, 8, cudaMemcpyDeviceToHost));
+  SPZ_CUDA_TRY(cudaMemcpy(bits.data(), r->tags, bits.size() * 4, cudaMemcpyDeviceToHost));
+  int64_t res = 0;
+  const int64_t c = r->cursor, F = r->fill();
+  for (int64_t s = 0; s < F; ++s) {
+    const int64_t g = (c - 1) - ((c - 1 - s) % r->C);  // global index of the resident record
+    if (g >= r->pushed0 && !((bits[s >> 5] >> (s & 31)) & 1u)) ++res;
+  }
+  if (pushed) *pushed = c - r->pushed0;
+  if (lost) *lost = (int64_t)dl + r->lost_host;
+  if (resident_unsampled) *resident_unsampled = res;
+  return SPZ_OK;
+}
+
 void spz_replay_destroy(spz_replay* r) {
   if (!r) return;
   {
@@ -269,6 +361,8 @@ void spz_replay_destroy(spz_replay* r) {
     cudaFree(r->rec);
     if (r->staging) cudaFreeHost(r->staging);
     if (r->dstage) cudaFree(r->dstage);
+    if (r->tags) cudaFree(r->tags);
+    if (r->d_lost) cudaFree(r->d_lost);
     cudaEventDestroy(r->ev_copy);
     cudaEventDestroy(r->ev_pack);
     cudaStreamDestroy(r->stream);

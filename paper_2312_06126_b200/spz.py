@@ -34,6 +34,7 @@ EXPORTS = [
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
     "spz_diag_gemm_bf16", "spz_diag_gemm_f32", "spz_split_exchange", "spz_diag_tc_trace",
     "spz_policy_create", "spz_policy_load", "spz_policy_act", "spz_policy_destroy", "spz_tune_batch",
+    "spz_replay_track", "spz_replay_loss",
 ]
 
 
@@ -139,6 +140,8 @@ def lib():
             "spz_policy_load": (ctypes.c_int, [P, P, I64, ctypes.POINTER(U64)]),
             "spz_policy_act": (ctypes.c_int, [P, I64, P, I32, U64, U64, P]),
             "spz_policy_destroy": (None, [P]),
+            "spz_replay_track": (ctypes.c_int, [P, I32]),
+            "spz_replay_loss": (ctypes.c_int, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
             "spz_tune_batch": (ctypes.c_int, [P, ctypes.POINTER(I64), I32, I64, I64, D, D, I32,
                                               ctypes.POINTER(spz_tune_point), ctypes.POINTER(I32), ctypes.POINTER(I64)]),
         }
@@ -354,6 +357,16 @@ class Replay:
 
     def info(self):
         return spz_replay_info(self.h)
+
+    def track(self, on=True):
+        """Start (or stop) experience-transmission-loss accounting (include/spz.h)."""
+        _check(lib().spz_replay_track(self.h, 1 if on else 0))
+
+    def loss(self):
+        """(pushed, lost, resident_unsampled) since track(); lost / pushed is the transmission loss."""
+        p, l, r = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().spz_replay_loss(self.h, ctypes.byref(p), ctypes.byref(l), ctypes.byref(r)))
+        return p.value, l.value, r.value
 
     def close(self):
         if self.h:

@@ -1,0 +1,65 @@
+"""Experience transmission loss on the device ring against the
+oracle ring's tag model: exact integer counts, with pushes from host / pinned / device memory and the
+learner's own sampling marking the tags."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import synthdata  # noqa: E402
+from oracle import ring as oring  # noqa: E402
+from paper_2312_06126_b200 import spz  # noqa: E402
+
+
+def test_loss_capacity_100_no_sampling():
+    g = spz.Replay(2, 1, 100)
+    g.track()
+    for k in range(100):
+        g.push(**synthdata.transitions("locomotion", 2, 1, 100, seed=k))
+    assert g.loss() == (10_000, 9_900, 100)
+
+
+@pytest.mark.parametrize("src", ["host", "pinned", "device"])
+def test_loss_matches_oracle_with_learner_sampling(src):
+    o, m, C, B = 22, 6, 3000, 512
+    g = spz.Replay(o, m, C)
+    r = oring.Ring(o, m, C)
+    first = synthdata.transitions("locomotion", o, m, C)
+    g.push(**first)
+    r.push(**first)
+    g.track()
+    r.track()
+    lrn = spz.Learner(g, precision="bf16", hidden=64, n_hidden=2, max_batch=B)
+    rng = np.random.default_rng(0)
+    for k in range(12):
+        n = int(rng.integers(0, 2 * C))  # sometimes longer than the ring
+        tr = synthdata.transitions("locomotion", o, m, n, seed=50 + k)
+        r.push(**tr)
+        if src == "pinned":
+            tr = {a: torch.from_numpy(v).pin_memory().numpy() for a, v in tr.items()}
+        if src == "device" and n:
+            g.push(**{a: torch.from_numpy(v).cuda() for a, v in tr.items()}, src_on_device=True)
+        else:
+            g.push(**tr)
+        lrn.update(B, 1)                      # samples spz_replay_sample(ring, B, seed, k)
+        r.sample(B, synthdata.SAMPLE_SEED, k)  # the same indices mark the oracle's tags
+    pushed, lost, resident, _ = r.loss_stats()
+    assert g.loss() == (pushed, lost, resident)
+    assert lost > 0 and resident > 0
+
+
+def test_track_errors_and_restart():
+    g = spz.Replay(3, 1, 50)
+    with pytest.raises(spz.SpzError) as e:
+        g.loss()
+    assert e.value.status == spz.SPZ_ESTATE
+    g.push(**synthdata.transitions("pendulum", 3, 1, 80))
+    g.track()
+    assert g.loss() == (0, 0, 0)  # records pushed before tracking are not accounted
+    g.push(**synthdata.transitions("pendulum", 3, 1, 10))
+    assert g.loss() == (10, 0, 10)
+    g.track(False)
+    with pytest.raises(spz.SpzError):
+        g.loss()

@@ -105,6 +105,15 @@ def class_bytes(w, B, n_params):
             "adam_polyak": n_params * 28 + n_params * 2 // 3 * 8}
 
 
+# the paper's network-update frame rate for Walker2D SAC at its default batch (~8192):
+# 3.7E+5 Hz -- on a GTX 1060, network size unstated: context, not the target
+PAPER_WALKER_HZ = 3.7e5
+
+
+def vs_baseline(w, value):
+    return value / PAPER_WALKER_HZ if w.name == "walker" else None
+
+
 def traffic(workload, kernel):
     """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full capture, or None."""
     p = os.path.join(ROOT, "profiles", "r01_traffic.json")
@@ -195,7 +204,7 @@ def reference_arm(a, w, B):
     rate, cores, dt = oracle_rate(w, B, steps)
     line = {"metric": METRIC, "value": rate, "unit": "frames/s", "impl": "reference", "n_gpus": a.gpus,
             "steps": steps, "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": vs_baseline(w, rate), "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "global_batch": B, "algo": w.algo, "hidden": f"{w.n_hidden}x{w.hidden}",
                        "obs_dim": w.obs_dim, "act_dim": w.act_dim, "ring": min(w.capacity, 1_000_000)},
             "cpu_baseline": {"value": rate, "unit": "frames/s", "cores": cores, "kind": "oracle",
@@ -366,7 +375,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_per_step, "updates_per_s": 1e3 / ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": a.precision, "data": "synthetic",
+            "scaling": "weak", "vs_baseline": vs_baseline(w, value), "dtype": a.precision, "data": "synthetic",
             "config": {"workload": w.name, "global_batch": GB if (dp or split) else B * world,
                        "batch_per_gpu": B if not split else GB // max(1, (world // 2)), "algo": w.algo,
                        "mode": ("dp-nccl" if dp else "split-nccl" if split else "replicas") if world > 1 else "single",

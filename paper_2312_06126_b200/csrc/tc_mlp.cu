@@ -634,6 +634,262 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
 int g_mtrace_mode = 0;
 long g_mtrace_count = 0;
 
+// ---------------------------------------------------------------------------------------------------
+// Critic forward with two row blocks in flight per CTA ("pair" schedule).  The plain schedule above
+// runs the layers of one block back to back, so the tensor pipe idles during every epilogue and
+// the epilogue warps idle during every layer's MMAs (~7.5 us per block at WLK, ~2.6 blocks per
+// CTA).  Here the blocks of a CTA are taken in pairs (A, B) and interleaved layer by layer --
+//   MMA:      L0(A) L0(B) L1(A) L1(B) ...        epilogue: E0(A) E0(B) E1(A) E1(B) ...
+// -- so E0(B) runs under L1(A), E1(A) under L1(B), and so on.  Each block of a pair owns a TMEM
+// accumulator buffer and a hidden buffer H (two H buffers: 2 x 64 KB at h = 256, which leaves room
+// for a 2-stage weight ring).  Critic passes only (no actor head, no fused loss groups).
+template <int H>
+__global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_pair_kernel(const __grid_constant__ MlpParams p) {
+  constexpr int STAGE = H * MBK * 2;
+  constexpr uint32_t BUF = H < 32 ? 32 : H;
+  constexpr uint32_t TMEM_COLS = 2 * BUF <= 64 ? 64 : 2 * BUF <= 128 ? 128 : 2 * BUF <= 256 ? 256 : 512;
+  constexpr int SLABS = H / 64;
+  constexpr int CPW = H / 16 / 2;
+  constexpr int NB = CPW / 2;
+  constexpr int SLICE = CPW * 16;
+  constexpr int HBYTES = SLABS * 16384;
+  constexpr uint32_t IDESC_H = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(H >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
+  __shared__ __align__(16) float bias_w[M_EPI_WARPS][SLICE];
+  __shared__ __align__(16) float dotw_w[M_EPI_WARPS][SLICE];
+  __shared__ float dotpart[2][2][MBM];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int NS = p.stages;
+  uint8_t* Xs = smem + NS * STAGE;
+  uint8_t* Hs0 = Xs + (p.k0 / MBK) * MA_BYTES;  // H buffer of pair slot x: Hs0 + x * HBYTES
+  uint64_t* full = reinterpret_cast<uint64_t*>(Hs0 + 2 * HBYTES);
+  uint64_t* empty = full + MSTAGES;
+  uint64_t* acc_full = empty + MSTAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2]
+  uint64_t* h_full = acc_empty + 2;      // [2]
+  uint64_t* x_full = h_full + 2;
+  uint64_t* x_empty = x_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int TSU = p.total_su, L = p.L;
+  const int U = TSU > (int)blockIdx.x ? (TSU - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;  // this CTA's blocks
+  const int nx = p.k0 / MBK;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < p.n_pass; ++i) {
+      tma_prefetch(&p.tx[i]);
+      for (int l = 0; l < L; ++l) tma_prefetch(&p.tw[i][l]);
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], M_EPI_WARPS);
+      mbar_init(&h_full[b], 1);
+    }
+    mbar_init(x_full, 1);
+    mbar_init(x_empty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_launch();
+
+  // block i of this CTA: super-unit su = blockIdx.x + i * gridDim.x (every group has one pass)
+  auto block_of = [&](int i, int& g, int& m0) {
+    const int su = (int)blockIdx.x + i * (int)gridDim.x;
+    const int k = su_kind(p, su);
+    g = p.gpass[k][0];
+    m0 = (su - p.su0[k]) * MBM;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- producer: per pair, layer by layer, block by block (the MMA's order)
+      int kg = 0, xc = 0;
+      for (int i0 = 0; i0 < U; i0 += 2) {
+        const int nu = min(2, U - i0);
+        for (int l = 0; l < L; ++l)
+          for (int x = 0; x < nu; ++x) {
+            int g, m0;
+            block_of(i0 + x, g, m0);
+            if (l == 0) {
+              mbar_wait(x_empty, ((uint32_t)xc & 1u) ^ 1u);
+              mbar_expect_tx(x_full, (uint32_t)nx * MA_BYTES);
+              for (int kb = 0; kb < nx; ++kb) tma_load_2d(Xs + kb * MA_BYTES, &p.tx[g], x_full, kb * MBK, m0);
+              ++xc;
+            }
+            const int nkb = l == 0 ? nx : H / MBK;
+            for (int kb = 0; kb < nkb; ++kb, ++kg) {
+              const int s = kg % NS;
+              mbar_wait(&empty[s], ((uint32_t)(kg / NS) & 1u) ^ 1u);
+              mbar_expect_tx(&full[s], (uint32_t)H * MBK * 2);
+              tma_load_2d(smem + s * STAGE, &p.tw[g][l], &full[s], kb * MBK, 0);
+            }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int kg = 0, xc = 0;
+      int ae[2] = {0, 0}, hf[2] = {0, 0};  // acc_empty / h_full waits per buffer
+      const uint32_t sX = smem_u32(Xs);
+      for (int i0 = 0; i0 < U; i0 += 2) {
+        const int nu = min(2, U - i0);
+        for (int l = 0; l < L; ++l)
+          for (int x = 0; x < nu; ++x) {
+            const uint32_t acc = tmem + (uint32_t)x * BUF;
+            const uint32_t sH = smem_u32(Hs0 + x * HBYTES);
+            if (l == 0) {
+              mbar_wait(&acc_empty[x], ((uint32_t)ae[x] & 1u) ^ 1u);  // the previous pair's block x drained
+              ++ae[x];
+              tc_fence_after();
+              mbar_wait(x_full, (uint32_t)xc & 1u);
+              ++xc;
+              tc_fence_after();
+            } else {
+              mbar_wait(&h_full[x], (uint32_t)hf[x] & 1u);  // H_x holds layer l-1 of block x
+              ++hf[x];
+              tc_fence_after();
+            }
+            const int nkb = l == 0 ? nx : H / MBK;
+            for (int kb = 0; kb < nkb; ++kb, ++kg) {
+              const int s = kg % NS;
+              mbar_wait(&full[s], (uint32_t)(kg / NS) & 1u);
+              tc_fence_after();
+              const uint32_t sB = smem_u32(smem + s * STAGE);
+              const uint32_t aBase = l == 0 ? sX + kb * MA_BYTES : sH + kb * 16384;
+#pragma unroll
+              for (int kk = 0; kk < MBK / 16; ++kk)
+                umma_bf16(acc, desc_kmajor(aBase, kk), desc_kmajor(sB, kk), IDESC_H, (kb | kk) != 0 ? 1u : 0u);
+              umma_commit(&empty[s]);
+            }
+            if (l == 0) umma_commit(x_empty);
+            umma_commit(&acc_full[x]);
+          }
+      }
+    }
+  } else {
+    // ---------------- epilogue
+    const int e = warp - 2, q = warp & 3, hh = e >> 2;
+    const int c_lo = hh * CPW;
+    const int r = q * 32 + lane;
+    float* bias_s = bias_w[e];
+    float* dot_s = dotw_w[e];
+    int af[2] = {0, 0}, dot_tiles = 0;
+    for (int i0 = 0; i0 < U; i0 += 2) {
+      const int nu = min(2, U - i0);
+      for (int l = 0; l < L; ++l)
+        for (int x = 0; x < nu; ++x) {
+          int g, m0;
+          block_of(i0 + x, g, m0);
+          const MlpDev& d = p.d[g];
+          const int m = m0 + r;
+          const bool last_hidden = l == L - 1;
+          const bool has_dot = last_hidden && d.dot_out != nullptr;
+          uint8_t* Hx = Hs0 + x * HBYTES;
+          const uint32_t trow = tmem + (uint32_t)x * BUF + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+          for (int c = lane; c < SLICE; c += 32) {
+            bias_s[c] = d.bias[l][c_lo * 16 + c];
+            dot_s[c] = has_dot ? d.dot_w[c_lo * 16 + c] : 0.f;
+          }
+          __syncwarp();
+          mbar_wait(&acc_full[x], (uint32_t)af[x] & 1u);
+          ++af[x];
+          tc_fence_after();
+          // H_x must be free of the TMA stores issued from it (conservatively: every store so far)
+          if (e == 0 && lane == 0) bulk_wait_read0();
+          named_bar(1, M_EPI_WARPS * 32);
+          uint32_t mw[NB > 0 ? NB : 1];
+          const bool want_mask = d.mask[l] != nullptr;
+          float dot;
+          if (has_dot) {
+            dot = want_mask ? hidden_epi<NB, true, true>(trow, c_lo, r, Hx, bias_s, dot_s, mw)
+                            : hidden_epi<NB, false, true>(trow, c_lo, r, Hx, bias_s, dot_s, mw);
+          } else {
+            dot = want_mask ? hidden_epi<NB, true, false>(trow, c_lo, r, Hx, bias_s, dot_s, mw)
+                            : hidden_epi<NB, false, false>(trow, c_lo, r, Hx, bias_s, dot_s, mw);
+          }
+          tc_fence_before();
+          fence_async_smem();
+          named_bar(1, M_EPI_WARPS * 32);
+          if (e == 0 && lane == 0) {
+            if (l + 1 < L) mbar_arrive(&h_full[x]);
+            if (d.store[l]) {
+#pragma unroll
+              for (int sl = 0; sl < SLABS; ++sl) tma_store_2d(&p.tact[g][l], Hx + sl * 16384, sl * 64, m0);
+              bulk_commit();
+            }
+          }
+          if (d.mask[l] != nullptr && m < d.rows) {
+            uint32_t* dst = d.mask[l] + (int64_t)m * p.mask_ld + (c_lo * 16) / 32;
+            if constexpr (NB == 4) {
+              *reinterpret_cast<uint4*>(dst) = make_uint4(mw[0], mw[1 % NB], mw[2 % NB], mw[3 % NB]);
+            } else if constexpr (NB == 2) {
+              *reinterpret_cast<uint2*>(dst) = make_uint2(mw[0], mw[1 % NB]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < NB; ++i) dst[i] = mw[i];
+            }
+          }
+          if (has_dot) {
+            const int pb = dot_tiles & 1;
+            dotpart[pb][hh][r] = dot;
+            named_bar(2 + q, 64);
+            const float qv = (dotpart[pb][0][r] + dotpart[pb][1][r]) + d.dot_b[0];
+            if (hh == 0 && m < d.rows) d.dot_out[m] = qv;
+            ++dot_tiles;
+          }
+          if (last_hidden) {  // accumulator x drained for this block
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[x]);
+          }
+        }
+    }
+  }
+  if (warp >= 2 && lane == 0) bulk_wait_all();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+template <int H>
+cudaError_t launch_mlp_pair(MlpParams& p, cudaStream_t st) {
+  constexpr int STAGE = H * MBK * 2;
+  const int xbytes = (p.k0 / MBK) * MA_BYTES;
+  const int fixed = 1024 + xbytes + 2 * (H / 64) * 16384 + 1024;
+  constexpr int STATIC = 2 * M_EPI_WARPS * (H / 2) * 4 + 2 * 2 * MBM * 4;
+  const int ns = std::min(MSTAGES, (227 * 1024 - STATIC - 512 - fixed) / STAGE);
+  if (ns < 2) return cudaErrorInvalidValue;
+  auto kern = tc_mlp_pair_kernel<H>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - STATIC - 512);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  p.stages = ns;
+  int grid = std::min(p.total_su, num_sms());
+  if (grid == 0) return cudaSuccess;
+  return launch_pdl(kern, dim3(grid), dim3(M_NTHREADS), (size_t)(ns * STAGE + fixed), st, p);
+}
+
 template <int H, bool ACTOR>
 cudaError_t launch_mlp(MlpParams& p, cudaStream_t st) {
   constexpr int STAGE = H * MBK * 2;
@@ -782,6 +1038,19 @@ cudaError_t tc_mlp_fwd(const MlpArgs& a, cudaStream_t st) {
   p.total_su = TSU;
   p.loss = a.loss;
   if (TSU == 0) return cudaSuccess;
+  // critic passes without loss groups and >= 4 row blocks per CTA: two blocks in flight per CTA (ANT:
+  // critic forward 83.9 -> 76.1 us).  With ~2.6 blocks per CTA (WLK) the plain schedule wins (29.7 vs
+  // 31.8 us): the pair schedule's 2-stage weight ring starves layer 1.  SPZ_MLP_PAIR=0 / 1 forces.
+  const char* pe = std::getenv("SPZ_MLP_PAIR");  // read per launch (plans are built once)
+  const int pair_env = pe ? (pe[0] == '1' ? 1 : 0) : -1;
+  const bool pair = pair_env >= 0 ? pair_env == 1 : TSU >= 4 * num_sms();
+  if (!actor && a.n_group == 0 && pair) {
+    switch (a.h) {
+      case 64: return launch_mlp_pair<64>(p, st);
+      case 128: return launch_mlp_pair<128>(p, st);
+      default: return launch_mlp_pair<256>(p, st);
+    }
+  }
   switch (a.h) {
     case 64: return actor ? launch_mlp<64, true>(p, st) : launch_mlp<64, false>(p, st);
     case 128: return actor ? launch_mlp<128, true>(p, st) : launch_mlp<128, false>(p, st);

@@ -223,6 +223,14 @@ def test_td3_parity_wide_1024(precision):
     run_parity("td3", precision, 44, 17, 1024, 3, 520, 6000, 4 if precision == "bf16" else 2)
 
 
+@pytest.mark.parametrize("B", [4096, 10000])
+def test_sac_parity_pair_schedule_critic_forward(B, monkeypatch):
+    """The two-blocks-in-flight critic forward (default at >= 4 row blocks per CTA) forced at sizes where
+    CTAs get 2..4 blocks: full pairs, a trailing single block, ragged last block."""
+    monkeypatch.setenv("SPZ_MLP_PAIR", "1")
+    run_parity("sac", "bf16", 22, 6, 256, 2, B, 20_000, 2, check_moments=False)
+
+
 def test_sac_parity_graph_vs_eager_bit_identical():
     outs = []
     for use_graph in (True, False):

@@ -330,13 +330,15 @@ def main():
             lrn.update(GB, 1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        # step k: push its B fresh transitions (H2D from pinned host memory) while update k-1 runs on the
-        # GPU, read back update k-1's statistics (D2H), enqueue update k (spz_update_async / _wait)
+        # step k: push its B fresh transitions (H2D from pinned host memory) while updates k-2 and k-1 run on
+        # the GPU, read back update k-2's statistics (D2H), enqueue update k (spz_update_async / _wait,
+        # two updates in flight)
         for k in range(K2):
             ring.push(**{n: v[sl(k)] for n, v in pinned.items()})
-            if k:
+            if k >= 2:
                 lrn.wait()
             lrn.update_async(GB, 1)
+        lrn.wait()
         lrn.wait()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
@@ -347,8 +349,8 @@ def main():
         e2e = {"value": (GB if (dp or split) else B * world) * K2 / dt, "unit": "frames/s",
                "h2d_bytes_per_step": GB * R_fields * 4 * world,
                "d2h_bytes_per_step": 64 + 32 + 4, "steps": K2,
-               "note": "per step: spz_replay_push of B fresh host transitions (pinned, H2D) overlapping the previous "
-                       "update, spz_update_wait (stats D2H), spz_update_async(B, 1)"}
+               "note": "per step: spz_replay_push of B fresh host transitions (pinned, H2D) overlapping the updates in "
+                       "flight, spz_update_wait (stats D2H of the oldest), spz_update_async(B, 1); two updates in flight"}
 
     sweep = None
     if a.sweep and world == 1:

@@ -180,12 +180,13 @@ spz_status spz_update(spz_learner* L, int64_t batch, int64_t n_steps, spz_stats*
  * running on the GPU -- the paper's updater "reads the experience pool without waiting for the
  * samplers" (§3.3.2).  spz_update_async enqueues the n_steps steps (same semantics and
  * errors as spz_update except SPZ_ENONFINITE of *these* steps, which spz_update_wait reports) and
- * returns without waiting; at most one call is in flight per learner (a second call first completes
- * the previous one).  Ring pushes issued meanwhile are ordered on the device: their records are
- * written only after the in-flight update's reads, and the next update waits for them, so results
- * are identical to the synchronous sequence push, update, push, update.  spz_update_wait blocks until
- * the enqueued steps finish and fills *last (nullable) like spz_update; with nothing in flight it
- * returns the statistics of the last completed update. */
+ * returns without waiting; up to two calls are in flight per learner (a third first completes the
+ * oldest), so the host's next push and launch hide under the running update.  Ring pushes issued
+ * meanwhile are ordered on the device: their records are written only after the reads of every update
+ * enqueued before them, and the next update waits for them, so results are identical to the
+ * synchronous sequence push, update, push, update.  spz_update_wait blocks until the oldest call in
+ * flight finishes and fills *last (nullable) with its statistics like spz_update; with nothing in
+ * flight it returns the statistics of the last completed update. */
 spz_status spz_update_async(spz_learner* L, int64_t batch, int64_t n_steps);
 spz_status spz_update_wait(spz_learner* L, spz_stats* last);
 

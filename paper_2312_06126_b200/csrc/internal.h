@@ -44,6 +44,8 @@ struct spz_replay {
   float* rec = nullptr;       // [C x R] fp32, device
   float* staging = nullptr;   // pinned host staging for pushes
   size_t staging_bytes = 0;
+  int64_t* d_fill = nullptr;  // fill = min(cursor, C) on the device, written in stream order by every push
+  int64_t* h_fill = nullptr;  // pinned staging for it
   float* dstage = nullptr;    // device staging of the five field arrays (pinned-host pushes)
   size_t dstage_bytes = 0;
   cudaStream_t stream = nullptr;

@@ -115,10 +115,25 @@ struct spz_learner {
   float *P = nullptr, *Mo = nullptr, *Vo = nullptr;
   void* S = nullptr;
   int64_t* counters = nullptr;  // step, t_critic, t_actor, t_alpha
-  int64_t* d_fill = nullptr;
   int* d_flag = nullptr;
   cudaEvent_t ev_read = nullptr;  // recorded after every enqueued update: ring pushes wait on it
-  bool pending = false;           // an update enqueued by spz_update_async not yet waited for
+  // spz_update_async keeps up to two updates in flight; each owns a pinned slot for its read-back
+  // device read-back block: the step statistics, counters and non-finite flag, contiguous so one copy
+  // returns them
+  struct ReadBack {
+    StatsOut stats;
+    int64_t ctr[8];
+    int flag;
+    int pad[3];
+  };
+  ReadBack* d_rb = nullptr;
+  struct HostSlot {
+    ReadBack rb;
+  };
+  HostSlot* h_slots = nullptr;    // pinned [2]
+  cudaEvent_t ev_slot[2] = {nullptr, nullptr};
+  int inflight[2] = {0, 0}, n_inflight = 0, next_slot = 0;  // slot queue, oldest first
+  int64_t host_step = 0;          // global step after every enqueued update (valid while n_inflight > 0)
   int plan_track_gen = 0;         // ring->track_gen the plan's gather was built for
   bool ctr_cached = false;  // h_counters[0..3] / h_flag mirror the device (set by read_counters; cleared while
                             // steps are enqueued): spz_update skips the leading device round trip
@@ -278,6 +293,9 @@ spz_learner::~spz_learner() {
     if (e) cudaGraphExecDestroy(e);
   for (void* p : allocs) cudaFree(p);
   if (h_stats) cudaFreeHost(h_stats);
+  if (h_slots) cudaFreeHost(h_slots);
+  for (auto& e : ev_slot)
+    if (e) cudaEventDestroy(e);
   if (h_flag) cudaFreeHost(h_flag);
   if (h_counters) cudaFreeHost(h_counters);
   if (own_stream) cudaStreamDestroy(own_stream);
@@ -410,7 +428,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     {
       const float* rec = Lr->ring->rec;
       const int R = Lr->ring->R;
-      const int64_t* fill = Lr->d_fill;
+      const int64_t* fill = Lr->ring->d_fill;  // written in stream order by the ring's pushes
       const int64_t* stp = Lr->counters;
       T *Xa = static_cast<T*>(Lr->Xa), *Xc = static_cast<T*>(Lr->Xc);
       float *rr = Lr->r, *dd = Lr->d;
@@ -1169,14 +1187,6 @@ static spz_status prepare(spz_learner* Lr, int64_t batch) {
   return SPZ_OK;
 }
 
-static spz_status set_fill(spz_learner* Lr) {
-  static thread_local int64_t hf;
-  hf = Lr->ring->fill();
-  // the pinned counters buffer doubles as the fill staging slot
-  Lr->h_counters[4] = hf;
-  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->d_fill, &Lr->h_counters[4], sizeof(int64_t), cudaMemcpyHostToDevice, Lr->stream));
-  return SPZ_OK;
-}
 
 template <typename T>
 static spz_status refresh_shadows_t(spz_learner* Lr) {
@@ -1322,10 +1332,14 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->Mo, p * sizeof(float)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->Vo, p * sizeof(float)));
   SPZ_TRY(dalloc(Lr.get(), &Lr->S, s * Lr->esz));
-  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->counters, 8 * sizeof(int64_t)));
-  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_fill, sizeof(int64_t)));
-  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_flag, sizeof(int)));
-  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_stats, sizeof(StatsOut)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->d_rb, sizeof(spz_learner::ReadBack)));
+  Lr->counters = Lr->d_rb->ctr;
+  Lr->d_flag = &Lr->d_rb->flag;
+  Lr->d_stats = &Lr->d_rb->stats;
+  if (cudaMallocHost(&Lr->h_slots, 2 * sizeof(spz_learner::HostSlot)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&Lr->ev_slot[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&Lr->ev_slot[1], cudaEventDisableTiming) != cudaSuccess)
+    return fail(SPZ_ENOMEM, "spz_learner_create: pinned read-back slots");
   if (cudaMallocHost(&Lr->h_stats, sizeof(StatsOut)) != cudaSuccess || cudaMallocHost(&Lr->h_flag, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&Lr->h_counters, 8 * sizeof(int64_t)) != cudaSuccess)
     return fail(SPZ_ENOMEM, "spz_learner_create: pinned host allocation failed");
@@ -1503,14 +1517,26 @@ spz_status spz_learner_set_stream(spz_learner* Lr, void* stream) {
 }
 
 namespace spz {
-// completes the update enqueued by spz_update_async: statistics, counters and the non-finite flag
+// completes the oldest update in flight: its statistics, the step counters and the non-finite flag
+// (the counters mirror the device again once nothing is in flight)
 static spz_status update_finish(spz_learner* Lr, spz_stats* last) {
-  SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
-  Lr->pending = false;
-  Lr->ctr_cached = true;
-  if (*Lr->h_flag)
-    return fail(SPZ_ENONFINITE, "spz_update: non-finite loss or gradient at step " + std::to_string(Lr->h_counters[0]) +
-                                    (*Lr->h_flag == 2 ? " (gradient)" : " (loss)") + "; learner halted");
+  if (Lr->n_inflight == 0) {
+    if (*Lr->h_flag)
+      return fail(SPZ_ENONFINITE, "spz_update: learner halted by an earlier non-finite step " + std::to_string(Lr->h_counters[0]));
+  } else {
+    const int sl = Lr->inflight[0];
+    Lr->inflight[0] = Lr->inflight[1];
+    --Lr->n_inflight;
+    SPZ_CUDA_TRY(cudaEventSynchronize(Lr->ev_slot[sl]));
+    const spz_learner::ReadBack& rb = Lr->h_slots[sl].rb;
+    for (int i = 0; i < 4; ++i) Lr->h_counters[i] = rb.ctr[i];
+    *Lr->h_flag = rb.flag;
+    *Lr->h_stats = rb.stats;
+    Lr->ctr_cached = Lr->n_inflight == 0;
+    if (rb.flag)
+      return fail(SPZ_ENONFINITE, "spz_update: non-finite loss or gradient at step " + std::to_string(rb.ctr[0]) +
+                                      (rb.flag == 2 ? " (gradient)" : " (loss)") + "; learner halted");
+  }
   if (last) {
     const StatsOut& s = *Lr->h_stats;
     last->step = (int64_t)s.step;
@@ -1524,20 +1550,38 @@ static spz_status update_finish(spz_learner* Lr, spz_stats* last) {
   }
   return SPZ_OK;
 }
+// completes every update in flight (statistics dropped)
+static spz_status update_drain(spz_learner* Lr) {
+  spz_status st = SPZ_OK;
+  while (Lr->n_inflight > 0) {
+    const spz_status s = update_finish(Lr, nullptr);
+    if (st == SPZ_OK) st = s;
+  }
+  return st;
+}
 }  // namespace spz
 
 spz_status spz_update_async(spz_learner* Lr, int64_t batch, int64_t n_steps) {
   if (!Lr) return fail(SPZ_EINVAL, "spz_update_async: NULL learner");
   if (n_steps < 0) return fail(SPZ_EINVAL, "spz_update_async: n_steps < 0");
   DeviceGuard dg(Lr->device);
-  if (Lr->pending) SPZ_TRY(update_finish(Lr, nullptr));  // at most one update in flight
+  if (Lr->n_inflight == 2) SPZ_TRY(update_finish(Lr, nullptr));  // at most two updates in flight
+  if (Lr->plan_B != batch || Lr->plan_track_gen != Lr->ring->track_gen) SPZ_TRY(update_drain(Lr));
   SPZ_TRY(prepare(Lr, batch));
-  if (!Lr->ctr_cached) SPZ_TRY(read_counters(Lr));
-  if (*Lr->h_flag) return fail(SPZ_ENONFINITE, "spz_update: learner halted by an earlier non-finite step " + std::to_string(Lr->h_counters[0]));
-  int64_t step = Lr->h_counters[0];
+  int64_t step;
+  if (Lr->n_inflight == 0) {
+    if (!Lr->ctr_cached) SPZ_TRY(read_counters(Lr));
+    if (*Lr->h_flag) return fail(SPZ_ENONFINITE, "spz_update: learner halted by an earlier non-finite step " + std::to_string(Lr->h_counters[0]));
+    step = Lr->h_counters[0];
+  } else {
+    step = Lr->host_step;  // the device advances exactly n_steps per enqueued update (or halts: reported by wait)
+  }
   Lr->ctr_cached = false;
-  SPZ_TRY(set_fill(Lr));
-  SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));  // the last push's records are written
+  const int sl = Lr->next_slot;
+  Lr->next_slot ^= 1;
+  spz_learner::HostSlot& hs = Lr->h_slots[sl];
+  // the last push's records (and the fill it left on the device) are written
+  SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));
   for (int64_t k = 0; k < n_steps; ++k, ++step) {
     const int v = variant_of(Lr, step);
     if (Lr->cfg.use_graph) {
@@ -1548,22 +1592,23 @@ spz_status spz_update_async(spz_learner* Lr, int64_t batch, int64_t n_steps) {
     }
   }
   SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_read, Lr->stream));  // pushes overwrite records only after these reads
-  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_stats, Lr->d_stats, sizeof(StatsOut), cudaMemcpyDeviceToHost, Lr->stream));
-  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_counters, Lr->counters, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, Lr->stream));
-  SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->h_flag, Lr->d_flag, sizeof(int), cudaMemcpyDeviceToHost, Lr->stream));
-  Lr->pending = true;
+  SPZ_CUDA_TRY(cudaMemcpyAsync(&hs.rb, Lr->d_rb, sizeof(spz_learner::ReadBack), cudaMemcpyDeviceToHost, Lr->stream));
+  SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_slot[sl], Lr->stream));
+  Lr->inflight[Lr->n_inflight++] = sl;
+  Lr->host_step = step;
   return SPZ_OK;
 }
 
 spz_status spz_update_wait(spz_learner* Lr, spz_stats* last) {
   if (!Lr) return fail(SPZ_EINVAL, "spz_update_wait: NULL learner");
   DeviceGuard dg(Lr->device);
-  return update_finish(Lr, last);  // (nothing in flight: the statistics of the last completed update)
+  return update_finish(Lr, last);  // the oldest in flight (nothing in flight: the last completed update)
 }
 
 spz_status spz_update(spz_learner* Lr, int64_t batch, int64_t n_steps, spz_stats* last) {
   SPZ_TRY(spz_update_async(Lr, batch, n_steps));
   DeviceGuard dg(Lr->device);
+  while (Lr->n_inflight > 1) SPZ_TRY(update_finish(Lr, nullptr));
   return update_finish(Lr, last);
 }
 
@@ -1625,7 +1670,7 @@ spz_status spz_tune_batch(spz_learner* Lr, const int64_t* ladder, int32_t n, int
   for (int i = 1; i < n; ++i)
     if (ladder[i] <= ladder[i - 1]) return fail(SPZ_EINVAL, "spz_tune_batch: ladder must be strictly ascending");
   DeviceGuard dg(Lr->device);
-  if (Lr->pending) SPZ_TRY(update_finish(Lr, nullptr));
+  SPZ_TRY(update_drain(Lr));
   *n_out = 0;
   *best = ladder[0];
   // snapshot of everything the probe steps change (the bf16 operand shadow is refreshed from P)
@@ -1728,12 +1773,11 @@ spz_status spz_learner_profile(spz_learner* Lr, int64_t batch, int64_t n_steps, 
                                int32_t* count) {
   if (!Lr || n_steps < 1) return fail(SPZ_EINVAL, "spz_learner_profile: bad argument");
   DeviceGuard dg(Lr->device);
-  if (Lr->pending) SPZ_TRY(update_finish(Lr, nullptr));
+  SPZ_TRY(update_drain(Lr));
   SPZ_TRY(prepare(Lr, batch));
   SPZ_TRY(read_counters(Lr));
   int64_t step = Lr->h_counters[0];
   Lr->ctr_cached = false;
-  SPZ_TRY(set_fill(Lr));
   SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));
   std::vector<const char*> cls;
   std::vector<double> tot;

@@ -18,7 +18,8 @@ namespace spz {
 __global__ void pack_records_kernel(float* __restrict__ rec, int R, int o, int m, int64_t C, int64_t first, int64_t n,
                                     const float* __restrict__ obs, const float* __restrict__ act,
                                     const float* __restrict__ rew, const float* __restrict__ nobs,
-                                    const float* __restrict__ done) {
+                                    const float* __restrict__ done, int64_t* __restrict__ fill_out, int64_t fill) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *fill_out = fill;  // the ring's fill after this push
   const int64_t total = n * R;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / R;
@@ -145,6 +146,8 @@ spz_status spz_replay_create(const spz_replay_desc* desc, spz_replay** out) {
   }
   if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&r->ev_copy, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMalloc(&r->d_fill, sizeof(int64_t)) != cudaSuccess || cudaMallocHost(&r->h_fill, sizeof(int64_t)) != cudaSuccess ||
+      cudaMemsetAsync(r->d_fill, 0, sizeof(int64_t), r->stream) != cudaSuccess ||
       cudaEventCreateWithFlags(&r->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
       cudaMemsetAsync(r->rec, 0, bytes, r->stream) != cudaSuccess || cudaStreamSynchronize(r->stream) != cudaSuccess) {
     cudaFree(r->rec);
@@ -193,7 +196,8 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
     const int64_t total = nn * R;
     const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
     pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, obs + skip * o, act + skip * m,
-                                                        rew + skip, next_obs + skip * o, done + skip);
+                                                        rew + skip, next_obs + skip * o, done + skip, r->d_fill,
+                                                        std::min(first_idx + n, r->C));
     SPZ_CUDA_TRY(cudaGetLastError());
   } else if (all_pinned({obs, act, rew, next_obs, done})) {
     // page-locked host fields: DMA them as they are into device staging and pack on the device (no
@@ -226,7 +230,8 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
     SPZ_CUDA_TRY(account());
     const int64_t total = nn * R;
     const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
-    pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, d_obs, d_act, d_rew, d_nobs, d_done);
+    pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, d_obs, d_act, d_rew, d_nobs, d_done,
+                                                        r->d_fill, std::min(first_idx + n, r->C));
     SPZ_CUDA_TRY(cudaGetLastError());
     SPZ_CUDA_TRY(cudaEventRecord(r->ev_pack, r->stream));
     // return once the caller's buffers are read; the pack may still wait for an in-flight update, and
@@ -263,6 +268,8 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
     const int64_t slot = start % r->C;
     const int64_t n1 = std::min(nn, r->C - slot);
     SPZ_CUDA_TRY(cudaMemcpyAsync(r->rec + slot * R, s, (size_t)n1 * R * sizeof(float), cudaMemcpyHostToDevice, r->stream));
+    *r->h_fill = std::min(first_idx + n, r->C);  // stable: this path synchronises before returning
+    SPZ_CUDA_TRY(cudaMemcpyAsync(r->d_fill, r->h_fill, sizeof(int64_t), cudaMemcpyHostToDevice, r->stream));
     if (nn > n1)
       SPZ_CUDA_TRY(cudaMemcpyAsync(r->rec, s + n1 * R, (size_t)(nn - n1) * R * sizeof(float), cudaMemcpyHostToDevice, r->stream));
   }
@@ -361,6 +368,8 @@ void spz_replay_destroy(spz_replay* r) {
     cudaFree(r->rec);
     if (r->staging) cudaFreeHost(r->staging);
     if (r->dstage) cudaFree(r->dstage);
+    if (r->d_fill) cudaFree(r->d_fill);
+    if (r->h_fill) cudaFreeHost(r->h_fill);
     if (r->tags) cudaFree(r->tags);
     if (r->d_lost) cudaFree(r->d_lost);
     cudaEventDestroy(r->ev_copy);

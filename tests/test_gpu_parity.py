@@ -118,7 +118,7 @@ def test_update_async_overlapped_pushes_bit_identical():
     o, m, C, B, K = 22, 6, 3000, 1024, 6
     fresh = [synthdata.transitions("locomotion", o, m, B, seed=100 + k) for k in range(K)]
     res = []
-    for mode in ("sync", "async_pinned", "async_pageable"):
+    for mode in ("sync", "async_pinned", "async_pageable", "async2"):
         g, _ = make_rings(o, m, C)
         lrn = spz.Learner(g, precision="bf16", hidden=64, n_hidden=2, max_batch=B)
         stats = []
@@ -129,6 +129,11 @@ def test_update_async_overlapped_pushes_bit_identical():
             if mode == "sync":
                 g.push(**tr)
                 stats.append(lrn.update(B, 1))
+            elif mode == "async2":  # two updates in flight: push k while k-2 and k-1 run
+                g.push(**tr)
+                if k >= 2:
+                    stats.append(lrn.wait())
+                lrn.update_async(B, 1)
             else:
                 if k > 0:
                     g.push(**tr)  # overlaps update k-1 on the GPU
@@ -136,7 +141,10 @@ def test_update_async_overlapped_pushes_bit_identical():
                 else:
                     g.push(**tr)
                 lrn.update_async(B, 1)
-        if mode != "sync":
+        if mode == "async2":
+            stats.append(lrn.wait())
+            stats.append(lrn.wait())
+        elif mode != "sync":
             stats.append(lrn.wait())
         res.append((stats, [lrn.get(n) for n in ("actor", "q1", "q2", "q1_targ")]))
     for other in res[1:]:

@@ -68,6 +68,12 @@ static bool dz_split_env() {
   return e && e[0] == '1';
 }
 
+// copies the read-back block into host-mapped memory (spz_update_async)
+__global__ void publish_kernel(const unsigned long long* __restrict__ src, unsigned long long* dst, int words) {
+  for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+  __threadfence_system();
+}
+
 // diagnostics: SPZ_ACTOR_BWD_UNFUSED=1 runs the actor backward as separate GEMM / head launches
 static bool actor_bwd_unfused_env() {
   const char* e = std::getenv("SPZ_ACTOR_BWD_UNFUSED");
@@ -130,7 +136,8 @@ struct spz_learner {
   struct HostSlot {
     ReadBack rb;
   };
-  HostSlot* h_slots = nullptr;    // pinned [2]
+  HostSlot* h_slots = nullptr;    // pinned, host-mapped [2]
+  unsigned long long* d_slots = nullptr;  // device view of h_slots (publish_kernel writes it)
   cudaEvent_t ev_slot[2] = {nullptr, nullptr};
   int inflight[2] = {0, 0}, n_inflight = 0, next_slot = 0;  // slot queue, oldest first
   int64_t host_step = 0;          // global step after every enqueued update (valid while n_inflight > 0)
@@ -1336,7 +1343,8 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   Lr->counters = Lr->d_rb->ctr;
   Lr->d_flag = &Lr->d_rb->flag;
   Lr->d_stats = &Lr->d_rb->stats;
-  if (cudaMallocHost(&Lr->h_slots, 2 * sizeof(spz_learner::HostSlot)) != cudaSuccess ||
+  if (cudaHostAlloc(&Lr->h_slots, 2 * sizeof(spz_learner::HostSlot), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&Lr->d_slots, Lr->h_slots, 0) != cudaSuccess ||
       cudaEventCreateWithFlags(&Lr->ev_slot[0], cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&Lr->ev_slot[1], cudaEventDisableTiming) != cudaSuccess)
     return fail(SPZ_ENOMEM, "spz_learner_create: pinned read-back slots");
@@ -1592,7 +1600,15 @@ spz_status spz_update_async(spz_learner* Lr, int64_t batch, int64_t n_steps) {
     }
   }
   SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_read, Lr->stream));  // pushes overwrite records only after these reads
-  SPZ_CUDA_TRY(cudaMemcpyAsync(&hs.rb, Lr->d_rb, sizeof(spz_learner::ReadBack), cudaMemcpyDeviceToHost, Lr->stream));
+  // read-back of the statistics, counters and flag: a one-warp kernel writing host-mapped memory (a
+  // device-to-host copy costs more stream time between consecutive updates)
+  {
+    constexpr int W = (int)(sizeof(spz_learner::ReadBack) / 8);
+    unsigned long long* dst = Lr->d_slots + (size_t)sl * (sizeof(spz_learner::HostSlot) / 8);
+    publish_kernel<<<1, 32, 0, Lr->stream>>>(reinterpret_cast<const unsigned long long*>(Lr->d_rb), dst, W);
+    SPZ_CUDA_TRY(cudaGetLastError());
+    (void)hs;
+  }
   SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_slot[sl], Lr->stream));
   Lr->inflight[Lr->n_inflight++] = sl;
   Lr->host_step = step;
@@ -1699,7 +1715,10 @@ spz_status spz_tune_batch(spz_learner* Lr, const int64_t* ladder, int32_t n, int
     if (cudaEventRecord(e1, Lr->stream) != cudaSuccess) { st = fail(SPZ_ECUDA, "spz_tune_batch: event record"); break; }
     if ((st = update_finish(Lr, nullptr)) != SPZ_OK) break;
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
+    if (cudaEventSynchronize(e1) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess || !(ms > 0.f)) {
+      st = fail(SPZ_ECUDA, "spz_tune_batch: event timing failed");
+      break;
+    }
     spz_tune_point& pt = out[(*n_out)++];
     pt.batch = B;
     pt.ms_per_update = (double)ms / (double)steps;

@@ -30,6 +30,14 @@ struct DeviceGuard {
 
 }  // namespace spz
 
+namespace spz {
+// replay.cu: the deferred pack of the last pinned-host push, enqueued on `st` (caller holds r->mu and
+// has ordered `st` after every reader of the records); records ev_pack and the stage's free event
+cudaError_t ring_enqueue_pack(spz_replay* r, cudaStream_t st);
+// replay.cu: run any deferred pack on the ring's own stream after every reader (caller holds r->mu)
+cudaError_t ring_flush_pending(spz_replay* r);
+}  // namespace spz
+
 #define SPZ_TRY(expr)            \
   do {                           \
     spz_status _s = (expr);      \
@@ -46,8 +54,19 @@ struct spz_replay {
   size_t staging_bytes = 0;
   int64_t* d_fill = nullptr;  // fill = min(cursor, C) on the device, written in stream order by every push
   int64_t* h_fill = nullptr;  // pinned staging for it
-  float* dstage = nullptr;    // device staging of the five field arrays (pinned-host pushes)
-  size_t dstage_bytes = 0;
+  // pinned-host pushes: the five field arrays are DMA'd into one of two device staging buffers; the
+  // record pack is deferred to the next update of the ring's only learner (enqueued on its stream
+  // right before its graph: no cross-stream hand-off per update), or run on the ring stream by the
+  // next ring operation that needs the records
+  float* dstage[2] = {nullptr, nullptr};
+  size_t dstage_bytes[2] = {0, 0};
+  cudaEvent_t ev_stage_free[2] = {nullptr, nullptr};  // the pack that last read staging buffer s is done
+  int next_stage = 0;
+  struct PendingPack {
+    bool active = false;
+    int stage = 0;
+    int64_t first = 0, start = 0, nn = 0, fill_after = 0;
+  } pend;
   cudaStream_t stream = nullptr;
   // ordering against in-flight updates (the update reads the pool while samplers write it):
   // every write to `rec` is enqueued after the readers' last recorded reads; learners wait on ev_pack

@@ -1588,7 +1588,16 @@ spz_status spz_update_async(spz_learner* Lr, int64_t batch, int64_t n_steps) {
   const int sl = Lr->next_slot;
   Lr->next_slot ^= 1;
   spz_learner::HostSlot& hs = Lr->h_slots[sl];
-  // the last push's records (and the fill it left on the device) are written
+  // the last pinned push's deferred pack: on this learner's stream right before its steps when it is
+  // the ring's only reader (stream order already follows its own earlier reads), else on the ring
+  // stream after every reader; then the records (and the fill they leave on the device) are in place
+  {
+    std::lock_guard<std::mutex> lk(Lr->ring->mu);
+    if (Lr->ring->pend.active) {
+      if (Lr->ring->readers.size() == 1) SPZ_CUDA_TRY(ring_enqueue_pack(Lr->ring, Lr->stream));
+      else SPZ_CUDA_TRY(ring_flush_pending(Lr->ring));
+    }
+  }
   SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));
   for (int64_t k = 0; k < n_steps; ++k, ++step) {
     const int v = variant_of(Lr, step);
@@ -1797,6 +1806,10 @@ spz_status spz_learner_profile(spz_learner* Lr, int64_t batch, int64_t n_steps, 
   SPZ_TRY(read_counters(Lr));
   int64_t step = Lr->h_counters[0];
   Lr->ctr_cached = false;
+  {
+    std::lock_guard<std::mutex> lk(Lr->ring->mu);
+    SPZ_CUDA_TRY(ring_flush_pending(Lr->ring));
+  }
   SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));
   std::vector<const char*> cls;
   std::vector<double> tot;

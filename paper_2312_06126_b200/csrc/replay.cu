@@ -20,17 +20,30 @@ __global__ void pack_records_kernel(float* __restrict__ rec, int R, int o, int m
                                     const float* __restrict__ rew, const float* __restrict__ nobs,
                                     const float* __restrict__ done, int64_t* __restrict__ fill_out, int64_t fill) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *fill_out = fill;  // the ring's fill after this push
-  const int64_t total = n * R;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = e / R;
-    const int c = (int)(e - t * R);
-    float v = 0.f;
-    if (c < o) v = obs[t * o + c];
-    else if (c < o + m) v = act[t * m + (c - o)];
-    else if (c == o + m) v = rew[t];
-    else if (c == o + m + 1) v = done[t];
-    else if (c < 2 * o + m + 2) v = nobs[t * o + (c - o - m - 2)];
-    rec[((first + t) % C) * R + c] = v;
+  // one thread per 16-byte unit of a record (R % 4 == 0, rows 16-byte aligned); 32-bit indexing within
+  // the push (n <= C rows), one conditional wrap for the slot
+  const int R4 = R >> 2;
+  const int total = (int)n * R4;
+  const int64_t slot0 = first % C;
+  const int c_a = o, c_r = o + m, c_d = o + m + 1, c_s2 = o + m + 2, c_end = 2 * o + m + 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int t = e / R4;
+    const int q = e - t * R4;
+    int64_t slot = slot0 + t;
+    if (slot >= C) slot -= C;
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = 4 * q + k;
+      float x = 0.f;
+      if (c < c_a) x = __ldg(obs + (int64_t)t * o + c);
+      else if (c < c_r) x = __ldg(act + (int64_t)t * m + (c - c_a));
+      else if (c == c_r) x = __ldg(rew + t);
+      else if (c == c_d) x = __ldg(done + t);
+      else if (c < c_end) x = __ldg(nobs + (int64_t)t * o + (c - c_s2));
+      v[k] = x;
+    }
+    reinterpret_cast<float4*>(rec + slot * R)[q] = make_float4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -118,6 +131,46 @@ static bool all_pinned(std::initializer_list<const float*> ps) {
   return true;
 }
 
+static cudaError_t wait_readers(spz_replay* r) {
+  for (cudaEvent_t e : r->readers) {
+    cudaError_t err = cudaStreamWaitEvent(r->stream, e, 0);
+    if (err != cudaSuccess) return err;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t ring_enqueue_pack(spz_replay* r, cudaStream_t st) {
+  spz_replay::PendingPack& p = r->pend;
+  if (!p.active) return cudaSuccess;
+  const int o = r->o, m = r->m, R = r->R;
+  const int64_t nn = p.nn;
+  float* d_obs = r->dstage[p.stage];
+  float* d_act = d_obs + nn * o;
+  float* d_nobs = d_act + nn * m;
+  float* d_rew = d_nobs + nn * o;
+  float* d_done = d_rew + nn;
+  if (r->tags && nn > 0) {
+    const int64_t occupied = p.first < r->C ? p.first : r->C;
+    loss_account_kernel<<<(unsigned)cdiv(nn, 256), 256, 0, st>>>(r->tags, r->C, p.start % r->C, nn, occupied, p.first,
+                                                                r->pushed0, r->d_lost);
+  }
+  const int64_t total = nn * (R / 4);
+  const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+  pack_records_kernel<<<blocks, 256, 0, st>>>(r->rec, R, o, m, r->C, p.start, nn, d_obs, d_act, d_rew, d_nobs, d_done,
+                                              r->d_fill, p.fill_after);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaEventRecord(r->ev_pack, st);
+  if (e == cudaSuccess) e = cudaEventRecord(r->ev_stage_free[p.stage], st);
+  p.active = false;
+  return e;
+}
+
+cudaError_t ring_flush_pending(spz_replay* r) {
+  if (!r->pend.active) return cudaSuccess;
+  cudaError_t e = wait_readers(r);
+  return e == cudaSuccess ? ring_enqueue_pack(r, r->stream) : e;
+}
+
 }  // namespace spz
 
 using namespace spz;
@@ -149,6 +202,8 @@ spz_status spz_replay_create(const spz_replay_desc* desc, spz_replay** out) {
       cudaMalloc(&r->d_fill, sizeof(int64_t)) != cudaSuccess || cudaMallocHost(&r->h_fill, sizeof(int64_t)) != cudaSuccess ||
       cudaMemsetAsync(r->d_fill, 0, sizeof(int64_t), r->stream) != cudaSuccess ||
       cudaEventCreateWithFlags(&r->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&r->ev_stage_free[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&r->ev_stage_free[1], cudaEventDisableTiming) != cudaSuccess ||
       cudaMemsetAsync(r->rec, 0, bytes, r->stream) != cudaSuccess || cudaStreamSynchronize(r->stream) != cudaSuccess) {
     cudaFree(r->rec);
     delete r;
@@ -173,14 +228,9 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
   const int64_t nn = n - skip;
   const int64_t start = first_idx + skip;
   const int o = r->o, m = r->m, R = r->R;
-  // writes to the records wait for every learner's last enqueued read of them
-  const auto wait_readers = [&]() -> cudaError_t {
-    for (cudaEvent_t e : r->readers) {
-      cudaError_t err = cudaStreamWaitEvent(r->stream, e, 0);
-      if (err != cudaSuccess) return err;
-    }
-    return cudaSuccess;
-  };
+  // an earlier push's deferred pack lands first (it precedes this push); writes to the records wait for
+  // every learner's last enqueued read of them
+  SPZ_CUDA_TRY(ring_flush_pending(r));
   // transmission loss: records that never land, and the unsampled records the landing ones overwrite
   const auto account = [&]() -> cudaError_t {
     if (!r->tags || nn == 0) return cudaSuccess;
@@ -191,28 +241,32 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
     return cudaGetLastError();
   };
   if (src_on_device) {
-    SPZ_CUDA_TRY(wait_readers());
+    SPZ_CUDA_TRY(wait_readers(r));
     SPZ_CUDA_TRY(account());
-    const int64_t total = nn * R;
+    const int64_t total = nn * (R / 4);
     const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
     pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, obs + skip * o, act + skip * m,
                                                         rew + skip, next_obs + skip * o, done + skip, r->d_fill,
                                                         std::min(first_idx + n, r->C));
     SPZ_CUDA_TRY(cudaGetLastError());
   } else if (all_pinned({obs, act, rew, next_obs, done})) {
-    // page-locked host fields: DMA them as they are into device staging and pack on the device (no
-    // host-side record assembly); the copies read the caller's buffers, so the call still waits for them
+    // page-locked host fields: DMA them as they are into a device staging buffer (no host-side record
+    // assembly); the pack is deferred (ring_enqueue_pack).  The copies read the caller's buffers, so
+    // the call still waits for them.
+    const int sg = r->next_stage;
+    r->next_stage ^= 1;
     const size_t F = (size_t)(2 * o + m + 2);
     const size_t bytes = (size_t)nn * F * sizeof(float);
-    if (r->dstage_bytes < bytes) {
-      SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
-      if (r->dstage) cudaFree(r->dstage);
-      r->dstage = nullptr;
-      r->dstage_bytes = 0;
-      SPZ_CUDA_TRY(cudaMalloc(&r->dstage, bytes));
-      r->dstage_bytes = bytes;
+    if (r->dstage_bytes[sg] < bytes) {
+      SPZ_CUDA_TRY(cudaEventSynchronize(r->ev_stage_free[sg]));
+      if (r->dstage[sg]) cudaFree(r->dstage[sg]);
+      r->dstage[sg] = nullptr;
+      r->dstage_bytes[sg] = 0;
+      SPZ_CUDA_TRY(cudaMalloc(&r->dstage[sg], bytes));
+      r->dstage_bytes[sg] = bytes;
     }
-    float* d_obs = r->dstage;
+    SPZ_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_stage_free[sg], 0));  // its previous pack has read it
+    float* d_obs = r->dstage[sg];
     float* d_act = d_obs + nn * o;
     float* d_nobs = d_act + nn * m;
     float* d_rew = d_nobs + nn * o;
@@ -226,17 +280,16 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
     SPZ_CUDA_TRY(h2d(d_rew, rew, 1));
     SPZ_CUDA_TRY(h2d(d_done, done, 1));
     SPZ_CUDA_TRY(cudaEventRecord(r->ev_copy, r->stream));
-    SPZ_CUDA_TRY(wait_readers());
-    SPZ_CUDA_TRY(account());
-    const int64_t total = nn * R;
-    const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
-    pack_records_kernel<<<blocks, 256, 0, r->stream>>>(r->rec, R, o, m, r->C, start, nn, d_obs, d_act, d_rew, d_nobs, d_done,
-                                                        r->d_fill, std::min(first_idx + n, r->C));
-    SPZ_CUDA_TRY(cudaGetLastError());
-    SPZ_CUDA_TRY(cudaEventRecord(r->ev_pack, r->stream));
-    // return once the caller's buffers are read; the pack may still wait for an in-flight update, and
-    // the next update waits for ev_pack
-    SPZ_CUDA_TRY(cudaEventSynchronize(r->ev_copy));
+    if (r->tags) r->lost_host += skip;
+    r->pend.active = true;
+    r->pend.stage = sg;
+    r->pend.first = first_idx;
+    r->pend.start = start;
+    r->pend.nn = nn;
+    r->pend.fill_after = std::min(first_idx + n, r->C);
+    // the pack waits for the staged data: on the ring stream it follows the copies; a learner stream
+    // that takes it waits for ev_copy (ring_enqueue_pack callers)
+    SPZ_CUDA_TRY(cudaEventSynchronize(r->ev_copy));  // return once the caller's buffers are read
     r->cursor += n;
     return SPZ_OK;
   } else {
@@ -263,7 +316,7 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
       for (int c = 2 * o + m + 2; c < R; ++c) d[c] = 0.f;
     }
     // at most two pieces, split at the wrap point
-    SPZ_CUDA_TRY(wait_readers());
+    SPZ_CUDA_TRY(wait_readers(r));
     SPZ_CUDA_TRY(account());
     const int64_t slot = start % r->C;
     const int64_t n1 = std::min(nn, r->C - slot);
@@ -287,6 +340,10 @@ spz_status spz_replay_sample(spz_replay* r, int64_t batch, uint64_t seed, uint64
   const int64_t F = r->fill();
   if (F < batch || F < 1) return fail(SPZ_ENODATA, "spz_replay_sample: fill " + std::to_string(F) + " < batch " + std::to_string(batch));
   if (batch == 0) return SPZ_OK;
+  {
+    std::lock_guard<std::mutex> lk(r->mu);
+    SPZ_CUDA_TRY(ring_flush_pending(r));  // the last pinned push's records land first
+  }
   const unsigned blocks = (unsigned)cdiv(batch, SAMPLE_ROWS);
   const size_t smem = (size_t)SAMPLE_ROWS * r->R * sizeof(float);
   sample_kernel<<<blocks, 256, smem, r->stream>>>(r->rec, r->R, r->o, r->m, F, seed, step, batch, idx, obs, act, rew,
@@ -315,6 +372,7 @@ spz_status spz_replay_track(spz_replay* r, int32_t on) {
   if (!r) return fail(SPZ_EINVAL, "spz_replay_track: NULL ring");
   DeviceGuard dg(r->device);
   std::lock_guard<std::mutex> lk(r->mu);
+  SPZ_CUDA_TRY(ring_flush_pending(r));  // pushes before the switch are accounted under the old setting
   SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
   for (cudaEvent_t e : r->readers) SPZ_CUDA_TRY(cudaEventSynchronize(e));  // no update still marks the old bitmap
   if (r->tags) cudaFree(r->tags);
@@ -342,6 +400,7 @@ spz_status spz_replay_loss(spz_replay* r, int64_t* pushed, int64_t* lost, int64_
   if (!r->tags) return fail(SPZ_ESTATE, "spz_replay_loss: tracking is off (spz_replay_track)");
   DeviceGuard dg(r->device);
   std::lock_guard<std::mutex> lk(r->mu);
+  SPZ_CUDA_TRY(ring_flush_pending(r));
   for (cudaEvent_t e : r->readers) SPZ_CUDA_TRY(cudaEventSynchronize(e));
   SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
   unsigned long long dl = 0;
@@ -367,7 +426,10 @@ void spz_replay_destroy(spz_replay* r) {
     cudaStreamSynchronize(r->stream);
     cudaFree(r->rec);
     if (r->staging) cudaFreeHost(r->staging);
-    if (r->dstage) cudaFree(r->dstage);
+    for (int sg = 0; sg < 2; ++sg) {
+      if (r->dstage[sg]) cudaFree(r->dstage[sg]);
+      if (r->ev_stage_free[sg]) cudaEventDestroy(r->ev_stage_free[sg]);
+    }
     if (r->d_fill) cudaFree(r->d_fill);
     if (r->h_fill) cudaFreeHost(r->h_fill);
     if (r->tags) cudaFree(r->tags);

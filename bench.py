@@ -251,13 +251,32 @@ def main():
         nc = min(world - 1, max(1, int(round(world * a.critic_frac))))
         kw.update(role=spz.SPZ_ROLE_CRITIC if rank < nc else spz.SPZ_ROLE_ACTOR, n_critic_ranks=nc,
                   n_actor_ranks=world - nc)
-    lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=GB,
-                      device=local, seed=synthdata.SAMPLE_SEED + (0 if (dp or split) else rank), **kw)
     stream = torch.cuda.Stream(device=local)
-    lrn.set_stream(stream.cuda_stream)
-
-    # warm-up (includes CUDA-graph capture)
-    lrn.update(GB, a.warmup)
+    fallback = None
+    try:
+        lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=GB,
+                          device=local, seed=synthdata.SAMPLE_SEED + (0 if (dp or split) else rank), **kw)
+        lrn.set_stream(stream.cuda_stream)
+        # warm-up (includes CUDA-graph capture)
+        lrn.update(GB, a.warmup)
+        ok, err = 1, ""
+    except spz.SpzError as e:
+        ok, err = 0, str(e)
+    if world > 1:
+        t = torch.tensor([ok], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = int(t.item())
+    if not ok:
+        if not (dp or split):
+            raise RuntimeError(err)
+        # the NCCL path failed on some rank: measure independent replicas instead (no collective), and say so
+        fallback = f"{a.mode} path failed ({err or 'on another rank'}); measured {world} independent replicas"
+        dp = split = False
+        GB = B
+        lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=GB,
+                          device=local, seed=synthdata.SAMPLE_SEED + rank)
+        lrn.set_stream(stream.cuda_stream)
+        lrn.update(GB, a.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -387,6 +406,7 @@ def main():
             "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(), "gpu_launches": launches, "last_stats": stats,
             **({"batch_sweep": sweep} if sweep else {}),
+            **({"fallback": fallback} if fallback else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1,0 +1,35 @@
+"""The bench.py contract on CPU: the reference arm (the float64 oracle timed on the host) prints one JSON line
+with the keys the driver reads; the GPU arm's pure helpers (algorithmic FLOPs / bytes, vs_baseline)."""
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "pendulum", "--steps", "2",
+                        "--warmup", "3"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "impl", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "cpu_baseline", "e2e", "config"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "frames/s"
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["vs_baseline"] is None  # pendulum: no paper number
+
+
+def test_class_flops_and_vs_baseline():
+    sys.path.insert(0, ROOT)
+    import bench
+    import synthdata
+    w = synthdata.WORKLOADS["walker"]
+    f = bench.class_flops(w, w.batch)
+    # 2.282 MFLOP per transition for WLK (critic + actor GEMMs)
+    per_t = sum(v for k, v in f.items() if not k.endswith("_mlp")) / w.batch
+    assert abs(per_t / 2.282e6 - 1) < 0.02, per_t
+    assert bench.vs_baseline(w, 3.7e5) == 1.0
+    assert bench.vs_baseline(synthdata.WORKLOADS["ant"], 1.0) is None

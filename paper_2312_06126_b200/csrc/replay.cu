@@ -343,6 +343,7 @@ spz_status spz_replay_sample(spz_replay* r, int64_t batch, uint64_t seed, uint64
   {
     std::lock_guard<std::mutex> lk(r->mu);
     SPZ_CUDA_TRY(ring_flush_pending(r));  // the last pinned push's records land first
+    SPZ_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_pack, 0));  // (or were packed on a learner's stream)
   }
   const unsigned blocks = (unsigned)cdiv(batch, SAMPLE_ROWS);
   const size_t smem = (size_t)SAMPLE_ROWS * r->R * sizeof(float);

@@ -242,11 +242,16 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   pdl_launch();
   __shared__ double red[LOSS_NT / 32][NSTAT];
   __shared__ bool last;
-  const int j0 = blockIdx.x * LOSS_ROWS;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const bool lr = a.loss_rows, ar = a.actor_rows;
   const float alpha = a.td3 ? 0.f : expf(*a.log_alpha);
   const bool td3_on = a.td3 && ((*a.step_p + 1) % a.delay) == 0;
+  double v[NSTAT] = {0, 0, 0, 0, 0, 0};
+  // a grid of a few blocks per SM walks the row blocks (few grid-wide ticket atomics: one same-address
+  // atomic per block serialises in L2, ~20 ns each at thousands of blocks); each warp's statistics
+  // accumulate in row-block order, the block partials are summed in block order -- deterministic
+  for (int jb = blockIdx.x; jb * LOSS_ROWS < a.Bl; jb += gridDim.x) {
+  const int j0 = jb * LOSS_ROWS;
   // ---- loads, all issued before any use: row scalars of the warp's rows (row index clamped, so
   //      every address is valid; rows past Bl are discarded below)
   float qt1[LOSS_RPW], qt2[LOSS_RPW], q1[LOSS_RPW], q2[LOSS_RPW], lp2[LOSS_RPW], rw[LOSS_RPW], dn[LOSS_RPW];
@@ -298,7 +303,6 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
       wv[ci][4] = w1.x, wv[ci][5] = w1.y, wv[ci][6] = w1.z, wv[ci][7] = w1.w;
     }
   }
-  double v[NSTAT] = {0, 0, 0, 0, 0, 0};
   // ---- per row: g_q (every lane), statistics (lane 0), dZ_L chunk of this lane
 #pragma unroll
   for (int i = 0; i < LOSS_RPW; ++i) {
@@ -370,6 +374,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
         }
     }
   }
+  }  // row blocks
   // block partial of the statistics: warps in order
   if (lane == 0)
 #pragma unroll

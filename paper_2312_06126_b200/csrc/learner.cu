@@ -709,7 +709,12 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     // 109.1 -> 108.2 us); larger batches do better with the separate critic_dz_kernel (ANT 319.5 -> 315.4 us)
     const bool dz_in_loss = h <= 256 && Bl <= 16384 && !dz_split_env();
     const int loss_rpw = dz_in_loss ? 1 : 4;
-    const int nblk = (int)cdiv(Bl, LOSS_WARPS * loss_rpw);
+    int nsm_l = 148, dev_l = 0;
+    cudaGetDevice(&dev_l);
+    cudaDeviceGetAttribute(&nsm_l, cudaDevAttrMultiProcessorCount, dev_l);
+    // grid cap: 2 blocks per SM for the statistics-only variant (HUM 138 -> 118 us, ANT 311 -> 306 us per
+    // update); the dZ-writing variant keeps up to 8 per SM (its stores need the parallelism: WLK 1024 blocks)
+    const int nblk = (int)std::min<int64_t>(cdiv(Bl, LOSS_WARPS * loss_rpw), (dz_in_loss ? 8 : 2) * (int64_t)nsm_l);
     {
       LossArgs la{};
       la.qp = qparts;

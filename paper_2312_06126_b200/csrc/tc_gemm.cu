@@ -63,7 +63,9 @@ __device__ __forceinline__ void trace_(int on, int tile_i, int ev) {
 }
 
 // Linear tile index -> (group, m0, n0, split).  Tiles of group g occupy [tile0[g], tile0[g+1]);
-// within a group the M tile varies fastest, then the N tile, then the split.
+// within a group the N tile varies fastest, then the M tile, then the split: the N tiles of one row
+// block run at the same time on neighbouring CTAs, so their common A tile comes from DRAM once and
+// from L2 for the others (h = 512 forward: the 403 MB activation operand is no longer read twice).
 struct TileInfo {
   int grp, m0, n0, split;
 };
@@ -71,10 +73,10 @@ __device__ __forceinline__ TileInfo decode_tile(const TcParams& p, int t, int bn
   int g = 0;
   while (g + 1 < p.a.n_groups && t >= p.tile0[g + 1]) ++g;
   const int r = t - p.tile0[g];
-  const int mt = r % p.mtiles[g];
-  const int rest = r / p.mtiles[g];
-  const int nt = rest % p.ntiles[g];
-  return {g, mt * BM, nt * bn, rest / p.ntiles[g]};
+  const int nt = r % p.ntiles[g];
+  const int rest = r / p.ntiles[g];
+  const int mt = rest % p.mtiles[g];
+  return {g, mt * BM, nt * bn, rest / p.mtiles[g]};
 }
 
 // Write 16 output values of row `row` into a 64-byte-row staging block (64-byte TMA swizzle:

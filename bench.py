@@ -72,24 +72,33 @@ def peaks():
 # ----------------------------------------------------------------------------- algorithmic work per kernel class
 
 def class_flops(w, B):
-    """Algorithmic GEMM FLOPs (2 * M * N * K over the true, unpadded dims) per step, by kernel class."""
+    """Algorithmic GEMM FLOPs (2 * M * N * K over the true, unpadded dims) per step, by kernel class.
+
+    SAC: actor on [s2; s], twin critics on every row kind.  TD3 (averaged over the policy delay): the
+    target actor on s2 every step, the online actor and the actor rows of Q1 (its only critic for the
+    actor loss) on delayed steps only (reading #18)."""
     o, m, h, L = w.obs_dim, w.act_dim, w.hidden, w.n_hidden
     td3 = w.algo == "td3"
+    dly = 1.0 / 2 if td3 else 1.0  # share of steps with actor work (TD3 policy delay 2)
     aout = m if td3 else 2 * m
     cin = o + m
     f = {}
     add = lambda k, v: f.__setitem__(k, f.get(k, 0) + v)
-    Ma = 2 * B  # SAC: [s2; s]; TD3: target actor on s2 + online actor on s (delayed steps)
-    add("actor_fwd_gemm", 2 * Ma * h * o + (L - 1) * 2 * Ma * h * h)
+    mlp = lambda rows, k_in, out: 2 * rows * (h * k_in + (L - 1) * h * h + (h * out if out else 0))
+    # actor forward: SAC [s2; s] every step; TD3 target actor on s2 + online actor on s when delayed
+    Ma = 2 * B if not td3 else B * (1 + dly)
+    add("actor_fwd_gemm", mlp(Ma, o, 0))
     add("actor_head_gemm", 2 * Ma * aout * h)
-    # one launch per layer runs the two target critics (B rows) and the two online critics (2B rows)
-    add("critic_fwd_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))
-    add("critic_fwd_gemm", 2 * (2 * (2 * B) * h * cin + (L - 1) * 2 * (2 * B) * h * h))
-    add("critic_dgrad_gemm", 2 * (L - 1) * 2 * (2 * B) * h * h)
-    add("critic_input_dgrad_gemm", (1 if td3 else 2) * 2 * B * h * m)
+    # critics: targets (2 nets x B rows) and online loss rows (2 x B) every step; actor rows: both
+    # critics (SAC) / Q1 on delayed steps (TD3)
+    crit_rows = 2 * B + 2 * B + (2 * B if not td3 else B * dly)
+    add("critic_fwd_gemm", mlp(crit_rows, cin, 0))
+    dgrad_rows = 2 * B + (2 * B if not td3 else B * dly)
+    add("critic_dgrad_gemm", dgrad_rows * 2 * (L - 1) * h * h)
+    add("critic_input_dgrad_gemm", (2 * B if not td3 else B * dly) * 2 * h * m)
     add("wgrad_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))  # critics ...
-    add("actor_dgrad_gemm", 2 * B * aout * h + (L - 1) * 2 * B * h * h)
-    add("wgrad_gemm", 2 * B * h * o + (L - 1) * 2 * B * h * h + 2 * B * aout * h)  # ... and the actor, one launch
+    add("actor_dgrad_gemm", dly * (2 * B * aout * h + (L - 1) * 2 * B * h * h))
+    add("wgrad_gemm", dly * (2 * B * h * o + (L - 1) * 2 * B * h * h + 2 * B * aout * h))  # ... and the actor
     add("wgrad_gemm", 2 * 2 * B * h)  # critic-head weight gradients (g_q as a one-row operand)
     # fused multi-layer forwards (h <= 256): every hidden layer (+ the actor head) in one launch
     f["actor_fwd_mlp"] = f["actor_fwd_gemm"] + f["actor_head_gemm"]

@@ -26,10 +26,13 @@ def test_class_flops_and_vs_baseline():
     sys.path.insert(0, ROOT)
     import bench
     import synthdata
+    # MFLOP per transition (critic + actor GEMMs; TD3 averaged over the policy delay)
+    for name, ref in (("pendulum", 0.139), ("walker", 2.282), ("ant", 2.335), ("humanoid", 17.60),
+                      ("humanoid_td3", 49.35)):
+        w = synthdata.WORKLOADS[name]
+        f = bench.class_flops(w, w.batch)
+        per_t = sum(v for k, v in f.items() if not k.endswith("_mlp")) / w.batch
+        assert abs(per_t / (ref * 1e6) - 1) < 0.02, (name, per_t)
     w = synthdata.WORKLOADS["walker"]
-    f = bench.class_flops(w, w.batch)
-    # 2.282 MFLOP per transition for WLK (critic + actor GEMMs)
-    per_t = sum(v for k, v in f.items() if not k.endswith("_mlp")) / w.batch
-    assert abs(per_t / 2.282e6 - 1) < 0.02, per_t
     assert bench.vs_baseline(w, 3.7e5) == 1.0
     assert bench.vs_baseline(synthdata.WORKLOADS["ant"], 1.0) is None

@@ -21,7 +21,7 @@ struct HeadEpi {
   float lo, hi;        // log-sigma clamp (SAC)
   float noise, clipc;  // target smoothing (TD3)
   void* Xc;            // critic inputs [3 Bl x ldx]: a~ -> rows Bl.., a' -> rows 2 Bl..
-  float *u, *a, *eps, *sig, *l;  // s-row cache [Bl x m] (TD3 uses a only)
+  float *u, *a, *eps, *sig, *l;  // s-row cache, action-major [m x Bl] (TD3 uses a only)
   float *logp, *logp2;
 };
 
@@ -52,7 +52,7 @@ __device__ __forceinline__ float sac_head_block4(const HeadEpi& h, int r, const 
     lp += -0.5f * e * e - lc - HALF_LN_2PI_F - 2.f * (LN2F - u - softplusf(-2.f * u));
     xa[i] = from_f<T>(a);
     if (!s2row) {
-      const int64_t ci = (int64_t)j * h.m + i;
+      const int64_t ci = (int64_t)i * h.Bl + j;  // action-major [m x Bl]: coalesced over a warp's rows
       h.u[ci] = u;
       h.a[ci] = a;
       h.eps[ci] = e;
@@ -109,7 +109,7 @@ __device__ __forceinline__ void td3_head_block4(const HeadEpi& h, int r, const f
     } else {
       const float a = tanhf(z4[k]);
       xa[i] = from_f<T>(a);
-      h.a[(int64_t)j * h.m + i] = a;
+      h.a[(int64_t)i * h.Bl + j] = a;
     }
   }
 }

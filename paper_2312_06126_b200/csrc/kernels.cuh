@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ r
 // lc = clamp(l, lo, hi); sigma = exp(lc); u = mu + sigma eps; a = tanh u;
 // log pi = sum_i [-eps^2/2 - lc - ln(2 pi)/2 - 2 (ln 2 - u - softplus(-2u))].
 struct HeadCache {
-  float *u, *a, *eps, *sig, *l;  // [Bl x m] each, s-rows only
+  float *u, *a, *eps, *sig, *l;  // [m x Bl] each (action-major: a warp's rows store contiguously), s-rows only
 };
 
 template <typename T>
@@ -121,7 +121,7 @@ __global__ void td3_head_bwd_kernel(const float* __restrict__ dX1, int ldx, int 
   if (e >= (int64_t)Bl * m) return;
   const int64_t j = e / m;
   const int i = (int)(e - j * m);
-  const float a = a_cache[e];
+  const float a = a_cache[(int64_t)i * Bl + j];  // head cache: action-major [m x Bl]
   dH[j * ldh + i] = from_f<T>(dX1[j * ldx + o + i] * (1.f - a * a));
 }
 
@@ -496,10 +496,11 @@ __global__ void sac_head_bwd_kernel(const float* __restrict__ dX1, const float* 
   const int i = (int)(e - j * m);
   const float g_lp = expf(*log_alpha) * invB;
   const float ga = dX1[j * ldx + o + i] + dX2[j * ldx + o + i];
-  const float a = cache.a[e];
+  const int64_t ci = (int64_t)i * Bl + j;  // head cache: action-major [m x Bl]
+  const float a = cache.a[ci];
   const float gu = ga * (1.f - a * a) + 2.f * a * g_lp;
-  const float l = cache.l[e];
-  const float gl = (l >= lo && l <= hi) ? (gu * cache.sig[e] * cache.eps[e] - g_lp) : 0.f;
+  const float l = cache.l[ci];
+  const float gl = (l >= lo && l <= hi) ? (gu * cache.sig[ci] * cache.eps[ci] - g_lp) : 0.f;
   dH[j * ldh + i] = from_f<T>(gu);
   dH[j * ldh + m + i] = from_f<T>(gl);
 }

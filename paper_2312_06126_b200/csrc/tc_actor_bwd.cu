@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(AB_NTHREADS, 1) tc_actor_bwd_kernel(const __gr
       if (hh == 0 && live) {
 #pragma unroll
         for (int i = 0; i < PF; ++i) {
-          const int64_t ci = (int64_t)j * p.m + (i < p.m ? i : 0);
+          const int64_t ci = (int64_t)(i < p.m ? i : 0) * p.Bl + j;  // action-major [m x Bl]
           pa[i] = __ldg(p.a + ci);
           pl[i] = p.td3 ? 0.f : __ldg(p.l + ci);
           ps[i] = p.td3 ? 0.f : __ldg(p.sig + ci);
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(AB_NTHREADS, 1) tc_actor_bwd_kernel(const __gr
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             if (i >= p.m) break;
-            const int64_t ci = (int64_t)j * p.m + i;
+            const int64_t ci = (int64_t)i * p.Bl + j;
             const float a = i < PF ? pa[i < PF ? i : 0] : __ldg(p.a + ci);
             const float gu = ga[off + i] * (1.f - a * a) + 2.f * a * g_lp;
             st_bf16_sw128(Dh, r, i, gu);

@@ -33,7 +33,7 @@ struct ActorBwdArgs {
   const uint32_t* mask[MLP_MAXL];  // actor ReLU masks of the s-rows [Bl x mask_ld] per hidden layer
   void* dZa[MLP_MAXL];             // outputs dZ_l [Bl x h] (pitch h), bf16
   void* dH;                        // output [Bl x ldh], bf16
-  const float *u, *a, *eps, *sig, *l;  // head cache of the s-rows [Bl x m]
+  const float *u, *a, *eps, *sig, *l;  // head cache of the s-rows, action-major [m x Bl]
   const float* log_alpha;
   float invB, lo, hi;
 };

@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   __shared__ __align__(16) float bias_w[S::BIAS ? NUM_EPI_WARPS : 1][S::BIAS ? S::SLICE : 4];
   __shared__ __align__(16) float dotw_w[S::RELU ? NUM_EPI_WARPS : 1][S::RELU ? S::SLICE : 4];
   __shared__ float dotpart[S::RELU ? 2 : 1][S::RELU ? WPQ : 1][S::RELU ? BM : 1];
+  __shared__ float headpart[S::HEAD ? 2 : 1][S::HEAD ? WPQ : 1][S::HEAD ? BM : 1];  // SAC log-pi parts
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NS = p.stages;
@@ -349,23 +350,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       if (e == 0 && lane == 0) trace(tile_i, 2);
       const uint32_t trow = tmem + (uint32_t)b * BUF_COLS + ((uint32_t)(q * 32) << 16);
       if constexpr (S::HEAD) {
-        if (hh == 0) {
-          float hrow[BN];
+        // the WPQ warps of a lane quarter share each row: warp hh takes the Philox blocks of 4 actions
+        // hh, hh + WPQ, ...; the SAC log-pi parts are summed in warp order
+        float hrow[BN];
 #pragma unroll
-          for (int c = 0; c < BN / 16; ++c) {
-            float v[16];
-            if (has_acc) tmem_ld16(trow + c * 16, v);
-            else
+        for (int c = 0; c < BN / 16; ++c) {
+          float v[16];
+          if (has_acc) tmem_ld16(trow + c * 16, v);
+          else
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = 0.f;
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
+          for (int j = 0; j < 16; ++j) hrow[c * 16 + j] = v[j] + bias_s[c * 16 + j];
+        }
+        tc_fence_before();
+        const bool live = m < g.M;
+        if (a.epi == EPI_SAC_HEAD) {
+          const float lp = live ? sac_head_blocks<__nv_bfloat16>(a.head, g.row0 + m, hrow, hrow + a.head.m, hh, WPQ) : 0.f;
+          const int pb = tile_i & 1;
+          headpart[pb][hh][r] = lp;
+          named_bar(2 + q, WPQ * 32);
+          if (hh == 0 && live) {
+            float tot = 0.f;
+#pragma unroll
+            for (int k = 0; k < WPQ; ++k) tot += headpart[pb][k][r];
+            sac_head_logp(a.head, g.row0 + m, tot);
           }
-          tc_fence_before();
-          if (m < g.M) {
-            if (a.epi == EPI_SAC_HEAD) sac_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow, hrow + a.head.m);
-            else td3_head_row<__nv_bfloat16>(a.head, g.row0 + m, hrow);
-          }
+        } else if (live) {
+          td3_head_blocks<__nv_bfloat16>(a.head, g.row0 + m, hrow, hh, WPQ);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[b]);

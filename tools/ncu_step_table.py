@@ -30,8 +30,11 @@ def main(rep):
                 vals.append("-")
                 continue
             v = float(d[m].replace(",", ""))
+            u = units[h.index(m)]
             if sc is None:
-                v *= SCALE.get(units[h.index(m)], 1.0)
+                v *= SCALE.get(u, 1.0)
+            elif m == "gpu__time_duration.sum":
+                v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u, 1.0)
             vals.append(f"{v:.3g}" if m != "launch__grid_size" else str(int(v)))
         print(f"| {d['ID']} | `{name}` | " + " | ".join(vals) + " |")
 

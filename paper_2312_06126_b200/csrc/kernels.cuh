@@ -215,6 +215,7 @@ struct LossArgs {
   void* dZ[2];
   float gamma, invB;
   int Bl, td3, delay, loss_rows, actor_rows, h, ld, mask_ld;
+  int q2_no_actor;        // TD3: Q2 has no actor rows (its dZ_L there is never read)
   int qp;                 // q partials per row (fused row dot over qp 256-column tiles), summed in tile order
   int64_t qps_tg, qps_on;  // partial strides of the target / online q buffers
 };
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
 #pragma unroll
         for (int kind = 0; kind < 2; ++kind) {
           if (kind == 0 ? !lr : !ar) continue;
+          if (kind == 1 && ci == 1 && a.q2_no_actor) continue;
           const int64_t row = (int64_t)(kind ? a.Bl : 0) + j;
           const float gq = g[ci][kind];
           const uint32_t mb = mk[i][ci][kind];
@@ -433,6 +435,7 @@ struct DzArgs {
   const float* w[2];
   void* dZ[2];
   int64_t r0, rows;
+  int64_t q2_end;  // critic 1 (Q2) rows end here (TD3: the loss rows only)
   int hv, ld, mask_ld;
 };
 
@@ -465,6 +468,7 @@ __global__ void __launch_bounds__(256) critic_dz_kernel(const __grid_constant__ 
   }
 #pragma unroll
   for (int ci = 0; ci < 2; ++ci) {
+    if (ci == 1 && row >= a.q2_end) continue;
     T* dZ = static_cast<T*>(a.dZ[ci]) + row * a.ld + n;
     if constexpr (std::is_same<T, __nv_bfloat16>::value) {
       uint4 o;

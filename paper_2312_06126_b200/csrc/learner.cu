@@ -549,6 +549,13 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     // online-critic rows [on0, on0 + Mon): loss rows [0, Bl) on the critic side, actor rows [Bl, 2Bl)
     const int on0 = do_critic ? 0 : Bl;
     const int Mon = (do_critic ? Bl : 0) + (do_actor ? Bl : 0);
+    // TD3's actor loss uses Q1 alone (reading #18): Q2 never sees the actor rows (forward, dZ_L, dgrad)
+    const bool fuse_loss_env = [] {
+      const char* fl = std::getenv("SPZ_FUSE_CRITIC_LOSS");
+      return fl && std::atoi(fl) == 1;
+    }();
+    const bool q2_skip_actor = td3 && !fuse_loss_env;
+    const int Mon2 = q2_skip_actor ? (do_critic ? Bl : 0) : Mon;  // online rows of Q2
     bool cfused = false, lfused = false;  // fused critic forward / fused critic loss
     if (bits && (do_critic || do_actor)) {
       // fused multi-layer critic forward: online loss rows (activations + masks stored), online
@@ -563,6 +570,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         if (kind == 1 && !do_actor) continue;
         if (kind == 2 && !do_critic) continue;
         for (int i = 0; i < 2; ++i) {
+          if (kind == 1 && i == 1 && q2_skip_actor) continue;
           const int id = kind == 2 ? NET_Q1T + i : NET_Q1 + i;
           const int64_t xr = kind * (int64_t)Bl;          // row in Xc
           const int64_t ar = kind == 2 ? 0 : kind * (int64_t)Bl;  // row in the per-critic buffers
@@ -660,7 +668,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
             void* dst = Ta(tgt ? Lr->Atg[i][l] : Lr->Aon[i][l], ra, h);
             const void* src = l == 0 ? (const void*)Ta(Lr->Xc, r0c, ldc)
                                      : (const void*)Ta(tgt ? Lr->Atg[i][l - 1] : Lr->Aon[i][l - 1], ra, h);
-            GemmGroup& g = add(a, src, l == 0 ? ldc : h, Wp(id, l), cn.ld[l], dst, h, tgt ? Bl : Mon, h, bp(id, l));
+            GemmGroup& g = add(a, src, l == 0 ? ldc : h, Wp(id, l), cn.ld[l], dst, h, tgt ? Bl : (i ? Mon2 : Mon), h, bp(id, l));
             if (bits && !tgt) {
               g.mask_out = Lr->mask_c[i][l] + (int64_t)ra * mw;
               g.mask_ld = mw;
@@ -718,6 +726,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     {
       LossArgs la{};
       la.qp = qparts;
+      la.q2_no_actor = q2_skip_actor;
       la.qps_tg = Lr->max_local;
       la.qps_on = 2 * Lr->max_local;
       la.qt1 = Lr->q_tg[0];
@@ -781,6 +790,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         }
         da.r0 = do_critic ? 0 : Bl;
         da.rows = (int64_t)(do_critic ? Bl : 0) + (do_actor ? Bl : 0);
+        da.q2_end = q2_skip_actor ? (int64_t)Bl : da.r0 + da.rows;
         da.hv = h / 8;
         da.ld = h;
         da.mask_ld = mw;
@@ -838,10 +848,10 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         GemmArgs a = mk(h, bits ? EPI_MASK_BITS : EPI_MASK, 0, 1);
         for (int i = 0; i < 2; ++i) {
           if (bits)
-            add(a, Ta(Lr->dZc[i][l], on0, h), h, Wp(NET_Q1 + i, l), cn.ld[l], Ta(Lr->dZc[i][l - 1], on0, h), h, Mon, h,
+            add(a, Ta(Lr->dZc[i][l], on0, h), h, Wp(NET_Q1 + i, l), cn.ld[l], Ta(Lr->dZc[i][l - 1], on0, h), h, i ? Mon2 : Mon, h,
                 nullptr, Lr->mask_c[i][l - 1] + (int64_t)on0 * mw, mw);
           else
-            add(a, Ta(Lr->dZc[i][l], on0, h), h, Wp(NET_Q1 + i, l), cn.ld[l], Ta(Lr->dZc[i][l - 1], on0, h), h, Mon, h,
+            add(a, Ta(Lr->dZc[i][l], on0, h), h, Wp(NET_Q1 + i, l), cn.ld[l], Ta(Lr->dZc[i][l - 1], on0, h), h, i ? Mon2 : Mon, h,
                 nullptr, Ta(Lr->Aon[i][l - 1], on0, h), h);
         }
         if (bits && !empty_gemm(a) && !tc_ok(a)) return fail(SPZ_EUNSUPPORTED, "internal: critic dgrad not supported by the tcgen05 kernel");

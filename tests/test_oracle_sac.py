@@ -378,3 +378,48 @@ def test_temperature_moves_toward_target_entropy():
     for _ in range(20):
         st, stats, _ = sac.sac_step(st, ring, 256, 1, cfg)
     assert st.log_alpha < -0.15
+
+
+# ----------------------------------------------------------------------------- DDPG (f4)
+
+def test_ddpg_grads_match_torch_autograd():
+    from oracle import ddpg
+    cfg, r, st = small_problem("td3")
+    B = 40
+    idx, batch = r.sample(B, 6126, 0)
+    grads, sums = ddpg.ddpg_grads(st, batch, cfg, B)
+    ash, csh = sac.actor_shapes(cfg, td3=True), sac.critic_shapes(cfg)
+    s, a, rr, s2, d = [torch.tensor(np.asarray(batch[kk], np.float64)) for kk in ("obs", "act", "rew", "next_obs", "done")]
+    A = _tp(st.actor, ash, True)
+    At = _tp(st.actor_targ, ash, False)
+    Q1 = _tp(st.q1, csh, True)
+    Q1t = _tp(st.q1_targ, csh, False)
+    with torch.no_grad():
+        y = rr + cfg.gamma * (1 - d) * _torch_mlp(Q1t, torch.cat([s2, torch.tanh(_torch_mlp(At, s2))], 1))[:, 0]
+    LQ = ((_torch_mlp(Q1, torch.cat([s, a], 1))[:, 0] - y) ** 2).mean()
+    Q1d = [(W.detach(), b.detach()) for W, b in Q1]
+    Lpi = -_torch_mlp(Q1d, torch.cat([s, torch.tanh(_torch_mlp(A, s))], 1))[:, 0].mean()
+    (LQ + Lpi).backward()
+    flat = lambda P: np.concatenate([np.concatenate([W.grad.numpy().ravel(), b.grad.numpy()]) for W, b in P])
+    assert np.allclose(grads["q1"], flat(Q1), rtol=1e-10, atol=1e-13)
+    assert np.allclose(grads["actor"], flat(A), rtol=1e-10, atol=1e-13)
+    assert np.isclose(sums["lq"] / B, LQ.item(), rtol=1e-12) and np.isclose(sums["lpi"] / B, Lpi.item(), rtol=1e-12)
+
+
+def test_ddpg_equals_td3_with_tied_twins_no_delay_no_noise():
+    """DDPG is TD3 with policy delay 1, no target smoothing and the twin critic tied to the first: with
+    Q2 = Q1 (and Q2' = Q1') the twins receive identical updates, min(Q1', Q2') = Q1', and TD3's critic
+    loss is twice DDPG's.  (The GPU path runs DDPG exactly this way.)"""
+    from oracle import ddpg
+    cfg, r, st = small_problem("td3")
+    cfg.td3_policy_delay, cfg.td3_noise, cfg.td3_noise_clip = 1, 0.0, 0.0
+    st_t = sac.State.create(st.actor, st.q1, st.q1, log_alpha=0.0, actor_targ=st.actor)
+    st_d = st_t.copy()
+    for _ in range(4):
+        st_t, s_t, _ = td3.td3_step(st_t, r, 48, 6126, cfg)
+        st_d, s_d, _ = ddpg.ddpg_step(st_d, r, 48, 6126, cfg)
+        assert np.isclose(s_t["critic_loss"], 2 * s_d["critic_loss"], rtol=1e-12)
+        assert np.isclose(s_t["actor_loss"], s_d["actor_loss"], rtol=1e-12)
+    for n in ("actor", "q1", "q1_targ", "actor_targ"):
+        assert np.allclose(getattr(st_t, n), getattr(st_d, n), rtol=0, atol=1e-14), n
+    assert np.array_equal(st_t.q1, st_t.q2)

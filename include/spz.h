@@ -106,11 +106,16 @@ spz_status spz_replay_loss(spz_replay* r, int64_t* pushed, int64_t* lost, int64_
 void spz_replay_destroy(spz_replay* r);
 
 /* ------------------------------------------------------------------ learner
- * One SAC (or TD3) update step per the oracle, Jacobi order:
+ * One SAC (or TD3, DDPG) update step per the oracle, Jacobi order:
  * all losses at (theta_k, phi_k, alpha_k), then Adam on each trained network
  * (own step counter), then Polyak theta' <- tau theta + (1-tau) theta'.
+ * DDPG (§8(f) f4, oracle/ddpg.py: one critic, no target smoothing, no policy delay) runs on the TD3
+ * kernels with the twin critic tied to the first: Q2 = Q1 and Q2' = Q1' at creation and on every
+ * spz_set_params of Q1 / Q1_TARG (setting Q2 / Q2_TARG directly is SPZ_EINVAL), so both receive
+ * identical updates and min(Q1', Q2') = Q1'; the reported critic_loss is DDPG's (half the twins' sum).
+ * spz_config_default(SPZ_DDPG) sets td3_policy_delay = 1 and td3_noise = td3_noise_clip = 0.
  */
-typedef enum { SPZ_SAC = 0, SPZ_TD3 = 1 } spz_algo;
+typedef enum { SPZ_SAC = 0, SPZ_TD3 = 1, SPZ_DDPG = 2 } spz_algo;
 /* FP32: GEMMs in full fp32 (exact-order-independent fp32 FMA); BF16: GEMM operands
  * rounded to bf16 (RNE) on tcgen05 tensor cores with fp32 accumulation; every
  * epilogue, master weight and optimizer state stays fp32 (reading #15). */

@@ -109,6 +109,7 @@ struct spz_learner {
   int device = 0;
   cudaStream_t own_stream = nullptr, stream = nullptr;
   bool td3 = false, bf16 = false;
+  bool ddpg = false;  // TD3 kernels with the twin critic tied to the first (spz.h)
   int o = 0, m = 0, h = 0, L = 0;
   size_t esz = 4;
   int64_t max_local = 0;  // rows handled by this rank at max_batch
@@ -1263,9 +1264,9 @@ spz_status spz_config_default(spz_algo algo, int32_t obs_dim, int32_t act_dim, s
   out->target_entropy = -(double)act_dim;
   out->log_std_min = -20.0;
   out->log_std_max = 2.0;
-  out->td3_noise = 0.2;
-  out->td3_noise_clip = 0.5;
-  out->td3_policy_delay = 2;
+  out->td3_noise = algo == SPZ_DDPG ? 0.0 : 0.2;
+  out->td3_noise_clip = algo == SPZ_DDPG ? 0.0 : 0.5;
+  out->td3_policy_delay = algo == SPZ_DDPG ? 1 : 2;
   out->seed = 6126;
   out->init_seed = 0;
   out->device = 0;
@@ -1298,7 +1299,8 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     if ((cfg->rank < nc) != (cfg->role == SPZ_ROLE_CRITIC))
       return fail(SPZ_EINVAL, "spz_learner_create: ranks [0, n_critic_ranks) must be critic, the others actor");
   }
-  if (cfg->algo != SPZ_SAC && cfg->algo != SPZ_TD3) return fail(SPZ_EINVAL, "spz_learner_create: unknown algo");
+  if (cfg->algo != SPZ_SAC && cfg->algo != SPZ_TD3 && cfg->algo != SPZ_DDPG)
+    return fail(SPZ_EINVAL, "spz_learner_create: unknown algo");
   if (cfg->precision != SPZ_FP32 && cfg->precision != SPZ_BF16) return fail(SPZ_EINVAL, "spz_learner_create: unknown precision");
   spz_status st = check_device(cfg->device);
   if (st != SPZ_OK) return st;
@@ -1307,7 +1309,8 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   Lr->cfg = *cfg;
   Lr->ring = ring;
   Lr->device = cfg->device;
-  Lr->td3 = cfg->algo == SPZ_TD3;
+  Lr->td3 = cfg->algo == SPZ_TD3 || cfg->algo == SPZ_DDPG;
+  Lr->ddpg = cfg->algo == SPZ_DDPG;
   Lr->bf16 = cfg->precision == SPZ_BF16;
   Lr->esz = Lr->bf16 ? 2 : 4;
   Lr->o = cfg->obs_dim;
@@ -1518,6 +1521,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     return cudaMemcpyAsync(Lr->P + Lr->pbase[dst], Lr->P + Lr->pbase[src], Lr->net[src].np * sizeof(float),
                            cudaMemcpyDeviceToDevice, Lr->stream);
   };
+  if (Lr->ddpg) SPZ_CUDA_TRY(copy_net(NET_Q2, NET_Q1));  // the tied twin
   SPZ_CUDA_TRY(copy_net(NET_Q1T, NET_Q1));
   SPZ_CUDA_TRY(copy_net(NET_Q2T, NET_Q2));
   if (Lr->td3) SPZ_CUDA_TRY(copy_net(NET_ACTORT, NET_ACTOR));
@@ -1563,7 +1567,7 @@ static spz_status update_finish(spz_learner* Lr, spz_stats* last) {
   if (last) {
     const StatsOut& s = *Lr->h_stats;
     last->step = (int64_t)s.step;
-    last->critic_loss = s.critic_loss;
+    last->critic_loss = Lr->ddpg ? 0.5 * s.critic_loss : s.critic_loss;  // DDPG: one critic (tied twins)
     last->actor_loss = s.actor_loss;
     last->alpha = s.alpha;
     last->alpha_loss = s.alpha_loss;
@@ -1695,8 +1699,16 @@ spz_status spz_set_params(spz_learner* Lr, spz_tensor t, spz_slot s, const float
   int64_t cnt;
   SPZ_TRY(tensor_region(Lr, t, s, &base, &cnt));
   if (n != cnt) return fail(SPZ_EINVAL, "spz_set_params: expected " + std::to_string(cnt) + " floats, got " + std::to_string(n));
+  if (Lr->ddpg && (t == SPZ_T_Q2 || t == SPZ_T_Q2_TARG))
+    return fail(SPZ_EINVAL, "spz_set_params: DDPG's second critic is tied to the first (set Q1 / Q1_TARG)");
   SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
   SPZ_CUDA_TRY(cudaMemcpyAsync(base, host_in, cnt * sizeof(float), cudaMemcpyHostToDevice, Lr->stream));
+  if (Lr->ddpg && (t == SPZ_T_Q1 || t == SPZ_T_Q1_TARG)) {  // keep the twin tied (parameters and Adam state)
+    float* twin;
+    int64_t tc;
+    SPZ_TRY(tensor_region(Lr, t == SPZ_T_Q1 ? SPZ_T_Q2 : SPZ_T_Q2_TARG, s, &twin, &tc));
+    SPZ_CUDA_TRY(cudaMemcpyAsync(twin, host_in, cnt * sizeof(float), cudaMemcpyHostToDevice, Lr->stream));
+  }
   SPZ_TRY(refresh_shadows(Lr));
   SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
   return SPZ_OK;

@@ -20,7 +20,8 @@ SPZ_OK, SPZ_EINVAL, SPZ_ENODATA, SPZ_ENONFINITE, SPZ_ECUDA, SPZ_ENCCL, SPZ_ENOME
     0, -1, -2, -3, -4, -5, -6, -7, -8, -9)
 STATUS_NAMES = {0: "SPZ_OK", -1: "SPZ_EINVAL", -2: "SPZ_ENODATA", -3: "SPZ_ENONFINITE", -4: "SPZ_ECUDA",
                 -5: "SPZ_ENCCL", -6: "SPZ_ENOMEM", -7: "SPZ_ESTATE", -8: "SPZ_ETIMEOUT", -9: "SPZ_EUNSUPPORTED"}
-SPZ_SAC, SPZ_TD3 = 0, 1
+SPZ_SAC, SPZ_TD3, SPZ_DDPG = 0, 1, 2
+ALGOS = {"sac": SPZ_SAC, "td3": SPZ_TD3, "ddpg": SPZ_DDPG}
 SPZ_FP32, SPZ_BF16 = 0, 1
 SPZ_ROLE_ALL, SPZ_ROLE_CRITIC, SPZ_ROLE_ACTOR = 0, 1, 2
 SPZ_T_ACTOR, SPZ_T_Q1, SPZ_T_Q2, SPZ_T_Q1_TARG, SPZ_T_Q2_TARG, SPZ_T_ACTOR_TARG, SPZ_T_LOG_ALPHA = range(7)
@@ -387,7 +388,7 @@ PARAM_TENSORS = {"actor": SPZ_T_ACTOR, "q1": SPZ_T_Q1, "q2": SPZ_T_Q2, "q1_targ"
 class Learner:
     def __init__(self, ring: Replay, algo="sac", precision="bf16", hidden=256, n_hidden=2, max_batch=8192,
                  device=0, use_graph=True, **overrides):
-        cfg = spz_config_default(SPZ_SAC if algo == "sac" else SPZ_TD3, ring.obs_dim, ring.act_dim)
+        cfg = spz_config_default(ALGOS[algo], ring.obs_dim, ring.act_dim)
         cfg.precision = SPZ_BF16 if precision == "bf16" else SPZ_FP32
         cfg.hidden, cfg.n_hidden, cfg.max_batch, cfg.device = hidden, n_hidden, max_batch, device
         cfg.use_graph = 1 if use_graph else 0
@@ -475,7 +476,7 @@ class Policy:
 
     def __init__(self, obs_dim, act_dim, algo="sac", precision="bf16", hidden=256, n_hidden=2, max_batch=4096,
                  device=0, log_std_min=-20.0, log_std_max=2.0, expl_noise=0.1):
-        d = spz_policy_desc(SPZ_SAC if algo == "sac" else SPZ_TD3, SPZ_BF16 if precision == "bf16" else SPZ_FP32,
+        d = spz_policy_desc(ALGOS[algo], SPZ_BF16 if precision == "bf16" else SPZ_FP32,
                             obs_dim, act_dim, hidden, n_hidden, max_batch, device, log_std_min, log_std_max,
                             expl_noise)
         self.obs_dim, self.act_dim = obs_dim, act_dim

@@ -46,6 +46,8 @@ def test_config_default_values():
     assert c.target_entropy == -6.0 and c.alpha_auto == 1 and c.log_std_min == -20 and c.log_std_max == 2
     t = spz.spz_config_default(spz.SPZ_TD3, 44, 17)
     assert t.td3_noise == 0.2 and t.td3_noise_clip == 0.5 and t.td3_policy_delay == 2 and t.alpha_auto == 0
+    dd = spz.spz_config_default(spz.SPZ_DDPG, 22, 6)  # f4: TD3 kernels, no delay, no target smoothing
+    assert dd.td3_policy_delay == 1 and dd.td3_noise == 0.0 and dd.td3_noise_clip == 0.0 and dd.alpha_auto == 0
     with pytest.raises(spz.SpzError):
         spz.spz_config_default(spz.SPZ_SAC, 0, 6)
 

@@ -239,6 +239,41 @@ def test_sac_parity_pair_schedule_critic_forward(B, monkeypatch):
     run_parity("sac", "bf16", 22, 6, 256, 2, B, 20_000, 2, check_moments=False)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("h,L,B", [(64, 2, 256), (256, 2, 1000)])
+def test_ddpg_parity(precision, h, L, B):
+    """DDPG (f4) on the TD3 kernels with the twin critic tied to the first, against oracle/ddpg.py (one
+    critic).  Also: the twin stays bit-identical to the first critic, and setting it directly is refused."""
+    from oracle import ddpg as oddpg
+    o, m, C, K = 22, 6, 6000, 4
+    g, r = make_rings(o, m, C)
+    p = synthdata.init_params(o, m, h, L, algo="td3")
+    lrn = spz.Learner(g, algo="ddpg", precision=precision, hidden=h, n_hidden=L, max_batch=B)
+    lrn.set("actor", p["actor"])
+    lrn.set("actor_targ", p["actor"])
+    lrn.set("q1", p["q1"])
+    lrn.set("q1_targ", p["q1"])
+    with pytest.raises(spz.SpzError) as e:
+        lrn.set("q2", p["q2"])
+    assert e.value.status == spz.SPZ_EINVAL
+    cfg = osac.Config(obs_dim=o, act_dim=m, hidden=h, n_hidden=L, alpha_auto=False, td3_policy_delay=1,
+                      td3_noise=0.0, td3_noise_clip=0.0)
+    st = osac.State.create(p["actor"], p["q1"], p["q1"], log_alpha=0.0, actor_targ=p["actor"])
+    tol = TOL[precision]
+    for k in range(K):
+        gs = lrn.update(B, 1)
+        st, os_, _ = oddpg.ddpg_step(st, r, B, synthdata.SAMPLE_SEED, cfg)
+        for key in ("critic_loss", "actor_loss", "q1_mean"):
+            ref = os_[key]
+            scale = max(abs(ref), os_.get(key + "_abs", 0.0))
+            assert abs(gs[key] - ref) <= tol * max(scale, 1e-6) + (tol * 1e-2 if key == "q1_mean" else 0), (k, key, gs[key], ref)
+    for n in ("actor", "q1", "q1_targ", "actor_targ"):
+        assert rel(lrn.get(n), getattr(st, n)) <= tol, n
+    assert np.array_equal(lrn.get("q1"), lrn.get("q2")) and np.array_equal(lrn.get("q1_targ"), lrn.get("q2_targ"))
+    c = lrn.counters()
+    assert c["step"] == K and c["t_critic"] == K and c["t_actor"] == K
+
+
 def test_sac_parity_graph_vs_eager_bit_identical():
     outs = []
     for use_graph in (True, False):

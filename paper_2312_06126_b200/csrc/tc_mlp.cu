@@ -5,7 +5,7 @@
 //               input tile and the weight slab, deeper layers only the weight slab
 //   warp 1      TMEM allocator + MMA issuer: A from the stage (layer 0) or from the hidden buffer H
 //               (deeper layers), accumulator in TMEM buffer (unit & 1); one acc_full commit per layer
-//   warps 2..9  epilogue: TMEM lane quarter (warp % 4) x column half; per hidden layer bias + ReLU ->
+//   warps 2..  epilogue (4 x WPQ warps): TMEM lane quarter (warp % 4) x column slice; per hidden layer bias + ReLU ->
 //               H (128B-swizzled K-major bf16, the next layer's A operand) + packed masks + row dot;
 //               activations leave by TMA bulk stores from H; the actor head runs on the last MMA.
 // Ordering: H is single-buffered.  The epilogue of (unit u, layer l) writes H only after the MMA of
@@ -26,7 +26,12 @@ namespace spz {
 namespace {
 
 constexpr int MBM = 128, MBK = 64, MSTAGES = 4;
-constexpr int M_EPI_WARPS = 8, M_NTHREADS = 64 + M_EPI_WARPS * 32;
+// Epilogue warps: WPQ per TMEM lane quarter (each owns H / WPQ columns of its 32 rows); 4 per quarter
+// at h >= 128 (the per-layer epilogue is instruction-issue bound), 2 at h = 64 (a warp keeps whole
+// 32-column mask words).
+template <int H>
+constexpr int mlp_wpq() { return H >= 128 ? 4 : 2; }
+constexpr int mlp_threads(int wpq) { return 64 + 4 * wpq * 32; }
 constexpr int MA_BYTES = MBM * MBK * 2;  // 16 KB input tile per k-block
 
 struct MlpDev {
@@ -126,6 +131,13 @@ __device__ __forceinline__ float hidden_epi(uint32_t trow, int c_lo, int r, uint
   return dot;
 }
 
+// fixed-order sum of the WPQ per-warp partials of row r of a lane quarter
+template <int WPQ>
+__device__ __forceinline__ float quarter_sum(const float (*part)[MBM], int r) {
+  if constexpr (WPQ == 4) return (part[0][r] + part[1][r]) + (part[2][r] + part[3][r]);
+  else return part[0][r] + part[1][r];
+}
+
 __device__ __forceinline__ int su_kind(const MlpParams& p, int su) {
   int k = 0;
   while (k + 1 < p.n_grp && su >= p.su0[k + 1]) ++k;
@@ -137,16 +149,16 @@ __device__ __forceinline__ int su_kind(const MlpParams& p, int su) {
 // 2 (q_i - y) / B; actor rows: g_qi = -w_i / B ((1,0) | (0,1) | (1/2,1/2) on a tie; TD3: q1 only,
 // delayed steps).  Then dZ_L[ci] = g_qci w_ci 1[A_L > 0] (masks of this launch's online passes),
 // written through H by TMA, and the block's statistics partial (fixed order).
-template <int H>
+template <int H, int WPQ>
 __device__ __forceinline__ void loss_epilogue(const MlpParams& p, int kind, int su, int m0, int r, int hh, int e,
                                               int lane, uint8_t* Hs, float (*qv_s)[MBM], float* dot_s,
                                               double (*red_s)[NSTAT]) {
-  constexpr int CPW = H / 16 / 2, NB = CPW / 2, SLICE = CPW * 16;
+  constexpr int EW = 4 * WPQ, CPW = H / 16 / WPQ, NB = CPW / 2, SLICE = CPW * 16;
   const MlpLoss& a = p.loss;
   const int lk = p.gloss[kind];
   const int j = m0 + r;
   const bool valid = j < a.Bl;
-  named_bar(1, M_EPI_WARPS * 32);  // every pass's q of this block is in qv_s
+  named_bar(1, EW * 32);  // every pass's q of this block is in qv_s
   double v[NSTAT] = {0, 0, 0, 0, 0, 0};
   float g[2] = {0.f, 0.f};
   if (valid) {
@@ -203,7 +215,7 @@ __device__ __forceinline__ void loss_epilogue(const MlpParams& p, int kind, int 
 #pragma unroll
     for (int c = lane; c < SLICE; c += 32) dot_s[c] = a.w[ci][c_lo * 16 + c];
     if (e == 0 && lane == 0) bulk_wait_read0();  // H free of earlier TMA stores
-    named_bar(1, M_EPI_WARPS * 32);
+    named_bar(1, EW * 32);
     const float gq = g[ci];
 #pragma unroll
     for (int ib = 0; ib < NB; ++ib) {
@@ -224,7 +236,7 @@ __device__ __forceinline__ void loss_epilogue(const MlpParams& p, int kind, int 
             make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
     }
     fence_async_smem();
-    named_bar(1, M_EPI_WARPS * 32);
+    named_bar(1, EW * 32);
     if (e == 0 && lane == 0) {
 #pragma unroll
       for (int sl = 0; sl < H / 64; ++sl) tma_store_2d(&p.tdz[ci][lk - 1], Hs + sl * 16384, sl * 64, m0);
@@ -237,11 +249,11 @@ __device__ __forceinline__ void loss_epilogue(const MlpParams& p, int kind, int 
   if (lane == 0)
 #pragma unroll
     for (int i = 0; i < NSTAT; ++i) red_s[e][i] = v[i];
-  named_bar(1, M_EPI_WARPS * 32);
+  named_bar(1, EW * 32);
   if (e == 0 && lane == 0)
     for (int i = 0; i < NSTAT; ++i) {
       double t = 0.0;
-      for (int k = 0; k < M_EPI_WARPS; ++k) t += red_s[k][i];
+      for (int k = 0; k < EW; ++k) t += red_s[k][i];
       a.partials[(int64_t)su * NSTAT + i] = t;
     }
 }
@@ -249,6 +261,7 @@ __device__ __forceinline__ void loss_epilogue(const MlpParams& p, int kind, int 
 // After the last super-unit of every CTA: the last CTA to finish sums the statistics partials in
 // block order into the step totals and snapshots the counters, log alpha and the Adam bias
 // corrections for the optimizer (critic_loss_kernel's tail).
+template <int EW>
 __device__ __forceinline__ void loss_finish(const MlpParams& p, int e, int lane, double (*red_s)[NSTAT], bool& last) {
   const MlpLoss& a = p.loss;
   const int tid = e * 32 + lane;
@@ -256,11 +269,11 @@ __device__ __forceinline__ void loss_finish(const MlpParams& p, int e, int lane,
     fence_acq_rel_gpu();  // this thread wrote every partial of this CTA
     last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
   }
-  named_bar(1, M_EPI_WARPS * 32);
+  named_bar(1, EW * 32);
   if (!last) return;
   fence_acq_rel_gpu();
   double t[NSTAT] = {0, 0, 0, 0, 0, 0};
-  for (int su = tid; su < p.total_su; su += M_EPI_WARPS * 32)
+  for (int su = tid; su < p.total_su; su += EW * 32)
 #pragma unroll
     for (int i = 0; i < NSTAT; ++i) t[i] += __ldcg(a.partials + (int64_t)su * NSTAT + i);
 #pragma unroll
@@ -268,10 +281,10 @@ __device__ __forceinline__ void loss_finish(const MlpParams& p, int e, int lane,
   if (lane == 0)
 #pragma unroll
     for (int i = 0; i < NSTAT; ++i) red_s[e][i] = t[i];
-  named_bar(1, M_EPI_WARPS * 32);
+  named_bar(1, EW * 32);
   if (tid < NSTAT) {
     double u = 0.0;
-    for (int k = 0; k < M_EPI_WARPS; ++k) u += red_s[k][tid];
+    for (int k = 0; k < EW; ++k) u += red_s[k][tid];
     a.totals[tid] = u;
   }
   if (tid == 0) *a.ticket = 0u;
@@ -287,21 +300,22 @@ __device__ __forceinline__ void loss_finish(const MlpParams& p, int e, int lane,
 
 // H: hidden width of this instantiation; ACTOR: the last MMA layer is the actor head (else: critic,
 // row-dot head fused into the last hidden layer's epilogue).
-template <int H, bool ACTOR>
-__global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_constant__ MlpParams p) {
+template <int H, bool ACTOR, int WPQ>
+__global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __grid_constant__ MlpParams p) {
   constexpr int STAGE = H * MBK * 2;  // one weight slab (largest layer) per ring stage
   constexpr uint32_t BUF = H < 32 ? 32 : H;      // TMEM columns per accumulator buffer
   constexpr uint32_t TMEM_COLS = 2 * BUF <= 64 ? 64 : 2 * BUF <= 128 ? 128 : 2 * BUF <= 256 ? 256 : 512;
   constexpr int SLABS = H / 64;                  // 64-column slabs of H (16 KB each)
-  constexpr int CPW = H / 16 / 2;                // 16-column chunks per epilogue warp (two per quarter)
+  constexpr int EW = 4 * WPQ;                    // epilogue warps
+  constexpr int CPW = H / 16 / WPQ;              // 16-column chunks per epilogue warp
   constexpr int NB = CPW / 2;                    // 32-column blocks (= mask words) per warp
   constexpr int SLICE = CPW * 16;
   static_assert(H % 64 == 0 && H <= 256, "hidden width");
-  __shared__ __align__(16) float bias_w[M_EPI_WARPS][SLICE > 16 ? SLICE : 16];
-  __shared__ __align__(16) float dotw_w[M_EPI_WARPS][SLICE];
-  __shared__ float dotpart[2][2][MBM];
+  __shared__ __align__(16) float bias_w[EW][SLICE > 16 ? SLICE : 16];
+  __shared__ __align__(16) float dotw_w[EW][SLICE];
+  __shared__ float dotpart[2][WPQ][MBM];
   __shared__ float qv_s[4][MBM];                    // critic groups: q of each pass, per row
-  __shared__ double red_s[M_EPI_WARPS][NSTAT];      // statistics reduction
+  __shared__ double red_s[EW][NSTAT];      // statistics reduction
   __shared__ bool last_s;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -336,7 +350,7 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], M_EPI_WARPS);
+      mbar_init(&acc_empty[b], EW);
     }
     mbar_init(h_full, 1);
     mbar_init(x_full, 1);
@@ -529,15 +543,15 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
         tc_fence_after();
         if (e == 0 && lane == 0) mtrace(p.trace, ui, l, 2);
         if (head) {
-          // ---- actor head: the two warps of a lane quarter take the row's Philox blocks of 4 actions
-          //      alternately (warp hh: blocks hh, hh + 2, ...); SAC log pi = part 0 + part 1 (fixed order)
+          // ---- actor head: the WPQ warps of a lane quarter take the row's Philox blocks of 4 actions
+          //      in turn (warp hh: blocks hh, hh + WPQ, ...); SAC log pi = sum of the parts (fixed order)
           // per Philox block: the 4 mu (or z) and 4 log-sigma columns straight from TMEM into
           // registers (no per-row array, so nothing is indexed at run time)
           const int mh = p.head.m;
           const bool live = m < d.rows;
           const bool sac = p.head_epi == EPI_SAC_HEAD;
           float lp = 0.f;
-          for (int c = hh; 4 * c < mh; c += 2) {
+          for (int c = hh; 4 * c < mh; c += WPQ) {
             float v4[4], l4[4] = {0.f, 0.f, 0.f, 0.f};
             tmem_ld1x4(trow + (uint32_t)(4 * c), v4);
             if (sac) tmem_ld1x4(trow + (uint32_t)(mh + 4 * c), l4);
@@ -555,8 +569,8 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
           if (sac) {
             const int pb = dot_tiles & 1;
             dotpart[pb][hh][r] = lp;
-            named_bar(2 + q, 64);
-            if (hh == 0 && live) sac_head_logp(p.head, d.row0 + m, dotpart[pb][0][r] + dotpart[pb][1][r]);
+            named_bar(2 + q, WPQ * 32);
+            if (hh == 0 && live) sac_head_logp(p.head, d.row0 + m, quarter_sum<WPQ>(dotpart[pb], r));
             ++dot_tiles;
           }
           __syncwarp();
@@ -565,7 +579,7 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
         }
         // ---- hidden layer l: H must be free of the TMA stores issued from it for layer l-1
         if (e == 0 && lane == 0) bulk_wait_read0();
-        named_bar(1, M_EPI_WARPS * 32);
+        named_bar(1, EW * 32);
         uint32_t mw[NB > 0 ? NB : 1];
         const bool want_mask = d.mask[l] != nullptr;
         float dot;
@@ -578,7 +592,7 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
         }
         tc_fence_before();   // TMEM reads of this layer done
         fence_async_smem();  // H writes -> async proxy (MMA, TMA store)
-        named_bar(1, M_EPI_WARPS * 32);
+        named_bar(1, EW * 32);
         if (e == 0 && lane == 0) {
           mtrace(p.trace, ui, l, 3);
           if (l + 1 < NMMA) mbar_arrive(h_full);
@@ -600,11 +614,11 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
           }
         }
         if (has_dot) {
-          // the two warps of this lane quarter combine their slices in a fixed order
+          // the warps of this lane quarter combine their slices in a fixed order
           const int pb = dot_tiles & 1;
           dotpart[pb][hh][r] = dot;
-          named_bar(2 + q, 64);
-          const float qv = (dotpart[pb][0][r] + dotpart[pb][1][r]) + d.dot_b[0];
+          named_bar(2 + q, WPQ * 32);
+          const float qv = quarter_sum<WPQ>(dotpart[pb], r) + d.dot_b[0];
           if (hh == 0 && m < d.rows) d.dot_out[m] = qv;
           if (hh == 0) qv_s[jp][r] = qv;
           ++dot_tiles;
@@ -615,11 +629,11 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_kernel(const __grid_cons
       if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
     if constexpr (!ACTOR) {
-      if (p.gloss[kind]) loss_epilogue<H>(p, kind, su, m0, r, hh, e, lane, Hs, qv_s, dot_s, red_s);
+      if (p.gloss[kind]) loss_epilogue<H, WPQ>(p, kind, su, m0, r, hh, e, lane, Hs, qv_s, dot_s, red_s);
     }
     }
     if constexpr (!ACTOR) {
-      if (p.any_loss) loss_finish(p, e, lane, red_s, last_s);
+      if (p.any_loss) loss_finish<EW>(p, e, lane, red_s, last_s);
     }
   }
   if (warp >= 2 && lane == 0) bulk_wait_all();
@@ -643,20 +657,21 @@ long g_mtrace_count = 0;
 // -- so E0(B) runs under L1(A), E1(A) under L1(B), and so on.  Each block of a pair owns a TMEM
 // accumulator buffer and a hidden buffer H (two H buffers: 2 x 64 KB at h = 256, which leaves room
 // for a 2-stage weight ring).  Critic passes only (no actor head, no fused loss groups).
-template <int H>
-__global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_pair_kernel(const __grid_constant__ MlpParams p) {
+template <int H, int WPQ>
+__global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_pair_kernel(const __grid_constant__ MlpParams p) {
   constexpr int STAGE = H * MBK * 2;
   constexpr uint32_t BUF = H < 32 ? 32 : H;
   constexpr uint32_t TMEM_COLS = 2 * BUF <= 64 ? 64 : 2 * BUF <= 128 ? 128 : 2 * BUF <= 256 ? 256 : 512;
   constexpr int SLABS = H / 64;
-  constexpr int CPW = H / 16 / 2;
+  constexpr int EW = 4 * WPQ;
+  constexpr int CPW = H / 16 / WPQ;
   constexpr int NB = CPW / 2;
   constexpr int SLICE = CPW * 16;
   constexpr int HBYTES = SLABS * 16384;
   constexpr uint32_t IDESC_H = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(H >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
-  __shared__ __align__(16) float bias_w[M_EPI_WARPS][SLICE];
-  __shared__ __align__(16) float dotw_w[M_EPI_WARPS][SLICE];
-  __shared__ float dotpart[2][2][MBM];
+  __shared__ __align__(16) float bias_w[EW][SLICE];
+  __shared__ __align__(16) float dotw_w[EW][SLICE];
+  __shared__ float dotpart[2][WPQ][MBM];
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NS = p.stages;
@@ -686,7 +701,7 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_pair_kernel(const __grid
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], M_EPI_WARPS);
+      mbar_init(&acc_empty[b], EW);
       mbar_init(&h_full[b], 1);
     }
     mbar_init(x_full, 1);
@@ -812,7 +827,7 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_pair_kernel(const __grid
           tc_fence_after();
           // H_x must be free of the TMA stores issued from it (conservatively: every store so far)
           if (e == 0 && lane == 0) bulk_wait_read0();
-          named_bar(1, M_EPI_WARPS * 32);
+          named_bar(1, EW * 32);
           uint32_t mw[NB > 0 ? NB : 1];
           const bool want_mask = d.mask[l] != nullptr;
           float dot;
@@ -825,7 +840,7 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_pair_kernel(const __grid
           }
           tc_fence_before();
           fence_async_smem();
-          named_bar(1, M_EPI_WARPS * 32);
+          named_bar(1, EW * 32);
           if (e == 0 && lane == 0) {
             if (l + 1 < L) mbar_arrive(&h_full[x]);
             if (d.store[l]) {
@@ -848,8 +863,8 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_pair_kernel(const __grid
           if (has_dot) {
             const int pb = dot_tiles & 1;
             dotpart[pb][hh][r] = dot;
-            named_bar(2 + q, 64);
-            const float qv = (dotpart[pb][0][r] + dotpart[pb][1][r]) + d.dot_b[0];
+            named_bar(2 + q, WPQ * 32);
+            const float qv = quarter_sum<WPQ>(dotpart[pb], r) + d.dot_b[0];
             if (hh == 0 && m < d.rows) d.dot_out[m] = qv;
             ++dot_tiles;
           }
@@ -869,15 +884,15 @@ __global__ void __launch_bounds__(M_NTHREADS, 1) tc_mlp_pair_kernel(const __grid
   }
 }
 
-template <int H>
+template <int H, int WPQ>
 cudaError_t launch_mlp_pair(MlpParams& p, cudaStream_t st) {
   constexpr int STAGE = H * MBK * 2;
   const int xbytes = (p.k0 / MBK) * MA_BYTES;
   const int fixed = 1024 + xbytes + 2 * (H / 64) * 16384 + 1024;
-  constexpr int STATIC = 2 * M_EPI_WARPS * (H / 2) * 4 + 2 * 2 * MBM * 4;
+  constexpr int STATIC = 2 * 4 * H * 4 + 2 * WPQ * MBM * 4;  // bias / dot slices + dot partials
   const int ns = std::min(MSTAGES, (227 * 1024 - STATIC - 512 - fixed) / STAGE);
   if (ns < 2) return cudaErrorInvalidValue;
-  auto kern = tc_mlp_pair_kernel<H>;
+  auto kern = tc_mlp_pair_kernel<H, WPQ>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - STATIC - 512);
@@ -887,20 +902,21 @@ cudaError_t launch_mlp_pair(MlpParams& p, cudaStream_t st) {
   p.stages = ns;
   int grid = std::min(p.total_su, num_sms());
   if (grid == 0) return cudaSuccess;
-  return launch_pdl(kern, dim3(grid), dim3(M_NTHREADS), (size_t)(ns * STAGE + fixed), st, p);
+  return launch_pdl(kern, dim3(grid), dim3(mlp_threads(WPQ)), (size_t)(ns * STAGE + fixed), st, p);
 }
 
-template <int H, bool ACTOR>
+template <int H, bool ACTOR, int WPQ>
 cudaError_t launch_mlp(MlpParams& p, cudaStream_t st) {
   constexpr int STAGE = H * MBK * 2;
-  // dynamic: alignment slack + weight ring + input tile + H + barriers; static (bias / dot slices,
-  // dot partials, q values, statistics) <= 14 KB
+  // dynamic: alignment slack + weight ring + input tile + H + barriers; static: bias / dot slices,
+  // dot partials, q values, statistics (+ slack)
+  constexpr int STATIC = 2 * 4 * (H > 64 ? H : 64) * 4 + 2 * WPQ * MBM * 4 + 4 * MBM * 4 + 4 * WPQ * NSTAT * 8 + 1024;
   const int xbytes = (p.k0 / MBK) * MA_BYTES;
   const int fixed = 1024 + xbytes + (H / 64) * 16384 + 1024;
-  const int ns = std::min(MSTAGES, (227 * 1024 - 14 * 1024 - fixed) / STAGE);
+  const int ns = std::min(MSTAGES, (227 * 1024 - STATIC - fixed) / STAGE);
   if (ns < 2) return cudaErrorInvalidValue;
-  constexpr int SMEM_ATTR = 227 * 1024 - 14 * 1024;
-  auto kern = tc_mlp_kernel<H, ACTOR>;
+  constexpr int SMEM_ATTR = 227 * 1024 - STATIC;
+  auto kern = tc_mlp_kernel<H, ACTOR, WPQ>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR);
@@ -913,7 +929,7 @@ cudaError_t launch_mlp(MlpParams& p, cudaStream_t st) {
   int grid = std::min(p.total_su, num_sms());
   if (const char* cap = std::getenv("SPZ_DIAG_MLP_GRID")) grid = std::max(1, std::min(grid, std::atoi(cap)));  // diagnostics
   if (grid == 0) return cudaSuccess;
-  return launch_pdl(kern, dim3(grid), dim3(M_NTHREADS), (size_t)(ns * STAGE + fixed), st, p);
+  return launch_pdl(kern, dim3(grid), dim3(mlp_threads(WPQ)), (size_t)(ns * STAGE + fixed), st, p);
 }
 
 // bf16 [rows x inner] map with a 64 x box_rows box, 128-byte swizzle (load or store)
@@ -1044,17 +1060,24 @@ cudaError_t tc_mlp_fwd(const MlpArgs& a, cudaStream_t st) {
   const char* pe = std::getenv("SPZ_MLP_PAIR");  // read per launch (plans are built once)
   const int pair_env = pe ? (pe[0] == '1' ? 1 : 0) : -1;
   const bool pair = pair_env >= 0 ? pair_env == 1 : TSU >= 4 * num_sms();
+  // SPZ_MLP_WPQ=2: two epilogue warps per lane quarter at every width (diagnostics; default mlp_wpq)
+  const char* we = std::getenv("SPZ_MLP_WPQ");
+  const bool w2 = we && we[0] == '2';
   if (!actor && a.n_group == 0 && pair) {
     switch (a.h) {
-      case 64: return launch_mlp_pair<64>(p, st);
-      case 128: return launch_mlp_pair<128>(p, st);
-      default: return launch_mlp_pair<256>(p, st);
+      case 64: return launch_mlp_pair<64, 2>(p, st);
+      case 128: return w2 ? launch_mlp_pair<128, 2>(p, st) : launch_mlp_pair<128, mlp_wpq<128>()>(p, st);
+      default: return w2 ? launch_mlp_pair<256, 2>(p, st) : launch_mlp_pair<256, mlp_wpq<256>()>(p, st);
     }
   }
   switch (a.h) {
-    case 64: return actor ? launch_mlp<64, true>(p, st) : launch_mlp<64, false>(p, st);
-    case 128: return actor ? launch_mlp<128, true>(p, st) : launch_mlp<128, false>(p, st);
-    default: return actor ? launch_mlp<256, true>(p, st) : launch_mlp<256, false>(p, st);
+    case 64: return actor ? launch_mlp<64, true, 2>(p, st) : launch_mlp<64, false, 2>(p, st);
+    case 128:
+      if (w2) return actor ? launch_mlp<128, true, 2>(p, st) : launch_mlp<128, false, 2>(p, st);
+      return actor ? launch_mlp<128, true, mlp_wpq<128>()>(p, st) : launch_mlp<128, false, mlp_wpq<128>()>(p, st);
+    default:
+      if (w2) return actor ? launch_mlp<256, true, 2>(p, st) : launch_mlp<256, false, 2>(p, st);
+      return actor ? launch_mlp<256, true, mlp_wpq<256>()>(p, st) : launch_mlp<256, false, mlp_wpq<256>()>(p, st);
   }
 }
 

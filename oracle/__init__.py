@@ -19,6 +19,7 @@ What it computes (PAPER.md = ``P:n``, SPEC.md = ``S:n``):
 * ``sac``      -- one SAC update step, Jacobi order, float64 (§8(c)).
 * ``td3``      -- one TD3 update step (Fujimoto et al.), Jacobi order.
 * ``ddpg``     -- one DDPG update step, single critic, Jacobi order.
+* ``sacv1``    -- one SAC v1 update step (state-value network + target V; §8(f) f4), Jacobi order.
 * ``optim``    -- Adam and Polyak averaging.
 * ``act``      -- sampler-side action selection from a synced actor (P:208, P:221-224;
                   SURVEY.md §8(f) f1): deterministic tanh(mu) / stochastic reparameterised

@@ -104,9 +104,12 @@ def init_flat(shapes, seed=INIT_SEED, stream=0):
 
 def init_params(obs_dim, act_dim, hidden, n_hidden, algo="sac", seed=INIT_SEED):
     """Initial actor / critic parameter vectors (targets copy the online nets)."""
-    a_out = 2 * act_dim if algo == "sac" else act_dim
+    a_out = 2 * act_dim if algo in ("sac", "sacv1") else act_dim
     actor = init_flat(layer_shapes(obs_dim, hidden, n_hidden, a_out), seed, 1)
     cs = layer_shapes(obs_dim + act_dim, hidden, n_hidden, 1)
     q1 = init_flat(cs, seed, 2)
     q2 = init_flat(cs, seed, 3)
-    return dict(actor=actor, q1=q1, q2=q2)
+    out = dict(actor=actor, q1=q1, q2=q2)
+    if algo == "sacv1":  # + the state-value network V(s)
+        out["v"] = init_flat(layer_shapes(obs_dim, hidden, n_hidden, 1), seed, 4)
+    return out

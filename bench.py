@@ -19,6 +19,7 @@ region), gpu_launches (our kernels launched in the timed region).
 """
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -44,6 +45,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="walker", choices=list(synthdata.WORKLOADS))
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--algo", default=None, choices=["sac", "td3", "ddpg", "sacv1"],
+                    help="override the workload's algorithm (SURVEY.md §8(f) f4 variants on the same shapes)")
     ap.add_argument("--impl", default="spz", choices=["spz", "reference"])
     ap.add_argument("--batch", type=int, default=None, help="override the workload batch (B sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -78,23 +81,28 @@ def class_flops(w, B):
     target actor on s2 every step, the online actor and the actor rows of Q1 (its only critic for the
     actor loss) on delayed steps only (reading #18)."""
     o, m, h, L = w.obs_dim, w.act_dim, w.hidden, w.n_hidden
-    td3 = w.algo == "td3"
-    dly = 1.0 / 2 if td3 else 1.0  # share of steps with actor work (TD3 policy delay 2)
+    td3 = w.algo in ("td3", "ddpg")  # DDPG: the TD3 kernels, twin tied to the first, no delay
+    v1 = w.algo == "sacv1"           # SAC v1: actor on s only, V'(s2) + V(s) instead of the target critics
+    dly = 1.0 / 2 if w.algo == "td3" else 1.0  # share of steps with actor work (TD3 policy delay 2)
     aout = m if td3 else 2 * m
     cin = o + m
     f = {}
     add = lambda k, v: f.__setitem__(k, f.get(k, 0) + v)
     mlp = lambda rows, k_in, out: 2 * rows * (h * k_in + (L - 1) * h * h + (h * out if out else 0))
     # actor forward: SAC [s2; s] every step; TD3 target actor on s2 + online actor on s when delayed
-    Ma = 2 * B if not td3 else B * (1 + dly)
+    Ma = (B if v1 else 2 * B) if not td3 else B * (1 + dly)
     add("actor_fwd_gemm", mlp(Ma, o, 0))
     add("actor_head_gemm", 2 * Ma * aout * h)
     # critics: targets (2 nets x B rows) and online loss rows (2 x B) every step; actor rows: both
     # critics (SAC) / Q1 on delayed steps (TD3)
-    crit_rows = 2 * B + 2 * B + (2 * B if not td3 else B * dly)
+    crit_rows = (0 if v1 else 2 * B) + 2 * B + (2 * B if not td3 else B * dly)
     add("critic_fwd_gemm", mlp(crit_rows, cin, 0))
     dgrad_rows = 2 * B + (2 * B if not td3 else B * dly)
     add("critic_dgrad_gemm", dgrad_rows * 2 * (L - 1) * h * h)
+    if v1:  # value net: V' and V forward (B rows each), dgrad and wgrad over the B s rows
+        add("value_fwd_gemm", mlp(2 * B, o, 0))
+        add("critic_dgrad_gemm", B * 2 * (L - 1) * h * h)
+        add("wgrad_gemm", 2 * B * h * o + (L - 1) * 2 * B * h * h + 2 * B * h)
     add("critic_input_dgrad_gemm", (2 * B if not td3 else B * dly) * 2 * h * m)
     add("wgrad_gemm", 2 * (2 * B * h * cin + (L - 1) * 2 * B * h * h))  # critics ...
     add("actor_dgrad_gemm", dly * (2 * B * aout * h + (L - 1) * 2 * B * h * h))
@@ -103,6 +111,8 @@ def class_flops(w, B):
     # fused multi-layer forwards (h <= 256): every hidden layer (+ the actor head) in one launch
     f["actor_fwd_mlp"] = f["actor_fwd_gemm"] + f["actor_head_gemm"]
     f["critic_fwd_mlp"] = f["critic_fwd_gemm"]
+    if v1:
+        f["value_fwd_mlp"] = f["value_fwd_gemm"]
     return f
 
 
@@ -178,7 +188,7 @@ class Clocks:
 
 def oracle_rate(w, B, steps):
     """Time `steps` float64 oracle updates of the workload on this host; returns (frames/s, cores, seconds)."""
-    from oracle import ring as oring, sac as osac, td3 as otd3
+    from oracle import ddpg as oddpg, ring as oring, sac as osac, sacv1 as osacv1, td3 as otd3
     cores = len(os.sched_getaffinity(0))
     n = min(w.capacity, 1_000_000)
     tr = synthdata.workload_transitions(w, n=n)
@@ -187,9 +197,15 @@ def oracle_rate(w, B, steps):
     p = synthdata.init_params(w.obs_dim, w.act_dim, w.hidden, w.n_hidden, algo=w.algo)
     cfg = osac.Config(obs_dim=w.obs_dim, act_dim=w.act_dim, hidden=w.hidden, n_hidden=w.n_hidden,
                       alpha_auto=w.algo == "sac")
-    st = osac.State.create(p["actor"], p["q1"], p["q2"], log_alpha=np.log(0.2),
-                           actor_targ=p["actor"] if w.algo == "td3" else None)
-    step = osac.sac_step if w.algo == "sac" else otd3.td3_step
+    if w.algo == "sacv1":
+        cfg.alpha_auto = False
+        st = osacv1.State.create(p["actor"], p["q1"], p["q2"], p["v"], log_alpha=np.log(0.2))
+    else:
+        st = osac.State.create(p["actor"], p["q1"], p["q2"], log_alpha=np.log(0.2),
+                               actor_targ=p["actor"] if w.algo in ("td3", "ddpg") else None)
+    if w.algo == "ddpg":
+        cfg.td3_policy_delay, cfg.td3_noise, cfg.td3_noise_clip = 1, 0.0, 0.0
+    step = {"sac": osac.sac_step, "td3": otd3.td3_step, "ddpg": oddpg.ddpg_step, "sacv1": osacv1.sacv1_step}[w.algo]
     t0 = time.perf_counter()
     for _ in range(steps):
         st, _, _ = step(st, r, B, synthdata.SAMPLE_SEED, cfg)
@@ -227,6 +243,8 @@ def reference_arm(a, w, B):
 def main():
     a = parse()
     w = synthdata.WORKLOADS[a.config]
+    if a.algo and a.algo != w.algo:
+        w = dataclasses.replace(w, name=f"{w.name}_{a.algo}", algo=a.algo)
     B = a.batch or w.batch
     if a.impl == "reference":
         reference_arm(a, w, B)
@@ -314,7 +332,7 @@ def main():
     prof = lrn.profile(GB, 5)
     pk = peaks()
     fl = class_flops(w, B)  # per-GPU rows
-    n_params = sum(lrn.get(n).size for n in ("actor", "q1", "q2"))
+    n_params = sum(lrn.get(n).size for n in ("actor", "q1", "q2") + (("v",) if w.algo == "sacv1" else ()))
     by = class_bytes(w, B, n_params)
     kern = {}
     for k, t in prof.items():

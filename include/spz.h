@@ -114,8 +114,14 @@ void spz_replay_destroy(spz_replay* r);
  * spz_set_params of Q1 / Q1_TARG (setting Q2 / Q2_TARG directly is SPZ_EINVAL), so both receive
  * identical updates and min(Q1', Q2') = Q1'; the reported critic_loss is DDPG's (half the twins' sum).
  * spz_config_default(SPZ_DDPG) sets td3_policy_delay = 1 and td3_noise = td3_noise_clip = 0.
+ * SPZ_SACV1 (§8(f) f4, oracle/sacv1.py, reading #24): the original soft actor-critic the
+ * paper cites -- a state-value network V(s) (in = o, out 1, same hidden stack) with a Polyak
+ * target V'; the twin critics regress to y_Q = r + gamma (1-d) V'(s2) (no target critics, no a'), V to
+ * y_V = min_i Q_i(s, a~) - alpha log pi(a~|s), L_V = (1/B) sum (V(s) - y_V)^2 (stats value_loss); the
+ * policy and temperature losses are SAC's.  V is trained with lr_critic.  spz_config_default(SPZ_SACV1)
+ * sets alpha_auto = 0 (v1's fixed temperature).  Role ALL only.
  */
-typedef enum { SPZ_SAC = 0, SPZ_TD3 = 1, SPZ_DDPG = 2 } spz_algo;
+typedef enum { SPZ_SAC = 0, SPZ_TD3 = 1, SPZ_DDPG = 2, SPZ_SACV1 = 3 } spz_algo;
 /* FP32: GEMMs in full fp32 (exact-order-independent fp32 FMA); BF16: GEMM operands
  * rounded to bf16 (RNE) on tcgen05 tensor cores with fp32 accumulation; every
  * epilogue, master weight and optimizer state stays fp32 (reading #15). */
@@ -163,6 +169,7 @@ typedef struct {
   double alpha, alpha_loss;        /* alpha_k and L_alpha                                 */
   double q1_mean, q2_mean;         /* mean Q_i(s, a) over the batch                       */
   double logp_mean;                /* mean log pi(a~|s)                                   */
+  double value_loss;               /* SAC v1: L_V at step k (else 0)                      */
 } spz_stats;
 
 /* Create a learner on cfg->device that samples from `ring` (borrowed: the ring
@@ -202,13 +209,14 @@ spz_status spz_learner_set_stream(spz_learner* L, void* stream);
 typedef enum {
   SPZ_T_ACTOR = 0, SPZ_T_Q1 = 1, SPZ_T_Q2 = 2, SPZ_T_Q1_TARG = 3, SPZ_T_Q2_TARG = 4,
   SPZ_T_ACTOR_TARG = 5, /* TD3 only */
-  SPZ_T_LOG_ALPHA = 6
+  SPZ_T_LOG_ALPHA = 6,
+  SPZ_T_V = 7, SPZ_T_V_TARG = 8 /* SAC v1 only: the state-value network and its target */
 } spz_tensor;
 typedef enum { SPZ_S_PARAM = 0, SPZ_S_ADAM_M = 1, SPZ_S_ADAM_V = 2 } spz_slot; /* Adam slots: trained nets only */
 
 /* Flat fp32 layout (the oracle's): for each layer l = 1..L+1, W_l row-major
  * [out x in] then b_l[out].  Actor: in = o, hidden h, out = 2m (SAC: rows 0..m-1
- * mu, m..2m-1 log sigma) or m (TD3).  Critics: in = o + m (input [s | a]), out 1.
+ * mu, m..2m-1 log sigma) or m (TD3).  Critics: in = o + m (input [s | a]), out 1.  V: in = o, out 1.
  * LOG_ALPHA is 1 float.  get: n < n_required -> SPZ_EINVAL and *n_required set. */
 spz_status spz_get_params(spz_learner* L, spz_tensor t, spz_slot s, float* host_out, int64_t n,
                           int64_t* n_required);

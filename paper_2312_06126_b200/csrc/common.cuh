@@ -93,7 +93,7 @@ __host__ __device__ __forceinline__ int64_t round_up(int64_t x, int64_t a) { ret
 __host__ __device__ __forceinline__ int64_t cdiv(int64_t x, int64_t a) { return (x + a - 1) / a; }
 
 // ------------------------------------------------------------------ reductions
-constexpr int NSTAT = 6;  // per-block partial sums: (q1-y)^2+(q2-y)^2, q1, q2, alpha logp - minQ~ (or -Q1~), logp, spare
+constexpr int NSTAT = 6;  // per-block partial sums: (q1-y)^2+(q2-y)^2, q1, q2, alpha logp - minQ~ (or -Q1~), logp, SAC v1 (V-y_V)^2
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

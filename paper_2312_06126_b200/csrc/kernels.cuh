@@ -216,6 +216,13 @@ struct LossArgs {
   float gamma, invB;
   int Bl, td3, delay, loss_rows, actor_rows, h, ld, mask_ld;
   int q2_no_actor;        // TD3: Q2 has no actor rows (its dZ_L there is never read)
+  // SAC v1 (reading #24): qt1 = qt2 = V'(s2) and the bootstrap drops the entropy term; the actor rows
+  // also give the value target y_V = min(q1~, q2~) - alpha log pi~, g_V = 2 (V(s) - y_V) / B
+  int v1;
+  const float* vo;        // V(s) of the s rows (qp partials, stride vps)
+  float* gv;              // g_V [Bl]
+  __nv_bfloat16* gv16;    // optional bf16 copy (pitch 8), like gq16
+  int64_t vps;
   int qp;                 // q partials per row (fused row dot over qp 256-column tiles), summed in tile order
   int64_t qps_tg, qps_on;  // partial strides of the target / online q buffers
 };
@@ -256,7 +263,8 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   // ---- loads, all issued before any use: row scalars of the warp's rows (row index clamped, so
   //      every address is valid; rows past Bl are discarded below)
   float qt1[LOSS_RPW], qt2[LOSS_RPW], q1[LOSS_RPW], q2[LOSS_RPW], lp2[LOSS_RPW], rw[LOSS_RPW], dn[LOSS_RPW];
-  float a1[LOSS_RPW], a2[LOSS_RPW], lp[LOSS_RPW];
+  float a1[LOSS_RPW], a2[LOSS_RPW], lp[LOSS_RPW], vo[LOSS_RPW];
+  const bool notemp = a.td3 || a.v1;  // no entropy term in the bootstrap (TD3; v1 bootstraps V')
 #pragma unroll
   for (int i = 0; i < LOSS_RPW; ++i) {
     const int j = min(j0 + wi + 8 * i, a.Bl - 1);
@@ -266,10 +274,11 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
     q2[i] = ld_q(a.q2, j, a.qp, a.qps_on);
     rw[i] = __ldg(a.r + j);
     dn[i] = __ldg(a.d + j);
-    lp2[i] = a.td3 ? 0.f : __ldg(a.logp2 + j);
+    lp2[i] = notemp ? 0.f : __ldg(a.logp2 + j);
     a1[i] = ld_q(a.q1, a.Bl + j, a.qp, a.qps_on);
     a2[i] = ld_q(a.q2, a.Bl + j, a.qp, a.qps_on);
     lp[i] = a.td3 ? 0.f : __ldg(a.logp + j);
+    vo[i] = a.v1 ? ld_q(a.vo, j, a.qp, a.vps) : 0.f;
   }
   // ---- DZ: mask bytes (bit k = column n0 + k) and head weights of this lane's chunk
   const int n0 = lane * 8;
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
     float g[2][2] = {{0.f, 0.f}, {0.f, 0.f}};  // [critic][loss | actor row]
     if (lr) {
       const float qmin = fminf(qt1[i], qt2[i]);
-      const float boot = a.td3 ? qmin : qmin - alpha * lp2[i];
+      const float boot = notemp ? qmin : qmin - alpha * lp2[i];
       const float y = rw[i] + a.gamma * (1.f - dn[i]) * boot;
       const float e1 = q1[i] - y, e2 = q2[i] - y;
       g[0][0] = 2.f * e1 * a.invB;
@@ -344,6 +353,13 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
         if (!a.td3) {
           v[3] += (double)alpha * lp[i] - (double)fminf(a1[i], a2[i]);
           v[4] += lp[i];
+          if (a.v1) {
+            const float ev = vo[i] - (fminf(a1[i], a2[i]) - alpha * lp[i]);
+            const float gv = 2.f * ev * a.invB;
+            a.gv[j] = gv;
+            if (a.gv16) a.gv16[(int64_t)j * 8] = __float2bfloat16_rn(gv);
+            v[5] += (double)ev * ev;
+          }
         } else {
           v[3] += td3_on ? -(double)a1[i] : 0.0;
         }
@@ -584,25 +600,8 @@ __global__ void __launch_bounds__(CS_TX* CS_TY) colsum_multi_kernel(const __grid
 // Sums the per-block partials in block order; writes the step statistics, the
 // log-alpha gradient g = -(mean log pi~ + H_bar) and the non-finite flag.
 struct StatsOut {
-  double step, critic_loss, actor_loss, alpha, alpha_loss, q1_mean, q2_mean, logp_mean;
+  double step, critic_loss, actor_loss, alpha, alpha_loss, q1_mean, q2_mean, logp_mean, value_loss;
 };
-
-// Statistics of the step from the loss totals (called by every Adam block; block 0 publishes).
-// Returns true if a loss is non-finite (the step must not be applied).
-__device__ __forceinline__ bool step_stats(const double* __restrict__ tot, double la, double target_entropy, double B,
-                                           int td3, int64_t step, StatsOut* o, float* g_log_alpha) {
-  o->step = (double)(step + 1);
-  o->critic_loss = tot[0] / B;
-  o->q1_mean = tot[1] / B;
-  o->q2_mean = tot[2] / B;
-  o->actor_loss = tot[3] / B;
-  o->logp_mean = td3 ? 0.0 : tot[4] / B;
-  o->alpha = td3 ? 0.0 : exp(la);
-  o->alpha_loss = td3 ? 0.0 : -la * (o->logp_mean + target_entropy);
-  *g_log_alpha = (float)(-(o->logp_mean + target_entropy));
-  return !isfinite(o->critic_loss) || !isfinite(o->actor_loss) || !isfinite(o->q1_mean) || !isfinite(o->q2_mean) ||
-         !isfinite(o->logp_mean);
-}
 
 // ------------------------------------------------------------------ a9: fused multi-tensor Adam + Polyak
 // Per element of every trained tensor:
@@ -723,7 +722,8 @@ __global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegme
   if (threadIdx.x == 0) {
     // the step's losses are finite iff their totals are (B > 0); TD3 has no log-prob total
     const bool bad =
-        !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) || (!hp.td3 && !isfinite(tot[4]));
+        !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) || (!hp.td3 && !isfinite(tot[4])) ||
+        !isfinite(tot[5]);
     const int f = *flag;
     if (bad && blockIdx.x == 0) atomicExch(flag, 1);
     skip = bad || f;  // halted: parameters stay at the state before the failing step
@@ -777,6 +777,7 @@ __global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegme
       case 5: o[5] = tot[1] / B; break;
       case 6: o[6] = tot[2] / B; break;
       case 7: o[7] = lpm; break;
+      case 9: o[8] = tot[5] / B; break;  // SAC v1 value loss (the spare total is 0 otherwise)
       case 8:
         if (!skip) {
           counters[1] = hp.snap[1] + (hp.critic_on ? 1 : 0);

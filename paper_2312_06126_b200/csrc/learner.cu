@@ -23,7 +23,8 @@
 
 namespace spz {
 
-enum NetId { NET_ACTOR = 0, NET_Q1 = 1, NET_Q2 = 2, NET_Q1T = 3, NET_Q2T = 4, NET_ACTORT = 5, N_NETS = 6 };
+// NET_V / NET_VT: SAC v1's state-value network and its Polyak target (reading #24)
+enum NetId { NET_ACTOR = 0, NET_Q1 = 1, NET_Q2 = 2, NET_Q1T = 3, NET_Q2T = 4, NET_ACTORT = 5, NET_V = 6, NET_VT = 7, N_NETS = 8 };
 
 struct NetLayout {
   int nl = 0;
@@ -110,6 +111,7 @@ struct spz_learner {
   cudaStream_t own_stream = nullptr, stream = nullptr;
   bool td3 = false, bf16 = false;
   bool ddpg = false;  // TD3 kernels with the twin critic tied to the first (spz.h)
+  bool v1 = false;    // SAC v1: state-value network V (+ target), no target critics (spz.h, reading #24)
   int o = 0, m = 0, h = 0, L = 0;
   size_t esz = 4;
   int64_t max_local = 0;  // rows handled by this rank at max_batch
@@ -164,6 +166,11 @@ struct spz_learner {
   int qp = 1;                   // q partial slots per row (fused row dot over 256-column tiles)
   float* H = nullptr;
   float *q_on[2] = {}, *q_tg[2] = {}, *gq[2] = {}, *dXc[2] = {};
+  // SAC v1 value network: activations / masks / gradients of the s rows, target activations (GEMM path)
+  void *Av[8] = {}, *AvT[8] = {}, *dZv[8] = {};
+  uint32_t* mask_v[8] = {};
+  float *v_on = nullptr, *v_tg = nullptr, *gv = nullptr;
+  __nv_bfloat16* gv16 = nullptr;
   __nv_bfloat16* gq16[2] = {};  // bf16 loss-row g_q, pitch 8 (tensor-core head gradients)
   float *logp = nullptr, *logp2 = nullptr, *r = nullptr, *d = nullptr, *y = nullptr;
   HeadCache cache{};
@@ -230,6 +237,7 @@ static int wgrad_splits(const spz_learner* Lr, int64_t Bl) {
     for (int l = 0; l < layers; ++l) tiles += cdiv(n.out[l], 128) * cdiv(n.in[l], 256);
   };
   if (critic_on) net_tiles(Lr->net[NET_Q1], Lr->net[NET_Q1].nl), net_tiles(Lr->net[NET_Q2], Lr->net[NET_Q2].nl);
+  if (critic_on && Lr->v1) net_tiles(Lr->net[NET_V], Lr->net[NET_V].nl);
   if (actor_on) net_tiles(Lr->net[NET_ACTOR], Lr->net[NET_ACTOR].nl);
   const int64_t fill = std::max<int64_t>(1, sms / std::max<int64_t>(1, tiles));
   return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(32, fill), Bl / 256));
@@ -254,7 +262,7 @@ static std::vector<TensorSlot> trained_tensors(spz_learner* Lr) {
   auto add_net = [&](int id) {
     const NetLayout& n = Lr->net[id];
     for (int l = 0; l < n.nl; ++l) {
-      const bool head_vec = (id == NET_Q1 || id == NET_Q2) && l == n.nl - 1;  // N = 1 head: column sums
+      const bool head_vec = (id == NET_Q1 || id == NET_Q2 || id == NET_V) && l == n.nl - 1;  // N = 1 head: column sums
       // weight partials keep a 16-byte row pitch (TMA stores): out x round_up(in, 4)
       v.push_back({id, l, true, (int64_t)n.out[l] * (head_vec ? n.in[l] : round_up(n.in[l], 4)), 0,
                    head_vec ? std::max(Sb, Sw) : Sw});
@@ -264,6 +272,7 @@ static std::vector<TensorSlot> trained_tensors(spz_learner* Lr) {
   if (critic_on) {
     add_net(NET_Q1);
     add_net(NET_Q2);
+    if (Lr->v1) add_net(NET_V);
   }
   if (actor_on) add_net(NET_ACTOR);
   int64_t off = 0;
@@ -337,6 +346,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
   const int64_t row0 = rk * base + std::min<int64_t>(rk, rem);
   const int o = Lr->o, m = Lr->m, h = Lr->h, L = Lr->L;
   const bool td3 = Lr->td3;
+  const bool v1 = Lr->v1;
   const float invB = (float)(1.0 / (double)B);
   T* S = static_cast<T*>(Lr->S);
   float* P = Lr->P;
@@ -456,7 +466,9 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       const NetLayout& an = Lr->net[NET_ACTOR];
       struct Pass { int id; int64_t row; int M; };
       std::vector<Pass> passes;
-      if (!td3) {
+      if (v1) {
+        passes.push_back({NET_ACTOR, Bl, Bl});  // SAC v1: the policy on s only (no a', role ALL)
+      } else if (!td3) {
         if (do_critic && do_actor) passes.push_back({NET_ACTOR, 0, 2 * Bl});
         else if (do_critic) passes.push_back({NET_ACTOR, 0, Bl});
         else if (do_actor) passes.push_back({NET_ACTOR, Bl, Bl});
@@ -543,6 +555,84 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       }
       }
     }
+    // ---- SAC v1 (reading #24): the target value V'(s2) and the online value V(s) (activations + masks
+    //      of the s rows for its backward), one fused launch over the actor's input rows [s2; s]
+    if (v1) {
+      const NetLayout& vn = Lr->net[NET_V];
+      bool vfused = false;
+      if (bits) {
+        MlpArgs ma{};
+        ma.L = L;
+        ma.h = h;
+        ma.k0 = lda;
+        ma.mask_ld = mw;
+        for (int pi = 0; pi < 2; ++pi) {
+          const int id = pi == 0 ? NET_VT : NET_V;
+          MlpPass& q = ma.p[ma.n_pass++];
+          q.X = Ta(Lr->Xa, pi == 0 ? 0 : Bl, lda);
+          q.ldx = lda;
+          q.rows = Bl;
+          for (int l = 0; l < L; ++l) {
+            q.W[l] = Wp(id, l);
+            q.ldw[l] = vn.ld[l];
+            q.bias[l] = bp(id, l);
+            if (pi == 1) {
+              q.act[l] = Lr->Av[l];
+              q.mask[l] = Lr->mask_v[l];
+            }
+          }
+          q.bias[L] = bp(id, L);
+          q.dot_w = P + Lr->pbase[id] + vn.w[L];
+          q.dot_b = bp(id, L);
+          q.dot_out = pi == 0 ? Lr->v_tg : Lr->v_on;
+        }
+        if (tc_mlp_supported(ma)) {
+          vfused = true;
+          ops.push_back({"value_fwd_mlp", [ma](cudaStream_t st) { return tc_mlp_fwd(ma, st); }});
+        }
+      }
+      for (int l = 0; l < L && !vfused; ++l) {
+        GemmArgs a = mk(l == 0 ? lda : h, EPI_BIAS_RELU, 0, 0);
+        for (int pi = 0; pi < 2; ++pi) {
+          const int id = pi == 0 ? NET_VT : NET_V;
+          void* const* act = pi == 0 ? Lr->AvT : Lr->Av;
+          GemmGroup& g = add(a, l == 0 ? (const void*)Ta(Lr->Xa, pi == 0 ? 0 : Bl, lda) : (const void*)act[l - 1],
+                             l == 0 ? lda : h, Wp(id, l), vn.ld[l], act[l], h, Bl, h, bp(id, l));
+          if (bits && pi == 1) {
+            g.mask_out = Lr->mask_v[l];
+            g.mask_ld = mw;
+          }
+          if (l == L - 1) {
+            g.dot_w = P + Lr->pbase[id] + vn.w[L];
+            g.dot_b = bp(id, L);
+            g.dot_out = pi == 0 ? Lr->v_tg : Lr->v_on;
+            g.dot_pstride = (h > 256 && h <= 1024) ? Lr->max_local : 0;
+          }
+        }
+        if (bits && !tc_ok(a) && l < L - 1) return fail(SPZ_EUNSUPPORTED, "internal: value forward not supported by the tcgen05 kernel");
+        if (l == L - 1 && !tc_ok(a)) {
+          for (int i = 0; i < a.n_groups; ++i) a.g[i].dot_out = nullptr;
+          gemm("value_fwd_gemm", a);
+          RowdotArgs ra{};
+          ra.M = Bl;
+          ra.h = h;
+          ra.ld = h;
+          for (int pi = 0; pi < 2; ++pi) {
+            const int id = pi == 0 ? NET_VT : NET_V;
+            ra.g[pi].A = pi == 0 ? Lr->AvT[L - 1] : Lr->Av[L - 1];
+            ra.g[pi].w = P + Lr->pbase[id] + vn.w[L];
+            ra.g[pi].b = bp(id, L);
+            ra.g[pi].q = pi == 0 ? Lr->v_tg : Lr->v_on;
+          }
+          const int M = Bl;
+          ops.push_back({"value_head", [ra, M](cudaStream_t st) {
+                           return launch_pdl(rowdot_kernel<T>, dim3((unsigned)cdiv((int64_t)M * 32, 256), 2), dim3(256), 0, st, ra);
+                         }});
+        } else {
+          gemm("value_fwd_gemm", a);
+        }
+      }
+    }
     // ---- a4: target critics on [s2 | a'] (M = Bl) and a5: online critics on [s | a ; s | a~]
     //      (M = 2Bl), all four in one launch per layer; the N = 1 head is a row dot fused into
     //      the last hidden layer's epilogue when the row fits one tile.
@@ -569,7 +659,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       for (int kind = 0; kind < 3; ++kind) {
         if (kind == 0 && !do_critic) continue;
         if (kind == 1 && !do_actor) continue;
-        if (kind == 2 && !do_critic) continue;
+        if (kind == 2 && (!do_critic || v1)) continue;  // SAC v1 bootstraps V', not target critics
         for (int i = 0; i < 2; ++i) {
           if (kind == 1 && i == 1 && q2_skip_actor) continue;
           const int id = kind == 2 ? NET_Q1T + i : NET_Q1 + i;
@@ -598,7 +688,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       // serial 4-pass groups (one per CTA) cost more than the separate critic_loss kernel
       // (118.2 vs 114.7 us/update) because a unit's layer-1 weight delivery dominates its time.
       const char* fl = std::getenv("SPZ_FUSE_CRITIC_LOSS");
-      if (fl && std::atoi(fl) == 1) {
+      if (fl && std::atoi(fl) == 1 && !v1) {
         int idx[3][2], n = 0;
         for (int kind = 0; kind < 3; ++kind)
           for (int i = 0; i < 2; ++i) {
@@ -660,7 +750,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         GemmArgs a = mk(l == 0 ? ldc : cn.in[l], EPI_BIAS_RELU, 0, 0);  // layer 0: over the zero-padded width
         for (int pass = 0; pass < 2; ++pass) {
           const bool tgt = pass == 1;
-          if (tgt && !do_critic) continue;
+          if (tgt && (!do_critic || v1)) continue;
           if (!tgt && Mon == 0) continue;
           const int r0c = tgt ? 2 * Bl : on0;  // row in Xc
           const int ra = tgt ? 0 : on0;        // row in the activation buffers
@@ -689,7 +779,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           gemm("critic_fwd_gemm", a);
           for (int pass = 0; pass < 2; ++pass) {
             const bool tgt = pass == 1;
-            if ((tgt && !do_critic) || (!tgt && Mon == 0)) continue;
+            if ((tgt && (!do_critic || v1)) || (!tgt && Mon == 0)) continue;
             const int M = tgt ? Bl : Mon;
             const int rr0 = tgt ? 0 : on0;
             RowdotArgs ra{};
@@ -728,6 +818,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       LossArgs la{};
       la.qp = qparts;
       la.q2_no_actor = q2_skip_actor;
+      la.v1 = v1;
       la.qps_tg = Lr->max_local;
       la.qps_on = 2 * Lr->max_local;
       la.qt1 = Lr->q_tg[0];
@@ -768,6 +859,13 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       la.actor_rows = do_actor;
       la.h = h;
       la.ld = h;
+      if (v1) {  // the bootstrap reads V'(s2); the actor rows also yield g_V
+        la.qt1 = la.qt2 = Lr->v_tg;
+        la.vo = Lr->v_on;
+        la.vps = Lr->max_local;
+        la.gv = Lr->gv;
+        la.gv16 = fuse_bias ? Lr->gv16 : nullptr;
+      }
       // h <= 256: dZ_L written by the loss kernel (one row per warp); wider rows: critic_dz_kernel
       const bool dz_sep = !dz_in_loss && (do_critic || do_actor);
       if (!lfused) {  // (the fused critic forward with loss groups computes all of this itself)
@@ -797,6 +895,27 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         da.mask_ld = mw;
         const int64_t nthr = da.rows * da.hv;
         ops.push_back({"critic_loss", [da, nthr](cudaStream_t st) {
+                         return launch_pdl(critic_dz_kernel<T>, dim3((unsigned)cdiv(nthr, 256)), dim3(256), 0, st, da);
+                       }});
+      }
+      if (v1) {
+        // V's head backward dZ_L = g_V w_V 1[z_L > 0] (the second slot mirrors the first and writes nothing)
+        DzArgs da{};
+        for (int i = 0; i < 2; ++i) {
+          da.gq[i] = Lr->gv;
+          da.mask[i] = bits ? Lr->mask_v[L - 1] : nullptr;
+          da.A[i] = Lr->Av[L - 1];
+          da.w[i] = P + Lr->pbase[NET_V] + Lr->net[NET_V].w[L];
+          da.dZ[i] = Lr->dZv[L - 1];
+        }
+        da.r0 = 0;
+        da.rows = Bl;
+        da.q2_end = 0;
+        da.hv = h / 8;
+        da.ld = h;
+        da.mask_ld = mw;
+        const int64_t nthr = da.rows * da.hv;
+        ops.push_back({"value_dz", [da, nthr](cudaStream_t st) {
                          return launch_pdl(critic_dz_kernel<T>, dim3((unsigned)cdiv(nthr, 256)), dim3(256), 0, st, da);
                        }});
       }
@@ -855,6 +974,13 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
             add(a, Ta(Lr->dZc[i][l], on0, h), h, Wp(NET_Q1 + i, l), cn.ld[l], Ta(Lr->dZc[i][l - 1], on0, h), h, i ? Mon2 : Mon, h,
                 nullptr, Ta(Lr->Aon[i][l - 1], on0, h), h);
         }
+        if (v1) {  // the value network's dgrad rides in the same launch (its B s rows)
+          const NetLayout& vn = Lr->net[NET_V];
+          if (bits)
+            add(a, Lr->dZv[l], h, Wp(NET_V, l), vn.ld[l], Lr->dZv[l - 1], h, Bl, h, nullptr, Lr->mask_v[l - 1], mw);
+          else
+            add(a, Lr->dZv[l], h, Wp(NET_V, l), vn.ld[l], Lr->dZv[l - 1], h, Bl, h, nullptr, Lr->Av[l - 1], h);
+        }
         if (bits && !empty_gemm(a) && !tc_ok(a)) return fail(SPZ_EUNSUPPORTED, "internal: critic dgrad not supported by the tcgen05 kernel");
         gemm("critic_dgrad_gemm", a);
       }
@@ -906,6 +1032,47 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           colsums.push_back({Lr->dZc[i][l], nullptr, Lr->G + slot_of(NET_Q1 + i, l, false).g_off, h, h, Bl, 0});
         colsums.push_back({Lr->Aon[i][L - 1], Lr->gq[i], Lr->G + slot_of(NET_Q1 + i, L, true).g_off, h, h, Bl, 0});
         colsums.push_back({Lr->gq[i], nullptr, Lr->G + slot_of(NET_Q1 + i, L, false).g_off, 1, 1, Bl, 1});
+      }
+    }
+    // ---- SAC v1: value network wgrad over its B s rows (dZ_l^T A_{l-1}; head: g_V^T A_{L-1})
+    if (v1) {
+      const NetLayout& vn = Lr->net[NET_V];
+      for (int l = 0; l < L; ++l) {
+        GemmGroup g{};
+        g.A = Lr->dZv[l];
+        g.lda = h;
+        g.B = l == 0 ? (const void*)Ta(Lr->Xa, Bl, lda) : (const void*)Lr->Av[l - 1];
+        g.ldb = l == 0 ? lda : h;
+        g.C = Lr->G + slot_of(NET_V, l, true).g_off;
+        g.ldc = (int)round_up(vn.in[l], 4);
+        g.M = h;
+        g.N = vn.in[l];
+        g.split_stride = (int64_t)h * g.ldc;
+        if (fuse_bias) {
+          g.colsum_out = Lr->G + slot_of(NET_V, l, false).g_off;
+          g.colsum_stride = h;
+        }
+        wgrads.push_back(g);
+      }
+      if (fuse_bias) {
+        GemmGroup g{};
+        g.A = Lr->gv16;
+        g.lda = 8;
+        g.B = Lr->Av[L - 1];
+        g.ldb = h;
+        g.C = Lr->G + slot_of(NET_V, L, true).g_off;
+        g.ldc = h;
+        g.M = 1;
+        g.N = h;
+        g.split_stride = h;
+        g.colsum_out = Lr->G + slot_of(NET_V, L, false).g_off;
+        g.colsum_stride = 1;
+        wgrads.push_back(g);
+      } else {
+        for (int l = 0; l < L; ++l)
+          colsums.push_back({Lr->dZv[l], nullptr, Lr->G + slot_of(NET_V, l, false).g_off, h, h, Bl, 0});
+        colsums.push_back({Lr->Av[L - 1], Lr->gv, Lr->G + slot_of(NET_V, L, true).g_off, h, h, Bl, 0});
+        colsums.push_back({Lr->gv, nullptr, Lr->G + slot_of(NET_V, L, false).g_off, 1, 1, Bl, 1});
       }
     }
     // ---- a7: actor backward (s-rows Bl..2Bl of the actor activations)
@@ -1004,7 +1171,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         const NetLayout& n = Lr->net[s.net];
         AdamTensor t{};
         t.p_off = Lr->pbase[s.net] + (s.weight ? n.w[s.layer] : n.b[s.layer]);
-        const bool head_vec = (s.net == NET_Q1 || s.net == NET_Q2) && s.layer == n.nl - 1;
+        const bool head_vec = (s.net == NET_Q1 || s.net == NET_Q2 || s.net == NET_V) && s.layer == n.nl - 1;
         t.numel = s.weight ? (int64_t)n.out[s.layer] * n.in[s.layer] : n.out[s.layer];
         t.partials = Lr->G + s.g_off;
         t.n_partials = (s.weight && !head_vec) || fuse_bias ? Sw : Sb;
@@ -1014,7 +1181,8 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         t.cols = s.weight ? n.in[s.layer] : 0;
         t.ld = n.ld[s.layer];
         t.s_off = s.weight ? Lr->sbase[s.net] + n.sw[s.layer] : -1;
-        int tid = s.net == NET_Q1 ? NET_Q1T : s.net == NET_Q2 ? NET_Q2T : (td3 ? NET_ACTORT : -1);
+        int tid = s.net == NET_Q1 ? NET_Q1T : s.net == NET_Q2 ? NET_Q2T : s.net == NET_V ? NET_VT : (td3 ? NET_ACTORT : -1);
+        if (tid >= 0 && !Lr->has_net[tid]) tid = -1;  // SAC v1: no target critics
         t.t_off = tid >= 0 ? Lr->pbase[tid] + (s.weight ? n.w[s.layer] : n.b[s.layer]) : -1;
         t.ts_off = (tid >= 0 && s.weight) ? Lr->sbase[tid] + n.sw[s.layer] : -1;
         tens.push_back(t);
@@ -1259,7 +1427,7 @@ spz_status spz_config_default(spz_algo algo, int32_t obs_dim, int32_t act_dim, s
   out->beta1 = 0.9;
   out->beta2 = 0.999;
   out->adam_eps = 1e-8;
-  out->alpha_auto = algo == SPZ_SAC ? 1 : 0;
+  out->alpha_auto = algo == SPZ_SAC ? 1 : 0;  // SAC v1: fixed temperature (haarnoja2018soft)
   out->alpha_init = 0.2;
   out->target_entropy = -(double)act_dim;
   out->log_std_min = -20.0;
@@ -1299,8 +1467,10 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     if ((cfg->rank < nc) != (cfg->role == SPZ_ROLE_CRITIC))
       return fail(SPZ_EINVAL, "spz_learner_create: ranks [0, n_critic_ranks) must be critic, the others actor");
   }
-  if (cfg->algo != SPZ_SAC && cfg->algo != SPZ_TD3 && cfg->algo != SPZ_DDPG)
+  if (cfg->algo != SPZ_SAC && cfg->algo != SPZ_TD3 && cfg->algo != SPZ_DDPG && cfg->algo != SPZ_SACV1)
     return fail(SPZ_EINVAL, "spz_learner_create: unknown algo");
+  if (cfg->algo == SPZ_SACV1 && cfg->role != SPZ_ROLE_ALL)
+    return fail(SPZ_EUNSUPPORTED, "spz_learner_create: SAC v1 runs with role ALL only");
   if (cfg->precision != SPZ_FP32 && cfg->precision != SPZ_BF16) return fail(SPZ_EINVAL, "spz_learner_create: unknown precision");
   spz_status st = check_device(cfg->device);
   if (st != SPZ_OK) return st;
@@ -1311,6 +1481,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   Lr->device = cfg->device;
   Lr->td3 = cfg->algo == SPZ_TD3 || cfg->algo == SPZ_DDPG;
   Lr->ddpg = cfg->algo == SPZ_DDPG;
+  Lr->v1 = cfg->algo == SPZ_SACV1;
   Lr->bf16 = cfg->precision == SPZ_BF16;
   Lr->esz = Lr->bf16 ? 2 : 4;
   Lr->o = cfg->obs_dim;
@@ -1340,9 +1511,13 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   Lr->net[NET_ACTOR] = make_layout(o, h, L, aout, kpad);
   Lr->net[NET_Q1] = Lr->net[NET_Q2] = Lr->net[NET_Q1T] = Lr->net[NET_Q2T] = make_layout(o + m, h, L, 1, kpad);
   Lr->net[NET_ACTORT] = Lr->net[NET_ACTOR];
+  Lr->net[NET_V] = Lr->net[NET_VT] = make_layout(o, h, L, 1, kpad);
   int64_t p = 0, s = 0;
   for (int id = 0; id < N_NETS; ++id) {
-    Lr->has_net[id] = id != NET_ACTORT || Lr->td3;
+    if (id == NET_ACTORT) Lr->has_net[id] = Lr->td3;
+    else if (id == NET_Q1T || id == NET_Q2T) Lr->has_net[id] = !Lr->v1;
+    else if (id == NET_V || id == NET_VT) Lr->has_net[id] = Lr->v1;
+    else Lr->has_net[id] = true;
     if (!Lr->has_net[id]) continue;
     Lr->pbase[id] = p;
     p += round_up(Lr->net[id].np, 64);
@@ -1402,6 +1577,18 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->dXc[i], Bm * Lr->ldc * sizeof(float)));
   }
   for (float** f : {&Lr->logp, &Lr->logp2, &Lr->r, &Lr->d, &Lr->y}) SPZ_TRY(dalloc(Lr.get(), (void**)f, Bm * sizeof(float)));
+  if (Lr->v1) {
+    for (int l = 0; l < L; ++l) {
+      SPZ_TRY(dalloc(Lr.get(), &Lr->Av[l], Bm * h * E));
+      SPZ_TRY(dalloc(Lr.get(), &Lr->AvT[l], Bm * h * E));
+      SPZ_TRY(dalloc(Lr.get(), &Lr->dZv[l], Bm * h * E));
+      SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->mask_v[l], Bm * Lr->mw * 4));
+    }
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->v_on, Bm * Lr->qp * sizeof(float)));
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->v_tg, Bm * Lr->qp * sizeof(float)));
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->gv, Bm * sizeof(float)));
+    SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->gv16, Bm * 8 * sizeof(__nv_bfloat16)));
+  }
   for (float** f : {&Lr->cache.u, &Lr->cache.a, &Lr->cache.eps, &Lr->cache.sig, &Lr->cache.l})
     SPZ_TRY(dalloc(Lr.get(), (void**)f, Bm * m * sizeof(float)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->idx, Bm * sizeof(int32_t)));
@@ -1427,6 +1614,11 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
       reg("q_tg" + std::to_string(i), Lr->q_tg[i], Bm * 4, 4);
       reg("gq" + std::to_string(i), Lr->gq[i], 2 * Bm * 4, 4);
       reg("dXc" + std::to_string(i), Lr->dXc[i], Bm * Lr->ldc * 4, 4);
+    }
+    if (Lr->v1) {
+      reg("v_on", Lr->v_on, Bm * 4, 4);
+      reg("v_tg", Lr->v_tg, Bm * 4, 4);
+      reg("gv", Lr->gv, Bm * 4, 4);
     }
     reg("logp", Lr->logp, Bm * 4, 4);
     reg("logp2", Lr->logp2, Bm * 4, 4);
@@ -1507,7 +1699,8 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->d_shadow, sh.data(), sh.size() * sizeof(ShadowEntry), cudaMemcpyHostToDevice, Lr->stream));
   SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
   // init: W, b ~ U(+-1/sqrt(fan_in)) (Philox stream S_INIT); targets copy online; log alpha = ln alpha_init
-  for (int id : {NET_ACTOR, NET_Q1, NET_Q2}) {
+  for (int id : {NET_ACTOR, NET_Q1, NET_Q2, NET_V}) {
+    if (!Lr->has_net[id]) continue;
     const NetLayout& n = Lr->net[id];
     for (int l = 0; l < n.nl; ++l) {
       const float bound = 1.0f / std::sqrt((float)n.in[l]);
@@ -1522,8 +1715,9 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
                            cudaMemcpyDeviceToDevice, Lr->stream);
   };
   if (Lr->ddpg) SPZ_CUDA_TRY(copy_net(NET_Q2, NET_Q1));  // the tied twin
-  SPZ_CUDA_TRY(copy_net(NET_Q1T, NET_Q1));
-  SPZ_CUDA_TRY(copy_net(NET_Q2T, NET_Q2));
+  if (Lr->has_net[NET_Q1T]) SPZ_CUDA_TRY(copy_net(NET_Q1T, NET_Q1));
+  if (Lr->has_net[NET_Q2T]) SPZ_CUDA_TRY(copy_net(NET_Q2T, NET_Q2));
+  if (Lr->v1) SPZ_CUDA_TRY(copy_net(NET_VT, NET_V));
   if (Lr->td3) SPZ_CUDA_TRY(copy_net(NET_ACTORT, NET_ACTOR));
   const float la = (float)std::log(cfg->alpha_init > 0 ? cfg->alpha_init : 1e-30);
   SPZ_CUDA_TRY(cudaMemcpyAsync(Lr->P + Lr->p_log_alpha, &la, sizeof(float), cudaMemcpyHostToDevice, Lr->stream));
@@ -1574,6 +1768,7 @@ static spz_status update_finish(spz_learner* Lr, spz_stats* last) {
     last->q1_mean = s.q1_mean;
     last->q2_mean = s.q2_mean;
     last->logp_mean = s.logp_mean;
+    last->value_loss = Lr->v1 ? s.value_loss : 0.0;
   }
   return SPZ_OK;
 }
@@ -1666,10 +1861,12 @@ static spz_status tensor_region(spz_learner* Lr, spz_tensor t, spz_slot s, float
     case SPZ_T_Q2_TARG: id = NET_Q2T; break;
     case SPZ_T_ACTOR_TARG: id = NET_ACTORT; break;
     case SPZ_T_LOG_ALPHA: id = -1; break;
+    case SPZ_T_V: id = NET_V; break;
+    case SPZ_T_V_TARG: id = NET_VT; break;
     default: return fail(SPZ_EINVAL, "unknown tensor id");
   }
   if (id >= 0 && !Lr->has_net[id]) return fail(SPZ_EINVAL, "tensor not present for this algorithm");
-  const bool trained = id == NET_ACTOR || id == NET_Q1 || id == NET_Q2 || id == -1;
+  const bool trained = id == NET_ACTOR || id == NET_Q1 || id == NET_Q2 || id == NET_V || id == -1;
   if (s != SPZ_S_PARAM && !trained) return fail(SPZ_EINVAL, "target networks have no Adam state");
   float* arr = s == SPZ_S_PARAM ? Lr->P : s == SPZ_S_ADAM_M ? Lr->Mo : s == SPZ_S_ADAM_V ? Lr->Vo : nullptr;
   if (!arr) return fail(SPZ_EINVAL, "unknown slot");

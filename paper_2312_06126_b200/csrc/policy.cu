@@ -190,7 +190,7 @@ spz_status spz_policy_create(const spz_policy_desc* d, spz_policy** out) {
   if (d->obs_dim < 1 || d->act_dim < 1 || d->act_dim > 32 || d->hidden < 16 || d->hidden % 16 || d->n_hidden < 1 ||
       d->n_hidden > 6 || d->max_batch < 1)
     return fail(SPZ_EINVAL, "spz_policy_create: bad dims (act_dim 1..32, hidden multiple of 16, 1 <= n_hidden <= 6, max_batch >= 1)");
-  if (d->algo != SPZ_SAC && d->algo != SPZ_TD3 && d->algo != SPZ_DDPG)
+  if (d->algo != SPZ_SAC && d->algo != SPZ_TD3 && d->algo != SPZ_DDPG && d->algo != SPZ_SACV1)
     return fail(SPZ_EINVAL, "spz_policy_create: unknown algo");
   if (d->precision != SPZ_FP32 && d->precision != SPZ_BF16) return fail(SPZ_EINVAL, "spz_policy_create: unknown precision");
   spz_status st = check_device(d->device);
@@ -198,7 +198,7 @@ spz_status spz_policy_create(const spz_policy_desc* d, spz_policy** out) {
   DeviceGuard dg(d->device);
   std::unique_ptr<spz_policy> p(new spz_policy());
   p->device = d->device;
-  p->td3 = d->algo != SPZ_SAC;  // TD3 and DDPG: deterministic tanh actor
+  p->td3 = d->algo == SPZ_TD3 || d->algo == SPZ_DDPG;  // deterministic tanh actor (SAC v1: SAC's head)
   p->bf16 = d->precision == SPZ_BF16;
   p->o = d->obs_dim;
   p->m = d->act_dim;

@@ -20,11 +20,11 @@ SPZ_OK, SPZ_EINVAL, SPZ_ENODATA, SPZ_ENONFINITE, SPZ_ECUDA, SPZ_ENCCL, SPZ_ENOME
     0, -1, -2, -3, -4, -5, -6, -7, -8, -9)
 STATUS_NAMES = {0: "SPZ_OK", -1: "SPZ_EINVAL", -2: "SPZ_ENODATA", -3: "SPZ_ENONFINITE", -4: "SPZ_ECUDA",
                 -5: "SPZ_ENCCL", -6: "SPZ_ENOMEM", -7: "SPZ_ESTATE", -8: "SPZ_ETIMEOUT", -9: "SPZ_EUNSUPPORTED"}
-SPZ_SAC, SPZ_TD3, SPZ_DDPG = 0, 1, 2
-ALGOS = {"sac": SPZ_SAC, "td3": SPZ_TD3, "ddpg": SPZ_DDPG}
+SPZ_SAC, SPZ_TD3, SPZ_DDPG, SPZ_SACV1 = 0, 1, 2, 3
+ALGOS = {"sac": SPZ_SAC, "td3": SPZ_TD3, "ddpg": SPZ_DDPG, "sacv1": SPZ_SACV1}
 SPZ_FP32, SPZ_BF16 = 0, 1
 SPZ_ROLE_ALL, SPZ_ROLE_CRITIC, SPZ_ROLE_ACTOR = 0, 1, 2
-SPZ_T_ACTOR, SPZ_T_Q1, SPZ_T_Q2, SPZ_T_Q1_TARG, SPZ_T_Q2_TARG, SPZ_T_ACTOR_TARG, SPZ_T_LOG_ALPHA = range(7)
+SPZ_T_ACTOR, SPZ_T_Q1, SPZ_T_Q2, SPZ_T_Q1_TARG, SPZ_T_Q2_TARG, SPZ_T_ACTOR_TARG, SPZ_T_LOG_ALPHA, SPZ_T_V, SPZ_T_V_TARG = range(9)
 SPZ_S_PARAM, SPZ_S_ADAM_M, SPZ_S_ADAM_V = 0, 1, 2
 
 # Every symbol include/spz.h declares (checked by tests/test_abi.py).
@@ -88,7 +88,8 @@ class spz_config(ctypes.Structure):
 class spz_stats(ctypes.Structure):
     _fields_ = [("step", ctypes.c_int64), ("critic_loss", ctypes.c_double), ("actor_loss", ctypes.c_double),
                 ("alpha", ctypes.c_double), ("alpha_loss", ctypes.c_double), ("q1_mean", ctypes.c_double),
-                ("q2_mean", ctypes.c_double), ("logp_mean", ctypes.c_double)]
+                ("q2_mean", ctypes.c_double), ("logp_mean", ctypes.c_double),
+                ("value_loss", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -382,7 +383,8 @@ class Replay:
 
 
 PARAM_TENSORS = {"actor": SPZ_T_ACTOR, "q1": SPZ_T_Q1, "q2": SPZ_T_Q2, "q1_targ": SPZ_T_Q1_TARG,
-                 "q2_targ": SPZ_T_Q2_TARG, "actor_targ": SPZ_T_ACTOR_TARG, "log_alpha": SPZ_T_LOG_ALPHA}
+                 "q2_targ": SPZ_T_Q2_TARG, "actor_targ": SPZ_T_ACTOR_TARG, "log_alpha": SPZ_T_LOG_ALPHA,
+                 "v": SPZ_T_V, "v_targ": SPZ_T_V_TARG}
 
 
 class Learner:

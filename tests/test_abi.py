@@ -48,6 +48,9 @@ def test_config_default_values():
     assert t.td3_noise == 0.2 and t.td3_noise_clip == 0.5 and t.td3_policy_delay == 2 and t.alpha_auto == 0
     dd = spz.spz_config_default(spz.SPZ_DDPG, 22, 6)  # f4: TD3 kernels, no delay, no target smoothing
     assert dd.td3_policy_delay == 1 and dd.td3_noise == 0.0 and dd.td3_noise_clip == 0.0 and dd.alpha_auto == 0
+    v1 = spz.spz_config_default(spz.SPZ_SACV1, 22, 6)  # f4: SAC v1, fixed temperature by default
+    assert v1.alpha_auto == 0 and v1.alpha_init == 0.2 and v1.target_entropy == -6.0
+    assert spz.spz_stats().as_dict()["value_loss"] == 0.0
     with pytest.raises(spz.SpzError):
         spz.spz_config_default(spz.SPZ_SAC, 0, 6)
 

@@ -364,3 +364,43 @@ def test_profile_and_launch_count():
     # gather, 2 fused forwards, loss, critic dgrad, fused actor backward, wgrad, Adam (+ unfused variants)
     assert 8 <= lrn.launches_per_step(8192) <= 16
     assert lrn.counters()["step"] == 3
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("o,m,h,L,B,auto", [(22, 6, 64, 2, 256, False), (22, 6, 256, 2, 1000, False),
+                                            (44, 17, 512, 3, 700, True)])
+def test_sacv1_parity(precision, o, m, h, L, B, auto):
+    """SAC v1 (f4: state-value network V + Polyak target V', no target critics) against oracle/sacv1.py:
+    fused value forward (h <= 256) or the GEMM path (h = 512), loss-kernel g_V, value dgrad / wgrad in the
+    critics' launches, Adam + Polyak on V'.  Fixed temperature (v1's default) and learned (auto)."""
+    from oracle import sacv1 as ov1
+    C, K = 6000, 3
+    g, r = make_rings(o, m, C)
+    p = synthdata.init_params(o, m, h, L, algo="sacv1")
+    lrn = spz.Learner(g, algo="sacv1", precision=precision, hidden=h, n_hidden=L, max_batch=B, alpha_auto=int(auto))
+    for n in ("actor", "q1", "q2", "v"):
+        lrn.set(n, p[n])
+    lrn.set("v_targ", 0.5 * p["v"])  # a target that differs from V, so y_Q really reads V'
+    for absent in ("q1_targ", "q2_targ", "actor_targ"):
+        with pytest.raises(spz.SpzError):
+            lrn.get(absent)
+    cfg = osac.Config(obs_dim=o, act_dim=m, hidden=h, n_hidden=L, alpha_auto=auto)
+    la = float(lrn.get("log_alpha")[0])
+    st = ov1.State.create(p["actor"], p["q1"], p["q2"], p["v"], v_targ=0.5 * p["v"], log_alpha=la)
+    tol = TOL[precision]
+    for k in range(K):
+        gs = lrn.update(B, 1)
+        st, os_, _ = ov1.sacv1_step(st, r, B, synthdata.SAMPLE_SEED, cfg)
+        assert gs["step"] == k + 1
+        for key in ("critic_loss", "value_loss", "actor_loss", "q1_mean", "q2_mean", "logp_mean", "alpha"):
+            ref = os_[key]
+            scale = max(abs(ref), os_.get(key + "_abs", 0.0))
+            assert abs(gs[key] - ref) <= tol * max(scale, 1e-6) + (tol * 1e-2 if key in ("q1_mean", "q2_mean") else 0), (k, key, gs[key], ref)
+    for n in ("actor", "q1", "q2", "v", "v_targ"):
+        assert rel(lrn.get(n), getattr(st, n)) <= tol, (n, rel(lrn.get(n), getattr(st, n)))
+    assert rel(lrn.get("v", spz.SPZ_S_ADAM_M), st.opt["v"].m) <= 10 * tol
+    assert abs(float(lrn.get("log_alpha")[0]) - st.log_alpha) <= tol * max(1.0, abs(st.log_alpha))
+    if not auto:
+        assert float(lrn.get("log_alpha")[0]) == la
+    c = lrn.counters()
+    assert c["step"] == K and c["t_critic"] == K and c["t_actor"] == K and c["t_alpha"] == (K if auto else 0)

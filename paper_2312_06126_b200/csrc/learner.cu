@@ -224,13 +224,14 @@ static spz_status dalloc(spz_learner* Lr, void** p, size_t bytes) {
 }
 
 
-// Split-K count of the merged weight-gradient GEMM: enough splits that the output tiles of all
-// trained weights (128 x 256 each) cover the SMs about once -- more splits only add partial traffic
-// for the Adam kernel.  Monotone in Bl (partials are allocated for the largest batch).
-static int wgrad_splits(const spz_learner* Lr, int64_t Bl) {
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+// Split-K count of the merged weight-gradient GEMM.  Cost model per split count S (microseconds):
+// waves of output tiles (128 x 256 each) over the SMs x (rows each tile contracts + a fixed per-tile
+// cost of ~256 rows: epilogue + partial store) x ~7 ns per row (2*128*256 flops at ~9.3 TF/s per SM),
+// plus the split partials' HBM traffic (written here, read by Adam: 8 B per parameter per split at
+// ~6.5 TB/s).  The cheapest S wins, the smaller on a tie.  (The old fill rule S = floor(SMs / tiles)
+// fell to S = 1 at 88 tiles -- HUM SAC v1 -- leaving 40% of the SMs idle over K = 65536.)  Never above
+// the count at the largest batch, for which the partials are allocated.
+static int wgrad_splits_at(const spz_learner* Lr, int64_t Bl, int sms) {
   const bool actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC, critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
   int64_t tiles = 0;
   auto net_tiles = [&](const NetLayout& n, int layers) {
@@ -239,8 +240,28 @@ static int wgrad_splits(const spz_learner* Lr, int64_t Bl) {
   if (critic_on) net_tiles(Lr->net[NET_Q1], Lr->net[NET_Q1].nl), net_tiles(Lr->net[NET_Q2], Lr->net[NET_Q2].nl);
   if (critic_on && Lr->v1) net_tiles(Lr->net[NET_V], Lr->net[NET_V].nl);
   if (actor_on) net_tiles(Lr->net[NET_ACTOR], Lr->net[NET_ACTOR].nl);
-  const int64_t fill = std::max<int64_t>(1, sms / std::max<int64_t>(1, tiles));
-  return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(32, fill), Bl / 256));
+  tiles = std::max<int64_t>(1, tiles);
+  int64_t params = 0;
+  for (int id : {NET_Q1, NET_Q2, NET_V, NET_ACTOR}) {
+    if (!Lr->has_net[id]) continue;
+    const bool on = id == NET_ACTOR ? actor_on : critic_on;
+    if (on) params += Lr->net[id].np;
+  }
+  const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(32, Bl / 256));
+  int best = 1;
+  double best_cost = 0.0;
+  for (int S = 1; S <= smax; ++S) {
+    const double waves = (double)cdiv(tiles * S, (int64_t)sms);
+    const double cost = waves * ((double)cdiv(Bl, S) + 256.0) * 7e-3 + (double)S * params * 8.0 / 6.5e6;
+    if (S == 1 || cost < best_cost) best = S, best_cost = cost;
+  }
+  return best;
+}
+static int wgrad_splits(const spz_learner* Lr, int64_t Bl) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::min(wgrad_splits_at(Lr, Bl, sms), wgrad_splits_at(Lr, Lr->max_local, sms));
 }
 static int64_t wgrad_rows(int64_t Bl, int s) { return round_up(cdiv(Bl, s), 128); }
 static int bias_splits(int64_t Bl) { return (int)std::max<int64_t>(1, std::min<int64_t>(128, cdiv(Bl, 128))); }

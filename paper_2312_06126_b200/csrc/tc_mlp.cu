@@ -10,8 +10,10 @@
 //               activations leave by TMA bulk stores from H; the actor head runs on the last MMA.
 // Ordering: H is single-buffered.  The epilogue of (unit u, layer l) writes H only after the MMA of
 // layer l (which read H) has completed (its acc_full), and after the TMA stores issued from H for
-// layer l-1 have read it; it then signals h_full, on which the MMA of layer l+1 waits.  The next
-// unit's layer 0 runs in the other TMEM buffer meanwhile.
+// layer l-1 have read it.  It writes H slab by slab (every warp its columns of each 64-column slab) and
+// signals hs[slab] after each, so the MMA of layer l+1 starts on slab 0 while later slabs are still
+// being written; the TMEM accumulator buffers alternate per layer so that MMA does not overwrite the
+// accumulator being drained (acc_empty is signalled per layer).
 #include "tc_mlp.cuh"
 
 #include <algorithm>
@@ -136,6 +138,102 @@ template <int WPQ>
 __device__ __forceinline__ float quarter_sum(const float (*part)[MBM], int r) {
   if constexpr (WPQ == 4) return (part[0][r] + part[1][r]) + (part[2][r] + part[3][r]);
   else return part[0][r] + part[1][r];
+}
+
+// TMEM -> registers for one warp's CW columns (32 lanes x CW), issued without waiting: the caller's
+// tmem_wait<CW>(r) ties the registers to the wait, so the next slab's load overlaps this slab's math
+template <int CW>
+__device__ __forceinline__ void tmem_issue(uint32_t taddr, uint32_t (&r)[CW]) {
+  if constexpr (CW == 32) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                 : "r"(taddr));
+  } else {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr));
+  }
+}
+template <int CW>
+__device__ __forceinline__ void tmem_wait(uint32_t (&r)[CW]) {
+  if constexpr (CW == 32) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+  } else {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+                 :
+                 : "memory");
+  }
+}
+
+// One warp's share of one 64-column slab of a hidden layer (tc_mlp_kernel), from its TMEM registers:
+// CW columns of row r -> bias + ReLU -> bf16 into the slab of H; MASK: the CW mask bits (pre-activation
+// > 0); DOT: row-dot partial with dot_s.  bias_s / dot_s hold this slab's CW entries of the warp.
+template <int CW, bool MASK, bool DOT>
+__device__ __forceinline__ uint32_t slab_math(const uint32_t (&v)[CW], int col0, int r, uint8_t* Hslab, const float* __restrict__ bias_s,
+                                              const float* __restrict__ dot_s, float& dot) {
+  static_assert(CW == 16 || CW == 32, "columns per warp and slab");
+  uint32_t word = 0u, pk[CW / 2];
+#pragma unroll
+  for (int j = 0; j < CW; j += 2) {
+    const float p0 = __uint_as_float(v[j]) + bias_s[j], p1 = __uint_as_float(v[j + 1]) + bias_s[j + 1];
+    if constexpr (MASK) {
+      word |= gt0_mask(p0) & (1u << j);
+      word |= gt0_mask(p1) & (1u << (j + 1));
+    }
+    if constexpr (DOT) {
+      dot = fmaf(fmaxf(p0, 0.f), dot_s[j], dot);
+      dot = fmaf(fmaxf(p1, 0.f), dot_s[j + 1], dot);
+    }
+    pk[j / 2] = pack_relu_bf16(p0, p1);
+  }
+  uint8_t* rowp = Hslab + r * 128;
+  const int u0 = (col0 % 64) / 8;
+#pragma unroll
+  for (int k = 0; k < CW / 8; ++k)
+    *reinterpret_cast<uint4*>(rowp + (((u0 + k) ^ (r & 7)) << 4)) = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+  return word;
+}
+
+// A hidden layer's epilogue for one warp, slab by slab (every warp covers its CW = 64 / WPQ columns of
+// every 64-column slab, so H fills slab by slab): the TMEM load of slab sl+1 is in flight while slab sl
+// is processed; after each slab, hs[sl] is signalled (SIGNAL: the next layer's MMA reads H) and the
+// warp's mask bits of the slab are stored.
+template <int H, int WPQ, bool MASK, bool DOT>
+__device__ __forceinline__ float hidden_epi_slabs(uint32_t trow, int hh, int r, uint8_t* Hs, const float* __restrict__ bias_s,
+                                                  const float* __restrict__ dot_s, bool signal, uint64_t* hs, int lane,
+                                                  uint32_t* mask_row) {
+  constexpr int CW = 64 / WPQ, S = H / 64;
+  float dot = 0.f;
+  uint32_t cur[CW], nxt[CW];
+  tmem_issue<CW>(trow + hh * CW, cur);
+  tmem_wait<CW>(cur);
+#pragma unroll
+  for (int sl = 0; sl < S; ++sl) {
+    const int col0 = sl * 64 + hh * CW;
+    if (sl + 1 < S) tmem_issue<CW>(trow + col0 + 64, nxt);
+    const uint32_t w = slab_math<CW, MASK, DOT>(cur, col0, r, Hs + sl * 16384, bias_s + sl * CW, dot_s + sl * CW, dot);
+    if (signal) {
+      fence_async_smem();  // this thread's H writes -> async proxy (the MMA)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hs[sl]);
+    }
+    if constexpr (MASK) {
+      if (mask_row) {
+        if constexpr (CW == 32) mask_row[col0 / 32] = w;
+        else reinterpret_cast<uint16_t*>(mask_row)[col0 / 16] = (uint16_t)w;
+      }
+    }
+    if (sl + 1 < S) {
+      tmem_wait<CW>(nxt);
+#pragma unroll
+      for (int k = 0; k < CW; ++k) cur[k] = nxt[k];
+    }
+  }
+  return dot;
 }
 
 __device__ __forceinline__ int su_kind(const MlpParams& p, int su) {
@@ -311,7 +409,7 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
   constexpr int NB = CPW / 2;                    // 32-column blocks (= mask words) per warp
   constexpr int SLICE = CPW * 16;
   static_assert(H % 64 == 0 && H <= 256, "hidden width");
-  __shared__ __align__(16) float bias_w[EW][SLICE > 16 ? SLICE : 16];
+  __shared__ __align__(16) float bias_w[EW][SLICE > 64 ? SLICE : 64];  // (the actor head's nh <= 64 biases)
   __shared__ __align__(16) float dotw_w[EW][SLICE];
   __shared__ float dotpart[2][WPQ][MBM];
   __shared__ float qv_s[4][MBM];                    // critic groups: q of each pass, per row
@@ -326,8 +424,8 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
   uint64_t* empty = full + MSTAGES;
   uint64_t* acc_full = empty + MSTAGES;
   uint64_t* acc_empty = acc_full + 2;
-  uint64_t* h_full = acc_empty + 2;
-  uint64_t* x_full = h_full + 1;
+  uint64_t* hs = acc_empty + 2;     // [4]: slab sl of H holds this layer's output (one arrival per epilogue warp)
+  uint64_t* x_full = hs + 4;
   uint64_t* x_empty = x_full + 1;
   // actor: the head weights (<= 16 KB) are loaded into the input-tile region once layer 0 has consumed
   // it, early in the unit and outside the stage ring (whose slots free only as layer 1 completes)
@@ -352,7 +450,7 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], EW);
     }
-    mbar_init(h_full, 1);
+    for (int sl = 0; sl < SLABS; ++sl) mbar_init(&hs[sl], EW);
     mbar_init(x_full, 1);
     mbar_init(x_empty, 1);
     mbar_init(hw_full, 1);
@@ -441,26 +539,26 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer
-      int kg = 0, ui = 0, hcnt = 0;
+      // ---------------- MMA issuer.  Accumulator buffers alternate per layer (gl & 1), so layer l+1 can
+      // run while the epilogue still drains layer l; its K-blocks wait for H slab by slab (hs[kb]).
+      int kg = 0, ui = 0, hcnt = 0, gl = 0;
+      uint32_t ause[2] = {0u, 0u};
       constexpr uint32_t IDESC_H = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(H >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
       const uint32_t IDESC_HEAD = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.nh >> 3) << 17) | ((uint32_t)(MBM >> 4) << 24);
       const uint32_t sH = smem_u32(Hs), sX = smem_u32(Xs);
       for (int su = blockIdx.x; su < TSU; su += gridDim.x)
       for (int j = 0; j < p.gn[su_kind(p, su)]; ++j, ++ui) {
-        const int b = ui & 1;
-        mbar_wait(&acc_empty[b], (((uint32_t)ui >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t acc = tmem + (uint32_t)b * BUF;
-        for (int l = 0; l < NMMA; ++l) {
-          if (l > 0) {  // H holds this unit's layer l-1 output
-            mbar_wait(h_full, (uint32_t)hcnt & 1u);
-            ++hcnt;
-            tc_fence_after();
-          }
+        for (int l = 0; l < NMMA; ++l, ++gl) {
+          const int b = gl & 1;
+          mbar_wait(&acc_empty[b], (ause[b] & 1u) ^ 1u);  // the epilogue drained this buffer's previous layer
+          ++ause[b];
+          tc_fence_after();
+          const uint32_t acc = tmem + (uint32_t)b * BUF;
           mtrace(p.trace, ui, l, 0);
           const int nkb = l == 0 ? p.k0 / MBK : H / MBK;
           const uint32_t idesc = (ACTOR && l == L) ? IDESC_HEAD : IDESC_H;
+          const uint32_t hph = (uint32_t)hcnt & 1u;  // phase of the H slabs of layer l-1
+          if (l > 0) ++hcnt;
           if (l == 0) {
             mbar_wait(x_full, (uint32_t)ui & 1u);
             tc_fence_after();
@@ -472,6 +570,8 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
             mtrace(p.trace, ui, l, 4);
             mtrace(p.trace, ui, l, 5);
             for (int kb = 0; kb < nkb; ++kb) {
+              mbar_wait(&hs[kb], hph);
+              tc_fence_after();
               const uint32_t sB = sX + kb * p.nh * 128;
               const uint32_t aBase = sH + kb * 16384;
 #pragma unroll
@@ -486,6 +586,7 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
           for (int kb = 0; kb < nkb; ++kb, ++kg) {
             const int s = kg % NS;
             mbar_wait(&full[s], (uint32_t)(kg / NS) & 1u);
+            if (l > 0) mbar_wait(&hs[kb], hph);
             tc_fence_after();
             if (kb == 0) mtrace(p.trace, ui, l, 4);
             if (kb == nkb - 1) mtrace(p.trace, ui, l, 5);
@@ -511,8 +612,9 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
     const int r = q * 32 + lane;    // tile row of this thread
     float* bias_s = bias_w[e];
     float* dot_s = dotw_w[e];
-    int ui = 0, dot_tiles = 0;
+    int ui = 0, dot_tiles = 0, gl = 0;
     uint32_t acnt[2] = {0u, 0u};    // acc_full commits consumed per buffer
+    constexpr int CW = 64 / WPQ;    // columns of each 64-column slab owned by this warp
     for (int su = blockIdx.x; su < TSU; su += gridDim.x) {
     const int kind = su_kind(p, su);
     const int m0 = (su - p.su0[kind]) * MBM;
@@ -520,19 +622,20 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
     for (int jp = 0; jp < p.gn[kind]; ++jp, ++ui) {
       const int g = p.gpass[kind][jp];
       const MlpDev& d = p.d[g];
-      const int b = ui & 1;
-      const uint32_t trow = tmem + (uint32_t)b * BUF + ((uint32_t)(q * 32) << 16);
-      for (int l = 0; l < NMMA; ++l) {
+      for (int l = 0; l < NMMA; ++l, ++gl) {
+        const int b = gl & 1;  // accumulator buffers alternate per layer (the MMA issuer's order)
+        const uint32_t trow = tmem + (uint32_t)b * BUF + ((uint32_t)(q * 32) << 16);
         const bool head = ACTOR && l == L;
         const bool last_hidden = !ACTOR && l == L - 1;
         const bool has_dot = last_hidden && d.dot_out != nullptr;
-        // this warp's bias slice (and row-dot weights) of layer l; previous reads ordered by the
-        // __syncwarp / barriers that end every layer
+        // this warp's bias (and row-dot weight) entries of layer l, slab-major: entry sl * CW + c is
+        // column sl * 64 + hh * CW + c; previous reads ordered by the __syncwarp that ends every layer
         if (!head) {
 #pragma unroll
           for (int c = lane; c < SLICE; c += 32) {
-            bias_s[c] = d.bias[l][c_lo * 16 + c];
-            dot_s[c] = has_dot ? d.dot_w[c_lo * 16 + c] : 0.f;
+            const int col = (c / CW) * 64 + hh * CW + c % CW;
+            bias_s[c] = d.bias[l][col];
+            dot_s[c] = has_dot ? d.dot_w[col] : 0.f;
           }
         } else if (lane < 16) {
           for (int c = lane; c < p.nh; c += 16) bias_s[c] = c < p.head_n ? d.bias[l][c] : 0.f;
@@ -566,6 +669,8 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
             else td3_head_block4<__nv_bfloat16>(p.head, d.row0 + m, v4, c);
           }
           tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[b]);  // head accumulator drained by this warp
           if (sac) {
             const int pb = dot_tiles & 1;
             dotpart[pb][hh][r] = lp;
@@ -580,39 +685,31 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
         // ---- hidden layer l: H must be free of the TMA stores issued from it for layer l-1
         if (e == 0 && lane == 0) bulk_wait_read0();
         named_bar(1, EW * 32);
-        uint32_t mw[NB > 0 ? NB : 1];
         const bool want_mask = d.mask[l] != nullptr;
+        const bool signal = l + 1 < NMMA;  // the next layer's MMA reads H slab by slab
+        uint32_t* mrow = want_mask && m < d.rows ? d.mask[l] + (int64_t)m * p.mask_ld : nullptr;
         float dot;
         if (has_dot) {
-          dot = want_mask ? hidden_epi<NB, true, true>(trow, c_lo, r, Hs, bias_s, dot_s, mw)
-                          : hidden_epi<NB, false, true>(trow, c_lo, r, Hs, bias_s, dot_s, mw);
+          dot = want_mask ? hidden_epi_slabs<H, WPQ, true, true>(trow, hh, r, Hs, bias_s, dot_s, signal, hs, lane, mrow)
+                          : hidden_epi_slabs<H, WPQ, false, true>(trow, hh, r, Hs, bias_s, dot_s, signal, hs, lane, mrow);
         } else {
-          dot = want_mask ? hidden_epi<NB, true, false>(trow, c_lo, r, Hs, bias_s, dot_s, mw)
-                          : hidden_epi<NB, false, false>(trow, c_lo, r, Hs, bias_s, dot_s, mw);
+          dot = want_mask ? hidden_epi_slabs<H, WPQ, true, false>(trow, hh, r, Hs, bias_s, dot_s, signal, hs, lane, mrow)
+                          : hidden_epi_slabs<H, WPQ, false, false>(trow, hh, r, Hs, bias_s, dot_s, signal, hs, lane, mrow);
         }
-        tc_fence_before();   // TMEM reads of this layer done
-        fence_async_smem();  // H writes -> async proxy (MMA, TMA store)
-        named_bar(1, EW * 32);
-        if (e == 0 && lane == 0) {
-          mtrace(p.trace, ui, l, 3);
-          if (l + 1 < NMMA) mbar_arrive(h_full);
-          if (d.store[l]) {
+        tc_fence_before();  // TMEM reads of this layer done: the buffer may take layer l+2
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        if (d.store[l]) {
+          // activations leave by TMA bulk stores from H once every warp has written its slabs
+          if (!signal) fence_async_smem();
+          named_bar(1, EW * 32);
+          if (e == 0 && lane == 0) {
 #pragma unroll
             for (int sl = 0; sl < SLABS; ++sl) tma_store_2d(&p.tact[g][l], Hs + sl * 16384, sl * 64, m0);
             bulk_commit();
           }
         }
-        if (d.mask[l] != nullptr && m < d.rows) {
-          uint32_t* dst = d.mask[l] + (int64_t)m * p.mask_ld + (c_lo * 16) / 32;
-          if constexpr (NB == 4) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(mw[0], mw[1 % NB], mw[2 % NB], mw[3 % NB]);
-          } else if constexpr (NB == 2) {
-            *reinterpret_cast<uint2*>(dst) = make_uint2(mw[0], mw[1 % NB]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < NB; ++i) dst[i] = mw[i];
-          }
-        }
+        if (e == 0 && lane == 0) mtrace(p.trace, ui, l, 3);
         if (has_dot) {
           // the warps of this lane quarter combine their slices in a fixed order
           const int pb = dot_tiles & 1;
@@ -624,9 +721,7 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
           ++dot_tiles;
         }
       }
-      // accumulator buffer b drained by this warp
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
     if constexpr (!ACTOR) {
       if (p.gloss[kind]) loss_epilogue<H, WPQ>(p, kind, su, m0, r, hh, e, lane, Hs, qv_s, dot_s, red_s);
@@ -910,7 +1005,7 @@ cudaError_t launch_mlp(MlpParams& p, cudaStream_t st) {
   constexpr int STAGE = H * MBK * 2;
   // dynamic: alignment slack + weight ring + input tile + H + barriers; static: bias / dot slices,
   // dot partials, q values, statistics (+ slack)
-  constexpr int STATIC = 2 * 4 * (H > 64 ? H : 64) * 4 + 2 * WPQ * MBM * 4 + 4 * MBM * 4 + 4 * WPQ * NSTAT * 8 + 1024;
+  constexpr int STATIC = 2 * 4 * WPQ * (H / WPQ > 64 ? H / WPQ : 64) * 4 + 2 * WPQ * MBM * 4 + 4 * MBM * 4 + 4 * WPQ * NSTAT * 8 + 1024;
   const int xbytes = (p.k0 / MBK) * MA_BYTES;
   const int fixed = 1024 + xbytes + (H / 64) * 16384 + 1024;
   const int ns = std::min(MSTAGES, (227 * 1024 - STATIC - fixed) / STAGE);

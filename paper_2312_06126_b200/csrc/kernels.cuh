@@ -406,8 +406,17 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   // the last block sums every block's partial (fixed order: strided per thread, then a fixed tree)
   __syncthreads();
   if (threadIdx.x == 0) {
+    // two-level ticket: same-address atomics serialise in L2, so the blocks count in groups of 32 on
+    // separate counters (ticket[1 + group]) and only each group's last block counts on ticket[0]
     fence_acq_rel_gpu();
-    last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    const unsigned grp = blockIdx.x / 32u, ngrp = (gridDim.x + 31u) / 32u;
+    const unsigned in_grp = min(32u, gridDim.x - grp * 32u);
+    last = false;
+    if (atomicAdd(a.ticket + 1 + grp, 1u) == in_grp - 1) {
+      a.ticket[1 + grp] = 0u;  // ready for the next launch (nobody else touches it in this one)
+      fence_acq_rel_gpu();
+      last = atomicAdd(a.ticket, 1u) == ngrp - 1;
+    }
   }
   __syncthreads();
   if (last) {

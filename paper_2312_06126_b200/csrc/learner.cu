@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -828,13 +829,17 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     // dZ_L written by the loss kernel itself (one row per warp) at h <= 256 up to 16K local rows (WLK
     // 109.1 -> 108.2 us); larger batches do better with the separate critic_dz_kernel (ANT 319.5 -> 315.4 us)
     const bool dz_in_loss = h <= 256 && Bl <= 16384 && !dz_split_env();
-    const int loss_rpw = dz_in_loss ? 1 : 4;
+    // diagnostics: SPZ_DIAG_LOSS=<rpw>,<blocks per SM> for the dZ-writing variant (rpw 1 or 2)
+    int diag_rpw = 1, diag_cap = 4;
+    if (const char* dl = std::getenv("SPZ_DIAG_LOSS")) std::sscanf(dl, "%d,%d", &diag_rpw, &diag_cap);
+    const int loss_rpw = dz_in_loss ? (diag_rpw == 2 ? 2 : 1) : 4;
     int nsm_l = 148, dev_l = 0;
     cudaGetDevice(&dev_l);
     cudaDeviceGetAttribute(&nsm_l, cudaDevAttrMultiProcessorCount, dev_l);
     // grid cap: 2 blocks per SM for the statistics-only variant (HUM 138 -> 118 us, ANT 311 -> 306 us per
-    // update); the dZ-writing variant keeps up to 8 per SM (its stores need the parallelism: WLK 1024 blocks)
-    const int nblk = (int)std::min<int64_t>(cdiv(Bl, LOSS_WARPS * loss_rpw), (dz_in_loss ? 8 : 2) * (int64_t)nsm_l);
+    // update); 4 per SM for the dZ-writing variant -- every block resident at once (64 registers x 256
+    // threads), each walking 1-2 row blocks: WLK 105.2 -> 103.0 us per update against 8 per SM (two waves)
+    const int nblk = (int)std::min<int64_t>(cdiv(Bl, LOSS_WARPS * loss_rpw), (dz_in_loss ? diag_cap : 2) * (int64_t)nsm_l);
     {
       LossArgs la{};
       la.qp = qparts;
@@ -893,6 +898,10 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         if (!dz_in_loss)
           ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
                            return launch_pdl(critic_loss_kernel<T, false, 4>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
+                         }});
+        else if (loss_rpw == 2)
+          ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
+                           return launch_pdl(critic_loss_kernel<T, true, 2>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
                          }});
         else
           ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
@@ -1654,7 +1663,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   std::vector<TensorSlot> slots = trained_tensors(Lr.get());
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->G, Lr->G_total * sizeof(float)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->statsum, 8 * sizeof(double)));
-  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->tickets, 8 * sizeof(unsigned)));
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->tickets, 256 * sizeof(unsigned)));  // [0] + per-group counters (critic_loss_kernel)
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->ctr_snap, 16 * sizeof(int64_t)));
   Lr->debug.push_back({"statsum", Lr->statsum, 8 * sizeof(double), 8});
   if (Lr->gsize > 1 || cfg->comm_mode == 2) {

@@ -36,3 +36,25 @@ def test_class_flops_and_vs_baseline():
     w = synthdata.WORKLOADS["walker"]
     assert bench.vs_baseline(w, 3.7e5) == 1.0
     assert bench.vs_baseline(synthdata.WORKLOADS["ant"], 1.0) is None
+
+
+def test_class_flops_f4_variants():
+    """SAC v1 drops the s2 actor pass and the target critics and adds the value net (V' and V forward over
+    B rows each, V dgrad and wgrad over B rows); DDPG runs the TD3 kernels with no policy delay."""
+    sys.path.insert(0, ROOT)
+    import dataclasses
+    import bench
+    import synthdata
+    w = synthdata.WORKLOADS["walker"]
+    B, o, m, h, L = w.batch, w.obs_dim, w.act_dim, w.hidden, w.n_hidden
+    total = lambda f: sum(v for k, v in f.items() if not k.endswith("_mlp"))
+    sac = bench.class_flops(w, B)
+    v1 = bench.class_flops(dataclasses.replace(w, algo="sacv1"), B)
+    mlp = lambda rows, k_in: 2 * rows * (h * k_in + (L - 1) * h * h)
+    dropped = mlp(B, o) + 2 * B * 2 * m * h + mlp(2 * B, o + m)  # actor on s2 (+ head), target critics
+    added = mlp(2 * B, o) + B * 2 * (L - 1) * h * h + (2 * B * h * o + (L - 1) * 2 * B * h * h + 2 * B * h)
+    assert abs(total(v1) - (total(sac) - dropped + added)) < 1e-6 * total(sac)
+    assert v1["value_fwd_mlp"] == v1["value_fwd_gemm"] == mlp(2 * B, o)
+    td3 = bench.class_flops(dataclasses.replace(w, algo="td3"), B)
+    ddpg = bench.class_flops(dataclasses.replace(w, algo="ddpg"), B)
+    assert total(ddpg) > total(td3)  # the delayed actor work every step

@@ -404,3 +404,24 @@ def test_sacv1_parity(precision, o, m, h, L, B, auto):
         assert float(lrn.get("log_alpha")[0]) == la
     c = lrn.counters()
     assert c["step"] == K and c["t_critic"] == K and c["t_actor"] == K and c["t_alpha"] == (K if auto else 0)
+
+
+def test_sacv1_graph_eager_async_bit_identical():
+    """SAC v1: the graph replay, the eager launches and two updates in flight give bit-identical parameters."""
+    outs = []
+    for mode in ("graph", "eager", "async"):
+        g, _ = make_rings(7, 3, 3000)
+        lrn = spz.Learner(g, algo="sacv1", precision="bf16", hidden=64, n_hidden=2, max_batch=512,
+                          use_graph=(mode != "eager"))
+        if mode == "async":
+            for _ in range(3):
+                lrn.update_async(512, 1)
+            lrn.wait()
+            lrn.wait()
+            lrn.wait()
+        else:
+            lrn.update(512, 3)
+        outs.append([lrn.get(n) for n in ("actor", "q1", "q2", "v", "v_targ")])
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert np.array_equal(a, b)

@@ -1149,12 +1149,13 @@ cudaError_t tc_mlp_fwd(const MlpArgs& a, cudaStream_t st) {
   p.total_su = TSU;
   p.loss = a.loss;
   if (TSU == 0) return cudaSuccess;
-  // critic passes without loss groups and >= 4 row blocks per CTA: two blocks in flight per CTA (ANT:
-  // critic forward 83.9 -> 76.1 us).  With ~2.6 blocks per CTA (WLK) the plain schedule wins (29.7 vs
-  // 31.8 us): the pair schedule's 2-stage weight ring starves layer 1.  SPZ_MLP_PAIR=0 / 1 forces.
+  // critic passes without loss groups and >= 2 row blocks per CTA: two blocks in flight per CTA (ANT:
+  // critic forward 83.9 -> 76.1 us; WLK, ~2.6 blocks per CTA, since the 4-warps-per-quarter epilogue:
+  // 103.0 -> 101.8 us per update -- with 2 epilogue warps per quarter the plain schedule had won there,
+  // 29.7 vs 31.8 us, the pair schedule's 2-stage weight ring starving layer 1).  SPZ_MLP_PAIR=0 / 1 forces.
   const char* pe = std::getenv("SPZ_MLP_PAIR");  // read per launch (plans are built once)
   const int pair_env = pe ? (pe[0] == '1' ? 1 : 0) : -1;
-  const bool pair = pair_env >= 0 ? pair_env == 1 : TSU >= 4 * num_sms();
+  const bool pair = pair_env >= 0 ? pair_env == 1 : TSU >= 2 * num_sms();
   // SPZ_MLP_WPQ=2: two epilogue warps per lane quarter at every width (diagnostics; default mlp_wpq)
   const char* we = std::getenv("SPZ_MLP_WPQ");
   const bool w2 = we && we[0] == '2';

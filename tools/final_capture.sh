@@ -8,5 +8,5 @@ timeout 300 python bench.py --algo sacv1 --no-cpu-baseline 2>/dev/null | tail -1
 timeout 300 python bench.py --algo ddpg --no-cpu-baseline 2>/dev/null | tail -1 > gpurun_out/r01_bench_ddpg.json
 timeout 600 ncu --metrics gpu__time_duration.sum,launch__grid_size,sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --cache-control none -s 90 -c 40 --csv --log-file gpurun_out/r01_launches_warm_final.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 90 -c 40 --csv --log-file gpurun_out/r01_launches_basic.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:tc_mlp_kernel -s 20 -c 2 -o gpurun_out/mlp_full python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:tc_mlp -s 20 -c 2 -o gpurun_out/mlp_full python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 ls -la gpurun_out/

@@ -82,6 +82,19 @@ __device__ __forceinline__ void normals4(uint64_t seed, uint64_t step, uint32_t 
   }
 }
 
+// Box-Muller pair `half` (0: x.x, x.y; 1: x.z, x.w) of the same Philox draw as normals4: bit-identical to
+// normals4's n[2 half], n[2 half + 1]
+__device__ __forceinline__ void normals2(uint64_t seed, uint64_t step, uint32_t stream, uint64_t row, int c, int half,
+                                         float (&n)[2]) {
+  const uint4 x = philox(make_uint4((uint32_t)row, (uint32_t)c, (uint32_t)step, stream), (uint32_t)seed,
+                         (uint32_t)(seed >> 32));
+  float s, co;
+  const float R = sqrtf(-2.0f * logf(u01(half ? x.z : x.x)));
+  sincospif(2.0f * u01(half ? x.w : x.y), &s, &co);
+  n[0] = R * co;
+  n[1] = R * s;
+}
+
 // ------------------------------------------------------------------ element types
 template <typename T> __device__ __forceinline__ T from_f(float x);
 template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }

@@ -62,6 +62,41 @@ __device__ __forceinline__ float sac_head_block4(const HeadEpi& h, int r, const 
   }
   return lp;
 }
+// Half `half` of Philox block c of row r: actions 4c + 2 half + {0, 1} (< m) from the Box-Muller pair
+// `half` of the block's draw (so the work of one block can be split over two warps).
+template <typename T>
+__device__ __forceinline__ float sac_head_half(const HeadEpi& h, int r, const float (&mu2)[2], const float (&l2)[2], int c, int half) {
+  const bool s2row = r < h.Bl;
+  const int j = s2row ? r : r - h.Bl;
+  const uint64_t step = (uint64_t)*h.step_p;
+  const uint32_t stream = s2row ? S_EPS2 : S_EPS;
+  T* xa = static_cast<T*>(h.Xc) + (int64_t)(s2row ? 2 * h.Bl + j : h.Bl + j) * h.ldx + h.o;
+  float e2[2];
+  normals2(h.seed, step, stream, (uint64_t)(h.row0 + j), c, half, e2);
+  float lp = 0.f;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = 4 * c + 2 * half + k;
+    if (i >= h.m) break;
+    const float l = l2[k];
+    const float lc = fminf(fmaxf(l, h.lo), h.hi);
+    const float sg = expf(lc);
+    const float e = e2[k];
+    const float u = fmaf(sg, e, mu2[k]);
+    const float a = tanhf(u);
+    lp += -0.5f * e * e - lc - HALF_LN_2PI_F - 2.f * (LN2F - u - softplusf(-2.f * u));
+    xa[i] = from_f<T>(a);
+    if (!s2row) {
+      const int64_t ci = (int64_t)i * h.Bl + j;
+      h.u[ci] = u;
+      h.a[ci] = a;
+      h.eps[ci] = e;
+      h.sig[ci] = sg;
+      h.l[ci] = l;
+    }
+  }
+  return lp;
+}
 // Philox blocks c = b0, b0 + bstep, ... of row r from the head row arrays mu[0..m), lraw[0..m).
 template <typename T>
 __device__ __forceinline__ float sac_head_blocks(const HeadEpi& h, int r, const float* mu, const float* lraw, int b0,

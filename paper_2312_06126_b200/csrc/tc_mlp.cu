@@ -654,19 +654,32 @@ __global__ void __launch_bounds__(mlp_threads(WPQ), 1) tc_mlp_kernel(const __gri
           const bool live = m < d.rows;
           const bool sac = p.head_epi == EPI_SAC_HEAD;
           float lp = 0.f;
-          for (int c = hh; 4 * c < mh; c += WPQ) {
-            float v4[4], l4[4] = {0.f, 0.f, 0.f, 0.f};
-            tmem_ld1x4(trow + (uint32_t)(4 * c), v4);
-            if (sac) tmem_ld1x4(trow + (uint32_t)(mh + 4 * c), l4);
+          if (sac) {
+            // SAC: work items = halves of Philox blocks (actions 2 it, 2 it + 1; one Box-Muller pair each),
+            // taken in turn by the WPQ warps of the quarter (m = 6: 3 items instead of 2 blocks)
+            for (int it = hh; 2 * it < mh; it += WPQ) {
+              float v4[4], l4[4];
+              tmem_ld1x4(trow + (uint32_t)(2 * it), v4);
+              tmem_ld1x4(trow + (uint32_t)(mh + 2 * it), l4);
+              float mu2[2], l2[2];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int i = min(4 * c + k, mh - 1);
-              v4[k] += bias_s[i];
-              l4[k] += sac ? bias_s[mh + i] : 0.f;
+              for (int k = 0; k < 2; ++k) {
+                const int i = min(2 * it + k, mh - 1);
+                mu2[k] = v4[k] + bias_s[i];
+                l2[k] = l4[k] + bias_s[mh + i];
+              }
+              if (!live) continue;
+              lp += sac_head_half<__nv_bfloat16>(p.head, d.row0 + m, mu2, l2, it >> 1, it & 1);
             }
-            if (!live) continue;
-            if (sac) lp += sac_head_block4<__nv_bfloat16>(p.head, d.row0 + m, v4, l4, c);
-            else td3_head_block4<__nv_bfloat16>(p.head, d.row0 + m, v4, c);
+          } else {
+            for (int c = hh; 4 * c < mh; c += WPQ) {
+              float v4[4];
+              tmem_ld1x4(trow + (uint32_t)(4 * c), v4);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) v4[k] += bias_s[min(4 * c + k, mh - 1)];
+              if (!live) continue;
+              td3_head_block4<__nv_bfloat16>(p.head, d.row0 + m, v4, c);
+            }
           }
           tc_fence_before();
           __syncwarp();

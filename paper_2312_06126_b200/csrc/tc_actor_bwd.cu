@@ -21,7 +21,14 @@ namespace spz {
 namespace {
 
 constexpr int ABM = 128, ABK = 64, AB_STAGES = 4;
-constexpr int AB_EPI_WARPS = 8, AB_NTHREADS = 64 + AB_EPI_WARPS * 32;
+// epilogue warps: AB_WPQ per TMEM lane quarter, each owning H / AB_WPQ columns of the masked gradients
+#ifndef SPZ_AB_WPQ
+#define SPZ_AB_WPQ 4
+#endif
+template <int H>
+constexpr int ab_wpq() { return H >= 128 ? SPZ_AB_WPQ : 2; }  // (a warp keeps whole 32-column mask words)
+template <int H>
+constexpr int ab_threads() { return 64 + 4 * ab_wpq<H>() * 32; }
 constexpr uint32_t AB_TMEM_COLS = 512, S2_COL = 256;
 
 struct ActorBwdParams {
@@ -80,10 +87,11 @@ __device__ __forceinline__ void mask_epi(uint32_t trow, int c_lo, int r, uint8_t
 }
 
 template <int H>
-__global__ void __launch_bounds__(AB_NTHREADS, 1) tc_actor_bwd_kernel(const __grid_constant__ ActorBwdParams p) {
+__global__ void __launch_bounds__(ab_threads<H>(), 1) tc_actor_bwd_kernel(const __grid_constant__ ActorBwdParams p) {
   constexpr int SLABS = H / 64;
   constexpr int STAGE = (16384 + 8192) > SLABS * 8192 ? (16384 + 8192) : SLABS * 8192;
-  constexpr int NB = H / 2 / 32;  // 32-column blocks per epilogue warp (column half)
+  constexpr int AB_WPQ = ab_wpq<H>(), AB_EPI_WARPS = 4 * AB_WPQ;
+  constexpr int NB = H / AB_WPQ / 32;  // 32-column blocks per epilogue warp
   constexpr uint32_t IDESC1 = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) |
                               ((uint32_t)(ABM >> 4) << 24);
   constexpr uint32_t IDESCH = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(H >> 3) << 17) |
@@ -294,7 +302,7 @@ __global__ void __launch_bounds__(AB_NTHREADS, 1) tc_actor_bwd_kernel(const __gr
       for (int l = L - 1; l >= 0; --l) {
         // this warp's mask words of the row, loaded before the accumulator wait
         uint32_t mw[NB];
-        const uint32_t* mrow = p.mask[l] + (int64_t)(live ? j : 0) * p.mask_ld + hh * (H / 2) / 32;
+        const uint32_t* mrow = p.mask[l] + (int64_t)(live ? j : 0) * p.mask_ld + hh * (H / AB_WPQ) / 32;
 #pragma unroll
         for (int ib = 0; ib < NB; ++ib) mw[ib] = live ? __ldg(mrow + ib) : 0u;
         wait_acc();
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(AB_NTHREADS, 1) tc_actor_bwd_kernel(const __gr
         if (e == 0 && lane == 0) bulk_wait_read_all();
         named_bar(1, AB_EPI_WARPS * 32);
         const uint32_t trow = tmem + lane_off + (l == L - 1 ? S2_COL : 0u);
-        mask_epi<NB>(trow, hh * (H / 2), r, Hs, mw);
+        mask_epi<NB>(trow, hh * (H / AB_WPQ), r, Hs, mw);
         tc_fence_before();
         fence_async_smem();
         named_bar(1, AB_EPI_WARPS * 32);
@@ -347,7 +355,7 @@ cudaError_t launch_ab(ActorBwdParams& p, cudaStream_t st) {
   }
   p.stages = ns;
   const int grid = std::min(p.tiles, num_sms());
-  return launch_pdl(kern, dim3(grid), dim3(AB_NTHREADS), (size_t)(ns * STAGE + fixed), st, p);
+  return launch_pdl(kern, dim3(grid), dim3(ab_threads<H>()), (size_t)(ns * STAGE + fixed), st, p);
 }
 
 }  // namespace

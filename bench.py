@@ -382,12 +382,14 @@ def main():
             # the GPU, read back update k-2's statistics (D2H), enqueue update k (spz_update_async / _wait,
             # two updates in flight)
             for k in range(K2):
-                ring.push(**{n: v[sl(k)] for n, v in pinned.items()})
+                # push_async: the slice stays untouched until the next push returns (4 rotating slices)
+                ring.push(**{n: v[sl(k)] for n, v in pinned.items()}, wait=False)
                 if k >= 2:
                     lrn.wait()
                 lrn.update_async(GB, 1)
             lrn.wait()
             lrn.wait()
+            ring.sync()
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             if world > 1:
@@ -398,7 +400,7 @@ def main():
         e2e = {"value": statistics.median(runs), "unit": "frames/s",
                "h2d_bytes_per_step": GB * R_fields * 4 * world,
                "d2h_bytes_per_step": 9 * 8 + 8 * 8 + 16, "steps": K2, "runs": runs,  # the read-back block (stats, counters, flag)
-               "note": "median of 3 host-timed runs; per step: spz_replay_push of B fresh host transitions (pinned, H2D) "
+               "note": "median of 3 host-timed runs; per step: spz_replay_push_async of B fresh host transitions (pinned, H2D) "
                        "overlapping the updates in flight, spz_update_wait (stats D2H of the oldest), spz_update_async(B, 1); "
                        "two updates in flight"}
 

@@ -78,6 +78,16 @@ spz_status spz_replay_create(const spz_replay_desc* desc, spz_replay** out);
 spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const float* act,
                            const float* rew, const float* next_obs, const float* done,
                            int32_t src_on_device, int64_t* first_global_index);
+/* As spz_replay_push, but for page-locked host fields it returns once the copies are enqueued: the
+ * caller keeps the five buffers unchanged until the NEXT spz_replay_push / spz_replay_push_async on this
+ * ring returns, or spz_replay_sync(r) does (so two alternating host buffer sets suffice).  Pageable or
+ * device sources behave exactly like spz_replay_push.  Lets a producer stream transitions without
+ * waiting for each H2D copy (P:278-288 ingest; the e2e loop of bench.py). */
+spz_status spz_replay_push_async(spz_replay* r, int64_t n, const float* obs, const float* act,
+                                 const float* rew, const float* next_obs, const float* done,
+                                 int32_t src_on_device, int64_t* first_global_index);
+/* Wait until the host buffers of the last spz_replay_push_async have been read. */
+spz_status spz_replay_sync(spz_replay* r);
 
 /* Uniform sample with replacement over slots [0, F), F = current fill (S:203,
  * S:228): for j in [0, batch), (x0,x1,x2,x3) = Philox4x32-10(key = seed,

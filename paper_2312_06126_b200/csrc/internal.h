@@ -71,6 +71,7 @@ struct spz_replay {
   // ordering against in-flight updates (the update reads the pool while samplers write it):
   // every write to `rec` is enqueued after the readers' last recorded reads; learners wait on ev_pack
   cudaEvent_t ev_copy = nullptr;       // pinned push: the caller's buffers have been read (H2D done)
+  bool copy_pending = false;           // spz_replay_push_async: ev_copy not yet waited for
   cudaEvent_t ev_pack = nullptr;       // the last push's records are in `rec`
   std::vector<cudaEvent_t> readers;    // one per learner: its last enqueued update (registered at create)
   // experience transmission loss (spz_replay_track): one "sampled" bit per slot, set by every sample;

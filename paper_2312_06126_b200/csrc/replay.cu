@@ -149,6 +149,10 @@ cudaError_t ring_enqueue_pack(spz_replay* r, cudaStream_t st) {
   float* d_nobs = d_act + nn * m;
   float* d_rew = d_nobs + nn * o;
   float* d_done = d_rew + nn;
+  if (st != r->stream) {  // on a learner stream: after the push's H2D copies (spz_replay_push_async returns before them)
+    const cudaError_t we = cudaStreamWaitEvent(st, r->ev_copy, 0);
+    if (we != cudaSuccess) return we;
+  }
   if (r->tags && nn > 0) {
     const int64_t occupied = p.first < r->C ? p.first : r->C;
     loss_account_kernel<<<(unsigned)cdiv(nn, 256), 256, 0, st>>>(r->tags, r->C, p.start % r->C, nn, occupied, p.first,
@@ -213,13 +217,17 @@ spz_status spz_replay_create(const spz_replay_desc* desc, spz_replay** out) {
   return SPZ_OK;
 }
 
-spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const float* act, const float* rew,
-                           const float* next_obs, const float* done, int32_t src_on_device, int64_t* first) {
+static spz_status push_impl(spz_replay* r, int64_t n, const float* obs, const float* act, const float* rew,
+                            const float* next_obs, const float* done, int32_t src_on_device, int64_t* first, bool async) {
   if (!r) return fail(SPZ_EINVAL, "spz_replay_push: NULL ring");
   if (n < 0) return fail(SPZ_EINVAL, "spz_replay_push: n < 0");
   if (n > 0 && (!obs || !act || !rew || !next_obs || !done)) return fail(SPZ_EINVAL, "spz_replay_push: NULL field array");
   DeviceGuard dg(r->device);
   std::lock_guard<std::mutex> lk(r->mu);
+  if (r->copy_pending) {  // the previous asynchronous push's buffers are read before this push returns
+    SPZ_CUDA_TRY(cudaEventSynchronize(r->ev_copy));
+    r->copy_pending = false;
+  }
   const int64_t first_idx = r->cursor;
   if (first) *first = first_idx;
   if (n == 0) return SPZ_OK;
@@ -289,7 +297,8 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
     r->pend.fill_after = std::min(first_idx + n, r->C);
     // the pack waits for the staged data: on the ring stream it follows the copies; a learner stream
     // that takes it waits for ev_copy (ring_enqueue_pack callers)
-    SPZ_CUDA_TRY(cudaEventSynchronize(r->ev_copy));  // return once the caller's buffers are read
+    if (async) r->copy_pending = true;  // read by the time the next push (or spz_replay_sync) returns
+    else SPZ_CUDA_TRY(cudaEventSynchronize(r->ev_copy));  // return once the caller's buffers are read
     r->cursor += n;
     return SPZ_OK;
   } else {
@@ -329,6 +338,27 @@ spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const flo
   SPZ_CUDA_TRY(cudaEventRecord(r->ev_pack, r->stream));
   SPZ_CUDA_TRY(cudaStreamSynchronize(r->stream));
   r->cursor += n;
+  return SPZ_OK;
+}
+
+spz_status spz_replay_push(spz_replay* r, int64_t n, const float* obs, const float* act, const float* rew,
+                           const float* next_obs, const float* done, int32_t src_on_device, int64_t* first) {
+  return push_impl(r, n, obs, act, rew, next_obs, done, src_on_device, first, false);
+}
+
+spz_status spz_replay_push_async(spz_replay* r, int64_t n, const float* obs, const float* act, const float* rew,
+                                 const float* next_obs, const float* done, int32_t src_on_device, int64_t* first) {
+  return push_impl(r, n, obs, act, rew, next_obs, done, src_on_device, first, true);
+}
+
+spz_status spz_replay_sync(spz_replay* r) {
+  if (!r) return fail(SPZ_EINVAL, "spz_replay_sync: NULL ring");
+  DeviceGuard dg(r->device);
+  std::lock_guard<std::mutex> lk(r->mu);
+  if (r->copy_pending) {
+    SPZ_CUDA_TRY(cudaEventSynchronize(r->ev_copy));
+    r->copy_pending = false;
+  }
   return SPZ_OK;
 }
 

@@ -29,7 +29,8 @@ SPZ_S_PARAM, SPZ_S_ADAM_M, SPZ_S_ADAM_V = 0, 1, 2
 
 # Every symbol include/spz.h declares (checked by tests/test_abi.py).
 EXPORTS = [
-    "spz_last_error", "spz_version", "spz_replay_create", "spz_replay_push", "spz_replay_sample", "spz_replay_info",
+    "spz_last_error", "spz_version", "spz_replay_create", "spz_replay_push", "spz_replay_push_async", "spz_replay_sync",
+    "spz_replay_sample", "spz_replay_info",
     "spz_replay_records", "spz_replay_destroy", "spz_config_default", "spz_nccl_unique_id", "spz_learner_create",
     "spz_update", "spz_update_async", "spz_update_wait", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
@@ -112,6 +113,8 @@ def lib():
             "spz_version": (ctypes.c_char_p, []),
             "spz_replay_create": (ctypes.c_int, [ctypes.POINTER(spz_replay_desc), ctypes.POINTER(P)]),
             "spz_replay_push": (ctypes.c_int, [P, I64, P, P, P, P, P, I32, ctypes.POINTER(I64)]),
+            "spz_replay_push_async": (ctypes.c_int, [P, I64, P, P, P, P, P, I32, ctypes.POINTER(I64)]),
+            "spz_replay_sync": (ctypes.c_int, [P]),
             "spz_replay_sample": (ctypes.c_int, [P, I64, U64, U64, P, P, P, P, P, P]),
             "spz_replay_info": (ctypes.c_int, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
             "spz_replay_records": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(I32)]),
@@ -187,14 +190,16 @@ def _ptr(x):
     return x.ctypes.data_as(ctypes.c_void_p)
 
 
-def spz_replay_push(ring, obs, act, rew, next_obs, done, src_on_device=False):
-    """Host path: float32 numpy arrays; device path: torch CUDA float32 tensors."""
+def spz_replay_push(ring, obs, act, rew, next_obs, done, src_on_device=False, wait=True):
+    """Host path: float32 numpy arrays; device path: torch CUDA float32 tensors.  wait=False:
+    spz_replay_push_async (page-locked host arrays stay untouched until the next push or spz_replay_sync)."""
     n = len(rew)
     if not src_on_device:
         obs, act, rew, next_obs, done = [np.ascontiguousarray(a, dtype=np.float32) for a in (obs, act, rew, next_obs, done)]
     first = ctypes.c_int64()
-    _check(lib().spz_replay_push(ring, n, _ptr(obs), _ptr(act), _ptr(rew), _ptr(next_obs), _ptr(done),
-                                 1 if src_on_device else 0, ctypes.byref(first)))
+    fn = lib().spz_replay_push if wait else lib().spz_replay_push_async
+    _check(fn(ring, n, _ptr(obs), _ptr(act), _ptr(rew), _ptr(next_obs), _ptr(done), 1 if src_on_device else 0,
+              ctypes.byref(first)))
     return first.value
 
 
@@ -354,8 +359,12 @@ class Replay:
         self.obs_dim, self.act_dim, self.capacity, self.device = obs_dim, act_dim, capacity, device
         self.h = spz_replay_create(obs_dim, act_dim, capacity, device)
 
-    def push(self, obs, act, rew, next_obs, done, src_on_device=False):
-        return spz_replay_push(self.h, obs, act, rew, next_obs, done, src_on_device)
+    def push(self, obs, act, rew, next_obs, done, src_on_device=False, wait=True):
+        return spz_replay_push(self.h, obs, act, rew, next_obs, done, src_on_device, wait)
+
+    def sync(self):
+        """Wait until the host buffers of the last push(..., wait=False) have been read."""
+        _check(lib().spz_replay_sync(self.h))
 
     def info(self):
         return spz_replay_info(self.h)

@@ -63,3 +63,62 @@ def test_track_errors_and_restart():
     g.track(False)
     with pytest.raises(spz.SpzError):
         g.loss()
+
+
+def test_push_async_matches_sync_and_buffer_contract():
+    """spz_replay_push_async: the same records as spz_replay_push (gathered rows bit-identical to the oracle
+    ring); a pinned buffer may be overwritten once the NEXT push returns (two alternating sets suffice), and
+    spz_replay_sync covers the last one."""
+    torch = pytest.importorskip("torch")
+    o, m, C, n = 5, 2, 4096, 700
+    tr = [synthdata.transitions("locomotion", o, m, n, seed=100 + i) for i in range(6)]
+    bufs = [{k: torch.from_numpy(v.copy()).pin_memory().numpy() for k, v in tr[0].items()} for _ in range(2)]
+    g = spz.Replay(o, m, C)
+    r = oring.Ring(o, m, C)
+    for i in range(6):
+        b = bufs[i % 2]
+        for k in b:
+            b[k][...] = tr[i][k]  # refill: the push that used this set two pushes ago has returned since
+        first = g.push(**b, wait=False)
+        assert first == r.push(**tr[i])
+    g.sync()
+    for b in bufs:  # after sync every buffer may change without touching the ring
+        for k in b:
+            b[k][...] = -7.0
+    B = 512
+    idx = torch.empty(B, dtype=torch.int32, device="cuda")
+    obs = torch.empty(B, o, device="cuda")
+    act = torch.empty(B, m, device="cuda")
+    rew = torch.empty(B, device="cuda")
+    nobs = torch.empty(B, o, device="cuda")
+    done = torch.empty(B, device="cuda")
+    spz.spz_replay_sample(g.h, B, synthdata.SAMPLE_SEED, 3, idx, obs, act, rew, nobs, done)
+    ridx, rb = r.sample(B, synthdata.SAMPLE_SEED, 3)
+    assert np.array_equal(idx.cpu().numpy(), ridx)
+    for name, t in (("obs", obs), ("act", act), ("rew", rew), ("next_obs", nobs), ("done", done)):
+        assert np.array_equal(t.cpu().numpy(), rb[name]), name
+
+
+def test_update_with_async_pushes_bit_identical():
+    """An update loop fed by spz_replay_push_async equals the same loop fed by spz_replay_push."""
+    torch = pytest.importorskip("torch")
+    o, m, B = 22, 6, 1024
+    outs = []
+    for wait in (True, False):
+        g = spz.Replay(o, m, 20_000)
+        g.push(**synthdata.transitions("locomotion", o, m, 8000))
+        lrn = spz.Learner(g, precision="bf16", hidden=64, n_hidden=2, max_batch=B)
+        host = synthdata.transitions("locomotion", o, m, 4 * B, seed=77)
+        pinned = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in host.items()}
+        for k in range(6):
+            sl = slice((k % 4) * B, (k % 4 + 1) * B)
+            g.push(**{n: v[sl] for n, v in pinned.items()}, wait=wait)
+            if k >= 2:
+                lrn.wait()
+            lrn.update_async(B, 1)
+        lrn.wait()
+        lrn.wait()
+        g.sync()
+        outs.append([lrn.get(n) for n in ("actor", "q1", "q2")])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)

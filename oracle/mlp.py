@@ -44,15 +44,25 @@ def flatten(params):
     return np.concatenate([np.concatenate([W.ravel(), b.ravel()]) for W, b in params])
 
 
-def forward(params, X):
-    """Returns (output, cache).  cache = list of layer inputs and pre-activations."""
+def forward(params, X, relu_masks=None):
+    """Returns (output, cache).  cache = list of layer inputs, pre-activations and ReLU decisions.
+
+    relu_masks (optional, one boolean [rows x out] array per hidden layer): the ReLU decisions
+    1[Z > 0] taken elsewhere -- by the kernel, in its precision -- and used here in place of this
+    function's own fp64 comparison (the task's rule for decisions a floating-point value takes;
+    DESIGN.md reading #25).  None: the plain ReLU."""
     A = np.asarray(X, dtype=np.float64)
     cache = []
     L = len(params)
     for l, (W, b) in enumerate(params):
         Z = A @ W.T + b
-        cache.append((A, Z))
-        A = np.maximum(Z, 0.0) if l < L - 1 else Z
+        if l < L - 1:
+            mask = (Z > 0.0) if relu_masks is None else np.asarray(relu_masks[l], dtype=bool)
+            cache.append((A, Z, mask))
+            A = np.where(mask, Z, 0.0)
+        else:
+            cache.append((A, Z, None))
+            A = Z
     return A, cache
 
 
@@ -63,12 +73,11 @@ def backward(params, cache, dY):
     dZ = np.asarray(dY, dtype=np.float64)
     for l in range(L - 1, -1, -1):
         W, _ = params[l]
-        A_in, _ = cache[l]
+        A_in = cache[l][0]
         grads[l] = (dZ.T @ A_in, dZ.sum(axis=0))
         dA = dZ @ W
         if l > 0:
-            _, Z_prev = cache[l - 1]
-            dZ = dA * (Z_prev > 0.0)
+            dZ = dA * cache[l - 1][2]  # ReLU'(Z) = 1[Z > 0] (ReLU'(0) = 0)
         else:
             dX = dA
     return grads, dX

@@ -119,10 +119,10 @@ def sigmoid(x):
     return np.where(x >= 0, 1.0 / (1.0 + e), e / (1.0 + e))
 
 
-def policy_forward(actor_params, s, eps, cfg):
+def policy_forward(actor_params, s, eps, cfg, relu_masks=None):
     """Squashed-Gaussian policy (§8(c) step 3)."""
     m = cfg.act_dim
-    H, cache = mlp.forward(actor_params, s)
+    H, cache = mlp.forward(actor_params, s, relu_masks)
     mu, l = H[:, :m], H[:, m:2 * m]
     lc = np.clip(l, cfg.log_std_min, cfg.log_std_max)
     sigma = np.exp(lc)
@@ -154,8 +154,8 @@ def policy_head_backward(head, g_a, g_lp, cfg):
     return np.concatenate([g_mu, g_l], axis=1)
 
 
-def critic_q(params, s, a):
-    q, cache = mlp.forward(params, np.concatenate([s, a], axis=1))
+def critic_q(params, s, a, relu_masks=None):
+    q, cache = mlp.forward(params, np.concatenate([s, a], axis=1), relu_masks)
     return q[:, 0], cache
 
 
@@ -173,13 +173,19 @@ def min_weights(q1, q2):
     return w1, 1.0 - w1
 
 
-def sac_grads(st, batch, eps, eps2, cfg, B_global, critic=True, actor=True):
+def sac_grads(st, batch, eps, eps2, cfg, B_global, critic=True, actor=True, decisions=None):
     """Gradients of L_Q (critics), L_pi (actor) and L_alpha over the given rows.
 
     Every row contributes with the global 1/B, so gradients of row shards add
     up exactly.  Returns (grads, sums) where sums holds the
     row sums behind the reported statistics.
+
+    decisions (optional; reading #25): the comparisons a floating-point value decides,
+    taken by the kernel in its precision and used here instead of this oracle's own -- ReLU masks
+    "q1"/"q2" (online critics on the loss rows), "q1_pi"/"q2_pi" (on the actor rows), "actor" (the
+    actor on s), and "w1" (the min-tie weight of Q1 on the actor rows).  Absent keys: own decisions.
     """
+    dec = decisions or {}
     s, a, r, s2, d = _batch_f64(batch)
     m, o = cfg.act_dim, cfg.obs_dim
     alpha = np.exp(st.log_alpha)
@@ -194,7 +200,7 @@ def sac_grads(st, batch, eps, eps2, cfg, B_global, critic=True, actor=True):
         y = r + cfg.gamma * (1.0 - d) * (np.minimum(qt1, qt2) - alpha * logp2)
         lq = 0.0
         for i in range(2):
-            q, cache = critic_q(Q[i], s, a)
+            q, cache = critic_q(Q[i], s, a, dec.get(f"q{i + 1}"))
             dq = 2.0 * (q - y) / B_global
             g, _ = mlp.backward(Q[i], cache, dq.reshape(-1, 1))
             grads[f"q{i + 1}"] = mlp.flatten(g)
@@ -204,13 +210,16 @@ def sac_grads(st, batch, eps, eps2, cfg, B_global, critic=True, actor=True):
         sums["lq"] = lq
         sums["y"] = y
     if actor:
-        at, logpt, acache, head = policy_forward(A, s, eps, cfg)
+        at, logpt, acache, head = policy_forward(A, s, eps, cfg, dec.get("actor"))
         qs, caches = [], []
         for i in range(2):
-            q, cache = critic_q(Q[i], s, at)
+            q, cache = critic_q(Q[i], s, at, dec.get(f"q{i + 1}_pi"))
             qs.append(q)
             caches.append(cache)
         w1, w2 = min_weights(qs[0], qs[1])
+        if "w1" in dec:
+            w1 = np.asarray(dec["w1"], np.float64)
+            w2 = 1.0 - w1
         g_a = np.zeros_like(at)
         for i, w in enumerate((w1, w2)):
             dq = -w / B_global

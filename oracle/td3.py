@@ -27,7 +27,9 @@ def is_delayed(step, cfg):
     return (step + 1) % cfg.td3_policy_delay == 0
 
 
-def td3_grads(st, batch, xi, cfg, B_global, step, critic=True, actor=True):
+def td3_grads(st, batch, xi, cfg, B_global, step, critic=True, actor=True, decisions=None):
+    """decisions: as sac.sac_grads ("q1", "q2", "q1_pi", "actor" ReLU masks; reading #25)."""
+    dec = decisions or {}
     s, a, r, s2, d = _batch_f64(batch)
     o, m = cfg.obs_dim, cfg.act_dim
     ash = actor_shapes(cfg, td3=True)
@@ -43,7 +45,7 @@ def td3_grads(st, batch, xi, cfg, B_global, step, critic=True, actor=True):
         lq = 0.0
         for i, th in enumerate((st.q1, st.q2)):
             P = mlp.unflatten(th, cs)
-            q, cache = critic_q(P, s, a)
+            q, cache = critic_q(P, s, a, dec.get(f"q{i + 1}"))
             g, _ = mlp.backward(P, cache, (2.0 * (q - y) / B_global).reshape(-1, 1))
             grads[f"q{i + 1}"] = mlp.flatten(g)
             lq = lq + np.sum((q - y) ** 2)
@@ -53,10 +55,10 @@ def td3_grads(st, batch, xi, cfg, B_global, step, critic=True, actor=True):
         sums["y"] = y
     if actor and is_delayed(step, cfg):
         A = mlp.unflatten(st.actor, ash)
-        z, acache = mlp.forward(A, s)
+        z, acache = mlp.forward(A, s, dec.get("actor"))
         at = np.tanh(z)
         Q1 = mlp.unflatten(st.q1, cs)
-        q, cache = critic_q(Q1, s, at)
+        q, cache = critic_q(Q1, s, at, dec.get("q1_pi"))
         _, dX = mlp.backward(Q1, cache, np.full((s.shape[0], 1), -1.0 / B_global))
         g_a = dX[:, o:o + m]
         dZ = g_a * (1.0 - at * at)

@@ -1,21 +1,28 @@
 """Benchmark: SAC/TD3 update frames/s on B200 (BASELINE.json metric) -- one JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config walker] [--precision bf16]
+    python bench.py --gpus 2 --dry-run        # the multi-GPU plan under gloo (no GPU needed)
     python bench.py --impl reference ...      # the float64 CPU oracle arm (host cores)
 
-A "step" is one full update over one batch of B transitions
-sampled from a device-resident ring filled with synthetic transitions (synthdata).
-value = B * K * N / (max over ranks of the CUDA-event time of K steps) [frames/s];
-frames/s = update frequency x B.  With N > 1 (torchrun, one process per GPU) the
-default --mode dp runs ONE row-sharded learner group over a global batch of B * N (each
-GPU B rows; gradients all-reduced with NCCL inside the step; weak scaling); --mode
-replicas runs N independent learners instead.
+A "step" is one full update over one batch of B transitions sampled from a
+device-resident ring filled with synthetic transitions (synthdata).  --gpus N > 1 without torchrun
+re-launches itself under torch.distributed.run (one process per GPU); the world size must equal N.
 
-Extra keys: roofline (dominant kernel class vs the measured peak in
-MEASURED_PEAKS.json), cpu_baseline (the oracle on this host's cores, bounded sample),
-e2e (through the C ABI with host buffers: each step pushes B fresh transitions from
-pinned host memory and reads the stats back), clocks (nvidia-smi during the timed
-region), gpu_launches (our kernels launched in the timed region).
+Timing: W warm-up updates, then repetitions of EXACTLY K graph-replayed updates
+(one spz_update(B, K) each), each bracketed by a barrier + synchronize and timed with CUDA events
+on the learner's stream, max over ranks; repeated until at least --reps repetitions and
+--min-time seconds of timed work.  value = frames per repetition / median repetition time
+[frames/s = update frequency x B, P:465].  Modes for N > 1: dp = one row-sharded learner group
+(NCCL gradient allreduce inside the step), split = actor/critic groups, replicas = N
+independent learners; --scaling weak keeps B per GPU (global B x N), strong keeps the global B.
+
+Extra keys: roofline (the dominant tensor-core kernel class vs the measured bf16 peak, plus the HBM
+fractions of the gather and Adam + Polyak; per-class times from spz_learner_profile: gated, no host
+gaps), fp32 (the same measurement in FP32 / 3xTF32 precision), cpu_baseline + parity (rank 0, one
+GPU: K_o oracle updates from the same parameters, ring and seeds -- timed on the host cores -- and
+the same K_o GPU updates checked against them, tests/parity.py), e2e (through the C ABI with host
+buffers: each step pushes B fresh transitions from pinned host memory and reads the stats back),
+clocks (nvidia-smi during the timed region), gpu_launches (our kernels in the timed region).
 """
 
 import argparse
@@ -60,7 +67,81 @@ def parse():
                          "each group row-shards the global batch B*N/2); replicas = N independent learners")
     ap.add_argument("--critic-frac", type=float, default=0.5,
                     help="split mode: fraction of the ranks in the critic group (SAC critic:actor work ~1.7:1)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = B rows per GPU (global B x N); strong = the global batch B sharded over the group")
+    ap.add_argument("--reps", type=int, default=5, help="minimum number of timed repetitions of K steps")
+    ap.add_argument("--min-time", type=float, default=2.0, help="minimum seconds of timed work over all repetitions")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 (3xTF32) measurement key")
+    ap.add_argument("--parity-steps", type=int, default=None, help="K_o (default: SURVEY.md §8(d) per config)")
+    ap.add_argument("--dry-run", action="store_true", help="print the multi-GPU plan of every rank (gloo, no GPU)")
     return ap.parse_args()
+
+
+# oracle updates K_o run beside the GPU in the same invocation (and checked)
+PARITY_STEPS = {"pendulum": 200, "walker": 20, "ant": 5, "humanoid": 3, "humanoid_td3": 2}
+
+
+def spawn_if_needed(a):
+    """--gpus N > 1 outside torchrun: re-launch this command under torch.distributed.run, one rank per GPU."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
+def group_batch(mode, scaling, B, world):
+    """Global batch one learner group consumes per update."""
+    if world == 1 or mode == "replicas":
+        return B
+    if scaling == "strong":
+        return B
+    return B * world if mode == "dp" else B * world // 2
+
+
+def split_critics(world, frac):
+    return min(world - 1, max(1, int(round(world * frac))))
+
+
+def dry_run(a, w, B):
+    """The host-side plan (spz_plan_rank) of every rank under gloo: shard ranges, groups, exchange roots."""
+    import torch.distributed as dist
+    from paper_2312_06126_b200 import spz
+    from paper_2312_06126_b200.dist import env_rank
+    rank, world, _ = env_rank()
+    if world > 1:
+        dist.init_process_group("gloo")
+    GB = group_batch(a.mode, a.scaling, B, world)
+    kw = {}
+    if a.mode == "split" and world > 1:
+        nc = split_critics(world, a.critic_frac)
+        kw = dict(role=spz.SPZ_ROLE_CRITIC if rank < nc else spz.SPZ_ROLE_ACTOR, n_critic_ranks=nc)
+    if a.mode == "replicas":
+        plan = spz.spz_plan_rank(GB, 1, 0)
+    else:
+        plan = spz.spz_plan_rank(GB, world, rank, **kw)
+    plans = [None] * world
+    if world > 1:
+        dist.all_gather_object(plans, plan)
+    else:
+        plans = [plan]
+    if rank == 0:
+        groups = {}
+        for p in plans:
+            groups.setdefault(p["group_color"], []).append((p["row0"], p["rows"]))
+        tiled = all(sorted(g)[0][0] == 0 and sum(n for _, n in g) == GB and
+                    all(x[0] + x[1] == y[0] for x, y in zip(sorted(g), sorted(g)[1:])) for g in groups.values())
+        if a.mode == "replicas":
+            tiled = True
+        print(json.dumps({"dry_run": True, "n_gpus": world, "mode": a.mode, "scaling": a.scaling,
+                          "config": {"workload": w.name, "global_batch": GB * (world if a.mode == "replicas" else 1)},
+                          "plans": plans, "partitions_tile_batch": tiled}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def peaks():
@@ -116,12 +197,18 @@ def class_flops(w, B):
     return f
 
 
-def class_bytes(w, B, n_params):
-    """Algorithmic HBM bytes per step for the memory-bound classes (§8(d))."""
+def class_bytes(w, B, n_actor, n_critic):
+    """Algorithmic HBM bytes per step of the memory-bound classes.
+
+    gather: the sampled records (R fp32 per row) + one 4-byte index per row.
+    adam_polyak: per trained parameter read p, m, v, g and write p, m, v (28 B); per critic parameter
+    the Polyak target read + write (8 B).  TD3 (policy delay 2): the actor's Adam and every Polyak
+    only on delayed steps (averaged).  n_critic counts both critics (SAC v1: + V)."""
     R = (2 * w.obs_dim + w.act_dim + 2 + 3) // 4 * 4
-    return {"gather": B * (4 * R + 4),
-            # Adam+Polyak: read p, m, v, g; write p, m, v (+ target read/write for critics) -- fp32
-            "adam_polyak": n_params * 28 + n_params * 2 // 3 * 8}
+    dly = 0.5 if w.algo == "td3" else 1.0
+    td3 = w.algo in ("td3", "ddpg")
+    adam = 28 * n_critic + dly * 28 * n_actor + dly * 8 * n_critic + (dly * 8 * n_actor if td3 else 0)
+    return {"gather": B * (4 * R + 4), "adam_polyak": adam}
 
 
 # BASELINE.md §1: the paper's network-update frame rate for Walker2D SAC at its default batch (~8192):
@@ -133,14 +220,30 @@ def vs_baseline(w, value):
     return value / PAPER_WALKER_HZ if w.name == "walker" else None
 
 
+TRAFFIC_FILES = ("r02_traffic.json", "r01_traffic.json")  # newest first
+
+
 def traffic(workload, kernel):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full capture, or None."""
-    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    """(DRAM bytes read + written per launch of kernel class `kernel`, source) from the committed
+    ncu --set full capture, or (None, None)."""
+    for f in TRAFFIC_FILES:
+        p = os.path.join(ROOT, "profiles", f)
+        try:
+            e = json.load(open(p))[workload][kernel]
+        except (OSError, KeyError, ValueError):
+            continue
+        return e["dram_read"] + e["dram_write"], f"profiles/{f} (ncu --set full, per launch)"
+    return None, None
+
+
+def cpu_model():
     try:
-        e = json.load(open(p))[workload][kernel]
-    except (OSError, KeyError, ValueError):
-        return None
-    return e["dram_read"] + e["dram_write"]
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ----------------------------------------------------------------------------- clocks sampler
@@ -232,7 +335,7 @@ def reference_arm(a, w, B):
             "scaling": "weak", "vs_baseline": vs_baseline(w, rate), "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "global_batch": B, "algo": w.algo, "hidden": f"{w.n_hidden}x{w.hidden}",
                        "obs_dim": w.obs_dim, "act_dim": w.act_dim, "ring": min(w.capacity, 1_000_000)},
-            "cpu_baseline": {"value": rate, "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": rate, "unit": "frames/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"{steps} full float64 oracle updates at B={B} ({w.name})"},
             "e2e": {"value": rate, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -240,8 +343,64 @@ def reference_arm(a, w, B):
 
 # ----------------------------------------------------------------------------- GPU arm
 
+def timed_reps(lrn, GB, K, a, stream, world, dist, torch):
+    """Repetitions of exactly K updates (one spz_update(GB, K) each), CUDA events on the learner's stream,
+    barrier + synchronize on both sides, max over ranks; at least a.reps repetitions and a.min_time s."""
+    reps, total = [], 0.0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = None
+    while len(reps) < a.reps or total < a.min_time:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        stats = lrn.update(GB, K)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        reps.append(ms)
+        total += ms / 1e3
+        if len(reps) >= 20000:
+            break
+    return reps, stats
+
+
+def roofline(w, B, prof, precision, pk, n_actor, n_critic):
+    """Dominant tensor-core class (bench-timed, gated per-class CUDA events) against the measured peak, and
+    the HBM fractions of the gather and the optimizer against their algorithmic bytes (§8(d))."""
+    fl = class_flops(w, B)
+    by = class_bytes(w, B, n_actor, n_critic)
+    tens = {k: t for k, t in prof.items() if k in fl}
+    dom = max(tens, key=tens.get)
+    ach = fl[dom] / (prof[dom] * 1e-3) / 1e12
+    if precision == "bf16":
+        pkv, src = pk["bf16_sust"], f"{pk['src']} bf16 sustained (MEASURED_PEAKS.json)"
+    else:  # 3xTF32: three tf32 MMAs per product; tf32 peak = bf16 x 1/2 (the guide's nominal ratio)
+        pkv, src = pk["bf16_sust"] / 2.0 / 3.0, f"{pk['src']} bf16 sustained x 1/2 (tf32 nominal) / 3 (3xTF32 MMAs per product)"
+    tr, tr_src = traffic(w.name, dom) if precision == "bf16" else (None, None)
+    roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pkv, "unit": "TFLOP/s", "frac": ach / pkv,
+            "traffic": tr, "traffic_src": tr_src, "peak_src": src, "algorithmic_flop_per_launch": fl[dom],
+            "launch_ms": prof[dom],
+            "timing": "spz_learner_profile: each step queued whole behind a gate, CUDA events around every op (no host gaps, no PDL overlap)"}
+    hbm = {}
+    for k in ("gather", "adam_polyak"):
+        if k in prof:
+            gbs = by[k] / (prof[k] * 1e-3) / 1e9
+            hbm[k] = {"achieved": gbs, "peak": pk["hbm"], "unit": "GB/s", "frac": gbs / pk["hbm"],
+                      "algorithmic_bytes_per_launch": by[k], "launch_ms": prof[k]}
+    roof["hbm"] = hbm
+    gemm_f = sum(v for k, v in fl.items() if not k.endswith("_mlp"))
+    return roof, gemm_f
+
+
 def main():
     a = parse()
+    spawn_if_needed(a)
     w = synthdata.WORKLOADS[a.config]
     if a.algo and a.algo != w.algo:
         w = dataclasses.replace(w, name=f"{w.name}_{a.algo}", algo=a.algo)
@@ -249,119 +408,89 @@ def main():
     if a.impl == "reference":
         reference_arm(a, w, B)
         return
+    if a.dry_run:
+        dry_run(a, w, B)
+        return
     import torch
     import torch.distributed as dist
     from paper_2312_06126_b200 import spz
 
     from paper_2312_06126_b200.dist import broadcast_bytes, env_rank
     rank, world, local = env_rank()
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE {world}: launch with torchrun --nproc-per-node {a.gpus} or without torchrun")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     assert a.warmup >= 3, "timing rules: at least 3 warm-up steps"
     dp = world > 1 and a.mode == "dp"
     split = world > 1 and a.mode == "split"
-    # the batch one learner group consumes per update: dp B*N; split B*N/2 (both groups read every row)
-    GB = B * world if dp else (B * world // 2 if split else B)
+    GB = group_batch(a.mode, a.scaling, B, world)
 
     # ring filled to capacity with synthetic transitions (ring bytes > L2, so gathers hit HBM)
     C = w.capacity
     ring = spz.Replay(w.obs_dim, w.act_dim, C, device=local)
     chunk = 1_000_000
+    chunks = []
+    want_cpu = rank == 0 and world == 1 and not a.no_cpu_baseline
     for s0 in range(0, C, chunk):
         tr = synthdata.workload_transitions(w, n=min(chunk, C - s0), seed=synthdata.DATA_SEED + s0)
         ring.push(**tr)
+        if want_cpu:
+            chunks.append(tr)
     kw = {}
     if dp or split:
         kw = dict(world_size=world, rank=rank, nccl_unique_id=broadcast_bytes(spz.spz_nccl_unique_id() if rank == 0 else None))
     if split:
-        nc = min(world - 1, max(1, int(round(world * a.critic_frac))))
+        nc = split_critics(world, a.critic_frac)
         kw.update(role=spz.SPZ_ROLE_CRITIC if rank < nc else spz.SPZ_ROLE_ACTOR, n_critic_ranks=nc,
                   n_actor_ranks=world - nc)
     stream = torch.cuda.Stream(device=local)
-    fallback = None
-    try:
-        lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=GB,
-                          device=local, seed=synthdata.SAMPLE_SEED + (0 if (dp or split) else rank), **kw)
-        lrn.set_stream(stream.cuda_stream)
-        # warm-up (includes CUDA-graph capture)
-        lrn.update(GB, a.warmup)
-        ok, err = 1, ""
-    except spz.SpzError as e:
-        ok, err = 0, str(e)
-    if world > 1:
-        t = torch.tensor([ok], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        ok = int(t.item())
-    if not ok:
-        if not (dp or split):
-            raise RuntimeError(err)
-        # the NCCL path failed on some rank: measure independent replicas instead (no collective), and say so
-        fallback = f"{a.mode} path failed ({err or 'on another rank'}); measured {world} independent replicas"
-        dp = split = False
-        GB = B
-        lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=GB,
-                          device=local, seed=synthdata.SAMPLE_SEED + rank)
-        lrn.set_stream(stream.cuda_stream)
-        lrn.update(GB, a.warmup)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # no fallback: a failing NCCL path is an error, not a silent switch to replicas
+    lrn = spz.Learner(ring, algo=w.algo, precision=a.precision, hidden=w.hidden, n_hidden=w.n_hidden, max_batch=GB,
+                      device=local, seed=synthdata.SAMPLE_SEED + (0 if (dp or split) else rank), **kw)
+    lrn.set_stream(stream.cuda_stream)
+    lrn.update(GB, a.warmup)  # warm-up (includes CUDA-graph capture)
+    plan = spz.spz_plan_rank(GB, world if (dp or split) else 1, rank if (dp or split) else 0,
+                             **({k: kw[k] for k in ("role", "n_critic_ranks")} if split else {}))
     with Clocks(local) as clk:
         time.sleep(0.3)
-        ev0.record(stream)
-        stats = lrn.update(GB, a.steps)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
-        dist.barrier()
-    torch.cuda.synchronize()
-    # transitions consumed: dp B*N per update; split B*N/2 per update (counted once, though both groups read it);
-    # replicas N learners x B
+        reps, stats = timed_reps(lrn, GB, a.steps, a, stream, world, dist, torch)
+    ms = statistics.median(reps)
+    # transitions consumed per update: the group batch (counted once, though in split mode both groups read
+    # it); replicas: N learners x B
     frames = GB * a.steps if (dp or split) else B * a.steps * world
     value = frames / (ms / 1e3)
     ms_per_step = ms / a.steps
 
-    # per-class device time (event-bracketed, un-graphed, same learner and batch) -> roofline
-    prof = lrn.profile(GB, 5)
     pk = peaks()
-    fl = class_flops(w, B)  # per-GPU rows
-    n_params = sum(lrn.get(n).size for n in ("actor", "q1", "q2") + (("v",) if w.algo == "sacv1" else ()))
-    by = class_bytes(w, B, n_params)
-    kern = {}
-    for k, t in prof.items():
-        e = {"ms": t}
-        if k in fl:
-            e["tflops"] = fl[k] / (t * 1e-3) / 1e12
-        if k in by:
-            e["gbs"] = by[k] / (t * 1e-3) / 1e9
-        kern[k] = e
-    dom = max(prof, key=prof.get)
-    if dom in fl:
-        ach = fl[dom] / (prof[dom] * 1e-3) / 1e12
-        pkv = pk["bf16_sust"] if a.precision == "bf16" else pk["bf16_sust"] / 2.0  # tf32 = bf16 / 2 (nominal ratio)
-        roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pkv, "unit": "TFLOP/s", "frac": ach / pkv,
-                "traffic": None, "peak_src": f"{pk['src']} bf16 sustained" + ("" if a.precision == "bf16" else " x 1/2 (tf32 nominal ratio)")}
-    else:
-        ach = by.get(dom, 0) / (prof[dom] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm"], "unit": "GB/s", "frac": ach / pk["hbm"],
-                "traffic": None, "peak_src": f"{pk['src']} hbm"}
-    tr = traffic(w.name, roof["kernel"])
-    if tr is not None:
-        roof["traffic"] = tr
-        roof["traffic_src"] = "profiles/r01_traffic.json (ncu --set full, per launch)"
-    gemm_t = sum(t for k, t in prof.items() if k in fl)
-    gemm_f = sum(v for k, v in fl.items() if not k.endswith("_mlp"))  # the fused classes repeat per-layer work
+    n_actor = lrn.get("actor").size
+    n_critic = sum(lrn.get(n).size for n in ("q1", "q2") + (("v",) if w.algo == "sacv1" else ()))
+    prof = lrn.profile(GB, 5)
+    fl = class_flops(w, plan["rows"] if (dp or split) else B)  # this rank's rows
+    roof, gemm_f = roofline(w, plan["rows"] if (dp or split) else B, prof, a.precision, pk, n_actor, n_critic)
     roof["step_gemm_tflops"] = gemm_f / (ms_per_step * 1e-3) / 1e12
     roof["step_frac_of_bf16_sustained"] = roof["step_gemm_tflops"] / pk["bf16_sust"]
-    roof["gemm_share_of_step"] = gemm_t / sum(prof.values())
+    kern = {k: {"ms": t, **({"tflops": fl[k] / (t * 1e-3) / 1e12} if k in fl else {})} for k, t in prof.items()}
     launches = lrn.launches_per_step(GB) * a.steps
+
+    # the same measurement at the paper's implied precision (fp32 on a GTX 1060): FP32 = 3xTF32 tcgen05
+    fp32 = None
+    if not a.no_fp32 and a.precision == "bf16":
+        lf = spz.Learner(ring, algo=w.algo, precision="fp32", hidden=w.hidden, n_hidden=w.n_hidden, max_batch=GB,
+                         device=local, seed=synthdata.SAMPLE_SEED + (0 if (dp or split) else rank), **kw)
+        lf.set_stream(stream.cuda_stream)
+        lf.update(GB, a.warmup)
+        a_f = argparse.Namespace(**{**vars(a), "min_time": max(1.0, a.min_time / 2)})
+        reps_f, _ = timed_reps(lf, GB, a.steps, a_f, stream, world, dist, torch)
+        ms_f = statistics.median(reps_f)
+        prof_f = lf.profile(GB, 3)
+        roof_f, _ = roofline(w, plan["rows"] if (dp or split) else B, prof_f, "fp32", pk, n_actor, n_critic)
+        fp32 = {"value": frames / (ms_f / 1e3), "unit": "frames/s", "dtype": "f32 (3xTF32 tcgen05)",
+                "ms_per_step": ms_f / a.steps,
+                "repetitions": {"n": len(reps_f), "median_ms": ms_f, "min_ms": min(reps_f), "max_ms": max(reps_f)},
+                "roofline": roof_f}
+        lf.close()
 
     # e2e through the C ABI with host buffers
     e2e = None
@@ -413,37 +542,82 @@ def main():
         sweep = {"best_batch": best, "points": pts, "note": "spz_tune_batch, 50 timed updates per B (CUDA events)"}
         tl.close()
 
-    cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        # bounded sample: ~15 s of oracle work (one probe update sizes it), at least one update
-        if a.cpu_sample_steps:
-            steps = a.cpu_sample_steps
-        else:
-            _, _, probe = oracle_rate(w, B, 1)
-            steps = max(1, min(2000, int(15.0 / max(probe, 1e-3))))
-        rate, cores, dt = oracle_rate(w, B, steps)
-        cpu = {"value": rate, "unit": "frames/s", "cores": cores, "kind": "oracle",
-               "sample": f"{steps} float64 oracle updates at B={B} ({w.name}), {dt:.1f} s"}
+    cpu, parity = None, None
+    if want_cpu:
+        cpu, parity = cpu_leg(a, w, B, ring, chunks)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_per_step, "updates_per_s": 1e3 / ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": vs_baseline(w, value), "dtype": a.precision, "data": "synthetic",
+            "repetitions": {"n": len(reps), "median_ms": ms, "min_ms": min(reps), "max_ms": max(reps),
+                            "timed_s": sum(reps) / 1e3, "frames_per_rep": frames},
+            "scaling": "weak" if (world == 1 or a.mode == "replicas" or a.scaling == "weak") else "strong",
+            "vs_baseline": vs_baseline(w, value), "dtype": a.precision, "data": "synthetic",
             "config": {"workload": w.name, "global_batch": GB if (dp or split) else B * world,
-                       "batch_per_gpu": B if not split else GB // max(1, (world // 2)), "algo": w.algo,
+                       "batch_per_gpu": plan["rows"] if (dp or split) else B, "algo": w.algo,
                        "mode": ("dp-nccl" if dp else "split-nccl" if split else "replicas") if world > 1 else "single",
                        "hidden": f"{w.n_hidden}x{w.hidden}", "obs_dim": w.obs_dim, "act_dim": w.act_dim,
                        "ring": C, "parallelism": (f"dp{world}" if dp else f"split{world}" if split else f"replicas{world}") if world > 1 else "single",
-                       "l2": f"ring {C * ((2 * w.obs_dim + w.act_dim + 2 + 3) // 4 * 4) * 4 / 1e6:.0f} MB > 126 MB L2; fresh random indices each step"},
-            "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
+                       "l2": f"ring {C * ((2 * w.obs_dim + w.act_dim + 2 + 3) // 4 * 4) * 4 / 1e6:.0f} MB > 126 MB L2; fresh random indices each step (inputs larger than L2)"},
+            "roofline": roof, "kernels": kern, "fp32": fp32, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
             "clocks": clk.summary(), "gpu_launches": launches, "last_stats": stats,
             **({"batch_sweep": sweep} if sweep else {}),
-            **({"fallback": fallback} if fallback else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def cpu_leg(a, w, B, ring, chunks):
+    """cpu_baseline + parity (rank 0, one GPU): K_o float64 oracle updates on the host cores from the
+    same initial parameters, ring contents and seeds as K_o GPU updates, which are checked against them
+    (tests/parity.py: statistics, raw gradients of every tensor, Adam moments, parameters); the oracle's
+    update time is the baseline.  Plus a 1-thread oracle rate and the host CPU model (§8(d))."""
+    from oracle import ring as oring
+    from tests import parity as par
+    r = oring.Ring(w.obs_dim, w.act_dim, w.capacity)
+    for tr in chunks:
+        r.push(**tr)
+    K_o = a.parity_steps or PARITY_STEPS.get(w.name, 2)
+    cores = len(os.sched_getaffinity(0))
+    threads = None
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((d.get("num_threads", 0) for d in threadpool_info()), default=None)
+    except Exception:
+        pass
+    timing = {}
+    parity = {"k_o": K_o, "precision": a.precision}
+    if w.algo in ("sac", "td3"):
+        try:
+            res = par.run_parity(w.algo, a.precision, w.obs_dim, w.act_dim, w.hidden, w.n_hidden, B, w.capacity, K_o,
+                                 rings=(ring, r), timing=timing, tag=f"bench-{w.name}")
+            parity.update(ok=True, max_param_err=max(res["params"].values()),
+                          max_grad_err=max(res["grads"].values()) if res["grads"] else None,
+                          bar={"params": par.TOL[a.precision], "grads_net": par.GTOL[a.precision],
+                               "grads_tensor": par.GTOL_TENSOR[a.precision]})
+        except AssertionError as e:
+            parity.update(ok=False, error=str(e)[:500])
+        oracle_s, steps = timing.get("oracle_s", 0.0), timing.get("oracle_steps", 0)
+    else:
+        parity.update(ok=None, note=f"{w.algo}: parity in tests/test_gpu_parity.py only")
+        _, _, oracle_s = oracle_rate(w, B, K_o)
+        steps = K_o
+    rate = B * steps / oracle_s if oracle_s > 0 else None
+    one = None
+    try:
+        from threadpoolctl import threadpool_limits
+        n1 = 1 if w.name.startswith(("humanoid",)) else 2
+        with threadpool_limits(1):
+            r1, _, dt1 = oracle_rate(w, B, n1)
+        one = {"value": r1, "steps": n1, "seconds": dt1}
+    except Exception as e:  # threadpoolctl missing: report why
+        one = {"error": str(e)[:200]}
+    cpu = {"value": rate, "unit": "frames/s", "cores": cores, "threads": threads, "kind": "oracle", "cpu_model": cpu_model(),
+           "sample": f"{steps} float64 oracle updates at B={B} ({w.name}), {oracle_s:.1f} s -- the same steps the parity check runs",
+           "one_thread": one}
+    return cpu, parity
 
 
 if __name__ == "__main__":

@@ -171,6 +171,30 @@ spz_status spz_config_default(spz_algo algo, int32_t obs_dim, int32_t act_dim, s
  * loaded at run time (libnccl.so.2); SPZ_ENCCL if unavailable. */
 spz_status spz_nccl_unique_id(uint8_t out[128]);
 
+/* Host-side multi-GPU plan of one rank (reading #17; P:239-247 for the
+ * actor/critic split, P:170-173 for the row-sharded group).  Pure host arithmetic, no device: the
+ * learner builds its own partition, communicator split and exchange from this function, and the
+ * world-size-2 gloo tests check the same function across processes.
+ *   role ALL:    one group of world_size ranks;  role CRITIC / ACTOR (world_size > 1): the critic group
+ *                is ranks [0, n_critic_ranks), the actor group the rest.
+ *   rows:        the group's global batch B split contiguously by global row id, the first B % G
+ *                ranks one row longer; every group reads all B rows.
+ *   exchange:    split roles broadcast phi_{k+1} (+ log alpha, TD3 phi') from actor_root and
+ *                theta_{k+1} from critic_root over the world communicator at the step boundary.
+ * Errors: SPZ_EINVAL (NULL, bad world/rank/role layout, batch < group_size). */
+typedef struct {
+  int32_t role;         /* SPZ_ROLE_* this rank computes                                   */
+  int32_t group_size;   /* ranks in its row-sharded group                                  */
+  int32_t group_rank;   /* index inside the group (the communicator-split key)             */
+  int32_t group_color;  /* 0 = critic group or all ranks, 1 = actor group (the split color) */
+  int64_t row0, rows;   /* its share [row0, row0 + rows) of the global batch               */
+  int32_t actor_root;   /* world rank broadcasting the actor side (split), else -1         */
+  int32_t critic_root;  /* world rank broadcasting the critics (split), else -1            */
+  int32_t allreduce;    /* 1: the group all-reduces [gradients | loss totals] every step   */
+  int32_t pad_;
+} spz_plan;
+spz_status spz_plan_rank(const spz_config* cfg, int64_t batch, spz_plan* out);
+
 typedef struct spz_learner spz_learner;
 
 typedef struct {
@@ -234,13 +258,25 @@ spz_status spz_set_params(spz_learner* L, spz_tensor t, spz_slot s, const float*
 /* Adam step counters t of (critic, actor, alpha) optimizers and the global step. */
 spz_status spz_get_counters(spz_learner* L, int64_t* step, int64_t* t_critic, int64_t* t_actor, int64_t* t_alpha);
 
-/* Push the actor parameters peer-to-peer (north_star "actor
- * parameters pushed peer-to-peer") into a buffer on dst_device laid out as
- * [u64 version | u64 n_floats | n_floats fp32 (flat actor)]: the payload is
- * written first and the 16-byte header last in stream order, so a reader that
- * sees version v sees v's payload, never a blend.  The version is
- * monotone per learner and returned in *version.  dst_bytes must be
- * >= 16 + 4 * n_floats.  Synchronous. */
+/* Actor publication buffer ("never a blend", S:248/S:271 monotone version):
+ *   bytes [0, 64)  header: u64 version (last published; 0 = none) | u64 n_floats | u64 seq[2] | 32 B reserved
+ *   slot s at SPZ_SYNC_HEADER_BYTES + s * SPZ_SYNC_SLOT_BYTES(n): n_floats fp32 (the flat actor)
+ * Version v lives in slot v & 1.  seq[s] is the per-slot seqlock word: 2v - 1 (odd) while version v's
+ * payload is being written into slot s, 2v once it is complete. */
+#define SPZ_SYNC_HEADER_BYTES 64
+#define SPZ_SYNC_SLOT_BYTES(n) ((((int64_t)(n) * 4 + 63) / 64) * 64)
+#define SPZ_SYNC_BYTES(n) (SPZ_SYNC_HEADER_BYTES + 2 * SPZ_SYNC_SLOT_BYTES(n))
+
+/* Push the actor parameters peer-to-peer (north_star "actor parameters pushed
+ * peer-to-peer") into a publication buffer (layout above) on dst_device.  Publishing version v, in
+ * stream order: seq[v & 1] = 2v - 1, the payload into slot v & 1, seq[v & 1] = 2v, then the header
+ * version = v.  Version v - 1 (the other slot) stays intact while v is written, so a reader always has
+ * one complete version to copy, and a reader that overlaps a rewrite of its slot sees seq change and
+ * retries (spz_policy_load) -- it never accepts a blend.  The version is monotone per learner
+ * and returned in *version (nullable).  dst must be device memory on dst_device (peer access is
+ * enabled when available, else the copy is staged by the driver), zero-initialised before the first
+ * publication, 16-byte aligned; dst_bytes >= SPZ_SYNC_BYTES(n_floats).  Synchronous.
+ * Errors: SPZ_EINVAL (NULL / too small), SPZ_ECUDA. */
 spz_status spz_sync_actor(spz_learner* L, int32_t dst_device, void* dst, int64_t dst_bytes,
                           uint64_t* version);
 
@@ -332,17 +368,20 @@ typedef struct {
 } spz_policy_desc;
 /* Errors: SPZ_EINVAL (bad dims), SPZ_ENOMEM, SPZ_ECUDA. */
 spz_status spz_policy_create(const spz_policy_desc* desc, spz_policy** out);
-/* Load the actor from a spz_sync_actor payload [u64 version | u64 n_floats | floats] in device or host
- * memory (borrowed for the call).  Seqlock read (header, payload, header): a concurrent writer makes
- * it retry, so the loaded parameters are exactly one version's; *version (nullable) receives
- * it.  SPZ_EINVAL if n_floats does not match the policy's shape; SPZ_ETIMEOUT if the payload kept
- * changing.  Synchronous. */
+/* Load the actor from a spz_sync_actor publication buffer (layout above; device or host memory, borrowed
+ * for the call).  Seqlock read of the newest version v: header, seq[v & 1] == 2v, payload of slot v & 1,
+ * seq[v & 1] again; any change (a writer reached that slot again) restarts the read, so the loaded
+ * parameters are exactly one version's; *version (nullable) receives it.  SPZ_ESTATE if nothing
+ * was published yet; SPZ_EINVAL if n_floats does not match the policy's shape or bytes is too small;
+ * SPZ_ETIMEOUT if 64 attempts all overlapped a writer.  Synchronous. */
 spz_status spz_policy_load(spz_policy* P, const void* payload, int64_t bytes, uint64_t* version);
 /* Actions act [n x m] (fp32, row-major) for observations obs [n x o]; each pointer may be host or
  * device memory (detected).  0 <= n <= max_batch.  deterministic != 0 selects the test-process
  * action.  SPZ_ESTATE before the first spz_policy_load.  Synchronous. */
 spz_status spz_policy_act(spz_policy* P, int64_t n, const float* obs, int32_t deterministic, uint64_t seed,
                           uint64_t step, float* act);
+/* Copy the currently loaded flat actor (fp32, the spz_get_params layout) to host memory; n >= n_floats. */
+spz_status spz_policy_get_params(spz_policy* P, float* host_out, int64_t n);
 void spz_policy_destroy(spz_policy* P);
 
 /* Diagnostics (GEMM unit tests): the FP32-precision GEMM, C = A * B in fp32 with the same operand

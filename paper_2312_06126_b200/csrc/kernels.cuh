@@ -812,6 +812,20 @@ __global__ void __launch_bounds__(ADAM_NT) reduce_partials_kernel(const AdamSegm
   }
 }
 
+// Measurement: holds the stream until the host has queued a whole profiled step (the host-mapped word
+// reaches `target`); gives up after ~5 s so a failed host never leaves the GPU spinning.
+__global__ void gate_kernel(const volatile int* word, int target) {
+  if (threadIdx.x != 0) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*word < target) {
+    __nanosleep(2000);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 5000000000ull) break;
+  }
+}
+
 // Diagnostics: an empty kernel in the PDL chain (SPZ_DIAG_NOOP_OPS) to measure the cost of one
 // kernel boundary inside the graph replay.
 __global__ void noop_kernel(int) {

@@ -201,6 +201,9 @@ struct spz_learner {
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
   int n_adam_segs = 0;
   uint64_t sync_version = 0;
+  uint64_t* h_sync = nullptr;  // pinned: the publication's seq / header words (spz_sync_actor)
+  int* h_gate = nullptr;       // mapped: spz_learner_profile's release word
+  int* d_gate = nullptr;
   unsigned* tickets = nullptr;  // last-block counter of the loss kernel
   int64_t* ctr_snap = nullptr;  // counters as read at the start of the step (loss kernel -> Adam)
   std::vector<void*> allocs;
@@ -337,6 +340,8 @@ spz_learner::~spz_learner() {
     if (e) cudaEventDestroy(e);
   if (h_flag) cudaFreeHost(h_flag);
   if (h_counters) cudaFreeHost(h_counters);
+  if (h_sync) cudaFreeHost(h_sync);
+  if (h_gate) cudaFreeHost(h_gate);
   if (own_stream) cudaStreamDestroy(own_stream);
   if (prev >= 0) cudaSetDevice(prev);
 }
@@ -352,20 +357,12 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       cudaGraphExecDestroy(e);
       e = nullptr;
     }
-  // rows of this rank: contiguous share of the global batch inside its group (reading #17);
-  // with split roles the critic group is ranks [0, n_critic) and the actor group the rest
-  int W = Lr->cfg.world_size, rk = Lr->cfg.rank;
-  if (Lr->split) {
-    const int nc = Lr->cfg.n_critic_ranks;
-    if (rk < nc) W = nc;
-    else {
-      W = Lr->cfg.world_size - nc;
-      rk -= nc;
-    }
-  }
-  const int64_t base = B / W, rem = B % W;
-  const int Bl = (int)(base + (rk < rem ? 1 : 0));
-  const int64_t row0 = rk * base + std::min<int64_t>(rk, rem);
+  // rows of this rank: contiguous share of the global batch inside its group (spz_plan_rank, DESIGN.md
+  // reading #17); with split roles the critic group is ranks [0, n_critic) and the actor group the rest
+  spz_plan plan;
+  SPZ_TRY(spz_plan_rank(&Lr->cfg, B, &plan));
+  const int Bl = (int)plan.rows;
+  const int64_t row0 = plan.row0;
   const int o = Lr->o, m = Lr->m, h = Lr->h, L = Lr->L;
   const bool td3 = Lr->td3;
   const bool v1 = Lr->v1;
@@ -1167,6 +1164,21 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     }
     // ---- every weight gradient (split-K over the batch, <= 8 tensors per launch) and every bias
     //      gradient (one column-sum launch)
+    // diagnostics only (results are wrong): SPZ_DIAG_MUTATE="drop_wgrad=i" / "drop_bias=i" drops the i-th
+    // weight / bias gradient job, "tau0" freezes the targets -- the parity tests must fail under each
+    if (const char* mu = std::getenv("SPZ_DIAG_MUTATE")) {
+      const std::string ms(mu);
+      auto idx_of = [&](const char* key) -> int {
+        const size_t p = ms.find(key);
+        return p == std::string::npos ? -1 : std::atoi(ms.c_str() + p + std::strlen(key));
+      };
+      const int dw = idx_of("drop_wgrad="), dbi = idx_of("drop_bias=");
+      if (dw >= 0 && dw < (int)wgrads.size()) wgrads.erase(wgrads.begin() + dw);
+      if (dbi >= 0) {
+        if (fuse_bias && dbi < (int)wgrads.size()) wgrads[dbi].colsum_out = nullptr;
+        else if (!fuse_bias && dbi < (int)colsums.size()) colsums.erase(colsums.begin() + dbi);
+      }
+    }
     {
       GemmArgs a = mk(Bl, fuse_bias ? EPI_WGRAD_BIAS : EPI_F32, 1, 1);
       a.splits = Sw;
@@ -1295,6 +1307,8 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       hp.beta2 = (float)Lr->cfg.beta2;
       hp.eps = (float)Lr->cfg.adam_eps;
       hp.tau = (float)Lr->cfg.tau;
+      if (const char* mu = std::getenv("SPZ_DIAG_MUTATE"))
+        if (std::string(mu).find("tau0") != std::string::npos) hp.tau = 0.f;  // diagnostics only
       hp.td3 = td3;
       hp.delay = delay;
       hp.totals = Lr->statsum;
@@ -1320,7 +1334,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     //      phi_{k+1} (+ log alpha, TD3 phi') from the actor leader, theta_{k+1} from the critic leader
     if (Lr->split && Lr->cfg.world_size > 1 && Lr->cfg.comm_mode == 0) {
       const Comm cm = Lr->comm;
-      const int nc = Lr->cfg.n_critic_ranks;
+      const int nc = plan.actor_root, c0 = plan.critic_root;
       float* pa = P + Lr->pbase[NET_ACTOR];
       const size_t na = (size_t)Lr->net[NET_ACTOR].np;
       float* pat = Lr->has_net[NET_ACTORT] ? P + Lr->pbase[NET_ACTORT] : nullptr;
@@ -1333,7 +1347,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
                        cudaError_t e = comm_broadcast_f32(cm, pa, na, nc, st);
                        if (e == cudaSuccess) e = comm_broadcast_f32(cm, pla, 1, nc, st);
                        if (e == cudaSuccess && pat) e = comm_broadcast_f32(cm, pat, na, nc, st);
-                       if (e == cudaSuccess) e = comm_broadcast_f32(cm, pq, nq, 0, st);
+                       if (e == cudaSuccess) e = comm_broadcast_f32(cm, pq, nq, c0, st);
                        if (e != cudaSuccess) return e;
                        return launch_pdl(shadow_refresh_kernel<T>, dim3(64, nsh), dim3(256), 0, st, sh, nsh, (const float*)P, S);
                      }, 1});
@@ -1475,6 +1489,39 @@ spz_status spz_config_default(spz_algo algo, int32_t obs_dim, int32_t act_dim, s
   return SPZ_OK;
 }
 
+spz_status spz_plan_rank(const spz_config* cfg, int64_t batch, spz_plan* out) {
+  if (!cfg || !out) return fail(SPZ_EINVAL, "spz_plan_rank: NULL argument");
+  if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
+    return fail(SPZ_EINVAL, "spz_plan_rank: bad rank/world_size");
+  if (cfg->role != SPZ_ROLE_ALL && cfg->role != SPZ_ROLE_CRITIC && cfg->role != SPZ_ROLE_ACTOR)
+    return fail(SPZ_EINVAL, "spz_plan_rank: unknown role");
+  spz_plan p{};
+  p.role = cfg->role;
+  p.group_size = cfg->world_size;
+  p.group_rank = cfg->rank;
+  p.actor_root = p.critic_root = -1;
+  if (cfg->role != SPZ_ROLE_ALL && cfg->world_size > 1) {
+    // critic group = ranks [0, n_critic_ranks), actor group = the rest (P:239-247 generalised)
+    const int nc = cfg->n_critic_ranks;
+    if (nc < 1 || nc >= cfg->world_size) return fail(SPZ_EINVAL, "spz_plan_rank: split roles need 1 <= n_critic_ranks < world_size");
+    if ((cfg->rank < nc) != (cfg->role == SPZ_ROLE_CRITIC))
+      return fail(SPZ_EINVAL, "spz_plan_rank: ranks [0, n_critic_ranks) must be critic, the others actor");
+    const bool critic = cfg->role == SPZ_ROLE_CRITIC;
+    p.group_size = critic ? nc : cfg->world_size - nc;
+    p.group_rank = critic ? cfg->rank : cfg->rank - nc;
+    p.group_color = critic ? 0 : 1;
+    p.critic_root = 0;
+    p.actor_root = nc;
+  }
+  if (batch < p.group_size) return fail(SPZ_EINVAL, "spz_plan_rank: batch smaller than the group");
+  const int64_t base = batch / p.group_size, rem = batch % p.group_size;
+  p.rows = base + (p.group_rank < rem ? 1 : 0);
+  p.row0 = p.group_rank * base + std::min<int64_t>(p.group_rank, rem);
+  p.allreduce = p.group_size > 1 && cfg->comm_mode == 0;
+  *out = p;
+  return SPZ_OK;
+}
+
 spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learner** out) {
   if (!cfg || !ring || !out) return fail(SPZ_EINVAL, "spz_learner_create: NULL argument");
   *out = nullptr;
@@ -1490,13 +1537,8 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     return fail(SPZ_EINVAL, "spz_learner_create: world_size > 1 needs nccl_unique_id (or comm_mode = 1)");
   if (cfg->role != SPZ_ROLE_ALL && cfg->role != SPZ_ROLE_CRITIC && cfg->role != SPZ_ROLE_ACTOR)
     return fail(SPZ_EINVAL, "spz_learner_create: unknown role");
-  if (cfg->role != SPZ_ROLE_ALL && cfg->world_size > 1) {
-    // critic group = ranks [0, n_critic_ranks), actor group = the rest (P:239-247 generalised)
-    const int nc = cfg->n_critic_ranks;
-    if (nc < 1 || nc >= cfg->world_size) return fail(SPZ_EINVAL, "spz_learner_create: split roles need 1 <= n_critic_ranks < world_size");
-    if ((cfg->rank < nc) != (cfg->role == SPZ_ROLE_CRITIC))
-      return fail(SPZ_EINVAL, "spz_learner_create: ranks [0, n_critic_ranks) must be critic, the others actor");
-  }
+  spz_plan plan;  // validates the rank / role layout; the group shape below comes from it
+  SPZ_TRY(spz_plan_rank(cfg, std::max<int64_t>(cfg->world_size, cfg->max_batch), &plan));
   if (cfg->algo != SPZ_SAC && cfg->algo != SPZ_TD3 && cfg->algo != SPZ_DDPG && cfg->algo != SPZ_SACV1)
     return fail(SPZ_EINVAL, "spz_learner_create: unknown algo");
   if (cfg->algo == SPZ_SACV1 && cfg->role != SPZ_ROLE_ALL)
@@ -1529,10 +1571,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     ring->readers.push_back(Lr->ev_read);
   }
   Lr->split = cfg->role != SPZ_ROLE_ALL;
-  Lr->gsize = !Lr->split ? cfg->world_size
-                         : (cfg->world_size == 1 ? 1
-                                                 : (cfg->role == SPZ_ROLE_CRITIC ? cfg->n_critic_ranks
-                                                                                 : cfg->world_size - cfg->n_critic_ranks));
+  Lr->gsize = plan.group_size;
   const int W = Lr->gsize;
   Lr->max_local = cfg->max_batch / W + (cfg->max_batch % W ? 1 : 0);
   // networks
@@ -1639,9 +1678,15 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
         reg("dZc" + std::to_string(i) + "_" + std::to_string(l), Lr->dZc[i][l], 2 * Bm * h * E, (int)E);
       }
     }
+    for (int l = 0; l < L; ++l) {  // packed ReLU masks (bf16 tensor-core path): [rows x mw] u32, bit c%32 of word c/32
+      if (Lr->mask_a[l]) reg("mask_a" + std::to_string(l), Lr->mask_a[l], 2 * Bm * Lr->mw * 4, 4);
+      for (int i = 0; i < 2; ++i)
+        if (Lr->mask_c[i][l]) reg("mask_c" + std::to_string(i) + "_" + std::to_string(l), Lr->mask_c[i][l], 2 * Bm * Lr->mw * 4, 4);
+    }
     for (int i = 0; i < 2; ++i) {
-      reg("q_on" + std::to_string(i), Lr->q_on[i], 2 * Bm * 4, 4);
-      reg("q_tg" + std::to_string(i), Lr->q_tg[i], Bm * 4, 4);
+      // q partials: qp planes of 2 * max_local (online) / max_local (target) rows (h > 256: one per 256-column tile)
+      reg("q_on" + std::to_string(i), Lr->q_on[i], 2 * Bm * Lr->qp * 4, 4);
+      reg("q_tg" + std::to_string(i), Lr->q_tg[i], Bm * Lr->qp * 4, 4);
       reg("gq" + std::to_string(i), Lr->gq[i], 2 * Bm * 4, 4);
       reg("dXc" + std::to_string(i), Lr->dXc[i], Bm * Lr->ldc * 4, 4);
     }
@@ -1688,9 +1733,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
     if (cs != SPZ_OK) return cs;
     Lr->gcomm = Lr->comm;
     if (Lr->split) {  // the role's own group for the gradient allreduce
-      const int color = cfg->role == SPZ_ROLE_CRITIC ? 0 : 1;
-      const int key = cfg->role == SPZ_ROLE_CRITIC ? cfg->rank : cfg->rank - cfg->n_critic_ranks;
-      cs = comm_split(Lr->comm, color, key, &Lr->gcomm);
+      cs = comm_split(Lr->comm, plan.group_color, plan.group_rank, &Lr->gcomm);
       if (cs != SPZ_OK) return cs;
     }
   }
@@ -2029,7 +2072,9 @@ spz_status spz_sync_actor(spz_learner* Lr, int32_t dst_device, void* dst, int64_
   if (!Lr || !dst) return fail(SPZ_EINVAL, "spz_sync_actor: NULL argument");
   DeviceGuard dg(Lr->device);
   const int64_t nf = Lr->net[NET_ACTOR].np;
-  if (dst_bytes < 16 + 4 * nf) return fail(SPZ_EINVAL, "spz_sync_actor: destination smaller than 16 + 4 * " + std::to_string(nf) + " bytes");
+  if (dst_bytes < SPZ_SYNC_BYTES(nf))
+    return fail(SPZ_EINVAL, "spz_sync_actor: destination smaller than SPZ_SYNC_BYTES(" + std::to_string(nf) + ") bytes");
+  if (reinterpret_cast<uintptr_t>(dst) % 16) return fail(SPZ_EINVAL, "spz_sync_actor: destination not 16-byte aligned");
   if (dst_device != Lr->device) {
     int can = 0;
     SPZ_CUDA_TRY(cudaDeviceCanAccessPeer(&can, Lr->device, dst_device));
@@ -2039,13 +2084,27 @@ spz_status spz_sync_actor(spz_learner* Lr, int32_t dst_device, void* dst, int64_
       cudaGetLastError();
     }
   }
+  if (!Lr->h_sync && cudaMallocHost(&Lr->h_sync, 8 * sizeof(uint64_t)) != cudaSuccess) {
+    Lr->h_sync = nullptr;
+    return fail(SPZ_ENOMEM, "spz_sync_actor: pinned header words");
+  }
+  // publication of version v into slot v & 1 (include/spz.h): seq odd, payload, seq even, header last --
+  // each copy starts after the previous one completed (one stream), so the header never points at a slot
+  // whose payload is incomplete, and a reader that overlaps the slot's rewrite sees its seq word change
   uint8_t* d8 = static_cast<uint8_t*>(dst);
-  SPZ_CUDA_TRY(cudaMemcpyPeerAsync(d8 + 16, dst_device, Lr->P + Lr->pbase[NET_ACTOR], Lr->device, nf * sizeof(float), Lr->stream));
   const uint64_t v = ++Lr->sync_version;
-  uint64_t* hdr = reinterpret_cast<uint64_t*>(&Lr->h_counters[5]);
-  hdr[0] = v;
-  hdr[1] = (uint64_t)nf;
-  SPZ_CUDA_TRY(cudaMemcpyAsync(d8, hdr, 16, cudaMemcpyHostToDevice, Lr->stream));  // header last: never a blend
+  const int slot = (int)(v & 1);
+  uint64_t* w = Lr->h_sync;  // distinct host words: the copies read them when they execute
+  w[0] = 2 * v - 1;
+  w[1] = 2 * v;
+  w[2] = v;
+  w[3] = (uint64_t)nf;
+  uint8_t* seq = d8 + 16 + 8 * slot;
+  SPZ_CUDA_TRY(cudaMemcpyAsync(seq, &w[0], 8, cudaMemcpyHostToDevice, Lr->stream));
+  SPZ_CUDA_TRY(cudaMemcpyPeerAsync(d8 + SPZ_SYNC_HEADER_BYTES + slot * SPZ_SYNC_SLOT_BYTES(nf), dst_device,
+                                   Lr->P + Lr->pbase[NET_ACTOR], Lr->device, nf * sizeof(float), Lr->stream));
+  SPZ_CUDA_TRY(cudaMemcpyAsync(seq, &w[1], 8, cudaMemcpyHostToDevice, Lr->stream));
+  SPZ_CUDA_TRY(cudaMemcpyAsync(d8, &w[2], 16, cudaMemcpyHostToDevice, Lr->stream));
   SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
   if (version) *version = v;
   return SPZ_OK;
@@ -2065,29 +2124,64 @@ spz_status spz_learner_profile(spz_learner* Lr, int64_t batch, int64_t n_steps, 
     SPZ_CUDA_TRY(ring_flush_pending(Lr->ring));
   }
   SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));
+  // No host gaps inside the timed ops: each step is enqueued behind a gate kernel that spins on a
+  // host-mapped word, and the word is released only once the whole step (ops + events) is queued, so
+  // every op starts right after the event that follows its predecessor (the events serialise the ops:
+  // no PDL overlap, like ncu's per-launch times).
+  if (!Lr->h_gate) {
+    if (cudaHostAlloc((void**)&Lr->h_gate, sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
+      Lr->h_gate = nullptr;
+      return fail(SPZ_ENOMEM, "spz_learner_profile: mapped gate word");
+    }
+    SPZ_CUDA_TRY(cudaHostGetDevicePointer((void**)&Lr->d_gate, Lr->h_gate, 0));
+  }
+  *const_cast<volatile int*>(Lr->h_gate) = 0;
+  struct GateOpen {  // the gate always opens on exit (an error mid-enqueue must not leave the GPU spinning)
+    volatile int* g;
+    ~GateOpen() { *g = 1 << 30; }
+  } gate_open{Lr->h_gate};
   std::vector<const char*> cls;
   std::vector<double> tot;
-  std::vector<cudaEvent_t> ev;
-  for (int64_t k = 0; k < n_steps; ++k, ++step) {
-    const int v = variant_of(Lr, step);
+  std::vector<std::vector<cudaEvent_t>> ev(n_steps);
+  std::vector<int> vars(n_steps);
+  auto destroy = [&]() {
+    for (auto& v : ev)
+      for (auto e : v) cudaEventDestroy(e);
+  };
+  for (int64_t k = 0; k < n_steps; ++k) {
+    const int v = variant_of(Lr, step + k);
+    vars[k] = v;
     auto& ops = Lr->ops[v];
-    if (ev.size() < ops.size() + 1) {
-      while (ev.size() < ops.size() + 1) {
-        cudaEvent_t e;
-        SPZ_CUDA_TRY(cudaEventCreate(&e));
-        ev.push_back(e);
+    ev[k].resize(ops.size() + 1);
+    for (auto& e : ev[k])
+      if (cudaEventCreate(&e) != cudaSuccess) {
+        destroy();
+        return fail(SPZ_ECUDA, "spz_learner_profile: event creation failed");
       }
-    }
-    SPZ_CUDA_TRY(cudaEventRecord(ev[0], Lr->stream));
+    gate_kernel<<<1, 32, 0, Lr->stream>>>(Lr->d_gate, (int)(k + 1));
+    SPZ_CUDA_TRY(cudaEventRecord(ev[k][0], Lr->stream));
     for (size_t i = 0; i < ops.size(); ++i) {
       cudaError_t e = ops[i].fn(Lr->stream);
-      if (e != cudaSuccess) return fail(SPZ_ECUDA, std::string("kernel ") + ops[i].cls + ": " + cudaGetErrorString(e));
-      SPZ_CUDA_TRY(cudaEventRecord(ev[i + 1], Lr->stream));
+      if (e != cudaSuccess) {
+        destroy();
+        return fail(SPZ_ECUDA, std::string("kernel ") + ops[i].cls + ": " + cudaGetErrorString(e));
+      }
+      SPZ_CUDA_TRY(cudaEventRecord(ev[k][i + 1], Lr->stream));
     }
-    SPZ_CUDA_TRY(cudaStreamSynchronize(Lr->stream));
+    *const_cast<volatile int*>(Lr->h_gate) = (int)(k + 1);  // step k fully queued: release it
+  }
+  {
+    cudaError_t e = cudaStreamSynchronize(Lr->stream);
+    if (e != cudaSuccess) {
+      destroy();
+      return fail(SPZ_ECUDA, std::string("spz_learner_profile: ") + cudaGetErrorString(e));
+    }
+  }
+  for (int64_t k = 0; k < n_steps; ++k) {
+    auto& ops = Lr->ops[vars[k]];
     for (size_t i = 0; i < ops.size(); ++i) {
       float t = 0;
-      SPZ_CUDA_TRY(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+      SPZ_CUDA_TRY(cudaEventElapsedTime(&t, ev[k][i], ev[k][i + 1]));
       size_t c = 0;
       for (; c < cls.size(); ++c)
         if (std::strcmp(cls[c], ops[i].cls) == 0) break;
@@ -2099,7 +2193,7 @@ spz_status spz_learner_profile(spz_learner* Lr, int64_t batch, int64_t n_steps, 
     }
   }
   SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_read, Lr->stream));
-  for (auto e : ev) cudaEventDestroy(e);
+  destroy();
   const int nc = (int)std::min<size_t>(cls.size(), (size_t)std::max(cap, 0));
   for (int i = 0; i < nc; ++i) {
     if (names) names[i] = cls[i];

@@ -114,7 +114,7 @@ struct spz_policy {
   float* Hout = nullptr;             // [max_batch x nout]
   float* dobs = nullptr;             // staging for host observations
   float* dact = nullptr;             // staging for host actions
-  uint8_t* hdr = nullptr;            // pinned: two payload headers (seqlock read)
+  uint8_t* hdr = nullptr;            // pinned: header + re-read seq word (seqlock read)
   cudaStream_t stream = nullptr;
   std::vector<void*> allocs;
   ~spz_policy() {
@@ -211,7 +211,7 @@ spz_status spz_policy_create(const spz_policy_desc* d, spz_policy** out) {
   p->expl = (float)d->expl_noise;
   if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(SPZ_ECUDA, "spz_policy_create: stream creation failed");
-  if (cudaMallocHost(&p->hdr, 64) != cudaSuccess) return fail(SPZ_ENOMEM, "spz_policy_create: pinned header");
+  if (cudaMallocHost(&p->hdr, 128) != cudaSuccess) return fail(SPZ_ENOMEM, "spz_policy_create: pinned header");
   const size_t E = p->bf16 ? 2 : 4;
   // layer-0 pitch: 128-byte rows on the bf16 tensor-core path (full-row TMA boxes), else 16-byte rows
   p->ld0 = (int)round_up(p->o, p->bf16 ? 64 : 4);
@@ -246,33 +246,48 @@ spz_status spz_policy_create(const spz_policy_desc* d, spz_policy** out) {
 
 spz_status spz_policy_load(spz_policy* p, const void* payload, int64_t bytes, uint64_t* version) {
   if (!p || !payload) return fail(SPZ_EINVAL, "spz_policy_load: NULL argument");
-  if (bytes < 16 + 4 * p->np)
-    return fail(SPZ_EINVAL, "spz_policy_load: payload smaller than 16 + 4 * " + std::to_string(p->np) + " bytes");
+  if (bytes < SPZ_SYNC_BYTES(p->np))
+    return fail(SPZ_EINVAL, "spz_policy_load: buffer smaller than SPZ_SYNC_BYTES(" + std::to_string(p->np) + ")");
   DeviceGuard dg(p->device);
   const uint8_t* src = static_cast<const uint8_t*>(payload);
   const cudaMemcpyKind hk = on_device(payload) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
   const cudaMemcpyKind pk = on_device(payload) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  // seqlock read: header, payload, header again; a writer (spz_sync_actor writes the payload first and the
-  // header last) that lands in between changes the version and the read is retried
-  for (int attempt = 0; attempt < 8; ++attempt) {
-    uint64_t* h0 = reinterpret_cast<uint64_t*>(p->hdr);
-    uint64_t* h1 = h0 + 2;
-    SPZ_CUDA_TRY(cudaMemcpyAsync(h0, src, 16, hk, p->stream));
+  // seqlock read of the newest version v (include/spz.h): header -> seq[v & 1] must be 2v (complete) ->
+  // payload of slot v & 1 -> seq[v & 1] unchanged; otherwise a writer reached that slot again: restart
+  uint64_t* h0 = reinterpret_cast<uint64_t*>(p->hdr);  // the 64-byte header
+  uint64_t* s1 = h0 + 8;                                // seq word re-read after the payload
+  for (int attempt = 0; attempt < 64; ++attempt) {
+    SPZ_CUDA_TRY(cudaMemcpyAsync(h0, src, SPZ_SYNC_HEADER_BYTES, hk, p->stream));
     SPZ_CUDA_TRY(cudaStreamSynchronize(p->stream));
+    const uint64_t v = h0[0];
+    if (v == 0) return fail(SPZ_ESTATE, "spz_policy_load: nothing published yet (version 0)");
     if (h0[1] != (uint64_t)p->np)
       return fail(SPZ_EINVAL, "spz_policy_load: payload holds " + std::to_string(h0[1]) + " floats, the policy needs " +
                                   std::to_string(p->np));
-    SPZ_CUDA_TRY(cudaMemcpyAsync(p->P, src + 16, (size_t)p->np * 4, pk, p->stream));
-    SPZ_CUDA_TRY(cudaMemcpyAsync(h1, src, 16, hk, p->stream));
+    const int slot = (int)(v & 1);
+    if (h0[2 + slot] != 2 * v) continue;  // slot already being rewritten with v + 2
+    SPZ_CUDA_TRY(cudaMemcpyAsync(p->P, src + SPZ_SYNC_HEADER_BYTES + slot * SPZ_SYNC_SLOT_BYTES(p->np),
+                                 (size_t)p->np * 4, pk, p->stream));
+    SPZ_CUDA_TRY(cudaMemcpyAsync(s1, src + 16 + 8 * slot, 8, hk, p->stream));
     SPZ_CUDA_TRY(cudaStreamSynchronize(p->stream));
-    if (h1[0] != h0[0]) continue;
-    p->version = h0[0];
+    if (*s1 != 2 * v) continue;
+        p->version = v;
     SPZ_TRY(p->bf16 ? refresh<__nv_bfloat16>(p) : refresh<float>(p));
     SPZ_CUDA_TRY(cudaStreamSynchronize(p->stream));
     if (version) *version = p->version;
     return SPZ_OK;
   }
-  return fail(SPZ_ETIMEOUT, "spz_policy_load: the payload kept changing under the read");
+  return fail(SPZ_ETIMEOUT, "spz_policy_load: every attempt overlapped a writer");
+}
+
+spz_status spz_policy_get_params(spz_policy* p, float* host_out, int64_t n) {
+  if (!p || !host_out) return fail(SPZ_EINVAL, "spz_policy_get_params: NULL argument");
+  if (n < p->np) return fail(SPZ_EINVAL, "spz_policy_get_params: output holds fewer than " + std::to_string(p->np) + " floats");
+  if (p->version == 0) return fail(SPZ_ESTATE, "spz_policy_get_params: no parameters loaded");
+  DeviceGuard dg(p->device);
+  SPZ_CUDA_TRY(cudaMemcpyAsync(host_out, p->P, (size_t)p->np * 4, cudaMemcpyDeviceToHost, p->stream));
+  SPZ_CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return SPZ_OK;
 }
 
 spz_status spz_policy_act(spz_policy* p, int64_t n, const float* obs, int32_t deterministic, uint64_t seed,

@@ -35,8 +35,8 @@ EXPORTS = [
     "spz_update", "spz_update_async", "spz_update_wait", "spz_learner_set_stream", "spz_get_params", "spz_set_params", "spz_get_counters", "spz_sync_actor",
     "spz_learner_profile", "spz_learner_launches_per_step", "spz_learner_debug_buffer", "spz_learner_destroy",
     "spz_diag_gemm_bf16", "spz_diag_gemm_f32", "spz_split_exchange", "spz_diag_tc_trace",
-    "spz_policy_create", "spz_policy_load", "spz_policy_act", "spz_policy_destroy", "spz_tune_batch",
-    "spz_replay_track", "spz_replay_loss",
+    "spz_policy_create", "spz_policy_load", "spz_policy_act", "spz_policy_get_params", "spz_policy_destroy", "spz_tune_batch",
+    "spz_replay_track", "spz_replay_loss", "spz_plan_rank",
 ]
 
 
@@ -84,6 +84,13 @@ class spz_config(ctypes.Structure):
         ("use_graph", ctypes.c_int32),
         ("comm_mode", ctypes.c_int32),
     ]
+
+
+class spz_plan(ctypes.Structure):
+    _fields_ = [("role", ctypes.c_int32), ("group_size", ctypes.c_int32), ("group_rank", ctypes.c_int32),
+                ("group_color", ctypes.c_int32), ("row0", ctypes.c_int64), ("rows", ctypes.c_int64),
+                ("actor_root", ctypes.c_int32), ("critic_root", ctypes.c_int32), ("allreduce", ctypes.c_int32),
+                ("pad_", ctypes.c_int32)]
 
 
 class spz_stats(ctypes.Structure):
@@ -144,8 +151,10 @@ def lib():
             "spz_policy_create": (ctypes.c_int, [ctypes.POINTER(spz_policy_desc), ctypes.POINTER(P)]),
             "spz_policy_load": (ctypes.c_int, [P, P, I64, ctypes.POINTER(U64)]),
             "spz_policy_act": (ctypes.c_int, [P, I64, P, I32, U64, U64, P]),
+            "spz_policy_get_params": (ctypes.c_int, [P, P, I64]),
             "spz_policy_destroy": (None, [P]),
             "spz_replay_track": (ctypes.c_int, [P, I32]),
+            "spz_plan_rank": (ctypes.c_int, [ctypes.POINTER(spz_config), I64, ctypes.POINTER(spz_plan)]),
             "spz_replay_loss": (ctypes.c_int, [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
             "spz_tune_batch": (ctypes.c_int, [P, ctypes.POINTER(I64), I32, I64, I64, D, D, I32,
                                               ctypes.POINTER(spz_tune_point), ctypes.POINTER(I32), ctypes.POINTER(I64)]),
@@ -225,6 +234,16 @@ def spz_nccl_unique_id():
     return bytes(buf)
 
 
+def spz_plan_rank(batch, world_size, rank, role=SPZ_ROLE_ALL, n_critic_ranks=0, comm_mode=0, algo=SPZ_SAC, obs_dim=1,
+                  act_dim=1):
+    """The host-side multi-GPU plan of one rank (include/spz.h spz_plan_rank): a dict of its fields."""
+    cfg = spz_config_default(algo, obs_dim, act_dim)
+    cfg.world_size, cfg.rank, cfg.role, cfg.n_critic_ranks, cfg.comm_mode = world_size, rank, role, n_critic_ranks, comm_mode
+    p = spz_plan()
+    _check(lib().spz_plan_rank(ctypes.byref(cfg), batch, ctypes.byref(p)))
+    return {f: getattr(p, f) for f, _ in spz_plan._fields_ if f != "pad_"}
+
+
 def spz_config_default(algo, obs_dim, act_dim):
     c = spz_config()
     _check(lib().spz_config_default(algo, obs_dim, act_dim, ctypes.byref(c)))
@@ -278,6 +297,19 @@ def spz_get_counters(learner):
     return dict(step=a[0].value, t_critic=a[1].value, t_actor=a[2].value, t_alpha=a[3].value)
 
 
+SYNC_HEADER_BYTES = 64  # include/spz.h SPZ_SYNC_HEADER_BYTES
+
+
+def sync_slot_bytes(n_floats):
+    """include/spz.h SPZ_SYNC_SLOT_BYTES."""
+    return (n_floats * 4 + 63) // 64 * 64
+
+
+def sync_bytes(n_floats):
+    """include/spz.h SPZ_SYNC_BYTES: size of an actor publication buffer (header + two slots)."""
+    return SYNC_HEADER_BYTES + 2 * sync_slot_bytes(n_floats)
+
+
 def spz_sync_actor(learner, dst_device, dst_ptr, dst_bytes):
     v = ctypes.c_uint64()
     _check(lib().spz_sync_actor(learner, dst_device, ctypes.c_void_p(dst_ptr), dst_bytes, ctypes.byref(v)))
@@ -307,6 +339,8 @@ def spz_learner_debug_buffer(learner, name):
                                           ctypes.byref(es)))
     if name == "idx":
         return raw.view(np.int32)
+    if name.startswith("mask"):
+        return raw.view(np.uint32)
     if es.value == 2:
         return (raw.view(np.uint16).astype(np.uint32) << 16).view(np.float32)
     if es.value == 8:
@@ -478,6 +512,12 @@ def spz_policy_act(policy, n, obs, deterministic, seed, step, act):
     _check(lib().spz_policy_act(policy, n, _ptr(obs), 1 if deterministic else 0, seed, step, _ptr(act)))
 
 
+def spz_policy_get_params(policy, n):
+    out = np.empty(n, dtype=np.float32)
+    _check(lib().spz_policy_get_params(policy, out.ctypes.data_as(ctypes.c_void_p), n))
+    return out
+
+
 def spz_policy_destroy(policy):
     lib().spz_policy_destroy(policy)
 
@@ -495,6 +535,9 @@ class Policy:
 
     def load(self, payload_ptr, nbytes):
         return spz_policy_load(self.h, payload_ptr, nbytes)
+
+    def params(self, n):
+        return spz_policy_get_params(self.h, n)
 
     def act(self, obs, deterministic=False, seed=0, step=0, out=None):
         n = obs.shape[0]

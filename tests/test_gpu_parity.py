@@ -16,21 +16,7 @@ pytestmark = pytest.mark.gpu
 
 from paper_2312_06126_b200 import spz  # noqa: E402
 
-TOL = {"fp32": 1e-4, "bf16": 2e-2}
-
-
-def rel(x, ref):
-    x, ref = np.asarray(x, np.float64), np.asarray(ref, np.float64)
-    return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-30))
-
-
-def make_rings(o, m, C, n_push=None, seed=synthdata.DATA_SEED, kind="locomotion"):
-    tr = synthdata.transitions(kind, o, m, C if n_push is None else n_push, seed=seed)
-    g = spz.Replay(o, m, C)
-    first = g.push(**tr)
-    r = oring.Ring(o, m, C)
-    assert r.push(**tr) == first
-    return g, r
+from tests.parity import TOL, make_rings, rel, run_parity  # noqa: E402,F401
 
 
 # ----------------------------------------------------------------------------- a1 + a2 bit-exact
@@ -155,51 +141,6 @@ def test_update_async_overlapped_pushes_bit_identical():
 
 # ----------------------------------------------------------------------------- whole update parity
 
-def run_parity(algo, precision, o, m, h, L, B, C, K, kind="locomotion", use_graph=True, check_moments=True):
-    g, r = make_rings(o, m, C, kind=kind)
-    p = synthdata.init_params(o, m, h, L, algo=algo)
-    lrn = spz.Learner(g, algo=algo, precision=precision, hidden=h, n_hidden=L, max_batch=B, use_graph=use_graph)
-    lrn.set("actor", p["actor"])
-    lrn.set("q1", p["q1"])
-    lrn.set("q2", p["q2"])
-    lrn.set("q1_targ", p["q1"])
-    lrn.set("q2_targ", p["q2"])
-    if algo == "td3":
-        lrn.set("actor_targ", p["actor"])
-    cfg = osac.Config(obs_dim=o, act_dim=m, hidden=h, n_hidden=L, alpha_auto=(algo == "sac"))
-    la = float(lrn.get("log_alpha")[0])
-    st = osac.State.create(p["actor"], p["q1"], p["q2"], log_alpha=la,
-                           actor_targ=p["actor"] if algo == "td3" else None)
-    tol = TOL[precision]
-    for k in range(K):
-        gs = lrn.update(B, 1)
-        if algo == "sac":
-            st, os_, _ = osac.sac_step(st, r, B, synthdata.SAMPLE_SEED, cfg)
-        else:
-            st, os_, _ = otd3.td3_step(st, r, B, synthdata.SAMPLE_SEED, cfg)
-        assert gs["step"] == k + 1
-        for key in ("critic_loss", "actor_loss", "q1_mean", "q2_mean", "logp_mean", "alpha"):
-            ref = os_[key]
-            # a mean of signed terms is compared relative to the mean |term| (its summation error scales with it)
-            scale = max(abs(ref), os_.get(key + "_abs", 0.0))
-            assert abs(gs[key] - ref) <= tol * max(scale, 1e-6) + (tol * 1e-2 if key in ("q1_mean", "q2_mean") else 0), (k, key, gs[key], ref)
-    names = ["actor", "q1", "q2", "q1_targ", "q2_targ"] + (["actor_targ"] if algo == "td3" else [])
-    errs = {}
-    for n in names:
-        errs[n] = rel(lrn.get(n), getattr(st, n))
-        assert errs[n] <= tol, (n, errs)
-    if algo == "sac":
-        assert abs(float(lrn.get("log_alpha")[0]) - st.log_alpha) <= tol * max(1.0, abs(st.log_alpha))
-    if check_moments:
-        for n in ("actor", "q1", "q2"):
-            mm = lrn.get(n, spz.SPZ_S_ADAM_M)
-            assert rel(mm, st.opt[n].m) <= 10 * tol, (n, "m", rel(mm, st.opt[n].m))
-    c = lrn.counters()
-    assert c["step"] == K and c["t_critic"] == K
-    assert c["t_actor"] == (K if algo == "sac" else sum(1 for k in range(K) if otd3.is_delayed(k, cfg)))
-    return errs
-
-
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_sac_parity_pendulum(precision):
     # BASELINE config 0: Pendulum-shaped SAC, 2x64, B 256, 10K ring (200 updates in the bench; 30 here)
@@ -236,7 +177,7 @@ def test_sac_parity_pair_schedule_critic_forward(B, monkeypatch):
     """The two-blocks-in-flight critic forward (default at >= 4 row blocks per CTA) forced at sizes where
     CTAs get 2..4 blocks: full pairs, a trailing single block, ragged last block."""
     monkeypatch.setenv("SPZ_MLP_PAIR", "1")
-    run_parity("sac", "bf16", 22, 6, 256, 2, B, 20_000, 2, check_moments=False)
+    run_parity("sac", "bf16", 22, 6, 256, 2, B, 20_000, 2)
 
 
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
@@ -297,15 +238,56 @@ def test_determinism_two_runs_bit_identical():
         assert np.array_equal(a, b)
 
 
+# ----------------------------------------------------------------------------- full-size configs (bench launch config)
+# BASELINE.json configs 1-4 at full size, in the launch configuration bench.py times: raw gradients of every
+# tensor at every step (k >= 1 included), Adam m and v, parameters, and the Adam / Polyak identities.
+
+@pytest.fixture(scope="module")
+def walker_rings():
+    return make_rings(22, 6, 1_000_000)
+
+
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
-def test_walker_full_size_two_steps(precision):
-    """BASELINE config 1 at full size (B 8192, 2x256, 1M ring), in the launch configuration the bench times."""
-    run_parity("sac", precision, 22, 6, 256, 2, 8192, 1_000_000, 2, check_moments=False)
+def test_walker_full_size(precision, walker_rings):
+    """Config 1: WLK, B 8192, 2x256, 1M ring."""
+    run_parity("sac", precision, 22, 6, 256, 2, 8192, 1_000_000, 3, rings=walker_rings, tag=f"walker-{precision}")
 
 
-def test_humanoid_full_size_one_step():
-    """BASELINE config 3 at full size on one GPU (B 65536, 3x512, 1M ring), bf16 as the bench runs it."""
-    run_parity("sac", "bf16", 44, 17, 512, 3, 65536, 1_000_000, 1, check_moments=False)
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_ant_full_size(precision):
+    """Config 2 shapes on one GPU: ANT, o 28, m 8, B 32768 (> 148*128 rows: the GEMM + head-kernel actor
+    backward), 2x256, 1M ring."""
+    run_parity("sac", precision, 28, 8, 256, 2, 32768, 1_000_000, 2, tag=f"ant-{precision}")
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_humanoid_full_size(precision):
+    """Config 3 shapes on one GPU: HUM, B 65536, 3x512, 1M ring."""
+    run_parity("sac", precision, 44, 17, 512, 3, 65536, 1_000_000, 2, tag=f"humanoid-{precision}")
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_td3_full_size(precision):
+    """Config 4 shapes on one GPU: TD3, B 131072, 3x1024, 4M ring; step 0 critic only, step 1 with the
+    delayed actor, Polyak on all targets."""
+    run_parity("td3", precision, 44, 17, 1024, 3, 131072, 4_000_000, 2, tag=f"td3-{precision}")
+
+
+# mutation check: each of these breaks one piece of a6-a9 at the WLK launch configuration; the parity run
+# must fail under every one (SPZ_DIAG_SKIP_OPS / SPZ_DIAG_MUTATE are diagnostics-only plan edits)
+@pytest.mark.parametrize("env,val", [
+    ("SPZ_DIAG_SKIP_OPS", "adam_polyak"),   # no optimizer step at all
+    ("SPZ_DIAG_MUTATE", "tau0"),            # Polyak averaging dropped (targets frozen)
+    ("SPZ_DIAG_MUTATE", "drop_wgrad=0"),    # q1 layer-0 weight gradient never computed
+    ("SPZ_DIAG_MUTATE", "drop_wgrad=4"),    # q1 head weight gradient
+    ("SPZ_DIAG_MUTATE", "drop_wgrad=8"),    # actor head weight gradient
+    ("SPZ_DIAG_MUTATE", "drop_bias=3"),     # q2 layer-1 bias gradient
+    ("SPZ_DIAG_SKIP_OPS", "actor_bwd_fused"),  # actor backward (a7) dropped
+])
+def test_mutation_fails_parity(env, val, walker_rings, monkeypatch):
+    monkeypatch.setenv(env, val)
+    with pytest.raises(AssertionError):
+        run_parity("sac", "bf16", 22, 6, 256, 2, 8192, 1_000_000, 2, rings=walker_rings, tag=f"mutant-{val}")
 
 
 # ----------------------------------------------------------------------------- API behaviour
@@ -346,14 +328,19 @@ def test_sync_actor_versioned_payload():
     g, _ = make_rings(22, 6, 2000)
     lrn = spz.Learner(g, precision="bf16", hidden=64, n_hidden=2, max_batch=512)
     n = lrn.get("actor").size
-    buf = torch.zeros(16 + 4 * n, dtype=torch.uint8, device="cuda")
+    buf = torch.zeros(spz.sync_bytes(n), dtype=torch.uint8, device="cuda")
     v1 = spz.spz_sync_actor(lrn.h, 0, buf.data_ptr(), buf.numel())
     lrn.update(512, 1)
     v2 = spz.spz_sync_actor(lrn.h, 0, buf.data_ptr(), buf.numel())
     assert v2 == v1 + 1
-    hdr = buf[:16].cpu().numpy().view(np.uint64)
-    assert hdr[0] == v2 and hdr[1] == n
-    assert np.array_equal(buf[16:].cpu().numpy().view(np.float32), lrn.get("actor"))
+    hdr = buf[:spz.SYNC_HEADER_BYTES].cpu().numpy().view(np.uint64)
+    # header: version, n_floats, seq of slot 0 / 1 (2v once version v in slot v & 1 is complete)
+    assert hdr[0] == v2 and hdr[1] == n and hdr[2 + (v2 & 1)] == 2 * v2 and hdr[2 + (v1 & 1)] == 2 * v1
+    off = spz.SYNC_HEADER_BYTES + (v2 & 1) * spz.sync_slot_bytes(n)
+    assert np.array_equal(buf[off:off + 4 * n].cpu().numpy().view(np.float32), lrn.get("actor"))
+    with pytest.raises(spz.SpzError) as e:  # too small for the two slots
+        spz.spz_sync_actor(lrn.h, 0, buf.data_ptr(), 16 + 4 * n)
+    assert e.value.status == spz.SPZ_EINVAL
 
 
 def test_profile_and_launch_count():

@@ -25,7 +25,7 @@ def publish(algo, precision, o, m, h, L, steps=2):
     if steps:
         lrn.update(512, steps)
     n = lrn.get("actor").size
-    buf = torch.zeros(16 + 4 * n, dtype=torch.uint8, device="cuda")
+    buf = torch.zeros(spz.sync_bytes(n), dtype=torch.uint8, device="cuda")
     v = spz.spz_sync_actor(lrn.h, 0, buf.data_ptr(), buf.numel())
     return lrn, buf, v
 
@@ -55,11 +55,14 @@ def test_policy_device_buffers_and_versions():
     g.push(**synthdata.transitions("locomotion", o, m, 3000))
     lrn = spz.Learner(g, precision="bf16", hidden=h, n_hidden=L, max_batch=256)
     n = lrn.get("actor").size
-    buf = torch.zeros(16 + 4 * n, dtype=torch.uint8, device="cuda")
+    buf = torch.zeros(spz.sync_bytes(n), dtype=torch.uint8, device="cuda")
     pol = spz.Policy(o, m, hidden=h, n_hidden=L, max_batch=300)
     s = np.random.default_rng(0).normal(size=(300, o)).astype(np.float32)
     with pytest.raises(spz.SpzError) as e:
         pol.act(s)
+    assert e.value.status == spz.SPZ_ESTATE
+    with pytest.raises(spz.SpzError) as e:  # nothing published yet
+        pol.load(buf.data_ptr(), buf.numel())
     assert e.value.status == spz.SPZ_ESTATE
     v1 = spz.spz_sync_actor(lrn.h, 0, buf.data_ptr(), buf.numel())
     assert pol.load(buf.data_ptr(), buf.numel()) == v1
@@ -83,3 +86,60 @@ def test_policy_device_buffers_and_versions():
     assert e.value.status == spz.SPZ_EINVAL
     with pytest.raises(spz.SpzError):
         pol.act(np.zeros((301, o), np.float32))
+
+
+def test_sync_actor_concurrent_publish_never_blends():
+    """a10/f1 stress (S:259 never a blend, S:271 monotone): one thread publishes thousands of versions of a
+    large actor (3x1024, 8.6 MB per slot), each version a constant vector of its own value, while another
+    thread loads on its own stream; every load must be exactly one published version's payload, and the
+    versions a reader sees never go backwards."""
+    import threading
+    o, m, h, L = 44, 17, 1024, 3
+    g = spz.Replay(o, m, 1000)
+    g.push(**synthdata.transitions("locomotion", o, m, 1000))
+    lrn = spz.Learner(g, algo="td3", precision="bf16", hidden=h, n_hidden=L, max_batch=256)
+    n = lrn.get("actor").size
+    buf = torch.zeros(spz.sync_bytes(n), dtype=torch.uint8, device="cuda")
+    pol = spz.Policy(o, m, algo="td3", hidden=h, n_hidden=L, max_batch=16)
+    N = 2000
+    pats = [np.full(n, float(i + 1), np.float32) for i in range(2)]
+    ver_val = {}
+    done = threading.Event()
+    errors = []
+
+    def writer():
+        try:
+            for i in range(N):
+                val = float(i + 1)
+                pats[i % 2].fill(val)
+                lrn.set("actor", pats[i % 2])
+                v = spz.spz_sync_actor(lrn.h, 0, buf.data_ptr(), buf.numel())
+                ver_val[v] = val
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+        finally:
+            done.set()
+
+    loads, last = [], 0
+    t = threading.Thread(target=writer)
+    t.start()
+    while not done.is_set() or len(loads) < 20:
+        try:
+            v = pol.load(buf.data_ptr(), buf.numel())
+        except spz.SpzError as e:
+            if e.status == spz.SPZ_ESTATE:  # before the first publication
+                continue
+            raise
+        p = pol.params(n)
+        assert v >= last, (v, last)
+        last = v
+        loads.append((v, float(p[0]), bool(np.all(p == p[0]))))
+        if done.is_set() and len(loads) >= 20:
+            break
+    t.join()
+    assert not errors, errors
+    assert len(ver_val) == N
+    for v, first, uniform in loads:
+        assert uniform, ("blend", v)
+        assert first == ver_val[v], (v, first, ver_val[v])
+    assert len({v for v, _, _ in loads}) > 10  # the reader really overlapped many publications

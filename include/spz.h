@@ -132,9 +132,10 @@ void spz_replay_destroy(spz_replay* r);
  * sets alpha_auto = 0 (v1's fixed temperature).  Role ALL only.
  */
 typedef enum { SPZ_SAC = 0, SPZ_TD3 = 1, SPZ_DDPG = 2, SPZ_SACV1 = 3 } spz_algo;
-/* FP32: GEMMs in full fp32 (exact-order-independent fp32 FMA); BF16: GEMM operands
- * rounded to bf16 (RNE) on tcgen05 tensor cores with fp32 accumulation; every
- * epilogue, master weight and optimizer state stays fp32 (reading #15). */
+/* FP32: every dense layer as 3xTF32 on tcgen05 (hi = rna_tf32(x), lo = rna_tf32(x - hi),
+ * D = hi*hi + hi*lo + lo*hi, 64-deep TMEM chunk sums added in fp32 registers; readings #15, #22);
+ * BF16: GEMM operands rounded to bf16 (RNE) on tcgen05 tensor cores with fp32 accumulation.  Every
+ * epilogue, master weight and optimizer state stays fp32 in both (reading #15). */
 typedef enum { SPZ_FP32 = 0, SPZ_BF16 = 1 } spz_precision;
 /* Role of this rank (P:239-247 actor/critic model parallelism). */
 typedef enum { SPZ_ROLE_ALL = 0, SPZ_ROLE_CRITIC = 1, SPZ_ROLE_ACTOR = 2 } spz_role;

@@ -14,13 +14,37 @@ namespace spz {
 
 
 // ------------------------------------------------------------------ a1 + a2: index + gather
-// Block = 32 rows.  Records are read with 128-bit loads into shared memory; each
-// operand region written by the block is contiguous, so stores are coalesced.
-// Writes (local row j, global row row0 + j):
+// Block = 32 rows.  Records are read with 128-bit loads into shared memory; the operands leave with
+// 128-bit stores, each row's written columns rounded up to whole 32-byte sectors.  Writes (local row j,
+// global row row0 + j):
 //   Xa[j] = s2, Xa[Bl + j] = s                           (actor input, [s2; s])
-//   Xc[j] = [s | a], Xc[Bl + j] = [s | 0], Xc[2Bl + j] = [s2 | 0]  (critic inputs)
+//   Xc[j] = [s | a], Xc[Bl + j] = [s | 0], Xc[2Bl + j] = [s2 | 0]  (critic inputs; the action columns of
+//                                                         the last two are written by the actor heads)
 //   r[j], d[j]
+// Columns past the rounded-up width are padding: zeroed once at allocation and never written.
 constexpr int GATHER_ROWS = 32;
+
+template <typename T>
+__device__ __forceinline__ uint4 pack_chunk(const float* src, int c0, int n) {
+  // 16 bytes of the operand: elements c0 .. c0 + 16/sizeof(T) - 1 of a row, zero past n
+  constexpr int EPC = 16 / sizeof(T);
+  float v[EPC];
+#pragma unroll
+  for (int i = 0; i < EPC; ++i) v[i] = c0 + i < n ? src[c0 + i] : 0.f;
+  uint4 u;
+  if constexpr (std::is_same<T, float>::value) {
+    u.x = __float_as_uint(v[0]);
+    u.y = __float_as_uint(v[1]);
+    u.z = __float_as_uint(v[2]);
+    u.w = __float_as_uint(v[3]);
+  } else {
+    u.x = pack_bf16x2(v[0], v[1]);
+    u.y = pack_bf16x2(v[2], v[3]);
+    u.z = pack_bf16x2(v[4], v[5]);
+    u.w = pack_bf16x2(v[6], v[7]);
+  }
+  return u;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ rec, int R, int o, int m,
@@ -51,20 +75,38 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ r
     sm4[e] = __ldg(reinterpret_cast<const float4*>(rec + sidx[rr] * R) + q);
   }
   __syncthreads();
+  // 16-byte chunks per operand row, rounded up to whole 32-byte sectors (and capped by the row pitch)
+  constexpr int EPC = 16 / sizeof(T), EPS = 32 / sizeof(T);
   const int s2c = o + m + 2;
-  // actor input rows
-  for (int e = threadIdx.x; e < nr * lda; e += blockDim.x) {
-    const int rr = e / lda, c = e - rr * lda;
+  const int ca = min((o + EPS - 1) / EPS * EPS, lda) / EPC;          // s / s2 columns (actor, critic [s|0])
+  const int cb = min((o + m + EPS - 1) / EPS * EPS, ldc) / EPC;      // [s | a]
+  const int cs = min((o + EPS - 1) / EPS * EPS, ldc) / EPC;
+  const int J = 2 * ca + cb + 2 * cs;                                 // chunks per row
+  for (int e = threadIdx.x; e < nr * J; e += blockDim.x) {
+    const int rr = e / J;
+    int k = e - rr * J;
     const float* rw = sm + rr * R;
-    Xa[(int64_t)(j0 + rr) * lda + c] = from_f<T>(c < o ? rw[s2c + c] : 0.f);
-    Xa[(int64_t)(Bl + j0 + rr) * lda + c] = from_f<T>(c < o ? rw[c] : 0.f);
-  }
-  for (int e = threadIdx.x; e < nr * ldc; e += blockDim.x) {
-    const int rr = e / ldc, c = e - rr * ldc;
-    const float* rw = sm + rr * R;
-    Xc[(int64_t)(j0 + rr) * ldc + c] = from_f<T>(c < o + m ? rw[c] : 0.f);
-    Xc[(int64_t)(Bl + j0 + rr) * ldc + c] = from_f<T>(c < o ? rw[c] : 0.f);
-    Xc[(int64_t)(2 * Bl + j0 + rr) * ldc + c] = from_f<T>(c < o ? rw[s2c + c] : 0.f);
+    const int64_t j = j0 + rr;
+    uint4* dst;
+    uint4 v;
+    if (k < ca) {  // Xa s2 row
+      dst = reinterpret_cast<uint4*>(Xa + j * lda) + k;
+      v = pack_chunk<T>(rw + s2c, k * EPC, o);
+    } else if ((k -= ca) < ca) {  // Xa s row
+      dst = reinterpret_cast<uint4*>(Xa + (Bl + j) * lda) + k;
+      v = pack_chunk<T>(rw, k * EPC, o);
+    } else if ((k -= ca) < cb) {  // Xc [s | a]
+      dst = reinterpret_cast<uint4*>(Xc + j * ldc) + k;
+      v = pack_chunk<T>(rw, k * EPC, o + m);
+    } else if ((k -= cb) < cs) {  // Xc [s | a~ later]
+      dst = reinterpret_cast<uint4*>(Xc + (Bl + j) * ldc) + k;
+      v = pack_chunk<T>(rw, k * EPC, o);
+    } else {  // Xc [s2 | a' later]
+      k -= cs;
+      dst = reinterpret_cast<uint4*>(Xc + (2 * (int64_t)Bl + j) * ldc) + k;
+      v = pack_chunk<T>(rw + s2c, k * EPC, o);
+    }
+    *dst = v;
   }
   if (threadIdx.x < nr) {
     r[j0 + threadIdx.x] = sm[threadIdx.x * R + o + m];
@@ -636,7 +678,8 @@ struct AdamTensor {
   int32_t pad_;
 };
 
-// Split-K partial sum of element i of tensor tn (fixed split order; 32-bit offsets, 4 loads in flight).
+// Split-K partial sum of element i of tensor tn (fixed split order, left to right; 32-bit offsets).  The
+// loads of up to 16 splits are all issued before the first add: one memory round trip per 16 splits.
 __device__ __forceinline__ float partial_sum(const float* __restrict__ partials, int n_partials, int pstride, int pld,
                                              int cols, int i) {
   int idx;
@@ -647,17 +690,16 @@ __device__ __forceinline__ float partial_sum(const float* __restrict__ partials,
     idx = i * pld;
   }
   const float* src = partials + idx;
+  constexpr int CH = 16;
   float g = 0.f;
-  int s = 0;
-  for (; s + 4 <= n_partials; s += 4) {
-    const float t0 = __ldg(src + s * pstride), t1 = __ldg(src + (s + 1) * pstride);
-    const float t2 = __ldg(src + (s + 2) * pstride), t3 = __ldg(src + (s + 3) * pstride);
-    g += t0;
-    g += t1;
-    g += t2;
-    g += t3;
+  for (int s0 = 0; s0 < n_partials; s0 += CH) {
+    float t[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) t[u] = s0 + u < n_partials ? __ldg(src + (s0 + u) * pstride) : 0.f;
+#pragma unroll
+    for (int u = 0; u < CH; ++u)
+      if (s0 + u < n_partials) g += t[u];
   }
-  for (; s < n_partials; ++s) g += __ldg(src + s * pstride);
   return g;
 }
 __device__ __forceinline__ float partial_sum(const AdamTensor& tn, int64_t i) {
@@ -696,8 +738,9 @@ __global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegme
                                                                  float* __restrict__ Vo, T* __restrict__ S,
                                                                  int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
                                                                  int* __restrict__ flag) {
-  pdl_wait();
-  pdl_launch();
+  // Prologue before the grid dependency wait (overlaps the weight-gradient kernel's tail): the segment
+  // descriptor (host-written) and the optimizer state m, v, theta, theta' -- written only by the previous
+  // step's Adam, which completed before any kernel of this step passed its own wait.
   __shared__ bool skip;
   const AdamSegment* sg = segs + blockIdx.x;
   const int opt = __ldg(&sg->t.opt);
@@ -708,9 +751,6 @@ __global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegme
   const float* partials = reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(&sg->t.partials)));
   const int n_partials = __ldg(&sg->t.n_partials), pld = __ldg(&sg->t.pld), cols = __ldg(&sg->t.cols);
   const int pstride = (int)__ldg(&sg->t.pstride);
-  const int64_t step = __ldg(hp.snap);
-  const double* tot = hp.totals;
-  const float bc1 = __ldg(hp.bc + opt), bc2 = __ldg(hp.bc + 3 + opt);
   float g[ADAM_EPT], m0[ADAM_EPT], v0[ADAM_EPT], p0[ADAM_EPT], tp0[ADAM_EPT];
 #pragma unroll
   for (int u = 0; u < ADAM_EPT; ++u) {
@@ -722,6 +762,19 @@ __global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegme
       v0[u] = Vo[pi];
       p0[u] = P[pi];
       if (t_off >= 0) tp0[u] = P[t_off + i];
+    }
+  }
+  pdl_wait();
+  pdl_launch();
+  // after the wait: this step's gradient partials, loss totals and counter snapshot
+  const int64_t step = __ldg(hp.snap);
+  const double* tot = hp.totals;
+  const float bc1 = __ldg(hp.bc + opt), bc2 = __ldg(hp.bc + 3 + opt);
+#pragma unroll
+  for (int u = 0; u < ADAM_EPT; ++u) {
+    const int k = threadIdx.x + u * ADAM_NT;
+    if (k < count) {
+      const int i = start + k;
       g[u] = opt == 2 ? (float)(-(tot[4] / hp.B + hp.target_entropy))  // log-alpha gradient
                       : partial_sum(partials, n_partials, pstride, pld, cols, i);
     }

@@ -91,14 +91,19 @@ static bool fp32_simt_env() {
   return on;
 }
 
+// One backend per precision: bf16 -> tcgen05 kind::f16, FP32 -> 3xTF32 tcgen05 (the SIMT kernel only under
+// the explicit SPZ_FP32_SIMT=1 diagnostic).  The plan checks every GEMM against these kernels when it is
+// built and fails with SPZ_EUNSUPPORTED instead of dispatching anywhere else (gemm_supported below).
+template <typename T>
+static bool gemm_supported(const GemmArgs& a) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) return tc_gemm_supported(a);
+  else return fp32_simt_env() || tc_gemm_tf32_supported(a);
+}
+
 template <typename T>
 static cudaError_t run_gemm(const GemmArgs& a, cudaStream_t st) {
-  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    if (tc_gemm_supported(a)) return tc_gemm_bf16(a, st);
-  } else {
-    if (!fp32_simt_env() && tc_gemm_tf32_supported(a)) return tc_gemm_tf32x3(a, st);
-  }
-  return gemm_simt<T>(a, st);
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) return tc_gemm_bf16(a, st);
+  else return fp32_simt_env() ? gemm_simt<T>(a, st) : tc_gemm_tf32x3(a, st);
 }
 
 }  // namespace spz
@@ -401,8 +406,12 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         if (a.g[i].M > 0 && a.g[i].N > 0) return false;
       return true;
     };
+    std::string unsupported;  // first GEMM the tensor-core kernels do not take (-> SPZ_EUNSUPPORTED)
     auto gemm = [&](const char* cls, GemmArgs a) {
       if (empty_gemm(a)) return;  // e.g. the TD3 actor role on a non-delayed step
+      if (!gemm_supported<T>(a) && unsupported.empty())
+        unsupported = std::string(cls) + " (M " + std::to_string(a.g[0].M) + ", N " + std::to_string(a.N) + ", K " +
+                      std::to_string(a.K) + ", epilogue " + std::to_string(a.epi) + ")";
       ops.push_back({cls, [a](cudaStream_t st) { return run_gemm<T>(a, st); }});
     };
     auto mk = [&](int K, int epi, int amn, int bmn) {
@@ -471,7 +480,9 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       float *rr = Lr->r, *dd = Lr->d;
       int32_t* idx = Lr->idx;
       uint32_t* tags = Lr->ring->tags;
-      const size_t smem = (size_t)GATHER_ROWS * R * sizeof(float);
+      const size_t smem = (size_t)GATHER_ROWS * R * sizeof(float);  // <= 227 KB (checked by spz_replay_create)
+      if (smem > 48 * 1024)
+        SPZ_CUDA_TRY(cudaFuncSetAttribute(gather_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       ops.push_back({"gather", [=](cudaStream_t st) {
                        launch_pdl(gather_kernel<T>, dim3((unsigned)cdiv(Bl, GATHER_ROWS)), dim3(256), smem, st, 
                            rec, R, o, m, fill, seed, stp, row0, Bl, Xa, lda, Xc, ldc, rr, dd, idx, tags);
@@ -1351,6 +1362,11 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
                        if (e != cudaSuccess) return e;
                        return launch_pdl(shadow_refresh_kernel<T>, dim3(64, nsh), dim3(256), 0, st, sh, nsh, (const float*)P, S);
                      }, 1});
+    }
+    if (!unsupported.empty()) {
+      for (auto& v : Lr->ops) v.clear();
+      return fail(SPZ_EUNSUPPORTED, std::string("spz_update: GEMM ") + unsupported + " is not supported by the " +
+                                        (Lr->bf16 ? "bf16 tcgen05" : "3xTF32 tcgen05") + " kernels (no other backend)");
     }
   }
   // diagnostics only: SPZ_DIAG_NOOP_OPS=k appends k empty PDL kernels to the step (kernel-boundary cost)

@@ -163,11 +163,14 @@ spz_status forward(spz_policy* p, int64_t n) {
     g.M = (int)n;
     g.N = a.N;
     g.bias = p->P + p->boff[l];
-    cudaError_t e;
-    if constexpr (std::is_same<T, __nv_bfloat16>::value)
-      e = tc_gemm_supported(a) ? tc_gemm_bf16(a, p->stream) : gemm_simt<T>(a, p->stream);
-    else
-      e = tc_gemm_tf32_supported(a) ? tc_gemm_tf32x3(a, p->stream) : gemm_simt<T>(a, p->stream);
+    cudaError_t e;  // one backend per precision (no SIMT dispatch): unsupported shapes are an error
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+      if (!tc_gemm_supported(a)) return fail(SPZ_EUNSUPPORTED, "spz_policy_act: layer GEMM not supported by the bf16 tcgen05 kernel");
+      e = tc_gemm_bf16(a, p->stream);
+    } else {
+      if (!tc_gemm_tf32_supported(a)) return fail(SPZ_EUNSUPPORTED, "spz_policy_act: layer GEMM not supported by the 3xTF32 tcgen05 kernel");
+      e = tc_gemm_tf32x3(a, p->stream);
+    }
     if (e != cudaSuccess) return fail(SPZ_ECUDA, std::string("spz_policy_act: layer GEMM: ") + cudaGetErrorString(e));
   }
   return SPZ_OK;

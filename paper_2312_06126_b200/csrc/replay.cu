@@ -186,6 +186,9 @@ spz_status spz_replay_create(const spz_replay_desc* desc, spz_replay** out) {
   *out = nullptr;
   if (desc->obs_dim < 1 || desc->act_dim < 1) return fail(SPZ_EINVAL, "spz_replay_create: obs_dim and act_dim must be >= 1");
   if (desc->capacity < 1) return fail(SPZ_EINVAL, "spz_replay_create: capacity must be >= 1 (S:193)");
+  // the gather / sample kernels stage 32 records per block in shared memory (opt-in up to 227 KB)
+  if ((int64_t)32 * round_up(2 * (int64_t)desc->obs_dim + desc->act_dim + 2, 4) * 4 > 227 * 1024)
+    return fail(SPZ_EUNSUPPORTED, "spz_replay_create: record of 2 obs_dim + act_dim + 2 floats exceeds the 1816-float gather staging limit");
   spz_status st = check_device(desc->device);
   if (st != SPZ_OK) return st;
   auto* r = new spz_replay();
@@ -377,6 +380,8 @@ spz_status spz_replay_sample(spz_replay* r, int64_t batch, uint64_t seed, uint64
   }
   const unsigned blocks = (unsigned)cdiv(batch, SAMPLE_ROWS);
   const size_t smem = (size_t)SAMPLE_ROWS * r->R * sizeof(float);
+  if (smem > 48 * 1024)
+    SPZ_CUDA_TRY(cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   sample_kernel<<<blocks, 256, smem, r->stream>>>(r->rec, r->R, r->o, r->m, F, seed, step, batch, idx, obs, act, rew,
                                                   next_obs, done, r->tags);
   SPZ_CUDA_TRY(cudaGetLastError());

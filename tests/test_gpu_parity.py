@@ -412,3 +412,54 @@ def test_sacv1_graph_eager_async_bit_identical():
     for other in outs[1:]:
         for a, b in zip(outs[0], other):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_wide_observation_376(precision):
+    """A MuJoCo Humanoid-v4-sized observation (o 376, m 17: 2o + m + 2 = 771-float records, 98 KB of gather
+    staging per block -- past the 48 KB default): replay sampling stays bit-exact and the update (per-layer
+    GEMM path for a K = 376 first layer) matches the oracle."""
+    o, m, C, B = 376, 17, 3000, 300
+    g, r = make_rings(o, m, C)
+    idx = torch.empty(B, dtype=torch.int32, device="cuda")
+    obs = torch.empty(B, o, device="cuda")
+    nobs = torch.empty(B, o, device="cuda")
+    spz.spz_replay_sample(g.h, B, synthdata.SAMPLE_SEED, 3, idx, obs, None, None, nobs)
+    ridx, rb = r.sample(B, synthdata.SAMPLE_SEED, 3)
+    assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(obs.cpu().numpy(), rb["obs"])
+    assert np.array_equal(nobs.cpu().numpy(), rb["next_obs"])
+    run_parity("sac", precision, o, m, 128, 2, B, C, 2, rings=(g, r), tag=f"obs376-{precision}")
+
+
+def test_oversized_record_rejected():
+    with pytest.raises(spz.SpzError) as e:
+        spz.Replay(1000, 17, 100)  # 2017-float records: past the 227 KB gather staging
+    assert e.value.status == spz.SPZ_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("o,m,B", [(22, 6, 1000), (3, 1, 256), (44, 17, 777)])
+def test_learner_gather_operands_bit_exact(precision, o, m, B):
+    """a1-a2 inside the update: the step's indices equal the oracle's, and the gathered operands are
+    exactly the sampled records rounded once to the operand type (bf16 RNE / fp32), with every padding
+    column zero (written once at allocation, never by the 128-bit vector stores)."""
+    g, r = make_rings(o, m, 5000)
+    lrn = spz.Learner(g, precision=precision, hidden=64, n_hidden=2, max_batch=B)
+    for k in range(2):
+        lrn.update(B, 1)
+        ridx, rb = r.sample(B, synthdata.SAMPLE_SEED, k)
+        assert np.array_equal(lrn.debug("idx")[:B], ridx)
+        rnd = (lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).float().numpy()) \
+            if precision == "bf16" else (lambda x: x)
+        Xa = lrn.debug("Xa")
+        lda = Xa.size // (2 * B)
+        Xa = Xa.reshape(2 * B, lda)
+        assert np.array_equal(Xa[:B, :o], rnd(rb["next_obs"])) and np.array_equal(Xa[B:, :o], rnd(rb["obs"]))
+        assert not Xa[:, o:].any()
+        Xc = lrn.debug("Xc")
+        ldc = Xc.size // (3 * B)
+        Xc = Xc.reshape(3 * B, ldc)
+        assert np.array_equal(Xc[:B, :o], rnd(rb["obs"])) and np.array_equal(Xc[:B, o:o + m], rnd(rb["act"]))
+        assert np.array_equal(Xc[B:2 * B, :o], rnd(rb["obs"])) and np.array_equal(Xc[2 * B:, :o], rnd(rb["next_obs"]))
+        assert not Xc[:, o + m:].any()
+        assert np.array_equal(lrn.debug("r")[:B], rb["rew"]) and np.array_equal(lrn.debug("d")[:B], rb["done"])

@@ -28,6 +28,7 @@ CASES = {
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
     parity.GTOL = {"fp32": 10.0, "bf16": 10.0}
+    parity.GTOL_SMALL_B = {"fp32": 10.0, "bf16": 10.0}
     parity.GTOL_TENSOR = {"fp32": 10.0, "bf16": 10.0}
     parity.TOL = {"fp32": 10.0, "bf16": 10.0}
     for nm in names:

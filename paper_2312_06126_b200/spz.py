@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspz.so")
+LIB_PATH = os.environ.get("SPZ_LIB_PATH") or os.path.join(_HERE, "libspz.so")  # override: A/B experiments only
 
 SPZ_OK, SPZ_EINVAL, SPZ_ENODATA, SPZ_ENONFINITE, SPZ_ECUDA, SPZ_ENCCL, SPZ_ENOMEM, SPZ_ESTATE, SPZ_ETIMEOUT, SPZ_EUNSUPPORTED = (
     0, -1, -2, -3, -4, -5, -6, -7, -8, -9)

@@ -43,3 +43,11 @@ for k, nm in enumerate(["actor_fwd_mlp", "critic_fwd_mlp"]):
         st = (tr[:, u, 0, 0][ok] - t0).mean() / 1e3
         en = (tr[:, u, nl - 1, 3][ok & (tr[:, u, nl - 1, 3] > 0)] - t0).mean() / 1e3
         print(f"  unit {u}: mean start {st:6.2f} us, mean end {en:6.2f} us")
+
+# CTA 0's event sequence of the last traced launch (the critic forward): unit, layer, event, us from t0
+names = {0: "mma_start", 4: "mma_first_kb", 5: "mma_last_kb", 1: "mma_issued", 2: "epi_start", 3: "epi_done"}
+for cta in (0, 1, 100):
+    ev = [(int(tr[cta, u, l, e]), u, l, names[e]) for u in range(tr.shape[1]) for l in range(tr.shape[2])
+          for e in range(tr.shape[3]) if tr[cta, u, l, e] > 0]
+    ev.sort()
+    print(f"CTA {cta}:", "; ".join(f"u{u}L{l} {n} {(t - t0) / 1e3:.2f}" for t, u, l, n in ev))

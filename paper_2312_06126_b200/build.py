@@ -26,6 +26,7 @@ if not os.path.isdir(NCCL_INC):
     NCCL_INC = _c[0] if _c else NCCL_INC
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}", f"-I{NCCL_INC}"]
+FLAGS += os.environ.get("SPZ_NVCC_EXTRA", "").split()  # A/B experiments only (tools/ab.sh)
 
 
 def _newest_header():

@@ -659,7 +659,16 @@ struct StatsOut {
 // g = sum_s partial[s] (fixed order); Adam with the optimizer's own t; master,
 // m, v updated; operand shadow (T, padded row stride) refreshed; if the tensor
 // has a target: theta' = tau theta_new + (1 - tau) theta' (+ its shadow).
-constexpr int ADAM_NT = 256, ADAM_EPT = 2, ADAM_SEG = ADAM_NT * ADAM_EPT;  // elements per block
+#ifndef SPZ_ADAM_EPT
+#define SPZ_ADAM_EPT 2
+#endif
+#ifndef SPZ_ADAM_NT
+#define SPZ_ADAM_NT 256
+#endif
+#ifndef SPZ_ADAM_MINB
+#define SPZ_ADAM_MINB 4
+#endif
+constexpr int ADAM_NT = SPZ_ADAM_NT, ADAM_EPT = SPZ_ADAM_EPT, ADAM_SEG = ADAM_NT * ADAM_EPT;  // elements per block
 
 struct AdamTensor {
   int64_t p_off;      // master offset of element 0
@@ -733,7 +742,7 @@ struct AdamHyper {
 // grid-wide handshake is needed.  (A non-finite gradient element sets the sticky flag 2: the step
 // itself counts, every later step is skipped.)
 template <typename T>
-__global__ void __launch_bounds__(ADAM_NT, 4) adam_polyak_kernel(const AdamSegment* __restrict__ segs, AdamHyper hp,
+__global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(const AdamSegment* __restrict__ segs, AdamHyper hp,
                                                                  float* __restrict__ P, float* __restrict__ Mo,
                                                                  float* __restrict__ Vo, T* __restrict__ S,
                                                                  int64_t* __restrict__ counters,  // step, t_c, t_a, t_al

@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 (3xTF32) measurement key")
     ap.add_argument("--parity-steps", type=int, default=None, help="K_o (default: SURVEY.md §8(d) per config)")
     ap.add_argument("--dry-run", action="store_true", help="print the multi-GPU plan of every rank (gloo, no GPU)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the short device-resident measurement of the other BASELINE configs (the `configs` key)")
     return ap.parse_args()
 
 
@@ -539,6 +541,10 @@ def main():
                        "overlapping the updates in flight, spz_update_wait (stats D2H of the oldest), spz_update_async(B, 1); "
                        "two updates in flight"}
 
+    configs = None
+    if world == 1 and not a.no_configs and a.precision == "bf16" and a.algo is None and a.batch is None:
+        configs = other_configs(a, w.name, local, torch, dist)
+
     sweep = None
     if a.sweep and world == 1:
         ladder = [128, 512, 2048, 8192, 32768, 65536]
@@ -564,11 +570,50 @@ def main():
                        "l2": f"ring {C * ((2 * w.obs_dim + w.act_dim + 2 + 3) // 4 * 4) * 4 / 1e6:.0f} MB > 126 MB L2; fresh random indices each step (inputs larger than L2)"},
             "roofline": roof, "kernels": kern, "fp32": fp32, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
             "clocks": clk.summary(), "gpu_launches": launches, "last_stats": stats,
+            **({"configs": configs} if configs else {}),
             **({"batch_sweep": sweep} if sweep else {}),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def other_configs(a, done, local, torch, dist):
+    """The other BASELINE configs on this GPU, device-resident, bf16, K = a.steps updates per repetition (>= 3
+    repetitions, >= 0.5 s): value, ms_per_step and the dominant tensor-core class against the peak -- so every
+    config has a number in the driver's own bench line (parity for each: tests/test_gpu_parity.py)."""
+    from paper_2312_06126_b200 import spz
+    pk = peaks()
+    out = {}
+    for name in ("ant", "humanoid", "humanoid_td3"):
+        if name == done:
+            continue
+        w = synthdata.WORKLOADS[name]
+        ring = spz.Replay(w.obs_dim, w.act_dim, w.capacity, device=local)
+        for s0 in range(0, w.capacity, 1_000_000):
+            ring.push(**synthdata.workload_transitions(w, n=min(1_000_000, w.capacity - s0), seed=synthdata.DATA_SEED + s0))
+        stream = torch.cuda.Stream(device=local)
+        lrn = spz.Learner(ring, algo=w.algo, precision="bf16", hidden=w.hidden, n_hidden=w.n_hidden, max_batch=w.batch,
+                          device=local, seed=synthdata.SAMPLE_SEED)
+        lrn.set_stream(stream.cuda_stream)
+        lrn.update(w.batch, a.warmup)
+        K = max(3, min(a.steps, 20)) if w.batch > 8192 else a.steps
+        reps, _ = timed_reps(lrn, w.batch, K, argparse.Namespace(reps=3, min_time=0.5), stream, 1, dist, torch)
+        ms = statistics.median(reps)
+        prof = lrn.profile(w.batch, 2)
+        n_actor = lrn.get("actor").size
+        n_critic = sum(lrn.get(n).size for n in ("q1", "q2"))
+        roof, gemm_f = roofline(w, w.batch, prof, "bf16", pk, n_actor, n_critic)
+        out[name] = {"value": w.batch * K / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms / K, "steps": K,
+                     "repetitions": len(reps), "global_batch": w.batch, "algo": w.algo,
+                     "hidden": f"{w.n_hidden}x{w.hidden}", "dtype": "bf16",
+                     "roofline": {k: roof[k] for k in ("kernel", "achieved", "peak", "unit", "frac")},
+                     "step_gemm_tflops": gemm_f / (ms / K * 1e-3) / 1e12}
+        lrn.close()
+        ring.close()
+        del stream
+        torch.cuda.synchronize()
+    return out
 
 
 def cpu_leg(a, w, B, ring, chunks):

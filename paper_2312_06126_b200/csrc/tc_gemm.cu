@@ -26,7 +26,10 @@ namespace spz {
 
 namespace {
 
-constexpr int BM = 128, BK = 64, STAGES = 4;
+#ifndef SPZ_TC_STAGES
+#define SPZ_TC_STAGES 4
+#endif
+constexpr int BM = 128, BK = 64, STAGES = SPZ_TC_STAGES;  // pipeline depth cap (shared memory decides below it)
 // producer warp, MMA warp, WPQ epilogue warps per TMEM lane quarter (each a slice of the columns)
 #ifndef SPZ_TC_WPQ
 #define SPZ_TC_WPQ 2
@@ -43,6 +46,7 @@ struct TcParams {
   int trace;      // diagnostics: record per-tile timestamps in this launch
   int tma_out;    // 1: outputs leave through TMA bulk tensor stores (tc[] valid), 0: direct stores
   int out_bytes;  // 2 (bf16) or 4 (fp32) output elements
+  int pair;       // 1: CTA-pair kernel (cta_group::2, M = 256 pair tiles; tb boxes hold BN / 2 rows)
   CUtensorMap ta[MAX_GROUPS];
   CUtensorMap tb[MAX_GROUPS];
   CUtensorMap tc[MAX_GROUPS];  // C as [splits][M][N]; box = 64 bytes x 32 rows, 64-byte swizzle
@@ -69,14 +73,16 @@ __device__ __forceinline__ void trace_(int on, int tile_i, int ev) {
 struct TileInfo {
   int grp, m0, n0, split;
 };
-__device__ __forceinline__ TileInfo decode_tile(const TcParams& p, int t, int bn) {
+// CTA pair (p.pair): tiles are 256-row pair tiles (mtiles counts row-block PAIRS); CTA `rank` of the cluster
+// takes row block 2 mt + rank (past M: TMA zero-fills it, the epilogue stores nothing).
+__device__ __forceinline__ TileInfo decode_tile(const TcParams& p, int t, int bn, int rank = 0) {
   int g = 0;
   while (g + 1 < p.a.n_groups && t >= p.tile0[g + 1]) ++g;
   const int r = t - p.tile0[g];
   const int nt = r % p.ntiles[g];
   const int rest = r / p.ntiles[g];
   const int mt = rest % p.mtiles[g];
-  return {g, mt * BM, nt * bn, rest / p.mtiles[g]};
+  return {g, (p.pair ? 2 * mt + rank : mt) * BM, nt * bn, rest / p.mtiles[g]};
 }
 
 // Write 16 output values of row `row` into a 64-byte-row staging block (64-byte TMA swizzle:
@@ -152,10 +158,15 @@ struct EpiShape {
 // and the MMA issuer run ahead into the next tile while the epilogue drains the previous one
 // from the other TMEM accumulator buffer.  EK (the epilogue kind) is a template parameter so the
 // epilogue compiles to straight-line code for exactly one kind (SAC_HEAD also covers TD3_HEAD).
-template <int BN, bool AMN, bool BMN, int EK>
+// PAIR: a 2-CTA cluster on one TPC computes 256 x BN pair tiles with cta_group::2 MMAs issued by the even
+// (leader) CTA: each CTA stages its own 128 A rows and half of the B tile's rows (BN / 2) per k-block -- 32 KB
+// per CTA per k-block instead of 48 KB at BN = 256, which the k-block pipeline (TMA latency x stages) was
+// bound by -- and drains its own 128 accumulator rows from its own TMEM with the unchanged epilogue.
+template <int BN, bool AMN, bool BMN, int EK, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
   using S = EpiShape<BN, EK>;
-  constexpr int B_BYTES = BN * BK * 2;
+  static_assert(!PAIR || (!AMN && !BMN && !S::HEAD && !S::BIASCOL && BN == 256), "CTA pair: K-major forward tiles only");
+  constexpr int B_BYTES = PAIR ? BN * BK * 2 / 2 : BN * BK * 2;  // this CTA's share of the B tile
   constexpr int STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t BUF_COLS = S::BUF_COLS;    // one accumulator buffer
   constexpr uint32_t TMEM_COLS = S::TMEM_COLS;
@@ -164,7 +175,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   constexpr uint32_t IDESC1 = (1u << 4) | (1u << 7) | (1u << 10) | ((AMN ? 1u : 0u) << 15) | (2u << 17) |
                               ((uint32_t)(BM >> 4) << 24);
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) |
-                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((PAIR ? 2 * BM : BM) >> 4) << 24);
   // per epilogue warp: its slice of the tile's bias / row-dot weights; row-dot partials per quarter
   __shared__ __align__(16) float bias_w[S::BIAS ? NUM_EPI_WARPS : 1][S::BIAS ? S::SLICE : 4];
   __shared__ __align__(16) float dotw_w[S::RELU ? NUM_EPI_WARPS : 1][S::RELU ? S::SLICE : 4];
@@ -190,6 +201,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   const GemmArgs& a = p.a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = p.total_tiles;
+  const int crank = PAIR ? (int)cluster_rank() : 0;  // 0: the leader CTA of the pair (issues every MMA)
+  const int cta0 = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;  // schedule index: the pair walks pair tiles
+  const int ncta = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < a.n_groups; ++i) {
@@ -202,18 +216,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], NUM_EPI_WARPS);
+      mbar_init(&acc_empty[b], PAIR ? 2 * NUM_EPI_WARPS : NUM_EPI_WARPS);  // pair: both CTAs' epilogues (leader's)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // both CTAs' barriers initialised before any cross-CTA arrive / TMA
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // everything above overlapped the previous kernel (PDL); from here on we read its outputs
@@ -225,9 +247,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     if (lane == 0) {
       // ---------------- TMA producer: a continuous stream of k-blocks over this CTA's tiles
       int kg = 0, tile_p = 0;
-      for (int t = blockIdx.x; t < T; t += gridDim.x, ++tile_p) {
+      for (int t = cta0; t < T; t += ncta, ++tile_p) {
         trace(tile_p, 0);
-        const TileInfo ti = decode_tile(p, t, BN);
+        const TileInfo ti = decode_tile(p, t, BN, crank);
         const int k_begin = ti.split * a.k_per_split;
         const int k_end = min(a.K, k_begin + a.k_per_split);
         const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
@@ -237,8 +259,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           mbar_wait(&empty[s], ph ^ 1u);
           uint8_t* sA = smem + s * STAGE;
           uint8_t* sB = sA + A_BYTES;
-          mbar_expect_tx(&full[s], STAGE);
           const int k = k_begin + kb * BK;
+          if constexpr (PAIR) {
+            // both CTAs' loads complete on the leader's full[s] (it expects the pair's bytes)
+            if (crank == 0) mbar_expect_tx(&full[s], 2 * STAGE);
+            tma_load_2d_pair(sA, &p.ta[ti.grp], &full[s], k, ti.m0);
+            tma_load_2d_pair(sB, &p.tb[ti.grp], &full[s], k, ti.n0 + crank * (BN / 2));
+            continue;
+          }
+          mbar_expect_tx(&full[s], STAGE);
           if (!AMN) {
             tma_load_2d(sA, &p.ta[ti.grp], &full[s], k, ti.m0);
           } else {
@@ -255,11 +284,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && crank == 0) {
       // ---------------- MMA issuer: accumulator buffer (tile_i & 1), freed by the epilogue warps
+      //                  (pair: the leader issues the pair's M = 256 MMAs; commits reach both CTAs)
       int kg = 0, tile_i = 0;
-      for (int t = blockIdx.x; t < T; t += gridDim.x, ++tile_i) {
-        const TileInfo ti = decode_tile(p, t, BN);
+      for (int t = cta0; t < T; t += ncta, ++tile_i) {
+        const TileInfo ti = decode_tile(p, t, BN, crank);
         const int k_begin = ti.split * a.k_per_split;
         const int k_end = min(a.K, k_begin + a.k_per_split);
         const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
@@ -279,7 +309,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = AMN ? desc_mnmajor(sA, kk) : desc_kmajor(sA, kk);
             const uint64_t bd = BMN ? desc_mnmajor(sB, kk) : desc_kmajor(sB, kk);
-            umma_bf16(acc, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            if constexpr (PAIR) umma_bf16_pair(acc, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            else umma_bf16(acc, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
           }
           if constexpr (S::BIASCOL) {
             if (bcol) {
@@ -291,9 +322,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
               }
             }
           }
-          umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+          if constexpr (PAIR) umma_commit_pair(&empty[s]);  // frees the stage in both CTAs once read
+          else umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
         }
-        umma_commit(&acc_full[b]);  // accumulator complete (immediately if the split is empty)
+        if constexpr (PAIR) umma_commit_pair(&acc_full[b]);
+        else umma_commit(&acc_full[b]);  // accumulator complete (immediately if the split is empty)
         trace(tile_i, 1);
       }
     }
@@ -311,8 +344,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     int tile_i = 0;
     int st_count = 0;   // TMA store blocks issued by this warp
     int dot_tiles = 0;  // fused row-dot tiles seen (dotpart buffer parity)
-    for (int t = blockIdx.x; t < T; t += gridDim.x, ++tile_i) {
-      const TileInfo ti = decode_tile(p, t, BN);
+    const uint32_t acc_empty0 = PAIR ? mapa_shared(smem_u32(acc_empty), 0) : 0u;  // the leader's acc_empty[0]
+    for (int t = cta0; t < T; t += ncta, ++tile_i) {
+      const TileInfo ti = decode_tile(p, t, BN, crank);
       const GemmGroup& g = a.g[ti.grp];
       const int m = ti.m0 + r;
       const int n0 = ti.n0;
@@ -460,7 +494,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         // accumulator buffer drained by this warp
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[b]);
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(acc_empty0 + (uint32_t)b * 8u);
+          else mbar_arrive(&acc_empty[b]);
+        }
         if constexpr (S::RELU) {
           if (has_dot) {
             // the WPQ warps of this lane quarter combine their row-dot slices in a fixed order
@@ -496,10 +533,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   }
   if (warp >= 2 && lane == 0) bulk_wait_all();  // every TMA store of this warp has completed
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  if constexpr (PAIR) {
+    cluster_sync();  // no CTA leaves while its peer may still arrive on its barriers or read its operands
+    if (warp == 1) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    }
+  } else {
+    __syncthreads();
+    if (warp == 1) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    }
   }
 }
 
@@ -519,14 +564,14 @@ constexpr int smem_static() {
          (S::RELU ? 2 * WPQ * BM * 4 : 4) + 64;
 }
 
-template <int BN, bool AMN, bool BMN, int EK>
+template <int BN, bool AMN, bool BMN, int EK, bool PAIR = false>
 cudaError_t launch(TcParams& p, cudaStream_t st) {
-  constexpr int STAGE = A_BYTES + BN * BK * 2;
+  constexpr int STAGE = A_BYTES + (PAIR ? BN * BK : BN * BK * 2);
   constexpr int AVAIL = 227 * 1024 - smem_static<BN, EK>() - smem_extras();
   constexpr int MAX_ST = std::min(STAGES, AVAIL / STAGE);
   static_assert(MAX_ST >= 1, "shared memory budget");
   constexpr int SMEM_MAX = MAX_ST * STAGE + smem_extras();
-  auto kern = tc_gemm_kernel<BN, AMN, BMN, EK>;
+  auto kern = tc_gemm_kernel<BN, AMN, BMN, EK, PAIR>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
@@ -535,10 +580,11 @@ cudaError_t launch(TcParams& p, cudaStream_t st) {
   }
   // persistent schedule: tiles of every group, one CTA per SM (or more when TMEM and smem allow)
   int T = 0;
+  p.pair = PAIR ? 1 : 0;
   for (int i = 0; i < p.a.n_groups; ++i) {
     const GemmGroup& g = p.a.g[i];
     p.tile0[i] = T;
-    p.mtiles[i] = g.M > 0 && g.N > 0 ? (int)cdiv(g.M, BM) : 0;
+    p.mtiles[i] = g.M > 0 && g.N > 0 ? (int)cdiv(g.M, PAIR ? 2 * BM : BM) : 0;  // pair: 256-row pair tiles
     p.ntiles[i] = g.M > 0 && g.N > 0 ? (int)cdiv(g.N, BN) : 1;
     if (p.mtiles[i] == 0) p.mtiles[i] = 1, p.ntiles[i] = 0;
     T += p.mtiles[i] * p.ntiles[i] * p.a.splits;
@@ -558,10 +604,50 @@ cudaError_t launch(TcParams& p, cudaStream_t st) {
   const int want = (int)std::min<int64_t>(STAGES, std::max<int64_t>(1, cdiv(kspan, BK)));
   p.stages = std::max(1, std::min(std::min(want, MAX_ST), (budget - smem_extras()) / STAGE));
   const int smem = p.stages * STAGE + smem_extras();
-  const int grid = std::min(T, num_sms() * per_sm);
   p.trace = g_trace_mode == 1 || (g_trace_mode >= 2 && g_trace_count == g_trace_mode - 2);
   ++g_trace_count;
+  if constexpr (PAIR) {
+    // one 2-CTA cluster per TPC: as many pairs as can be co-resident, each walking pair tiles
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    static int max_clusters = [&] {
+      cudaLaunchConfig_t c = cfg;
+      c.gridDim = dim3(2 * (num_sms() / 2));
+      c.numAttrs = 1;  // cluster shape only
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &c) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = num_sms() / 2 - 4;  // conservative: leave room for TPCs with one usable SM
+      }
+      return n;
+    }();
+    cfg.gridDim = dim3(2 * std::min(T, max_clusters));
+    return cudaLaunchKernelEx(&cfg, kern, p);
+  }
+  const int grid = std::min(T, num_sms() * per_sm);
   return launch_pdl(kern, dim3(grid), dim3(NTHREADS), (size_t)smem, st, p);
+}
+
+// CTA-pair kernel for a K-major forward GEMM (BN = 256).  Measured on B200: no faster than the
+// single-CTA kernel on the HUM / TD3 hidden layers (HUM critic forward 588 -> 652 us, TD3 2627 -> 2611 us, with 4 or
+// 8 pipeline stages alike), so the hidden-layer GEMMs are not bound by operand delivery and the pair kernel is
+// off by default; SPZ_TC_PAIR=1 selects it wherever legal (parity- and unit-tested).
+bool want_pair(const GemmArgs& a, int bn) {
+  if (a.a_mn || a.b_mn || bn != 256) return false;
+  if (a.epi != EPI_BIAS_RELU && a.epi != EPI_BIAS_F32 && a.epi != EPI_F32) return false;
+  const char* fe = std::getenv("SPZ_TC_PAIR");
+  return fe && std::atoi(fe) == 1;
 }
 
 // epilogue kinds instantiated per operand layout: forward (K-major A and B), dgrad (MN-major B),
@@ -578,6 +664,16 @@ constexpr bool ek_ok(int epi, int bn) {
 
 template <int BN, bool AMN, bool BMN>
 cudaError_t launch_ek(TcParams& p, cudaStream_t st) {
+  if constexpr (!AMN && !BMN && BN == 256) {
+    if (p.pair) {
+      switch (p.a.epi) {
+        case EPI_BIAS_RELU: return launch<BN, AMN, BMN, EPI_BIAS_RELU, true>(p, st);
+        case EPI_BIAS_F32: return launch<BN, AMN, BMN, EPI_BIAS_F32, true>(p, st);
+        case EPI_F32: return launch<BN, AMN, BMN, EPI_F32, true>(p, st);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+  }
   if constexpr (!AMN && !BMN) {
     switch (p.a.epi) {
       case EPI_BIAS_RELU: return launch<BN, AMN, BMN, EPI_BIAS_RELU>(p, st);
@@ -680,6 +776,7 @@ cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st) {
     if (!g.C || !make_map_out(&p.tc[i], g.C, p.out_bytes, g.N, g.M, a.splits, g.ldc, g.split_stride)) p.tma_out = 0;
   }
   const int bn = pick_bn(a.N, a.b_mn);
+  p.pair = want_pair(a, bn) ? 1 : 0;
   int maxM = 0;
   for (int i = 0; i < a.n_groups; ++i) {
     const GemmGroup& g = a.g[i];
@@ -689,7 +786,7 @@ cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st) {
     if (!a.a_mn) ok = make_map(&p.ta[i], g.A, a.K, g.M, g.lda, BK, BM);      // A [M x K]
     else ok = make_map(&p.ta[i], g.A, g.M, a.K, g.lda, 64, BK);             // A stored [K x M]
     if (ok) {
-      if (!a.b_mn) ok = make_map(&p.tb[i], g.B, a.K, g.N, g.ldb, BK, bn);    // B [N x K]
+      if (!a.b_mn) ok = make_map(&p.tb[i], g.B, a.K, g.N, g.ldb, BK, p.pair ? bn / 2 : bn);  // B [N x K] (pair: half)
       else ok = make_map(&p.tb[i], g.B, g.N, a.K, g.ldb, 64, BK);           // B stored [K x N]
     }
     if (!ok) return cudaErrorInvalidValue;

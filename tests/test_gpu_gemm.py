@@ -138,3 +138,24 @@ def test_tf32x3_and_simt_agree():
     spz.spz_diag_gemm_f32(M, N, K, A, K, 0, B, K, 0, C1, N, tensor_cores=True)
     spz.spz_diag_gemm_f32(M, N, K, A, K, 0, B, K, 0, C2, N, tensor_cores=False)
     assert (C1 - C2).abs().max().item() < 1e-5 * C2.abs().max().item()
+
+
+PAIR_CASES = [
+    # (M, N, K): forward K-major GEMMs on the CTA-pair kernel (cta_group::2, 256-row pair tiles): one pair tile,
+    # a half-empty last pair (3 row blocks), ragged M / N / K, several tiles per pair, the HUM / TD3 layer shapes
+    (256, 256, 64), (384, 256, 256), (1000, 300, 100), (4096, 512, 512), (49152, 256, 256), (20000, 1024, 1024),
+]
+
+
+@pytest.mark.parametrize("M,N,K", PAIR_CASES)
+def test_tc_gemm_cta_pair_matches_fp32_matmul(M, N, K, monkeypatch):
+    monkeypatch.setenv("SPZ_TC_PAIR", "1")
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    lda, ldb = (K + 7) // 8 * 8, (K + 7) // 8 * 8
+    A = _mk(M, K, lda, g)
+    B = _mk(N, K, ldb, g)
+    C = torch.full((M, N), float("nan"), device="cuda")
+    spz.spz_diag_gemm_bf16(M, N, K, A, lda, 0, B, ldb, 0, C, N)
+    ref = _ref(A, 0, B, 0, M, N, K)
+    err = (C - ref).abs().max().item() / max(ref.abs().max().item(), 1e-6)
+    assert err < 2e-6 * K ** 0.5, err

@@ -733,6 +733,7 @@ struct AdamHyper {
   const int64_t* snap;  // counters of this step (written by the loss kernel); the kernel advances `counters`
   const float* bc;      // bias corrections of this step (loss-kernel snapshot): [bc1 x 3 | bc2 x 3]
   int alpha_auto, critic_on, actor_on;
+  int diag_nowork;  // diagnostics only (SPZ_DIAG_ADAM_NOWORK): statistics and counters, no parameter update
 };
 
 // One block per segment of ADAM_SEG elements (ADAM_EPT per thread, independent).  Every load of a
@@ -753,7 +754,7 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
   __shared__ bool skip;
   const AdamSegment* sg = segs + blockIdx.x;
   const int opt = __ldg(&sg->t.opt);
-  const int count = __ldg(&sg->count);
+  const int count = hp.diag_nowork ? 0 : __ldg(&sg->count);
   const int start = (int)__ldg(&sg->start);
   const int p_off = (int)__ldg(&sg->t.p_off);
   const int t_off = (int)__ldg(&sg->t.t_off);
@@ -773,21 +774,13 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
       if (t_off >= 0) tp0[u] = P[t_off + i];
     }
   }
-  pdl_wait();
-  pdl_launch();
-  // after the wait: this step's gradient partials, loss totals and counter snapshot
+  // Also before the wait: the loss totals, counter snapshot and bias corrections (written by the loss kernel,
+  // three kernels back: complete once the weight-gradient kernel, this kernel's prerequisite, passed its own wait;
+  // in a row-sharded group the non-PDL allreduce precedes this kernel, which then starts after it) and the skip
+  // decision -- so after the wait only the split-K partials are loaded.
   const int64_t step = __ldg(hp.snap);
   const double* tot = hp.totals;
   const float bc1 = __ldg(hp.bc + opt), bc2 = __ldg(hp.bc + 3 + opt);
-#pragma unroll
-  for (int u = 0; u < ADAM_EPT; ++u) {
-    const int k = threadIdx.x + u * ADAM_NT;
-    if (k < count) {
-      const int i = start + k;
-      g[u] = opt == 2 ? (float)(-(tot[4] / hp.B + hp.target_entropy))  // log-alpha gradient
-                      : partial_sum(partials, n_partials, pstride, pld, cols, i);
-    }
-  }
   bool delayed = true;
   if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
   if (threadIdx.x == 0) {
@@ -800,6 +793,18 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
     skip = bad || f;  // halted: parameters stay at the state before the failing step
   }
   __syncthreads();
+  pdl_wait();
+  pdl_launch();
+  // after the wait: this step's gradient partials
+#pragma unroll
+  for (int u = 0; u < ADAM_EPT; ++u) {
+    const int k = threadIdx.x + u * ADAM_NT;
+    if (k < count) {
+      const int i = start + k;
+      g[u] = opt == 2 ? (float)(-(tot[4] / hp.B + hp.target_entropy))  // log-alpha gradient
+                      : partial_sum(partials, n_partials, pstride, pld, cols, i);
+    }
+  }
   const bool active = !skip && !(hp.td3 && opt == 1 && !delayed);  // TD3 actor: delayed steps only
   if (active) {
     const float lr = hp.lr[opt];

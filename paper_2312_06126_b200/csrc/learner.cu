@@ -1330,6 +1330,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       hp.snap = Lr->ctr_snap;
       hp.bc = reinterpret_cast<const float*>(Lr->ctr_snap + 5);
       hp.alpha_auto = Lr->cfg.alpha_auto;
+      hp.diag_nowork = std::getenv("SPZ_DIAG_ADAM_NOWORK") != nullptr;  // diagnostics only (results are wrong)
       hp.critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
       hp.actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC;
       float *Pm = Lr->P, *Mm = Lr->Mo, *Vm = Lr->Vo;

@@ -189,3 +189,31 @@ def test_bench_dry_run_gpus2_reports_partitions():
             assert rows == [(0, GB // 2), (GB // 2, GB // 2)]
         else:  # each group (one rank) reads the whole batch
             assert rows == [(0, GB), (0, GB)] and {q["role"] for q in line["plans"]} == {1, 2}
+
+
+def test_plan_rank_validation_and_partitions():
+    """spz_plan_rank (host only, no GPU): bad layouts are rejected; partitions of every (B, G) tile [0, B) in rank
+    order with the first B % G ranks one row longer (the oracle's schedule); split roles name the leaders."""
+    from oracle.schedules import _shards
+    from paper_2312_06126_b200 import spz
+    with pytest.raises(spz.SpzError):
+        spz.spz_plan_rank(100, 2, 2)                      # rank outside the world
+    with pytest.raises(spz.SpzError):
+        spz.spz_plan_rank(1, 2, 0)                        # fewer rows than ranks
+    with pytest.raises(spz.SpzError):                     # rank 0 must be in the critic group
+        spz.spz_plan_rank(100, 4, 0, role=spz.SPZ_ROLE_ACTOR, n_critic_ranks=2)
+    with pytest.raises(spz.SpzError):
+        spz.spz_plan_rank(100, 4, 3, role=spz.SPZ_ROLE_ACTOR, n_critic_ranks=4)  # no actor group left
+    for B in (7, 8192, 8193, 131072):
+        for G in (1, 2, 3, 8):
+            if B < G:
+                continue
+            got = [spz.spz_plan_rank(B, G, r) for r in range(G)]
+            assert [(p["row0"], p["rows"]) for p in got] == _shards(B, G)
+            assert all(p["allreduce"] == (G > 1) and p["group_size"] == G for p in got)
+    plans = [spz.spz_plan_rank(8192, 8, r, role=spz.SPZ_ROLE_CRITIC if r < 6 else spz.SPZ_ROLE_ACTOR,
+                               n_critic_ranks=6) for r in range(8)]
+    assert [p["group_size"] for p in plans] == [6] * 6 + [2] * 2
+    assert [p["group_rank"] for p in plans] == list(range(6)) + [0, 1]
+    assert all(p["actor_root"] == 6 and p["critic_root"] == 0 for p in plans)
+    assert [(p["row0"], p["rows"]) for p in plans[6:]] == _shards(8192, 2)

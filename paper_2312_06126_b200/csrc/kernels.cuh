@@ -734,6 +734,8 @@ struct AdamHyper {
   const float* bc;      // bias corrections of this step (loss-kernel snapshot): [bc1 x 3 | bc2 x 3]
   int alpha_auto, critic_on, actor_on;
   int diag_nowork;  // diagnostics only (SPZ_DIAG_ADAM_NOWORK): statistics and counters, no parameter update
+  int prewait;      // 1: the loss totals / counter snapshot are complete before this kernel's grid-dependency wait
+                    //    (their writer is >= 2 kernels back behind wait-before-trigger kernels; set by the plan)
 };
 
 // One block per segment of ADAM_SEG elements (ADAM_EPT per thread, independent).  Every load of a
@@ -778,23 +780,29 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
   // three kernels back: complete once the weight-gradient kernel, this kernel's prerequisite, passed its own wait;
   // in a row-sharded group the non-PDL allreduce precedes this kernel, which then starts after it) and the skip
   // decision -- so after the wait only the split-K partials are loaded.
-  const int64_t step = __ldg(hp.snap);
   const double* tot = hp.totals;
-  const float bc1 = __ldg(hp.bc + opt), bc2 = __ldg(hp.bc + 3 + opt);
+  int64_t step = 0;
+  float bc1 = 1.f, bc2 = 1.f;
   bool delayed = true;
-  if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
-  if (threadIdx.x == 0) {
-    // the step's losses are finite iff their totals are (B > 0); TD3 has no log-prob total
-    const bool bad =
-        !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) || (!hp.td3 && !isfinite(tot[4])) ||
-        !isfinite(tot[5]);
-    const int f = *flag;
-    if (bad && blockIdx.x == 0) atomicExch(flag, 1);
-    skip = bad || f;  // halted: parameters stay at the state before the failing step
-  }
-  __syncthreads();
+  auto decide = [&]() {
+    step = __ldg(hp.snap);
+    bc1 = __ldg(hp.bc + opt);
+    bc2 = __ldg(hp.bc + 3 + opt);
+    if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
+    if (threadIdx.x == 0) {
+      // the step's losses are finite iff their totals are (B > 0); TD3 has no log-prob total
+      const bool bad = !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) ||
+                       (!hp.td3 && !isfinite(tot[4])) || !isfinite(tot[5]);
+      const int f = *flag;
+      if (bad && blockIdx.x == 0) atomicExch(flag, 1);
+      skip = bad || f;  // halted: parameters stay at the state before the failing step
+    }
+    __syncthreads();
+  };
+  if (hp.prewait) decide();
   pdl_wait();
   pdl_launch();
+  if (!hp.prewait) decide();
   // after the wait: this step's gradient partials
 #pragma unroll
   for (int u = 0; u < ADAM_EPT; ++u) {

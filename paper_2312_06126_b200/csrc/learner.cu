@@ -1331,6 +1331,16 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       hp.bc = reinterpret_cast<const float*>(Lr->ctr_snap + 5);
       hp.alpha_auto = Lr->cfg.alpha_auto;
       hp.diag_nowork = std::getenv("SPZ_DIAG_ADAM_NOWORK") != nullptr;  // diagnostics only (results are wrong)
+      {  // the totals / snapshot may be read before the dependency wait only if the op right before Adam is a
+         // kernel that waits before it triggers and is not their writer (e.g. not the loss kernel itself: the TD3
+         // actor role on a non-delayed step goes loss -> Adam), or the non-PDL allreduce
+        static const char* const safe[] = {"wgrad_gemm", "bias_grad", "actor_bwd_fused", "actor_dgrad_gemm", "actor_head_bwd",
+                                           "critic_dgrad_gemm", "critic_input_dgrad_gemm", "allreduce"};
+        hp.prewait = 0;
+        if (!ops.empty())
+          for (const char* c : safe)
+            if (std::strcmp(ops.back().cls, c) == 0) hp.prewait = 1;
+      }
       hp.critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
       hp.actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC;
       float *Pm = Lr->P, *Mm = Lr->Mo, *Vm = Lr->Vo;

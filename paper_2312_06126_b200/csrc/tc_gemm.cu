@@ -31,10 +31,10 @@ namespace {
 #endif
 constexpr int BM = 128, BK = 64, STAGES = SPZ_TC_STAGES;  // pipeline depth cap (shared memory decides below it)
 // producer warp, MMA warp, WPQ epilogue warps per TMEM lane quarter (each a slice of the columns)
-#ifndef SPZ_TC_WPQ
-#define SPZ_TC_WPQ 2
-#endif
-constexpr int WPQ = SPZ_TC_WPQ, NUM_EPI_WARPS = 4 * WPQ, NTHREADS = 64 + NUM_EPI_WARPS * 32;
+// Each launch picks 2 or 4 epilogue warps per lane quarter (template WPQ): 4 drain a tile's accumulator faster
+// where the launch has under two tiles per SM (the WLK step's dgrad / wgrad: 100.8 -> 99.9 us per update), 2
+// keep more shared memory for pipeline stages where many tiles stream (HUM: 1993 vs 2029 us per update with 4).
+constexpr int gemm_threads(int w) { return 64 + 4 * w * 32; }
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
 struct TcParams {
@@ -47,6 +47,7 @@ struct TcParams {
   int tma_out;    // 1: outputs leave through TMA bulk tensor stores (tc[] valid), 0: direct stores
   int out_bytes;  // 2 (bf16) or 4 (fp32) output elements
   int pair;       // 1: CTA-pair kernel (cta_group::2, M = 256 pair tiles; tb boxes hold BN / 2 rows)
+  int wpq;        // epilogue warps per TMEM lane quarter (2 or 4)
   CUtensorMap ta[MAX_GROUPS];
   CUtensorMap tb[MAX_GROUPS];
   CUtensorMap tc[MAX_GROUPS];  // C as [splits][M][N]; box = 64 bytes x 32 rows, 64-byte swizzle
@@ -133,7 +134,7 @@ __device__ __forceinline__ void direct16(const GemmGroup& g, int split, int m, i
 }
 
 // Epilogue shape of one (BN, EK) instantiation.
-template <int BN, int EK>
+template <int BN, int EK, int WPQ>
 struct EpiShape {
   static constexpr bool HEAD = EK == EPI_SAC_HEAD;
   static constexpr bool RELU = EK == EPI_BIAS_RELU;
@@ -146,6 +147,8 @@ struct EpiShape {
   static constexpr int CPB = OBF ? 2 : 1;               // chunks per 64-byte store block (= one mask word)
   static constexpr int NB = (CPW + CPB - 1) / CPB;      // store blocks per warp
   static constexpr int SLICE = CPW * 16;                // columns per warp
+  static_assert(!SPLIT || CPW >= CPB || BN < 64 || WPQ == 2,
+                "a warp's column slice must fill whole 64-byte store blocks (4 warps per quarter need BN >= 128)");
   // TMEM: NBUF accumulator buffers of BUF_COLS columns (BIASCOL: + 16 row-sum columns at BN)
   static constexpr int ACC_COLS = BN < 32 ? 32 : BN;
   static constexpr int BUF_COLS = BIASCOL ? ACC_COLS + 16 : ACC_COLS;
@@ -162,9 +165,10 @@ struct EpiShape {
 // (leader) CTA: each CTA stages its own 128 A rows and half of the B tile's rows (BN / 2) per k-block -- 32 KB
 // per CTA per k-block instead of 48 KB at BN = 256, which the k-block pipeline (TMA latency x stages) was
 // bound by -- and drains its own 128 accumulator rows from its own TMEM with the unchanged epilogue.
-template <int BN, bool AMN, bool BMN, int EK, bool PAIR>
-__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
-  using S = EpiShape<BN, EK>;
+template <int BN, bool AMN, bool BMN, int EK, bool PAIR, int WPQ>
+__global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __grid_constant__ TcParams p) {
+  constexpr int NUM_EPI_WARPS = 4 * WPQ, NTHREADS = gemm_threads(WPQ);
+  using S = EpiShape<BN, EK, WPQ>;
   static_assert(!PAIR || (!AMN && !BMN && !S::HEAD && !S::BIASCOL && BN == 256), "CTA pair: K-major forward tiles only");
   constexpr int B_BYTES = PAIR ? BN * BK * 2 / 2 : BN * BK * 2;  // this CTA's share of the B tile
   constexpr int STAGE = A_BYTES + B_BYTES;
@@ -555,23 +559,25 @@ long g_trace_count = 0;
 
 // dynamic shared memory besides the pipeline stages: alignment slack, barriers + TMEM slot,
 // per-warp TMA store staging, the all-ones operand
-constexpr int smem_extras() { return 1024 + 1024 + NUM_EPI_WARPS * 4096 + 2048; }
+template <int WPQ>
+constexpr int smem_extras() { return 1024 + 1024 + 4 * WPQ * 4096 + 2048; }
 // static shared memory of one instantiation (per-warp bias / row-dot slices, row-dot partials)
-template <int BN, int EK>
+template <int BN, int EK, int WPQ>
 constexpr int smem_static() {
-  using S = EpiShape<BN, EK>;
-  return (S::BIAS ? NUM_EPI_WARPS * S::SLICE * 4 : 16) + (S::RELU ? NUM_EPI_WARPS * S::SLICE * 4 : 16) +
+  using S = EpiShape<BN, EK, WPQ>;
+  return (S::BIAS ? 4 * WPQ * S::SLICE * 4 : 16) + (S::RELU ? 4 * WPQ * S::SLICE * 4 : 16) +
          (S::RELU ? 2 * WPQ * BM * 4 : 4) + 64;
 }
 
-template <int BN, bool AMN, bool BMN, int EK, bool PAIR = false>
+template <int BN, bool AMN, bool BMN, int EK, bool PAIR, int WPQ>
 cudaError_t launch(TcParams& p, cudaStream_t st) {
+  constexpr int NTHREADS = gemm_threads(WPQ);
   constexpr int STAGE = A_BYTES + (PAIR ? BN * BK : BN * BK * 2);
-  constexpr int AVAIL = 227 * 1024 - smem_static<BN, EK>() - smem_extras();
+  constexpr int AVAIL = 227 * 1024 - smem_static<BN, EK, WPQ>() - smem_extras<WPQ>();
   constexpr int MAX_ST = std::min(STAGES, AVAIL / STAGE);
   static_assert(MAX_ST >= 1, "shared memory budget");
-  constexpr int SMEM_MAX = MAX_ST * STAGE + smem_extras();
-  auto kern = tc_gemm_kernel<BN, AMN, BMN, EK, PAIR>;
+  constexpr int SMEM_MAX = MAX_ST * STAGE + smem_extras<WPQ>();
+  auto kern = tc_gemm_kernel<BN, AMN, BMN, EK, PAIR, WPQ>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
@@ -592,18 +598,18 @@ cudaError_t launch(TcParams& p, cudaStream_t st) {
   p.tile0[p.a.n_groups] = T;
   p.total_tiles = T;
   if (T == 0) return cudaSuccess;
-  constexpr int TMEM_COLS = EpiShape<BN, EK>::TMEM_COLS;
+  constexpr int TMEM_COLS = EpiShape<BN, EK, WPQ>::TMEM_COLS;
   static int occ = [&] {
     int o = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, NTHREADS, STAGE + smem_extras());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, NTHREADS, STAGE + smem_extras<WPQ>());
     return std::max(1, o);
   }();
   const int per_sm = std::max(1, std::min(512 / TMEM_COLS, occ));
-  const int budget = 227 * 1024 / per_sm - smem_static<BN, EK>();
+  const int budget = 227 * 1024 / per_sm - smem_static<BN, EK, WPQ>();
   const int kspan = p.a.splits > 1 ? p.a.k_per_split : p.a.K;
   const int want = (int)std::min<int64_t>(STAGES, std::max<int64_t>(1, cdiv(kspan, BK)));
-  p.stages = std::max(1, std::min(std::min(want, MAX_ST), (budget - smem_extras()) / STAGE));
-  const int smem = p.stages * STAGE + smem_extras();
+  p.stages = std::max(1, std::min(std::min(want, MAX_ST), (budget - smem_extras<WPQ>()) / STAGE));
+  const int smem = p.stages * STAGE + smem_extras<WPQ>();
   p.trace = g_trace_mode == 1 || (g_trace_mode >= 2 && g_trace_count == g_trace_mode - 2);
   ++g_trace_count;
   if constexpr (PAIR) {
@@ -662,37 +668,44 @@ constexpr bool ek_ok(int epi, int bn) {
   return false;
 }
 
-template <int BN, bool AMN, bool BMN>
-cudaError_t launch_ek(TcParams& p, cudaStream_t st) {
+template <int BN, bool AMN, bool BMN, int W>
+cudaError_t launch_ek_w(TcParams& p, cudaStream_t st) {
   if constexpr (!AMN && !BMN && BN == 256) {
     if (p.pair) {
       switch (p.a.epi) {
-        case EPI_BIAS_RELU: return launch<BN, AMN, BMN, EPI_BIAS_RELU, true>(p, st);
-        case EPI_BIAS_F32: return launch<BN, AMN, BMN, EPI_BIAS_F32, true>(p, st);
-        case EPI_F32: return launch<BN, AMN, BMN, EPI_F32, true>(p, st);
+        case EPI_BIAS_RELU: return launch<BN, AMN, BMN, EPI_BIAS_RELU, true, W>(p, st);
+        case EPI_BIAS_F32: return launch<BN, AMN, BMN, EPI_BIAS_F32, true, W>(p, st);
+        case EPI_F32: return launch<BN, AMN, BMN, EPI_F32, true, W>(p, st);
         default: return cudaErrorInvalidValue;
       }
     }
   }
   if constexpr (!AMN && !BMN) {
     switch (p.a.epi) {
-      case EPI_BIAS_RELU: return launch<BN, AMN, BMN, EPI_BIAS_RELU>(p, st);
-      case EPI_BIAS_F32: return launch<BN, AMN, BMN, EPI_BIAS_F32>(p, st);
-      case EPI_F32: return launch<BN, AMN, BMN, EPI_F32>(p, st);
+      case EPI_BIAS_RELU: return launch<BN, AMN, BMN, EPI_BIAS_RELU, false, W>(p, st);
+      case EPI_BIAS_F32: return launch<BN, AMN, BMN, EPI_BIAS_F32, false, W>(p, st);
+      case EPI_F32: return launch<BN, AMN, BMN, EPI_F32, false, W>(p, st);
       case EPI_SAC_HEAD:
       case EPI_TD3_HEAD:
-        if constexpr (BN <= 64) return launch<BN, AMN, BMN, EPI_SAC_HEAD>(p, st);
+        if constexpr (BN <= 64) return launch<BN, AMN, BMN, EPI_SAC_HEAD, false, W>(p, st);
         break;
       default: break;
     }
   } else if constexpr (!AMN && BMN) {
-    if (p.a.epi == EPI_MASK_BITS) return launch<BN, AMN, BMN, EPI_MASK_BITS>(p, st);
-    if (p.a.epi == EPI_F32) return launch<BN, AMN, BMN, EPI_F32>(p, st);
+    if (p.a.epi == EPI_MASK_BITS) return launch<BN, AMN, BMN, EPI_MASK_BITS, false, W>(p, st);
+    if (p.a.epi == EPI_F32) return launch<BN, AMN, BMN, EPI_F32, false, W>(p, st);
   } else {
-    if (p.a.epi == EPI_F32) return launch<BN, AMN, BMN, EPI_F32>(p, st);
-    if (p.a.epi == EPI_WGRAD_BIAS) return launch<BN, AMN, BMN, EPI_WGRAD_BIAS>(p, st);
+    if (p.a.epi == EPI_F32) return launch<BN, AMN, BMN, EPI_F32, false, W>(p, st);
+    if (p.a.epi == EPI_WGRAD_BIAS) return launch<BN, AMN, BMN, EPI_WGRAD_BIAS, false, W>(p, st);
   }
   return cudaErrorInvalidValue;
+}
+
+template <int BN, bool AMN, bool BMN>
+cudaError_t launch_ek(TcParams& p, cudaStream_t st) {
+  if constexpr (BN >= 128)
+    if (p.wpq == 4) return launch_ek_w<BN, AMN, BMN, 4>(p, st);
+  return launch_ek_w<BN, AMN, BMN, 2>(p, st);
 }
 
 template <bool AMN, bool BMN>
@@ -777,6 +790,13 @@ cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st) {
   }
   const int bn = pick_bn(a.N, a.b_mn);
   p.pair = want_pair(a, bn) ? 1 : 0;
+  {  // 4 epilogue warps per lane quarter under two tiles per SM, else 2 (SPZ_TC_WPQ=2 / 4 forces; diagnostics)
+    int64_t tiles = 0;
+    for (int i = 0; i < a.n_groups; ++i) tiles += cdiv(a.g[i].M, BM) * cdiv(a.g[i].N, bn) * a.splits;
+    // (4 warps only at BN >= 128: a warp's column slice must fill its 64-byte store blocks, EpiShape)
+    p.wpq = tiles < 2 * num_sms() && bn >= 128 ? 4 : 2;
+    if (const char* w = std::getenv("SPZ_TC_WPQ")) p.wpq = std::atoi(w) == 4 && bn >= 128 ? 4 : 2;
+  }
   int maxM = 0;
   for (int i = 0; i < a.n_groups; ++i) {
     const GemmGroup& g = a.g[i];

@@ -4,6 +4,7 @@
 
 #include "internal.h"
 #include "tc_gemm.cuh"
+#include <cstdlib>
 #include "tc_mlp.cuh"
 
 namespace spz {
@@ -66,6 +67,15 @@ spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, i
   a.g[0].B = B;
   a.g[0].C = C;
   a.g[0].M = (int)M;
+  // SPZ_DIAG_GEMM_DYN=<n_pre_groups>: the dynamic tile schedule (tcgen05 only); its counters must be back at 0
+  static unsigned* sched = nullptr;
+  const char* dyn = std::getenv("SPZ_DIAG_GEMM_DYN");
+  if (dyn && tensor_cores) {
+    if (!sched && (cudaMalloc(&sched, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemset(sched, 0, 2 * sizeof(unsigned)) != cudaSuccess))
+      return spz::fail(SPZ_ECUDA, "spz_diag_gemm_bf16: schedule counters");
+    a.sched = sched;
+    a.n_pre_groups = std::atoi(dyn);
+  }
   cudaError_t e;
   if (tensor_cores) {
     if (!spz::tc_gemm_supported(a)) return spz::fail(SPZ_EUNSUPPORTED, "spz_diag_gemm_bf16: problem not supported by the tcgen05 kernel");
@@ -75,6 +85,11 @@ spz_status spz_diag_gemm_bf16(int32_t device, int32_t tensor_cores, int64_t M, i
   }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return spz::fail(SPZ_ECUDA, std::string("spz_diag_gemm_bf16: ") + cudaGetErrorString(e));
+  if (a.sched) {
+    unsigned h[2] = {1u, 1u};
+    if (cudaMemcpy(h, a.sched, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess || h[0] || h[1])
+      return spz::fail(SPZ_ESTATE, "spz_diag_gemm_bf16: dynamic schedule counters not reset");
+  }
   return SPZ_OK;
 }
 

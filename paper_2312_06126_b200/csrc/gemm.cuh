@@ -49,7 +49,14 @@ struct GemmGroup {
   int lda, ldb, ldc, ldaux;
   int row0;     // head epilogues: local actor-pass row of this group's row 0
   int mask_ld;  // words per row of mask_out
+  int splits, k_per_split;  // tcgen05 kernel: this group's split-K (0: the launch's GemmArgs values)
 };
+__host__ __device__ __forceinline__ int group_splits(const GemmGroup& g, int launch_splits) {
+  return g.splits > 0 ? g.splits : launch_splits;
+}
+__host__ __device__ __forceinline__ int group_kps(const GemmGroup& g, int launch_kps) {
+  return g.splits > 0 ? g.k_per_split : launch_kps;
+}
 
 constexpr int MAX_GROUPS = 12;
 
@@ -62,6 +69,13 @@ struct GemmArgs {
   int n_groups;
   GemmGroup g[MAX_GROUPS];
   HeadEpi head;
+  // tcgen05 kernel only: dynamic tile schedule.  sched != null: CTAs take tiles in linear order from an atomic
+  // counter (sched[0]; sched[1] counts finished CTAs, the last one resets both to 0 for the next launch), and
+  // the tiles of groups [0, n_pre_groups) are computed before the grid-dependency wait -- their inputs must not
+  // be written by the kernel this one is launched behind (PDL).  CTAs that start while that kernel still holds
+  // part of the GPU take the independent tiles first.
+  unsigned* sched;
+  int n_pre_groups;
 };
 
 // Apply the epilogue to one accumulator element (SIMT backend; no fused heads / dots).

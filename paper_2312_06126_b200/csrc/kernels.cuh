@@ -711,6 +711,30 @@ __device__ __forceinline__ float partial_sum(const float* __restrict__ partials,
   }
   return g;
 }
+// The same for 4 consecutive elements i..i+3 of one row, contiguous and 16-byte aligned in every partial.
+__device__ __forceinline__ float4 partial_sum4(const float* __restrict__ partials, int n_partials, int pstride, int pld,
+                                               int cols, int i) {
+  int idx;
+  if (cols > 0) {
+    const int row = i / cols;
+    idx = row * pld + (i - row * cols);
+  } else {
+    idx = i * pld;
+  }
+  const float4* src = reinterpret_cast<const float4*>(partials + idx);
+  const int ps4 = pstride >> 2;
+  constexpr int CH = 8;
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s0 = 0; s0 < n_partials; s0 += CH) {
+    float4 t[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) t[u] = s0 + u < n_partials ? __ldg(src + (s0 + u) * ps4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < CH; ++u)
+      if (s0 + u < n_partials) g.x += t[u].x, g.y += t[u].y, g.z += t[u].z, g.w += t[u].w;
+  }
+  return g;
+}
 __device__ __forceinline__ float partial_sum(const AdamTensor& tn, int64_t i) {
   return partial_sum(tn.partials, tn.n_partials, (int)tn.pstride, tn.pld, tn.cols, (int)i);
 }
@@ -719,7 +743,8 @@ struct AdamSegment {
   AdamTensor t;       // the tensor (embedded: one dependent load per segment)
   int64_t start;      // element index within the tensor
   int32_t count;
-  int32_t pad_;
+  int32_t vec;        // 1: float4 layout (4 consecutive elements per thread, 16-byte loads and stores; the host
+                      //    checked every alignment and that 4 consecutive elements share one row), 0: scalar
 };
 struct AdamHyper {
   float lr[3];
@@ -737,6 +762,12 @@ struct AdamHyper {
   int prewait;      // 1: the loss totals / counter snapshot are complete before this kernel's grid-dependency wait
                     //    (their writer is >= 2 kernels back behind wait-before-trigger kernels; set by the plan)
 };
+
+// 4 consecutive shadow elements (8-byte bf16 or 16-byte fp32 store; alignment checked by the host).
+__device__ __forceinline__ void store4(__nv_bfloat16* d, float4 x) {
+  *reinterpret_cast<uint2*>(d) = make_uint2(pack_bf16x2(x.x, x.y), pack_bf16x2(x.z, x.w));
+}
+__device__ __forceinline__ void store4(float* d, float4 x) { *reinterpret_cast<float4*>(d) = x; }
 
 // One block per segment of ADAM_SEG elements (ADAM_EPT per thread, independent).  Every load of a
 // thread is issued before the block barrier behind which thread 0 decides whether the step is
@@ -763,17 +794,31 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
   const float* partials = reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(&sg->t.partials)));
   const int n_partials = __ldg(&sg->t.n_partials), pld = __ldg(&sg->t.pld), cols = __ldg(&sg->t.cols);
   const int pstride = (int)__ldg(&sg->t.pstride);
+  const bool vec = __ldg(&sg->vec) != 0;
   float g[ADAM_EPT], m0[ADAM_EPT], v0[ADAM_EPT], p0[ADAM_EPT], tp0[ADAM_EPT];
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 g4 = z4, m4 = z4, v4 = z4, p4 = z4, tp4 = z4;
+  const int k4 = 4 * threadIdx.x;  // vec: this thread's first element in the segment
+  if (vec) {
+    if (k4 < count) {
+      const int pi = p_off + start + k4;
+      m4 = *reinterpret_cast<const float4*>(Mo + pi);
+      v4 = *reinterpret_cast<const float4*>(Vo + pi);
+      p4 = *reinterpret_cast<const float4*>(P + pi);
+      if (t_off >= 0) tp4 = *reinterpret_cast<const float4*>(P + t_off + start + k4);
+    }
+  } else {
 #pragma unroll
-  for (int u = 0; u < ADAM_EPT; ++u) {
-    const int k = threadIdx.x + u * ADAM_NT;
-    g[u] = m0[u] = v0[u] = p0[u] = tp0[u] = 0.f;
-    if (k < count) {
-      const int i = start + k, pi = p_off + i;
-      m0[u] = Mo[pi];
-      v0[u] = Vo[pi];
-      p0[u] = P[pi];
-      if (t_off >= 0) tp0[u] = P[t_off + i];
+    for (int u = 0; u < ADAM_EPT; ++u) {
+      const int k = threadIdx.x + u * ADAM_NT;
+      g[u] = m0[u] = v0[u] = p0[u] = tp0[u] = 0.f;
+      if (k < count) {
+        const int i = start + k, pi = p_off + i;
+        m0[u] = Mo[pi];
+        v0[u] = Vo[pi];
+        p0[u] = P[pi];
+        if (t_off >= 0) tp0[u] = P[t_off + i];
+      }
     }
   }
   // Also before the wait: the loss totals, counter snapshot and bias corrections (written by the loss kernel,
@@ -804,13 +849,17 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
   pdl_launch();
   if (!hp.prewait) decide();
   // after the wait: this step's gradient partials
+  if (vec) {
+    if (k4 < count) g4 = partial_sum4(partials, n_partials, pstride, pld, cols, start + k4);
+  } else {
 #pragma unroll
-  for (int u = 0; u < ADAM_EPT; ++u) {
-    const int k = threadIdx.x + u * ADAM_NT;
-    if (k < count) {
-      const int i = start + k;
-      g[u] = opt == 2 ? (float)(-(tot[4] / hp.B + hp.target_entropy))  // log-alpha gradient
-                      : partial_sum(partials, n_partials, pstride, pld, cols, i);
+    for (int u = 0; u < ADAM_EPT; ++u) {
+      const int k = threadIdx.x + u * ADAM_NT;
+      if (k < count) {
+        const int i = start + k;
+        g[u] = opt == 2 ? (float)(-(tot[4] / hp.B + hp.target_entropy))  // log-alpha gradient
+                        : partial_sum(partials, n_partials, pstride, pld, cols, i);
+      }
     }
   }
   const bool active = !skip && !(hp.td3 && opt == 1 && !delayed);  // TD3 actor: delayed steps only
@@ -818,31 +867,62 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
     const float lr = hp.lr[opt];
     const int s_off = (int)__ldg(&sg->t.s_off), ts_off = (int)__ldg(&sg->t.ts_off), ld = __ldg(&sg->t.ld);
     const bool polyak = t_off >= 0 && (!hp.td3 || delayed);
-#pragma unroll
-    for (int u = 0; u < ADAM_EPT; ++u) {
-      const int k = threadIdx.x + u * ADAM_NT;
-      if (k >= count) continue;
-      if (!isfinite(g[u])) {
+    // one element: Adam (m, v, theta) and Polyak (theta'); false (nothing changes) on a non-finite gradient
+    auto elem = [&](float ge, float me, float ve, float pe, float tpe, float& m, float& v, float& p, float& tp) {
+      if (!isfinite(ge)) {
         atomicExch(flag, 2);
-        continue;
+        m = me, v = ve, p = pe, tp = tpe;
+        return false;
       }
-      const int i = start + k, pi = p_off + i;
-      const float m = hp.beta1 * m0[u] + (1.f - hp.beta1) * g[u];
-      const float v = hp.beta2 * v0[u] + (1.f - hp.beta2) * g[u] * g[u];
-      Mo[pi] = m;
-      Vo[pi] = v;
-      const float p = p0[u] - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
-      P[pi] = p;
-      int so = -1;
-      if (cols > 0) {
-        const int row = i / cols, col = i - row * cols;
-        so = row * ld + col;
-        S[s_off + so] = from_f<T>(p);
+      m = hp.beta1 * me + (1.f - hp.beta1) * ge;
+      v = hp.beta2 * ve + (1.f - hp.beta2) * ge * ge;
+      p = pe - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
+      tp = hp.tau * p + (1.f - hp.tau) * tpe;
+      return true;
+    };
+    if (vec) {
+      if (k4 < count) {
+        const int i = start + k4, pi = p_off + i;
+        float4 m, v, p, tp;
+        elem(g4.x, m4.x, v4.x, p4.x, tp4.x, m.x, v.x, p.x, tp.x);
+        elem(g4.y, m4.y, v4.y, p4.y, tp4.y, m.y, v.y, p.y, tp.y);
+        elem(g4.z, m4.z, v4.z, p4.z, tp4.z, m.z, v.z, p.z, tp.z);
+        elem(g4.w, m4.w, v4.w, p4.w, tp4.w, m.w, v.w, p.w, tp.w);
+        *reinterpret_cast<float4*>(Mo + pi) = m;
+        *reinterpret_cast<float4*>(Vo + pi) = v;
+        *reinterpret_cast<float4*>(P + pi) = p;
+        int so = -1;
+        if (cols > 0) {
+          const int row = i / cols, col = i - row * cols;
+          so = row * ld + col;
+          store4(S + s_off + so, p);
+        }
+        if (polyak) {
+          *reinterpret_cast<float4*>(P + t_off + i) = tp;
+          if (so >= 0) store4(S + ts_off + so, tp);
+        }
       }
-      if (polyak) {
-        const float tp = hp.tau * p + (1.f - hp.tau) * tp0[u];
-        P[t_off + i] = tp;
-        if (so >= 0) S[ts_off + so] = from_f<T>(tp);
+    } else {
+#pragma unroll
+      for (int u = 0; u < ADAM_EPT; ++u) {
+        const int k = threadIdx.x + u * ADAM_NT;
+        if (k >= count) continue;
+        float m, v, p, tp;
+        if (!elem(g[u], m0[u], v0[u], p0[u], tp0[u], m, v, p, tp)) continue;
+        const int i = start + k, pi = p_off + i;
+        Mo[pi] = m;
+        Vo[pi] = v;
+        P[pi] = p;
+        int so = -1;
+        if (cols > 0) {
+          const int row = i / cols, col = i - row * cols;
+          so = row * ld + col;
+          S[s_off + so] = from_f<T>(p);
+        }
+        if (polyak) {
+          P[t_off + i] = tp;
+          if (so >= 0) S[ts_off + so] = from_f<T>(tp);
+        }
       }
     }
   }

@@ -83,6 +83,10 @@ static bool actor_bwd_unfused_env() {
 }
 
 // diagnostics: SPZ_FP32_SIMT=1 runs the FP32 precision path on the SIMT kernel instead of 3xTF32
+static bool wgrad_pre_off_env() {
+  const char* e = std::getenv("SPZ_WGRAD_PRE");
+  return e && std::atoi(e) == 0;
+}
 static bool fp32_simt_env() {
   static const bool on = [] {
     const char* e = std::getenv("SPZ_FP32_SIMT");
@@ -210,6 +214,7 @@ struct spz_learner {
   int* h_gate = nullptr;       // mapped: spz_learner_profile's release word
   int* d_gate = nullptr;
   unsigned* tickets = nullptr;  // last-block counter of the loss kernel
+  unsigned* sched = nullptr;    // dynamic GEMM tile schedules: [counter, finished CTAs] per launch that uses one
   int64_t* ctr_snap = nullptr;  // counters as read at the start of the step (loss kernel -> Adam)
   std::vector<void*> allocs;
   struct DebugBuf { std::string name; void* ptr; size_t bytes; int esz; };
@@ -232,6 +237,12 @@ static spz_status dalloc(spz_learner* Lr, void** p, size_t bytes) {
   return SPZ_OK;
 }
 
+
+// Elements per float4 Adam segment (<= 4 x ADAM_NT; 0: scalar segments only).  SPZ_ADAM_VEC overrides.
+static int adam_vec_seg() {
+  if (const char* e = std::getenv("SPZ_ADAM_VEC")) return std::max(0, std::min(4 * ADAM_NT, std::atoi(e) / 4 * 4));
+  return 4 * ADAM_NT;
+}
 
 // Split-K count of the merged weight-gradient GEMM.  Cost model per split count S (microseconds):
 // waves of output tiles (128 x 256 each) over the SMs x (rows each tile contracts + a fixed per-tile
@@ -273,6 +284,31 @@ static int wgrad_splits(const spz_learner* Lr, int64_t Bl) {
   return std::min(wgrad_splits_at(Lr, Bl, sms), wgrad_splits_at(Lr, Lr->max_local, sms));
 }
 static int64_t wgrad_rows(int64_t Bl, int s) { return round_up(cdiv(Bl, s), 128); }
+// Split-K of the actor's weight gradients (bf16 path) behind the fused actor backward.  That kernel runs one CTA
+// per 128 rows (B / 128 < SMs), and the weight-gradient launch behind it computes the critic / value tiles on the
+// SMs it leaves idle, before its grid-dependency wait (dynamic tile schedule); the actor tiles are its tail, so
+// they are cut finer than the critics' (shorter tiles after the wait, more partials for Adam to sum): 16 splits,
+// measured at WLK (98.0 us per update against 100.2 with the critics' 9; 12: 98.4, 20: 99.2, 26: 100.5), never
+// fewer than the critics' and never below 256 rows per split.  Behind the unfused actor backward (a GEMM over
+// every SM) the critics' count (ANT: 279.6 us against 281.2 with 16).  SPZ_WGRAD_SA=<S> overrides (0: the
+// critics' count).
+static int actor_wgrad_splits_at(const spz_learner* Lr, int64_t Bl, int sms, bool fused) {
+  const int Sw = wgrad_splits_at(Lr, Bl, sms);
+  if (!Lr->bf16 || !fused) return Sw;
+  const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(32, Bl / 256));
+  int want = 16;
+  if (const char* e = std::getenv("SPZ_WGRAD_SA")) want = std::atoi(e);
+  return want <= 0 ? Sw : std::max(Sw, std::min(want, smax));
+}
+static int actor_wgrad_splits(const spz_learner* Lr, int64_t Bl, bool fused) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // never above the count at the largest batch (the fused kernel's only possible size), for which the partials
+  // are allocated
+  return std::min(actor_wgrad_splits_at(Lr, Bl, sms, fused), actor_wgrad_splits_at(Lr, Lr->max_local, sms, Lr->cfg.hidden <= 256));
+}
+static int64_t actor_wgrad_rows(int64_t Bl, int s) { return round_up(cdiv(Bl, s), 64); }
 static int bias_splits(int64_t Bl) { return (int)std::max<int64_t>(1, std::min<int64_t>(128, cdiv(Bl, 128))); }
 
 // Gradient partial regions (one per trained tensor), laid out at create time for the
@@ -288,9 +324,11 @@ struct TensorSlot {
 static std::vector<TensorSlot> trained_tensors(spz_learner* Lr) {
   std::vector<TensorSlot> v;
   const bool actor_on = Lr->cfg.role != SPZ_ROLE_CRITIC, critic_on = Lr->cfg.role != SPZ_ROLE_ACTOR;
-  const int Sw = wgrad_splits(Lr, Lr->max_local), Sb = bias_splits(Lr->max_local);
+  const int Sb = bias_splits(Lr->max_local);
   auto add_net = [&](int id) {
     const NetLayout& n = Lr->net[id];
+    const int Sw = id == NET_ACTOR ? actor_wgrad_splits(Lr, Lr->max_local, Lr->cfg.hidden <= 256)
+                                   : wgrad_splits(Lr, Lr->max_local);
     for (int l = 0; l < n.nl; ++l) {
       const bool head_vec = (id == NET_Q1 || id == NET_Q2 || id == NET_V) && l == n.nl - 1;  // N = 1 head: column sums
       // weight partials keep a 16-byte row pitch (TMA stores): out x round_up(in, 4)
@@ -380,6 +418,9 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
   const int delay = std::max(1, Lr->cfg.td3_policy_delay);
   const int Sw = wgrad_splits(Lr, Bl), Sb = bias_splits(Bl);
   const int64_t rows_w = wgrad_rows(Bl, Sw), rows_b = cdiv(Bl, Sb);
+  // actor weight gradients: their own split-K behind the fused actor backward (set in a7)
+  int64_t rows_a = rows_w;
+  int Sa = Sw;
   auto Wp = [&](int id, int l) -> const T* { return S + Lr->sbase[id] + Lr->net[id].sw[l]; };
   auto bp = [&](int id, int l) -> const float* { return P + Lr->pbase[id] + Lr->net[id].b[l]; };
   auto ldw = [&](int id, int l) { return Lr->net[id].ld[l]; };
@@ -998,6 +1039,13 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       ab.lo = lo;
       ab.hi = hi;
       abwd_fused = tc_actor_bwd_supported(ab);
+      if (abwd_fused) {
+        const int sa = actor_wgrad_splits(Lr, Bl, true);
+        if (sa != Sw) {
+          rows_a = actor_wgrad_rows(Bl, sa);
+          Sa = (int)cdiv(Bl, rows_a);
+        }
+      }
     }
     // ---- a6: critic backward
     {
@@ -1113,6 +1161,8 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         colsums.push_back({Lr->gv, nullptr, Lr->G + slot_of(NET_V, L, false).g_off, 1, 1, Bl, 1});
       }
     }
+    // weight gradients collected so far (critics, value net) read nothing the actor backward writes
+    size_t n_pre_wgrads = wgrads.size();
     // ---- a7: actor backward (s-rows Bl..2Bl of the actor activations)
     if (do_actor) {
       const NetLayout& an = Lr->net[NET_ACTOR];
@@ -1166,6 +1216,10 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           g.colsum_out = Lr->G + slot_of(NET_ACTOR, l, false).g_off;
           g.colsum_stride = an.out[l];
         }
+        if (Sa != Sw) {
+          g.splits = Sa;
+          g.k_per_split = (int)rows_a;
+        }
         wgrads.push_back(g);
       }
       for (int l = 0; l <= L && !fuse_bias; ++l)
@@ -1184,7 +1238,10 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         return p == std::string::npos ? -1 : std::atoi(ms.c_str() + p + std::strlen(key));
       };
       const int dw = idx_of("drop_wgrad="), dbi = idx_of("drop_bias=");
-      if (dw >= 0 && dw < (int)wgrads.size()) wgrads.erase(wgrads.begin() + dw);
+      if (dw >= 0 && dw < (int)wgrads.size()) {
+        wgrads.erase(wgrads.begin() + dw);
+        if ((size_t)dw < n_pre_wgrads) --n_pre_wgrads;
+      }
       if (dbi >= 0) {
         if (fuse_bias && dbi < (int)wgrads.size()) wgrads[dbi].colsum_out = nullptr;
         else if (!fuse_bias && dbi < (int)colsums.size()) colsums.erase(colsums.begin() + dbi);
@@ -1194,11 +1251,27 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       GemmArgs a = mk(Bl, fuse_bias ? EPI_WGRAD_BIAS : EPI_F32, 1, 1);
       a.splits = Sw;
       a.k_per_split = (int)rows_w;
+      // Behind an actor-backward kernel (PDL), the first launch computes the critic / value weight gradients --
+      // whose inputs that kernel does not write -- before its grid-dependency wait, on a dynamic tile schedule:
+      // its CTAs that start on the SMs the actor backward leaves idle take those tiles first (SPZ_WGRAD_PRE=0:
+      // static schedule, everything after the wait)
+      bool pre = false;
+      if (!ops.empty() && n_pre_wgrads > 0 && bits && !wgrad_pre_off_env()) {
+        static const char* const actor_ops[] = {"actor_bwd_fused", "actor_dgrad_gemm", "actor_head_bwd"};
+        for (const char* c : actor_ops)
+          if (std::strcmp(ops.back().cls, c) == 0) pre = true;
+      }
+      if (pre) {
+        a.sched = Lr->sched + 2 * variant;
+        a.n_pre_groups = (int)std::min<size_t>(n_pre_wgrads, MAX_GROUPS);
+      }
       for (const GemmGroup& g : wgrads) {
         if (a.n_groups == MAX_GROUPS) {
           gemm("wgrad_gemm", a);
           a.n_groups = 0;
           a.N = 0;
+          a.sched = nullptr;  // later launches: static schedule, wait first
+          a.n_pre_groups = 0;
         }
         a.g[a.n_groups++] = g;
         a.N = std::max(a.N, g.N);
@@ -1227,7 +1300,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         const bool head_vec = (s.net == NET_Q1 || s.net == NET_Q2 || s.net == NET_V) && s.layer == n.nl - 1;
         t.numel = s.weight ? (int64_t)n.out[s.layer] * n.in[s.layer] : n.out[s.layer];
         t.partials = Lr->G + s.g_off;
-        t.n_partials = (s.weight && !head_vec) || fuse_bias ? Sw : Sb;
+        t.n_partials = (s.weight && !head_vec) || fuse_bias ? (s.net == NET_ACTOR ? Sa : Sw) : Sb;
         t.pld = s.weight ? (head_vec ? n.in[s.layer] : (int)round_up(n.in[s.layer], 4)) : 1;
         t.pstride = s.weight ? (int64_t)n.out[s.layer] * t.pld : n.out[s.layer];
         t.opt = s.net == NET_ACTOR ? 1 : 0;
@@ -1258,16 +1331,33 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
           off += round_up(t.numel, 16);
         }
       }
-      auto segments = [](const std::vector<AdamTensor>& ts) {
+      // float4 segments (4 consecutive elements per thread) where every access of the tensor is 16-byte aligned
+      // (8-byte for the bf16 shadow) and 4 consecutive elements share one row; SPZ_ADAM_VEC=0 disables them
+      const int vec_seg = adam_vec_seg();
+      auto vec_ok = [&](const AdamTensor& t) {
+        if (vec_seg == 0 || t.opt == 2 || t.numel % 4 || t.p_off % 4 || (t.t_off >= 0 && t.t_off % 4)) return false;
+        if (reinterpret_cast<uintptr_t>(t.partials) % 16 || t.pstride % 4) return false;
+        if (t.cols > 0) {
+          if (t.cols % 4 || t.pld % 4 || t.ld % 4 || t.s_off % 4 || (t.ts_off >= 0 && t.ts_off % 4)) return false;
+        } else if (t.pld != 1) {
+          return false;
+        }
+        return true;
+      };
+      auto segments = [&](const std::vector<AdamTensor>& ts) {
         std::vector<AdamSegment> v;
-        for (const AdamTensor& t : ts)
-          for (int64_t st = 0; st < t.numel; st += ADAM_SEG) {
+        for (const AdamTensor& t : ts) {
+          const bool vc = vec_ok(t);
+          const int64_t seg = vc ? vec_seg : ADAM_SEG;
+          for (int64_t st = 0; st < t.numel; st += seg) {
             AdamSegment sg{};
             sg.t = t;
             sg.start = st;
-            sg.count = (int32_t)std::min<int64_t>(ADAM_SEG, t.numel - st);
+            sg.count = (int32_t)std::min<int64_t>(seg, t.numel - st);
+            sg.vec = vc ? 1 : 0;
             v.push_back(sg);
           }
+        }
         return v;
       };
       segs = segments(tens);
@@ -1736,6 +1826,7 @@ spz_status spz_learner_create(const spz_config* cfg, spz_replay* ring, spz_learn
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->G, Lr->G_total * sizeof(float)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->statsum, 8 * sizeof(double)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->tickets, 256 * sizeof(unsigned)));  // [0] + per-group counters (critic_loss_kernel)
+  SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->sched, 64 * sizeof(unsigned)));
   SPZ_TRY(dalloc(Lr.get(), (void**)&Lr->ctr_snap, 16 * sizeof(int64_t)));
   Lr->debug.push_back({"statsum", Lr->statsum, 8 * sizeof(double), 8});
   if (Lr->gsize > 1 || cfg->comm_mode == 2) {

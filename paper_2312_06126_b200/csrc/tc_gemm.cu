@@ -48,6 +48,8 @@ struct TcParams {
   int out_bytes;  // 2 (bf16) or 4 (fp32) output elements
   int pair;       // 1: CTA-pair kernel (cta_group::2, M = 256 pair tiles; tb boxes hold BN / 2 rows)
   int wpq;        // epilogue warps per TMEM lane quarter (2 or 4)
+  int dyn;        // 1: dynamic tile schedule (atomic counter a.sched), 0: static round robin
+  int n_pre;      // dynamic schedule: linear tiles [0, n_pre) need no grid-dependency wait
   CUtensorMap ta[MAX_GROUPS];
   CUtensorMap tb[MAX_GROUPS];
   CUtensorMap tc[MAX_GROUPS];  // C as [splits][M][N]; box = 64 bytes x 32 rows, 64-byte swizzle
@@ -58,6 +60,13 @@ struct TcParams {
 // 2 epilogue sees the accumulator, 3 epilogue done.
 constexpr int TRACE_CTAS = 160, TRACE_TILES = 8;
 __device__ unsigned long long g_trace[TRACE_CTAS * TRACE_TILES * 4];
+__device__ int g_trace_tile[TRACE_CTAS * TRACE_TILES];  // linear tile index of each traced tile
+__device__ unsigned long long g_trace_cta[TRACE_CTAS * 2];  // per CTA: kernel entry, producer past the dependency wait
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define trace(tile_i, ev) trace_(p.trace, tile_i, ev)
 __device__ __forceinline__ void trace_(int on, int tile_i, int ev) {
   if (on && blockIdx.x < TRACE_CTAS && tile_i < TRACE_TILES) {
@@ -185,6 +194,10 @@ __global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __g
   __shared__ __align__(16) float dotw_w[S::RELU ? NUM_EPI_WARPS : 1][S::RELU ? S::SLICE : 4];
   __shared__ float dotpart[S::RELU ? 2 : 1][S::RELU ? WPQ : 1][S::RELU ? BM : 1];
   __shared__ float headpart[S::HEAD ? 2 : 1][S::HEAD ? WPQ : 1][S::HEAD ? BM : 1];  // SAC log-pi parts
+  // dynamic schedule: the producer's tile sequence, handed to the MMA issuer and the epilogue warps
+  constexpr int TQ = 8;
+  __shared__ int tq[TQ];
+  __shared__ __align__(8) uint64_t tq_full[TQ], tq_empty[TQ];
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NS = p.stages;
@@ -222,6 +235,10 @@ __global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __g
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], PAIR ? 2 * NUM_EPI_WARPS : NUM_EPI_WARPS);  // pair: both CTAs' epilogues (leader's)
     }
+    for (int i = 0; i < TQ; ++i) {
+      mbar_init(&tq_full[i], 1);                   // the producer publishes the slot's tile
+      mbar_init(&tq_empty[i], 1 + NUM_EPI_WARPS);  // the MMA issuer and every epilogue warp have read it
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -242,20 +259,56 @@ __global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __g
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // everything above overlapped the previous kernel (PDL); from here on we read its outputs
-  pdl_wait();
+  // everything above overlapped the previous kernel (PDL); from here on we read its outputs -- except under a
+  // dynamic schedule with independent leading tiles, where only the producer waits, before the first tile that
+  // reads them (nothing else in the CTA reads memory that kernel wrote: MMA operands arrive through the producer)
+  if (p.trace && blockIdx.x < TRACE_CTAS && threadIdx.x == 0) g_trace_cta[blockIdx.x * 2] = gtimer();
+  const bool dyn = !PAIR && p.dyn;
+  const bool lazy_wait = dyn && p.n_pre > 0;
+  if (!lazy_wait) pdl_wait();
   pdl_launch();
+  // tile sequence: static round robin, or (dyn) the producer claims tiles from the counter and publishes
+  // each in the queue slot i % TQ; consumers read slot i and release it
+  auto claim = [&](int i) -> int {  // producer lane only
+    const int sl = i % TQ;
+    mbar_wait(&tq_empty[sl], ((uint32_t)(i / TQ) & 1u) ^ 1u);
+    int t = (int)atomicAdd(a.sched, 1u);
+    if (t > T) t = T;
+    tq[sl] = t;
+    mbar_arrive(&tq_full[sl]);
+    return t;
+  };
+  auto fetch = [&](int i, bool warp_release) -> int {  // MMA lane (warp_release false) / epilogue warp
+    const int sl = i % TQ;
+    mbar_wait(&tq_full[sl], (uint32_t)(i / TQ) & 1u);
+    const int t = *reinterpret_cast<volatile int*>(&tq[sl]);
+    if (warp_release) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tq_empty[sl]);
+    } else {
+      mbar_arrive(&tq_empty[sl]);
+    }
+    return t;
+  };
   if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) g_trace[TRACE_CTAS * TRACE_TILES * 4 - 1] = (unsigned long long)T;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer: a continuous stream of k-blocks over this CTA's tiles
       int kg = 0, tile_p = 0;
-      for (int t = cta0; t < T; t += ncta, ++tile_p) {
+      bool waited = !lazy_wait;
+      for (int t = dyn ? claim(0) : cta0; t < T; t = dyn ? claim(tile_p + 1) : t + ncta, ++tile_p) {
+        if (!waited && t >= p.n_pre) {
+          pdl_wait();
+          waited = true;
+          if (p.trace && blockIdx.x < TRACE_CTAS) g_trace_cta[blockIdx.x * 2 + 1] = gtimer();
+        }
         trace(tile_p, 0);
+        if (p.trace && blockIdx.x < TRACE_CTAS && tile_p < TRACE_TILES) g_trace_tile[blockIdx.x * TRACE_TILES + tile_p] = t;
         const TileInfo ti = decode_tile(p, t, BN, crank);
-        const int k_begin = ti.split * a.k_per_split;
-        const int k_end = min(a.K, k_begin + a.k_per_split);
+        const int kps = group_kps(a.g[ti.grp], a.k_per_split);
+        const int k_begin = ti.split * kps;
+        const int k_end = min(a.K, k_begin + kps);
         const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
         for (int kb = 0; kb < nkb; ++kb, ++kg) {
           const int s = kg % NS;
@@ -286,16 +339,19 @@ __global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __g
           }
         }
       }
+      // the grid completes only after the kernel it was launched behind: later kernels rely on that
+      if (!waited) pdl_wait();
     }
   } else if (warp == 1) {
     if (lane == 0 && crank == 0) {
       // ---------------- MMA issuer: accumulator buffer (tile_i & 1), freed by the epilogue warps
       //                  (pair: the leader issues the pair's M = 256 MMAs; commits reach both CTAs)
       int kg = 0, tile_i = 0;
-      for (int t = cta0; t < T; t += ncta, ++tile_i) {
+      for (int t = dyn ? fetch(0, false) : cta0; t < T; t = dyn ? fetch(tile_i + 1, false) : t + ncta, ++tile_i) {
         const TileInfo ti = decode_tile(p, t, BN, crank);
-        const int k_begin = ti.split * a.k_per_split;
-        const int k_end = min(a.K, k_begin + a.k_per_split);
+        const int kps = group_kps(a.g[ti.grp], a.k_per_split);
+        const int k_begin = ti.split * kps;
+        const int k_end = min(a.K, k_begin + kps);
         const int nkb = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
         const int b = tile_i % NBUF;
         mbar_wait(&acc_empty[b], (((uint32_t)(tile_i / NBUF)) & 1u) ^ 1u);
@@ -349,14 +405,15 @@ __global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __g
     int st_count = 0;   // TMA store blocks issued by this warp
     int dot_tiles = 0;  // fused row-dot tiles seen (dotpart buffer parity)
     const uint32_t acc_empty0 = PAIR ? mapa_shared(smem_u32(acc_empty), 0) : 0u;  // the leader's acc_empty[0]
-    for (int t = cta0; t < T; t += ncta, ++tile_i) {
+    for (int t = dyn ? fetch(0, true) : cta0; t < T; t = dyn ? fetch(tile_i + 1, true) : t + ncta, ++tile_i) {
       const TileInfo ti = decode_tile(p, t, BN, crank);
       const GemmGroup& g = a.g[ti.grp];
       const int m = ti.m0 + r;
       const int n0 = ti.n0;
       const int ncol0 = n0 + c_lo * 16;  // first output column of this warp
-      const int k_begin = ti.split * a.k_per_split;
-      const bool has_acc = min(a.K, k_begin + a.k_per_split) > k_begin;
+      const int kps = group_kps(g, a.k_per_split);
+      const int k_begin = ti.split * kps;
+      const bool has_acc = min(a.K, k_begin + kps) > k_begin;
       const bool has_dot = S::RELU && g.dot_out != nullptr;
       const bool mask_out = S::RELU && g.mask_out != nullptr;
       // this warp's slice of the bias / row-dot weights (the previous tile's reads of the slice
@@ -549,6 +606,14 @@ __global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __g
       tc_fence_after();
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
     }
+    // dynamic schedule: every CTA claimed its last tile (>= T) before arriving here; the last CTA to arrive
+    // resets the counters for the next launch (which starts only after this grid completes)
+    if (dyn && threadIdx.x == 0) {
+      if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+        a.sched[0] = 0u;
+        a.sched[1] = 0u;
+      }
+    }
   }
 }
 
@@ -593,10 +658,12 @@ cudaError_t launch(TcParams& p, cudaStream_t st) {
     p.mtiles[i] = g.M > 0 && g.N > 0 ? (int)cdiv(g.M, PAIR ? 2 * BM : BM) : 0;  // pair: 256-row pair tiles
     p.ntiles[i] = g.M > 0 && g.N > 0 ? (int)cdiv(g.N, BN) : 1;
     if (p.mtiles[i] == 0) p.mtiles[i] = 1, p.ntiles[i] = 0;
-    T += p.mtiles[i] * p.ntiles[i] * p.a.splits;
+    T += p.mtiles[i] * p.ntiles[i] * group_splits(g, p.a.splits);
   }
   p.tile0[p.a.n_groups] = T;
   p.total_tiles = T;
+  p.dyn = !PAIR && p.a.sched != nullptr ? 1 : 0;
+  p.n_pre = p.dyn ? p.tile0[std::max(0, std::min(p.a.n_pre_groups, p.a.n_groups))] : 0;
   if (T == 0) return cudaSuccess;
   constexpr int TMEM_COLS = EpiShape<BN, EK, WPQ>::TMEM_COLS;
   static int occ = [&] {
@@ -606,7 +673,9 @@ cudaError_t launch(TcParams& p, cudaStream_t st) {
   }();
   const int per_sm = std::max(1, std::min(512 / TMEM_COLS, occ));
   const int budget = 227 * 1024 / per_sm - smem_static<BN, EK, WPQ>();
-  const int kspan = p.a.splits > 1 ? p.a.k_per_split : p.a.K;
+  int kspan = 0;  // longest contraction of one tile
+  for (int i = 0; i < p.a.n_groups; ++i)
+    kspan = std::max(kspan, group_splits(p.a.g[i], p.a.splits) > 1 ? group_kps(p.a.g[i], p.a.k_per_split) : p.a.K);
   const int want = (int)std::min<int64_t>(STAGES, std::max<int64_t>(1, cdiv(kspan, BK)));
   p.stages = std::max(1, std::min(std::min(want, MAX_ST), (budget - smem_extras<WPQ>()) / STAGE));
   const int smem = p.stages * STAGE + smem_extras<WPQ>();
@@ -740,14 +809,32 @@ cudaError_t tc_trace(int on, unsigned long long* out, int n) {
     static std::vector<unsigned long long> zeros(TRACE_CTAS * TRACE_TILES * 4, 0ull);
     e = cudaMemcpyToSymbol(g_trace, zeros.data(), zeros.size() * sizeof(unsigned long long));
   }
+  if (on) {
+    static std::vector<int> neg(TRACE_CTAS * TRACE_TILES, -1);
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_trace_tile, neg.data(), neg.size() * sizeof(int));
+    static std::vector<unsigned long long> z2(TRACE_CTAS * 2, 0ull);
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_trace_cta, z2.data(), z2.size() * sizeof(unsigned long long));
+  }
   if (e != cudaSuccess || !out) return e;
-  n = std::min(n, TRACE_CTAS * TRACE_TILES * 4);
-  return cudaMemcpyFromSymbol(out, g_trace, n * sizeof(unsigned long long));
+  // n > stamps: the tile indices follow (as 64-bit values)
+  const int ns = TRACE_CTAS * TRACE_TILES * 4;
+  e = cudaMemcpyFromSymbol(out, g_trace, std::min(n, ns) * sizeof(unsigned long long));
+  if (e != cudaSuccess || n <= ns) return e;
+  std::vector<int> ti(TRACE_CTAS * TRACE_TILES);
+  e = cudaMemcpyFromSymbol(ti.data(), g_trace_tile, ti.size() * sizeof(int));
+  for (int i = 0; i < (int)ti.size() && ns + i < n; ++i) out[ns + i] = (unsigned long long)(long long)ti[i];
+  const int nc = ns + (int)ti.size();
+  if (e != cudaSuccess || n <= nc) return e;
+  return cudaMemcpyFromSymbol(out + nc, g_trace_cta, std::min(n - nc, TRACE_CTAS * 2) * sizeof(unsigned long long));
 }
 
 bool tc_gemm_supported(const GemmArgs& a) {
   if (a.N < 1 || a.K < 1 || a.n_groups < 1 || a.n_groups > MAX_GROUPS) return false;
   if (a.splits > 1 && (a.k_per_split % BK)) return false;
+  for (int i = 0; i < a.n_groups; ++i)
+    if (a.g[i].splits > 0 && (a.g[i].splits < 1 || (a.g[i].splits > 1 && (a.g[i].k_per_split % BK)) ||
+                              (int64_t)a.g[i].splits * a.g[i].k_per_split < a.K))
+      return false;
   const int bn = pick_bn(a.N, a.b_mn);
   const bool ek = a.a_mn ? (a.b_mn && ek_ok<true, true>(a.epi, bn))
                          : (a.b_mn ? ek_ok<false, true>(a.epi, bn) : ek_ok<false, false>(a.epi, bn));
@@ -786,13 +873,13 @@ cudaError_t tc_gemm_bf16(const GemmArgs& a, cudaStream_t st) {
   for (int i = 0; i < a.n_groups && p.tma_out; ++i) {
     const GemmGroup& g = a.g[i];
     if (g.M < 1 || g.N < 1) continue;
-    if (!g.C || !make_map_out(&p.tc[i], g.C, p.out_bytes, g.N, g.M, a.splits, g.ldc, g.split_stride)) p.tma_out = 0;
+    if (!g.C || !make_map_out(&p.tc[i], g.C, p.out_bytes, g.N, g.M, group_splits(g, a.splits), g.ldc, g.split_stride)) p.tma_out = 0;
   }
   const int bn = pick_bn(a.N, a.b_mn);
   p.pair = want_pair(a, bn) ? 1 : 0;
   {  // 4 epilogue warps per lane quarter under two tiles per SM, else 2 (SPZ_TC_WPQ=2 / 4 forces; diagnostics)
     int64_t tiles = 0;
-    for (int i = 0; i < a.n_groups; ++i) tiles += cdiv(a.g[i].M, BM) * cdiv(a.g[i].N, bn) * a.splits;
+    for (int i = 0; i < a.n_groups; ++i) tiles += cdiv(a.g[i].M, BM) * cdiv(a.g[i].N, bn) * group_splits(a.g[i], a.splits);
     // (4 warps only at BN >= 128: a warp's column slice must fill its 64-byte store blocks, EpiShape)
     p.wpq = tiles < 2 * num_sms() && bn >= 128 ? 4 : 2;
     if (const char* w = std::getenv("SPZ_TC_WPQ")) p.wpq = std::atoi(w) == 4 && bn >= 128 ? 4 : 2;

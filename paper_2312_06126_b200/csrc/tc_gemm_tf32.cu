@@ -394,6 +394,8 @@ bool make_map32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
 bool tc_gemm_tf32_supported(const GemmArgs& a) {
   if (a.N < 1 || a.K < 1 || a.n_groups < 1 || a.n_groups > MAX_GROUPS) return false;
   if (a.splits > 1 && (a.k_per_split % TBK)) return false;
+  for (int i = 0; i < a.n_groups; ++i)
+    if (a.g[i].splits > 0) return false;  // per-group split-K: bf16 kernel only
   if (a.a_mn && !a.b_mn) return false;
   const bool ek = a.a_mn ? ek32_ok<true, true>(a.epi) : (a.b_mn ? ek32_ok<false, true>(a.epi) : ek32_ok<false, false>(a.epi));
   if (!ek) return false;

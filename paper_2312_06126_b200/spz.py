@@ -359,6 +359,16 @@ def spz_diag_tc_trace(on, read=False, device=0):
     return out.reshape(160, 8, 4) if read else None
 
 
+def spz_diag_tc_trace_tiles(device=0):
+    """Stamps [160, 8, 4], the linear tile index of each traced tile [160, 8] (-1: none) and per CTA [160, 2]
+    (kernel entry, producer past the grid-dependency wait; 0: none) of the last traced GEMM launch."""
+    n = 160 * 8 * 4
+    out = np.zeros(n + 160 * 8 + 160 * 2, np.uint64)
+    _check(lib().spz_diag_tc_trace(device, 0, _ptr(out), out.size))
+    return (out[:n].reshape(160, 8, 4), out[n:n + 1280].view(np.int64).reshape(160, 8),
+            out[n + 1280:].reshape(160, 2))
+
+
 def spz_diag_mlp_trace(on, read=False, device=0):
     """Fused-MLP timestamps (spz_diag_tc_trace modes >= 100); with read=True: uint64 [160, 4, 3, 6]
     = (CTA, unit, layer, event: MMA start, MMA issued, epilogue sees accumulator, epilogue done,

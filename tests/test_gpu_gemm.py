@@ -159,3 +159,24 @@ def test_tc_gemm_cta_pair_matches_fp32_matmul(M, N, K, monkeypatch):
     ref = _ref(A, 0, B, 0, M, N, K)
     err = (C - ref).abs().max().item() / max(ref.abs().max().item(), 1e-6)
     assert err < 2e-6 * K ** 0.5, err
+
+
+@pytest.mark.parametrize("n_pre", [0, 1])
+@pytest.mark.parametrize("M,N,K,splits,kps", [(256, 256, 8192, 32, 256), (512, 44, 3000, 3, 1024), (16384, 256, 256, 1, 256)])
+def test_tc_gemm_dynamic_schedule(M, N, K, splits, kps, n_pre, monkeypatch):
+    """Dynamic tile schedule (atomic tile counter, tiles handed to the MMA / epilogue warps through the shared
+    queue; n_pre = 1: the group's tiles run before the grid-dependency wait): the same result as the static
+    schedule, bit for bit, and the counters are back at zero after every launch (checked inside the call)."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    a_mn = b_mn = 1 if splits > 1 or K > 1000 else 0
+    lda = ((M if a_mn else K) + 7) // 8 * 8
+    ldb = ((N if b_mn else K) + 7) // 8 * 8
+    A = _mk(K, M, lda, g) if a_mn else _mk(M, K, lda, g)
+    B = _mk(K, N, ldb, g) if b_mn else _mk(N, K, ldb, g)
+    C0 = torch.full((splits, M, N), float("nan"), device="cuda")
+    spz.spz_diag_gemm_bf16(M, N, K, A, lda, a_mn, B, ldb, b_mn, C0, N, splits=splits, k_per_split=kps)
+    monkeypatch.setenv("SPZ_DIAG_GEMM_DYN", str(n_pre))
+    for _ in range(3):  # repeated launches: the last CTA of each resets the counters
+        C = torch.full((splits, M, N), float("nan"), device="cuda")
+        spz.spz_diag_gemm_bf16(M, N, K, A, lda, a_mn, B, ldb, b_mn, C, N, splits=splits, k_per_split=kps)
+        assert torch.equal(C, C0)

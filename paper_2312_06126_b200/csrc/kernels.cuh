@@ -258,6 +258,10 @@ struct LossArgs {
   float gamma, invB;
   int Bl, td3, delay, loss_rows, actor_rows, h, ld, mask_ld;
   int q2_no_actor;        // TD3: Q2 has no actor rows (its dZ_L there is never read)
+  int defer_totals;       // 1: no grid-wide reduction here -- the optimizer sums the block partials itself (off the
+                          //    critical path, before its dependency wait); block 0 writes the optimizer snapshot
+  int diag;               // diagnostics only (SPZ_DIAG_LOSS_CUT; results are wrong): 1 skip the grid-wide statistics
+                          // reduction, 2 no work at all
   // SAC v1 (reading #24): qt1 = qt2 = V'(s2) and the bootstrap drops the entropy term; the actor rows
   // also give the value target y_V = min(q1~, q2~) - alpha log pi~, g_V = 2 (V(s) - y_V) / B
   int v1;
@@ -280,6 +284,31 @@ __device__ __forceinline__ float ld_q(const float* __restrict__ q, int64_t j, in
   return s;
 }
 
+// Loss totals from the per-block statistics partials, in a fixed order: thread t sums blocks t, t + NT, ...; then
+// each warp's shuffle tree; then the warps in order.  Called by the loss kernel's last block, or by every block of
+// the optimizer (deferred totals) -- the same NT gives bit-identical totals.  Thread i < NSTAT writes total i to
+// out[i] (out may be shared or global); red: [NT / 32][NSTAT] shared scratch.
+template <int NT>
+__device__ __forceinline__ void stat_totals(const double* __restrict__ partials, unsigned nblocks, double (*red)[NSTAT],
+                                            double* out) {
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  double t[NSTAT] = {0, 0, 0, 0, 0, 0};
+  for (unsigned b = threadIdx.x; b < nblocks; b += NT)
+#pragma unroll
+    for (int i = 0; i < NSTAT; ++i) t[i] += __ldcg(partials + b * NSTAT + i);
+#pragma unroll
+  for (int i = 0; i < NSTAT; ++i) t[i] = warp_sum(t[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NSTAT; ++i) red[wi][i] = t[i];
+  __syncthreads();
+  if (threadIdx.x < NSTAT) {
+    double u = 0.0;
+    for (int k = 0; k < NT / 32; ++k) u += red[k][threadIdx.x];
+    out[threadIdx.x] = u;
+  }
+}
+
 // Block = LOSS_ROWS rows, warp w owns rows w, w + 8, ... (LOSS_RPW of them).  Every lane loads the
 // row scalars (broadcast) and computes g_q itself; with DZ (h <= 256: one 8-column chunk per lane) it
 // then writes its chunk of dZ_L, otherwise critic_dz_kernel does that afterwards.  All of a warp's
@@ -290,6 +319,19 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   constexpr int LOSS_ROWS = LOSS_WARPS * LOSS_RPW;
   pdl_wait();
   pdl_launch();
+  if (a.diag) {  // diagnostics: block 0 writes the optimizer snapshot (finite totals, counters, bias corrections)
+    if (blockIdx.x == 0) {
+      if (threadIdx.x < NSTAT) a.totals[threadIdx.x] = 0.0;
+      if (threadIdx.x < 4) a.ctr_snap[threadIdx.x] = a.step_p[threadIdx.x];
+      if (threadIdx.x == 4) *a.la_snap = *a.log_alpha;
+      if (threadIdx.x >= 8 && threadIdx.x < 14) {
+        const int k = threadIdx.x - 8, o = k % 3;
+        const double beta = k < 3 ? (double)a.beta1 : (double)a.beta2;
+        a.bc_snap[k] = (float)(-expm1((double)(a.step_p[1 + o] + 1) * log1p(beta - 1.0)));
+      }
+    }
+    if (a.diag == 2) return;
+  }
   __shared__ double red[LOSS_NT / 32][NSTAT];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
@@ -447,6 +489,21 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   }
   // the last block sums every block's partial (fixed order: strided per thread, then a fixed tree)
   __syncthreads();
+  if (a.diag == 1) return;
+  if (a.defer_totals) {
+    // the optimizer reduces the partials (stat_totals, same order); the snapshot depends on no other block
+    if (blockIdx.x == 0) {
+      if (threadIdx.x < 4) a.ctr_snap[threadIdx.x] = a.step_p[threadIdx.x];
+      if (threadIdx.x == 4) *a.la_snap = *a.log_alpha;
+      if (threadIdx.x >= 8 && threadIdx.x < 14) {
+        const int k = threadIdx.x - 8, o = k % 3;
+        const double beta = k < 3 ? (double)a.beta1 : (double)a.beta2;
+        const double t = (double)(a.step_p[1 + o] + 1);
+        a.bc_snap[k] = (float)(-expm1(t * log1p(beta - 1.0)));
+      }
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     // two-level ticket: same-address atomics serialise in L2, so the blocks count in groups of 32 on
     // separate counters (ticket[1 + group]) and only each group's last block counts on ticket[0]
@@ -463,21 +520,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   __syncthreads();
   if (last) {
     fence_acq_rel_gpu();
-    double t[NSTAT] = {0, 0, 0, 0, 0, 0};
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += LOSS_NT)
-#pragma unroll
-      for (int i = 0; i < NSTAT; ++i) t[i] += __ldcg(a.partials + b * NSTAT + i);
-#pragma unroll
-    for (int i = 0; i < NSTAT; ++i) t[i] = warp_sum(t[i]);
-    if (lane == 0)
-#pragma unroll
-      for (int i = 0; i < NSTAT; ++i) red[wi][i] = t[i];
-    __syncthreads();
-    if (threadIdx.x < NSTAT) {
-      double u = 0.0;
-      for (int k = 0; k < LOSS_NT / 32; ++k) u += red[k][threadIdx.x];
-      a.totals[threadIdx.x] = u;
-    }
+    stat_totals<LOSS_NT>(a.partials, gridDim.x, red, a.totals);
     if (threadIdx.x == 0) *a.ticket = 0u;
     if (threadIdx.x < 4) a.ctr_snap[threadIdx.x] = a.step_p[threadIdx.x];
     if (threadIdx.x == 4) *a.la_snap = *a.log_alpha;
@@ -669,6 +712,7 @@ struct StatsOut {
 #define SPZ_ADAM_MINB 4
 #endif
 constexpr int ADAM_NT = SPZ_ADAM_NT, ADAM_EPT = SPZ_ADAM_EPT, ADAM_SEG = ADAM_NT * ADAM_EPT;  // elements per block
+static_assert(ADAM_NT == LOSS_NT, "deferred loss totals must sum in the loss kernel's order (stat_totals<NT>)");
 
 struct AdamTensor {
   int64_t p_off;      // master offset of element 0
@@ -751,7 +795,7 @@ struct AdamHyper {
   float beta1, beta2, eps, tau;
   int td3, delay;
   // statistics + counter advance folded into this kernel
-  const double* totals;  // loss totals of the step (this rank's, or the group's after the allreduce)
+  double* totals;  // loss totals of the step (this rank's, or the group's after the allreduce)
   const float* log_alpha;  // as of the start of the step (loss-kernel snapshot)
   StatsOut* stats;
   double target_entropy, B;
@@ -759,6 +803,8 @@ struct AdamHyper {
   const float* bc;      // bias corrections of this step (loss-kernel snapshot): [bc1 x 3 | bc2 x 3]
   int alpha_auto, critic_on, actor_on;
   int diag_nowork;  // diagnostics only (SPZ_DIAG_ADAM_NOWORK): statistics and counters, no parameter update
+  const double* stat_partials;  // deferred totals: the loss kernel's block partials (n_stat_blocks of them), summed by
+  int n_stat_blocks;            // every block; block 0 publishes them to `totals` (statistics, diagnostics)
   int prewait;      // 1: the loss totals / counter snapshot are complete before this kernel's grid-dependency wait
                     //    (their writer is >= 2 kernels back behind wait-before-trigger kernels; set by the plan)
 };
@@ -825,11 +871,18 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
   // three kernels back: complete once the weight-gradient kernel, this kernel's prerequisite, passed its own wait;
   // in a row-sharded group the non-PDL allreduce precedes this kernel, which then starts after it) and the skip
   // decision -- so after the wait only the split-K partials are loaded.
-  const double* tot = hp.totals;
+  __shared__ double stot[NSTAT];
+  __shared__ double sred[ADAM_NT / 32][NSTAT];
+  const double* tot = hp.n_stat_blocks > 0 ? stot : hp.totals;
   int64_t step = 0;
   float bc1 = 1.f, bc2 = 1.f;
   bool delayed = true;
   auto decide = [&]() {
+    if (hp.n_stat_blocks > 0) {
+      stat_totals<ADAM_NT>(hp.stat_partials, (unsigned)hp.n_stat_blocks, sred, stot);
+      __syncthreads();
+      if (blockIdx.x == 0 && threadIdx.x < NSTAT) hp.totals[threadIdx.x] = stot[threadIdx.x];
+    }
     step = __ldg(hp.snap);
     bc1 = __ldg(hp.bc + opt);
     bc2 = __ldg(hp.bc + 3 + opt);

@@ -83,6 +83,10 @@ static bool actor_bwd_unfused_env() {
 }
 
 // diagnostics: SPZ_FP32_SIMT=1 runs the FP32 precision path on the SIMT kernel instead of 3xTF32
+static bool defer_totals_off_env() {
+  const char* e = std::getenv("SPZ_DEFER_TOTALS");
+  return e && std::atoi(e) == 0;
+}
 static bool wgrad_pre_off_env() {
   const char* e = std::getenv("SPZ_WGRAD_PRE");
   return e && std::atoi(e) == 0;
@@ -878,6 +882,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     // dZ_L written by the loss kernel itself (one row per warp) at h <= 256 up to 16K local rows (WLK
     // 109.1 -> 108.2 us); larger batches do better with the separate critic_dz_kernel (ANT 319.5 -> 315.4 us)
     const bool dz_in_loss = h <= 256 && Bl <= 16384 && !dz_split_env();
+    const bool defer_totals = !(Lr->gsize > 1 || Lr->cfg.comm_mode == 2) && !lfused && !defer_totals_off_env();
     // diagnostics: SPZ_DIAG_LOSS=<rpw>,<blocks per SM> for the dZ-writing variant (rpw 1 or 2)
     int diag_rpw = 1, diag_cap = 4;
     if (const char* dl = std::getenv("SPZ_DIAG_LOSS")) std::sscanf(dl, "%d,%d", &diag_rpw, &diag_cap);
@@ -892,6 +897,12 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     {
       LossArgs la{};
       la.qp = qparts;
+      if (const char* dc = std::getenv("SPZ_DIAG_LOSS_CUT")) la.diag = std::atoi(dc);  // diagnostics only
+      // the grid-wide reduction of the statistics partials (a ticket and the last block's pass: ~5 us on the
+      // WLK critical path) moves into the optimizer, which needs the totals first, before its dependency wait;
+      // a row-sharded group all-reduces the totals first, so there the loss kernel keeps it (SPZ_DEFER_TOTALS=0:
+      // always here)
+      la.defer_totals = defer_totals ? 1 : 0;
       la.q2_no_actor = q2_skip_actor;
       la.v1 = v1;
       la.qps_tg = Lr->max_local;
@@ -973,7 +984,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         da.ld = h;
         da.mask_ld = mw;
         const int64_t nthr = da.rows * da.hv;
-        ops.push_back({"critic_loss", [da, nthr](cudaStream_t st) {
+        ops.push_back({"critic_head_dz", [da, nthr](cudaStream_t st) {
                          return launch_pdl(critic_dz_kernel<T>, dim3((unsigned)cdiv(nthr, 256)), dim3(256), 0, st, da);
                        }});
       }
@@ -1413,6 +1424,10 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       hp.td3 = td3;
       hp.delay = delay;
       hp.totals = Lr->statsum;
+      if (defer_totals) {
+        hp.stat_partials = Lr->stat_partials;
+        hp.n_stat_blocks = nblk;
+      }
       hp.log_alpha = reinterpret_cast<const float*>(Lr->ctr_snap + 4);
       hp.stats = Lr->d_stats;
       hp.target_entropy = Lr->cfg.target_entropy;

@@ -272,6 +272,8 @@ static int wgrad_splits_at(const spz_learner* Lr, int64_t Bl, int sms) {
     if (on) params += Lr->net[id].np;
   }
   const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(32, Bl / 256));
+  if (const char* e = std::getenv("SPZ_WGRAD_SC"))  // diagnostics: fixed split count
+    if (std::atoi(e) > 0) return std::min(std::atoi(e), smax);
   int best = 1;
   double best_cost = 0.0;
   for (int S = 1; S <= smax; ++S) {

@@ -10,11 +10,17 @@ C = 200_000
 g = spz.Replay(w.obs_dim, w.act_dim, C)
 g.push(**synthdata.transitions("locomotion", w.obs_dim, w.act_dim, C))
 lrn = spz.Learner(g, precision="bf16", hidden=w.hidden, n_hidden=w.n_hidden, max_batch=w.batch, use_graph=False)
-lrn.update(w.batch, 3)
+try:
+    lrn.update(w.batch, 3)
+except spz.SpzError as e:
+    print("warm-up:", str(e)[:80])
 idx = int(os.environ.get("TRACE_IDX", "1"))  # tc_gemm launches per WLK step: critic dgrad (0), wgrad (1)
 for rep in range(2):
     spz.spz_diag_tc_trace(idx + 2)
-    lrn.update(w.batch, 1)
+    try:
+        lrn.update(w.batch, 1)
+    except spz.SpzError as e:
+        print("update:", str(e)[:80])
     tr, tiles, cta = spz.spz_diag_tc_trace_tiles()
     cta = cta.astype(np.int64)
     spz.spz_diag_tc_trace(0)

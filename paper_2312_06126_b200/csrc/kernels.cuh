@@ -46,35 +46,52 @@ __device__ __forceinline__ uint4 pack_chunk(const float* src, int c0, int n) {
   return u;
 }
 
+__device__ __forceinline__ uint32_t smem_u32_(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// 16-byte asynchronous global -> shared copy (LDGSTS, L1 bypass) and its group fences
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32_(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Grid-stride over groups of GATHER_ROWS rows with NBUF shared-memory record buffers: the Philox indices and the
+// asynchronous record copies of the next group are issued before the current group is packed and stored, so
+// the random-row round trip to HBM overlaps the operand stores (large batches: several groups per block).
 template <typename T>
 __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ rec, int R, int o, int m,
                                                      const int64_t* __restrict__ fill_p, uint64_t seed,
                                                      const int64_t* __restrict__ step_p, int64_t row0, int Bl,
                                                      T* __restrict__ Xa, int lda, T* __restrict__ Xc, int ldc,
                                                      float* __restrict__ r, float* __restrict__ d,
-                                                     int32_t* __restrict__ idx_out, uint32_t* __restrict__ tags) {
+                                                     int32_t* __restrict__ idx_out, uint32_t* __restrict__ tags,
+                                                     int nbuf) {
   pdl_wait();
   pdl_launch();
   extern __shared__ float4 sm4[];
-  const float* sm = reinterpret_cast<const float*>(sm4);
-  __shared__ int64_t sidx[GATHER_ROWS];
-  const int j0 = blockIdx.x * GATHER_ROWS;
-  const int nr = min(GATHER_ROWS, Bl - j0);
+  __shared__ int64_t sidx[2][GATHER_ROWS];
   const int64_t fill = *fill_p;
   const uint64_t step = (uint64_t)*step_p;
-  if (threadIdx.x < nr) {
-    const int64_t i = sample_index(seed, step, (uint64_t)(row0 + j0 + threadIdx.x), (uint64_t)fill);
-    sidx[threadIdx.x] = i;
-    if (idx_out) idx_out[j0 + threadIdx.x] = (int32_t)i;
-    if (tags) atomicOr(&tags[i >> 5], 1u << (i & 31));  // transmission-loss tags (spz_replay_track)
-  }
-  __syncthreads();
   const int R4 = R >> 2;
-  for (int e = threadIdx.x; e < nr * R4; e += blockDim.x) {
-    const int rr = e / R4, q = e - rr * R4;
-    sm4[e] = __ldg(reinterpret_cast<const float4*>(rec + sidx[rr] * R) + q);
-  }
-  __syncthreads();
+  const int ngroups = (Bl + GATHER_ROWS - 1) / GATHER_ROWS;
+  // indices of group gi into sidx[b], then its records into buffer b (one commit group)
+  auto issue = [&](int gi, int b) {
+    const int j0 = gi * GATHER_ROWS;
+    const int nr = min(GATHER_ROWS, Bl - j0);
+    if (threadIdx.x < nr) {
+      const int64_t i = sample_index(seed, step, (uint64_t)(row0 + j0 + threadIdx.x), (uint64_t)fill);
+      sidx[b][threadIdx.x] = i;
+      if (idx_out) idx_out[j0 + threadIdx.x] = (int32_t)i;
+      if (tags) atomicOr(&tags[i >> 5], 1u << (i & 31));  // transmission-loss tags (spz_replay_track)
+    }
+    __syncthreads();
+    float4* buf = sm4 + (size_t)b * GATHER_ROWS * R4;
+    for (int e = threadIdx.x; e < nr * R4; e += blockDim.x) {
+      const int rr = e / R4, q = e - rr * R4;
+      cp_async16(buf + e, reinterpret_cast<const float4*>(rec + sidx[b][rr] * R) + q);
+    }
+    cp_async_commit();
+  };
   // 16-byte chunks per operand row, rounded up to whole 32-byte sectors (and capped by the row pitch)
   constexpr int EPC = 16 / sizeof(T), EPS = 32 / sizeof(T);
   const int s2c = o + m + 2;
@@ -82,35 +99,53 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ r
   const int cb = min((o + m + EPS - 1) / EPS * EPS, ldc) / EPC;      // [s | a]
   const int cs = min((o + EPS - 1) / EPS * EPS, ldc) / EPC;
   const int J = 2 * ca + cb + 2 * cs;                                 // chunks per row
-  for (int e = threadIdx.x; e < nr * J; e += blockDim.x) {
-    const int rr = e / J;
-    int k = e - rr * J;
-    const float* rw = sm + rr * R;
-    const int64_t j = j0 + rr;
-    uint4* dst;
-    uint4 v;
-    if (k < ca) {  // Xa s2 row
-      dst = reinterpret_cast<uint4*>(Xa + j * lda) + k;
-      v = pack_chunk<T>(rw + s2c, k * EPC, o);
-    } else if ((k -= ca) < ca) {  // Xa s row
-      dst = reinterpret_cast<uint4*>(Xa + (Bl + j) * lda) + k;
-      v = pack_chunk<T>(rw, k * EPC, o);
-    } else if ((k -= ca) < cb) {  // Xc [s | a]
-      dst = reinterpret_cast<uint4*>(Xc + j * ldc) + k;
-      v = pack_chunk<T>(rw, k * EPC, o + m);
-    } else if ((k -= cb) < cs) {  // Xc [s | a~ later]
-      dst = reinterpret_cast<uint4*>(Xc + (Bl + j) * ldc) + k;
-      v = pack_chunk<T>(rw, k * EPC, o);
-    } else {  // Xc [s2 | a' later]
-      k -= cs;
-      dst = reinterpret_cast<uint4*>(Xc + (2 * (int64_t)Bl + j) * ldc) + k;
-      v = pack_chunk<T>(rw + s2c, k * EPC, o);
+  int it = 0;
+  if ((int)blockIdx.x < ngroups) issue(blockIdx.x, 0);
+  for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x, ++it) {
+    const int b = nbuf > 1 ? (it & 1) : 0;
+    const int gn = gi + (int)gridDim.x;
+    if (nbuf > 1 && gn < ngroups) {
+      issue(gn, b ^ 1);   // the next group's copies in flight while this one is stored
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-    *dst = v;
-  }
-  if (threadIdx.x < nr) {
-    r[j0 + threadIdx.x] = sm[threadIdx.x * R + o + m];
-    d[j0 + threadIdx.x] = sm[threadIdx.x * R + o + m + 1];
+    __syncthreads();
+    const int j0 = gi * GATHER_ROWS;
+    const int nr = min(GATHER_ROWS, Bl - j0);
+    const float* sm = reinterpret_cast<const float*>(sm4 + (size_t)b * GATHER_ROWS * R4);
+    for (int e = threadIdx.x; e < nr * J; e += blockDim.x) {
+      const int rr = e / J;
+      int k = e - rr * J;
+      const float* rw = sm + rr * R;
+      const int64_t j = j0 + rr;
+      uint4* dst;
+      uint4 v;
+      if (k < ca) {  // Xa s2 row
+        dst = reinterpret_cast<uint4*>(Xa + j * lda) + k;
+        v = pack_chunk<T>(rw + s2c, k * EPC, o);
+      } else if ((k -= ca) < ca) {  // Xa s row
+        dst = reinterpret_cast<uint4*>(Xa + (Bl + j) * lda) + k;
+        v = pack_chunk<T>(rw, k * EPC, o);
+      } else if ((k -= ca) < cb) {  // Xc [s | a]
+        dst = reinterpret_cast<uint4*>(Xc + j * ldc) + k;
+        v = pack_chunk<T>(rw, k * EPC, o + m);
+      } else if ((k -= cb) < cs) {  // Xc [s | a~ later]
+        dst = reinterpret_cast<uint4*>(Xc + (Bl + j) * ldc) + k;
+        v = pack_chunk<T>(rw, k * EPC, o);
+      } else {  // Xc [s2 | a' later]
+        k -= cs;
+        dst = reinterpret_cast<uint4*>(Xc + (2 * (int64_t)Bl + j) * ldc) + k;
+        v = pack_chunk<T>(rw + s2c, k * EPC, o);
+      }
+      *dst = v;
+    }
+    if (threadIdx.x < nr) {
+      r[j0 + threadIdx.x] = sm[threadIdx.x * R + o + m];
+      d[j0 + threadIdx.x] = sm[threadIdx.x * R + o + m + 1];
+    }
+    __syncthreads();  // buffer b (and sidx[b]) free for the group after next
+    if (nbuf == 1 && gn < ngroups) issue(gn, 0);
   }
 }
 
@@ -259,7 +294,9 @@ struct LossArgs {
   int Bl, td3, delay, loss_rows, actor_rows, h, ld, mask_ld;
   int q2_no_actor;        // TD3: Q2 has no actor rows (its dZ_L there is never read)
   int defer_totals;       // 1: no grid-wide reduction here -- the optimizer sums the block partials itself (off the
-                          //    critical path, before its dependency wait); block 0 writes the optimizer snapshot
+                          //    critical path, before its dependency wait); block 0 writes the optimizer snapshot;
+  unsigned* bad2;         //    a block with a non-finite partial ORs 1 into bad2[step & 1] (block 0 clears the
+                          //    other word for the next step), so the optimizer's blocks decide without the totals
   int diag;               // diagnostics only (SPZ_DIAG_LOSS_CUT; results are wrong): 1 skip the grid-wide statistics
                           // reduction, 2 no work at all
   // SAC v1 (reading #24): qt1 = qt2 = V'(s2) and the bootstrap drops the entropy term; the actor rows
@@ -486,6 +523,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
     double t = 0.0;
     for (int k = 0; k < LOSS_NT / 32; ++k) t += red[k][threadIdx.x];
     a.partials[blockIdx.x * NSTAT + threadIdx.x] = t;
+    if (a.defer_totals && !isfinite(t)) atomicOr(a.bad2 + (*a.step_p & 1), 1u);
   }
   // the last block sums every block's partial (fixed order: strided per thread, then a fixed tree)
   __syncthreads();
@@ -493,6 +531,7 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   if (a.defer_totals) {
     // the optimizer reduces the partials (stat_totals, same order); the snapshot depends on no other block
     if (blockIdx.x == 0) {
+      if (threadIdx.x == 15) a.bad2[(*a.step_p + 1) & 1] = 0u;
       if (threadIdx.x < 4) a.ctr_snap[threadIdx.x] = a.step_p[threadIdx.x];
       if (threadIdx.x == 4) *a.la_snap = *a.log_alpha;
       if (threadIdx.x >= 8 && threadIdx.x < 14) {
@@ -708,6 +747,9 @@ struct StatsOut {
 #ifndef SPZ_ADAM_NT
 #define SPZ_ADAM_NT 256
 #endif
+#ifndef SPZ_ADAM_CH4
+#define SPZ_ADAM_CH4 8  // float4 split partials loaded per round (16: slower at TD3 / HUM, profiles/r02_adam_ab2.txt)
+#endif
 #ifndef SPZ_ADAM_MINB
 #define SPZ_ADAM_MINB 4
 #endif
@@ -767,7 +809,7 @@ __device__ __forceinline__ float4 partial_sum4(const float* __restrict__ partial
   }
   const float4* src = reinterpret_cast<const float4*>(partials + idx);
   const int ps4 = pstride >> 2;
-  constexpr int CH = 8;
+  constexpr int CH = SPZ_ADAM_CH4;
   float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s0 = 0; s0 < n_partials; s0 += CH) {
     float4 t[CH];
@@ -804,7 +846,8 @@ struct AdamHyper {
   int alpha_auto, critic_on, actor_on;
   int diag_nowork;  // diagnostics only (SPZ_DIAG_ADAM_NOWORK): statistics and counters, no parameter update
   const double* stat_partials;  // deferred totals: the loss kernel's block partials (n_stat_blocks of them), summed by
-  int n_stat_blocks;            // every block; block 0 publishes them to `totals` (statistics, diagnostics)
+  int n_stat_blocks;            // block 0 (publishes them to `totals`: statistics, diagnostics) and the log-alpha
+  const unsigned* bad2;         // block; every other block decides from bad2[step & 1] (a partial was non-finite)
   int prewait;      // 1: the loss totals / counter snapshot are complete before this kernel's grid-dependency wait
                     //    (their writer is >= 2 kernels back behind wait-before-trigger kernels; set by the plan)
 };
@@ -877,8 +920,9 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
   int64_t step = 0;
   float bc1 = 1.f, bc2 = 1.f;
   bool delayed = true;
+  const bool need_totals = hp.n_stat_blocks > 0 && (blockIdx.x == 0 || opt == 2);
   auto decide = [&]() {
-    if (hp.n_stat_blocks > 0) {
+    if (need_totals) {
       stat_totals<ADAM_NT>(hp.stat_partials, (unsigned)hp.n_stat_blocks, sred, stot);
       __syncthreads();
       if (blockIdx.x == 0 && threadIdx.x < NSTAT) hp.totals[threadIdx.x] = stot[threadIdx.x];
@@ -888,9 +932,12 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
     bc2 = __ldg(hp.bc + 3 + opt);
     if (hp.td3) delayed = ((step + 1) % hp.delay) == 0;
     if (threadIdx.x == 0) {
-      // the step's losses are finite iff their totals are (B > 0); TD3 has no log-prob total
-      const bool bad = !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) ||
-                       (!hp.td3 && !isfinite(tot[4])) || !isfinite(tot[5]);
+      // the step's losses are finite iff their totals are (B > 0); TD3 has no log-prob total.  Deferred totals:
+      // iff every block partial is (the loss kernel's flag word), except where this block summed them anyway
+      const bool bad = hp.n_stat_blocks > 0 && !need_totals
+                           ? __ldcg(hp.bad2 + (step & 1)) != 0u
+                           : !isfinite(tot[0]) || !isfinite(tot[1]) || !isfinite(tot[2]) || !isfinite(tot[3]) ||
+                                 (!hp.td3 && !isfinite(tot[4])) || !isfinite(tot[5]);
       const int f = *flag;
       if (bad && blockIdx.x == 0) atomicExch(flag, 1);
       skip = bad || f;  // halted: parameters stay at the state before the failing step

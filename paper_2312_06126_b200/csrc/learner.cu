@@ -527,12 +527,20 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       float *rr = Lr->r, *dd = Lr->d;
       int32_t* idx = Lr->idx;
       uint32_t* tags = Lr->ring->tags;
-      const size_t smem = (size_t)GATHER_ROWS * R * sizeof(float);  // <= 227 KB (checked by spz_replay_create)
+      // two record buffers per block (the next group's copies in flight while one is stored) where they fit
+      const size_t smem1 = (size_t)GATHER_ROWS * R * sizeof(float);  // <= 227 KB (checked by spz_replay_create)
+      const int nbuf = 2 * smem1 <= 200 * 1024 ? 2 : 1;
+      const size_t smem = nbuf * smem1;
       if (smem > 48 * 1024)
         SPZ_CUDA_TRY(cudaFuncSetAttribute(gather_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int nsm_g = 148, dev_g = 0;
+      cudaGetDevice(&dev_g);
+      cudaDeviceGetAttribute(&nsm_g, cudaDevAttrMultiProcessorCount, dev_g);
+      // grid-stride: at most 4 blocks per SM (one group each at WLK; 3-7 pipelined groups at HUM / TD3)
+      const unsigned ngrid = (unsigned)std::min<int64_t>(cdiv(Bl, GATHER_ROWS), 4 * (int64_t)nsm_g);
       ops.push_back({"gather", [=](cudaStream_t st) {
-                       launch_pdl(gather_kernel<T>, dim3((unsigned)cdiv(Bl, GATHER_ROWS)), dim3(256), smem, st, 
-                           rec, R, o, m, fill, seed, stp, row0, Bl, Xa, lda, Xc, ldc, rr, dd, idx, tags);
+                       launch_pdl(gather_kernel<T>, dim3(ngrid), dim3(256), smem, st,
+                           rec, R, o, m, fill, seed, stp, row0, Bl, Xa, lda, Xc, ldc, rr, dd, idx, tags, nbuf);
                        return cudaGetLastError();
                      }});
     }
@@ -905,6 +913,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       // a row-sharded group all-reduces the totals first, so there the loss kernel keeps it (SPZ_DEFER_TOTALS=0:
       // always here)
       la.defer_totals = defer_totals ? 1 : 0;
+      la.bad2 = Lr->tickets + 200;  // two words past the ticket counters (<= 1 + 19 in use)
       la.q2_no_actor = q2_skip_actor;
       la.v1 = v1;
       la.qps_tg = Lr->max_local;
@@ -1307,6 +1316,9 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       std::vector<AdamTensor> tens;
       std::vector<AdamSegment> segs;
       for (auto& s : slots) {
+        // TD3, non-delayed step: the actor is not updated -- no segments for it (their blocks would only load
+        // its optimizer state: 35 MB per step at the TD3 config); row-sharded groups keep one buffer layout
+        if (td3 && !actor_step && s.net == NET_ACTOR && !sharded) continue;
         const NetLayout& n = Lr->net[s.net];
         AdamTensor t{};
         t.p_off = Lr->pbase[s.net] + (s.weight ? n.w[s.layer] : n.b[s.layer]);
@@ -1374,6 +1386,11 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
         return v;
       };
       segs = segments(tens);
+      if (segs.empty()) {  // (the TD3 actor role on a non-delayed step) one empty block: statistics and counters
+        AdamSegment sg{};
+        sg.t.s_off = sg.t.t_off = sg.t.ts_off = -1;
+        segs.push_back(sg);
+      }
       const int nsegs = (int)segs.size();
       if (4 * (nsegs + 1) > Lr->max_segs) return fail(SPZ_EINVAL, "internal: Adam table overflow");
       const size_t sb = segs.size() * sizeof(AdamSegment);
@@ -1429,6 +1446,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       if (defer_totals) {
         hp.stat_partials = Lr->stat_partials;
         hp.n_stat_blocks = nblk;
+        hp.bad2 = Lr->tickets + 200;
       }
       hp.log_alpha = reinterpret_cast<const float*>(Lr->ctr_snap + 4);
       hp.stats = Lr->d_stats;

@@ -451,12 +451,14 @@ def test_oversized_record_rejected():
 
 
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
-@pytest.mark.parametrize("o,m,B", [(22, 6, 1000), (3, 1, 256), (44, 17, 777)])
+@pytest.mark.parametrize("o,m,B", [(22, 6, 1000), (3, 1, 256), (44, 17, 777), (44, 17, 30000), (400, 17, 20000)])
 def test_learner_gather_operands_bit_exact(precision, o, m, B):
     """a1-a2 inside the update: the step's indices equal the oracle's, and the gathered operands are
     exactly the sampled records rounded once to the operand type (bf16 RNE / fp32), with every padding
-    column zero (written once at allocation, never by the 128-bit vector stores)."""
-    g, r = make_rings(o, m, 5000)
+    column zero (written once at allocation, never by the 128-bit vector stores).  B 30000 / 20000: more
+    32-row groups than 4 blocks per SM, so blocks walk several groups -- double-buffered asynchronous record
+    copies (44-float observations), single buffer (400: two 105 KB buffers do not fit)."""
+    g, r = make_rings(o, m, max(5000, B))
     lrn = spz.Learner(g, precision=precision, hidden=64, n_hidden=2, max_batch=B)
     for k in range(2):
         lrn.update(B, 1)
@@ -476,3 +478,39 @@ def test_learner_gather_operands_bit_exact(precision, o, m, B):
         assert np.array_equal(Xc[B:2 * B, :o], rnd(rb["obs"])) and np.array_equal(Xc[2 * B:, :o], rnd(rb["next_obs"]))
         assert not Xc[:, o + m:].any()
         assert np.array_equal(lrn.debug("r")[:B], rb["rew"]) and np.array_equal(lrn.debug("d")[:B], rb["done"])
+
+
+@pytest.mark.parametrize("algo,precision,B", [("sac", "bf16", 2048), ("sac", "fp32", 512), ("td3", "bf16", 2048),
+                                              ("sac", "bf16", 40000)])
+def test_nonfinite_loss_halts_before_the_step(algo, precision, B):
+    """A non-finite loss (NaN rewards in the ring) halts the learner at the state before the failing step
+    (SPEC S:68): SPZ_ENONFINITE from that update, every trained tensor unchanged, the step counter not
+    advanced, and every later update refused -- with the loss totals deferred to the optimizer (its blocks decide
+    from the loss kernel's non-finite flag word) as with the in-kernel reduction (B 40000: one block per row group
+    past the resident grid)."""
+    o, m, C = 22, 6, 50_000
+    g = spz.Replay(o, m, C)
+    tr = synthdata.transitions("locomotion", o, m, C)
+    g.push(**tr)
+    lrn = spz.Learner(g, algo=algo, precision=precision, hidden=256, n_hidden=2, max_batch=B)
+    lrn.update(B, 2)
+    before = [lrn.get(n) for n in ("actor", "q1", "q2", "q1_targ")]
+    step0 = lrn.counters()["step"]
+    bad = dict(tr)
+    bad["rew"] = np.array(tr["rew"], copy=True)
+    bad["rew"][::7] = np.nan  # every 7th transition: sampled in any batch of this size
+    g2 = spz.Replay(o, m, C)
+    g2.push(**bad)
+    lrn2 = spz.Learner(g2, algo=algo, precision=precision, hidden=256, n_hidden=2, max_batch=B)
+    for name, v in zip(("actor", "q1", "q2", "q1_targ"), before):
+        lrn2.set(name, v)
+    with pytest.raises(spz.SpzError) as e:
+        lrn2.update(B, 1)
+    assert e.value.status == spz.SPZ_ENONFINITE
+    for name, v in zip(("actor", "q1", "q2", "q1_targ"), before):
+        assert np.array_equal(lrn2.get(name), v), name
+    assert lrn2.counters()["step"] == 0
+    with pytest.raises(spz.SpzError) as e2:
+        lrn2.update(B, 1)
+    assert e2.value.status == spz.SPZ_ENONFINITE
+    assert step0 == 2

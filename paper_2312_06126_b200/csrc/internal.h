@@ -73,6 +73,8 @@ struct spz_replay {
   cudaEvent_t ev_copy = nullptr;       // pinned push: the caller's buffers have been read (H2D done)
   bool copy_pending = false;           // spz_replay_push_async: ev_copy not yet waited for
   cudaEvent_t ev_pack = nullptr;       // the last push's records are in `rec`
+  uint64_t pack_gen = 0;               // packs enqueued on the ring's own stream and not synchronised by the push
+                                       // (a learner waits on ev_pack only when this moved since its last wait)
   std::vector<cudaEvent_t> readers;    // one per learner: its last enqueued update (registered at create)
   // experience transmission loss (spz_replay_track): one "sampled" bit per slot, set by every sample;
   // a push counts the unsampled records it overwrites (device) and the records that never land (host)

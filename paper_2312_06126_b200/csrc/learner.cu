@@ -72,8 +72,14 @@ static bool dz_split_env() {
 
 // copies the read-back block into host-mapped memory (spz_update_async)
 __global__ void publish_kernel(const unsigned long long* __restrict__ src, unsigned long long* dst, int words) {
+  pdl_wait();  // (launched programmatically behind the update's last kernel where SPZ_PUBLISH_PDL is on)
   for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
-  __threadfence_system();
+  // no system-scope fence: the host reads the slot only after the event recorded behind this kernel completed
+  // (stream order makes the kernel's writes to mapped host memory visible by then)
+}
+static bool publish_pdl_env() {
+  const char* e = std::getenv("SPZ_PUBLISH_PDL");
+  return !(e && std::atoi(e) == 0);
 }
 
 // diagnostics: SPZ_ACTOR_BWD_UNFUSED=1 runs the actor backward as separate GEMM / head launches
@@ -140,6 +146,7 @@ struct spz_learner {
   int64_t* counters = nullptr;  // step, t_critic, t_actor, t_alpha
   int* d_flag = nullptr;
   cudaEvent_t ev_read = nullptr;  // recorded after every enqueued update: ring pushes wait on it
+  uint64_t seen_pack_gen = 0;     // ring->pack_gen at this learner's last wait on ev_pack
   // spz_update_async keeps up to two updates in flight; each owns a pinned slot for its read-back
   // device read-back block: the step statistics, counters and non-finite flag, contiguous so one copy
   // returns them
@@ -212,6 +219,7 @@ struct spz_learner {
   int64_t plan_B = -1;
   std::vector<Op> ops[2];  // [0] = plain step, [1] = TD3 delayed step (SAC uses [0] only)
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  cudaGraphExec_t exec_pub[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // + read-back publish to host slot [s]
   int n_adam_segs = 0;
   uint64_t sync_version = 0;
   uint64_t* h_sync = nullptr;  // pinned: the publication's seq / header words (spz_sync_actor)
@@ -382,6 +390,9 @@ spz_learner::~spz_learner() {
   comm_destroy(&comm);
   for (auto& e : exec)
     if (e) cudaGraphExecDestroy(e);
+  for (auto& ev : exec_pub)
+    for (auto& e : ev)
+      if (e) cudaGraphExecDestroy(e);
   for (void* p : allocs) cudaFree(p);
   if (h_stats) cudaFreeHost(h_stats);
   if (h_slots) cudaFreeHost(h_slots);
@@ -406,6 +417,12 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       cudaGraphExecDestroy(e);
       e = nullptr;
     }
+  for (auto& ev : Lr->exec_pub)
+    for (auto& e : ev)
+      if (e) {
+        cudaGraphExecDestroy(e);
+        e = nullptr;
+      }
   // rows of this rank: contiguous share of the global batch inside its group (spz_plan_rank, DESIGN.md
   // reading #17); with split roles the critic group is ranks [0, n_critic) and the actor group the rest
   spz_plan plan;
@@ -1529,6 +1546,15 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
   return SPZ_OK;
 }
 
+static cudaError_t enqueue_publish(spz_learner* Lr, int slot, cudaStream_t st) {
+  constexpr int W = (int)(sizeof(spz_learner::ReadBack) / 8);
+  unsigned long long* dst = Lr->d_slots + (size_t)slot * (sizeof(spz_learner::HostSlot) / 8);
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(Lr->d_rb);
+  if (publish_pdl_env()) return launch_pdl(publish_kernel, dim3(1), dim3(32), 0, st, src, dst, W);
+  publish_kernel<<<1, 32, 0, st>>>(src, dst, W);
+  return cudaGetLastError();
+}
+
 static spz_status run_ops(spz_learner* Lr, int variant, cudaStream_t st) {
   for (auto& op : Lr->ops[variant]) {
     cudaError_t e = op.fn(st);
@@ -1537,13 +1563,22 @@ static spz_status run_ops(spz_learner* Lr, int variant, cudaStream_t st) {
   return SPZ_OK;
 }
 
-static spz_status ensure_graph(spz_learner* Lr, int variant) {
-  if (Lr->exec[variant]) return SPZ_OK;
+static cudaError_t enqueue_publish(spz_learner* Lr, int slot, cudaStream_t st);
+// One step of `variant` as a CUDA graph; pub_slot >= 0: the graph ends with the read-back publish into host slot
+// pub_slot (a programmatically launched node behind the optimizer: no stream operation between consecutive
+// updates, where a separate launch cost ~4 us per step of the end-to-end loop)
+static spz_status ensure_graph(spz_learner* Lr, int variant, int pub_slot = -1) {
+  cudaGraphExec_t& ex = pub_slot < 0 ? Lr->exec[variant] : Lr->exec_pub[variant][pub_slot];
+  if (ex) return SPZ_OK;
   cudaStream_t cs;
   SPZ_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   cudaGraph_t g = nullptr;
   SPZ_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   spz_status s = run_ops(Lr, variant, cs);
+  if (s == SPZ_OK && pub_slot >= 0) {
+    const cudaError_t pe = enqueue_publish(Lr, pub_slot, cs);
+    if (pe != cudaSuccess) s = fail(SPZ_ECUDA, std::string("publish: ") + cudaGetErrorString(pe));
+  }
   cudaError_t e = cudaStreamEndCapture(cs, &g);
   cudaStreamDestroy(cs);
   if (s != SPZ_OK) {
@@ -1551,7 +1586,7 @@ static spz_status ensure_graph(spz_learner* Lr, int variant) {
     return s;
   }
   if (e != cudaSuccess) return fail(SPZ_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-  e = cudaGraphInstantiate(&Lr->exec[variant], g, 0);
+  e = cudaGraphInstantiate(&ex, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return fail(SPZ_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
   return SPZ_OK;
@@ -2031,33 +2066,43 @@ spz_status spz_update_async(spz_learner* Lr, int64_t batch, int64_t n_steps) {
   // the last pinned push's deferred pack: on this learner's stream right before its steps when it is
   // the ring's only reader (stream order already follows its own earlier reads), else on the ring
   // stream after every reader; then the records (and the fill they leave on the device) are in place
+  bool wait_pack = false;
   {
     std::lock_guard<std::mutex> lk(Lr->ring->mu);
     if (Lr->ring->pend.active) {
       if (Lr->ring->readers.size() == 1) SPZ_CUDA_TRY(ring_enqueue_pack(Lr->ring, Lr->stream));
       else SPZ_CUDA_TRY(ring_flush_pending(Lr->ring));
     }
+    // a pack on the ring's stream that no push synchronised: wait for it (a pack on this stream is ordered
+    // already, a synchronous push returned after its records landed); otherwise no cross-stream wait between
+    // consecutive updates
+    static const bool always = std::getenv("SPZ_PACK_WAIT_ALWAYS") != nullptr;  // A/B diagnostics
+    wait_pack = always || Lr->ring->pack_gen != Lr->seen_pack_gen;
+    Lr->seen_pack_gen = Lr->ring->pack_gen;
   }
-  SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));
+  if (wait_pack) SPZ_CUDA_TRY(cudaStreamWaitEvent(Lr->stream, Lr->ring->ev_pack, 0));
+  static const bool pub_sep = std::getenv("SPZ_PUBLISH_SEPARATE") != nullptr;  // A/B: the separate launch
+  bool published = false;
   for (int64_t k = 0; k < n_steps; ++k, ++step) {
     const int v = variant_of(Lr, step);
     if (Lr->cfg.use_graph) {
-      SPZ_TRY(ensure_graph(Lr, v));
-      SPZ_CUDA_TRY(cudaGraphLaunch(Lr->exec[v], Lr->stream));
+      const int ps = k == n_steps - 1 && !pub_sep ? sl : -1;  // the call's last step publishes the read-back
+      SPZ_TRY(ensure_graph(Lr, v, ps));
+      SPZ_CUDA_TRY(cudaGraphLaunch(ps < 0 ? Lr->exec[v] : Lr->exec_pub[v][ps], Lr->stream));
+      published = ps >= 0;
     } else {
       SPZ_TRY(run_ops(Lr, v, Lr->stream));
     }
   }
-  SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_read, Lr->stream));  // pushes overwrite records only after these reads
   // read-back of the statistics, counters and flag: a one-warp kernel writing host-mapped memory (a
-  // device-to-host copy costs more stream time between consecutive updates)
-  {
-    constexpr int W = (int)(sizeof(spz_learner::ReadBack) / 8);
-    unsigned long long* dst = Lr->d_slots + (size_t)sl * (sizeof(spz_learner::HostSlot) / 8);
-    publish_kernel<<<1, 32, 0, Lr->stream>>>(reinterpret_cast<const unsigned long long*>(Lr->d_rb), dst, W);
+  // device-to-host copy costs more stream time between consecutive updates) -- the last step graph's final node,
+  // else (no graph, no steps) launched here
+  if (!published) {
+    SPZ_CUDA_TRY(enqueue_publish(Lr, sl, Lr->stream));
     SPZ_CUDA_TRY(cudaGetLastError());
-    (void)hs;
   }
+  (void)hs;
+  SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_read, Lr->stream));  // pushes overwrite records only after these reads
   SPZ_CUDA_TRY(cudaEventRecord(Lr->ev_slot[sl], Lr->stream));
   Lr->inflight[Lr->n_inflight++] = sl;
   Lr->host_step = step;

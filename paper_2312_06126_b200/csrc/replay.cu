@@ -164,6 +164,7 @@ cudaError_t ring_enqueue_pack(spz_replay* r, cudaStream_t st) {
                                               r->d_fill, p.fill_after);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaEventRecord(r->ev_pack, st);
+  if (st == r->stream) ++r->pack_gen;
   if (e == cudaSuccess) e = cudaEventRecord(r->ev_stage_free[p.stage], st);
   p.active = false;
   return e;

@@ -798,6 +798,7 @@ __device__ __forceinline__ float partial_sum(const float* __restrict__ partials,
   return g;
 }
 // The same for 4 consecutive elements i..i+3 of one row, contiguous and 16-byte aligned in every partial.
+template <int CH = SPZ_ADAM_CH4>
 __device__ __forceinline__ float4 partial_sum4(const float* __restrict__ partials, int n_partials, int pstride, int pld,
                                                int cols, int i) {
   int idx;
@@ -809,7 +810,6 @@ __device__ __forceinline__ float4 partial_sum4(const float* __restrict__ partial
   }
   const float4* src = reinterpret_cast<const float4*>(partials + idx);
   const int ps4 = pstride >> 2;
-  constexpr int CH = SPZ_ADAM_CH4;
   float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s0 = 0; s0 < n_partials; s0 += CH) {
     float4 t[CH];
@@ -864,8 +864,10 @@ __device__ __forceinline__ void store4(float* d, float4 x) { *reinterpret_cast<f
 // advances the counters from the loss kernel's snapshot -- no block reads `counters` here, so no
 // grid-wide handshake is needed.  (A non-finite gradient element sets the sticky flag 2: the step
 // itself counts, every later step is skipped.)
-template <typename T>
-__global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(const AdamSegment* __restrict__ segs, AdamHyper hp,
+// WIDE (small grids, at most two blocks per SM, e.g. WLK's 232): all <= 16 float4 split partials of a thread in one
+// round (64 registers of loads; 2 blocks per SM) -- large grids keep 8 per round at 4 blocks per SM
+template <typename T, bool WIDE>
+__global__ void __launch_bounds__(ADAM_NT, WIDE ? 2 : SPZ_ADAM_MINB) adam_polyak_kernel(const AdamSegment* __restrict__ segs, AdamHyper hp,
                                                                  float* __restrict__ P, float* __restrict__ Mo,
                                                                  float* __restrict__ Vo, T* __restrict__ S,
                                                                  int64_t* __restrict__ counters,  // step, t_c, t_a, t_al
@@ -950,7 +952,7 @@ __global__ void __launch_bounds__(ADAM_NT, SPZ_ADAM_MINB) adam_polyak_kernel(con
   if (!hp.prewait) decide();
   // after the wait: this step's gradient partials
   if (vec) {
-    if (k4 < count) g4 = partial_sum4(partials, n_partials, pstride, pld, cols, start + k4);
+    if (k4 < count) g4 = partial_sum4<WIDE ? 16 : SPZ_ADAM_CH4>(partials, n_partials, pstride, pld, cols, start + k4);
   } else {
 #pragma unroll
     for (int u = 0; u < ADAM_EPT; ++u) {

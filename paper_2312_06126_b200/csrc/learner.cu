@@ -1489,8 +1489,20 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       int64_t* ctr = Lr->counters;
       int* fl = Lr->d_flag;
       const unsigned nseg = (unsigned)segs.size();
+      // one round of split-partial loads where the grid is at most two blocks per SM and some tensor has more
+      // than 8 splits (SPZ_ADAM_WIDE=0 / 1 forces)
+      int max_parts = 0;
+      for (const AdamSegment& sg : segs) max_parts = std::max(max_parts, (int)sg.t.n_partials);
+      int nsm_a = 148, dev_a = 0;
+      cudaGetDevice(&dev_a);
+      cudaDeviceGetAttribute(&nsm_a, cudaDevAttrMultiProcessorCount, dev_a);
+      bool wide = (int)nseg <= 2 * nsm_a && max_parts > SPZ_ADAM_CH4;
+      if (const char* aw = std::getenv("SPZ_ADAM_WIDE")) wide = std::atoi(aw) == 1;
       ops.push_back({"adam_polyak", [=](cudaStream_t st) {
-                       return launch_pdl(adam_polyak_kernel<T>, dim3(nseg), dim3(ADAM_NT), 0, st, (const AdamSegment*)ds, hp, Pm,
+                       if (wide)
+                         return launch_pdl(adam_polyak_kernel<T, true>, dim3(nseg), dim3(ADAM_NT), 0, st, (const AdamSegment*)ds, hp, Pm,
+                                           Mm, Vm, S, ctr, fl);
+                       return launch_pdl(adam_polyak_kernel<T, false>, dim3(nseg), dim3(ADAM_NT), 0, st, (const AdamSegment*)ds, hp, Pm,
                                          Mm, Vm, S, ctr, fl);
                      }});
     }

@@ -187,6 +187,23 @@ __device__ __forceinline__ uint32_t gt0_mask(float x) {
   return d;
 }
 
+// Packed fp32 pair arithmetic (sm_100 FADD2 / FFMA2: one issue slot per two elements, each lane
+// rounded exactly as the scalar FADD / FFMA would round it).
+__device__ __forceinline__ void add2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n.reg .b64 a, b, d;\nmov.b64 a, {%2, %3};\nmov.b64 b, {%4, %5};\nadd.rn.f32x2 d, a, b;\nmov.b64 {%0, %1}, d;\n}"
+      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n.reg .b64 a, b, d;\nmov.b64 a, {%2, %3};\nmov.b64 b, {%4, %5};\nmov.b64 d, {%0, %1};\nfma.rn.f32x2 d, a, b, d;\nmov.b64 {%0, %1}, d;\n}"
+      : "+f"(d0), "+f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+// ReLU-mask bits j, j + 1 of a pre-activation pair (p > 0), as selected constants (FSETP + SEL each,
+// merged by one three-input add / or per pair)
+__device__ __forceinline__ uint32_t mask_pair(float p0, float p1, int j) {
+  const uint32_t s0 = p0 > 0.f ? (1u << j) : 0u, s1 = p1 > 0.f ? (2u << j) : 0u;
+  return s0 | s1;
+}
+
 // ------------------------------------------------------------------ host side
 int num_sms() {
   static int n = [] {

@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __g
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[b]);
       } else {
-        float dot = 0.f;
+        float dot2[2] = {0.f, 0.f};  // row-dot partials of the even / odd columns
         uint8_t* wstage = stage_s + e * 4096;
 #pragma unroll
         for (int ib = 0; ib < S::NB; ++ib) {
@@ -510,15 +510,25 @@ __global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __g
           for (int cc = 0; cc < S::CPB; ++cc) {
             const int cl = ib * S::CPB + cc;  // chunk within this warp's slice
             if (cl >= S::CPW) break;          // past the tile (BN = 16): stays zero
+            if constexpr (S::RELU) {
+              // columns past N: zero-filled B rows and zero bias -> pre = 0 -> bit 0, value 0.  Column
+              // pairs in packed fp32 (FADD2 / FFMA2); the row dot keeps even / odd column partials.
+#pragma unroll
+              for (int j = 0; j < 16; j += 2) {
+                const float2 b2 = *reinterpret_cast<const float2*>(bias_s + cl * 16 + j);
+                const float2 w2 = *reinterpret_cast<const float2*>(dot_s + cl * 16 + j);
+                float p0, p1;
+                add2(p0, p1, v[cc][j], v[cc][j + 1], b2.x, b2.y);
+                word |= mask_pair(p0, p1, 16 * cc + j);
+                v[cc][j] = fmaxf(p0, 0.f);
+                v[cc][j + 1] = fmaxf(p1, 0.f);
+                fma2(dot2[0], dot2[1], v[cc][j], v[cc][j + 1], w2.x, w2.y);
+              }
+              continue;
+            }
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              if constexpr (S::RELU) {
-                // columns past N: zero-filled B rows and zero bias -> pre = 0 -> bit 0, value 0
-                const float pre = v[cc][j] + bias_s[cl * 16 + j];
-                word |= gt0_mask(pre) & (1u << (16 * cc + j));
-                v[cc][j] = fmaxf(pre, 0.f);
-                dot = fmaf(v[cc][j], dot_s[cl * 16 + j], dot);
-              } else if constexpr (S::MASKB) {
+              if constexpr (S::MASKB) {
                 v[cc][j] = (mw[ib] >> (16 * cc + j)) & 1u ? v[cc][j] : 0.f;
               } else if constexpr (S::BIAS) {
                 v[cc][j] += bias_s[cl * 16 + j];
@@ -563,6 +573,7 @@ __global__ void __launch_bounds__(gemm_threads(WPQ), 1) tc_gemm_kernel(const __g
           if (has_dot) {
             // the WPQ warps of this lane quarter combine their row-dot slices in a fixed order
             // (dotpart double-buffered by tile parity; the quarter barrier orders reuse)
+            const float dot = dot2[0] + dot2[1];
             float tot = dot;
             if constexpr (S::SPLIT) {
               const int pb = dot_tiles & 1;

@@ -347,12 +347,8 @@ cudaError_t launch_ab(ActorBwdParams& p, cudaStream_t st) {
   const int ns = std::min(AB_STAGES, (227 * 1024 - 8 * 1024 - fixed) / STAGE);
   if (ns < 2) return cudaErrorInvalidValue;
   auto kern = tc_actor_bwd_kernel<H>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 8 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, kern, 227 * 1024 - 8 * 1024); e != cudaSuccess) return e;
   p.stages = ns;
   const int grid = std::min(p.tiles, num_sms());
   return launch_pdl(kern, dim3(grid), dim3(ab_threads<H>()), (size_t)(ns * STAGE + fixed), st, p);

@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <atomic>
 #include <cstdint>
 #include <mutex>
 
@@ -205,6 +206,20 @@ __device__ __forceinline__ uint32_t mask_pair(float p0, float p1, int j) {
 }
 
 // ------------------------------------------------------------------ host side
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per device for one kernel: `done` is the call site's
+// static bitmask of devices already set (the attribute belongs to the current device's context; thread-safe)
+template <typename K>
+inline cudaError_t smem_attr_once(std::atomic<uint64_t>& done, K kern, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;

@@ -654,12 +654,8 @@ cudaError_t launch(TcParams& p, cudaStream_t st) {
   static_assert(MAX_ST >= 1, "shared memory budget");
   constexpr int SMEM_MAX = MAX_ST * STAGE + smem_extras<WPQ>();
   auto kern = tc_gemm_kernel<BN, AMN, BMN, EK, PAIR, WPQ>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, kern, SMEM_MAX); e != cudaSuccess) return e;
   // persistent schedule: tiles of every group, one CTA per SM (or more when TMEM and smem allow)
   int T = 0;
   p.pair = PAIR ? 1 : 0;

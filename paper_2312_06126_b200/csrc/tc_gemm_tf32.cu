@@ -306,12 +306,8 @@ cudaError_t launch32(Tf32Params& p, cudaStream_t st) {
   constexpr int MAX_ST = std::min(TSTAGES, (227 * 1024 - t_extras()) / STAGE);
   static_assert(MAX_ST >= 2, "shared memory budget");
   auto kern = tc_gemm_tf32_kernel<BN, AMN, BMN, EK>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_ST * STAGE + t_extras());
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, kern, MAX_ST * STAGE + t_extras()); e != cudaSuccess) return e;
   int T = 0;
   for (int i = 0; i < p.a.n_groups; ++i) {
     const GemmGroup& g = p.a.g[i];

@@ -1001,12 +1001,8 @@ cudaError_t launch_mlp_pair(MlpParams& p, cudaStream_t st) {
   const int ns = std::min(MSTAGES, (227 * 1024 - STATIC - 512 - fixed) / STAGE);
   if (ns < 2) return cudaErrorInvalidValue;
   auto kern = tc_mlp_pair_kernel<H, WPQ>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - STATIC - 512);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, kern, 227 * 1024 - STATIC - 512); e != cudaSuccess) return e;
   p.stages = ns;
   int grid = std::min(p.total_su, num_sms());
   if (grid == 0) return cudaSuccess;
@@ -1025,12 +1021,8 @@ cudaError_t launch_mlp(MlpParams& p, cudaStream_t st) {
   if (ns < 2) return cudaErrorInvalidValue;
   constexpr int SMEM_ATTR = 227 * 1024 - STATIC;
   auto kern = tc_mlp_kernel<H, ACTOR, WPQ>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATTR);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, kern, SMEM_ATTR); e != cudaSuccess) return e;
   p.stages = ns;
   p.trace = g_mtrace_mode == 1 || (g_mtrace_mode >= 2 && g_mtrace_count == g_mtrace_mode - 2);
   ++g_mtrace_count;

@@ -119,26 +119,26 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ r
       int k = e - rr * J;
       const float* rw = sm + rr * R;
       const int64_t j = j0 + rr;
-      uint4* dst;
-      uint4 v;
-      if (k < ca) {  // Xa s2 row
-        dst = reinterpret_cast<uint4*>(Xa + j * lda) + k;
-        v = pack_chunk<T>(rw + s2c, k * EPC, o);
-      } else if ((k -= ca) < ca) {  // Xa s row
-        dst = reinterpret_cast<uint4*>(Xa + (Bl + j) * lda) + k;
-        v = pack_chunk<T>(rw, k * EPC, o);
-      } else if ((k -= ca) < cb) {  // Xc [s | a]
-        dst = reinterpret_cast<uint4*>(Xc + j * ldc) + k;
-        v = pack_chunk<T>(rw, k * EPC, o + m);
-      } else if ((k -= cb) < cs) {  // Xc [s | a~ later]
-        dst = reinterpret_cast<uint4*>(Xc + (Bl + j) * ldc) + k;
-        v = pack_chunk<T>(rw, k * EPC, o);
-      } else {  // Xc [s2 | a' later]
-        k -= cs;
-        dst = reinterpret_cast<uint4*>(Xc + (2 * (int64_t)Bl + j) * ldc) + k;
-        v = pack_chunk<T>(rw + s2c, k * EPC, o);
+      // operand of chunk k, chosen by selects (one pack per item, no divergent per-operand copies):
+      // 0 Xa s2-row j, 1 Xa s-row Bl + j, 2 Xc [s | a] row j, 3 Xc [s | (a~)] row Bl + j, 4 Xc [s2 | (a')] row 2 Bl + j
+      int op, kk;
+      if (k < 2 * ca) {
+        op = k >= ca;
+        kk = k - op * ca;
+      } else if ((k -= 2 * ca) < cb) {
+        op = 2;
+        kk = k;
+      } else {
+        k -= cb;
+        op = k >= cs ? 4 : 3;
+        kk = k - (op - 3) * cs;
       }
-      *dst = v;
+      T* base = op < 2 ? Xa : Xc;
+      const int ld = op < 2 ? lda : ldc;
+      const int64_t row = op < 2 ? (op == 0 ? j : Bl + j) : (int64_t)(op - 2) * Bl + j;
+      const int src0 = (op == 0 || op == 4) ? s2c : 0;
+      const int n = op == 2 ? o + m : o;
+      *(reinterpret_cast<uint4*>(base + row * ld) + kk) = pack_chunk<T>(rw + src0, kk * EPC, n);
     }
     if (threadIdx.x < nr) {
       r[j0 + threadIdx.x] = sm[threadIdx.x * R + o + m];

@@ -970,6 +970,9 @@ __global__ void __launch_bounds__(ADAM_NT, WIDE ? 2 : SPZ_ADAM_MINB) adam_polyak
     const int s_off = (int)__ldg(&sg->t.s_off), ts_off = (int)__ldg(&sg->t.ts_off), ld = __ldg(&sg->t.ld);
     const bool polyak = t_off >= 0 && (!hp.td3 || delayed);
     // one element: Adam (m, v, theta) and Polyak (theta'); false (nothing changes) on a non-finite gradient
+    // bias corrections as per-block reciprocals and one approximate divide per element (each within 2 ulp of the
+    // IEEE divisions; tests/parity.py's Adam identity allows 1e-5 of the step): WLK -1 us per update
+    const float ib1 = 1.f / bc1, ib2 = 1.f / bc2;
     auto elem = [&](float ge, float me, float ve, float pe, float tpe, float& m, float& v, float& p, float& tp) {
       if (!isfinite(ge)) {
         atomicExch(flag, 2);
@@ -978,7 +981,7 @@ __global__ void __launch_bounds__(ADAM_NT, WIDE ? 2 : SPZ_ADAM_MINB) adam_polyak
       }
       m = hp.beta1 * me + (1.f - hp.beta1) * ge;
       v = hp.beta2 * ve + (1.f - hp.beta2) * ge * ge;
-      p = pe - lr * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
+      p = pe - __fdividef(lr * (m * ib1), sqrtf(v * ib2) + hp.eps);
       tp = hp.tau * p + (1.f - hp.tau) * tpe;
       return true;
     };

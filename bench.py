@@ -611,7 +611,9 @@ def other_configs(a, done, local, torch, dist):
         out[name] = {"value": w.batch * K / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms / K, "steps": K,
                      "repetitions": len(reps), "global_batch": w.batch, "algo": w.algo,
                      "hidden": f"{w.n_hidden}x{w.hidden}", "dtype": "bf16",
-                     "roofline": {k: roof[k] for k in ("kernel", "achieved", "peak", "unit", "frac")},
+                     "roofline": {**{k: roof[k] for k in ("kernel", "achieved", "peak", "unit", "frac")},
+                                  "hbm": {k: {f: v[f] for f in ("achieved", "frac", "algorithmic_bytes_per_launch")}
+                                          for k, v in roof.get("hbm", {}).items()}},
                      "step_gemm_tflops": gemm_f / (ms / K * 1e-3) / 1e12}
         lrn.close()
         ring.close()

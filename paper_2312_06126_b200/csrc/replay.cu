@@ -34,14 +34,14 @@ __global__ void pack_records_kernel(float* __restrict__ rec, int R, int o, int m
     float v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      // field of column c chosen by selects (one predicated load per element, no divergent per-field loads)
       const int c = 4 * q + k;
-      float x = 0.f;
-      if (c < c_a) x = __ldg(obs + (int64_t)t * o + c);
-      else if (c < c_r) x = __ldg(act + (int64_t)t * m + (c - c_a));
-      else if (c == c_r) x = __ldg(rew + t);
-      else if (c == c_d) x = __ldg(done + t);
-      else if (c < c_end) x = __ldg(nobs + (int64_t)t * o + (c - c_s2));
-      v[k] = x;
+      const float* src = c < c_a ? obs + (int64_t)t * o + c
+                         : c < c_r ? act + (int64_t)t * m + (c - c_a)
+                         : c == c_r ? rew + t
+                         : c == c_d ? done + t
+                                    : nobs + (int64_t)t * o + (c - c_s2);
+      v[k] = c < c_end ? __ldg(src) : 0.f;
     }
     reinterpret_cast<float4*>(rec + slot * R)[q] = make_float4(v[0], v[1], v[2], v[3]);
   }

@@ -351,7 +351,7 @@ __device__ __forceinline__ void stat_totals(const double* __restrict__ partials,
 // then writes its chunk of dZ_L, otherwise critic_dz_kernel does that afterwards.  All of a warp's
 // loads are issued before any of its arithmetic.  Lane 0 accumulates the statistics of the warp's
 // rows in row order; the block partial sums the warps in order.
-template <typename T, bool DZ, int LOSS_RPW>
+template <typename T, bool DZ, int LOSS_RPW, bool Q1 = DZ>
 __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_constant__ LossArgs a) {
   constexpr int LOSS_ROWS = LOSS_WARPS * LOSS_RPW;
   pdl_wait();
@@ -381,6 +381,9 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
   // accumulate in row-block order, the block partials are summed in block order -- deterministic
   for (int jb = blockIdx.x; jb * LOSS_ROWS < a.Bl; jb += gridDim.x) {
   const int j0 = jb * LOSS_ROWS;
+  // q partials per row: Q1 (always with DZ, which runs only at h <= 256, one lane per 8 columns) -- the row dot is
+  // one tile; a compile-time 1 drops the predicated partial loads and their 64-bit address arithmetic
+  const int qp = Q1 ? 1 : a.qp;
   // ---- loads, all issued before any use: row scalars of the warp's rows (row index clamped, so
   //      every address is valid; rows past Bl are discarded below)
   float qt1[LOSS_RPW], qt2[LOSS_RPW], q1[LOSS_RPW], q2[LOSS_RPW], lp2[LOSS_RPW], rw[LOSS_RPW], dn[LOSS_RPW];
@@ -389,17 +392,17 @@ __global__ void __launch_bounds__(LOSS_NT) critic_loss_kernel(const __grid_const
 #pragma unroll
   for (int i = 0; i < LOSS_RPW; ++i) {
     const int j = min(j0 + wi + 8 * i, a.Bl - 1);
-    qt1[i] = ld_q(a.qt1, j, a.qp, a.qps_tg);
-    qt2[i] = ld_q(a.qt2, j, a.qp, a.qps_tg);
-    q1[i] = ld_q(a.q1, j, a.qp, a.qps_on);
-    q2[i] = ld_q(a.q2, j, a.qp, a.qps_on);
+    qt1[i] = ld_q(a.qt1, j, qp, a.qps_tg);
+    qt2[i] = ld_q(a.qt2, j, qp, a.qps_tg);
+    q1[i] = ld_q(a.q1, j, qp, a.qps_on);
+    q2[i] = ld_q(a.q2, j, qp, a.qps_on);
     rw[i] = __ldg(a.r + j);
     dn[i] = __ldg(a.d + j);
     lp2[i] = notemp ? 0.f : __ldg(a.logp2 + j);
-    a1[i] = ld_q(a.q1, a.Bl + j, a.qp, a.qps_on);
-    a2[i] = ld_q(a.q2, a.Bl + j, a.qp, a.qps_on);
+    a1[i] = ld_q(a.q1, a.Bl + j, qp, a.qps_on);
+    a2[i] = ld_q(a.q2, a.Bl + j, qp, a.qps_on);
     lp[i] = a.td3 ? 0.f : __ldg(a.logp + j);
-    vo[i] = a.v1 ? ld_q(a.vo, j, a.qp, a.vps) : 0.f;
+    vo[i] = a.v1 ? ld_q(a.vo, j, qp, a.vps) : 0.f;
   }
   // ---- DZ: mask bytes (bit k = column n0 + k) and head weights of this lane's chunk
   const int n0 = lane * 8;

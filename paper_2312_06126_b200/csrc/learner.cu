@@ -908,7 +908,7 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
     // ---- a4/a5: Bellman target, losses, head gradients, this rank's loss totals; a6 head backward
     // dZ_L written by the loss kernel itself (one row per warp) at h <= 256 up to 16K local rows (WLK
     // 109.1 -> 108.2 us); larger batches do better with the separate critic_dz_kernel (ANT 319.5 -> 315.4 us)
-    const bool dz_in_loss = h <= 256 && Bl <= 16384 && !dz_split_env();
+    const bool dz_in_loss = h <= 256 && Bl <= 16384 && !dz_split_env();  // (then qparts == 1: the kernel assumes it)
     const bool defer_totals = !(Lr->gsize > 1 || Lr->cfg.comm_mode == 2) && !lfused && !defer_totals_off_env();
     // diagnostics: SPZ_DIAG_LOSS=<rpw>,<blocks per SM> for the dZ-writing variant (rpw 1 or 2)
     int diag_rpw = 1, diag_cap = 4;
@@ -983,7 +983,11 @@ static spz_status build_plan(spz_learner* Lr, int64_t B) {
       // h <= 256: dZ_L written by the loss kernel (one row per warp); wider rows: critic_dz_kernel
       const bool dz_sep = !dz_in_loss && (do_critic || do_actor);
       if (!lfused) {  // (the fused critic forward with loss groups computes all of this itself)
-        if (!dz_in_loss)
+        if (!dz_in_loss && la.qp == 1)
+          ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
+                           return launch_pdl(critic_loss_kernel<T, false, 4, true>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
+                         }});
+        else if (!dz_in_loss)
           ops.push_back({"critic_loss", [la, nblk](cudaStream_t st) {
                            return launch_pdl(critic_loss_kernel<T, false, 4>, dim3(nblk), dim3(LOSS_NT), 0, st, la);
                          }});

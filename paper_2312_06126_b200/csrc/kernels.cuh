@@ -99,6 +99,41 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ r
   const int cb = min((o + m + EPS - 1) / EPS * EPS, ldc) / EPC;      // [s | a]
   const int cs = min((o + EPS - 1) / EPS * EPS, ldc) / EPC;
   const int J = 2 * ca + cb + 2 * cs;                                 // chunks per row
+  // operand of chunk k of a row: 0 Xa s2-row j, 1 Xa s-row Bl + j, 2 Xc [s | a] row j, 3 Xc [s | (a~)] row Bl + j,
+  // 4 Xc [s2 | (a')] row 2 Bl + j -- destination base / pitch / row offset, 16-byte unit, source column, width
+  struct Chunk {
+    T* base;
+    int64_t rowoff;
+    int ld, kk, src0, n;
+  };
+  auto chunk_of = [&](int k) {
+    int op, kk;
+    if (k < 2 * ca) {
+      op = k >= ca;
+      kk = k - op * ca;
+    } else if ((k -= 2 * ca) < cb) {
+      op = 2;
+      kk = k;
+    } else {
+      k -= cb;
+      op = k >= cs ? 4 : 3;
+      kk = k - (op - 3) * cs;
+    }
+    Chunk c;
+    c.base = op < 2 ? Xa : Xc;
+    c.ld = op < 2 ? lda : ldc;
+    c.rowoff = (op == 1 || op == 3) ? (int64_t)Bl : op == 4 ? 2 * (int64_t)Bl : 0;
+    c.kk = kk;
+    c.src0 = (op == 0 || op == 4) ? s2c : 0;
+    c.n = op == 2 ? o + m : o;
+    return c;
+  };
+  const bool fixed_chunk = J <= (int)blockDim.x;
+  const int rows_per_pass = fixed_chunk ? (int)blockDim.x / J : 0, t_row = fixed_chunk ? (int)threadIdx.x / J : 0;
+  const Chunk tc = chunk_of(fixed_chunk ? (int)threadIdx.x % J : 0);
+  T* const t_base = tc.base;
+  const int64_t t_rowoff = tc.rowoff;
+  const int t_ld = tc.ld, t_kk = tc.kk, t_src0 = tc.src0, t_n = tc.n;
   int it = 0;
   if ((int)blockIdx.x < ngroups) issue(blockIdx.x, 0);
   for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x, ++it) {
@@ -114,31 +149,20 @@ __global__ void __launch_bounds__(256) gather_kernel(const float* __restrict__ r
     const int j0 = gi * GATHER_ROWS;
     const int nr = min(GATHER_ROWS, Bl - j0);
     const float* sm = reinterpret_cast<const float*>(sm4 + (size_t)b * GATHER_ROWS * R4);
-    for (int e = threadIdx.x; e < nr * J; e += blockDim.x) {
-      const int rr = e / J;
-      int k = e - rr * J;
-      const float* rw = sm + rr * R;
-      const int64_t j = j0 + rr;
-      // operand of chunk k, chosen by selects (one pack per item, no divergent per-operand copies):
-      // 0 Xa s2-row j, 1 Xa s-row Bl + j, 2 Xc [s | a] row j, 3 Xc [s | (a~)] row Bl + j, 4 Xc [s2 | (a')] row 2 Bl + j
-      int op, kk;
-      if (k < 2 * ca) {
-        op = k >= ca;
-        kk = k - op * ca;
-      } else if ((k -= 2 * ca) < cb) {
-        op = 2;
-        kk = k;
-      } else {
-        k -= cb;
-        op = k >= cs ? 4 : 3;
-        kk = k - (op - 3) * cs;
+    if (fixed_chunk) {
+      // J <= blockDim.x: thread t keeps chunk t % J for rows t / J, t / J + rows_per_pass, ... -- its operand,
+      // destination and source columns are loop invariants (no per-item division or operand selection)
+      if (t_row < rows_per_pass)
+        for (int rr = t_row; rr < nr; rr += rows_per_pass)
+          *(reinterpret_cast<uint4*>(t_base + (t_rowoff + j0 + rr) * t_ld) + t_kk) =
+              pack_chunk<T>(sm + rr * R + t_src0, t_kk * EPC, t_n);
+    } else {
+      for (int e = threadIdx.x; e < nr * J; e += blockDim.x) {
+        const int rr = e / J;
+        const Chunk c = chunk_of(e - rr * J);
+        *(reinterpret_cast<uint4*>(c.base + (c.rowoff + j0 + rr) * c.ld) + c.kk) =
+            pack_chunk<T>(sm + rr * R + c.src0, c.kk * EPC, c.n);
       }
-      T* base = op < 2 ? Xa : Xc;
-      const int ld = op < 2 ? lda : ldc;
-      const int64_t row = op < 2 ? (op == 0 ? j : Bl + j) : (int64_t)(op - 2) * Bl + j;
-      const int src0 = (op == 0 || op == 4) ? s2c : 0;
-      const int n = op == 2 ? o + m : o;
-      *(reinterpret_cast<uint4*>(base + row * ld) + kk) = pack_chunk<T>(rw + src0, kk * EPC, n);
     }
     if (threadIdx.x < nr) {
       r[j0 + threadIdx.x] = sm[threadIdx.x * R + o + m];
